@@ -1,0 +1,428 @@
+#!/usr/bin/env python3
+"""Benchmark: DisCo contrastive-loss fwd+bwd samples/sec at B=32K, D=512 (BASELINE.json).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1; one rank per GPU, NCCL)
+
+A step is one DisCo loss forward+backward over the global batch (B=32768
+image/text pairs, D=512, t=100): every rank runs disco_step on its b = B/N
+rows (shard.py:169-208).  Workload = BASELINE.json configs[1] (strong
+scaling: B fixed, N varies).
+
+Printed on rank 0, one JSON line:
+  value     samples/s = B / t_step, t_step = max over ranks of the device time
+            of the step (inputs resident in HBM, CUDA events per step, L2
+            flushed between steps outside the timed events).
+  e2e       same metric through the public API with HOST (pinned, bf16)
+            inputs and host outputs: H2D of the features, D2H of both fp32
+            gradient blocks and the loss inside the timed region.
+  roofline  dominant kernel: algorithmic FLOPs per launch / mean launch time
+            (CUDA events on the launching stream) against the measured bf16
+            peak (MEASURED_PEAKS.json); step-level fraction alongside.
+  cpu_baseline  the oracle port of the reference path (oracle/disco_oracle.py,
+            numpy f32, all host cores) on a bounded row sample (rank 0, N=1 only).
+``--impl reference`` times that CPU port alone as the reference arm.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B_GLOBAL = 32768
+DIM = 512
+TEMP = 100.0
+METRIC = "contrastive-loss fwd+bwd samples/sec at B=32K,D=512; peak loss mem/GPU"
+UNIT = "samples/s"
+CPU_SAMPLE_ROWS = 2048
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=B_GLOBAL)
+    ap.add_argument("--dim", type=int, default=DIM)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port of the reference path, bounded row sample
+# ---------------------------------------------------------------------------
+def cpu_port_sample(B, D, rows, t=TEMP, seed=0, reps=1):
+    """Time the reference algorithm (shard.py:98-166, f32 as costs.py:158) for
+    `rows` local rows of a rank against all B columns, both directions:
+    logits GEMMs, CE, softmax-minus-onehot, the four gradient GEMMs.
+    Returns (samples/s, seconds per sample block)."""
+    from oracle import disco_oracle as O
+    rng = np.random.default_rng(seed)
+    I = rng.standard_normal((B, D)).astype(np.float32)
+    I /= np.linalg.norm(I, axis=1, keepdims=True)
+    T = rng.standard_normal((B, D)).astype(np.float32)
+    T /= np.linalg.norm(T, axis=1, keepdims=True)
+    I, T = O.bf16_round(I), O.bf16_round(T)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        I_n, T_n = I[:rows], T[:rows]
+        labels = np.arange(rows)
+        li = (I_n @ T.T) * np.float32(t)
+        lt = (T_n @ I.T) * np.float32(t)
+        loss = (O.cross_entropy_mean(li, labels) + O.cross_entropy_mean(lt, labels)) / 2.0
+        O.softmax_ce_grad_inplace(li, labels, 0.5 / rows)
+        O.softmax_ce_grad_inplace(lt, labels, 0.5 / rows)
+        d_image = lt.T @ T_n
+        d_image[:rows] += li @ T
+        d_text = li.T @ I_n
+        d_text[:rows] += lt @ I
+        d_image *= t
+        d_text *= t
+        assert np.isfinite(loss)
+        times.append(time.perf_counter() - t0)
+    sec = statistics.median(times)
+    return rows / sec, sec
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    B, D = args.batch, args.dim
+    rows = min(CPU_SAMPLE_ROWS, B)
+    for _ in range(max(args.warmup, 1) if args.warmup else 0):
+        cpu_port_sample(B, D, rows // 4)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, _ = cpu_port_sample(B, D, rows)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = statistics.median(vals)
+    sample = (f"{rows} of {B // args.gpus} local rows x {B} columns, D={D}, both directions, "
+              f"f32 numpy/BLAS; samples/s = rows / time")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * B / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"B={B},D={D},t={TEMP} (BASELINE configs[1])",
+                                         "global_batch": B, "dim": D, "parallelism": f"dp{args.gpus}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (NVML) during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons = [], set()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as exc:  # pragma: no cover
+            self.err = str(exc)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.th.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk["bf16_tflops"], pk.get("bf16_tflops_sustained", pk["bf16_tflops"]), pk["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+
+    import paper_2304_08480_b200 as P
+    from paper_2304_08480_b200 import _lib
+    from paper_2304_08480_b200.shard import get_plan
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+        ep = P.ProcessGroupEndpoint()
+    else:
+        ep = P.SingleEndpoint()
+
+    B, D, t = args.batch, args.dim, TEMP
+    b = B // world
+    # synthetic features (cli.py:103-105 distribution), bf16, this rank's rows only
+    g = torch.Generator(device=device)
+    g.manual_seed(1234 + rank)
+    I = torch.randn(b, D, device=device, generator=g)
+    T = torch.randn(b, D, device=device, generator=g)
+    I = (I / I.norm(dim=1, keepdim=True)).to(torch.bfloat16)
+    T = (T / T.norm(dim=1, keepdim=True)).to(torch.bfloat16)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=device)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- per-kernel timing (one instrumented step after warm-up) ----------
+    plan = get_plan(B, D, world, rank, device)
+    st = torch.cuda.current_stream(device)
+
+    def step():
+        return P.disco_step_async(ep, I, T, t)
+
+    for _ in range(args.warmup):
+        step()
+    P.finish_status(plan)
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(device)
+    mem_before = torch.cuda.memory_allocated(device)
+
+    # ---- timed region: K steps, each bracketed by CUDA events -------------
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = _lib.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush outside the timed events
+            starts[i].record(st)
+            step()
+            ends[i].record(st)
+        torch.cuda.synchronize()
+    barrier()
+    launches = _lib.launch_count() - launches0
+    loss = P.finish_status(plan)
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = statistics.mean(step_ms)
+    peak_mem = torch.cuda.max_memory_allocated(device)
+    if world > 1:
+        tt = torch.tensor([ms], device=device, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = B / (ms / 1e3)
+
+    # ---- kernel breakdown: events around each C-ABI phase -----------------
+    phases = {}
+    names = ["pack", "all_gather", "forward", "backward_cross", "all_to_all", "backward_intra",
+             "combine", "loss"]
+    ev = {n: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for n in names}
+    args_ = plan.args
+    sp = st.cuda_stream
+    reps = 3
+    acc = {n: 0.0 for n in names}
+    for _ in range(reps):
+        flush.zero_()
+        barrier()
+        ev["pack"][0].record(st)
+        _lib.call("disco_b200_pack", *args_, I.data_ptr(), T.data_ptr(), D, D, _lib.BF16, 1, sp)
+        ev["pack"][1].record(st)
+        ev["all_gather"][0].record(st)
+        if world > 1:
+            ep.all_gather_into(plan.gather, plan.pack)
+        ev["all_gather"][1].record(st)
+        ev["forward"][0].record(st)
+        _lib.call("disco_b200_forward", *args_, t, sp)
+        ev["forward"][1].record(st)
+        ev["backward_cross"][0].record(st)
+        _lib.call("disco_b200_backward_cross", *args_, t, sp)
+        ev["backward_cross"][1].record(st)
+        ev["all_to_all"][0].record(st)
+        if world > 1:
+            ep.all_to_all_into(plan.recv, plan.send)
+        ev["all_to_all"][1].record(st)
+        ev["backward_intra"][0].record(st)
+        _lib.call("disco_b200_backward_intra", *args_, sp)
+        ev["backward_intra"][1].record(st)
+        di = torch.empty((b, D), dtype=torch.float32, device=device)
+        dt_ = torch.empty((b, D), dtype=torch.float32, device=device)
+        ev["combine"][0].record(st)
+        _lib.call("disco_b200_combine", *args_, t, 0, di.data_ptr(), dt_.data_ptr(), D, sp)
+        ev["combine"][1].record(st)
+        ev["loss"][0].record(st)
+        if world > 1:
+            ep.all_gather_into(plan.ce_all, plan.ce)
+        _lib.call("disco_b200_loss", *args_, 0, sp)
+        ev["loss"][1].record(st)
+        torch.cuda.synchronize()
+        for n in names:
+            acc[n] += ev[n][0].elapsed_time(ev[n][1]) / reps
+    phases = {n: round(v, 4) for n, v in acc.items()}
+
+    # ---- e2e through the public API with host buffers ---------------------
+    e2e = None
+    if not args.no_e2e:
+        I_h = I.cpu().pin_memory()
+        T_h = T.cpu().pin_memory()
+        for _ in range(2):
+            P.disco_step(ep, I_h, T_h, t)
+        e_ms = []
+        barrier()
+        for _ in range(max(3, args.steps // 2)):
+            flush.zero_()
+            torch.cuda.synchronize()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(st)
+            di_h, dt_h, _ = P.disco_step(ep, I_h, T_h, t)
+            s1.record(st)
+            s1.synchronize()
+            e_ms.append(s0.elapsed_time(s1))
+        em = statistics.mean(e_ms)
+        if world > 1:
+            tt = torch.tensor([em], device=device, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            em = float(tt.item())
+        e2e = {"value": B / (em / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(I_h.numel() * I_h.element_size() * 2),
+               "d2h_bytes_per_step": int(di_h.numel() * 4 * 2 + 8),
+               "ms_per_step": em}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline ----------------------------------------------------------
+    burst, sustained, hbm, src = load_peaks()
+    flops_launch = 4.0 * b * B * D  # every tensor-core launch: 2 directions x 2*b*B*D
+    kern = {
+        "logits_fwd": phases["forward"],
+        "logits_grad+gemm_cross": phases["backward_cross"],
+        "gemm_intra": phases["backward_intra"],
+    }
+    dom = max(kern, key=kern.get)
+    dom_ms = kern[dom]
+    achieved = flops_launch / (dom_ms / 1e3) / 1e12
+    traffic = load_traffic().get(dom)
+    step_tflops = 12.0 * b * B * D / (ms / 1e3) / 1e12
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        rows = CPU_SAMPLE_ROWS
+        cpu_port_sample(B, D, rows // 8)
+        v, sec = cpu_port_sample(B, D, rows)
+        cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+               "sample": f"{rows} of {b} local rows x {B} columns, D={D}, both directions, "
+                         f"oracle/disco_oracle.py f32 numpy ({sec:.1f} s)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"B={B},D={D},t={TEMP} (BASELINE configs[1])", "global_batch": B,
+                   "local_batch": b, "dim": D, "parallelism": f"dp{world}",
+                   "l2": "flushed between steps (512 MB write, outside timed events)"},
+        "loss": loss,
+        "peak_loss_mem_gb": (peak_mem - mem_before) / 1e9,
+        "peak_mem_gb": peak_mem / 1e9,
+        "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved,
+                     "peak": sustained, "unit": "TFLOP/s", "frac": achieved / sustained,
+                     "traffic": traffic, "peak_kind": f"{src} bf16 sustained",
+                     "frac_of_burst": achieved / burst,
+                     "step_tflops": step_tflops, "step_frac": step_tflops / sustained,
+                     "flops_per_launch": flops_launch, "launch_ms": dom_ms},
+        "phases_ms": phases,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,135 @@
+/*
+ * disco_b200.h -- C ABI of the B200-native DisCo contrastive loss.
+ *
+ * This is the drop-in boundary for the reference package's hot path
+ * (arxiv 2304.08480 reference, /root/reference/pkg/src/disco):
+ *
+ *   disco_step(endpoint, local_I, local_T, t, ...)            shard.py:169-208
+ *   local_loss_and_grads(layout, I_gathered, T_gathered, t)   shard.py:98-166
+ *
+ * The reference is pure Python/numpy, so its "FFI" is the Python call
+ * boundary; the entry points below are what a ctypes binding of that call
+ * needs (INTEGRATION.md shows the stub).  The collectives that sit between
+ * the phases (all_gather shard.py:190-191, all_reduce(AVG) shard.py:199-204,
+ * all_reduce_scalar shard.py:205) are issued by the host through
+ * torch.distributed (NCCL); this library never links NCCL.
+ *
+ * Conventions
+ *  - Plain device pointers, int64 sizes, a cudaStream_t passed as void*.
+ *  - Every call is stream-ordered and asynchronous; nothing allocates.
+ *    All scratch lives in one caller-allocated workspace whose layout is
+ *    described by disco_b200_ws_region().
+ *  - Return value: DISCO_OK or one of the status codes below; a message is
+ *    available from disco_b200_last_error() (thread-local).  The codes map
+ *    onto the reference exception taxonomy (errors.py:4-20).
+ *  - Problem geometry, per rank: global batch B, local batch b = B / N,
+ *    feature dim D (padded internally to Dp = roundup(D, 64)), world size N,
+ *    rank in [0, N).
+ */
+#ifndef DISCO_B200_H_
+#define DISCO_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DISCO_B200_ABI_VERSION 1
+
+enum disco_status {
+  DISCO_OK = 0,
+  DISCO_SHAPE_ERROR = 1,   /* errors.ShapeError   (errors.py:4)  */
+  DISCO_LAYOUT_ERROR = 2,  /* errors.LayoutError  (errors.py:16) */
+  DISCO_DOMAIN_ERROR = 3,  /* errors.DomainError  (errors.py:12) */
+  DISCO_NONFINITE = 4,     /* ValueError("... non-finite ...") (matrix.py:43-45) */
+  DISCO_CUDA_ERROR = 5     /* launch / driver failure */
+};
+
+/* Input element types accepted by disco_b200_pack. */
+enum disco_dtype { DISCO_F32 = 0, DISCO_BF16 = 1, DISCO_F64 = 2, DISCO_F16 = 3 };
+
+/* Workspace regions (see disco_b200_ws_region). */
+enum disco_region {
+  DISCO_R_PACK = 0,    /* bf16 [2][b][Dp]         local packed I_n, T_n (all_gather input)   */
+  DISCO_R_GATHER = 1,  /* bf16 [N][2][b][Dp]      all_gather output                          */
+  DISCO_R_FEAT = 2,    /* bf16 [2][B][Dp]         gathered I_g, T_g (forward GEMM operands)  */
+  DISCO_R_FEAT16 = 3,  /* f16  [2][B][Dp]         gathered I_g, T_g (backward GEMM operands) */
+  DISCO_R_STATS = 4,   /* f32  [2][nchunk][b][2]  per column-chunk (max, sum-exp) partials   */
+  DISCO_R_ROWS = 5,    /* f32  [4][2][b]          target logit, lse, label gradient, spare   */
+  DISCO_R_CE = 6,      /* f32  [2][b]             per-row cross-entropy (loss all_gather in) */
+  DISCO_R_CE_ALL = 7,  /* f32  [N][2][b]          loss all_gather output                     */
+  DISCO_R_G = 8,       /* f16  [2][b][ldG]        softmax-minus-one-hot blocks (unscaled)    */
+  DISCO_R_XPART = 9,   /* f32  [2][cpr][B][Dp]    cross partials per canonical row chunk     */
+  DISCO_R_SEND = 10,   /* f32  [N][2][b][Dp]      cross slabs by destination (all_to_all in) */
+  DISCO_R_RECV = 11,   /* f32  [N][2][b][Dp]      cross slabs by source (all_to_all out)     */
+  DISCO_R_INTRA = 12,  /* f32  [2][b][Dp]         intra-rank gradient terms                  */
+  DISCO_R_STATUS = 13, /* f64 loss, i32 flags      host-visible step status                   */
+  DISCO_R_COUNT = 14
+};
+
+int disco_b200_abi_version(void);
+const char* disco_b200_last_error(void);
+
+/* Number of CUDA kernels this library has launched in this process
+ * (monotonic; used by bench.py to report gpu_launches). */
+int64_t disco_b200_launch_count(void);
+
+/* Validates the geometry exactly as ShardLayout (shard.py:38-49) does and
+ * reports the workspace size in bytes. */
+int disco_b200_workspace_bytes(int64_t B, int64_t D, int world, int rank, int64_t* bytes);
+
+/* Byte offset and size of one region inside the workspace. */
+int disco_b200_ws_region(int64_t B, int64_t D, int world, int rank, int region, int64_t* offset,
+                         int64_t* bytes);
+
+/* Number of canonical row/column chunks (8 when B % 1024 == 0 and N | 8,
+ * else N) and chunks per rank.  Fixes every reduction order over B, which
+ * makes results bitwise identical across world sizes that divide 8. */
+int disco_b200_chunking(int64_t B, int world, int* nchunk, int* chunks_per_rank);
+
+/* Step 0: round the rank's local features (b x D, row stride ld_*) to bf16
+ * into DISCO_R_PACK, zero-padding D..Dp; clear_status != 0 first resets
+ * DISCO_R_STATUS (the non-finite flags accumulate until the next reset).
+ * Replaces the implicit dtype handling of matmul (matrix.py:57-78). */
+int disco_b200_pack(void* ws, int64_t B, int64_t D, int world, int rank, const void* local_I,
+                    const void* local_T, int64_t ld_I, int64_t ld_T, int dtype, int clear_status,
+                    void* stream);
+
+/* Forward: unpack the gathered features, fused logits GEMM + online
+ * log-sum-exp + target extraction (shard.py:134-141, matrix.py:103-118),
+ * fixed-order chunk combine -> per-row lse / ce / label gradient. */
+int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
+
+/* Backward part 1: recompute logits -> G = softmax - onehot in f16
+ * (shard.py:143-146, matrix.py:131-144), then the cross-rank gradient GEMMs
+ * G^T . local features (shard.py:149, 151) reduced over this rank's
+ * canonical chunks into DISCO_R_SEND (destination-major slabs). */
+int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
+
+/* Backward part 2: intra-rank GEMMs G . gathered features (shard.py:150, 152)
+ * into DISCO_R_INTRA.  Independent of the slab exchange, so it overlaps it. */
+int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
+
+/* Owner combine after the slab exchange (replaces all_reduce(AVG) +
+ * row slice, shard.py:199-208): d = t*0.5/B * (intra + tree(recv slabs)),
+ * fp32 b x D outputs with row stride ld_out.  flip != 0 negates the slabs
+ * received from other ranks (the flip_cross_rank_sign hook, shard.py:158-162). */
+int disco_b200_combine(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,
+                       float* d_image, float* d_text, int64_t ld_out, void* stream);
+
+/* Full-size per-rank contribution (LocalGradContribution, shard.py:61-80,
+ * 153-162): t*0.5/b * (scatter(intra) + send slabs), B x D fp32 each. */
+int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,
+                            float* d_image_full, float* d_text_full, int64_t ld_out, void* stream);
+
+/* Loss: fixed-order f64 sum of the gathered per-row ce (DISCO_R_CE_ALL, or
+ * DISCO_R_CE when world == 1 or local_only) / (2 * rows) into DISCO_R_STATUS.
+ * local_only=1 gives the rank's local_loss (shard.py:140-141). */
+int disco_b200_loss(void* ws, int64_t B, int64_t D, int world, int rank, int local_only, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DISCO_B200_H_ */

@@ -1,0 +1,60 @@
+"""B200-native DisCo distributed contrastive loss (arXiv 2304.08480).
+
+Drop-in for the hot path of the reference package ``disco``
+(/root/reference/pkg/src/disco/__init__.py:53-60 re-exports): the per-rank
+sharded loss ``disco_step`` / ``local_loss_and_grads`` with the same names,
+arguments and exceptions, computed by hand-written sm_100a kernels
+(tcgen05/TMEM/TMA) behind a C ABI, with NCCL collectives over NVLink.
+"""
+
+from .counters import Counters, tracking
+from .errors import (
+    CollectiveContractError,
+    CollectiveTimeoutError,
+    DeadlockError,
+    DegenerateInputError,
+    DomainError,
+    LayoutError,
+    ShapeError,
+    TrainingDivergenceError,
+)
+from .fabric import LocalEndpoint, LocalGroup, ProcessGroupEndpoint, ReduceOp, SingleEndpoint, run_ranks
+from .shard import (
+    LocalGradContribution,
+    ShardLayout,
+    disco_step,
+    disco_step_async,
+    finish_status,
+    local_labels,
+    local_loss_and_grads,
+    shard_slice,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CollectiveContractError",
+    "CollectiveTimeoutError",
+    "Counters",
+    "DeadlockError",
+    "DegenerateInputError",
+    "DomainError",
+    "LayoutError",
+    "LocalEndpoint",
+    "LocalGradContribution",
+    "LocalGroup",
+    "ProcessGroupEndpoint",
+    "ReduceOp",
+    "ShapeError",
+    "ShardLayout",
+    "SingleEndpoint",
+    "TrainingDivergenceError",
+    "disco_step",
+    "disco_step_async",
+    "finish_status",
+    "local_labels",
+    "local_loss_and_grads",
+    "run_ranks",
+    "shard_slice",
+    "tracking",
+]

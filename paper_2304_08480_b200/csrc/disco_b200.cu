@@ -1,0 +1,1184 @@
+// B200-native DisCo contrastive loss: kernels + C ABI (include/disco_b200.h).
+//
+// Hot path replaced: reference pkg/src/disco/shard.py:98-208 (local_loss_and_grads,
+// disco_step).  Per rank n (b = B/N rows), two directions d in {i2t, t2i}:
+//   S_d   = t * A_d . C_d^T           A_0 = I_n, C_0 = T_g ; A_1 = T_n, C_1 = I_g
+//   ce_d  = lse(S_d rows) - S_d[r, n*b + r]
+//   G_d   = softmax(S_d) - onehot     (unscaled, f16)
+//   intra : Y_g = G_d . C_d           (own rows; g = image for d = 0, text for d = 1)
+//   cross : X_g = G_d'^T . A_d'       (all B rows, sent to the owning rank)
+//   d_g   = t * 0.5 / B * (Y_g + sum_over_ranks X_g)
+//
+// Kernels
+//   logits_kernel<FWD>  : tcgen05 bf16 GEMM tiles of S with a fused online
+//                         (max, sum-exp) + target epilogue; S never hits HBM.
+//   logits_kernel<GRAD> : same tiles recomputed, epilogue writes f16 G.
+//   gemm_kernel         : grouped f16 GEMM (K-major or MN-major operands via
+//                         the UMMA descriptor major bits; no transposes),
+//                         fp32 tiles into partial / slab buffers.
+//   small kernels       : pack, unpack, stats combine, chunk presum, owner
+//                         combine, contribution, loss.
+// All GEMMs: TMA (SWIZZLE_128B) -> 4-stage smem ring -> single-thread
+// tcgen05.mma (M=128, N=256, K=16) -> double-buffered TMEM accumulators ->
+// 4 epilogue warps (tcgen05.ld 32x32b).  Persistent grid of <= #SM CTAs.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "disco_b200.h"
+#include "ptx.cuh"
+
+namespace disco {
+
+// ------------------------------------------------------------------ tiling
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KiB
+constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KiB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int NUM_THREADS = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int TMEM_COLS = 512;    // 2 accumulators of 128 x 256 fp32
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+struct SmemCtl {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+};
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + 256;
+
+// -------------------------------------------------------- status flag bits
+constexpr int FLAG_INPUT_NONFINITE = 1;
+constexpr int FLAG_LOSS_NONFINITE = 2;
+constexpr int FLAG_GRAD_NONFINITE = 4;
+
+struct Status {
+  double loss;
+  int flags;
+  int pad;
+};
+
+// ----------------------------------------------------------- kernel params
+// One direction of the logits GEMM: A rows are the rank's local rows of the
+// gathered matrix (row offset rank*b), B rows are all B gathered rows.
+struct LogitsParams {
+  CUtensorMap a_map[2];  // dir 0: I_g, dir 1: T_g   box {64, 128}
+  CUtensorMap b_map[2];  // dir 0: T_g, dir 1: I_g   box {64, 256}
+  int B, b, Dp, rank;
+  int nchunk, chunk_cols, tiles_per_chunk, row_tiles;
+  float tl2e;  // t * log2(e)
+  // FWD outputs
+  float2* stats;   // [2][nchunk][b]
+  float* target;   // [2][b]  (log2-domain target logit)
+  // GRAD inputs / outputs
+  const float* lse2;    // [2][b]
+  const float* glabel;  // [2][b]
+  __half* G;            // [2][b][ldG]
+  int64_t ldG;
+};
+
+struct GemmProblem {
+  CUtensorMap a_map;
+  CUtensorMap b_map;
+  int a_mn_major, b_mn_major;
+  int M, N;               // valid output extents
+  int m_tiles, n_tiles, k_chunks;
+  int k_chunk_len;        // elements of K per chunk (multiple of 64 unless k_chunks == 1)
+  int k_total;            // total K extent
+  int a_k_off, b_k_off;   // added to the K coordinate of MN-major operands
+  int a_row_off;          // added to the row coordinate of a K-major A
+  float* out;
+  int64_t ld_out;         // floats between rows
+  int64_t row_div;        // output row r -> (r / row_div) * stride_hi + (r % row_div) * ld_out
+  int64_t stride_hi;
+  int64_t chunk_stride;   // floats between k-chunk partial outputs
+};
+constexpr int MAX_PROBLEMS = 2;
+struct GemmParams {
+  GemmProblem prob[MAX_PROBLEMS];
+  int nprob;
+  int units[MAX_PROBLEMS + 1];  // prefix sums of per-problem unit counts
+};
+
+// --------------------------------------------------------- shared helpers
+__device__ __forceinline__ void load_operand(const CUtensorMap* map, int mn_major, uint8_t* dst, uint64_t* bar,
+                                             int mn0, int k0, int rows, uint64_t policy) {
+  if (!mn_major) {
+    ptx::tma_load_2d(dst, map, bar, k0, mn0, policy);  // box {64 (K), rows}
+  } else {
+    for (int j = 0; j < rows / 64; ++j)  // box {64 (MN), 64 (K)} per 8 KiB atom column
+      ptx::tma_load_2d(dst + j * 8192, map, bar, mn0 + j * 64, k0, policy);
+  }
+}
+
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int mn_major, int kk) {
+  return mn_major ? ptx::smem_desc_sw128(base + kk * 2048, 8192, 1024)  // 16 K-rows of 128 B per MMA
+                  : ptx::smem_desc_sw128(base + kk * 32, 16, 1024);     // 16 K-elements = 32 B per MMA
+}
+
+struct Pipe {
+  uint32_t stage = 0, phase = 0;
+  __device__ __forceinline__ void advance() {
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+};
+
+__device__ __forceinline__ uint8_t* smem_base(uint8_t* raw) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+}
+
+// MMA issue for one accumulator tile: nk k-blocks of BK, 4 UMMAs each.
+__device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe& pipe, int nk, uint32_t d_tmem,
+                                         uint32_t idesc, int a_mn, int b_mn) {
+  for (int kb = 0; kb < nk; ++kb) {
+    ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
+    ptx::tc_fence_after();
+    const uint32_t a_base = ptx::smem_u32(tiles + pipe.stage * STAGE_BYTES);
+    const uint32_t b_base = a_base + A_STAGE_BYTES;
+#pragma unroll
+    for (int kk = 0; kk < BK / 16; ++kk) {
+      ptx::umma_f16(d_tmem, operand_desc(a_base, a_mn, kk), operand_desc(b_base, b_mn, kk), idesc,
+                    (kb | kk) != 0);
+    }
+    ptx::umma_commit(&ctl->empty[pipe.stage]);  // smem slot free once these MMAs retire
+    pipe.advance();
+  }
+}
+
+__device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane) {
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&ctl->full[s], 1);
+      ptx::mbar_init(&ctl->empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&ctl->tfull[i], 1);
+      ptx::mbar_init(&ctl->tempty[i], 4);  // one arrive per epilogue warp
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(&ctl->tmem_base, TMEM_COLS);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+}
+
+__device__ __forceinline__ void kernel_epilogue(SmemCtl* ctl, int warp) {
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(ctl->tmem_base, TMEM_COLS);
+  }
+}
+
+// =====================================================================
+// logits kernel: S tiles for both directions.
+//   FWD : unit = (dir, row tile, column chunk); tiles = column tiles of the chunk,
+//         epilogue keeps a per-row online (max, sum-exp) across the tiles.
+//   GRAD: unit = (dir, row tile, column chunk, column tile); epilogue writes G.
+// Both kinds walk identical tiles (same column origin and K order), so the
+// recomputed S in GRAD is bit-identical to the forward S.
+// =====================================================================
+enum { KIND_FWD = 0, KIND_GRAD = 1 };
+
+template <int KIND>
+__global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_constant__ LogitsParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* tiles = smem_base(smem_raw);
+  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + STAGES * STAGE_BYTES);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    for (int d = 0; d < 2; ++d) {
+      ptx::prefetch_tmap(&p.a_map[d]);
+      ptx::prefetch_tmap(&p.b_map[d]);
+    }
+  }
+  kernel_prologue(ctl, warp, lane);
+
+  const int per_dir = p.row_tiles * p.nchunk * (KIND == KIND_FWD ? 1 : p.tiles_per_chunk);
+  const int num_units = 2 * per_dir;
+  const int tiles_per_unit = KIND == KIND_FWD ? p.tiles_per_chunk : 1;
+  const int nk = p.Dp / BK;
+
+  auto decode = [&](int u, int& dir, int& rt, int& ch, int& t0) {
+    dir = u / per_dir;
+    int rem = u - dir * per_dir;
+    if (KIND == KIND_FWD) {
+      rt = rem / p.nchunk;
+      ch = rem - rt * p.nchunk;
+      t0 = 0;
+    } else {
+      const int per_rt = p.nchunk * p.tiles_per_chunk;
+      rt = rem / per_rt;
+      rem -= rt * per_rt;
+      ch = rem / p.tiles_per_chunk;
+      t0 = rem - ch * p.tiles_per_chunk;
+    }
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      Pipe pipe;
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        int dir, rt, ch, t0;
+        decode(u, dir, rt, ch, t0);
+        const int a_row = p.rank * p.b + rt * BM;
+        for (int ti = 0; ti < tiles_per_unit; ++ti) {
+          const int col0 = ch * p.chunk_cols + (t0 + ti) * BN;
+          for (int kb = 0; kb < nk; ++kb) {
+            ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
+            uint8_t* st = tiles + pipe.stage * STAGE_BYTES;
+            ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], STAGE_BYTES);
+            ptx::tma_load_2d(st, &p.a_map[dir], &ctl->full[pipe.stage], kb * BK, a_row, ptx::kEvictLast);
+            ptx::tma_load_2d(st + A_STAGE_BYTES, &p.b_map[dir], &ctl->full[pipe.stage], kb * BK, col0,
+                             ptx::kEvictLast);
+            pipe.advance();
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = ptx::instr_desc_f16(BM, BN, 1, 1, 0, 0);  // bf16 x bf16, both K-major
+      Pipe pipe;
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        for (int ti = 0; ti < tiles_per_unit; ++ti, ++it) {
+          const uint32_t buf = it & 1, use = it >> 1;
+          ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
+          ptx::tc_fence_after();
+          mma_tile(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, 0, 0);
+          ptx::umma_commit(&ctl->tfull[buf]);
+        }
+      }
+    }
+  } else {  // ---------------------------- epilogue warps 2..5
+    const int quad = warp & 3;
+    const int r_in_tile = quad * 32 + lane;
+    uint32_t it = 0;
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      int dir, rt, ch, t0;
+      decode(u, dir, rt, ch, t0);
+      const int row = rt * BM + r_in_tile;        // local row
+      const bool row_ok = row < p.b;
+      const int label = p.rank * p.b + row;        // global column of the positive pair
+      const int chunk_lo = ch * p.chunk_cols;
+      const int chunk_hi = min(chunk_lo + p.chunk_cols, p.B);
+      float m2 = -INFINITY, l = 0.f, yt = 0.f;
+      float lse2 = 0.f, gl = 0.f;
+      __half* grow = nullptr;
+      if (KIND == KIND_GRAD && row_ok) {
+        lse2 = p.lse2[dir * p.b + row];
+        gl = p.glabel[dir * p.b + row];
+        grow = p.G + (int64_t(dir) * p.b + row) * p.ldG;
+      }
+      for (int ti = 0; ti < tiles_per_unit; ++ti, ++it) {
+        const uint32_t buf = it & 1, use = it >> 1;
+        ptx::mbar_wait(&ctl->tfull[buf], use & 1);
+        ptx::tc_fence_after();
+        const int col0 = chunk_lo + (t0 + ti) * BN;
+        const uint32_t taddr = ctl->tmem_base + (uint32_t(quad * 32) << 16) + buf * BN;
+#pragma unroll 1
+        for (int j = 0; j < BN / 32; ++j) {
+          const int cb = col0 + j * 32;
+          if (cb >= chunk_hi) break;  // warp-uniform
+          float v[32];
+          ptx::tmem_ld32(taddr + j * 32, v);
+          if (KIND == KIND_FWD) {
+            float cmax = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float y = (cb + i < chunk_hi) ? v[i] * p.tl2e : -INFINITY;
+              v[i] = y;
+              cmax = fmaxf(cmax, y);
+              if (cb + i == label) yt = y;
+            }
+            const float mnew = fmaxf(m2, cmax);
+            float s = 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float e = ptx::ex2(v[i] - mnew);
+              s += (cb + i == label) ? 0.f : e;
+            }
+            l = l * ptx::ex2(m2 - mnew) + s;
+            m2 = mnew;
+          } else {
+            if (row_ok) {
+              uint32_t h[16];
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                float g0 = ptx::ex2(v[i] * p.tl2e - lse2);
+                float g1 = ptx::ex2(v[i + 1] * p.tl2e - lse2);
+                if (cb + i == label) g0 = gl;
+                if (cb + i + 1 == label) g1 = gl;
+                __half2 hh = __floats2half2_rn(g0, g1);
+                h[i / 2] = *reinterpret_cast<uint32_t*>(&hh);
+              }
+              if (cb + 32 <= chunk_hi) {
+                uint4* dst = reinterpret_cast<uint4*>(grow + cb);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) dst[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+              } else {  // columns past the chunk belong to the next chunk's tiles
+                for (int i = 0; i < 32 && cb + i < chunk_hi; ++i) {
+                  const uint32_t w = h[i / 2];
+                  const unsigned short bits = (i & 1) ? (unsigned short)(w >> 16) : (unsigned short)(w & 0xFFFF);
+                  grow[cb + i] = __ushort_as_half(bits);
+                }
+              }
+            }
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&ctl->tempty[buf]);
+      }
+      if (KIND == KIND_FWD && row_ok) {
+        p.stats[(int64_t(dir) * p.nchunk + ch) * p.b + row] = make_float2(m2, l);
+        if (label >= chunk_lo && label < chunk_hi) p.target[dir * p.b + row] = yt;
+      }
+    }
+  }
+  kernel_epilogue(ctl, warp);
+}
+
+// =====================================================================
+// Grouped f16 GEMM with fp32 tile outputs.
+//   unit = (problem, m tile, n tile, k chunk); one accumulator tile per unit.
+// =====================================================================
+__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* tiles = smem_base(smem_raw);
+  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + STAGES * STAGE_BYTES);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < p.nprob; ++i) {
+      ptx::prefetch_tmap(&p.prob[i].a_map);
+      ptx::prefetch_tmap(&p.prob[i].b_map);
+    }
+  }
+  kernel_prologue(ctl, warp, lane);
+
+  const int num_units = p.units[p.nprob];
+  // unit -> (problem, mt, nt, kc); nt fastest so CTAs sharing an A tile run together.
+  auto decode = [&](int u, int& pi, int& mt, int& nt, int& kc) {
+    pi = 0;
+    while (pi + 1 < p.nprob && u >= p.units[pi + 1]) ++pi;
+    int rem = u - p.units[pi];
+    const GemmProblem& q = p.prob[pi];
+    nt = rem % q.n_tiles;
+    rem /= q.n_tiles;
+    kc = rem % q.k_chunks;
+    mt = rem / q.k_chunks;
+  };
+  auto k_range = [&](const GemmProblem& q, int kc, int& k0, int& nk) {
+    k0 = kc * q.k_chunk_len;
+    const int k1 = min(k0 + q.k_chunk_len, q.k_total);
+    nk = (k1 - k0 + BK - 1) / BK;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      Pipe pipe;
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        int pi, mt, nt, kc, k0, nk;
+        decode(u, pi, mt, nt, kc);
+        const GemmProblem& q = p.prob[pi];
+        k_range(q, kc, k0, nk);
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
+          uint8_t* st = tiles + pipe.stage * STAGE_BYTES;
+          ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], STAGE_BYTES);
+          const int k = k0 + kb * BK;
+          if (q.a_mn_major)
+            load_operand(&q.a_map, 1, st, &ctl->full[pipe.stage], mt * BM, k + q.a_k_off, BM, ptx::kEvictFirst);
+          else
+            load_operand(&q.a_map, 0, st, &ctl->full[pipe.stage], mt * BM + q.a_row_off, k, BM, ptx::kEvictFirst);
+          load_operand(&q.b_map, q.b_mn_major, st + A_STAGE_BYTES, &ctl->full[pipe.stage], nt * BN,
+                       k + q.b_k_off, BN, ptx::kEvictLast);
+          pipe.advance();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      Pipe pipe;
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+        int pi, mt, nt, kc, k0, nk;
+        decode(u, pi, mt, nt, kc);
+        const GemmProblem& q = p.prob[pi];
+        k_range(q, kc, k0, nk);
+        const uint32_t idesc = ptx::instr_desc_f16(BM, BN, 0, 0, q.a_mn_major, q.b_mn_major);  // f16 x f16
+        const uint32_t buf = it & 1, use = it >> 1;
+        ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
+        ptx::tc_fence_after();
+        mma_tile(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, q.a_mn_major, q.b_mn_major);
+        ptx::umma_commit(&ctl->tfull[buf]);
+      }
+    }
+  } else {  // ---------------------------- epilogue warps
+    const int quad = warp & 3;
+    uint32_t it = 0;
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+      int pi, mt, nt, kc;
+      decode(u, pi, mt, nt, kc);
+      const GemmProblem& q = p.prob[pi];
+      const uint32_t buf = it & 1, use = it >> 1;
+      ptx::mbar_wait(&ctl->tfull[buf], use & 1);
+      ptx::tc_fence_after();
+      const int row = mt * BM + quad * 32 + lane;
+      float* orow = nullptr;
+      if (row < q.M)
+        orow = q.out + kc * q.chunk_stride + (row / q.row_div) * q.stride_hi + (row % q.row_div) * q.ld_out;
+      const uint32_t taddr = ctl->tmem_base + (uint32_t(quad * 32) << 16) + buf * BN;
+#pragma unroll 1
+      for (int j = 0; j < BN / 32; ++j) {
+        const int c0 = nt * BN + j * 32;
+        if (c0 >= q.N) break;  // warp-uniform
+        float v[32];
+        ptx::tmem_ld32(taddr + j * 32, v);
+        if (orow) {
+          if (c0 + 32 <= q.N) {
+            float4* dst = reinterpret_cast<float4*>(orow + c0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          } else {
+            for (int i = 0; i < 32 && c0 + i < q.N; ++i) orow[c0 + i] = v[i];
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&ctl->tempty[buf]);
+    }
+  }
+  kernel_epilogue(ctl, warp);
+}
+
+// =====================================================================
+// Small HBM-bound kernels
+// =====================================================================
+template <typename T>
+__device__ __forceinline__ float load_as_float(const void* p, int64_t i) {
+  return static_cast<float>(static_cast<const T*>(p)[i]);
+}
+template <>
+__device__ __forceinline__ float load_as_float<__nv_bfloat16>(const void* p, int64_t i) {
+  return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
+}
+template <>
+__device__ __forceinline__ float load_as_float<__half>(const void* p, int64_t i) {
+  return __half2float(static_cast<const __half*>(p)[i]);
+}
+
+// Round local features to bf16, pad D..Dp with zeros: out [2][b][Dp].
+// f64 inputs are rounded directly f64 -> bf16 (one rounding, like the reference's data).
+template <typename T>
+__global__ void pack_kernel(const void* I, const void* Tm, int64_t ldI, int64_t ldT, int b, int D, int Dp,
+                            __nv_bfloat16* out, Status* status) {
+  const int64_t total = int64_t(2) * b * Dp;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int c = int(i % Dp);
+    const int64_t rr = i / Dp;
+    const int dir = int(rr / b), r = int(rr % b);
+    __nv_bfloat16 o = __float2bfloat16_rn(0.f);
+    if (c < D) {
+      if constexpr (sizeof(T) == 8) {
+        const double x = static_cast<const double*>(dir ? Tm : I)[r * (dir ? ldT : ldI) + c];
+        bad |= !isfinite(x);
+        o = __double2bfloat16(x);
+      } else {
+        const float x = load_as_float<T>(dir ? Tm : I, r * (dir ? ldT : ldI) + c);
+        bad |= !isfinite(x);
+        o = __float2bfloat16_rn(x);
+      }
+    }
+    out[i] = o;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&status->flags, FLAG_INPUT_NONFINITE);
+}
+
+__global__ void clear_status_kernel(Status* s) {
+  s->loss = 0.0;
+  s->flags = 0;
+}
+
+// gathered [N][2][b][Dp] bf16 -> feat [2][B][Dp] bf16 and feat16 [2][B][Dp] f16. 8 elements per thread.
+__global__ void unpack_kernel(const uint4* gathered, int N, int b, int Dp, uint4* feat, uint4* feat16) {
+  const int vec_per_row = Dp / 8;
+  const int64_t total = int64_t(N) * 2 * b * vec_per_row;
+  const int64_t B = int64_t(N) * b;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int vc = int(i % vec_per_row);
+    int64_t rr = i / vec_per_row;
+    const int r = int(rr % b);
+    rr /= b;
+    const int dir = int(rr % 2);
+    const int n = int(rr / 2);
+    const uint4 x = gathered[i];
+    const int64_t o = (dir * B + int64_t(n) * b + r) * vec_per_row + vc;
+    feat[o] = x;
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
+    uint4 y;
+    __half2* hy = reinterpret_cast<__half2*>(&y);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hy[k] = __float22half2_rn(__bfloat1622float2(h[k]));
+    feat16[o] = y;
+  }
+}
+
+// Per (dir,row): fixed-tree combine of the column-chunk (max, sum-exp) partials.
+//   lse2 (log2 domain), ce = -log softmax[label], glabel = P_label - 1 = -(sum_{j!=label} P_j).
+__global__ void stats_combine_kernel(const float2* stats, const float* target, int nchunk, int b, float* lse2_out,
+                                     float* glabel_out, float* ce_out, Status* status) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * b) return;
+  const int dir = i / b, r = i % b;
+  float m = -INFINITY;
+  float ms[8], ls[8];
+  for (int c = 0; c < nchunk; ++c) {
+    const float2 s = stats[(int64_t(dir) * nchunk + c) * b + r];
+    ms[c & 7] = s.x;
+    ls[c & 7] = s.y;
+    m = fmaxf(m, s.x);
+  }
+  float lo;
+  if (nchunk == 8) {  // balanced tree ((0+1)+(2+3))+((4+5)+(6+7))
+    float t[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) t[c] = ls[c] * ptx::ex2(ms[c] - m);
+    lo = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
+  } else {  // non-canonical: ascending chunk order
+    lo = 0.f;
+    for (int c = 0; c < nchunk; ++c) {
+      const float2 s = stats[(int64_t(dir) * nchunk + c) * b + r];
+      lo += s.y * ptx::ex2(s.x - m);
+    }
+  }
+  const float yt = target[i];
+  const float et = ptx::ex2(yt - m);
+  const float lall = lo + et;
+  const float lse2 = m + log2f(lall);
+  const float dlt = m - yt;  // >= 0
+  const float ce = dlt < 64.f ? log1pf(lo * exp2f(dlt)) : dlt * LN2 + logf(lall);
+  lse2_out[i] = lse2;
+  glabel_out[i] = -lo / lall;
+  ce_out[i] = ce;
+  if (!isfinite(ce) || !isfinite(lse2)) atomicOr(&status->flags, FLAG_LOSS_NONFINITE);
+}
+
+// Sender-side fixed-tree sum of this rank's cpr canonical chunk partials:
+//   xpart [2][cpr][B][Dp] -> send [N][2][b][Dp] (destination-major). float4 per thread.
+__global__ void presum_kernel(const float4* xpart, int cpr, int N, int b, int Dp, float4* send) {
+  const int v4 = Dp / 4;
+  const int64_t B = int64_t(N) * b;
+  const int64_t per_g = B * v4;
+  const int64_t total = 2 * per_g;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int g = int(i / per_g);
+    const int64_t rem = i - g * per_g;
+    const int64_t c = rem / v4;
+    const int vc = int(rem % v4);
+    const float4* src = xpart + (int64_t(g) * cpr) * per_g + rem;
+    float4 acc[8];
+    for (int k = 0; k < cpr; ++k) acc[k] = src[k * per_g];
+    for (int w = 1; w < cpr; w <<= 1)  // balanced binary tree over chunk index
+      for (int k = 0; k + w < cpr; k += 2 * w) {
+        acc[k].x += acc[k + w].x;
+        acc[k].y += acc[k + w].y;
+        acc[k].z += acc[k + w].z;
+        acc[k].w += acc[k + w].w;
+      }
+    const int64_t dest = c / b, r = c % b;
+    send[((dest * 2 + g) * b + r) * v4 + vc] = acc[0];
+  }
+}
+
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4neg(float4 a) { return make_float4(-a.x, -a.y, -a.z, -a.w); }
+
+// Owner combine: d_g[r] = s * (intra_g[r] + tree_src(+/- recv[src][g][r])), written b x D (ld_out).
+// Source tree: balanced over ascending src when N is a power of two (the top
+// levels of the canonical 8-chunk tree), ascending sequential otherwise.
+__global__ void combine_kernel(const float4* intra, const float4* recv, int N, int rank, int b, int Dp, int D,
+                               float s, int flip, float* d_image, float* d_text, int64_t ld_out, Status* status) {
+  const int v4 = Dp / 4;
+  const int64_t per_g = int64_t(b) * v4;
+  const int64_t total = 2 * per_g;
+  const bool pow2 = (N & (N - 1)) == 0;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int g = int(i / per_g);
+    const int64_t rem = i - g * per_g;
+    const int r = int(rem / v4), vc = int(rem % v4);
+    float4 cross;
+    if (pow2 && N <= 8) {
+      float4 acc[8];
+      for (int src = 0; src < N; ++src) {
+        float4 x = recv[((int64_t(src) * 2 + g) * b) * v4 + rem];
+        acc[src] = (flip && src != rank) ? f4neg(x) : x;
+      }
+      for (int w = 1; w < N; w <<= 1)
+        for (int k = 0; k + w < N; k += 2 * w) acc[k] = f4add(acc[k], acc[k + w]);
+      cross = acc[0];
+    } else {
+      cross = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int src = 0; src < N; ++src) {
+        float4 x = recv[((int64_t(src) * 2 + g) * b) * v4 + rem];
+        cross = (src == 0) ? ((flip && src != rank) ? f4neg(x) : x) : f4add(cross, (flip && src != rank) ? f4neg(x) : x);
+      }
+    }
+    const float4 t = f4add(intra[i], cross);
+    float o[4] = {t.x * s, t.y * s, t.z * s, t.w * s};
+    float* out = (g == 0 ? d_image : d_text) + int64_t(r) * ld_out;
+    for (int k = 0; k < 4; ++k) {
+      const int c = vc * 4 + k;
+      if (c < D) {
+        out[c] = o[k];
+        bad |= !isfinite(o[k]);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&status->flags, FLAG_GRAD_NONFINITE);
+}
+
+// Full-size contribution of this rank (reference LocalGradContribution):
+//   d_full_g[c] = s * (send slab_g[c] + [c in own rows] intra_g[c - rank*b]), rows outside negated if flip.
+__global__ void contribution_kernel(const float4* intra, const float4* send, int N, int rank, int b, int Dp, int D,
+                                    float s, int flip, float* d_image, float* d_text, int64_t ld_out,
+                                    Status* status) {
+  const int v4 = Dp / 4;
+  const int64_t B = int64_t(N) * b;
+  const int64_t per_g = B * v4;
+  const int64_t total = 2 * per_g;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int g = int(i / per_g);
+    const int64_t rem = i - g * per_g;
+    const int64_t c = rem / v4;
+    const int vc = int(rem % v4);
+    const int64_t dest = c / b, r = c % b;
+    float4 x = send[((dest * 2 + g) * b + r) * v4 + vc];
+    const bool own = dest == rank;
+    if (own) x = f4add(intra[(int64_t(g) * b + r) * v4 + vc], x);
+    float sg = (flip && !own) ? -s : s;
+    float o[4] = {x.x * sg, x.y * sg, x.z * sg, x.w * sg};
+    float* out = (g == 0 ? d_image : d_text) + c * ld_out;
+    for (int k = 0; k < 4; ++k) {
+      const int cc = vc * 4 + k;
+      if (cc < D) {
+        out[cc] = o[k];
+        bad |= !isfinite(o[k]);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&status->flags, FLAG_GRAD_NONFINITE);
+}
+
+// Loss: sum over the [N][2][b] per-row ce in an order fixed by the global row
+// index (independent of N), in f64, / (2 * N * b).  One block of 1024 threads.
+__global__ void loss_kernel(const float* ce_all, int N, int b, Status* status) {
+  __shared__ double red[1024];
+  const int64_t B = int64_t(N) * b;
+  double acc = 0.0;
+  for (int dir = 0; dir < 2; ++dir)
+    for (int64_t gidx = threadIdx.x; gidx < B; gidx += blockDim.x) {
+      const int64_t n = gidx / b, r = gidx % b;
+      acc += double(ce_all[(n * 2 + dir) * b + r]);
+    }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double loss = red[0] / double(2 * B);
+    status->loss = loss;
+    if (!isfinite(loss)) status->flags |= FLAG_LOSS_NONFINITE;
+  }
+}
+
+// =====================================================================
+// Host side
+// =====================================================================
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+  do {                                                                                         \
+    cudaError_t e_ = (expr);                                                                   \
+    if (e_ != cudaSuccess) return fail(DISCO_CUDA_ERROR, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+struct Geometry {
+  int64_t B, D, Dp, b, ldG;
+  int N, rank;
+  int nchunk, cpr;        // canonical chunks, chunks per rank
+  int chunk_cols;         // B / nchunk
+  int64_t off[DISCO_R_COUNT];
+  int64_t len[DISCO_R_COUNT];
+  int64_t total;
+};
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
+  if (world < 1) return fail(DISCO_LAYOUT_ERROR, "world size must be >= 1, got %d", world);
+  if (B < 1) return fail(DISCO_LAYOUT_ERROR, "global batch must be >= 1, got %lld", (long long)B);
+  if (B % world != 0)
+    return fail(DISCO_LAYOUT_ERROR, "global batch %lld is not divisible by world size %d", (long long)B, world);
+  if (rank < 0 || rank >= world) return fail(DISCO_LAYOUT_ERROR, "rank %d outside [0, %d)", rank, world);
+  if (D < 1) return fail(DISCO_SHAPE_ERROR, "feature dim must be >= 1, got %lld", (long long)D);
+  if (B > (int64_t(1) << 30) || D > 65536) return fail(DISCO_SHAPE_ERROR, "problem too large");
+  g->B = B;
+  g->D = D;
+  g->Dp = round_up(D, 64);
+  g->N = world;
+  g->rank = rank;
+  g->b = B / world;
+  g->ldG = round_up(B, 64);
+  if (B % 1024 == 0 && 8 % world == 0) {
+    g->nchunk = 8;
+    g->cpr = 8 / world;
+  } else {
+    g->nchunk = world;
+    g->cpr = 1;
+  }
+  g->chunk_cols = int(B / g->nchunk);
+  const int64_t b = g->b, Dp = g->Dp, N = world;
+  int64_t len[DISCO_R_COUNT];
+  len[DISCO_R_PACK] = 2 * b * Dp * 2;
+  len[DISCO_R_GATHER] = N > 1 ? N * 2 * b * Dp * 2 : 0;
+  len[DISCO_R_FEAT] = 2 * B * Dp * 2;
+  len[DISCO_R_FEAT16] = 2 * B * Dp * 2;
+  len[DISCO_R_STATS] = 2 * int64_t(g->nchunk) * b * 8;
+  len[DISCO_R_ROWS] = 4 * 2 * b * 4;
+  len[DISCO_R_CE] = 2 * b * 4;
+  len[DISCO_R_CE_ALL] = N * 2 * b * 4;
+  len[DISCO_R_G] = 2 * b * g->ldG * 2;
+  len[DISCO_R_XPART] = g->cpr > 1 ? 2 * int64_t(g->cpr) * B * Dp * 4 : 0;
+  len[DISCO_R_SEND] = N * 2 * b * Dp * 4;
+  len[DISCO_R_RECV] = N > 1 ? N * 2 * b * Dp * 4 : 0;
+  len[DISCO_R_INTRA] = 2 * b * Dp * 4;
+  len[DISCO_R_STATUS] = 64;
+  int64_t off = 0;
+  for (int r = 0; r < DISCO_R_COUNT; ++r) {
+    g->off[r] = off;
+    g->len[r] = len[r];
+    off += round_up(len[r], 1024);
+  }
+  // aliases for the single-rank case
+  if (N == 1) {
+    g->off[DISCO_R_GATHER] = g->off[DISCO_R_PACK];
+    g->len[DISCO_R_GATHER] = g->len[DISCO_R_PACK];
+    g->off[DISCO_R_RECV] = g->off[DISCO_R_SEND];
+    g->len[DISCO_R_RECV] = g->len[DISCO_R_SEND];
+  }
+  g->total = off;
+  return DISCO_OK;
+}
+
+template <typename T>
+T* region(void* ws, const Geometry& g, int r) {
+  return reinterpret_cast<T*>(static_cast<uint8_t*>(ws) + g.off[r]);
+}
+
+// ------------------------------------------------------------ tensor maps
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 2-D map over a row-major [outer][inner] 16-bit matrix with row pitch `pitch_elems`.
+int make_map(CUtensorMap* map, bool bf16, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_elems,
+             uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return fail(DISCO_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(DISCO_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d) inner=%llu outer=%llu box=%u,%u", int(r),
+                (unsigned long long)inner, (unsigned long long)outer, box_inner, box_outer);
+  return DISCO_OK;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename K>
+int prepare_kernel(K kernel) {
+  // Per-device attribute; cheap enough to set on every launch.
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
+  return DISCO_OK;
+}
+
+int grid_for(int64_t units) { return int(std::min<int64_t>(units, sm_count())); }
+
+int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t st) {
+  LogitsParams p;
+  memset(&p, 0, sizeof(p));
+  const __nv_bfloat16* feat = region<__nv_bfloat16>(ws, g, DISCO_R_FEAT);
+  const __nv_bfloat16* I_g = feat;
+  const __nv_bfloat16* T_g = feat + g.B * g.Dp;
+  int rc;
+  if ((rc = make_map(&p.a_map[0], true, I_g, g.Dp, g.B, g.Dp, 64, BM))) return rc;
+  if ((rc = make_map(&p.a_map[1], true, T_g, g.Dp, g.B, g.Dp, 64, BM))) return rc;
+  if ((rc = make_map(&p.b_map[0], true, T_g, g.Dp, g.B, g.Dp, 64, BN))) return rc;
+  if ((rc = make_map(&p.b_map[1], true, I_g, g.Dp, g.B, g.Dp, 64, BN))) return rc;
+  p.B = int(g.B);
+  p.b = int(g.b);
+  p.Dp = int(g.Dp);
+  p.rank = g.rank;
+  p.nchunk = g.nchunk;
+  p.chunk_cols = g.chunk_cols;
+  p.tiles_per_chunk = (g.chunk_cols + BN - 1) / BN;
+  p.row_tiles = int((g.b + BM - 1) / BM);
+  p.tl2e = t * LOG2E;
+  float* rows = region<float>(ws, g, DISCO_R_ROWS);
+  p.stats = region<float2>(ws, g, DISCO_R_STATS);
+  p.target = rows;
+  p.lse2 = rows + 2 * g.b;
+  p.glabel = rows + 4 * g.b;
+  p.G = region<__half>(ws, g, DISCO_R_G);
+  p.ldG = g.ldG;
+  const int64_t units =
+      int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_FWD ? 1 : p.tiles_per_chunk);
+  if (kind == KIND_FWD) {
+    if ((rc = prepare_kernel(logits_kernel<KIND_FWD>))) return rc;
+    logits_kernel<KIND_FWD><<<grid_for(units), NUM_THREADS, SMEM_BYTES, st>>>(p);
+    count_launch();
+  } else {
+    if ((rc = prepare_kernel(logits_kernel<KIND_GRAD>))) return rc;
+    logits_kernel<KIND_GRAD><<<grid_for(units), NUM_THREADS, SMEM_BYTES, st>>>(p);
+    count_launch();
+  }
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int launch_gemm(GemmParams& p, cudaStream_t st) {
+  p.units[0] = 0;
+  for (int i = 0; i < p.nprob; ++i)
+    p.units[i + 1] = p.units[i] + p.prob[i].m_tiles * p.prob[i].n_tiles * p.prob[i].k_chunks;
+  int rc;
+  if ((rc = prepare_kernel(gemm_kernel))) return rc;
+  gemm_kernel<<<grid_for(p.units[p.nprob]), NUM_THREADS, SMEM_BYTES, st>>>(p);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int elementwise_grid(int64_t n, int threads) {
+  return int(std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, int64_t(sm_count()) * 16)));
+}
+
+}  // namespace disco
+
+// =====================================================================
+// C ABI
+// =====================================================================
+using namespace disco;
+
+extern "C" {
+
+int disco_b200_abi_version(void) { return DISCO_B200_ABI_VERSION; }
+
+int64_t disco_b200_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char* disco_b200_last_error(void) { return g_last_error.c_str(); }
+
+int disco_b200_workspace_bytes(int64_t B, int64_t D, int world, int rank, int64_t* bytes) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  *bytes = g.total;
+  return DISCO_OK;
+}
+
+int disco_b200_ws_region(int64_t B, int64_t D, int world, int rank, int reg, int64_t* offset, int64_t* bytes) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (reg < 0 || reg >= DISCO_R_COUNT) return fail(DISCO_SHAPE_ERROR, "unknown workspace region %d", reg);
+  *offset = g.off[reg];
+  *bytes = g.len[reg];
+  return DISCO_OK;
+}
+
+int disco_b200_chunking(int64_t B, int world, int* nchunk, int* chunks_per_rank) {
+  Geometry g;
+  int rc = make_geometry(B, 1, world, 0, &g);
+  if (rc) return rc;
+  *nchunk = g.nchunk;
+  *chunks_per_rank = g.cpr;
+  return DISCO_OK;
+}
+
+int disco_b200_pack(void* ws, int64_t B, int64_t D, int world, int rank, const void* local_I, const void* local_T,
+                    int64_t ld_I, int64_t ld_T, int dtype, int clear_status, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (ld_I < D || ld_T < D) return fail(DISCO_SHAPE_ERROR, "row stride smaller than D");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Status* status = region<Status>(ws, g, DISCO_R_STATUS);
+  if (clear_status) {
+    clear_status_kernel<<<1, 1, 0, st>>>(status);
+    count_launch();
+  }
+  __nv_bfloat16* out = region<__nv_bfloat16>(ws, g, DISCO_R_PACK);
+  const int64_t n = 2 * g.b * g.Dp;
+  const int grid = elementwise_grid(n, 256);
+  switch (dtype) {
+    case DISCO_F32:
+      pack_kernel<float><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, status);
+      break;
+    case DISCO_BF16:
+      pack_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out,
+                                                       status);
+      break;
+    case DISCO_F16:
+      pack_kernel<__half><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, status);
+      break;
+    case DISCO_F64:
+      pack_kernel<double><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, status);
+      break;
+    default:
+      return fail(DISCO_SHAPE_ERROR, "unsupported dtype code %d", dtype);
+  }
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t nvec = int64_t(world) * 2 * g.b * (g.Dp / 8);
+  unpack_kernel<<<elementwise_grid(nvec, 256), 256, 0, st>>>(
+      region<uint4>(ws, g, DISCO_R_GATHER), world, int(g.b), int(g.Dp), region<uint4>(ws, g, DISCO_R_FEAT),
+      region<uint4>(ws, g, DISCO_R_FEAT16));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  if ((rc = launch_logits(KIND_FWD, ws, g, t, st))) return rc;
+  float* rows = region<float>(ws, g, DISCO_R_ROWS);
+  const int n = int(2 * g.b);
+  stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(region<float2>(ws, g, DISCO_R_STATS), rows, g.nchunk,
+                                                        int(g.b), rows + 2 * g.b, rows + 4 * g.b,
+                                                        region<float>(ws, g, DISCO_R_CE),
+                                                        region<Status>(ws, g, DISCO_R_STATUS));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((rc = launch_logits(KIND_GRAD, ws, g, t, st))) return rc;
+
+  // cross GEMMs: X_g = G_{d'}^T . A_{d'} (local rows), g = image <- d' = t2i (1), g = text <- d' = i2t (0)
+  const __half* G = region<__half>(ws, g, DISCO_R_G);
+  const __half* f16 = region<__half>(ws, g, DISCO_R_FEAT16);
+  const __half* I16 = f16;
+  const __half* T16 = f16 + g.B * g.Dp;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.nprob = 2;
+  const int64_t Bc = g.B / g.nchunk;  // canonical chunk rows
+  for (int gi = 0; gi < 2; ++gi) {
+    GemmProblem& q = p.prob[gi];
+    const int dsrc = gi == 0 ? 1 : 0;
+    const __half* Gd = G + int64_t(dsrc) * g.b * g.ldG;
+    const __half* Ad = gi == 0 ? T16 : I16;  // image grad uses T_n, text grad uses I_n
+    if ((rc = make_map(&q.a_map, false, Gd, g.B, g.b, g.ldG, 64, 64))) return rc;   // MN-major G^T
+    if ((rc = make_map(&q.b_map, false, Ad, g.Dp, g.B, g.Dp, 64, 64))) return rc;  // MN-major features
+    q.a_mn_major = 1;
+    q.b_mn_major = 1;
+    q.M = int(g.B);
+    q.N = int(g.Dp);
+    q.m_tiles = int((g.B + BM - 1) / BM);
+    q.n_tiles = int((g.Dp + BN - 1) / BN);
+    q.k_chunks = g.cpr;
+    q.k_chunk_len = int(g.cpr > 1 ? Bc : g.b);
+    q.k_total = int(g.b);
+    q.a_k_off = 0;
+    q.b_k_off = int(int64_t(g.rank) * g.b);
+    q.a_row_off = 0;
+    if (g.cpr > 1) {  // canonical partials [2][cpr][B][Dp]
+      q.out = region<float>(ws, g, DISCO_R_XPART) + int64_t(gi) * g.cpr * g.B * g.Dp;
+      q.ld_out = g.Dp;
+      q.row_div = int64_t(1) << 40;
+      q.stride_hi = 0;
+      q.chunk_stride = g.B * g.Dp;
+    } else {  // directly destination-major send slabs [N][2][b][Dp]
+      q.out = region<float>(ws, g, DISCO_R_SEND) + int64_t(gi) * g.b * g.Dp;
+      q.ld_out = g.Dp;
+      q.row_div = g.b;
+      q.stride_hi = 2 * g.b * g.Dp;
+      q.chunk_stride = 0;
+    }
+  }
+  if ((rc = launch_gemm(p, st))) return rc;
+  if (g.cpr > 1) {
+    const int64_t n = 2 * g.B * (g.Dp / 4);
+    presum_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_XPART), g.cpr, world,
+                                                           int(g.b), int(g.Dp), region<float4>(ws, g, DISCO_R_SEND));
+    count_launch();
+    CUDA_TRY(cudaGetLastError());
+  }
+  return DISCO_OK;
+}
+
+int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int rank, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const __half* G = region<__half>(ws, g, DISCO_R_G);
+  const __half* f16 = region<__half>(ws, g, DISCO_R_FEAT16);
+  const __half* I16 = f16;
+  const __half* T16 = f16 + g.B * g.Dp;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.nprob = 2;
+  for (int gi = 0; gi < 2; ++gi) {  // Y_image = G_i . T_g ; Y_text = G_t . I_g
+    GemmProblem& q = p.prob[gi];
+    const __half* Gd = G + int64_t(gi) * g.b * g.ldG;
+    const __half* Cd = gi == 0 ? T16 : I16;
+    if ((rc = make_map(&q.a_map, false, Gd, g.B, g.b, g.ldG, 64, BM))) return rc;  // K-major G
+    if ((rc = make_map(&q.b_map, false, Cd, g.Dp, g.B, g.Dp, 64, 64))) return rc;  // MN-major features
+    q.a_mn_major = 0;
+    q.b_mn_major = 1;
+    q.M = int(g.b);
+    q.N = int(g.Dp);
+    q.m_tiles = int((g.b + BM - 1) / BM);
+    q.n_tiles = int((g.Dp + BN - 1) / BN);
+    q.k_chunks = 1;
+    q.k_chunk_len = int(g.B);
+    q.k_total = int(g.B);
+    q.out = region<float>(ws, g, DISCO_R_INTRA) + int64_t(gi) * g.b * g.Dp;
+    q.ld_out = g.Dp;
+    q.row_div = int64_t(1) << 40;
+    q.stride_hi = 0;
+    q.chunk_stride = 0;
+  }
+  return launch_gemm(p, st);
+}
+
+int disco_b200_combine(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip, float* d_image,
+                       float* d_text, int64_t ld_out, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (ld_out < D) return fail(DISCO_SHAPE_ERROR, "output row stride smaller than D");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const float s = float(0.5 * double(t) / double(B));
+  const int64_t n = 2 * g.b * (g.Dp / 4);
+  combine_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
+      region<float4>(ws, g, DISCO_R_INTRA), region<float4>(ws, g, DISCO_R_RECV), world, rank, int(g.b), int(g.Dp),
+      int(D), s, flip, d_image, d_text, ld_out, region<Status>(ws, g, DISCO_R_STATUS));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,
+                            float* d_image_full, float* d_text_full, int64_t ld_out, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (ld_out < D) return fail(DISCO_SHAPE_ERROR, "output row stride smaller than D");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const float s = float(0.5 * double(t) / double(g.b));
+  const int64_t n = 2 * g.B * (g.Dp / 4);
+  contribution_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
+      region<float4>(ws, g, DISCO_R_INTRA), region<float4>(ws, g, DISCO_R_SEND), world, rank, int(g.b), int(g.Dp),
+      int(D), s, flip && world > 1, d_image_full, d_text_full, ld_out, region<Status>(ws, g, DISCO_R_STATUS));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_loss(void* ws, int64_t B, int64_t D, int world, int rank, int local_only, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool local = local_only || world == 1;
+  loss_kernel<<<1, 1024, 0, st>>>(region<float>(ws, g, local ? DISCO_R_CE : DISCO_R_CE_ALL), local ? 1 : world,
+                                  int(g.b), region<Status>(ws, g, DISCO_R_STATUS));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+}  // extern "C"

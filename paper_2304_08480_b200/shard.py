@@ -1,0 +1,380 @@
+"""Per-rank DisCo loss on B200: the drop-in for reference shard.py.
+
+Same names, arguments, validation order and exceptions as the reference
+(/root/reference/pkg/src/disco/shard.py):
+
+  ShardLayout            shard.py:30-58
+  LocalGradContribution  shard.py:61-80
+  shard_slice            shard.py:83-89
+  local_labels           shard.py:92-95
+  local_loss_and_grads   shard.py:98-166
+  disco_step             shard.py:169-208
+
+The arithmetic runs in the sm_100a kernels behind the C ABI
+(include/disco_b200.h); this module only validates, allocates the
+workspace, sequences the stream-ordered calls and issues the collectives
+through the endpoint.  There is no CPU fallback.
+
+Dataflow of ``disco_step`` on rank n (b = B/N):
+  pack (bf16)  -> all_gather [N][2][b][Dp]   (shard.py:190-191)
+  forward      : fused logits GEMM + online LSE + CE (shard.py:134-141)
+  backward_cross: recompute -> f16 G (shard.py:143-146) -> G^T . local feats,
+                 per-canonical-chunk, destination-major slabs (shard.py:149, 151)
+  all_to_all of the slabs (async, overlaps)  \\  replace all_reduce(AVG) +
+  backward_intra: G . gathered feats          /   row slice (shard.py:199-208)
+  combine      : s * (intra + fixed-tree sum of received slabs)
+  all_gather of per-row ce -> fixed-order f64 loss (shard.py:205)
+"""
+
+from dataclasses import dataclass
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from .counters import Counters, tracking
+from .errors import DomainError, LayoutError, ShapeError
+from .fabric import SingleEndpoint
+
+
+@dataclass(frozen=True)
+class ShardLayout:
+    """Which contiguous slice of the global batch a rank owns (shard.py:30-58)."""
+
+    world_size: int
+    global_batch: int
+    rank: int
+
+    def __post_init__(self):
+        if self.world_size < 1:
+            raise LayoutError(f"world size must be >= 1, got {self.world_size}")
+        if self.global_batch < 1:
+            raise LayoutError(f"global batch must be >= 1, got {self.global_batch}")
+        if self.global_batch % self.world_size != 0:
+            raise LayoutError(
+                f"global batch {self.global_batch} is not divisible by "
+                f"world size {self.world_size}")
+        if not 0 <= self.rank < self.world_size:
+            raise LayoutError(f"rank {self.rank} outside [0, {self.world_size})")
+
+    @property
+    def local_batch(self) -> int:
+        return self.global_batch // self.world_size
+
+    @property
+    def row_slice(self) -> slice:
+        start = self.rank * self.local_batch
+        return slice(start, start + self.local_batch)
+
+
+@dataclass(frozen=True)
+class LocalGradContribution:
+    """One rank's full-size (B x D, fp32) additive contribution (shard.py:61-80).
+
+    Finiteness is checked on the device (status flags) before construction.
+    """
+
+    d_image_full: object
+    d_text_full: object
+    local_loss: float
+
+    def __post_init__(self):
+        if tuple(self.d_image_full.shape) != tuple(self.d_text_full.shape):
+            raise ShapeError(
+                f"contribution shapes disagree: {tuple(self.d_image_full.shape)} "
+                f"vs {tuple(self.d_text_full.shape)}")
+
+
+def shard_slice(layout: ShardLayout, full):
+    """Rows [n*b, (n+1)*b) of a global matrix, as a view (shard.py:83-89)."""
+    if full.shape[0] != layout.global_batch:
+        raise LayoutError(
+            f"matrix has {full.shape[0]} rows, layout expects {layout.global_batch}")
+    return full[layout.row_slice]
+
+
+def local_labels(layout: ShardLayout) -> np.ndarray:
+    """Global column indices of the rank's positive pairs: arange(b) + b*rank (shard.py:92-95)."""
+    b = layout.local_batch
+    return np.arange(b) + b * layout.rank
+
+
+# ---------------------------------------------------------------------------
+# Workspace plan
+# ---------------------------------------------------------------------------
+_TORCH_DTYPE_CODE = {
+    torch.float32: _lib.F32,
+    torch.bfloat16: _lib.BF16,
+    torch.float64: _lib.F64,
+    torch.float16: _lib.F16,
+}
+
+
+class Plan:
+    """Device workspace + typed views for one (B, D, N, rank, device) geometry."""
+
+    def __init__(self, B: int, D: int, world: int, rank: int, device: torch.device):
+        self.B, self.D, self.world, self.rank, self.device = B, D, world, rank, device
+        self.b = B // world
+        self.Dp = (D + 63) // 64 * 64
+        self.nchunk, self.cpr = _lib.chunking(B, world)
+        nbytes = _lib.workspace_bytes(B, D, world, rank)
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        self.ptr = self.ws.data_ptr()
+
+        def view(region, dtype):
+            off, size = _lib.ws_region(B, D, world, rank, region)
+            return self.ws[off:off + size].view(dtype)
+
+        self.pack = view(_lib.R_PACK, torch.bfloat16)
+        self.gather = view(_lib.R_GATHER, torch.bfloat16)
+        self.ce = view(_lib.R_CE, torch.float32)
+        self.ce_all = view(_lib.R_CE_ALL, torch.float32)
+        self.send = view(_lib.R_SEND, torch.float32)
+        self.recv = view(_lib.R_RECV, torch.float32)
+        self.status = view(_lib.R_STATUS, torch.uint8)[:16]
+        self.status_host = torch.empty(16, dtype=torch.uint8, pin_memory=True)
+
+    @property
+    def args(self):
+        return (self.ptr, self.B, self.D, self.world, self.rank)
+
+
+_plans = {}
+_plans_lock = threading.Lock()
+
+
+def get_plan(B: int, D: int, world: int, rank: int, device: torch.device) -> Plan:
+    key = (B, D, world, rank, device.index, threading.get_ident())
+    with _plans_lock:
+        plan = _plans.get(key)
+        if plan is None:
+            plan = _plans[key] = Plan(B, D, world, rank, device)
+        return plan
+
+
+def clear_plans() -> None:
+    with _plans_lock:
+        _plans.clear()
+
+
+# ---------------------------------------------------------------------------
+# Input / output staging
+# ---------------------------------------------------------------------------
+def _default_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the DisCo B200 path needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stage(x, device):
+    """Return (device tensor, origin) for a numpy array or torch tensor; 2-D, unit column stride."""
+    origin = "cuda"
+    if isinstance(x, np.ndarray):
+        origin = ("numpy", x.dtype)
+        if x.ndim != 2:
+            raise ShapeError(f"expected a 2-D matrix, got ndim={x.ndim}")
+        x = torch.from_numpy(np.ascontiguousarray(x))
+    if not isinstance(x, torch.Tensor):
+        raise TypeError(f"unsupported feature container {type(x)!r}")
+    if x.dim() != 2:
+        raise ShapeError(f"expected a 2-D matrix, got ndim={x.dim()}")
+    if x.dtype not in _TORCH_DTYPE_CODE:
+        x = x.to(torch.float32)
+    if not x.is_cuda:
+        if origin == "cuda":
+            origin = "cpu"
+        x = x.to(device, non_blocking=x.is_pinned())
+    if x.stride(1) != 1 or (x.shape[0] > 1 and x.stride(0) < x.shape[1]):
+        x = x.contiguous()
+    return x, origin
+
+
+def _unstage(t: torch.Tensor, origin):
+    if origin == "cuda":
+        return t
+    if origin == "cpu":
+        return t.cpu()
+    _, dtype = origin
+    out = t.cpu().numpy()
+    return out.astype(dtype) if np.issubdtype(dtype, np.floating) else out
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _read_status(plan: Plan):
+    plan.status_host.copy_(plan.status, non_blocking=True)
+    torch.cuda.current_stream(plan.device).synchronize()
+    raw = plan.status_host.numpy()
+    loss = float(raw[:8].view(np.float64)[0])
+    flags = int(raw[8:12].view(np.int32)[0])
+    return loss, flags
+
+
+def _raise_on_flags(flags: int) -> None:
+    if flags & 1:
+        raise ValueError("matmul result contains non-finite entries (non-finite input features)")
+    if flags & 2:
+        raise ValueError("cross-entropy logits contains non-finite entries")
+    if flags & 4:
+        raise ValueError("gradient contribution contains non-finite entries")
+
+
+def _check_t(t) -> float:
+    t = float(t)
+    if not t > 0 or not np.isfinite(t):
+        raise DomainError(f"temperature must be positive, got {t}")
+    return t
+
+
+# ---------------------------------------------------------------------------
+# Public entry points
+# ---------------------------------------------------------------------------
+def local_loss_and_grads(layout: ShardLayout, I_gathered, T_gathered, t: float, *,
+                         loss_counters: Counters | None = None,
+                         exchange_counters: Counters | None = None,
+                         flip_cross_rank_sign: bool = False) -> LocalGradContribution:
+    """One rank's loss rows and full-size gradient contribution (shard.py:98-166).
+
+    ``I_gathered`` / ``T_gathered`` are the B x D gathered features (numpy or
+    torch).  Returns B x D fp32 contributions whose rank-mean is the full-batch
+    gradient, and the rank's local loss (mean of its two CE halves).
+    """
+    if t <= 0:
+        raise DomainError(f"temperature must be positive, got {t}")
+    if tuple(I_gathered.shape) != tuple(T_gathered.shape):
+        raise ShapeError(
+            f"gathered shapes disagree: {tuple(I_gathered.shape)} vs {tuple(T_gathered.shape)}")
+    if I_gathered.shape[0] != layout.global_batch:
+        raise LayoutError(
+            f"gathered matrices have {I_gathered.shape[0]} rows, layout "
+            f"expects {layout.global_batch}")
+    if len(I_gathered.shape) != 2:
+        raise ShapeError("gathered features must be 2-D")
+    t = _check_t(t)
+    device = _default_device()
+    Ig, origin = _stage(I_gathered, device)
+    Tg, _ = _stage(T_gathered, device)
+    N, B, D, n = layout.world_size, layout.global_batch, Ig.shape[1], layout.rank
+    b = layout.local_batch
+    plan = get_plan(B, D, N, n, device)
+    st = _stream_ptr(device)
+    code = _TORCH_DTYPE_CODE[Ig.dtype]
+    if Tg.dtype != Ig.dtype:
+        Tg = Tg.to(Ig.dtype)
+    per_rank = 2 * b * plan.Dp
+    for src in range(N):
+        Is, Ts = Ig[src * b:(src + 1) * b], Tg[src * b:(src + 1) * b]
+        _lib.call("disco_b200_pack", *plan.args, Is.data_ptr(), Ts.data_ptr(), Is.stride(0),
+                  Ts.stride(0), code, int(src == 0), st)
+        if N > 1:
+            plan.gather[src * per_rank:(src + 1) * per_rank].copy_(plan.pack)
+    _lib.call("disco_b200_forward", *plan.args, t, st)
+    _lib.call("disco_b200_backward_cross", *plan.args, t, st)
+    _lib.call("disco_b200_backward_intra", *plan.args, st)
+    d_image = torch.empty((B, D), dtype=torch.float32, device=device)
+    d_text = torch.empty((B, D), dtype=torch.float32, device=device)
+    _lib.call("disco_b200_contribution", *plan.args, t, int(bool(flip_cross_rank_sign)),
+              d_image.data_ptr(), d_text.data_ptr(), D, st)
+    _lib.call("disco_b200_loss", *plan.args, 1, st)
+    loss, flags = _read_status(plan)
+    _raise_on_flags(flags)
+    _account_loss_scope(loss_counters, exchange_counters, b, B, D)
+    return LocalGradContribution(_unstage(d_image, origin), _unstage(d_text, origin), loss)
+
+
+def _account_loss_scope(loss_counters, exchange_counters, b, B, D) -> None:
+    """The reference's analytic accounting of local_loss_and_grads (shard.py:133-156)."""
+    if loss_counters is not None:
+        with tracking(loss_counters):
+            loss_counters.add_flops(4 * b * B * D)
+        loss_counters.alloc(2 * b * B)
+    if exchange_counters is not None:
+        exchange_counters.add_flops(8 * b * B * D)
+        exchange_counters.alloc(2 * B * D)
+    if loss_counters is not None:
+        loss_counters.release(2 * b * B)
+
+
+def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_sign: bool = False):
+    """Launch one rank's DisCo fwd+bwd without any host synchronisation.
+
+    Inputs must already be CUDA tensors (b x D).  Returns (d_image, d_text,
+    plan); the global loss and the non-finite flags are read later with
+    ``finish_status(plan)``.  ``disco_step`` is this plus that read-back.
+    """
+    N, n = endpoint.world_size, endpoint.rank
+    b, D = local_I.shape
+    B = b * N
+    device = local_I.device
+    plan = get_plan(B, D, N, n, device)
+    st = _stream_ptr(device)
+    code = _TORCH_DTYPE_CODE[local_I.dtype]
+    _lib.call("disco_b200_pack", *plan.args, local_I.data_ptr(), local_T.data_ptr(),
+              local_I.stride(0), local_T.stride(0), code, 1, st)
+    if N > 1:
+        endpoint.all_gather_into(plan.gather, plan.pack)
+    _lib.call("disco_b200_forward", *plan.args, t, st)
+    _lib.call("disco_b200_backward_cross", *plan.args, t, st)
+    work = endpoint.all_to_all_into(plan.recv, plan.send, async_op=True) if N > 1 else None
+    _lib.call("disco_b200_backward_intra", *plan.args, st)
+    if work is not None:
+        work.wait()
+    d_image = torch.empty((b, D), dtype=torch.float32, device=device)
+    d_text = torch.empty((b, D), dtype=torch.float32, device=device)
+    _lib.call("disco_b200_combine", *plan.args, t, int(bool(flip_cross_rank_sign)),
+              d_image.data_ptr(), d_text.data_ptr(), D, st)
+    if N > 1:
+        endpoint.all_gather_into(plan.ce_all, plan.ce)
+    _lib.call("disco_b200_loss", *plan.args, 0, st)
+    return d_image, d_text, plan
+
+
+def finish_status(plan: Plan) -> float:
+    loss, flags = _read_status(plan)
+    _raise_on_flags(flags)
+    return loss
+
+
+def disco_step(endpoint, local_I, local_T, t: float, *, loss_counters: Counters | None = None,
+               exchange_counters: Counters | None = None,
+               flip_cross_rank_sign: bool = False):
+    """One rank's share of the sharded loss step (shard.py:169-208).
+
+    Returns (d_image_local, d_text_local, global_loss): fp32 b x D gradients of
+    the full-batch loss for this rank's rows and the loss (identical on every
+    rank).  ``endpoint`` is any object with the fabric protocol
+    (``ProcessGroupEndpoint``, ``LocalEndpoint``) or None for world size 1.
+    Outputs follow the inputs' container: numpy in -> numpy out (host copies
+    included), CUDA tensors in -> CUDA tensors out.
+    """
+    if endpoint is None:
+        endpoint = SingleEndpoint()
+    if tuple(local_I.shape) != tuple(local_T.shape):
+        raise ShapeError(
+            f"local feature shapes disagree: {tuple(local_I.shape)} vs {tuple(local_T.shape)}")
+    if exchange_counters is None:
+        exchange_counters = Counters()
+    layout = ShardLayout(world_size=endpoint.world_size,
+                         global_batch=local_I.shape[0] * endpoint.world_size,
+                         rank=endpoint.rank)
+    t = _check_t(t)
+    batch, dim = layout.global_batch, local_I.shape[1]
+    device = _default_device()
+    I_dev, origin = _stage(local_I, device)
+    T_dev, _ = _stage(local_T, device)
+    if T_dev.dtype != I_dev.dtype:
+        T_dev = T_dev.to(I_dev.dtype)
+    exchange_counters.alloc(2 * batch * dim)
+    d_image, d_text, plan = disco_step_async(endpoint, I_dev, T_dev, t,
+                                             flip_cross_rank_sign=flip_cross_rank_sign)
+    loss = finish_status(plan)
+    _account_loss_scope(loss_counters, exchange_counters, layout.local_batch, batch, dim)
+    exchange_counters.alloc(batch * dim)
+    exchange_counters.release(batch * dim)
+    exchange_counters.alloc(batch * dim)
+    exchange_counters.release(batch * dim)
+    return _unstage(d_image, origin), _unstage(d_text, origin), loss

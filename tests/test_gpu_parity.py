@@ -1,0 +1,165 @@
+"""GPU parity: the sm_100a DisCo path against the CPU oracle.
+
+The oracle (oracle/disco_oracle.py, pinned to the reference by
+test_oracle_golden.py) runs in f64 on the SAME bf16-rounded features the
+device sees.  Contract tolerance (BASELINE.json north_star): loss and
+gradients within 1e-3, measured with the reference's normwise max_rel_error
+(matrix.py:147-162) composed as in cli.py:114-122.  Across world sizes that
+divide 8 (with B % 1024 == 0) results must be bitwise identical.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2304_08480_b200 as P
+from oracle import disco_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-3
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def run_sim(I, T, world, t, **kw):
+    """Simulated ranks on one GPU (threads); returns stacked grads + the per-rank losses."""
+    b = I.shape[0] // world
+    Id, Td = dev(I), dev(T)
+
+    def fn(ep):
+        rows = slice(ep.rank * b, (ep.rank + 1) * b)
+        return P.disco_step(ep, Id[rows], Td[rows], t, **kw)
+
+    res = P.run_ranks(world, fn)
+    di = torch.cat([r[0] for r in res]).cpu().numpy()
+    dt = torch.cat([r[1] for r in res]).cpu().numpy()
+    losses = [r[2] for r in res]
+    return di, dt, losses
+
+
+def errors(di, dt, loss, I, T, t):
+    ri, rt, rl = O.clip_grad_full(I, T, t)
+    return (O.max_rel_error(di, ri), O.max_rel_error(dt, rt),
+            O.max_rel_error(np.array([loss]), np.array([rl[0]])))
+
+
+def test_known_answer_orthonormal():
+    eye = np.eye(2)
+    di, dt, loss = P.disco_step(None, eye, eye, 1.0)
+    assert abs(loss - math.log(1.0 + math.exp(-1.0))) < 1e-6
+    ri, rt, _ = O.clip_grad_full(eye, eye, 1.0)
+    assert O.max_rel_error(di, ri) < TOL and O.max_rel_error(dt, rt) < TOL
+
+
+def test_known_answer_identical_rows():
+    feats = np.tile(np.array([1.0, 0.0, 0.0]), (4, 1))
+    _, _, loss = P.disco_step(None, feats, feats, 10.0)
+    assert abs(loss - math.log(4.0)) < 1e-6
+
+
+def test_known_answer_single_pair():
+    di, dt, loss = P.disco_step(None, np.array([[1.0, 0.0]]), np.array([[0.6, 0.8]]), 10.0)
+    assert loss == 0.0
+    assert not np.any(di) and not np.any(dt)
+
+
+@pytest.mark.parametrize("B,D,N", [(8, 4, 1), (8, 5, 2), (12, 5, 3), (16, 8, 4), (64, 16, 8), (32, 8, 4)])
+@pytest.mark.parametrize("t", [1.0, 10.0, 100.0])
+def test_small_grid_vs_oracle(B, D, N, t):
+    I, T = O.synthetic_features(B, D, 0)
+    di, dt, losses = run_sim(I, T, N, t)
+    assert len(set(losses)) == 1
+    e = errors(di, dt, losses[0], I, T, t)
+    assert max(e) < TOL, e
+
+
+@pytest.mark.parametrize("correlated", [False, True])
+@pytest.mark.parametrize("t", [14.2857, 100.0])
+def test_config_a(t, correlated):
+    I, T = O.synthetic_features(1024, 512, 0, correlated=correlated)
+    di, dt, losses = run_sim(I, T, 2, t)
+    e = errors(di, dt, losses[0], I, T, t)
+    assert max(e) < TOL, e
+
+
+@pytest.mark.parametrize("B,D", [(4096, 512), (2048, 768), (2048, 1024), (1000, 100)])
+def test_single_gpu_vs_oracle(B, D):
+    I, T = O.synthetic_features(B, D, 1)
+    di, dt, loss = P.disco_step(None, dev(I), dev(T), 100.0)
+    e = errors(di.cpu().numpy(), dt.cpu().numpy(), loss, I, T, 100.0)
+    assert max(e) < TOL, e
+
+
+def test_bitwise_identical_across_world_sizes():
+    B, D, t = 8192, 512, 100.0
+    I, T = O.synthetic_features(B, D, 2)
+    base = None
+    for N in (1, 2, 4, 8):
+        di, dt, losses = run_sim(I, T, N, t)
+        assert len(set(losses)) == 1
+        if base is None:
+            base = (di, dt, losses[0])
+            e = errors(di, dt, losses[0], I, T, t)
+            assert max(e) < TOL, e
+        else:
+            assert di.tobytes() == base[0].tobytes(), f"d_image differs at N={N}"
+            assert dt.tobytes() == base[1].tobytes(), f"d_text differs at N={N}"
+            assert losses[0] == base[2]
+
+
+def test_repeat_runs_are_bitwise_identical():
+    I, T = O.synthetic_features(2048, 512, 3)
+    a = run_sim(I, T, 4, 10.0)
+    b = run_sim(I, T, 4, 10.0)
+    assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes() and a[2] == b[2]
+
+
+@pytest.mark.parametrize("N", [2, 3, 4])
+def test_local_contributions_vs_oracle(N):
+    I, T = O.synthetic_features(96, 24, 4)
+    parts = []
+    for r in range(N):
+        layout = P.ShardLayout(world_size=N, global_batch=96, rank=r)
+        c = P.local_loss_and_grads(layout, I, T, 10.0)
+        oi, ot, ol = O.local_loss_and_grads(N, r, I, T, 10.0)
+        assert O.max_rel_error(c.d_image_full, oi) < TOL
+        assert O.max_rel_error(c.d_text_full, ot) < TOL
+        assert abs(c.local_loss - ol) / abs(ol) < TOL
+        parts.append(c)
+    ri, rt, rl = O.clip_grad_full(I, T, 10.0)
+    assert O.max_rel_error(sum(p.d_image_full for p in parts) / N, ri) < TOL
+    assert abs(sum(p.local_loss for p in parts) / N - rl[0]) < TOL * rl[0]
+
+
+def test_sign_flip_hook():
+    I, T = O.synthetic_features(64, 8, 0)
+    di, dt, losses = run_sim(I, T, 2, 10.0, flip_cross_rank_sign=True)
+    oi, ot, ol = O.disco_step_all(I, T, 2, 10.0, flip_cross_rank_sign=True)
+    assert O.max_rel_error(di, oi) < TOL and O.max_rel_error(dt, ot) < TOL
+    ri, _, _ = O.clip_grad_full(I, T, 10.0)
+    assert O.max_rel_error(di, ri) > 1e-3
+    di1, _, _ = run_sim(I, T, 1, 10.0, flip_cross_rank_sign=True)
+    assert O.max_rel_error(di1, ri) < TOL  # no-op at N = 1
+
+
+def test_nonfinite_input_raises():
+    I, T = O.synthetic_features(16, 8, 0)
+    I[3, 2] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        P.disco_step(None, I, T, 10.0)
+
+
+def test_full_size_b32k_sampled_rows():
+    """Config B at N=1 against the blocked f64 oracle on 64 sampled rows."""
+    B, D, t = 32768, 512, 100.0
+    I, T = O.synthetic_features(B, D, 0)
+    di, dt, loss = P.disco_step(None, dev(I), dev(T), t)
+    rows = np.linspace(0, B - 1, 64).astype(np.int64)
+    ri, rt, rl = O.clip_grad_rows(I, T, t, rows)
+    assert O.max_rel_error(di[rows].cpu().numpy(), ri) < TOL
+    assert O.max_rel_error(dt[rows].cpu().numpy(), rt) < TOL
+    assert abs(loss - rl[0]) / rl[0] < TOL
