@@ -60,7 +60,11 @@ struct SmemCtl {
   uint64_t tempty[2];
   uint32_t tmem_base;
 };
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + 256;
+// Epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B), TMA SWIZZLE_128B layout.
+constexpr int STAGING_TILE = 32 * 128;
+constexpr int STAGING_BYTES = 4 * 2 * STAGING_TILE;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + STAGING_BYTES + 256;
+static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory limit");
 
 // -------------------------------------------------------- status flag bits
 constexpr int FLAG_INPUT_NONFINITE = 1;
@@ -71,6 +75,7 @@ struct Status {
   double loss;
   int flags;
   int pad;
+  double loss_partial[128];  // loss_partial_kernel scratch (LOSS_BLOCKS)
 };
 
 // ----------------------------------------------------------- kernel params
@@ -79,6 +84,7 @@ struct Status {
 struct LogitsParams {
   CUtensorMap a_map[2];  // dir 0: I_g, dir 1: T_g   box {64, 128}
   CUtensorMap b_map[2];  // dir 0: T_g, dir 1: I_g   box {64, 256}
+  CUtensorMap g_map[2];  // G store maps, box {64, 32} f16
   int B, b, Dp, rank;
   int nchunk, chunk_cols, tiles_per_chunk, row_tiles;
   float tl2e;  // t * log2(e)
@@ -95,6 +101,8 @@ struct LogitsParams {
 struct GemmProblem {
   CUtensorMap a_map;
   CUtensorMap b_map;
+  CUtensorMap out_map;    // 3-D fp32 store map {N, row_div, z}, box {32, 32, 1}
+  int tma_store;          // 1: TMA stores through staging smem; 0: direct st.global
   int a_mn_major, b_mn_major;
   int M, N;               // valid output extents
   int m_tiles, n_tiles, k_chunks;
@@ -208,13 +216,15 @@ template <int KIND>
 __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_constant__ LogitsParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
-  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + STAGES * STAGE_BYTES);
+  uint8_t* staging = tiles + STAGES * STAGE_BYTES;
+  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(staging + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   if (warp == 0 && lane == 0) {
     for (int d = 0; d < 2; ++d) {
       ptx::prefetch_tmap(&p.a_map[d]);
       ptx::prefetch_tmap(&p.b_map[d]);
+      if (KIND == KIND_GRAD) ptx::prefetch_tmap(&p.g_map[d]);
     }
   }
   kernel_prologue(ctl, warp, lane);
@@ -280,6 +290,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
     const int quad = warp & 3;
     const int r_in_tile = quad * 32 + lane;
     uint32_t it = 0;
+    uint32_t gslice = 0;  // staging buffer parity (GRAD)
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
       int dir, rt, ch, t0;
       decode(u, dir, rt, ch, t0);
@@ -302,13 +313,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
         ptx::tc_fence_after();
         const int col0 = chunk_lo + (t0 + ti) * BN;
         const uint32_t taddr = ctl->tmem_base + (uint32_t(quad * 32) << 16) + buf * BN;
+        if (KIND == KIND_FWD) {
 #pragma unroll 1
-        for (int j = 0; j < BN / 32; ++j) {
-          const int cb = col0 + j * 32;
-          if (cb >= chunk_hi) break;  // warp-uniform
-          float v[32];
-          ptx::tmem_ld32(taddr + j * 32, v);
-          if (KIND == KIND_FWD) {
+          for (int j = 0; j < BN / 32; ++j) {
+            const int cb = col0 + j * 32;
+            if (cb >= chunk_hi) break;  // warp-uniform
+            float v[32];
+            ptx::tmem_ld32(taddr + j * 32, v);
             float cmax = -INFINITY;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
@@ -326,28 +337,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
             }
             l = l * ptx::ex2(m2 - mnew) + s;
             m2 = mnew;
-          } else {
-            if (row_ok) {
-              uint32_t h[16];
+          }
+        } else {
+          // G = exp2(y - lse2) (label column: P_label - 1), f16, 64-column slices
+          // staged in swizzled smem and written by TMA (coalesced, clipped at b / B).
+#pragma unroll 1
+          for (int j = 0; j < BN / 64; ++j) {
+            const int cb = col0 + j * 64;
+            if (cb >= chunk_hi) break;  // warp-uniform
+            uint32_t h[32];
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              float v[32];
+              ptx::tmem_ld32(taddr + j * 64 + half * 32, v);
 #pragma unroll
               for (int i = 0; i < 32; i += 2) {
+                const int c = cb + half * 32 + i;
                 float g0 = ptx::ex2(v[i] * p.tl2e - lse2);
                 float g1 = ptx::ex2(v[i + 1] * p.tl2e - lse2);
-                if (cb + i == label) g0 = gl;
-                if (cb + i + 1 == label) g1 = gl;
+                if (c == label) g0 = gl;
+                if (c + 1 == label) g1 = gl;
                 __half2 hh = __floats2half2_rn(g0, g1);
-                h[i / 2] = *reinterpret_cast<uint32_t*>(&hh);
+                h[half * 16 + i / 2] = *reinterpret_cast<uint32_t*>(&hh);
               }
-              if (cb + 32 <= chunk_hi) {
-                uint4* dst = reinterpret_cast<uint4*>(grow + cb);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) dst[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
-              } else {  // columns past the chunk belong to the next chunk's tiles
-                for (int i = 0; i < 32 && cb + i < chunk_hi; ++i) {
-                  const uint32_t w = h[i / 2];
-                  const unsigned short bits = (i & 1) ? (unsigned short)(w >> 16) : (unsigned short)(w & 0xFFFF);
-                  grow[cb + i] = __ushort_as_half(bits);
-                }
+            }
+            if ((chunk_lo & 63) == 0 && (cb + 64 <= chunk_hi || chunk_hi == p.B)) {
+              uint8_t* tile = staging + ((warp - 2) * 2 + (gslice & 1)) * STAGING_TILE;
+              if (lane == 0) ptx::bulk_wait_read<1>();  // buffer of slice-2 drained
+              __syncwarp();
+              ptx::st_swizzled_row(tile, lane, h);
+              ptx::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                ptx::tma_store_2d(&p.g_map[dir], tile, cb, rt * BM + quad * 32);
+                ptx::bulk_commit();
+              }
+              ++gslice;
+            } else if (row_ok) {  // non-canonical chunk edges (b not a multiple of 64): scalar path
+              for (int i = 0; i < 64 && cb + i < chunk_hi; ++i) {
+                const uint32_t w = h[i / 2];
+                grow[cb + i] = __ushort_as_half((i & 1) ? (unsigned short)(w >> 16) : (unsigned short)(w & 0xFFFF));
               }
             }
           }
@@ -361,6 +390,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
         if (label >= chunk_lo && label < chunk_hi) p.target[dir * p.b + row] = yt;
       }
     }
+    if (KIND == KIND_GRAD && lane == 0) ptx::bulk_wait_all();
   }
   kernel_epilogue(ctl, warp);
 }
@@ -372,7 +402,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
-  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + STAGES * STAGE_BYTES);
+  uint8_t* staging = tiles + STAGES * STAGE_BYTES;
+  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(staging + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   if (warp == 0 && lane == 0) {
@@ -444,6 +475,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
   } else {  // ---------------------------- epilogue warps
     const int quad = warp & 3;
     uint32_t it = 0;
+    uint32_t gslice = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
       int pi, mt, nt, kc;
       decode(u, pi, mt, nt, kc);
@@ -451,24 +483,52 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       const uint32_t buf = it & 1, use = it >> 1;
       ptx::mbar_wait(&ctl->tfull[buf], use & 1);
       ptx::tc_fence_after();
-      const int row = mt * BM + quad * 32 + lane;
-      float* orow = nullptr;
-      if (row < q.M)
-        orow = q.out + kc * q.chunk_stride + (row / q.row_div) * q.stride_hi + (row % q.row_div) * q.ld_out;
+      const int row0 = mt * BM + quad * 32;  // first row of this warp's 32-row slab
+      const int row = row0 + lane;
       const uint32_t taddr = ctl->tmem_base + (uint32_t(quad * 32) << 16) + buf * BN;
+      if (q.tma_store) {
+        // 32 x 32 fp32 slices through swizzled staging -> 3-D TMA store (clipped at M / N).
+        const int z = int(row0 / q.row_div) + kc;
+        const int rlo = int(row0 % q.row_div);
 #pragma unroll 1
-      for (int j = 0; j < BN / 32; ++j) {
-        const int c0 = nt * BN + j * 32;
-        if (c0 >= q.N) break;  // warp-uniform
-        float v[32];
-        ptx::tmem_ld32(taddr + j * 32, v);
-        if (orow) {
-          if (c0 + 32 <= q.N) {
-            float4* dst = reinterpret_cast<float4*>(orow + c0);
+        for (int j = 0; j < BN / 32; ++j) {
+          const int c0 = nt * BN + j * 32;
+          if (c0 >= q.N) break;  // warp-uniform
+          float v[32];
+          ptx::tmem_ld32(taddr + j * 32, v);
+          uint32_t w[32];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-          } else {
-            for (int i = 0; i < 32 && c0 + i < q.N; ++i) orow[c0 + i] = v[i];
+          for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(v[i]);
+          uint8_t* tile = staging + ((warp - 2) * 2 + (gslice & 1)) * STAGING_TILE;
+          if (lane == 0) ptx::bulk_wait_read<1>();
+          __syncwarp();
+          ptx::st_swizzled_row(tile, lane, w);
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && row0 < q.M) {
+            ptx::tma_store_3d(&q.out_map, tile, c0, rlo, z);
+            ptx::bulk_commit();
+          }
+          ++gslice;
+        }
+      } else {
+        float* orow = nullptr;
+        if (row < q.M)
+          orow = q.out + kc * q.chunk_stride + (row / q.row_div) * q.stride_hi + (row % q.row_div) * q.ld_out;
+#pragma unroll 1
+        for (int j = 0; j < BN / 32; ++j) {
+          const int c0 = nt * BN + j * 32;
+          if (c0 >= q.N) break;  // warp-uniform
+          float v[32];
+          ptx::tmem_ld32(taddr + j * 32, v);
+          if (orow) {
+            if (c0 + 32 <= q.N) {
+              float4* dst = reinterpret_cast<float4*>(orow + c0);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            } else {
+              for (int i = 0; i < 32 && c0 + i < q.N; ++i) orow[c0 + i] = v[i];
+            }
           }
         }
       }
@@ -476,6 +536,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&ctl->tempty[buf]);
     }
+    if (lane == 0) ptx::bulk_wait_all();
   }
   kernel_epilogue(ctl, warp);
 }
@@ -497,29 +558,39 @@ __device__ __forceinline__ float load_as_float<__half>(const void* p, int64_t i)
 }
 
 // Round local features to bf16, pad D..Dp with zeros: out [2][b][Dp].
-// f64 inputs are rounded directly f64 -> bf16 (one rounding, like the reference's data).
+// One thread per 8 output elements (one 16-byte store); f64 inputs are rounded
+// directly f64 -> bf16 (a single rounding).
 template <typename T>
 __global__ void pack_kernel(const void* I, const void* Tm, int64_t ldI, int64_t ldT, int b, int D, int Dp,
                             __nv_bfloat16* out, Status* status) {
-  const int64_t total = int64_t(2) * b * Dp;
+  const int v8 = Dp / 8;
+  const int64_t total = int64_t(2) * b * v8;
   bool bad = false;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int c = int(i % Dp);
-    const int64_t rr = i / Dp;
+    const int c0 = int(i % v8) * 8;
+    const int64_t rr = i / v8;
     const int dir = int(rr / b), r = int(rr % b);
-    __nv_bfloat16 o = __float2bfloat16_rn(0.f);
-    if (c < D) {
-      if constexpr (sizeof(T) == 8) {
-        const double x = static_cast<const double*>(dir ? Tm : I)[r * (dir ? ldT : ldI) + c];
-        bad |= !isfinite(x);
-        o = __double2bfloat16(x);
-      } else {
-        const float x = load_as_float<T>(dir ? Tm : I, r * (dir ? ldT : ldI) + c);
-        bad |= !isfinite(x);
-        o = __float2bfloat16_rn(x);
+    const void* src = dir ? Tm : I;
+    const int64_t base = r * (dir ? ldT : ldI);
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = c0 + k;
+      __nv_bfloat16 x = __float2bfloat16_rn(0.f);
+      if (c < D) {
+        if constexpr (sizeof(T) == 8) {
+          const double xv = static_cast<const double*>(src)[base + c];
+          bad |= !isfinite(xv);
+          x = __double2bfloat16(xv);
+        } else {
+          const float xv = load_as_float<T>(src, base + c);
+          bad |= !isfinite(xv);
+          x = __float2bfloat16_rn(xv);
+        }
       }
+      o[k] = x;
     }
-    out[i] = o;
+    reinterpret_cast<uint4*>(out)[i] = *reinterpret_cast<const uint4*>(o);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&status->flags, FLAG_INPUT_NONFINITE);
 }
@@ -703,25 +774,43 @@ __global__ void contribution_kernel(const float4* intra, const float4* send, int
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&status->flags, FLAG_GRAD_NONFINITE);
 }
 
-// Loss: sum over the [N][2][b] per-row ce in an order fixed by the global row
-// index (independent of N), in f64, / (2 * N * b).  One block of 1024 threads.
-__global__ void loss_kernel(const float* ce_all, int N, int b, Status* status) {
-  __shared__ double red[1024];
+// Loss: sum of the [N][2][b] per-row ce in an order fixed by the global row
+// index (independent of N), in f64, / (2 * N * b).  Stage 1: LOSS_BLOCKS
+// blocks each reduce a fixed contiguous slice of the flat index f = dir*B + g;
+// stage 2: one warp adds the block partials in a fixed tree.
+constexpr int LOSS_BLOCKS = 128;
+__global__ void loss_partial_kernel(const float* ce_all, int N, int b, double* partial) {
+  __shared__ double red[256];
   const int64_t B = int64_t(N) * b;
+  const int64_t n2 = 2 * B;
+  const int64_t per = (n2 + LOSS_BLOCKS - 1) / LOSS_BLOCKS;
+  const int64_t lo = blockIdx.x * per, hi = min(n2, lo + per);
   double acc = 0.0;
-  for (int dir = 0; dir < 2; ++dir)
-    for (int64_t gidx = threadIdx.x; gidx < B; gidx += blockDim.x) {
-      const int64_t n = gidx / b, r = gidx % b;
-      acc += double(ce_all[(n * 2 + dir) * b + r]);
-    }
+  for (int64_t f = lo + threadIdx.x; f < hi; f += blockDim.x) {
+    const int dir = int(f / B);
+    const int64_t gidx = f - dir * B;
+    const int64_t n = gidx / b, r = gidx % b;
+    acc += double(ce_all[(n * 2 + dir) * b + r]);
+  }
   red[threadIdx.x] = acc;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void loss_final_kernel(const double* partial, int64_t rows2, Status* status) {
+  __shared__ double red[LOSS_BLOCKS];
+  red[threadIdx.x] = partial[threadIdx.x];
+  __syncthreads();
+  for (int w = LOSS_BLOCKS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
-    const double loss = red[0] / double(2 * B);
+    const double loss = red[0] / double(rows2);
     status->loss = loss;
     if (!isfinite(loss)) status->flags |= FLAG_LOSS_NONFINITE;
   }
@@ -800,7 +889,7 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   len[DISCO_R_SEND] = N * 2 * b * Dp * 4;
   len[DISCO_R_RECV] = N > 1 ? N * 2 * b * Dp * 4 : 0;
   len[DISCO_R_INTRA] = 2 * b * Dp * 4;
-  len[DISCO_R_STATUS] = 64;
+  len[DISCO_R_STATUS] = int64_t(sizeof(Status));
   int64_t off = 0;
   for (int r = 0; r < DISCO_R_COUNT; ++r) {
     g->off[r] = off;
@@ -856,6 +945,48 @@ int make_map(CUtensorMap* map, bool bf16, const void* base, uint64_t inner, uint
   return DISCO_OK;
 }
 
+// 3-D fp32 map over [z][rows][cols] with arbitrary row / z pitches (in floats), box {32, 32, 1}.
+int make_map_f32_3d(CUtensorMap* map, const float* base, uint64_t cols, uint64_t rows, uint64_t nz,
+                    uint64_t row_pitch, uint64_t z_pitch) {
+  auto fn = encode_fn();
+  if (!fn) return fail(DISCO_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {cols, rows, nz};
+  cuuint64_t strides[2] = {row_pitch * 4, z_pitch * 4};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(DISCO_CUDA_ERROR, "cuTensorMapEncodeTiled(f32 3d) failed (%d)", int(r));
+  return DISCO_OK;
+}
+
+// Output addressing of a GEMM problem: row r of k-chunk kc lands at
+// out + kc*chunk_stride + (r / row_div)*stride_hi + (r % row_div)*ld_out.
+// TMA stores need 32-row slabs that never straddle a row_div boundary.
+int set_output(GemmProblem& q, float* out, int64_t ld_out, int64_t row_div, int64_t stride_hi, int64_t nz_rows,
+               int64_t chunk_stride, int64_t nz_chunks) {
+  q.out = out;
+  q.ld_out = ld_out;
+  q.row_div = row_div;
+  q.stride_hi = stride_hi;
+  q.chunk_stride = chunk_stride;
+  q.tma_store = 0;
+  const bool aligned = (row_div % 32 == 0) && (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  if (aligned && (nz_rows == 1 || nz_chunks == 1)) {
+    const uint64_t nz = uint64_t(nz_rows > 1 ? nz_rows : nz_chunks);
+    const uint64_t zp = uint64_t(nz_rows > 1 ? stride_hi : (nz_chunks > 1 ? chunk_stride : row_div * ld_out));
+    if (zp % 4 == 0) {
+      int rc = make_map_f32_3d(&q.out_map, out, uint64_t(q.N), uint64_t(std::min<int64_t>(row_div, q.M)), nz,
+                               uint64_t(ld_out), zp);
+      if (rc) return rc;
+      q.tma_store = 1;
+    }
+  }
+  return DISCO_OK;
+}
+
 int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -887,6 +1018,9 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   if ((rc = make_map(&p.a_map[1], true, T_g, g.Dp, g.B, g.Dp, 64, BM))) return rc;
   if ((rc = make_map(&p.b_map[0], true, T_g, g.Dp, g.B, g.Dp, 64, BN))) return rc;
   if ((rc = make_map(&p.b_map[1], true, I_g, g.Dp, g.B, g.Dp, 64, BN))) return rc;
+  const __half* Gbase = region<__half>(ws, g, DISCO_R_G);
+  for (int d = 0; d < 2; ++d)
+    if ((rc = make_map(&p.g_map[d], false, Gbase + int64_t(d) * g.b * g.ldG, g.B, g.b, g.ldG, 64, 32))) return rc;
   p.B = int(g.B);
   p.b = int(g.b);
   p.Dp = int(g.Dp);
@@ -989,7 +1123,7 @@ int disco_b200_pack(void* ws, int64_t B, int64_t D, int world, int rank, const v
     count_launch();
   }
   __nv_bfloat16* out = region<__nv_bfloat16>(ws, g, DISCO_R_PACK);
-  const int64_t n = 2 * g.b * g.Dp;
+  const int64_t n = 2 * g.b * (g.Dp / 8);
   const int grid = elementwise_grid(n, 256);
   switch (dtype) {
     case DISCO_F32:
@@ -1074,18 +1208,13 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
     q.b_k_off = int(int64_t(g.rank) * g.b);
     q.a_row_off = 0;
     if (g.cpr > 1) {  // canonical partials [2][cpr][B][Dp]
-      q.out = region<float>(ws, g, DISCO_R_XPART) + int64_t(gi) * g.cpr * g.B * g.Dp;
-      q.ld_out = g.Dp;
-      q.row_div = int64_t(1) << 40;
-      q.stride_hi = 0;
-      q.chunk_stride = g.B * g.Dp;
+      rc = set_output(q, region<float>(ws, g, DISCO_R_XPART) + int64_t(gi) * g.cpr * g.B * g.Dp, g.Dp, g.B, 0, 1,
+                      g.B * g.Dp, g.cpr);
     } else {  // directly destination-major send slabs [N][2][b][Dp]
-      q.out = region<float>(ws, g, DISCO_R_SEND) + int64_t(gi) * g.b * g.Dp;
-      q.ld_out = g.Dp;
-      q.row_div = g.b;
-      q.stride_hi = 2 * g.b * g.Dp;
-      q.chunk_stride = 0;
+      rc = set_output(q, region<float>(ws, g, DISCO_R_SEND) + int64_t(gi) * g.b * g.Dp, g.Dp, g.b, 2 * g.b * g.Dp,
+                      world, 0, 1);
     }
+    if (rc) return rc;
   }
   if ((rc = launch_gemm(p, st))) return rc;
   if (g.cpr > 1) {
@@ -1125,11 +1254,8 @@ int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int ran
     q.k_chunks = 1;
     q.k_chunk_len = int(g.B);
     q.k_total = int(g.B);
-    q.out = region<float>(ws, g, DISCO_R_INTRA) + int64_t(gi) * g.b * g.Dp;
-    q.ld_out = g.Dp;
-    q.row_div = int64_t(1) << 40;
-    q.stride_hi = 0;
-    q.chunk_stride = 0;
+    if ((rc = set_output(q, region<float>(ws, g, DISCO_R_INTRA) + int64_t(gi) * g.b * g.Dp, g.Dp, g.b, 0, 1, 0, 1)))
+      return rc;
   }
   return launch_gemm(p, st);
 }
@@ -1174,9 +1300,12 @@ int disco_b200_loss(void* ws, int64_t B, int64_t D, int world, int rank, int loc
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool local = local_only || world == 1;
-  loss_kernel<<<1, 1024, 0, st>>>(region<float>(ws, g, local ? DISCO_R_CE : DISCO_R_CE_ALL), local ? 1 : world,
-                                  int(g.b), region<Status>(ws, g, DISCO_R_STATUS));
-  count_launch();
+  Status* status = region<Status>(ws, g, DISCO_R_STATUS);
+  const int nw = local ? 1 : world;
+  loss_partial_kernel<<<LOSS_BLOCKS, 256, 0, st>>>(region<float>(ws, g, local ? DISCO_R_CE : DISCO_R_CE_ALL), nw,
+                                                   int(g.b), status->loss_partial);
+  loss_final_kernel<<<1, LOSS_BLOCKS, 0, st>>>(status->loss_partial, int64_t(2) * nw * g.b, status);
+  count_launch(2);
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
 }
