@@ -48,7 +48,7 @@ constexpr int STAGES = 4;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KiB
 constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KiB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-constexpr int NUM_THREADS = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int NUM_THREADS = 320;  // warp0 TMA, warp1 MMA, warps2-9 epilogue
 constexpr int TMEM_COLS = 512;    // 2 accumulators of 128 x 256 fp32
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -60,9 +60,9 @@ struct SmemCtl {
   uint64_t tempty[2];
   uint32_t tmem_base;
 };
-// Epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B), TMA SWIZZLE_128B layout.
+// Epilogue staging: 8 warps x (32 rows x 128 B), TMA SWIZZLE_128B layout.
 constexpr int STAGING_TILE = 32 * 128;
-constexpr int STAGING_BYTES = 4 * 2 * STAGING_TILE;
+constexpr int STAGING_BYTES = 8 * STAGING_TILE;
 constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + STAGING_BYTES + 256;
 static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory limit");
 
@@ -89,7 +89,7 @@ struct LogitsParams {
   int nchunk, chunk_cols, tiles_per_chunk, row_tiles;
   float tl2e;  // t * log2(e)
   // FWD outputs
-  float2* stats;   // [2][nchunk][b]
+  float2* stats;   // [2][nchunk][2 column halves][b]
   float* target;   // [2][b]  (log2-domain target logit)
   // GRAD inputs / outputs
   const float* lse2;    // [2][b]
@@ -103,6 +103,7 @@ struct GemmProblem {
   CUtensorMap b_map;
   CUtensorMap out_map;    // 3-D fp32 store map {N, row_div, z}, box {32, 32, 1}
   int tma_store;          // 1: TMA stores through staging smem; 0: direct st.global
+  int paired;             // 1: unit = chunks (2kc, 2kc+1), summed in the epilogue
   int a_mn_major, b_mn_major;
   int M, N;               // valid output extents
   int m_tiles, n_tiles, k_chunks;
@@ -179,7 +180,7 @@ __device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&ctl->tfull[i], 1);
-      ptx::mbar_init(&ctl->tempty[i], 4);  // one arrive per epilogue warp
+      ptx::mbar_init(&ctl->tempty[i], 8);  // one arrive per epilogue warp
     }
     ptx::fence_barrier_init();
   }
@@ -205,10 +206,13 @@ __device__ __forceinline__ void kernel_epilogue(SmemCtl* ctl, int warp) {
 // =====================================================================
 // logits kernel: S tiles for both directions.
 //   FWD : unit = (dir, row tile, column chunk); tiles = column tiles of the chunk,
-//         epilogue keeps a per-row online (max, sum-exp) across the tiles.
+//         each epilogue thread keeps an online (max, sum-exp) for its row over
+//         its column half of every tile of the unit.
 //   GRAD: unit = (dir, row tile, column chunk, column tile); epilogue writes G.
 // Both kinds walk identical tiles (same column origin and K order), so the
 // recomputed S in GRAD is bit-identical to the forward S.
+// Epilogue: 8 warps; warp w reads TMEM lane quadrant (w % 4) and column half
+// (w - 2) / 4 of the 128 x 256 accumulator.
 // =====================================================================
 enum { KIND_FWD = 0, KIND_GRAD = 1 };
 
@@ -286,11 +290,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
         }
       }
     }
-  } else {  // ---------------------------- epilogue warps 2..5
+  } else {  // ---------------------------- epilogue warps 2..9
+    const int ew = warp - 2;
     const int quad = warp & 3;
+    const int chalf = ew >> 2;  // column half of the 256-wide tile
     const int r_in_tile = quad * 32 + lane;
+    uint8_t* tile = staging + ew * STAGING_TILE;
     uint32_t it = 0;
-    uint32_t gslice = 0;  // staging buffer parity (GRAD)
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
       int dir, rt, ch, t0;
       decode(u, dir, rt, ch, t0);
@@ -300,6 +306,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
       const int chunk_lo = ch * p.chunk_cols;
       const int chunk_hi = min(chunk_lo + p.chunk_cols, p.B);
       float m2 = -INFINITY, l = 0.f, yt = 0.f;
+      bool has_t = false;
       float lse2 = 0.f, gl = 0.f;
       __half* grow = nullptr;
       if (KIND == KIND_GRAD && row_ok) {
@@ -311,11 +318,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
         const uint32_t buf = it & 1, use = it >> 1;
         ptx::mbar_wait(&ctl->tfull[buf], use & 1);
         ptx::tc_fence_after();
-        const int col0 = chunk_lo + (t0 + ti) * BN;
-        const uint32_t taddr = ctl->tmem_base + (uint32_t(quad * 32) << 16) + buf * BN;
+        const int col0 = chunk_lo + (t0 + ti) * BN + chalf * (BN / 2);
+        const uint32_t taddr = ctl->tmem_base + (uint32_t(quad * 32) << 16) + buf * BN + chalf * (BN / 2);
         if (KIND == KIND_FWD) {
 #pragma unroll 1
-          for (int j = 0; j < BN / 32; ++j) {
+          for (int j = 0; j < BN / 64; ++j) {
             const int cb = col0 + j * 32;
             if (cb >= chunk_hi) break;  // warp-uniform
             float v[32];
@@ -326,7 +333,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
               const float y = (cb + i < chunk_hi) ? v[i] * p.tl2e : -INFINITY;
               v[i] = y;
               cmax = fmaxf(cmax, y);
-              if (cb + i == label) yt = y;
+              if (cb + i == label && cb + i < chunk_hi) {  // masked columns belong to the next chunk
+                yt = y;
+                has_t = true;
+              }
             }
             const float mnew = fmaxf(m2, cmax);
             float s = 0.f;
@@ -342,7 +352,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
           // G = exp2(y - lse2) (label column: P_label - 1), f16, 64-column slices
           // staged in swizzled smem and written by TMA (coalesced, clipped at b / B).
 #pragma unroll 1
-          for (int j = 0; j < BN / 64; ++j) {
+          for (int j = 0; j < BN / 128; ++j) {
             const int cb = col0 + j * 64;
             if (cb >= chunk_hi) break;  // warp-uniform
             uint32_t h[32];
@@ -353,8 +363,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
 #pragma unroll
               for (int i = 0; i < 32; i += 2) {
                 const int c = cb + half * 32 + i;
-                float g0 = ptx::ex2(v[i] * p.tl2e - lse2);
-                float g1 = ptx::ex2(v[i + 1] * p.tl2e - lse2);
+                float g0 = ptx::ex2(fmaf(v[i], p.tl2e, -lse2));
+                float g1 = ptx::ex2(fmaf(v[i + 1], p.tl2e, -lse2));
                 if (c == label) g0 = gl;
                 if (c + 1 == label) g1 = gl;
                 __half2 hh = __floats2half2_rn(g0, g1);
@@ -362,8 +372,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
               }
             }
             if ((chunk_lo & 63) == 0 && (cb + 64 <= chunk_hi || chunk_hi == p.B)) {
-              uint8_t* tile = staging + ((warp - 2) * 2 + (gslice & 1)) * STAGING_TILE;
-              if (lane == 0) ptx::bulk_wait_read<1>();  // buffer of slice-2 drained
+              if (lane == 0) ptx::bulk_wait_read<0>();  // previous store drained the buffer
               __syncwarp();
               ptx::st_swizzled_row(tile, lane, h);
               ptx::fence_proxy_async_smem();
@@ -372,7 +381,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
                 ptx::tma_store_2d(&p.g_map[dir], tile, cb, rt * BM + quad * 32);
                 ptx::bulk_commit();
               }
-              ++gslice;
             } else if (row_ok) {  // non-canonical chunk edges (b not a multiple of 64): scalar path
               for (int i = 0; i < 64 && cb + i < chunk_hi; ++i) {
                 const uint32_t w = h[i / 2];
@@ -386,8 +394,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
         if (lane == 0) ptx::mbar_arrive(&ctl->tempty[buf]);
       }
       if (KIND == KIND_FWD && row_ok) {
-        p.stats[(int64_t(dir) * p.nchunk + ch) * p.b + row] = make_float2(m2, l);
-        if (label >= chunk_lo && label < chunk_hi) p.target[dir * p.b + row] = yt;
+        p.stats[((int64_t(dir) * p.nchunk + ch) * 2 + chalf) * p.b + row] = make_float2(m2, l);
+        if (has_t) p.target[dir * p.b + row] = yt;
       }
     }
     if (KIND == KIND_GRAD && lane == 0) ptx::bulk_wait_all();
@@ -397,7 +405,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
 
 // =====================================================================
 // Grouped f16 GEMM with fp32 tile outputs.
-//   unit = (problem, m tile, n tile, k chunk); one accumulator tile per unit.
+//   unit = (problem, m tile, n tile, k chunk); one accumulator tile per unit,
+//   or, for `paired` problems, two consecutive canonical K chunks accumulated
+//   into the two TMEM buffers and summed in the epilogue ((c0 + c1): the first
+//   level of the fixed reduction tree).
 // =====================================================================
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -410,6 +421,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     for (int i = 0; i < p.nprob; ++i) {
       ptx::prefetch_tmap(&p.prob[i].a_map);
       ptx::prefetch_tmap(&p.prob[i].b_map);
+      if (p.prob[i].tma_store) ptx::prefetch_tmap(&p.prob[i].out_map);
     }
   }
   kernel_prologue(ctl, warp, lane);
@@ -426,8 +438,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     kc = rem % q.k_chunks;
     mt = rem / q.k_chunks;
   };
-  auto k_range = [&](const GemmProblem& q, int kc, int& k0, int& nk) {
-    k0 = kc * q.k_chunk_len;
+  // canonical chunk index `c` -> [k0, k0 + nk*BK)
+  auto k_range = [&](const GemmProblem& q, int c, int& k0, int& nk) {
+    k0 = c * q.k_chunk_len;
     const int k1 = min(k0 + q.k_chunk_len, q.k_total);
     nk = (k1 - k0 + BK - 1) / BK;
   };
@@ -436,22 +449,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     if (lane == 0) {  // ---------------- TMA producer
       Pipe pipe;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-        int pi, mt, nt, kc, k0, nk;
+        int pi, mt, nt, kc;
         decode(u, pi, mt, nt, kc);
         const GemmProblem& q = p.prob[pi];
-        k_range(q, kc, k0, nk);
-        for (int kb = 0; kb < nk; ++kb) {
-          ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
-          uint8_t* st = tiles + pipe.stage * STAGE_BYTES;
-          ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], STAGE_BYTES);
-          const int k = k0 + kb * BK;
-          if (q.a_mn_major)
-            load_operand(&q.a_map, 1, st, &ctl->full[pipe.stage], mt * BM, k + q.a_k_off, BM, ptx::kEvictFirst);
-          else
-            load_operand(&q.a_map, 0, st, &ctl->full[pipe.stage], mt * BM + q.a_row_off, k, BM, ptx::kEvictFirst);
-          load_operand(&q.b_map, q.b_mn_major, st + A_STAGE_BYTES, &ctl->full[pipe.stage], nt * BN,
-                       k + q.b_k_off, BN, ptx::kEvictLast);
-          pipe.advance();
+        for (int sub = 0; sub <= q.paired; ++sub) {
+          int k0, nk;
+          k_range(q, kc * (1 + q.paired) + sub, k0, nk);
+          for (int kb = 0; kb < nk; ++kb) {
+            ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
+            uint8_t* st = tiles + pipe.stage * STAGE_BYTES;
+            ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], STAGE_BYTES);
+            const int k = k0 + kb * BK;
+            if (q.a_mn_major)
+              load_operand(&q.a_map, 1, st, &ctl->full[pipe.stage], mt * BM, k + q.a_k_off, BM, ptx::kEvictFirst);
+            else
+              load_operand(&q.a_map, 0, st, &ctl->full[pipe.stage], mt * BM + q.a_row_off, k, BM, ptx::kEvictFirst);
+            load_operand(&q.b_map, q.b_mn_major, st + A_STAGE_BYTES, &ctl->full[pipe.stage], nt * BN,
+                         k + q.b_k_off, BN, ptx::kEvictLast);
+            pipe.advance();
+          }
         }
       }
     }
@@ -459,48 +475,64 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     if (lane == 0) {  // ---------------- MMA issuer
       Pipe pipe;
       uint32_t it = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
-        int pi, mt, nt, kc, k0, nk;
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        int pi, mt, nt, kc;
         decode(u, pi, mt, nt, kc);
         const GemmProblem& q = p.prob[pi];
-        k_range(q, kc, k0, nk);
         const uint32_t idesc = ptx::instr_desc_f16(BM, BN, 0, 0, q.a_mn_major, q.b_mn_major);  // f16 x f16
-        const uint32_t buf = it & 1, use = it >> 1;
-        ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
-        ptx::tc_fence_after();
-        mma_tile(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, q.a_mn_major, q.b_mn_major);
-        ptx::umma_commit(&ctl->tfull[buf]);
+        for (int sub = 0; sub <= q.paired; ++sub, ++it) {
+          int k0, nk;
+          k_range(q, kc * (1 + q.paired) + sub, k0, nk);
+          const uint32_t buf = it & 1, use = it >> 1;
+          ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
+          ptx::tc_fence_after();
+          mma_tile(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, q.a_mn_major, q.b_mn_major);
+          ptx::umma_commit(&ctl->tfull[buf]);
+        }
       }
     }
-  } else {  // ---------------------------- epilogue warps
+  } else {  // ---------------------------- epilogue warps 2..9
+    const int ew = warp - 2;
     const int quad = warp & 3;
+    const int chalf = ew >> 2;
+    uint8_t* tile = staging + ew * STAGING_TILE;
     uint32_t it = 0;
-    uint32_t gslice = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
       int pi, mt, nt, kc;
       decode(u, pi, mt, nt, kc);
       const GemmProblem& q = p.prob[pi];
-      const uint32_t buf = it & 1, use = it >> 1;
-      ptx::mbar_wait(&ctl->tfull[buf], use & 1);
+      const uint32_t buf0 = it & 1, buf1 = (it + 1) & 1;
+      ptx::mbar_wait(&ctl->tfull[buf0], (it >> 1) & 1);
+      if (q.paired) ptx::mbar_wait(&ctl->tfull[buf1], ((it + 1) >> 1) & 1);
       ptx::tc_fence_after();
       const int row0 = mt * BM + quad * 32;  // first row of this warp's 32-row slab
       const int row = row0 + lane;
-      const uint32_t taddr = ctl->tmem_base + (uint32_t(quad * 32) << 16) + buf * BN;
-      if (q.tma_store) {
-        // 32 x 32 fp32 slices through swizzled staging -> 3-D TMA store (clipped at M / N).
-        const int z = int(row0 / q.row_div) + kc;
-        const int rlo = int(row0 % q.row_div);
+      const uint32_t lane_base = ctl->tmem_base + (uint32_t(quad * 32) << 16) + chalf * (BN / 2);
+      const uint32_t ta0 = lane_base + buf0 * BN, ta1 = lane_base + buf1 * BN;
+      const int cbase = nt * BN + chalf * (BN / 2);
+      float* orow = nullptr;
+      if (!q.tma_store && row < q.M)
+        orow = q.out + kc * q.chunk_stride + (row / q.row_div) * q.stride_hi + (row % q.row_div) * q.ld_out;
+      const int z = int(row0 / q.row_div) + kc;
+      const int rlo = int(row0 % q.row_div);
 #pragma unroll 1
-        for (int j = 0; j < BN / 32; ++j) {
-          const int c0 = nt * BN + j * 32;
-          if (c0 >= q.N) break;  // warp-uniform
-          float v[32];
-          ptx::tmem_ld32(taddr + j * 32, v);
+      for (int j = 0; j < BN / 64; ++j) {
+        const int c0 = cbase + j * 32;
+        if (c0 >= q.N) break;  // warp-uniform
+        float v[32];
+        ptx::tmem_ld32(ta0 + j * 32, v);
+        if (q.paired) {
+          float v1[32];
+          ptx::tmem_ld32(ta1 + j * 32, v1);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += v1[i];
+        }
+        if (q.tma_store) {
+          // 32 x 32 fp32 slice through swizzled staging -> 3-D TMA store (clipped at M / N).
           uint32_t w[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(v[i]);
-          uint8_t* tile = staging + ((warp - 2) * 2 + (gslice & 1)) * STAGING_TILE;
-          if (lane == 0) ptx::bulk_wait_read<1>();
+          if (lane == 0) ptx::bulk_wait_read<0>();
           __syncwarp();
           ptx::st_swizzled_row(tile, lane, w);
           ptx::fence_proxy_async_smem();
@@ -509,32 +541,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
             ptx::tma_store_3d(&q.out_map, tile, c0, rlo, z);
             ptx::bulk_commit();
           }
-          ++gslice;
-        }
-      } else {
-        float* orow = nullptr;
-        if (row < q.M)
-          orow = q.out + kc * q.chunk_stride + (row / q.row_div) * q.stride_hi + (row % q.row_div) * q.ld_out;
-#pragma unroll 1
-        for (int j = 0; j < BN / 32; ++j) {
-          const int c0 = nt * BN + j * 32;
-          if (c0 >= q.N) break;  // warp-uniform
-          float v[32];
-          ptx::tmem_ld32(taddr + j * 32, v);
-          if (orow) {
-            if (c0 + 32 <= q.N) {
-              float4* dst = reinterpret_cast<float4*>(orow + c0);
+        } else if (orow) {
+          if (c0 + 32 <= q.N) {
+            float4* dst = reinterpret_cast<float4*>(orow + c0);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            } else {
-              for (int i = 0; i < 32 && c0 + i < q.N; ++i) orow[c0 + i] = v[i];
-            }
+            for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          } else {
+            for (int i = 0; i < 32 && c0 + i < q.N; ++i) orow[c0 + i] = v[i];
           }
         }
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&ctl->tempty[buf]);
+      if (lane == 0) {
+        ptx::mbar_arrive(&ctl->tempty[buf0]);
+        if (q.paired) ptx::mbar_arrive(&ctl->tempty[buf1]);
+      }
+      it += 1 + q.paired;
     }
     if (lane == 0) ptx::bulk_wait_all();
   }
@@ -624,33 +647,32 @@ __global__ void unpack_kernel(const uint4* gathered, int N, int b, int Dp, uint4
   }
 }
 
-// Per (dir,row): fixed-tree combine of the column-chunk (max, sum-exp) partials.
+// Per (dir,row): fixed-order combine of the (column chunk, column half)
+// (max, sum-exp) partials.  Within a chunk: half 0 + half 1; across the 8
+// canonical chunks: balanced tree ((0+1)+(2+3))+((4+5)+(6+7)); non-canonical
+// chunkings: ascending order.
 //   lse2 (log2 domain), ce = -log softmax[label], glabel = P_label - 1 = -(sum_{j!=label} P_j).
 __global__ void stats_combine_kernel(const float2* stats, const float* target, int nchunk, int b, float* lse2_out,
                                      float* glabel_out, float* ce_out, Status* status) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 2 * b) return;
   const int dir = i / b, r = i % b;
+  auto at = [&](int c, int h) { return stats[((int64_t(dir) * nchunk + c) * 2 + h) * b + r]; };
   float m = -INFINITY;
-  float ms[8], ls[8];
-  for (int c = 0; c < nchunk; ++c) {
-    const float2 s = stats[(int64_t(dir) * nchunk + c) * b + r];
-    ms[c & 7] = s.x;
-    ls[c & 7] = s.y;
-    m = fmaxf(m, s.x);
-  }
+  for (int c = 0; c < nchunk; ++c) m = fmaxf(m, fmaxf(at(c, 0).x, at(c, 1).x));
+  auto chunk_sum = [&](int c) {
+    const float2 s0 = at(c, 0), s1 = at(c, 1);
+    return s0.y * ptx::ex2(s0.x - m) + s1.y * ptx::ex2(s1.x - m);
+  };
   float lo;
-  if (nchunk == 8) {  // balanced tree ((0+1)+(2+3))+((4+5)+(6+7))
+  if (nchunk == 8) {
     float t[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) t[c] = ls[c] * ptx::ex2(ms[c] - m);
+    for (int c = 0; c < 8; ++c) t[c] = chunk_sum(c);
     lo = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
-  } else {  // non-canonical: ascending chunk order
+  } else {
     lo = 0.f;
-    for (int c = 0; c < nchunk; ++c) {
-      const float2 s = stats[(int64_t(dir) * nchunk + c) * b + r];
-      lo += s.y * ptx::ex2(s.x - m);
-    }
+    for (int c = 0; c < nchunk; ++c) lo += chunk_sum(c);
   }
   const float yt = target[i];
   const float et = ptx::ex2(yt - m);
@@ -664,9 +686,31 @@ __global__ void stats_combine_kernel(const float2* stats, const float* target, i
   if (!isfinite(ce) || !isfinite(lse2)) atomicOr(&status->flags, FLAG_LOSS_NONFINITE);
 }
 
-// Sender-side fixed-tree sum of this rank's cpr canonical chunk partials:
-//   xpart [2][cpr][B][Dp] -> send [N][2][b][Dp] (destination-major). float4 per thread.
-__global__ void presum_kernel(const float4* xpart, int cpr, int N, int b, int Dp, float4* send) {
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4neg(float4 a) { return make_float4(-a.x, -a.y, -a.z, -a.w); }
+
+// Fixed-order sum of n float4 terms: balanced binary tree over ascending index
+// when n is a power of two <= 8 (a subtree of the canonical 8-chunk tree),
+// ascending sequential otherwise.
+template <typename Get>
+__device__ __forceinline__ float4 tree_sum(int n, Get get) {
+  if ((n & (n - 1)) == 0 && n <= 8) {
+    float4 acc[8];
+    for (int k = 0; k < n; ++k) acc[k] = get(k);
+    for (int w = 1; w < n; w <<= 1)
+      for (int k = 0; k + w < n; k += 2 * w) acc[k] = f4add(acc[k], acc[k + w]);
+    return acc[0];
+  }
+  float4 acc = get(0);
+  for (int k = 1; k < n; ++k) acc = f4add(acc, get(k));
+  return acc;
+}
+
+// Sender-side tree over this rank's np paired-chunk partials:
+//   xpart [2][np][B][Dp] -> send [N][2][b][Dp] (destination-major). float4 per thread.
+__global__ void presum_kernel(const float4* xpart, int np, int N, int b, int Dp, float4* send) {
   const int v4 = Dp / 4;
   const int64_t B = int64_t(N) * b;
   const int64_t per_g = B * v4;
@@ -676,56 +720,36 @@ __global__ void presum_kernel(const float4* xpart, int cpr, int N, int b, int Dp
     const int64_t rem = i - g * per_g;
     const int64_t c = rem / v4;
     const int vc = int(rem % v4);
-    const float4* src = xpart + (int64_t(g) * cpr) * per_g + rem;
-    float4 acc[8];
-    for (int k = 0; k < cpr; ++k) acc[k] = src[k * per_g];
-    for (int w = 1; w < cpr; w <<= 1)  // balanced binary tree over chunk index
-      for (int k = 0; k + w < cpr; k += 2 * w) {
-        acc[k].x += acc[k + w].x;
-        acc[k].y += acc[k + w].y;
-        acc[k].z += acc[k + w].z;
-        acc[k].w += acc[k + w].w;
-      }
+    const float4* src = xpart + (int64_t(g) * np) * per_g + rem;
+    const float4 acc = tree_sum(np, [&](int k) { return src[k * per_g]; });
     const int64_t dest = c / b, r = c % b;
-    send[((dest * 2 + g) * b + r) * v4 + vc] = acc[0];
+    send[((dest * 2 + g) * b + r) * v4 + vc] = acc;
   }
 }
 
-__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
-  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
-}
-__device__ __forceinline__ float4 f4neg(float4 a) { return make_float4(-a.x, -a.y, -a.z, -a.w); }
-
-// Owner combine: d_g[r] = s * (intra_g[r] + tree_src(+/- recv[src][g][r])), written b x D (ld_out).
-// Source tree: balanced over ascending src when N is a power of two (the top
-// levels of the canonical 8-chunk tree), ascending sequential otherwise.
-__global__ void combine_kernel(const float4* intra, const float4* recv, int N, int rank, int b, int Dp, int D,
-                               float s, int flip, float* d_image, float* d_text, int64_t ld_out, Status* status) {
+// Owner combine: d_g[r] = s * (intra_g[r] + cross_g[r]) written b x D (ld_out), where
+//   cross = tree over the N received slabs recv[src][g][r] (negated for src != rank if flip), or,
+//   single rank with canonical chunks (xpart != null), tree over the np local paired partials.
+__global__ void combine_kernel(const float4* intra, const float4* recv, const float4* xpart, int np, int N,
+                               int rank, int b, int Dp, int D, float s, int flip, float* d_image, float* d_text,
+                               int64_t ld_out, Status* status) {
   const int v4 = Dp / 4;
   const int64_t per_g = int64_t(b) * v4;
   const int64_t total = 2 * per_g;
-  const bool pow2 = (N & (N - 1)) == 0;
   bool bad = false;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     const int g = int(i / per_g);
     const int64_t rem = i - g * per_g;
     const int r = int(rem / v4), vc = int(rem % v4);
     float4 cross;
-    if (pow2 && N <= 8) {
-      float4 acc[8];
-      for (int src = 0; src < N; ++src) {
-        float4 x = recv[((int64_t(src) * 2 + g) * b) * v4 + rem];
-        acc[src] = (flip && src != rank) ? f4neg(x) : x;
-      }
-      for (int w = 1; w < N; w <<= 1)
-        for (int k = 0; k + w < N; k += 2 * w) acc[k] = f4add(acc[k], acc[k + w]);
-      cross = acc[0];
+    if (xpart) {
+      const float4* src = xpart + (int64_t(g) * np) * per_g + rem;
+      cross = tree_sum(np, [&](int k) { return src[k * per_g]; });
     } else {
-      cross = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int src = 0; src < N; ++src) {
-        float4 x = recv[((int64_t(src) * 2 + g) * b) * v4 + rem];
-        cross = (src == 0) ? ((flip && src != rank) ? f4neg(x) : x) : f4add(cross, (flip && src != rank) ? f4neg(x) : x);
-      }
+      cross = tree_sum(N, [&](int src) {
+        const float4 x = recv[((int64_t(src) * 2 + g) * b) * v4 + rem];
+        return (flip && src != rank) ? f4neg(x) : x;
+      });
     }
     const float4 t = f4add(intra[i], cross);
     float o[4] = {t.x * s, t.y * s, t.z * s, t.w * s};
@@ -742,10 +766,12 @@ __global__ void combine_kernel(const float4* intra, const float4* recv, int N, i
 }
 
 // Full-size contribution of this rank (reference LocalGradContribution):
-//   d_full_g[c] = s * (send slab_g[c] + [c in own rows] intra_g[c - rank*b]), rows outside negated if flip.
-__global__ void contribution_kernel(const float4* intra, const float4* send, int N, int rank, int b, int Dp, int D,
-                                    float s, int flip, float* d_image, float* d_text, int64_t ld_out,
-                                    Status* status) {
+//   d_full_g[c] = s * (cross_g[c] + [c in own rows] intra_g[c - rank*b]), rows outside negated if flip.
+//   cross_g[c] comes from the destination-major send slabs, or (single rank, canonical chunks) the
+//   tree over the paired partials.
+__global__ void contribution_kernel(const float4* intra, const float4* send, const float4* xpart, int np, int N,
+                                    int rank, int b, int Dp, int D, float s, int flip, float* d_image,
+                                    float* d_text, int64_t ld_out, Status* status) {
   const int v4 = Dp / 4;
   const int64_t B = int64_t(N) * b;
   const int64_t per_g = B * v4;
@@ -757,7 +783,13 @@ __global__ void contribution_kernel(const float4* intra, const float4* send, int
     const int64_t c = rem / v4;
     const int vc = int(rem % v4);
     const int64_t dest = c / b, r = c % b;
-    float4 x = send[((dest * 2 + g) * b + r) * v4 + vc];
+    float4 x;
+    if (xpart) {
+      const float4* src = xpart + (int64_t(g) * np) * per_g + rem;
+      x = tree_sum(np, [&](int k) { return src[k * per_g]; });
+    } else {
+      x = send[((dest * 2 + g) * b + r) * v4 + vc];
+    }
     const bool own = dest == rank;
     if (own) x = f4add(intra[(int64_t(g) * b + r) * v4 + vc], x);
     float sg = (flip && !own) ? -s : s;
@@ -843,6 +875,7 @@ struct Geometry {
   int64_t B, D, Dp, b, ldG;
   int N, rank;
   int nchunk, cpr;        // canonical chunks, chunks per rank
+  int np;                 // cross partials per rank after pairing chunks in the GEMM epilogue
   int chunk_cols;         // B / nchunk
   int64_t off[DISCO_R_COUNT];
   int64_t len[DISCO_R_COUNT];
@@ -874,18 +907,19 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
     g->cpr = 1;
   }
   g->chunk_cols = int(B / g->nchunk);
+  g->np = g->cpr >= 2 ? g->cpr / 2 : 1;
   const int64_t b = g->b, Dp = g->Dp, N = world;
   int64_t len[DISCO_R_COUNT];
   len[DISCO_R_PACK] = 2 * b * Dp * 2;
   len[DISCO_R_GATHER] = N > 1 ? N * 2 * b * Dp * 2 : 0;
   len[DISCO_R_FEAT] = 2 * B * Dp * 2;
   len[DISCO_R_FEAT16] = 2 * B * Dp * 2;
-  len[DISCO_R_STATS] = 2 * int64_t(g->nchunk) * b * 8;
+  len[DISCO_R_STATS] = 2 * int64_t(g->nchunk) * 2 * b * 8;
   len[DISCO_R_ROWS] = 4 * 2 * b * 4;
   len[DISCO_R_CE] = 2 * b * 4;
   len[DISCO_R_CE_ALL] = N * 2 * b * 4;
   len[DISCO_R_G] = 2 * b * g->ldG * 2;
-  len[DISCO_R_XPART] = g->cpr > 1 ? 2 * int64_t(g->cpr) * B * Dp * 4 : 0;
+  len[DISCO_R_XPART] = g->np > 1 ? 2 * int64_t(g->np) * B * Dp * 4 : 0;
   len[DISCO_R_SEND] = N * 2 * b * Dp * 4;
   len[DISCO_R_RECV] = N > 1 ? N * 2 * b * Dp * 4 : 0;
   len[DISCO_R_INTRA] = 2 * b * Dp * 4;
@@ -1201,15 +1235,16 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
     q.N = int(g.Dp);
     q.m_tiles = int((g.B + BM - 1) / BM);
     q.n_tiles = int((g.Dp + BN - 1) / BN);
-    q.k_chunks = g.cpr;
+    q.paired = g.cpr >= 2;
+    q.k_chunks = g.np;  // units along K (pairs of canonical chunks when paired)
     q.k_chunk_len = int(g.cpr > 1 ? Bc : g.b);
     q.k_total = int(g.b);
     q.a_k_off = 0;
     q.b_k_off = int(int64_t(g.rank) * g.b);
     q.a_row_off = 0;
-    if (g.cpr > 1) {  // canonical partials [2][cpr][B][Dp]
-      rc = set_output(q, region<float>(ws, g, DISCO_R_XPART) + int64_t(gi) * g.cpr * g.B * g.Dp, g.Dp, g.B, 0, 1,
-                      g.B * g.Dp, g.cpr);
+    if (g.np > 1) {  // paired canonical partials [2][np][B][Dp]
+      rc = set_output(q, region<float>(ws, g, DISCO_R_XPART) + int64_t(gi) * g.np * g.B * g.Dp, g.Dp, g.B, 0, 1,
+                      g.B * g.Dp, g.np);
     } else {  // directly destination-major send slabs [N][2][b][Dp]
       rc = set_output(q, region<float>(ws, g, DISCO_R_SEND) + int64_t(gi) * g.b * g.Dp, g.Dp, g.b, 2 * g.b * g.Dp,
                       world, 0, 1);
@@ -1217,9 +1252,9 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
     if (rc) return rc;
   }
   if ((rc = launch_gemm(p, st))) return rc;
-  if (g.cpr > 1) {
+  if (g.np > 1 && world > 1) {  // single rank: the owner combine reads the partials directly
     const int64_t n = 2 * g.B * (g.Dp / 4);
-    presum_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_XPART), g.cpr, world,
+    presum_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_XPART), g.np, world,
                                                            int(g.b), int(g.Dp), region<float4>(ws, g, DISCO_R_SEND));
     count_launch();
     CUDA_TRY(cudaGetLastError());
@@ -1270,8 +1305,9 @@ int disco_b200_combine(void* ws, int64_t B, int64_t D, int world, int rank, floa
   const float s = float(0.5 * double(t) / double(B));
   const int64_t n = 2 * g.b * (g.Dp / 4);
   combine_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
-      region<float4>(ws, g, DISCO_R_INTRA), region<float4>(ws, g, DISCO_R_RECV), world, rank, int(g.b), int(g.Dp),
-      int(D), s, flip, d_image, d_text, ld_out, region<Status>(ws, g, DISCO_R_STATUS));
+      region<float4>(ws, g, DISCO_R_INTRA), region<float4>(ws, g, DISCO_R_RECV),
+      (world == 1 && g.np > 1) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, world, rank, int(g.b),
+      int(g.Dp), int(D), s, flip, d_image, d_text, ld_out, region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
@@ -1287,8 +1323,9 @@ int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank,
   const float s = float(0.5 * double(t) / double(g.b));
   const int64_t n = 2 * g.B * (g.Dp / 4);
   contribution_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
-      region<float4>(ws, g, DISCO_R_INTRA), region<float4>(ws, g, DISCO_R_SEND), world, rank, int(g.b), int(g.Dp),
-      int(D), s, flip && world > 1, d_image_full, d_text_full, ld_out, region<Status>(ws, g, DISCO_R_STATUS));
+      region<float4>(ws, g, DISCO_R_INTRA), region<float4>(ws, g, DISCO_R_SEND),
+      (world == 1 && g.np > 1) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, world, rank, int(g.b),
+      int(g.Dp), int(D), s, flip && world > 1, d_image_full, d_text_full, ld_out, region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
