@@ -327,26 +327,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
             if (cb >= chunk_hi) break;  // warp-uniform
             float v[32];
             ptx::tmem_ld32(taddr + j * 32, v);
-            float cmax = -INFINITY;
+            const int li = label - cb;
+            const bool has_label = unsigned(li) < 32u && label < chunk_hi;
+            if (cb + 32 <= chunk_hi && !has_label) {
+              // fast path (all but one group per row): no masking, no label handling.
+              float cm = v[0];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float y = (cb + i < chunk_hi) ? v[i] * p.tl2e : -INFINITY;
-              v[i] = y;
-              cmax = fmaxf(cmax, y);
-              if (cb + i == label && cb + i < chunk_hi) {  // masked columns belong to the next chunk
-                yt = y;
-                has_t = true;
+              for (int i = 1; i < 32; ++i) cm = fmaxf(cm, v[i]);
+              const float mnew = fmaxf(m2, cm * p.tl2e);
+              float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                s0 += ptx::ex2(fmaf(v[i], p.tl2e, -mnew));
+                s1 += ptx::ex2(fmaf(v[i + 1], p.tl2e, -mnew));
               }
-            }
-            const float mnew = fmaxf(m2, cmax);
-            float s = 0.f;
+              l = l * ptx::ex2(m2 - mnew) + (s0 + s1);
+              m2 = mnew;
+            } else {
+              // edge / label group: mask columns past the chunk, keep the label term out of l.
+              float cm = -INFINITY;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float e = ptx::ex2(v[i] - mnew);
-              s += (cb + i == label) ? 0.f : e;
+              for (int i = 0; i < 32; ++i) {
+                const bool ok = cb + i < chunk_hi;
+                cm = ok ? fmaxf(cm, v[i]) : cm;
+                if (i == li && has_label) {
+                  yt = v[i] * p.tl2e;
+                  has_t = true;
+                }
+              }
+              const float mnew = fmaxf(m2, cm * p.tl2e);
+              float s = 0.f;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float e = ptx::ex2(fmaf(v[i], p.tl2e, -mnew));
+                s += (cb + i < chunk_hi && i != li) ? e : 0.f;
+              }
+              l = l * ptx::ex2(m2 - mnew) + s;
+              m2 = mnew;
             }
-            l = l * ptx::ex2(m2 - mnew) + s;
-            m2 = mnew;
           }
         } else {
           // G = exp2(y - lse2) (label column: P_label - 1), f16, 64-column slices
@@ -356,19 +374,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
             const int cb = col0 + j * 64;
             if (cb >= chunk_hi) break;  // warp-uniform
             uint32_t h[32];
+            const int li = label - cb;
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
               float v[32];
               ptx::tmem_ld32(taddr + j * 64 + half * 32, v);
 #pragma unroll
               for (int i = 0; i < 32; i += 2) {
-                const int c = cb + half * 32 + i;
                 float g0 = ptx::ex2(fmaf(v[i], p.tl2e, -lse2));
                 float g1 = ptx::ex2(fmaf(v[i + 1], p.tl2e, -lse2));
-                if (c == label) g0 = gl;
-                if (c + 1 == label) g1 = gl;
                 __half2 hh = __floats2half2_rn(g0, g1);
                 h[half * 16 + i / 2] = *reinterpret_cast<uint32_t*>(&hh);
+              }
+            }
+            if (unsigned(li) < 64u) {  // label column: P_label - 1 (warp-uniform for canonical layouts)
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                if (li >> 1 == k) {
+                  __half2 hh = *reinterpret_cast<__half2*>(&h[k]);
+                  if (li & 1) hh.y = __float2half_rn(gl); else hh.x = __float2half_rn(gl);
+                  h[k] = *reinterpret_cast<uint32_t*>(&hh);
+                }
               }
             }
             if ((chunk_lo & 63) == 0 && (cb + 64 <= chunk_hi || chunk_hi == p.B)) {
@@ -382,9 +408,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
                 ptx::bulk_commit();
               }
             } else if (row_ok) {  // non-canonical chunk edges (b not a multiple of 64): scalar path
-              for (int i = 0; i < 64 && cb + i < chunk_hi; ++i) {
+#pragma unroll
+              for (int i = 0; i < 64; i += 2) {
                 const uint32_t w = h[i / 2];
-                grow[cb + i] = __ushort_as_half((i & 1) ? (unsigned short)(w >> 16) : (unsigned short)(w & 0xFFFF));
+                if (cb + i < chunk_hi) grow[cb + i] = __ushort_as_half((unsigned short)(w & 0xFFFF));
+                if (cb + i + 1 < chunk_hi) grow[cb + i + 1] = __ushort_as_half((unsigned short)(w >> 16));
               }
             }
           }
