@@ -191,14 +191,22 @@ def _stage(x, device):
     return x, origin
 
 
-def _unstage(t: torch.Tensor, origin):
+def _unstage_async(t: torch.Tensor, origin):
+    """Start the device->host copy of an output into pinned memory (no sync)."""
     if origin == "cuda":
         return t
-    if origin == "cpu":
-        return t.cpu()
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t, non_blocking=True)
+    return host
+
+
+def _unstage_finish(h: torch.Tensor, origin):
+    """After the stream synchronised: hand the host copy out in the caller's container."""
+    if origin == "cuda" or origin == "cpu":
+        return h
     _, dtype = origin
-    out = t.cpu().numpy()
-    return out.astype(dtype) if np.issubdtype(dtype, np.floating) else out
+    out = h.numpy()
+    return out.astype(dtype) if np.issubdtype(dtype, np.floating) and out.dtype != dtype else out
 
 
 def _stream_ptr(device) -> int:
@@ -280,10 +288,11 @@ def local_loss_and_grads(layout: ShardLayout, I_gathered, T_gathered, t: float, 
     _lib.call("disco_b200_contribution", *plan.args, t, int(bool(flip_cross_rank_sign)),
               d_image.data_ptr(), d_text.data_ptr(), D, st)
     _lib.call("disco_b200_loss", *plan.args, 1, st)
+    h_image, h_text = _unstage_async(d_image, origin), _unstage_async(d_text, origin)
     loss, flags = _read_status(plan)
     _raise_on_flags(flags)
     _account_loss_scope(loss_counters, exchange_counters, b, B, D)
-    return LocalGradContribution(_unstage(d_image, origin), _unstage(d_text, origin), loss)
+    return LocalGradContribution(_unstage_finish(h_image, origin), _unstage_finish(h_text, origin), loss)
 
 
 def _account_loss_scope(loss_counters, exchange_counters, b, B, D) -> None:
@@ -371,10 +380,11 @@ def disco_step(endpoint, local_I, local_T, t: float, *, loss_counters: Counters 
     exchange_counters.alloc(2 * batch * dim)
     d_image, d_text, plan = disco_step_async(endpoint, I_dev, T_dev, t,
                                              flip_cross_rank_sign=flip_cross_rank_sign)
+    h_image, h_text = _unstage_async(d_image, origin), _unstage_async(d_text, origin)
     loss = finish_status(plan)
     _account_loss_scope(loss_counters, exchange_counters, layout.local_batch, batch, dim)
     exchange_counters.alloc(batch * dim)
     exchange_counters.release(batch * dim)
     exchange_counters.alloc(batch * dim)
     exchange_counters.release(batch * dim)
-    return _unstage(d_image, origin), _unstage(d_text, origin), loss
+    return _unstage_finish(h_image, origin), _unstage_finish(h_text, origin), loss

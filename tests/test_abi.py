@@ -1,0 +1,96 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol of include/disco_b200.h.
+
+Only host-side entry points (geometry, workspace layout, chunking) are called
+here; nothing touches a device.
+"""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2304_08480_b200 import _lib
+from paper_2304_08480_b200.errors import LayoutError, ShapeError
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(__file__)), "include", "disco_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(disco_b200_\w+)\s*\(", text)))
+
+
+def test_library_builds_and_loads():
+    from paper_2304_08480_b200 import build
+    build.build()
+    lib = _lib.load()
+    assert lib.disco_b200_abi_version() == _lib.ABI_VERSION
+
+
+def test_every_header_symbol_is_exported_and_bound():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 12
+    for name in syms:
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} has no ctypes binding"
+    assert set(_lib.SIGNATURES) == set(syms)
+
+
+def test_layout_validation_matches_shard_layout():
+    # ShardLayout rules (shard.py:38-49) enforced by the C side too
+    with pytest.raises(LayoutError, match="not divisible"):
+        _lib.workspace_bytes(8, 4, 3, 0)
+    with pytest.raises(LayoutError):
+        _lib.workspace_bytes(8, 4, 2, 2)
+    with pytest.raises(LayoutError):
+        _lib.workspace_bytes(8, 4, 0, 0)
+    with pytest.raises(LayoutError):
+        _lib.workspace_bytes(0, 4, 1, 0)
+    with pytest.raises(ShapeError):
+        _lib.workspace_bytes(8, 0, 1, 0)
+
+
+@pytest.mark.parametrize("B,N,expect", [(32768, 1, (8, 8)), (32768, 2, (8, 4)), (32768, 4, (8, 2)),
+                                         (32768, 8, (8, 1)), (1024, 2, (8, 4)), (12, 3, (3, 1)),
+                                         (8, 2, (2, 1)), (30000, 2, (2, 1)), (196608, 8, (8, 1))])
+def test_canonical_chunking(B, N, expect):
+    assert _lib.chunking(B, N) == expect
+
+
+def test_workspace_regions_are_disjoint_and_aligned():
+    B, D, N = 32768, 512, 8
+    total = _lib.workspace_bytes(B, D, N, 3)
+    spans = []
+    for r in range(14):
+        off, size = _lib.ws_region(B, D, N, 3, r)
+        assert off % 1024 == 0
+        assert off + size <= total
+        if size:
+            spans.append((off, off + size))
+    spans.sort()
+    for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+        assert a1 <= b0
+    b, Dp = B // N, 512
+    assert _lib.ws_region(B, D, N, 3, _lib.R_G)[1] == 2 * b * B * 2          # f16 G, O(B^2/N)
+    assert _lib.ws_region(B, D, N, 3, _lib.R_SEND)[1] == N * 2 * b * Dp * 4  # slabs by destination
+    assert _lib.ws_region(B, D, N, 3, _lib.R_GATHER)[1] == N * 2 * b * Dp * 2
+
+
+def test_single_rank_aliases_collective_buffers():
+    g = _lib.ws_region(4096, 100, 1, 0, _lib.R_GATHER)
+    p = _lib.ws_region(4096, 100, 1, 0, _lib.R_PACK)
+    assert g == p
+    assert _lib.ws_region(4096, 100, 1, 0, _lib.R_RECV) == _lib.ws_region(4096, 100, 1, 0, _lib.R_SEND)
+
+
+def test_loss_memory_scales_as_b_squared_over_n():
+    # per-GPU loss-scope memory (the f16 G blocks) falls as 1/N at fixed B
+    B, D = 65536, 768
+    g = [_lib.ws_region(B, D, N, 0, _lib.R_G)[1] for N in (1, 2, 4, 8)]
+    assert g[0] == 2 * g[1] == 4 * g[2] == 8 * g[3]
+
+
+def test_launch_counter_starts_at_zero_without_gpu():
+    assert _lib.launch_count() >= 0
