@@ -18,9 +18,13 @@
 //                         fp32 tiles into partial / slab buffers.
 //   small kernels       : pack, unpack, stats combine, chunk presum, owner
 //                         combine, contribution, loss.
-// All GEMMs: TMA (SWIZZLE_128B) -> 4-stage smem ring -> single-thread
-// tcgen05.mma (M=128, N=256, K=16) -> double-buffered TMEM accumulators ->
-// 4 epilogue warps (tcgen05.ld 32x32b).  Persistent grid of <= #SM CTAs.
+// All tensor-core kernels run on CTA pairs (cluster of 2, cta_group::2):
+//   TMA (SWIZZLE_128B; each CTA loads its 128 A rows and its 128-column half of
+//   B, completion counted on the leader's barrier) -> 6-stage smem ring ->
+//   single-thread tcgen05.mma M=256 N=256 K=16 issued by the leader ->
+//   double-buffered TMEM accumulators (each CTA holds its 128 rows x 256 cols)
+//   -> 8 epilogue warps per CTA (tcgen05.ld 32x32b).  Persistent grid of
+//   <= #SM CTAs; a unit of work is owned by a CTA pair.
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -29,6 +33,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -41,28 +46,30 @@
 namespace disco {
 
 // ------------------------------------------------------------------ tiling
-constexpr int BM = 128;
-constexpr int BN = 256;
+constexpr int BM = 128;      // rows per CTA (the pair covers 256)
+constexpr int BN = 256;      // accumulator columns (each CTA loads 128 of the B operand rows)
 constexpr int BK = 64;
-constexpr int STAGES = 4;
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KiB
-constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KiB
+constexpr int PAIR_M = 2 * BM;
+constexpr int STAGES = 6;
+constexpr int A_STAGE_BYTES = BM * BK * 2;        // 16 KiB
+constexpr int B_STAGE_BYTES = (BN / 2) * BK * 2;  // 16 KiB (this CTA's half of N)
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int NUM_THREADS = 320;  // warp0 TMA, warp1 MMA, warps2-9 epilogue
-constexpr int TMEM_COLS = 512;    // 2 accumulators of 128 x 256 fp32
+constexpr int NUM_EPI_WARPS = 8;
+constexpr int TMEM_COLS = 512;    // 2 accumulators of 128 lanes x 256 fp32 columns
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
 struct SmemCtl {
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
-  uint64_t tfull[2];
-  uint64_t tempty[2];
+  uint64_t full[STAGES];   // leader: TMA bytes of both CTAs landed
+  uint64_t empty[STAGES];  // both: MMA done reading the stage (multicast commit)
+  uint64_t tfull[2];       // both: accumulator ready (multicast commit)
+  uint64_t tempty[2];      // leader: both CTAs' epilogues drained the accumulator
   uint32_t tmem_base;
 };
-// Epilogue staging: 8 warps x (32 rows x 128 B), TMA SWIZZLE_128B layout.
+// Epilogue staging: 8 warps x (32 rows x 128 B), swizzled like TMA SWIZZLE_128B.
 constexpr int STAGING_TILE = 32 * 128;
-constexpr int STAGING_BYTES = 8 * STAGING_TILE;
+constexpr int STAGING_BYTES = NUM_EPI_WARPS * STAGING_TILE;
 constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + STAGING_BYTES + 256;
 static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory limit");
 
@@ -83,10 +90,9 @@ struct Status {
 // gathered matrix (row offset rank*b), B rows are all B gathered rows.
 struct LogitsParams {
   CUtensorMap a_map[2];  // dir 0: I_g, dir 1: T_g   box {64, 128}
-  CUtensorMap b_map[2];  // dir 0: T_g, dir 1: I_g   box {64, 256}
-  CUtensorMap g_map[2];  // G store maps, box {64, 32} f16
+  CUtensorMap b_map[2];  // dir 0: T_g, dir 1: I_g   box {64, 128} (each CTA loads its half of N)
   int B, b, Dp, rank;
-  int nchunk, chunk_cols, tiles_per_chunk, row_tiles;
+  int nchunk, chunk_cols, tiles_per_chunk, row_tiles;  // row_tiles counts 256-row pair tiles
   float tl2e;  // t * log2(e)
   // FWD outputs
   float2* stats;   // [2][nchunk][2 column halves][b]
@@ -94,8 +100,10 @@ struct LogitsParams {
   // GRAD inputs / outputs
   const float* lse2;    // [2][b]
   const float* glabel;  // [2][b]
-  __half* G;            // [2][b][ldG]
+  __half* G;            // [2][b][ldG] row-major, or blocked (see g_blocked)
   int64_t ldG;
+  int g_blocked;        // 1: G stored as [2][b/128][B/128][128][128] (contiguous 32 KiB blocks)
+  int debug_flags;      // DISCO_DEBUG_FLAGS (profiling experiments only): bit0 skip G stores
 };
 
 struct GemmProblem {
@@ -104,9 +112,10 @@ struct GemmProblem {
   CUtensorMap out_map;    // 3-D fp32 store map {N, row_div, z}, box {32, 32, 1}
   int tma_store;          // 1: TMA stores through staging smem; 0: direct st.global
   int paired;             // 1: unit = chunks (2kc, 2kc+1), summed in the epilogue
+  int a_blocked;          // 1: A is a blocked G ([rows/128][cols/128][128][128], 4-D map)
   int a_mn_major, b_mn_major;
   int M, N;               // valid output extents
-  int m_tiles, n_tiles, k_chunks;
+  int m_tiles, n_tiles, k_chunks;  // m tiles of 256 rows (CTA pair), n tiles of 256 columns
   int k_chunk_len;        // elements of K per chunk (multiple of 64 unless k_chunks == 1)
   int k_total;            // total K extent
   int a_k_off, b_k_off;   // added to the K coordinate of MN-major operands
@@ -125,13 +134,28 @@ struct GemmParams {
 };
 
 // --------------------------------------------------------- shared helpers
-__device__ __forceinline__ void load_operand(const CUtensorMap* map, int mn_major, uint8_t* dst, uint64_t* bar,
+// TMA load of one operand stage into this CTA's smem; completion on the leader's barrier.
+// Blocked operands (G in [r/128][c/128][128][128] layout) are addressed through a 4-D map:
+// K-major: rows = G rows, K = G columns; MN-major: MN = G columns, K = G rows.
+__device__ __forceinline__ void load_blocked(const CUtensorMap* map, int mn_major, uint8_t* dst, uint32_t bar,
                                              int mn0, int k0, int rows, uint64_t policy) {
   if (!mn_major) {
-    ptx::tma_load_2d(dst, map, bar, k0, mn0, policy);  // box {64 (K), rows}
+    ptx::tma_load_4d_pair(dst, map, bar, k0 & 127, mn0 & 127, k0 >> 7, mn0 >> 7, policy);  // box {64, rows, 1, 1}
+  } else {
+    for (int j = 0; j < rows / 64; ++j) {
+      const int c = mn0 + j * 64;
+      ptx::tma_load_4d_pair(dst + j * 8192, map, bar, c & 127, k0 & 127, c >> 7, k0 >> 7, policy);  // {64, 64, 1, 1}
+    }
+  }
+}
+
+__device__ __forceinline__ void load_operand(const CUtensorMap* map, int mn_major, uint8_t* dst, uint32_t bar,
+                                             int mn0, int k0, int rows, uint64_t policy) {
+  if (!mn_major) {
+    ptx::tma_load_2d_pair(dst, map, bar, k0, mn0, policy);  // box {64 (K), rows}
   } else {
     for (int j = 0; j < rows / 64; ++j)  // box {64 (MN), 64 (K)} per 8 KiB atom column
-      ptx::tma_load_2d(dst + j * 8192, map, bar, mn0 + j * 64, k0, policy);
+      ptx::tma_load_2d_pair(dst + j * 8192, map, bar, mn0 + j * 64, k0, policy);
   }
 }
 
@@ -154,7 +178,7 @@ __device__ __forceinline__ uint8_t* smem_base(uint8_t* raw) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
 }
 
-// MMA issue for one accumulator tile: nk k-blocks of BK, 4 UMMAs each.
+// Leader-side MMA issue for one accumulator tile: nk k-blocks of BK, 4 UMMAs each.
 __device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe& pipe, int nk, uint32_t d_tmem,
                                          uint32_t idesc, int a_mn, int b_mn) {
   for (int kb = 0; kb < nk; ++kb) {
@@ -164,12 +188,21 @@ __device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe& pip
     const uint32_t b_base = a_base + A_STAGE_BYTES;
 #pragma unroll
     for (int kk = 0; kk < BK / 16; ++kk) {
-      ptx::umma_f16(d_tmem, operand_desc(a_base, a_mn, kk), operand_desc(b_base, b_mn, kk), idesc,
-                    (kb | kk) != 0);
+      ptx::umma_f16_pair(d_tmem, operand_desc(a_base, a_mn, kk), operand_desc(b_base, b_mn, kk), idesc,
+                         (kb | kk) != 0);
     }
-    ptx::umma_commit(&ctl->empty[pipe.stage]);  // smem slot free once these MMAs retire
+    ptx::umma_commit_pair(&ctl->empty[pipe.stage], 0x3);  // both CTAs' smem slots free
     pipe.advance();
   }
+}
+
+// Producer side of one k-block: wait for the slot, arm the leader's barrier, load.
+__device__ __forceinline__ uint8_t* producer_acquire(SmemCtl* ctl, uint8_t* tiles, Pipe& pipe, bool leader,
+                                                     uint32_t& bar) {
+  ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
+  if (leader) ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], 2 * STAGE_BYTES);
+  bar = ptx::map_to_rank(&ctl->full[pipe.stage], 0);
+  return tiles + pipe.stage * STAGE_BYTES;
 }
 
 __device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane) {
@@ -180,55 +213,64 @@ __device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&ctl->tfull[i], 1);
-      ptx::mbar_init(&ctl->tempty[i], 8);  // one arrive per epilogue warp
+      ptx::mbar_init(&ctl->tempty[i], 2 * NUM_EPI_WARPS);  // every epilogue warp of both CTAs
     }
     ptx::fence_barrier_init();
   }
   if (warp == 1) {
-    ptx::tmem_alloc(&ctl->tmem_base, TMEM_COLS);
-    ptx::tmem_relinquish();
+    ptx::tmem_alloc_pair(&ctl->tmem_base, TMEM_COLS);
+    ptx::tmem_relinquish_pair();
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();
   ptx::tc_fence_after();
 }
 
 __device__ __forceinline__ void kernel_epilogue(SmemCtl* ctl, int warp) {
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();  // neither CTA leaves while the pair's MMAs / arrivals may touch it
   if (warp == 1) {
-    __syncwarp();
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(ctl->tmem_base, TMEM_COLS);
+    ptx::tmem_dealloc_pair(ctl->tmem_base, TMEM_COLS);
   }
 }
 
+// Epilogue warp releases an accumulator buffer on the leader's barrier.
+__device__ __forceinline__ void release_accumulator(SmemCtl* ctl, int buf, int lane) {
+  ptx::tc_fence_before();
+  __syncwarp();
+  if (lane == 0) ptx::mbar_arrive_cluster(ptx::map_to_rank(&ctl->tempty[buf], 0));
+}
+
 // =====================================================================
-// logits kernel: S tiles for both directions.
-//   FWD : unit = (dir, row tile, column chunk); tiles = column tiles of the chunk,
-//         each epilogue thread keeps an online (max, sum-exp) for its row over
-//         its column half of every tile of the unit.
-//   GRAD: unit = (dir, row tile, column chunk, column tile); epilogue writes G.
+// logits kernel: S tiles for both directions, CTA pair = 256 local rows.
+//   FWD : unit = (dir, row pair tile, column chunk); tiles = column tiles of
+//         the chunk; each epilogue thread keeps an online (max, sum-exp) for
+//         its row over its column half of every tile of the unit.
+//   GRAD: unit = (dir, row pair tile, column chunk, column tile); writes G.
 // Both kinds walk identical tiles (same column origin and K order), so the
 // recomputed S in GRAD is bit-identical to the forward S.
 // Epilogue: 8 warps; warp w reads TMEM lane quadrant (w % 4) and column half
-// (w - 2) / 4 of the 128 x 256 accumulator.
+// (w - 2) / 4 of this CTA's 128 x 256 accumulator.
 // =====================================================================
 enum { KIND_FWD = 0, KIND_GRAD = 1 };
 
 template <int KIND>
-__global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_constant__ LogitsParams p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    logits_kernel(const __grid_constant__ LogitsParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
   uint8_t* staging = tiles + STAGES * STAGE_BYTES;
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(staging + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int crank = int(ptx::cluster_ctarank());
+  const bool leader = crank == 0;
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
 
   if (warp == 0 && lane == 0) {
     for (int d = 0; d < 2; ++d) {
       ptx::prefetch_tmap(&p.a_map[d]);
       ptx::prefetch_tmap(&p.b_map[d]);
-      if (KIND == KIND_GRAD) ptx::prefetch_tmap(&p.g_map[d]);
     }
   }
   kernel_prologue(ctl, warp, lane);
@@ -255,38 +297,55 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
   };
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       Pipe pipe;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      // L2 prefetch of the operands of the tile after the current one: the G
+      // write stream (GRAD) evicts feature lines, and a demand miss behind the
+      // DRAM write queue is longer than the smem ring can cover.
+      auto prefetch_tile = [&](int u, int ti) {
+        if (u >= num_units) return;
+        if (ti >= tiles_per_unit) {
+          u += npairs;
+          ti = 0;
+          if (u >= num_units) return;
+        }
         int dir, rt, ch, t0;
         decode(u, dir, rt, ch, t0);
-        const int a_row = p.rank * p.b + rt * BM;
+        const int a_row = p.rank * p.b + rt * PAIR_M + crank * BM;
+        const int col0 = ch * p.chunk_cols + (t0 + ti) * BN + crank * (BN / 2);
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::tma_prefetch_2d(&p.a_map[dir], kb * BK, a_row);
+          ptx::tma_prefetch_2d(&p.b_map[dir], kb * BK, col0);
+        }
+      };
+      for (int u = pair; u < num_units; u += npairs) {
+        int dir, rt, ch, t0;
+        decode(u, dir, rt, ch, t0);
+        const int a_row = p.rank * p.b + rt * PAIR_M + crank * BM;
         for (int ti = 0; ti < tiles_per_unit; ++ti) {
-          const int col0 = ch * p.chunk_cols + (t0 + ti) * BN;
+          const int col0 = ch * p.chunk_cols + (t0 + ti) * BN + crank * (BN / 2);
           for (int kb = 0; kb < nk; ++kb) {
-            ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
-            uint8_t* st = tiles + pipe.stage * STAGE_BYTES;
-            ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], STAGE_BYTES);
-            ptx::tma_load_2d(st, &p.a_map[dir], &ctl->full[pipe.stage], kb * BK, a_row, ptx::kEvictLast);
-            ptx::tma_load_2d(st + A_STAGE_BYTES, &p.b_map[dir], &ctl->full[pipe.stage], kb * BK, col0,
-                             ptx::kEvictLast);
+            uint32_t bar;
+            uint8_t* st = producer_acquire(ctl, tiles, pipe, leader, bar);
+            ptx::tma_load_2d_pair(st, &p.a_map[dir], bar, kb * BK, a_row, ptx::kEvictLast);
+            ptx::tma_load_2d_pair(st + A_STAGE_BYTES, &p.b_map[dir], bar, kb * BK, col0, ptx::kEvictLast);
             pipe.advance();
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      constexpr uint32_t idesc = ptx::instr_desc_f16(BM, BN, 1, 1, 0, 0);  // bf16 x bf16, both K-major
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader CTA)
+      constexpr uint32_t idesc = ptx::instr_desc_f16(PAIR_M, BN, 1, 1, 0, 0);  // bf16 x bf16, both K-major
       Pipe pipe;
       uint32_t it = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      for (int u = pair; u < num_units; u += npairs) {
         for (int ti = 0; ti < tiles_per_unit; ++ti, ++it) {
           const uint32_t buf = it & 1, use = it >> 1;
           ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
           ptx::tc_fence_after();
           mma_tile(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, 0, 0);
-          ptx::umma_commit(&ctl->tfull[buf]);
+          ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
         }
       }
     }
@@ -294,13 +353,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
     const int ew = warp - 2;
     const int quad = warp & 3;
     const int chalf = ew >> 2;  // column half of the 256-wide tile
-    const int r_in_tile = quad * 32 + lane;
+    const int r_in_tile = crank * BM + quad * 32 + lane;
     uint8_t* tile = staging + ew * STAGING_TILE;
     uint32_t it = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+    for (int u = pair; u < num_units; u += npairs) {
       int dir, rt, ch, t0;
       decode(u, dir, rt, ch, t0);
-      const int row = rt * BM + r_in_tile;        // local row
+      const int row = rt * PAIR_M + r_in_tile;    // local row
       const bool row_ok = row < p.b;
       const int label = p.rank * p.b + row;        // global column of the positive pair
       const int chunk_lo = ch * p.chunk_cols;
@@ -368,7 +427,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
           }
         } else {
           // G = exp2(y - lse2) (label column: P_label - 1), f16, 64-column slices
-          // staged in swizzled smem and written by TMA (coalesced, clipped at b / B).
+          // transposed through swizzled smem and written as full 128-byte rows.
 #pragma unroll 1
           for (int j = 0; j < BN / 128; ++j) {
             const int cb = col0 + j * 64;
@@ -397,16 +456,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
                 }
               }
             }
-            if ((chunk_lo & 63) == 0 && (cb + 64 <= chunk_hi || chunk_hi == p.B)) {
-              if (lane == 0) ptx::bulk_wait_read<0>();  // previous store drained the buffer
-              __syncwarp();
+            if (p.debug_flags & 1) {
+              if (h[0] == 0x7fffffffu) grow[0] = __float2half(0.f);  // keep the math live
+            } else if (p.debug_flags & 4) {  // staging only, no global store
               ptx::st_swizzled_row(tile, lane, h);
-              ptx::fence_proxy_async_smem();
               __syncwarp();
-              if (lane == 0) {
-                ptx::tma_store_2d(&p.g_map[dir], tile, cb, rt * BM + quad * 32);
-                ptx::bulk_commit();
+              const uint4 v = *reinterpret_cast<const uint4*>(tile + ((lane * 16) ^ 16));
+              if (v.x == 0x7fffffffu) grow[0] = __float2half(0.f);
+              __syncwarp();
+            } else if ((p.debug_flags & 8) && p.g_blocked) {  // direct register -> global, no staging
+              const int rbase = rt * PAIR_M + crank * BM + quad * 32;
+              const int64_t nbc = p.B >> 7;
+              __half* blk = p.G + int64_t(dir) * p.b * p.B +
+                            ((int64_t(rbase >> 7) * nbc + (cb >> 7)) << 14) + (rbase & 127) * 128 + (cb & 127);
+              uint4* dst = reinterpret_cast<uint4*>(blk + lane * 128);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) dst[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+            } else if ((chunk_lo & 63) == 0 && (cb + 64 <= chunk_hi || (chunk_hi == p.B && (p.B & 63) == 0))) {
+              ptx::st_swizzled_row(tile, lane, h);
+              __syncwarp();
+              const int rbase = rt * PAIR_M + crank * BM + quad * 32;
+              if (p.g_blocked) {
+                // block (rbase/128, cb/128): 128 x 128 halves, row pitch 256 B -> this warp's
+                // two 64-column slices fill one contiguous 8 KiB run.
+                const int64_t nbc = p.B >> 7;
+                __half* blk = p.G + int64_t(dir) * p.b * p.B +
+                              ((int64_t(rbase >> 7) * nbc + (cb >> 7)) << 14) + (rbase & 127) * 128 + (cb & 127);
+                ptx::store_tile_rows(tile, lane, [&](int r) -> uint8_t* {
+                  return rbase + r < p.b ? reinterpret_cast<uint8_t*>(blk + r * 128) : nullptr;
+                }, ptx::kEvictFirst);
+              } else {
+                __half* gbase = p.G + int64_t(dir) * p.b * p.ldG + cb;
+                ptx::store_tile_rows(tile, lane, [&](int r) -> uint8_t* {
+                  return rbase + r < p.b ? reinterpret_cast<uint8_t*>(gbase + int64_t(rbase + r) * p.ldG) : nullptr;
+                }, ptx::kEvictFirst);
               }
+              __syncwarp();
             } else if (row_ok) {  // non-canonical chunk edges (b not a multiple of 64): scalar path
 #pragma unroll
               for (int i = 0; i < 64; i += 2) {
@@ -417,33 +502,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) logits_kernel(const __grid_con
             }
           }
         }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&ctl->tempty[buf]);
+        release_accumulator(ctl, buf, lane);
       }
       if (KIND == KIND_FWD && row_ok) {
         p.stats[((int64_t(dir) * p.nchunk + ch) * 2 + chalf) * p.b + row] = make_float2(m2, l);
         if (has_t) p.target[dir * p.b + row] = yt;
       }
     }
-    if (KIND == KIND_GRAD && lane == 0) ptx::bulk_wait_all();
   }
   kernel_epilogue(ctl, warp);
 }
 
 // =====================================================================
-// Grouped f16 GEMM with fp32 tile outputs.
+// Grouped f16 GEMM with fp32 tile outputs, CTA pair = 256 x 256 tile.
 //   unit = (problem, m tile, n tile, k chunk); one accumulator tile per unit,
 //   or, for `paired` problems, two consecutive canonical K chunks accumulated
 //   into the two TMEM buffers and summed in the epilogue ((c0 + c1): the first
 //   level of the fixed reduction tree).
 // =====================================================================
-__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
   uint8_t* staging = tiles + STAGES * STAGE_BYTES;
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(staging + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int crank = int(ptx::cluster_ctarank());
+  const bool leader = crank == 0;
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < p.nprob; ++i) {
@@ -455,7 +541,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
   kernel_prologue(ctl, warp, lane);
 
   const int num_units = p.units[p.nprob];
-  // unit -> (problem, mt, nt, kc); nt fastest so CTAs sharing an A tile run together.
+  // unit -> (problem, mt, nt, kc); nt fastest so pairs sharing an A tile run together.
   auto decode = [&](int u, int& pi, int& mt, int& nt, int& kc) {
     pi = 0;
     while (pi + 1 < p.nprob && u >= p.units[pi + 1]) ++pi;
@@ -474,40 +560,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
   };
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       Pipe pipe;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      for (int u = pair; u < num_units; u += npairs) {
         int pi, mt, nt, kc;
         decode(u, pi, mt, nt, kc);
         const GemmProblem& q = p.prob[pi];
+        const int m0 = mt * PAIR_M + crank * BM;
+        const int n0 = nt * BN + crank * (BN / 2);
         for (int sub = 0; sub <= q.paired; ++sub) {
           int k0, nk;
           k_range(q, kc * (1 + q.paired) + sub, k0, nk);
           for (int kb = 0; kb < nk; ++kb) {
-            ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
-            uint8_t* st = tiles + pipe.stage * STAGE_BYTES;
-            ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], STAGE_BYTES);
+            uint32_t bar;
+            uint8_t* st = producer_acquire(ctl, tiles, pipe, leader, bar);
             const int k = k0 + kb * BK;
-            if (q.a_mn_major)
-              load_operand(&q.a_map, 1, st, &ctl->full[pipe.stage], mt * BM, k + q.a_k_off, BM, ptx::kEvictFirst);
+            if (q.a_blocked)
+              load_blocked(&q.a_map, q.a_mn_major, st, bar, m0, k, BM, ptx::kEvictFirst);
+            else if (q.a_mn_major)
+              load_operand(&q.a_map, 1, st, bar, m0, k + q.a_k_off, BM, ptx::kEvictFirst);
             else
-              load_operand(&q.a_map, 0, st, &ctl->full[pipe.stage], mt * BM + q.a_row_off, k, BM, ptx::kEvictFirst);
-            load_operand(&q.b_map, q.b_mn_major, st + A_STAGE_BYTES, &ctl->full[pipe.stage], nt * BN,
-                         k + q.b_k_off, BN, ptx::kEvictLast);
+              load_operand(&q.a_map, 0, st, bar, m0 + q.a_row_off, k, BM, ptx::kEvictFirst);
+            load_operand(&q.b_map, q.b_mn_major, st + A_STAGE_BYTES, bar, n0, k + q.b_k_off, BN / 2,
+                         ptx::kEvictLast);
             pipe.advance();
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader CTA)
       Pipe pipe;
       uint32_t it = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      for (int u = pair; u < num_units; u += npairs) {
         int pi, mt, nt, kc;
         decode(u, pi, mt, nt, kc);
         const GemmProblem& q = p.prob[pi];
-        const uint32_t idesc = ptx::instr_desc_f16(BM, BN, 0, 0, q.a_mn_major, q.b_mn_major);  // f16 x f16
+        const uint32_t idesc = ptx::instr_desc_f16(PAIR_M, BN, 0, 0, q.a_mn_major, q.b_mn_major);  // f16 x f16
         for (int sub = 0; sub <= q.paired; ++sub, ++it) {
           int k0, nk;
           k_range(q, kc * (1 + q.paired) + sub, k0, nk);
@@ -515,7 +604,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
           ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
           ptx::tc_fence_after();
           mma_tile(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, q.a_mn_major, q.b_mn_major);
-          ptx::umma_commit(&ctl->tfull[buf]);
+          ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
         }
       }
     }
@@ -525,7 +614,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
     const int chalf = ew >> 2;
     uint8_t* tile = staging + ew * STAGING_TILE;
     uint32_t it = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+    for (int u = pair; u < num_units; u += npairs) {
       int pi, mt, nt, kc;
       decode(u, pi, mt, nt, kc);
       const GemmProblem& q = p.prob[pi];
@@ -533,7 +622,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
       ptx::mbar_wait(&ctl->tfull[buf0], (it >> 1) & 1);
       if (q.paired) ptx::mbar_wait(&ctl->tfull[buf1], ((it + 1) >> 1) & 1);
       ptx::tc_fence_after();
-      const int row0 = mt * BM + quad * 32;  // first row of this warp's 32-row slab
+      const int row0 = mt * PAIR_M + crank * BM + quad * 32;  // first row of this warp's 32-row slab
       const int row = row0 + lane;
       const uint32_t lane_base = ctl->tmem_base + (uint32_t(quad * 32) << 16) + chalf * (BN / 2);
       const uint32_t ta0 = lane_base + buf0 * BN, ta1 = lane_base + buf1 * BN;
@@ -579,12 +668,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_kernel(const __grid_const
           }
         }
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        ptx::mbar_arrive(&ctl->tempty[buf0]);
-        if (q.paired) ptx::mbar_arrive(&ctl->tempty[buf1]);
-      }
+      release_accumulator(ctl, buf0, lane);
+      if (q.paired) release_accumulator(ctl, buf1, lane);
       it += 1 + q.paired;
     }
     if (lane == 0) ptx::bulk_wait_all();
@@ -762,6 +847,7 @@ __global__ void combine_kernel(const float4* intra, const float4* recv, const fl
                                int rank, int b, int Dp, int D, float s, int flip, float* d_image, float* d_text,
                                int64_t ld_out, Status* status) {
   const int v4 = Dp / 4;
+  const bool vec_out = (ld_out % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_image) | reinterpret_cast<uintptr_t>(d_text)) % 16 == 0);
   const int64_t per_g = int64_t(b) * v4;
   const int64_t total = 2 * per_g;
   bool bad = false;
@@ -780,14 +866,15 @@ __global__ void combine_kernel(const float4* intra, const float4* recv, const fl
       });
     }
     const float4 t = f4add(intra[i], cross);
-    float o[4] = {t.x * s, t.y * s, t.z * s, t.w * s};
+    const float4 o = make_float4(t.x * s, t.y * s, t.z * s, t.w * s);
     float* out = (g == 0 ? d_image : d_text) + int64_t(r) * ld_out;
-    for (int k = 0; k < 4; ++k) {
-      const int c = vc * 4 + k;
-      if (c < D) {
-        out[c] = o[k];
-        bad |= !isfinite(o[k]);
-      }
+    const int c = vc * 4;
+    bad |= !(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w));
+    if (c + 4 <= D && vec_out) {
+      __stcs(reinterpret_cast<float4*>(out + c), o);  // streaming store: outputs are not re-read here
+    } else {
+      const float ov[4] = {o.x, o.y, o.z, o.w};
+      for (int k = 0; k < 4 && c + k < D; ++k) out[c + k] = ov[k];
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&status->flags, FLAG_GRAD_NONFINITE);
@@ -904,6 +991,7 @@ struct Geometry {
   int N, rank;
   int nchunk, cpr;        // canonical chunks, chunks per rank
   int np;                 // cross partials per rank after pairing chunks in the GEMM epilogue
+  int g_blocked;          // G in 128 x 128 blocks (canonical chunking: b and B multiples of 128)
   int chunk_cols;         // B / nchunk
   int64_t off[DISCO_R_COUNT];
   int64_t len[DISCO_R_COUNT];
@@ -936,6 +1024,7 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   }
   g->chunk_cols = int(B / g->nchunk);
   g->np = g->cpr >= 2 ? g->cpr / 2 : 1;
+  g->g_blocked = (g->nchunk == 8 && g->b % 128 == 0) ? 1 : 0;
   const int64_t b = g->b, Dp = g->Dp, N = world;
   int64_t len[DISCO_R_COUNT];
   len[DISCO_R_PACK] = 2 * b * Dp * 2;
@@ -1049,6 +1138,21 @@ int set_output(GemmProblem& q, float* out, int64_t ld_out, int64_t row_div, int6
   return DISCO_OK;
 }
 
+// 4-D f16 map over a blocked G: [rows/128][cols/128][128][128], box {64, box_rows, 1, 1}.
+int make_map_blocked(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(DISCO_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {128, 128, cols / 128, rows / 128};
+  cuuint64_t strides[3] = {256, 32768, (cols / 128) * 32768};
+  cuuint32_t box[4] = {64, box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DISCO_CUDA_ERROR, "cuTensorMapEncodeTiled(blocked G) failed (%d)", int(r));
+  return DISCO_OK;
+}
+
 int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -1067,7 +1171,8 @@ int prepare_kernel(K kernel) {
   return DISCO_OK;
 }
 
-int grid_for(int64_t units) { return int(std::min<int64_t>(units, sm_count())); }
+// Persistent grid of CTA pairs: one pair per unit, at most one CTA per SM.
+int grid_for(int64_t units) { return 2 * int(std::min<int64_t>(units, sm_count() / 2)); }
 
 int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t st) {
   LogitsParams p;
@@ -1078,11 +1183,8 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   int rc;
   if ((rc = make_map(&p.a_map[0], true, I_g, g.Dp, g.B, g.Dp, 64, BM))) return rc;
   if ((rc = make_map(&p.a_map[1], true, T_g, g.Dp, g.B, g.Dp, 64, BM))) return rc;
-  if ((rc = make_map(&p.b_map[0], true, T_g, g.Dp, g.B, g.Dp, 64, BN))) return rc;
-  if ((rc = make_map(&p.b_map[1], true, I_g, g.Dp, g.B, g.Dp, 64, BN))) return rc;
-  const __half* Gbase = region<__half>(ws, g, DISCO_R_G);
-  for (int d = 0; d < 2; ++d)
-    if ((rc = make_map(&p.g_map[d], false, Gbase + int64_t(d) * g.b * g.ldG, g.B, g.b, g.ldG, 64, 32))) return rc;
+  if ((rc = make_map(&p.b_map[0], true, T_g, g.Dp, g.B, g.Dp, 64, BN / 2))) return rc;
+  if ((rc = make_map(&p.b_map[1], true, I_g, g.Dp, g.B, g.Dp, 64, BN / 2))) return rc;
   p.B = int(g.B);
   p.b = int(g.b);
   p.Dp = int(g.Dp);
@@ -1090,7 +1192,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.nchunk = g.nchunk;
   p.chunk_cols = g.chunk_cols;
   p.tiles_per_chunk = (g.chunk_cols + BN - 1) / BN;
-  p.row_tiles = int((g.b + BM - 1) / BM);
+  p.row_tiles = int((g.b + PAIR_M - 1) / PAIR_M);
   p.tl2e = t * LOG2E;
   float* rows = region<float>(ws, g, DISCO_R_ROWS);
   p.stats = region<float2>(ws, g, DISCO_R_STATS);
@@ -1099,6 +1201,12 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.glabel = rows + 4 * g.b;
   p.G = region<__half>(ws, g, DISCO_R_G);
   p.ldG = g.ldG;
+  p.g_blocked = g.g_blocked;
+  static const int debug_flags = [] {
+    const char* e = getenv("DISCO_DEBUG_FLAGS");
+    return e ? atoi(e) : 0;
+  }();
+  p.debug_flags = debug_flags;
   const int64_t units =
       int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_FWD ? 1 : p.tiles_per_chunk);
   if (kind == KIND_FWD) {
@@ -1107,7 +1215,32 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
     count_launch();
   } else {
     if ((rc = prepare_kernel(logits_kernel<KIND_GRAD>))) return rc;
-    logits_kernel<KIND_GRAD><<<grid_for(units), NUM_THREADS, SMEM_BYTES, st>>>(p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid_for(units));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = 0;
+    if (debug_flags & 2) {  // experiment: persist the bf16 feature operands in L2 during the G write stream
+      static int maxp = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(v));
+        return v;
+      }();
+      const size_t bytes = size_t(2) * g.B * g.Dp * 2;
+      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      attr[0].val.accessPolicyWindow.base_ptr = const_cast<__nv_bfloat16*>(feat);
+      attr[0].val.accessPolicyWindow.num_bytes = bytes;
+      attr[0].val.accessPolicyWindow.hitRatio = std::min(1.0f, float(maxp) / float(bytes));
+      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cfg.numAttrs = 1;
+    }
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, logits_kernel<KIND_GRAD>, p));
     count_launch();
   }
   CUDA_TRY(cudaGetLastError());
@@ -1255,13 +1388,18 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
     const int dsrc = gi == 0 ? 1 : 0;
     const __half* Gd = G + int64_t(dsrc) * g.b * g.ldG;
     const __half* Ad = gi == 0 ? T16 : I16;  // image grad uses T_n, text grad uses I_n
-    if ((rc = make_map(&q.a_map, false, Gd, g.B, g.b, g.ldG, 64, 64))) return rc;   // MN-major G^T
+    if (g.g_blocked) {
+      if ((rc = make_map_blocked(&q.a_map, G + int64_t(dsrc) * g.b * g.B, g.b, g.B, 64))) return rc;
+      q.a_blocked = 1;
+    } else if ((rc = make_map(&q.a_map, false, Gd, g.B, g.b, g.ldG, 64, 64))) {  // MN-major G^T
+      return rc;
+    }
     if ((rc = make_map(&q.b_map, false, Ad, g.Dp, g.B, g.Dp, 64, 64))) return rc;  // MN-major features
     q.a_mn_major = 1;
     q.b_mn_major = 1;
     q.M = int(g.B);
     q.N = int(g.Dp);
-    q.m_tiles = int((g.B + BM - 1) / BM);
+    q.m_tiles = int((g.B + PAIR_M - 1) / PAIR_M);
     q.n_tiles = int((g.Dp + BN - 1) / BN);
     q.paired = g.cpr >= 2;
     q.k_chunks = g.np;  // units along K (pairs of canonical chunks when paired)
@@ -1306,13 +1444,18 @@ int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int ran
     GemmProblem& q = p.prob[gi];
     const __half* Gd = G + int64_t(gi) * g.b * g.ldG;
     const __half* Cd = gi == 0 ? T16 : I16;
-    if ((rc = make_map(&q.a_map, false, Gd, g.B, g.b, g.ldG, 64, BM))) return rc;  // K-major G
+    if (g.g_blocked) {
+      if ((rc = make_map_blocked(&q.a_map, G + int64_t(gi) * g.b * g.B, g.b, g.B, BM))) return rc;
+      q.a_blocked = 1;
+    } else if ((rc = make_map(&q.a_map, false, Gd, g.B, g.b, g.ldG, 64, BM))) {  // K-major G
+      return rc;
+    }
     if ((rc = make_map(&q.b_map, false, Cd, g.Dp, g.B, g.Dp, 64, 64))) return rc;  // MN-major features
     q.a_mn_major = 0;
     q.b_mn_major = 1;
     q.M = int(g.b);
     q.N = int(g.Dp);
-    q.m_tiles = int((g.b + BM - 1) / BM);
+    q.m_tiles = int((g.b + PAIR_M - 1) / PAIR_M);
     q.n_tiles = int((g.Dp + BN - 1) / BN);
     q.k_chunks = 1;
     q.k_chunk_len = int(g.B);
