@@ -168,7 +168,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.05)
+            self._stop.wait(0.01)
 
     def __enter__(self):
         if self.ok:
@@ -285,48 +285,35 @@ def run_ours(args):
         ms = float(tt.item())
     value = B / (ms / 1e3)
 
-    # ---- kernel breakdown: events around each C-ABI phase -----------------
-    phases = {}
-    names = ["pack", "all_gather", "forward", "backward_cross", "all_to_all", "backward_intra",
-             "combine", "loss"]
+    # ---- kernel breakdown: events around each C-ABI call (one tensor-core kernel each)
+    names = ["pack", "all_gather", "forward", "backward_grad", "backward_cross", "all_to_all",
+             "backward_intra", "combine", "loss"]
     ev = {n: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for n in names}
     args_ = plan.args
     sp = st.cuda_stream
-    reps = 3
+    reps = 5
     acc = {n: 0.0 for n in names}
+    di = torch.empty((b, D), dtype=torch.float32, device=device)
+    dt_ = torch.empty((b, D), dtype=torch.float32, device=device)
+
+    def timed(name, fn):
+        ev[name][0].record(st)
+        fn()
+        ev[name][1].record(st)
+
     for _ in range(reps):
         flush.zero_()
         barrier()
-        ev["pack"][0].record(st)
-        _lib.call("disco_b200_pack", *args_, I.data_ptr(), T.data_ptr(), D, D, _lib.BF16, 1, sp)
-        ev["pack"][1].record(st)
-        ev["all_gather"][0].record(st)
-        if world > 1:
-            ep.all_gather_into(plan.gather, plan.pack)
-        ev["all_gather"][1].record(st)
-        ev["forward"][0].record(st)
-        _lib.call("disco_b200_forward", *args_, t, sp)
-        ev["forward"][1].record(st)
-        ev["backward_cross"][0].record(st)
-        _lib.call("disco_b200_backward_cross", *args_, t, sp)
-        ev["backward_cross"][1].record(st)
-        ev["all_to_all"][0].record(st)
-        if world > 1:
-            ep.all_to_all_into(plan.recv, plan.send)
-        ev["all_to_all"][1].record(st)
-        ev["backward_intra"][0].record(st)
-        _lib.call("disco_b200_backward_intra", *args_, sp)
-        ev["backward_intra"][1].record(st)
-        di = torch.empty((b, D), dtype=torch.float32, device=device)
-        dt_ = torch.empty((b, D), dtype=torch.float32, device=device)
-        ev["combine"][0].record(st)
-        _lib.call("disco_b200_combine", *args_, t, 0, di.data_ptr(), dt_.data_ptr(), D, sp)
-        ev["combine"][1].record(st)
-        ev["loss"][0].record(st)
-        if world > 1:
-            ep.all_gather_into(plan.ce_all, plan.ce)
-        _lib.call("disco_b200_loss", *args_, 0, sp)
-        ev["loss"][1].record(st)
+        timed("pack", lambda: _lib.call("disco_b200_pack", *args_, I.data_ptr(), T.data_ptr(), D, D, _lib.BF16, 1, sp))
+        timed("all_gather", lambda: world > 1 and ep.all_gather_into(plan.gather, plan.pack))
+        timed("forward", lambda: _lib.call("disco_b200_forward", *args_, t, sp))
+        timed("backward_grad", lambda: _lib.call("disco_b200_backward_grad", *args_, t, sp))
+        timed("backward_cross", lambda: _lib.call("disco_b200_backward_cross", *args_, sp))
+        timed("all_to_all", lambda: world > 1 and ep.all_to_all_into(plan.recv, plan.send))
+        timed("backward_intra", lambda: _lib.call("disco_b200_backward_intra", *args_, sp))
+        timed("combine", lambda: _lib.call("disco_b200_combine", *args_, t, 0, di.data_ptr(), dt_.data_ptr(), D, sp))
+        timed("loss", lambda: (world > 1 and ep.all_gather_into(plan.ce_all, plan.ce),
+                               _lib.call("disco_b200_loss", *args_, 0, sp)))
         torch.cuda.synchronize()
         for n in names:
             acc[n] += ev[n][0].elapsed_time(ev[n][1]) / reps
@@ -351,6 +338,8 @@ def run_ours(args):
             s1.record(st)
             s1.synchronize()
             e_ms.append(s0.elapsed_time(s1))
+            out_bytes = int(di_h.numel() * 4 * 2 + 8)
+            del di_h, dt_h  # the caller consumes and drops the host gradients each step
         em = statistics.mean(e_ms)
         if world > 1:
             tt = torch.tensor([em], device=device, dtype=torch.float64)
@@ -358,7 +347,7 @@ def run_ours(args):
             em = float(tt.item())
         e2e = {"value": B / (em / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(I_h.numel() * I_h.element_size() * 2),
-               "d2h_bytes_per_step": int(di_h.numel() * 4 * 2 + 8),
+               "d2h_bytes_per_step": out_bytes,
                "ms_per_step": em}
 
     if rank != 0:
@@ -368,17 +357,25 @@ def run_ours(args):
 
     # ---- roofline ----------------------------------------------------------
     burst, sustained, hbm, src = load_peaks()
-    flops_launch = 4.0 * b * B * D  # every tensor-core launch: 2 directions x 2*b*B*D
-    kern = {
-        "logits_fwd": phases["forward"],
-        "logits_grad+gemm_cross": phases["backward_cross"],
-        "gemm_intra": phases["backward_intra"],
+    mm = 4.0 * b * B * D           # one launch = 2 directions x 2*b*B*D (12*b*B*D per step)
+    g_bytes = 2.0 * b * B * 2       # f16 G written by the grad launch (a6 output, both directions)
+    kernels = {
+        # name: (ms, bound, algorithmic work per launch, unit, peak)
+        "logits_fwd": (phases["forward"], "tensor", mm, "TFLOP/s", sustained),
+        "logits_grad": (phases["backward_grad"], "hbm", g_bytes, "GB/s", hbm),
+        "gemm_cross": (phases["backward_cross"], "tensor", mm, "TFLOP/s", sustained),
+        "gemm_intra": (phases["backward_intra"], "tensor", mm, "TFLOP/s", sustained),
     }
-    dom = max(kern, key=kern.get)
-    dom_ms = kern[dom]
-    achieved = flops_launch / (dom_ms / 1e3) / 1e12
+    table = {}
+    for k, (kms, bound, work, unit, peak) in kernels.items():
+        scale = 1e12 if unit == "TFLOP/s" else 1e9
+        ach = work / (kms / 1e3) / scale
+        table[k] = {"ms": kms, "bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak}
+    table["logits_grad"]["tensor_tflops_executed"] = mm / (phases["backward_grad"] / 1e3) / 1e12
+    dom = max(table, key=lambda k: table[k]["ms"])
     traffic = load_traffic().get(dom)
     step_tflops = 12.0 * b * B * D / (ms / 1e3) / 1e12
+    d = table[dom]
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -399,12 +396,11 @@ def run_ours(args):
         "loss": loss,
         "peak_loss_mem_gb": (peak_mem - mem_before) / 1e9,
         "peak_mem_gb": peak_mem / 1e9,
-        "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved,
-                     "peak": sustained, "unit": "TFLOP/s", "frac": achieved / sustained,
-                     "traffic": traffic, "peak_kind": f"{src} bf16 sustained",
-                     "frac_of_burst": achieved / burst,
-                     "step_tflops": step_tflops, "step_frac": step_tflops / sustained,
-                     "flops_per_launch": flops_launch, "launch_ms": dom_ms},
+        "roofline": {"bound": d["bound"], "kernel": dom, "achieved": d["achieved"], "peak": d["peak"],
+                     "unit": d["unit"], "frac": d["frac"], "traffic": traffic,
+                     "peak_kind": f"{src} ({'bf16 sustained' if d['unit'] == 'TFLOP/s' else 'HBM copy'})",
+                     "launch_ms": d["ms"], "step_tflops": step_tflops, "step_frac": step_tflops / sustained,
+                     "step_frac_of_burst": step_tflops / burst, "kernels": table},
         "phases_ms": phases,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -101,13 +101,16 @@ int disco_b200_pack(void* ws, int64_t B, int64_t D, int world, int rank, const v
  * fixed-order chunk combine -> per-row lse / ce / label gradient. */
 int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
 
-/* Backward part 1: recompute logits -> G = softmax - onehot in f16
- * (shard.py:143-146, matrix.py:131-144), then the cross-rank gradient GEMMs
- * G^T . local features (shard.py:149, 151) reduced over this rank's
- * canonical chunks into DISCO_R_SEND (destination-major slabs). */
-int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
+/* Backward part 1: recompute the logit tiles (bit-identical to the forward)
+ * -> G = softmax - onehot, unscaled, f16 (shard.py:143-146, matrix.py:131-144). */
+int disco_b200_backward_grad(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
 
-/* Backward part 2: intra-rank GEMMs G . gathered features (shard.py:150, 152)
+/* Backward part 2: cross-rank gradient GEMMs G^T . local features
+ * (shard.py:149, 151), canonical chunks pair-summed in the epilogue, reduced
+ * over this rank's chunks into DISCO_R_SEND (destination-major slabs). */
+int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
+
+/* Backward part 3: intra-rank GEMMs G . gathered features (shard.py:150, 152)
  * into DISCO_R_INTRA.  Independent of the slab exchange, so it overlaps it. */
 int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
 

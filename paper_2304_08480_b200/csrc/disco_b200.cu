@@ -1366,13 +1366,19 @@ int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, floa
   return DISCO_OK;
 }
 
-int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream) {
+int disco_b200_backward_grad(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream) {
   Geometry g;
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
+  return launch_logits(KIND_GRAD, ws, g, t, static_cast<cudaStream_t>(stream));
+}
+
+int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int rank, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if ((rc = launch_logits(KIND_GRAD, ws, g, t, st))) return rc;
 
   // cross GEMMs: X_g = G_{d'}^T . A_{d'} (local rows), g = image <- d' = t2i (1), g = text <- d' = i2t (0)
   const __half* G = region<__half>(ws, g, DISCO_R_G);

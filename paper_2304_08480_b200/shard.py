@@ -18,8 +18,9 @@ through the endpoint.  There is no CPU fallback.
 Dataflow of ``disco_step`` on rank n (b = B/N):
   pack (bf16)  -> all_gather [N][2][b][Dp]   (shard.py:190-191)
   forward      : fused logits GEMM + online LSE + CE (shard.py:134-141)
-  backward_cross: recompute -> f16 G (shard.py:143-146) -> G^T . local feats,
-                 per-canonical-chunk, destination-major slabs (shard.py:149, 151)
+  backward_grad : recompute logits -> f16 G = softmax - onehot (shard.py:143-146)
+  backward_cross: G^T . local feats per canonical chunk, destination-major slabs
+                 (shard.py:149, 151)
   all_to_all of the slabs (async, overlaps)  \\  replace all_reduce(AVG) +
   backward_intra: G . gathered feats          /   row slice (shard.py:199-208)
   combine      : s * (intra + fixed-tree sum of received slabs)
@@ -281,7 +282,8 @@ def local_loss_and_grads(layout: ShardLayout, I_gathered, T_gathered, t: float, 
         if N > 1:
             plan.gather[src * per_rank:(src + 1) * per_rank].copy_(plan.pack)
     _lib.call("disco_b200_forward", *plan.args, t, st)
-    _lib.call("disco_b200_backward_cross", *plan.args, t, st)
+    _lib.call("disco_b200_backward_grad", *plan.args, t, st)
+    _lib.call("disco_b200_backward_cross", *plan.args, st)
     _lib.call("disco_b200_backward_intra", *plan.args, st)
     d_image = torch.empty((B, D), dtype=torch.float32, device=device)
     d_text = torch.empty((B, D), dtype=torch.float32, device=device)
@@ -327,7 +329,8 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
     if N > 1:
         endpoint.all_gather_into(plan.gather, plan.pack)
     _lib.call("disco_b200_forward", *plan.args, t, st)
-    _lib.call("disco_b200_backward_cross", *plan.args, t, st)
+    _lib.call("disco_b200_backward_grad", *plan.args, t, st)
+    _lib.call("disco_b200_backward_cross", *plan.args, st)
     work = endpoint.all_to_all_into(plan.recv, plan.send, async_op=True) if N > 1 else None
     _lib.call("disco_b200_backward_intra", *plan.args, st)
     if work is not None:
