@@ -67,9 +67,10 @@ struct SmemCtl {
   uint64_t tempty[2];      // leader: both CTAs' epilogues drained the accumulator
   uint32_t tmem_base;
 };
-// Epilogue staging: 8 warps x (32 rows x 128 B), swizzled like TMA SWIZZLE_128B.
+// Epilogue staging: 8 warps x STAGING_BUFS x (32 rows x 128 B), swizzled like TMA SWIZZLE_128B.
 constexpr int STAGING_TILE = 32 * 128;
-constexpr int STAGING_BYTES = NUM_EPI_WARPS * STAGING_TILE;
+constexpr int STAGING_BUFS = 1;
+constexpr int STAGING_BYTES = NUM_EPI_WARPS * STAGING_BUFS * STAGING_TILE;
 constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + STAGING_BYTES + 256;
 static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory limit");
 
@@ -91,6 +92,7 @@ struct Status {
 struct LogitsParams {
   CUtensorMap a_map[2];  // dir 0: I_g, dir 1: T_g   box {64, 128}
   CUtensorMap b_map[2];  // dir 0: T_g, dir 1: I_g   box {64, 128} (each CTA loads its half of N)
+  CUtensorMap g_map[2];  // blocked-G store maps (4-D), box {64, 32, 1, 1}
   int B, b, Dp, rank;
   int nchunk, chunk_cols, tiles_per_chunk, row_tiles;  // row_tiles counts 256-row pair tiles
   float tl2e;  // t * log2(e)
@@ -354,8 +356,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int quad = warp & 3;
     const int chalf = ew >> 2;  // column half of the 256-wide tile
     const int r_in_tile = crank * BM + quad * 32 + lane;
-    uint8_t* tile = staging + ew * STAGING_TILE;
-    uint32_t it = 0;
+    uint8_t* tile = staging + ew * STAGING_BUFS * STAGING_TILE;
+    uint32_t it = 0, gslice = 0;
     for (int u = pair; u < num_units; u += npairs) {
       int dir, rt, ch, t0;
       decode(u, dir, rt, ch, t0);
@@ -456,41 +458,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 }
               }
             }
-            if (p.debug_flags & 1) {
-              if (h[0] == 0x7fffffffu) grow[0] = __float2half(0.f);  // keep the math live
-            } else if (p.debug_flags & 4) {  // staging only, no global store
-              ptx::st_swizzled_row(tile, lane, h);
-              __syncwarp();
-              const uint4 v = *reinterpret_cast<const uint4*>(tile + ((lane * 16) ^ 16));
-              if (v.x == 0x7fffffffu) grow[0] = __float2half(0.f);
-              __syncwarp();
-            } else if ((p.debug_flags & 8) && p.g_blocked) {  // direct register -> global, no staging
+            if (p.g_blocked) {
+              // asynchronous TMA bulk store of the 32 x 64 slice into its 128 x 128 block;
+              // the warp only waits when it reuses a staging buffer.
               const int rbase = rt * PAIR_M + crank * BM + quad * 32;
-              const int64_t nbc = p.B >> 7;
-              __half* blk = p.G + int64_t(dir) * p.b * p.B +
-                            ((int64_t(rbase >> 7) * nbc + (cb >> 7)) << 14) + (rbase & 127) * 128 + (cb & 127);
-              uint4* dst = reinterpret_cast<uint4*>(blk + lane * 128);
-#pragma unroll
-              for (int q = 0; q < 8; ++q) dst[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
-            } else if ((chunk_lo & 63) == 0 && (cb + 64 <= chunk_hi || (chunk_hi == p.B && (p.B & 63) == 0))) {
-              ptx::st_swizzled_row(tile, lane, h);
+              uint8_t* stile = staging + (ew * STAGING_BUFS + (gslice % STAGING_BUFS)) * STAGING_TILE;
+              if (lane == 0) ptx::bulk_wait_read<STAGING_BUFS - 1>();
               __syncwarp();
-              const int rbase = rt * PAIR_M + crank * BM + quad * 32;
-              if (p.g_blocked) {
-                // block (rbase/128, cb/128): 128 x 128 halves, row pitch 256 B -> this warp's
-                // two 64-column slices fill one contiguous 8 KiB run.
-                const int64_t nbc = p.B >> 7;
-                __half* blk = p.G + int64_t(dir) * p.b * p.B +
-                              ((int64_t(rbase >> 7) * nbc + (cb >> 7)) << 14) + (rbase & 127) * 128 + (cb & 127);
-                ptx::store_tile_rows(tile, lane, [&](int r) -> uint8_t* {
-                  return rbase + r < p.b ? reinterpret_cast<uint8_t*>(blk + r * 128) : nullptr;
-                }, ptx::kEvictFirst);
-              } else {
-                __half* gbase = p.G + int64_t(dir) * p.b * p.ldG + cb;
-                ptx::store_tile_rows(tile, lane, [&](int r) -> uint8_t* {
-                  return rbase + r < p.b ? reinterpret_cast<uint8_t*>(gbase + int64_t(rbase + r) * p.ldG) : nullptr;
-                }, ptx::kEvictFirst);
+              ptx::st_swizzled_row(stile, lane, h);
+              ptx::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                if (rbase < p.b) ptx::tma_store_4d(&p.g_map[dir], stile, cb & 127, rbase & 127, cb >> 7, rbase >> 7);
+                ptx::bulk_commit();
               }
+              ++gslice;
+            } else if ((chunk_lo & 63) == 0 && (cb + 64 <= chunk_hi || (chunk_hi == p.B && (p.B & 63) == 0))) {
+              // row-major G: transpose through swizzled smem, 4 full 128-byte rows per store
+              ptx::st_swizzled_row(tile, lane, h);
+              __syncwarp();
+              const int rbase = rt * PAIR_M + crank * BM + quad * 32;
+              __half* gbase = p.G + int64_t(dir) * p.b * p.ldG + cb;
+              ptx::store_tile_rows(tile, lane, [&](int r) -> uint8_t* {
+                return rbase + r < p.b ? reinterpret_cast<uint8_t*>(gbase + int64_t(rbase + r) * p.ldG) : nullptr;
+              }, ptx::kEvictFirst);
               __syncwarp();
             } else if (row_ok) {  // non-canonical chunk edges (b not a multiple of 64): scalar path
 #pragma unroll
@@ -509,6 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (has_t) p.target[dir * p.b + row] = yt;
       }
     }
+    if (KIND == KIND_GRAD && lane == 0) ptx::bulk_wait_all();  // drain any bulk stores
   }
   kernel_epilogue(ctl, warp);
 }
@@ -612,8 +604,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int ew = warp - 2;
     const int quad = warp & 3;
     const int chalf = ew >> 2;
-    uint8_t* tile = staging + ew * STAGING_TILE;
-    uint32_t it = 0;
+    uint8_t* tile = staging + ew * STAGING_BUFS * STAGING_TILE;
+    uint32_t it = 0, gslice = 0;
     for (int u = pair; u < num_units; u += npairs) {
       int pi, mt, nt, kc;
       decode(u, pi, mt, nt, kc);
@@ -649,15 +641,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           uint32_t w[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(v[i]);
-          if (lane == 0) ptx::bulk_wait_read<0>();
+          uint8_t* stile = tile + (gslice % STAGING_BUFS) * STAGING_TILE;
+          if (lane == 0) ptx::bulk_wait_read<STAGING_BUFS - 1>();
           __syncwarp();
-          ptx::st_swizzled_row(tile, lane, w);
+          ptx::st_swizzled_row(stile, lane, w);
           ptx::fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0 && row0 < q.M) {
-            ptx::tma_store_3d(&q.out_map, tile, c0, rlo, z);
+          if (lane == 0) {
+            if (row0 < q.M) ptx::tma_store_3d(&q.out_map, stile, c0, rlo, z);
             ptx::bulk_commit();
           }
+          ++gslice;
         } else if (orow) {
           if (c0 + 32 <= q.N) {
             float4* dst = reinterpret_cast<float4*>(orow + c0);
@@ -1202,6 +1196,11 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.G = region<__half>(ws, g, DISCO_R_G);
   p.ldG = g.ldG;
   p.g_blocked = g.g_blocked;
+  if (kind == KIND_GRAD && g.g_blocked) {
+    const __half* Gb = region<__half>(ws, g, DISCO_R_G);
+    for (int d = 0; d < 2; ++d)
+      if ((rc = make_map_blocked(&p.g_map[d], Gb + int64_t(d) * g.b * g.B, g.b, g.B, 32))) return rc;
+  }
   static const int debug_flags = [] {
     const char* e = getenv("DISCO_DEBUG_FLAGS");
     return e ? atoi(e) : 0;
