@@ -50,10 +50,17 @@ constexpr int BM = 128;      // rows per CTA (the pair covers 256)
 constexpr int BN = 256;      // accumulator columns (each CTA loads 128 of the B operand rows)
 constexpr int BK = 64;
 constexpr int PAIR_M = 2 * BM;
-constexpr int STAGES = 6;
 constexpr int A_STAGE_BYTES = BM * BK * 2;        // 16 KiB
-constexpr int B_STAGE_BYTES = (BN / 2) * BK * 2;  // 16 KiB (this CTA's half of N)
-constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int B_STAGE_BYTES = (BN / 2) * BK * 2;  // 16 KiB (this CTA's half of one 256-column N tile)
+constexpr int TILE_RING_BYTES = 192 * 1024;      // operand ring: 6 x 32 KiB (NB=1) or 4 x 48 KiB (NB=2)
+// NB = number of 256-column N tiles per unit (2 = "wide": all 512 columns of D, two accumulators)
+template <int NB> struct Ring {
+  static constexpr int STAGE_BYTES = A_STAGE_BYTES + NB * B_STAGE_BYTES;
+  static constexpr int STAGES = TILE_RING_BYTES / STAGE_BYTES;
+};
+constexpr int STAGES = Ring<1>::STAGES;  // max stage count (barrier arrays)
+constexpr int STAGE_BYTES = Ring<1>::STAGE_BYTES;
+static_assert(Ring<1>::STAGES == 6 && Ring<2>::STAGES == 4, "ring geometry");
 constexpr int NUM_THREADS = 320;  // warp0 TMA, warp1 MMA, warps2-9 epilogue
 constexpr int NUM_EPI_WARPS = 8;
 constexpr int TMEM_COLS = 512;    // 2 accumulators of 128 lanes x 256 fp32 columns
@@ -71,7 +78,7 @@ struct SmemCtl {
 constexpr int STAGING_TILE = 32 * 128;
 constexpr int STAGING_BUFS = 1;
 constexpr int STAGING_BYTES = NUM_EPI_WARPS * STAGING_BUFS * STAGING_TILE;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + STAGING_BYTES + 256;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(TILE_RING_BYTES) + STAGING_BYTES + 256;
 static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory limit");
 
 // -------------------------------------------------------- status flag bits
@@ -166,10 +173,11 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int mn_major, in
                   : ptx::smem_desc_sw128(base + kk * 32, 16, 1024);     // 16 K-elements = 32 B per MMA
 }
 
+template <int NSTAGES = STAGES>
 struct Pipe {
   uint32_t stage = 0, phase = 0;
   __device__ __forceinline__ void advance() {
-    if (++stage == STAGES) {
+    if (++stage == NSTAGES) {
       stage = 0;
       phase ^= 1;
     }
@@ -180,18 +188,23 @@ __device__ __forceinline__ uint8_t* smem_base(uint8_t* raw) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
 }
 
-// Leader-side MMA issue for one accumulator tile: nk k-blocks of BK, 4 UMMAs each.
-__device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe& pipe, int nk, uint32_t d_tmem,
-                                         uint32_t idesc, int a_mn, int b_mn) {
+// Leader-side MMA issue for one unit: nk k-blocks of BK, 4 UMMAs per N tile each.
+// NB = 2: the same A stage feeds two N tiles into accumulators d_tmem and d_tmem + BN.
+template <int NB>
+__device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<Ring<NB>::STAGES>& pipe, int nk,
+                                         uint32_t d_tmem, uint32_t idesc, int a_mn, int b_mn) {
   for (int kb = 0; kb < nk; ++kb) {
     ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
     ptx::tc_fence_after();
-    const uint32_t a_base = ptx::smem_u32(tiles + pipe.stage * STAGE_BYTES);
+    const uint32_t a_base = ptx::smem_u32(tiles + pipe.stage * Ring<NB>::STAGE_BYTES);
     const uint32_t b_base = a_base + A_STAGE_BYTES;
 #pragma unroll
     for (int kk = 0; kk < BK / 16; ++kk) {
-      ptx::umma_f16_pair(d_tmem, operand_desc(a_base, a_mn, kk), operand_desc(b_base, b_mn, kk), idesc,
-                         (kb | kk) != 0);
+      const uint64_t ad = operand_desc(a_base, a_mn, kk);
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        ptx::umma_f16_pair(d_tmem + j * BN, ad, operand_desc(b_base + j * B_STAGE_BYTES, b_mn, kk), idesc,
+                           (kb | kk) != 0);
     }
     ptx::umma_commit_pair(&ctl->empty[pipe.stage], 0x3);  // both CTAs' smem slots free
     pipe.advance();
@@ -199,17 +212,18 @@ __device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe& pip
 }
 
 // Producer side of one k-block: wait for the slot, arm the leader's barrier, load.
-__device__ __forceinline__ uint8_t* producer_acquire(SmemCtl* ctl, uint8_t* tiles, Pipe& pipe, bool leader,
-                                                     uint32_t& bar) {
+template <int NB>
+__device__ __forceinline__ uint8_t* producer_acquire(SmemCtl* ctl, uint8_t* tiles, Pipe<Ring<NB>::STAGES>& pipe,
+                                                     bool leader, uint32_t& bar) {
   ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
-  if (leader) ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], 2 * STAGE_BYTES);
+  if (leader) ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], 2 * Ring<NB>::STAGE_BYTES);
   bar = ptx::map_to_rank(&ctl->full[pipe.stage], 0);
-  return tiles + pipe.stage * STAGE_BYTES;
+  return tiles + pipe.stage * Ring<NB>::STAGE_BYTES;
 }
 
 __device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane) {
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {  // the NB=2 ring uses the first Ring<2>::STAGES
       ptx::mbar_init(&ctl->full[s], 1);
       ptx::mbar_init(&ctl->empty[s], 1);
     }
@@ -262,7 +276,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     logits_kernel(const __grid_constant__ LogitsParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
-  uint8_t* staging = tiles + STAGES * STAGE_BYTES;
+  uint8_t* staging = tiles + TILE_RING_BYTES;
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(staging + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int crank = int(ptx::cluster_ctarank());
@@ -328,7 +342,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           const int col0 = ch * p.chunk_cols + (t0 + ti) * BN + crank * (BN / 2);
           for (int kb = 0; kb < nk; ++kb) {
             uint32_t bar;
-            uint8_t* st = producer_acquire(ctl, tiles, pipe, leader, bar);
+            uint8_t* st = producer_acquire<1>(ctl, tiles, pipe, leader, bar);
             ptx::tma_load_2d_pair(st, &p.a_map[dir], bar, kb * BK, a_row, ptx::kEvictLast);
             ptx::tma_load_2d_pair(st + A_STAGE_BYTES, &p.b_map[dir], bar, kb * BK, col0, ptx::kEvictLast);
             pipe.advance();
@@ -346,7 +360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           const uint32_t buf = it & 1, use = it >> 1;
           ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
           ptx::tc_fence_after();
-          mma_tile(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, 0, 0);
+          mma_tile<1>(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, 0, 0);
           ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
         }
       }
@@ -512,11 +526,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 //   into the two TMEM buffers and summed in the epilogue ((c0 + c1): the first
 //   level of the fixed reduction tree).
 // =====================================================================
+template <int NB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ GemmParams p) {
+  constexpr int RS = Ring<NB>::STAGES;
+  static_assert(NB == 1 || NB == 2, "one or two N tiles per unit");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
-  uint8_t* staging = tiles + STAGES * STAGE_BYTES;
+  uint8_t* staging = tiles + TILE_RING_BYTES;
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(staging + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int crank = int(ptx::cluster_ctarank());
@@ -553,19 +570,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
-      Pipe pipe;
+      Pipe<RS> pipe;
       for (int u = pair; u < num_units; u += npairs) {
         int pi, mt, nt, kc;
         decode(u, pi, mt, nt, kc);
         const GemmProblem& q = p.prob[pi];
         const int m0 = mt * PAIR_M + crank * BM;
-        const int n0 = nt * BN + crank * (BN / 2);
+        const int n0 = nt * NB * BN + crank * (BN / 2);
         for (int sub = 0; sub <= q.paired; ++sub) {
           int k0, nk;
           k_range(q, kc * (1 + q.paired) + sub, k0, nk);
           for (int kb = 0; kb < nk; ++kb) {
             uint32_t bar;
-            uint8_t* st = producer_acquire(ctl, tiles, pipe, leader, bar);
+            uint8_t* st = producer_acquire<NB>(ctl, tiles, pipe, leader, bar);
             const int k = k0 + kb * BK;
             if (q.a_blocked)
               load_blocked(&q.a_map, q.a_mn_major, st, bar, m0, k, BM, ptx::kEvictFirst);
@@ -573,8 +590,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               load_operand(&q.a_map, 1, st, bar, m0, k + q.a_k_off, BM, ptx::kEvictFirst);
             else
               load_operand(&q.a_map, 0, st, bar, m0 + q.a_row_off, k, BM, ptx::kEvictFirst);
-            load_operand(&q.b_map, q.b_mn_major, st + A_STAGE_BYTES, bar, n0, k + q.b_k_off, BN / 2,
-                         ptx::kEvictLast);
+#pragma unroll
+            for (int j = 0; j < NB; ++j)
+              load_operand(&q.b_map, q.b_mn_major, st + A_STAGE_BYTES + j * B_STAGE_BYTES, bar, n0 + j * BN,
+                           k + q.b_k_off, BN / 2, ptx::kEvictLast);
             pipe.advance();
           }
         }
@@ -582,21 +601,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {  // ---------------- MMA issuer (leader CTA)
-      Pipe pipe;
+      Pipe<RS> pipe;
       uint32_t it = 0;
       for (int u = pair; u < num_units; u += npairs) {
         int pi, mt, nt, kc;
         decode(u, pi, mt, nt, kc);
         const GemmProblem& q = p.prob[pi];
         const uint32_t idesc = ptx::instr_desc_f16(PAIR_M, BN, 0, 0, q.a_mn_major, q.b_mn_major);  // f16 x f16
-        for (int sub = 0; sub <= q.paired; ++sub, ++it) {
+        if constexpr (NB == 2) {  // wide unit: both accumulators, one pass over K
           int k0, nk;
-          k_range(q, kc * (1 + q.paired) + sub, k0, nk);
-          const uint32_t buf = it & 1, use = it >> 1;
-          ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
+          k_range(q, kc, k0, nk);
+          ptx::mbar_wait(&ctl->tempty[0], ((it >> 1) & 1) ^ 1);
+          ptx::mbar_wait(&ctl->tempty[1], ((it >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
-          mma_tile(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, q.a_mn_major, q.b_mn_major);
-          ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
+          mma_tile<NB>(ctl, tiles, pipe, nk, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major);
+          ptx::umma_commit_pair(&ctl->tfull[0], 0x3);
+          ptx::umma_commit_pair(&ctl->tfull[1], 0x3);
+          it += 2;
+        }
+        if constexpr (NB == 1) {
+          for (int sub = 0; sub <= q.paired; ++sub, ++it) {
+            int k0, nk;
+            k_range(q, kc * (1 + q.paired) + sub, k0, nk);
+            const uint32_t buf = it & 1, use = it >> 1;
+            ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
+            ptx::tc_fence_after();
+            mma_tile<1>(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, q.a_mn_major, q.b_mn_major);
+            ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
+          }
         }
       }
     }
@@ -610,27 +642,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int pi, mt, nt, kc;
       decode(u, pi, mt, nt, kc);
       const GemmProblem& q = p.prob[pi];
+      const bool two = q.paired || NB == 2;  // unit occupies both accumulators
       const uint32_t buf0 = it & 1, buf1 = (it + 1) & 1;
       ptx::mbar_wait(&ctl->tfull[buf0], (it >> 1) & 1);
-      if (q.paired) ptx::mbar_wait(&ctl->tfull[buf1], ((it + 1) >> 1) & 1);
+      if (two) ptx::mbar_wait(&ctl->tfull[buf1], ((it + 1) >> 1) & 1);
       ptx::tc_fence_after();
       const int row0 = mt * PAIR_M + crank * BM + quad * 32;  // first row of this warp's 32-row slab
       const int row = row0 + lane;
       const uint32_t lane_base = ctl->tmem_base + (uint32_t(quad * 32) << 16) + chalf * (BN / 2);
       const uint32_t ta0 = lane_base + buf0 * BN, ta1 = lane_base + buf1 * BN;
-      const int cbase = nt * BN + chalf * (BN / 2);
+      const int cbase = nt * NB * BN + chalf * (BN / 2);
       float* orow = nullptr;
       if (!q.tma_store && row < q.M)
         orow = q.out + kc * q.chunk_stride + (row / q.row_div) * q.stride_hi + (row % q.row_div) * q.ld_out;
       const int z = int(row0 / q.row_div) + kc;
       const int rlo = int(row0 % q.row_div);
 #pragma unroll 1
-      for (int j = 0; j < BN / 64; ++j) {
-        const int c0 = cbase + j * 32;
-        if (c0 >= q.N) break;  // warp-uniform
+      for (int jj = 0; jj < NB * (BN / 64); ++jj) {
+        // NB = 2: slices 0..3 from accumulator 0 (columns [0,256)), 4..7 from accumulator 1
+        const int j = jj % (BN / 64), acc = jj / (BN / 64);
+        const int c0 = cbase + acc * BN + j * 32;
+        if (c0 >= q.N) continue;  // warp-uniform
         float v[32];
-        ptx::tmem_ld32(ta0 + j * 32, v);
-        if (q.paired) {
+        ptx::tmem_ld32((acc ? ta1 : ta0) + j * 32, v);
+        if (NB == 1 && q.paired) {
           float v1[32];
           ptx::tmem_ld32(ta1 + j * 32, v1);
 #pragma unroll
@@ -663,8 +698,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       }
       release_accumulator(ctl, buf0, lane);
-      if (q.paired) release_accumulator(ctl, buf1, lane);
-      it += 1 + q.paired;
+      if (two) release_accumulator(ctl, buf1, lane);
+      it += two ? 2 : 1;
     }
     if (lane == 0) ptx::bulk_wait_all();
   }
@@ -800,19 +835,32 @@ __device__ __forceinline__ float4 f4neg(float4 a) { return make_float4(-a.x, -a.
 
 // Fixed-order sum of n float4 terms: balanced binary tree over ascending index
 // when n is a power of two <= 8 (a subtree of the canonical 8-chunk tree),
-// ascending sequential otherwise.
+// ascending sequential otherwise.  Fixed-size cases are fully unrolled so the
+// terms stay in registers (all loads issued before the adds).
+template <int N, typename Get>
+__device__ __forceinline__ float4 tree_fixed(Get get) {
+  float4 acc[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) acc[k] = get(k);
+#pragma unroll
+  for (int w = 1; w < N; w <<= 1)
+#pragma unroll
+    for (int k = 0; k + w < N; k += 2 * w) acc[k] = f4add(acc[k], acc[k + w]);
+  return acc[0];
+}
 template <typename Get>
 __device__ __forceinline__ float4 tree_sum(int n, Get get) {
-  if ((n & (n - 1)) == 0 && n <= 8) {
-    float4 acc[8];
-    for (int k = 0; k < n; ++k) acc[k] = get(k);
-    for (int w = 1; w < n; w <<= 1)
-      for (int k = 0; k + w < n; k += 2 * w) acc[k] = f4add(acc[k], acc[k + w]);
-    return acc[0];
+  switch (n) {
+    case 1: return get(0);
+    case 2: return tree_fixed<2>(get);
+    case 4: return tree_fixed<4>(get);
+    case 8: return tree_fixed<8>(get);
+    default: {
+      float4 acc = get(0);
+      for (int k = 1; k < n; ++k) acc = f4add(acc, get(k));
+      return acc;
+    }
   }
-  float4 acc = get(0);
-  for (int k = 1; k < n; ++k) acc = f4add(acc, get(k));
-  return acc;
 }
 
 // Sender-side tree over this rank's np paired-chunk partials:
@@ -837,9 +885,9 @@ __global__ void presum_kernel(const float4* xpart, int np, int N, int b, int Dp,
 // Owner combine: d_g[r] = s * (intra_g[r] + cross_g[r]) written b x D (ld_out), where
 //   cross = tree over the N received slabs recv[src][g][r] (negated for src != rank if flip), or,
 //   single rank with canonical chunks (xpart != null), tree over the np local paired partials.
-__global__ void combine_kernel(const float4* intra, const float4* recv, const float4* xpart, int np, int N,
-                               int rank, int b, int Dp, int D, float s, int flip, float* d_image, float* d_text,
-                               int64_t ld_out, Status* status) {
+__global__ void combine_kernel(const float4* intra, int ksplit, const float4* recv, const float4* xpart, int np,
+                               int N, int rank, int b, int Dp, int D, float s, int flip, float* d_image,
+                               float* d_text, int64_t ld_out, Status* status) {
   const int v4 = Dp / 4;
   const bool vec_out = (ld_out % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_image) | reinterpret_cast<uintptr_t>(d_text)) % 16 == 0);
   const int64_t per_g = int64_t(b) * v4;
@@ -859,7 +907,9 @@ __global__ void combine_kernel(const float4* intra, const float4* recv, const fl
         return (flip && src != rank) ? f4neg(x) : x;
       });
     }
-    const float4 t = f4add(intra[i], cross);
+    const float4* ib = intra + (int64_t(g) * ksplit) * per_g + rem;  // intra K-split partials, fixed order
+    const float4 yi = ksplit == 2 ? f4add(ib[0], ib[per_g]) : ib[0];
+    const float4 t = f4add(yi, cross);
     const float4 o = make_float4(t.x * s, t.y * s, t.z * s, t.w * s);
     float* out = (g == 0 ? d_image : d_text) + int64_t(r) * ld_out;
     const int c = vc * 4;
@@ -878,9 +928,9 @@ __global__ void combine_kernel(const float4* intra, const float4* recv, const fl
 //   d_full_g[c] = s * (cross_g[c] + [c in own rows] intra_g[c - rank*b]), rows outside negated if flip.
 //   cross_g[c] comes from the destination-major send slabs, or (single rank, canonical chunks) the
 //   tree over the paired partials.
-__global__ void contribution_kernel(const float4* intra, const float4* send, const float4* xpart, int np, int N,
-                                    int rank, int b, int Dp, int D, float s, int flip, float* d_image,
-                                    float* d_text, int64_t ld_out, Status* status) {
+__global__ void contribution_kernel(const float4* intra, int ksplit, const float4* send, const float4* xpart,
+                                    int np, int N, int rank, int b, int Dp, int D, float s, int flip,
+                                    float* d_image, float* d_text, int64_t ld_out, Status* status) {
   const int v4 = Dp / 4;
   const int64_t B = int64_t(N) * b;
   const int64_t per_g = B * v4;
@@ -900,7 +950,11 @@ __global__ void contribution_kernel(const float4* intra, const float4* send, con
       x = send[((dest * 2 + g) * b + r) * v4 + vc];
     }
     const bool own = dest == rank;
-    if (own) x = f4add(intra[(int64_t(g) * b + r) * v4 + vc], x);
+    if (own) {
+      const int64_t per_b = int64_t(b) * v4;
+      const float4* ib = intra + (int64_t(g) * ksplit) * per_b + r * v4 + vc;
+      x = f4add(ksplit == 2 ? f4add(ib[0], ib[per_b]) : ib[0], x);
+    }
     float sg = (flip && !own) ? -s : s;
     float o[4] = {x.x * sg, x.y * sg, x.z * sg, x.w * sg};
     float* out = (g == 0 ? d_image : d_text) + c * ld_out;
@@ -986,6 +1040,8 @@ struct Geometry {
   int nchunk, cpr;        // canonical chunks, chunks per rank
   int np;                 // cross partials per rank after pairing chunks in the GEMM epilogue
   int g_blocked;          // G in 128 x 128 blocks (canonical chunking: b and B multiples of 128)
+  int wide;               // Dp % 512 == 0: GEMM units cover all of D (two accumulators, G read once)
+  int ksplit;             // intra K split (fixed function of B, D): partials [2][ksplit][b][Dp]
   int chunk_cols;         // B / nchunk
   int64_t off[DISCO_R_COUNT];
   int64_t len[DISCO_R_COUNT];
@@ -1017,8 +1073,12 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
     g->cpr = 1;
   }
   g->chunk_cols = int(B / g->nchunk);
-  g->np = g->cpr >= 2 ? g->cpr / 2 : 1;
   g->g_blocked = (g->nchunk == 8 && g->b % 128 == 0) ? 1 : 0;
+  g->wide = (g->Dp % 512 == 0) ? 1 : 0;
+  // cross partials per rank: wide units keep one partial per canonical chunk (the first tree
+  // level then runs in presum/combine); narrow units pair chunks in the two accumulators.
+  g->np = g->wide ? g->cpr : (g->cpr >= 2 ? g->cpr / 2 : 1);
+  g->ksplit = (g->wide && B % 128 == 0 && B >= 4096) ? 2 : 1;
   const int64_t b = g->b, Dp = g->Dp, N = world;
   int64_t len[DISCO_R_COUNT];
   len[DISCO_R_PACK] = 2 * b * Dp * 2;
@@ -1033,7 +1093,7 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   len[DISCO_R_XPART] = g->np > 1 ? 2 * int64_t(g->np) * B * Dp * 4 : 0;
   len[DISCO_R_SEND] = N * 2 * b * Dp * 4;
   len[DISCO_R_RECV] = N > 1 ? N * 2 * b * Dp * 4 : 0;
-  len[DISCO_R_INTRA] = 2 * b * Dp * 4;
+  len[DISCO_R_INTRA] = 2 * int64_t(g->ksplit) * b * Dp * 4;
   len[DISCO_R_STATUS] = int64_t(sizeof(Status));
   int64_t off = 0;
   for (int r = 0; r < DISCO_R_COUNT; ++r) {
@@ -1246,13 +1306,19 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   return DISCO_OK;
 }
 
-int launch_gemm(GemmParams& p, cudaStream_t st) {
+// wide = 1: every unit covers all N columns (n_tiles counts 512-column tiles), NB = 2 kernel.
+int launch_gemm(GemmParams& p, cudaStream_t st, int wide) {
   p.units[0] = 0;
   for (int i = 0; i < p.nprob; ++i)
     p.units[i + 1] = p.units[i] + p.prob[i].m_tiles * p.prob[i].n_tiles * p.prob[i].k_chunks;
   int rc;
-  if ((rc = prepare_kernel(gemm_kernel))) return rc;
-  gemm_kernel<<<grid_for(p.units[p.nprob]), NUM_THREADS, SMEM_BYTES, st>>>(p);
+  if (wide) {
+    if ((rc = prepare_kernel(gemm_kernel<2>))) return rc;
+    gemm_kernel<2><<<grid_for(p.units[p.nprob]), NUM_THREADS, SMEM_BYTES, st>>>(p);
+  } else {
+    if ((rc = prepare_kernel(gemm_kernel<1>))) return rc;
+    gemm_kernel<1><<<grid_for(p.units[p.nprob]), NUM_THREADS, SMEM_BYTES, st>>>(p);
+  }
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
@@ -1388,6 +1454,7 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
   memset(&p, 0, sizeof(p));
   p.nprob = 2;
   const int64_t Bc = g.B / g.nchunk;  // canonical chunk rows
+  const int cross_wide = g.wide;  // wide units read G once; otherwise chunks are paired
   for (int gi = 0; gi < 2; ++gi) {
     GemmProblem& q = p.prob[gi];
     const int dsrc = gi == 0 ? 1 : 0;
@@ -1405,8 +1472,8 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
     q.M = int(g.B);
     q.N = int(g.Dp);
     q.m_tiles = int((g.B + PAIR_M - 1) / PAIR_M);
-    q.n_tiles = int((g.Dp + BN - 1) / BN);
-    q.paired = g.cpr >= 2;
+    q.n_tiles = cross_wide ? int(g.Dp / (2 * BN)) : int((g.Dp + BN - 1) / BN);
+    q.paired = !cross_wide && g.cpr >= 2;
     q.k_chunks = g.np;  // units along K (pairs of canonical chunks when paired)
     q.k_chunk_len = int(g.cpr > 1 ? Bc : g.b);
     q.k_total = int(g.b);
@@ -1422,7 +1489,7 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
     }
     if (rc) return rc;
   }
-  if ((rc = launch_gemm(p, st))) return rc;
+  if ((rc = launch_gemm(p, st, cross_wide))) return rc;
   if (g.np > 1 && world > 1) {  // single rank: the owner combine reads the partials directly
     const int64_t n = 2 * g.B * (g.Dp / 4);
     presum_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_XPART), g.np, world,
@@ -1461,14 +1528,15 @@ int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int ran
     q.M = int(g.b);
     q.N = int(g.Dp);
     q.m_tiles = int((g.b + PAIR_M - 1) / PAIR_M);
-    q.n_tiles = int((g.Dp + BN - 1) / BN);
-    q.k_chunks = 1;
-    q.k_chunk_len = int(g.B);
+    q.n_tiles = g.wide ? int(g.Dp / (2 * BN)) : int((g.Dp + BN - 1) / BN);
+    q.k_chunks = g.ksplit;  // fixed K halves [0, B/2), [B/2, B): independent of N
+    q.k_chunk_len = int(g.B / g.ksplit);
     q.k_total = int(g.B);
-    if ((rc = set_output(q, region<float>(ws, g, DISCO_R_INTRA) + int64_t(gi) * g.b * g.Dp, g.Dp, g.b, 0, 1, 0, 1)))
+    if ((rc = set_output(q, region<float>(ws, g, DISCO_R_INTRA) + int64_t(gi) * g.ksplit * g.b * g.Dp, g.Dp, g.b, 0,
+                         1, g.b * g.Dp, g.ksplit)))
       return rc;
   }
-  return launch_gemm(p, st);
+  return launch_gemm(p, st, g.wide);
 }
 
 int disco_b200_combine(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip, float* d_image,
@@ -1481,7 +1549,7 @@ int disco_b200_combine(void* ws, int64_t B, int64_t D, int world, int rank, floa
   const float s = float(0.5 * double(t) / double(B));
   const int64_t n = 2 * g.b * (g.Dp / 4);
   combine_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
-      region<float4>(ws, g, DISCO_R_INTRA), region<float4>(ws, g, DISCO_R_RECV),
+      region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float4>(ws, g, DISCO_R_RECV),
       (world == 1 && g.np > 1) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, world, rank, int(g.b),
       int(g.Dp), int(D), s, flip, d_image, d_text, ld_out, region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
@@ -1499,7 +1567,7 @@ int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank,
   const float s = float(0.5 * double(t) / double(g.b));
   const int64_t n = 2 * g.B * (g.Dp / 4);
   contribution_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
-      region<float4>(ws, g, DISCO_R_INTRA), region<float4>(ws, g, DISCO_R_SEND),
+      region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float4>(ws, g, DISCO_R_SEND),
       (world == 1 && g.np > 1) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, world, rank, int(g.b),
       int(g.Dp), int(D), s, flip && world > 1, d_image_full, d_text_full, ld_out, region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
