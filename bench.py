@@ -40,6 +40,8 @@ sys.path.insert(0, ROOT)
 B_GLOBAL = 32768
 DIM = 512
 TEMP = 100.0
+# BASELINE.json configs (B, D): 1 = headline; 2-4 are extra measurement points
+CONFIGS = {"A": (1024, 512), "B": (32768, 512), "C": (65536, 768), "D": (196608, 512), "E": (16384, 1024)}
 METRIC = "contrastive-loss fwd+bwd samples/sec at B=32K,D=512; peak loss mem/GPU"
 UNIT = "samples/s"
 CPU_SAMPLE_ROWS = 2048
@@ -51,8 +53,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=B_GLOBAL)
-    ap.add_argument("--dim", type=int, default=DIM)
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--dim", type=int, default=None)
+    ap.add_argument("--config", default="B", choices=sorted(CONFIGS),
+                    help="BASELINE.json config letter (SURVEY 8.0); --batch/--dim override")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -123,7 +127,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * B / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": f"B={B},D={D},t={TEMP} (BASELINE configs[1])",
+        "data": "synthetic", "config": {"workload": f"B={B},D={D},t={TEMP} (BASELINE config {args.config})",
                                          "global_batch": B, "dim": D, "parallelism": f"dp{args.gpus}"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
                          "sample": sample},
@@ -390,7 +394,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"B={B},D={D},t={TEMP} (BASELINE configs[1])", "global_batch": B,
+        "config": {"workload": f"B={B},D={D},t={TEMP} (BASELINE config {args.config})", "global_batch": B,
                    "local_batch": b, "dim": D, "parallelism": f"dp{world}",
                    "l2": "flushed between steps (512 MB write, outside timed events)"},
         "loss": loss,
@@ -415,6 +419,9 @@ def run_ours(args):
 
 def main():
     args = parse()
+    cb, cd = CONFIGS[args.config]
+    args.batch = args.batch or cb
+    args.dim = args.dim or cd
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

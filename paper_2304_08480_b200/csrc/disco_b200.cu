@@ -725,9 +725,10 @@ __device__ __forceinline__ float load_as_float<__half>(const void* p, int64_t i)
 // Round local features to bf16, pad D..Dp with zeros: out [2][b][Dp].
 // One thread per 8 output elements (one 16-byte store); f64 inputs are rounded
 // directly f64 -> bf16 (a single rounding).
+// out16 (optional): also write the f16 copy (single rank: packed == gathered layout).
 template <typename T>
 __global__ void pack_kernel(const void* I, const void* Tm, int64_t ldI, int64_t ldT, int b, int D, int Dp,
-                            __nv_bfloat16* out, Status* status) {
+                            __nv_bfloat16* out, __half* out16, Status* status) {
   const int v8 = Dp / 8;
   const int64_t total = int64_t(2) * b * v8;
   bool bad = false;
@@ -756,6 +757,12 @@ __global__ void pack_kernel(const void* I, const void* Tm, int64_t ldI, int64_t 
       o[k] = x;
     }
     reinterpret_cast<uint4*>(out)[i] = *reinterpret_cast<const uint4*>(o);
+    if (out16) {
+      __align__(16) __half h[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) h[k] = __float2half_rn(__bfloat162float(o[k]));
+      reinterpret_cast<uint4*>(out16)[i] = *reinterpret_cast<const uint4*>(h);
+    }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&status->flags, FLAG_INPUT_NONFINITE);
 }
@@ -1101,8 +1108,9 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
     g->len[r] = len[r];
     off += round_up(len[r], 1024);
   }
-  // aliases for the single-rank case
+  // aliases for the single-rank case: packed == gathered == forward operand layout
   if (N == 1) {
+    g->off[DISCO_R_PACK] = g->off[DISCO_R_FEAT];
     g->off[DISCO_R_GATHER] = g->off[DISCO_R_PACK];
     g->len[DISCO_R_GATHER] = g->len[DISCO_R_PACK];
     g->off[DISCO_R_RECV] = g->off[DISCO_R_SEND];
@@ -1383,21 +1391,22 @@ int disco_b200_pack(void* ws, int64_t B, int64_t D, int world, int rank, const v
     count_launch();
   }
   __nv_bfloat16* out = region<__nv_bfloat16>(ws, g, DISCO_R_PACK);
+  __half* out16 = world == 1 ? region<__half>(ws, g, DISCO_R_FEAT16) : nullptr;  // PACK aliases FEAT
   const int64_t n = 2 * g.b * (g.Dp / 8);
   const int grid = elementwise_grid(n, 256);
   switch (dtype) {
     case DISCO_F32:
-      pack_kernel<float><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, status);
+      pack_kernel<float><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, out16, status);
       break;
     case DISCO_BF16:
       pack_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out,
-                                                       status);
+                                                       out16, status);
       break;
     case DISCO_F16:
-      pack_kernel<__half><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, status);
+      pack_kernel<__half><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, out16, status);
       break;
     case DISCO_F64:
-      pack_kernel<double><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, status);
+      pack_kernel<double><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, out16, status);
       break;
     default:
       return fail(DISCO_SHAPE_ERROR, "unsupported dtype code %d", dtype);
@@ -1413,12 +1422,14 @@ int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, floa
   if (rc) return rc;
   if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t nvec = int64_t(world) * 2 * g.b * (g.Dp / 8);
-  unpack_kernel<<<elementwise_grid(nvec, 256), 256, 0, st>>>(
-      region<uint4>(ws, g, DISCO_R_GATHER), world, int(g.b), int(g.Dp), region<uint4>(ws, g, DISCO_R_FEAT),
-      region<uint4>(ws, g, DISCO_R_FEAT16));
-  count_launch();
-  CUDA_TRY(cudaGetLastError());
+  if (world > 1) {  // single rank: pack already wrote FEAT / FEAT16
+    const int64_t nvec = int64_t(world) * 2 * g.b * (g.Dp / 8);
+    unpack_kernel<<<elementwise_grid(nvec, 256), 256, 0, st>>>(
+        region<uint4>(ws, g, DISCO_R_GATHER), world, int(g.b), int(g.Dp), region<uint4>(ws, g, DISCO_R_FEAT),
+        region<uint4>(ws, g, DISCO_R_FEAT16));
+    count_launch();
+    CUDA_TRY(cudaGetLastError());
+  }
   if ((rc = launch_logits(KIND_FWD, ws, g, t, st))) return rc;
   float* rows = region<float>(ws, g, DISCO_R_ROWS);
   const int n = int(2 * g.b);

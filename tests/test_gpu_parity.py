@@ -163,3 +163,41 @@ def test_full_size_b32k_sampled_rows():
     assert O.max_rel_error(di[rows].cpu().numpy(), ri) < TOL
     assert O.max_rel_error(dt[rows].cpu().numpy(), rt) < TOL
     assert abs(loss - rl[0]) / rl[0] < TOL
+
+
+@pytest.fixture
+def release_plans():
+    yield
+    from paper_2304_08480_b200.shard import clear_plans
+    clear_plans()
+    torch.cuda.empty_cache()
+
+
+def test_config_c_bitwise_and_sampled_oracle(release_plans):
+    """BASELINE config C (B=65536, D=768): N=8 simulated ranks == N=1 bitwise, sampled f64 oracle."""
+    B, D, t = 65536, 768, 100.0
+    I, T = O.synthetic_features(B, D, 5)
+    d8 = run_sim(I, T, 8, t)
+    from paper_2304_08480_b200.shard import clear_plans
+    clear_plans()
+    torch.cuda.empty_cache()
+    di, dt, loss = P.disco_step(None, dev(I), dev(T), t)
+    di, dt = di.cpu().numpy(), dt.cpu().numpy()
+    assert di.tobytes() == d8[0].tobytes() and dt.tobytes() == d8[1].tobytes() and loss == d8[2][0]
+    rows = np.linspace(0, B - 1, 32).astype(np.int64)
+    ri, rt, rl = O.clip_grad_rows(I, T, t, rows)
+    assert O.max_rel_error(di[rows], ri) < TOL
+    assert O.max_rel_error(dt[rows], rt) < TOL
+    assert abs(loss - rl[0]) / rl[0] < TOL
+
+
+def test_large_index_space(release_plans):
+    """b*B = 4.3e9 G elements per direction (> 2^31): 64-bit offsets, narrow (D=64) GEMM path."""
+    B, D, t = 65536, 64, 14.2857
+    I, T = O.synthetic_features(B, D, 6)
+    di, dt, loss = P.disco_step(None, dev(I), dev(T), t)
+    rows = np.array([0, 1, 4095, 32768, 54321, B - 1])
+    ri, rt, rl = O.clip_grad_rows(I, T, t, rows, stats=O.clip_stats_blocked(I, T, t, block=4096))
+    assert O.max_rel_error(di[rows].cpu().numpy(), ri) < TOL
+    assert O.max_rel_error(dt[rows].cpu().numpy(), rt) < TOL
+    assert abs(loss - rl[0]) / rl[0] < TOL
