@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define DISCO_B200_ABI_VERSION 1
+#define DISCO_B200_ABI_VERSION 2
 
 enum disco_status {
   DISCO_OK = 0,
@@ -65,7 +65,9 @@ enum disco_region {
   DISCO_R_RECV = 11,   /* f32  [N][2][b][Dp]      cross slabs by source (all_to_all out)     */
   DISCO_R_INTRA = 12,  /* f32  [2][b][Dp]         intra-rank gradient terms                  */
   DISCO_R_STATUS = 13, /* f64 loss, i32 flags      host-visible step status                   */
-  DISCO_R_COUNT = 14
+  DISCO_R_SCALE = 14,  /* f32  [2][B/128][b]      E -> G factor exp2(m_g - lse2) per row and
+                          128-column group (canonical shapes; empty otherwise)                */
+  DISCO_R_COUNT = 15
 };
 
 int disco_b200_abi_version(void);
@@ -98,11 +100,17 @@ int disco_b200_pack(void* ws, int64_t B, int64_t D, int world, int rank, const v
 
 /* Forward: unpack the gathered features, fused logits GEMM + online
  * log-sum-exp + target extraction (shard.py:134-141, matrix.py:103-118),
- * fixed-order chunk combine -> per-row lse / ce / label gradient. */
+ * fixed-order chunk combine -> per-row lse / ce / label gradient.
+ * Canonical shapes (B % 1024 == 0, N | 8): the same epilogue also stores
+ * E = exp2(t*log2(e)*s - m_g) (f16, DISCO_R_G) with m_g the row max over its
+ * 128-column group, and the combine turns m_g into exp2(m_g - lse2)
+ * (DISCO_R_SCALE), so the backward needs no logit recompute. */
 int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
 
 /* Backward part 1: recompute the logit tiles (bit-identical to the forward)
- * -> G = softmax - onehot, unscaled, f16 (shard.py:143-146, matrix.py:131-144). */
+ * -> G = softmax - onehot, unscaled, f16 (shard.py:143-146, matrix.py:131-144).
+ * Canonical shapes: no-op (G = E * scale, label column P_label - 1, is formed
+ * inside the two backward GEMMs' shared-memory stages). */
 int disco_b200_backward_grad(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
 
 /* Backward part 2: cross-rank gradient GEMMs G^T . local features

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_disco_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "disco_b200.h")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # status codes (disco_status)
 OK, SHAPE, LAYOUT, DOMAIN, NONFINITE, CUDA = 0, 1, 2, 3, 4, 5
@@ -25,7 +25,7 @@ F32, BF16, F64, F16 = 0, 1, 2, 3
 
 # workspace regions (disco_region)
 R_PACK, R_GATHER, R_FEAT, R_FEAT16, R_STATS, R_ROWS, R_CE, R_CE_ALL, R_G, R_XPART, R_SEND, R_RECV, \
-    R_INTRA, R_STATUS = range(14)
+    R_INTRA, R_STATUS, R_SCALE = range(15)
 
 _i64 = ctypes.c_int64
 _int = ctypes.c_int

@@ -63,6 +63,10 @@ constexpr int STAGE_BYTES = Ring<1>::STAGE_BYTES;
 static_assert(Ring<1>::STAGES == 6 && Ring<2>::STAGES == 4, "ring geometry");
 constexpr int NUM_THREADS = 320;  // warp0 TMA, warp1 MMA, warps2-9 epilogue
 constexpr int NUM_EPI_WARPS = 8;
+// E-operand GEMMs add 4 transform warps (10-13) that rescale each A stage in smem (E -> G).
+constexpr int NUM_XF_WARPS = 4;
+constexpr int NUM_THREADS_XF = NUM_THREADS + 32 * NUM_XF_WARPS;
+constexpr int GROUP_COLS = 128;   // E offset granularity: one exp2 offset per (row, 128-column group)
 constexpr int TMEM_COLS = 512;    // 2 accumulators of 128 lanes x 256 fp32 columns
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -72,6 +76,7 @@ struct SmemCtl {
   uint64_t empty[STAGES];  // both: MMA done reading the stage (multicast commit)
   uint64_t tfull[2];       // both: accumulator ready (multicast commit)
   uint64_t tempty[2];      // leader: both CTAs' epilogues drained the accumulator
+  uint64_t xfull[STAGES];  // leader: both CTAs' transform warps rescaled the stage (E-operand GEMMs)
   uint32_t tmem_base;
 };
 // Epilogue staging: 8 warps x STAGING_BUFS x (32 rows x 128 B), swizzled like TMA SWIZZLE_128B.
@@ -113,6 +118,9 @@ struct LogitsParams {
   int64_t ldG;
   int g_blocked;        // 1: G stored as [2][b/128][B/128][128][128] (contiguous 32 KiB blocks)
   int debug_flags;      // DISCO_DEBUG_FLAGS (profiling experiments only): bit0 skip G stores
+  // FWDE outputs: E = exp2(y - m_g) into the blocked G region, m_g per (dir, 128-column group, row)
+  float* mg;            // [2][groups][b]
+  int groups;           // B / 128
 };
 
 struct GemmProblem {
@@ -134,6 +142,12 @@ struct GemmProblem {
   int64_t row_div;        // output row r -> (r / row_div) * stride_hi + (r % row_div) * ld_out
   int64_t stride_hi;
   int64_t chunk_stride;   // floats between k-chunk partial outputs
+  // E operand (xform = 1): A holds blocked E; the transform warps rescale every A stage to G
+  int xform;
+  const float* xscale;    // [groups][xb] exp2(m_g - lse2) of this problem's direction
+  const float* xlabel;    // [xb] label-column value P_label - 1
+  int xb;                 // local rows b (pitch of xscale)
+  int lab_off;            // rank * b: global column of local row 0's positive pair
 };
 constexpr int MAX_PROBLEMS = 2;
 struct GemmParams {
@@ -190,11 +204,11 @@ __device__ __forceinline__ uint8_t* smem_base(uint8_t* raw) {
 
 // Leader-side MMA issue for one unit: nk k-blocks of BK, 4 UMMAs per N tile each.
 // NB = 2: the same A stage feeds two N tiles into accumulators d_tmem and d_tmem + BN.
-template <int NB>
+template <int NB, bool XF = false>
 __device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<Ring<NB>::STAGES>& pipe, int nk,
                                          uint32_t d_tmem, uint32_t idesc, int a_mn, int b_mn) {
   for (int kb = 0; kb < nk; ++kb) {
-    ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
+    ptx::mbar_wait(XF ? &ctl->xfull[pipe.stage] : &ctl->full[pipe.stage], pipe.phase);
     ptx::tc_fence_after();
     const uint32_t a_base = ptx::smem_u32(tiles + pipe.stage * Ring<NB>::STAGE_BYTES);
     const uint32_t b_base = a_base + A_STAGE_BYTES;
@@ -212,13 +226,40 @@ __device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<Ring
 }
 
 // Producer side of one k-block: wait for the slot, arm the leader's barrier, load.
-template <int NB>
+// LOCAL (E-operand GEMMs): each CTA counts its own bytes on its own barrier, which its
+// transform warps wait on; otherwise the leader's barrier counts both CTAs' bytes.
+template <int NB, bool LOCAL = false>
 __device__ __forceinline__ uint8_t* producer_acquire(SmemCtl* ctl, uint8_t* tiles, Pipe<Ring<NB>::STAGES>& pipe,
-                                                     bool leader, uint32_t& bar) {
+                                                     bool leader, uint32_t& bar, uint32_t crank = 0) {
   ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
-  if (leader) ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], 2 * Ring<NB>::STAGE_BYTES);
-  bar = ptx::map_to_rank(&ctl->full[pipe.stage], 0);
+  if (LOCAL) {
+    ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], Ring<NB>::STAGE_BYTES);
+    bar = ptx::map_to_rank(&ctl->full[pipe.stage], crank);
+  } else {
+    if (leader) ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], 2 * Ring<NB>::STAGE_BYTES);
+    bar = ptx::map_to_rank(&ctl->full[pipe.stage], 0);
+  }
   return tiles + pipe.stage * Ring<NB>::STAGE_BYTES;
+}
+
+// E -> G on one 128-byte smem row (64 f16 of one G row i, G columns [j0, j0 + 64)) of a
+// SWIZZLE_128B operand stage: multiply by sc in fp32, round to f16; the label column
+// (j == lab) gets P_label - 1.  Logical 16-byte chunk c sits at physical c ^ (row & 7);
+// walking physical chunks in lane order keeps the 8 rows of a quarter-warp on distinct banks.
+__device__ __forceinline__ void xform_row(uint8_t* rowp, int sw, float sc, int lab_rel, float glab) {
+  const __half2 s2 = __float2half2_rn(sc);  // packed f16 multiply: 4 HMUL2 per 16-byte chunk
+  uint4 x[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) x[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    __half2* h = reinterpret_cast<__half2*>(&x[c]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __hmul2(h[k], s2);
+    *reinterpret_cast<uint4*>(rowp + ((c ^ sw) << 4)) = x[c];
+  }
+  if (unsigned(lab_rel) < 64u)
+    *reinterpret_cast<__half*>(rowp + ((((lab_rel >> 3) ^ sw)) << 4) + (lab_rel & 7) * 2) = __float2half_rn(glab);
 }
 
 __device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane) {
@@ -231,6 +272,7 @@ __device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane
       ptx::mbar_init(&ctl->tfull[i], 1);
       ptx::mbar_init(&ctl->tempty[i], 2 * NUM_EPI_WARPS);  // every epilogue warp of both CTAs
     }
+    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&ctl->xfull[s], 2 * NUM_XF_WARPS);
     ptx::fence_barrier_init();
   }
   if (warp == 1) {
@@ -269,7 +311,11 @@ __device__ __forceinline__ void release_accumulator(SmemCtl* ctl, int buf, int l
 // Epilogue: 8 warps; warp w reads TMEM lane quadrant (w % 4) and column half
 // (w - 2) / 4 of this CTA's 128 x 256 accumulator.
 // =====================================================================
-enum { KIND_FWD = 0, KIND_GRAD = 1 };
+// FWDE (canonical shapes): the forward epilogue also stores E = exp2(y - m_g), f16, where
+// m_g is the max of the row over its 128-column group, plus m_g itself.  The backward
+// GEMMs turn E into G = E * exp2(m_g - lse2) (label column: P_label - 1) in shared memory,
+// so the logits are never recomputed.
+enum { KIND_FWD = 0, KIND_GRAD = 1, KIND_FWDE = 2 };
 
 template <int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
@@ -291,15 +337,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   }
   kernel_prologue(ctl, warp, lane);
 
-  const int per_dir = p.row_tiles * p.nchunk * (KIND == KIND_FWD ? 1 : p.tiles_per_chunk);
+  constexpr bool CHUNK_UNITS = KIND != KIND_GRAD;  // unit = all tiles of one column chunk
+  const int per_dir = p.row_tiles * p.nchunk * (CHUNK_UNITS ? 1 : p.tiles_per_chunk);
   const int num_units = 2 * per_dir;
-  const int tiles_per_unit = KIND == KIND_FWD ? p.tiles_per_chunk : 1;
+  const int tiles_per_unit = CHUNK_UNITS ? p.tiles_per_chunk : 1;
   const int nk = p.Dp / BK;
 
   auto decode = [&](int u, int& dir, int& rt, int& ch, int& t0) {
     dir = u / per_dir;
     int rem = u - dir * per_dir;
-    if (KIND == KIND_FWD) {
+    if (CHUNK_UNITS) {
       rt = rem / p.nchunk;
       ch = rem - rt * p.nchunk;
       t0 = 0;
@@ -441,6 +488,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               m2 = mnew;
             }
           }
+        } else if (KIND == KIND_FWDE) {
+          // canonical chunks: this warp's 128 columns are entirely inside or past the chunk
+          if (col0 < chunk_hi) {  // warp-uniform
+            float v[32];
+            float cm = -INFINITY;
+#pragma unroll 1
+            for (int j = 0; j < 4; ++j) {  // pass 1: group max
+              ptx::tmem_ld32(taddr + j * 32, v);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) cm = fmaxf(cm, v[i]);
+            }
+            const float mg = cm * p.tl2e;
+            float s0 = 0.f, s1 = 0.f;
+            const int li = label - col0;  // label column relative to the group
+#pragma unroll 1
+            for (int j = 0; j < 2; ++j) {  // pass 2: E, sum of the non-label terms, 64-column slices
+              uint32_t h[32];
+#pragma unroll
+              for (int half = 0; half < 2; ++half) {
+                ptx::tmem_ld32(taddr + j * 64 + half * 32, v);
+                const int lg = li - (j * 64 + half * 32);
+                if (unsigned(lg) >= 32u) {  // warp-uniform: labels of a warp's 32 rows share a 32-column group
+#pragma unroll
+                  for (int i = 0; i < 32; i += 2) {
+                    const float e0 = ptx::ex2(fmaf(v[i], p.tl2e, -mg));
+                    const float e1 = ptx::ex2(fmaf(v[i + 1], p.tl2e, -mg));
+                    s0 += e0;
+                    s1 += e1;
+                    __half2 hh = __floats2half2_rn(e0, e1);
+                    h[half * 16 + i / 2] = *reinterpret_cast<uint32_t*>(&hh);
+                  }
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 32; i += 2) {
+                    const float e0 = ptx::ex2(fmaf(v[i], p.tl2e, -mg));
+                    const float e1 = ptx::ex2(fmaf(v[i + 1], p.tl2e, -mg));
+                    if (i == lg) yt = v[i] * p.tl2e; else s0 += e0;
+                    if (i + 1 == lg) yt = v[i + 1] * p.tl2e; else s1 += e1;
+                    __half2 hh = __floats2half2_rn(e0, e1);
+                    h[half * 16 + i / 2] = *reinterpret_cast<uint32_t*>(&hh);
+                  }
+                  has_t = true;
+                }
+              }
+              const int cb = col0 + j * 64;
+              const int rbase = rt * PAIR_M + crank * BM + quad * 32;
+              if (lane == 0) ptx::bulk_wait_read<0>();
+              __syncwarp();
+              ptx::st_swizzled_row(tile, lane, h);
+              ptx::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                if (rbase < p.b) ptx::tma_store_4d(&p.g_map[dir], tile, cb & 127, rbase & 127, cb >> 7, rbase >> 7);
+                ptx::bulk_commit();
+              }
+            }
+            const float mnew = fmaxf(m2, mg);
+            l = l * ptx::ex2(m2 - mnew) + (s0 + s1) * ptx::ex2(mg - mnew);
+            m2 = mnew;
+            if (row_ok) p.mg[(int64_t(dir) * p.groups + col0 / GROUP_COLS) * p.b + row] = mg;
+          }
         } else {
           // G = exp2(y - lse2) (label column: P_label - 1), f16, 64-column slices
           // transposed through swizzled smem and written as full 128-byte rows.
@@ -509,12 +617,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         release_accumulator(ctl, buf, lane);
       }
-      if (KIND == KIND_FWD && row_ok) {
+      if (KIND != KIND_GRAD && row_ok) {
         p.stats[((int64_t(dir) * p.nchunk + ch) * 2 + chalf) * p.b + row] = make_float2(m2, l);
         if (has_t) p.target[dir * p.b + row] = yt;
       }
     }
-    if (KIND == KIND_GRAD && lane == 0) ptx::bulk_wait_all();  // drain any bulk stores
+    if (KIND != KIND_FWD && lane == 0) ptx::bulk_wait_all();  // drain any bulk stores
   }
   kernel_epilogue(ctl, warp);
 }
@@ -526,8 +634,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 //   into the two TMEM buffers and summed in the epilogue ((c0 + c1): the first
 //   level of the fixed reduction tree).
 // =====================================================================
-template <int NB>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+template <int NB, bool XF>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF : NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ GemmParams p) {
   constexpr int RS = Ring<NB>::STAGES;
   static_assert(NB == 1 || NB == 2, "one or two N tiles per unit");
@@ -582,7 +690,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           k_range(q, kc * (1 + q.paired) + sub, k0, nk);
           for (int kb = 0; kb < nk; ++kb) {
             uint32_t bar;
-            uint8_t* st = producer_acquire<NB>(ctl, tiles, pipe, leader, bar);
+            uint8_t* st = producer_acquire<NB, XF>(ctl, tiles, pipe, leader, bar, crank);
             const int k = k0 + kb * BK;
             if (q.a_blocked)
               load_blocked(&q.a_map, q.a_mn_major, st, bar, m0, k, BM, ptx::kEvictFirst);
@@ -614,7 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           ptx::mbar_wait(&ctl->tempty[0], ((it >> 1) & 1) ^ 1);
           ptx::mbar_wait(&ctl->tempty[1], ((it >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
-          mma_tile<NB>(ctl, tiles, pipe, nk, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major);
+          mma_tile<NB, XF>(ctl, tiles, pipe, nk, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major);
           ptx::umma_commit_pair(&ctl->tfull[0], 0x3);
           ptx::umma_commit_pair(&ctl->tfull[1], 0x3);
           it += 2;
@@ -626,13 +734,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const uint32_t buf = it & 1, use = it >> 1;
             ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
             ptx::tc_fence_after();
-            mma_tile<1>(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, q.a_mn_major, q.b_mn_major);
+            mma_tile<1, XF>(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, q.a_mn_major, q.b_mn_major);
             ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
           }
         }
       }
     }
-  } else {  // ---------------------------- epilogue warps 2..9
+  } else if (XF && warp >= 2 + NUM_EPI_WARPS) {  // ---------------- transform warps 10..13
+    // Thread xt owns one 128-byte row of this CTA's A stage:
+    //   K-major A (intra, G rows = M): row xt = G row m0 + xt, G columns [k, k + 64);
+    //   MN-major A (cross, G^T): atom xt / 64, K-row xt % 64 = G row k + xt % 64,
+    //   G columns [m0 + 64 * (xt / 64), +64).
+    // The scale of the next stage is loaded one stage ahead (it only depends on K within a unit).
+    const int xt = threadIdx.x - 32 * (2 + NUM_EPI_WARPS);
+    const uint32_t xbar = 0;  // transform completion is counted on the leader's xfull barriers
+    Pipe<RS> pipe;
+    for (int u = pair; u < num_units; u += npairs) {
+      int pi, mt, nt, kc;
+      decode(u, pi, mt, nt, kc);
+      const GemmProblem& q = p.prob[pi];
+      const int m0 = mt * PAIR_M + crank * BM;
+      const int rowoff = q.a_mn_major ? (xt >> 6) * 8192 + (xt & 63) * 128 : xt * 128;
+      const int sw = (rowoff >> 7) & 7;
+      // per-stage scale index: K-major: (k / 128) * xb + (m0 + xt); MN-major: (m0 / 128) * xb + k + xt % 64
+      auto sidx = [&](int k) -> int64_t {
+        return q.a_mn_major ? int64_t(m0 >> 7) * q.xb + k + (xt & 63) : int64_t(k >> 7) * q.xb + m0 + xt;
+      };
+      // rows past b (last pair tile when b / 128 is odd) were zero-filled by TMA: nothing to scale
+      const bool active = q.xform && (q.a_mn_major || m0 + xt < q.xb);
+      const float glab_row = (active && !q.a_mn_major) ? q.xlabel[m0 + xt] : 0.f;
+      for (int sub = 0; sub <= q.paired; ++sub) {
+        int k0, nk;
+        k_range(q, kc * (1 + q.paired) + sub, k0, nk);
+        // scales run XPF stages ahead of the stage being transformed (the scale array is
+        // L2-cold: one stage of lead time does not cover an HBM round trip); the loop is
+        // unrolled by XPF so every prefetch register keeps a fixed role (no moves that would
+        // wait on an in-flight load).
+        constexpr int XPF = 4;
+        auto ld_scale = [&](int kb) { return (active && kb < nk) ? q.xscale[sidx(k0 + kb * BK)] : 0.f; };
+        float sq[XPF];
+#pragma unroll
+        for (int r = 0; r < XPF; ++r) sq[r] = ld_scale(r);
+        for (int kb0 = 0; kb0 < nk; kb0 += XPF) {
+#pragma unroll
+          for (int r = 0; r < XPF; ++r) {
+            const int kb = kb0 + r;
+            if (kb >= nk) break;
+            const int k = k0 + kb * BK;
+            const float sc = sq[r];
+            sq[r] = ld_scale(kb + XPF);
+            ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
+            if (active) {
+              uint8_t* rowp = tiles + pipe.stage * Ring<NB>::STAGE_BYTES + rowoff;
+              int lab_rel;
+              float glab;
+              if (q.a_mn_major) {  // row = G row i = k + xt % 64; label column lab_off + i
+                const int i = k + (xt & 63);
+                lab_rel = q.lab_off + i - (m0 + (xt >> 6) * 64);
+                glab = unsigned(lab_rel) < 64u ? q.xlabel[i] : 0.f;
+              } else {  // row = G row m0 + xt
+                lab_rel = q.lab_off + m0 + xt - k;
+                glab = glab_row;
+              }
+              xform_row(rowp, sw, sc, lab_rel, glab);
+              ptx::fence_proxy_async_smem();
+            }
+            __syncwarp();
+            // CTA-scope release is enough: the pair MMA reads each CTA's stage with that CTA's own
+            // tensor core, and fence.proxy.async above already published the writes to it.  A
+            // cluster-scope release would emit MEMBAR.GPU, which also drains the scale prefetches.
+            if (lane == 0) ptx::mbar_arrive_cluster(ptx::map_to_rank(&ctl->xfull[pipe.stage], xbar));
+            pipe.advance();
+          }
+        }
+      }
+    }
+  } else if (warp >= 2) {  // ---------------------------- epilogue warps 2..9
     const int ew = warp - 2;
     const int quad = warp & 3;
     const int chalf = ew >> 2;
@@ -801,8 +978,10 @@ __global__ void unpack_kernel(const uint4* gathered, int N, int b, int Dp, uint4
 // canonical chunks: balanced tree ((0+1)+(2+3))+((4+5)+(6+7)); non-canonical
 // chunkings: ascending order.
 //   lse2 (log2 domain), ce = -log softmax[label], glabel = P_label - 1 = -(sum_{j!=label} P_j).
+// scale (E path, optional): m_g [2][groups][b] -> exp2(m_g - lse2) in place, the E -> G factor
+// of every (row, 128-column group).
 __global__ void stats_combine_kernel(const float2* stats, const float* target, int nchunk, int b, float* lse2_out,
-                                     float* glabel_out, float* ce_out, Status* status) {
+                                     float* glabel_out, float* ce_out, float* scale, int groups, Status* status) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 2 * b) return;
   const int dir = i / b, r = i % b;
@@ -832,6 +1011,11 @@ __global__ void stats_combine_kernel(const float2* stats, const float* target, i
   lse2_out[i] = lse2;
   glabel_out[i] = -lo / lall;
   ce_out[i] = ce;
+  if (scale) {
+    float* sc = scale + int64_t(dir) * groups * b + r;
+#pragma unroll 4
+    for (int g = 0; g < groups; ++g) sc[int64_t(g) * b] = ptx::ex2(sc[int64_t(g) * b] - lse2);
+  }
   if (!isfinite(ce) || !isfinite(lse2)) atomicOr(&status->flags, FLAG_LOSS_NONFINITE);
 }
 
@@ -1049,6 +1233,8 @@ struct Geometry {
   int g_blocked;          // G in 128 x 128 blocks (canonical chunking: b and B multiples of 128)
   int wide;               // Dp % 512 == 0: GEMM units cover all of D (two accumulators, G read once)
   int ksplit;             // intra K split (fixed function of B, D): partials [2][ksplit][b][Dp]
+  int estore;             // forward stores E + group offsets; backward GEMMs rescale E -> G (no recompute)
+  int groups;             // B / 128 column groups (E offsets)
   int chunk_cols;         // B / nchunk
   int64_t off[DISCO_R_COUNT];
   int64_t len[DISCO_R_COUNT];
@@ -1086,6 +1272,12 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   // level then runs in presum/combine); narrow units pair chunks in the two accumulators.
   g->np = g->wide ? g->cpr : (g->cpr >= 2 ? g->cpr / 2 : 1);
   g->ksplit = (g->wide && B % 128 == 0 && B >= 4096) ? 2 : 1;
+  static const bool no_estore = [] {  // DISCO_RECOMPUTE=1: A/B switch to the recompute (GRAD) path
+    const char* e = getenv("DISCO_RECOMPUTE");
+    return e && atoi(e) != 0;
+  }();
+  g->estore = (g->g_blocked && !no_estore) ? 1 : 0;
+  g->groups = int(B / GROUP_COLS);
   const int64_t b = g->b, Dp = g->Dp, N = world;
   int64_t len[DISCO_R_COUNT];
   len[DISCO_R_PACK] = 2 * b * Dp * 2;
@@ -1102,6 +1294,7 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   len[DISCO_R_RECV] = N > 1 ? N * 2 * b * Dp * 4 : 0;
   len[DISCO_R_INTRA] = 2 * int64_t(g->ksplit) * b * Dp * 4;
   len[DISCO_R_STATUS] = int64_t(sizeof(Status));
+  len[DISCO_R_SCALE] = g->estore ? 2 * int64_t(g->groups) * b * 4 : 0;
   int64_t off = 0;
   for (int r = 0; r < DISCO_R_COUNT; ++r) {
     g->off[r] = off;
@@ -1264,7 +1457,9 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.G = region<__half>(ws, g, DISCO_R_G);
   p.ldG = g.ldG;
   p.g_blocked = g.g_blocked;
-  if (kind == KIND_GRAD && g.g_blocked) {
+  p.mg = region<float>(ws, g, DISCO_R_SCALE);
+  p.groups = g.groups;
+  if (kind != KIND_FWD && g.g_blocked) {
     const __half* Gb = region<__half>(ws, g, DISCO_R_G);
     for (int d = 0; d < 2; ++d)
       if ((rc = make_map_blocked(&p.g_map[d], Gb + int64_t(d) * g.b * g.B, g.b, g.B, 32))) return rc;
@@ -1275,10 +1470,14 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   }();
   p.debug_flags = debug_flags;
   const int64_t units =
-      int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_FWD ? 1 : p.tiles_per_chunk);
+      int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
   if (kind == KIND_FWD) {
     if ((rc = prepare_kernel(logits_kernel<KIND_FWD>))) return rc;
     logits_kernel<KIND_FWD><<<grid_for(units), NUM_THREADS, SMEM_BYTES, st>>>(p);
+    count_launch();
+  } else if (kind == KIND_FWDE) {
+    if ((rc = prepare_kernel(logits_kernel<KIND_FWDE>))) return rc;
+    logits_kernel<KIND_FWDE><<<grid_for(units), NUM_THREADS, SMEM_BYTES, st>>>(p);
     count_launch();
   } else {
     if ((rc = prepare_kernel(logits_kernel<KIND_GRAD>))) return rc;
@@ -1315,21 +1514,38 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
 }
 
 // wide = 1: every unit covers all N columns (n_tiles counts 512-column tiles), NB = 2 kernel.
-int launch_gemm(GemmParams& p, cudaStream_t st, int wide) {
+// xform = 1: A operands hold E (transform warps rescale to G in smem).
+template <int NB, bool XF>
+int launch_gemm_t(GemmParams& p, cudaStream_t st) {
+  int rc;
+  if ((rc = prepare_kernel(gemm_kernel<NB, XF>))) return rc;
+  gemm_kernel<NB, XF><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS, SMEM_BYTES, st>>>(p);
+  return DISCO_OK;
+}
+
+int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform) {
   p.units[0] = 0;
   for (int i = 0; i < p.nprob; ++i)
     p.units[i + 1] = p.units[i] + p.prob[i].m_tiles * p.prob[i].n_tiles * p.prob[i].k_chunks;
   int rc;
-  if (wide) {
-    if ((rc = prepare_kernel(gemm_kernel<2>))) return rc;
-    gemm_kernel<2><<<grid_for(p.units[p.nprob]), NUM_THREADS, SMEM_BYTES, st>>>(p);
-  } else {
-    if ((rc = prepare_kernel(gemm_kernel<1>))) return rc;
-    gemm_kernel<1><<<grid_for(p.units[p.nprob]), NUM_THREADS, SMEM_BYTES, st>>>(p);
-  }
+  if (wide)
+    rc = xform ? launch_gemm_t<2, true>(p, st) : launch_gemm_t<2, false>(p, st);
+  else
+    rc = xform ? launch_gemm_t<1, true>(p, st) : launch_gemm_t<1, false>(p, st);
+  if (rc) return rc;
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
+}
+
+// E operand of direction `dir` (estore): per-(row, group) scales and label-column values.
+void set_xform(GemmProblem& q, void* ws, const Geometry& g, int dir) {
+  q.xform = g.estore;
+  if (!g.estore) return;
+  q.xscale = region<float>(ws, g, DISCO_R_SCALE) + int64_t(dir) * g.groups * g.b;
+  q.xlabel = region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b + int64_t(dir) * g.b;
+  q.xb = int(g.b);
+  q.lab_off = int(int64_t(g.rank) * g.b);
 }
 
 int elementwise_grid(int64_t n, int threads) {
@@ -1430,13 +1646,13 @@ int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, floa
     count_launch();
     CUDA_TRY(cudaGetLastError());
   }
-  if ((rc = launch_logits(KIND_FWD, ws, g, t, st))) return rc;
+  if ((rc = launch_logits(g.estore ? KIND_FWDE : KIND_FWD, ws, g, t, st))) return rc;
   float* rows = region<float>(ws, g, DISCO_R_ROWS);
   const int n = int(2 * g.b);
-  stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(region<float2>(ws, g, DISCO_R_STATS), rows, g.nchunk,
-                                                        int(g.b), rows + 2 * g.b, rows + 4 * g.b,
-                                                        region<float>(ws, g, DISCO_R_CE),
-                                                        region<Status>(ws, g, DISCO_R_STATUS));
+  stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(
+      region<float2>(ws, g, DISCO_R_STATS), rows, g.nchunk, int(g.b), rows + 2 * g.b, rows + 4 * g.b,
+      region<float>(ws, g, DISCO_R_CE), g.estore ? region<float>(ws, g, DISCO_R_SCALE) : nullptr, g.groups,
+      region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
@@ -1447,6 +1663,7 @@ int disco_b200_backward_grad(void* ws, int64_t B, int64_t D, int world, int rank
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
+  if (g.estore) return DISCO_OK;  // the forward already stored E; the backward GEMMs finish G in smem
   return launch_logits(KIND_GRAD, ws, g, t, static_cast<cudaStream_t>(stream));
 }
 
@@ -1491,6 +1708,7 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
     q.a_k_off = 0;
     q.b_k_off = int(int64_t(g.rank) * g.b);
     q.a_row_off = 0;
+    set_xform(q, ws, g, dsrc);
     if (g.np > 1) {  // paired canonical partials [2][np][B][Dp]
       rc = set_output(q, region<float>(ws, g, DISCO_R_XPART) + int64_t(gi) * g.np * g.B * g.Dp, g.Dp, g.B, 0, 1,
                       g.B * g.Dp, g.np);
@@ -1500,7 +1718,7 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
     }
     if (rc) return rc;
   }
-  if ((rc = launch_gemm(p, st, cross_wide))) return rc;
+  if ((rc = launch_gemm(p, st, cross_wide, g.estore))) return rc;
   if (g.np > 1 && world > 1) {  // single rank: the owner combine reads the partials directly
     const int64_t n = 2 * g.B * (g.Dp / 4);
     presum_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_XPART), g.np, world,
@@ -1543,11 +1761,12 @@ int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int ran
     q.k_chunks = g.ksplit;  // fixed K halves [0, B/2), [B/2, B): independent of N
     q.k_chunk_len = int(g.B / g.ksplit);
     q.k_total = int(g.B);
+    set_xform(q, ws, g, gi);
     if ((rc = set_output(q, region<float>(ws, g, DISCO_R_INTRA) + int64_t(gi) * g.ksplit * g.b * g.Dp, g.Dp, g.b, 0,
                          1, g.b * g.Dp, g.ksplit)))
       return rc;
   }
-  return launch_gemm(p, st, g.wide);
+  return launch_gemm(p, st, g.wide, g.estore);
 }
 
 int disco_b200_combine(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip, float* d_image,
