@@ -65,7 +65,8 @@ enum disco_region {
   DISCO_R_RECV = 11,   /* f32  [N][2][b][Dp]      cross slabs by source (all_to_all out)     */
   DISCO_R_INTRA = 12,  /* f32  [2][b][Dp]         intra-rank gradient terms                  */
   DISCO_R_STATUS = 13, /* f64 loss, i32 flags      host-visible step status                   */
-  DISCO_R_SCALE = 14,  /* f32  [2][B/128][b]      E -> G factor exp2(m_g - lse2) per row and
+  DISCO_R_SCALE = 14,  /* f32  [2][B/128][b]      group offsets m_g, then
+                          f16  [2][B/128][b]      E -> G factors exp2(m_g - lse2) per row and
                           128-column group (canonical shapes; empty otherwise)                */
   DISCO_R_COUNT = 15
 };
@@ -121,6 +122,12 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
 /* Backward part 3: intra-rank GEMMs G . gathered features (shard.py:150, 152)
  * into DISCO_R_INTRA.  Independent of the slab exchange, so it overlaps it. */
 int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
+
+/* Backward parts 2 + 3 in one persistent launch (single rank, where no slab
+ * exchange has to overlap the intra GEMM): the intra and cross units are
+ * interleaved in proportion to their counts.  Same outputs as
+ * disco_b200_backward_cross followed by disco_b200_backward_intra. */
+int disco_b200_backward_fused(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
 
 /* Owner combine after the slab exchange (replaces all_reduce(AVG) +
  * row slice, shard.py:199-208): d = t*0.5/B * (intra + tree(recv slabs)),

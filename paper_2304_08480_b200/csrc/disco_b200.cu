@@ -128,6 +128,7 @@ struct GemmProblem {
   CUtensorMap b_map;
   CUtensorMap out_map;    // 3-D fp32 store map {N, row_div, z}, box {32, 32, 1}
   int tma_store;          // 1: TMA stores through staging smem; 0: direct st.global
+  int skip_store;         // profiling experiment (DISCO_DEBUG_FLAGS bit4): drain TMEM, store nothing
   int paired;             // 1: unit = chunks (2kc, 2kc+1), summed in the epilogue
   int a_blocked;          // 1: A is a blocked G ([rows/128][cols/128][128][128], 4-D map)
   int a_mn_major, b_mn_major;
@@ -144,16 +145,20 @@ struct GemmProblem {
   int64_t chunk_stride;   // floats between k-chunk partial outputs
   // E operand (xform = 1): A holds blocked E; the transform warps rescale every A stage to G
   int xform;
-  const float* xscale;    // [groups][xb] exp2(m_g - lse2) of this problem's direction
+  const __half* xscale;   // [groups][xb] exp2(m_g - lse2) of this problem's direction (f16)
   const float* xlabel;    // [xb] label-column value P_label - 1
   int xb;                 // local rows b (pitch of xscale)
   int lab_off;            // rank * b: global column of local row 0's positive pair
 };
-constexpr int MAX_PROBLEMS = 2;
+constexpr int MAX_PROBLEMS = 4;
 struct GemmParams {
   GemmProblem prob[MAX_PROBLEMS];
   int nprob;
   int units[MAX_PROBLEMS + 1];  // prefix sums of per-problem unit counts
+  // split > 0: problems [0, split) (list A) and [split, nprob) (list B) are interleaved in
+  // proportion to their unit counts (Bresenham), so pairs walking the unit sequence with a
+  // stride of #pairs see A and B units in different phases (spreads the accumulator drains).
+  int split;
 };
 
 // --------------------------------------------------------- shared helpers
@@ -243,11 +248,11 @@ __device__ __forceinline__ uint8_t* producer_acquire(SmemCtl* ctl, uint8_t* tile
 }
 
 // E -> G on one 128-byte smem row (64 f16 of one G row i, G columns [j0, j0 + 64)) of a
-// SWIZZLE_128B operand stage: multiply by sc in fp32, round to f16; the label column
+// SWIZZLE_128B operand stage: multiply by the f16 factor sc (HMUL2); the label column
 // (j == lab) gets P_label - 1.  Logical 16-byte chunk c sits at physical c ^ (row & 7);
 // walking physical chunks in lane order keeps the 8 rows of a quarter-warp on distinct banks.
-__device__ __forceinline__ void xform_row(uint8_t* rowp, int sw, float sc, int lab_rel, float glab) {
-  const __half2 s2 = __float2half2_rn(sc);  // packed f16 multiply: 4 HMUL2 per 16-byte chunk
+__device__ __forceinline__ void xform_row(uint8_t* rowp, int sw, __half sc, int lab_rel, float glab) {
+  const __half2 s2 = __half2half2(sc);  // packed f16 multiply: 4 HMUL2 per 16-byte chunk
   uint4 x[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) x[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
@@ -660,6 +665,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
   const int num_units = p.units[p.nprob];
   // unit -> (problem, mt, nt, kc); nt fastest so pairs sharing an A tile run together.
   auto decode = [&](int u, int& pi, int& mt, int& nt, int& kc) {
+    if (p.split > 0) {
+      const int64_t nA = p.units[p.split];
+      const int64_t cA = int64_t(u) * nA / num_units, cA1 = int64_t(u + 1) * nA / num_units;
+      u = cA1 > cA ? int(cA) : int(nA + u - cA1);
+    }
     pi = 0;
     while (pi + 1 < p.nprob && u >= p.units[pi + 1]) ++pi;
     int rem = u - p.units[pi];
@@ -771,8 +781,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
         // unrolled by XPF so every prefetch register keeps a fixed role (no moves that would
         // wait on an in-flight load).
         constexpr int XPF = 4;
-        auto ld_scale = [&](int kb) { return (active && kb < nk) ? q.xscale[sidx(k0 + kb * BK)] : 0.f; };
-        float sq[XPF];
+        auto ld_scale = [&](int kb) { return (active && kb < nk) ? q.xscale[sidx(k0 + kb * BK)] : __float2half(0.f); };
+        __half sq[XPF];
 #pragma unroll
         for (int r = 0; r < XPF; ++r) sq[r] = ld_scale(r);
         for (int kb0 = 0; kb0 < nk; kb0 += XPF) {
@@ -781,7 +791,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             const int kb = kb0 + r;
             if (kb >= nk) break;
             const int k = k0 + kb * BK;
-            const float sc = sq[r];
+            const __half sc = sq[r];
             sq[r] = ld_scale(kb + XPF);
             ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
             if (active) {
@@ -848,7 +858,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] += v1[i];
         }
-        if (q.tma_store) {
+        if (q.skip_store) {
+          if (v[0] == 12345.678f) asm volatile("trap;");  // keep the TMEM load live
+        } else if (q.tma_store == 2) {
+          // 32 x 32 fp32 slice transposed through swizzled smem, then written by the warp as
+          // 128-byte row segments (4 rows per instruction); no async-proxy round trip.
+          uint32_t w[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(v[i]);
+          ptx::st_swizzled_row(tile, lane, w);
+          __syncwarp();
+          ptx::store_tile_rows(tile, lane, [&](int r) -> uint8_t* {
+            const int rr = row0 + r;
+            if (rr >= q.M || c0 + 32 > q.N) return nullptr;
+            return reinterpret_cast<uint8_t*>(q.out + kc * q.chunk_stride + (rr / q.row_div) * q.stride_hi +
+                                              (rr % q.row_div) * q.ld_out + c0);
+          }, ptx::kEvictFirst);
+          __syncwarp();
+        } else if (q.tma_store) {
           // 32 x 32 fp32 slice through swizzled staging -> 3-D TMA store (clipped at M / N).
           uint32_t w[32];
 #pragma unroll
@@ -978,10 +1005,8 @@ __global__ void unpack_kernel(const uint4* gathered, int N, int b, int Dp, uint4
 // canonical chunks: balanced tree ((0+1)+(2+3))+((4+5)+(6+7)); non-canonical
 // chunkings: ascending order.
 //   lse2 (log2 domain), ce = -log softmax[label], glabel = P_label - 1 = -(sum_{j!=label} P_j).
-// scale (E path, optional): m_g [2][groups][b] -> exp2(m_g - lse2) in place, the E -> G factor
-// of every (row, 128-column group).
 __global__ void stats_combine_kernel(const float2* stats, const float* target, int nchunk, int b, float* lse2_out,
-                                     float* glabel_out, float* ce_out, float* scale, int groups, Status* status) {
+                                     float* glabel_out, float* ce_out, Status* status) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 2 * b) return;
   const int dir = i / b, r = i % b;
@@ -1011,12 +1036,29 @@ __global__ void stats_combine_kernel(const float2* stats, const float* target, i
   lse2_out[i] = lse2;
   glabel_out[i] = -lo / lall;
   ce_out[i] = ce;
-  if (scale) {
-    float* sc = scale + int64_t(dir) * groups * b + r;
-#pragma unroll 4
-    for (int g = 0; g < groups; ++g) sc[int64_t(g) * b] = ptx::ex2(sc[int64_t(g) * b] - lse2);
-  }
+
   if (!isfinite(ce) || !isfinite(lse2)) atomicOr(&status->flags, FLAG_LOSS_NONFINITE);
+}
+
+// E path: m_g [2][groups][b] (f32, log2 domain) -> sc [2][groups][b] = exp2(m_g - lse2[dir][r]) as f16,
+// the E -> G factor of every (row, 128-column group).  8 elements per thread (b % 8 == 0).
+__global__ void scale_kernel(const float4* mg, const float* lse2, int groups, int b, uint4* sc) {
+  const int64_t per_dir = int64_t(groups) * b / 8;
+  const int64_t total = 2 * per_dir;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int dir = int(i / per_dir);
+    const int r = int((i * 8) % b);
+    const float4 m0 = mg[2 * i], m1 = mg[2 * i + 1];
+    const float4 l0 = *reinterpret_cast<const float4*>(lse2 + int64_t(dir) * b + r);
+    const float4 l1 = *reinterpret_cast<const float4*>(lse2 + int64_t(dir) * b + r + 4);
+    uint4 o;
+    __half2* h = reinterpret_cast<__half2*>(&o);
+    h[0] = __floats2half2_rn(ptx::ex2(m0.x - l0.x), ptx::ex2(m0.y - l0.y));
+    h[1] = __floats2half2_rn(ptx::ex2(m0.z - l0.z), ptx::ex2(m0.w - l0.w));
+    h[2] = __floats2half2_rn(ptx::ex2(m1.x - l1.x), ptx::ex2(m1.y - l1.y));
+    h[3] = __floats2half2_rn(ptx::ex2(m1.z - l1.z), ptx::ex2(m1.w - l1.w));
+    sc[i] = o;
+  }
 }
 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
@@ -1243,6 +1285,17 @@ struct Geometry {
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+// DISCO_DEBUG_FLAGS (profiling experiments only): bit0 skip G stores (recompute GRAD), bit1 L2
+// persistence for the features in GRAD, bit4 skip GEMM output stores, bit5 GEMM epilogues store
+// with st.global instead of TMA.
+int debug_flag_bits() {
+  static const int bits = [] {
+    const char* e = getenv("DISCO_DEBUG_FLAGS");
+    return e ? atoi(e) : 0;
+  }();
+  return bits;
+}
+
 int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   if (world < 1) return fail(DISCO_LAYOUT_ERROR, "world size must be >= 1, got %d", world);
   if (B < 1) return fail(DISCO_LAYOUT_ERROR, "global batch must be >= 1, got %lld", (long long)B);
@@ -1294,7 +1347,7 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   len[DISCO_R_RECV] = N > 1 ? N * 2 * b * Dp * 4 : 0;
   len[DISCO_R_INTRA] = 2 * int64_t(g->ksplit) * b * Dp * 4;
   len[DISCO_R_STATUS] = int64_t(sizeof(Status));
-  len[DISCO_R_SCALE] = g->estore ? 2 * int64_t(g->groups) * b * 4 : 0;
+  len[DISCO_R_SCALE] = g->estore ? 2 * int64_t(g->groups) * b * (4 + 2) : 0;  // f32 m_g, then f16 scales
   int64_t off = 0;
   for (int r = 0; r < DISCO_R_COUNT; ++r) {
     g->off[r] = off;
@@ -1379,7 +1432,9 @@ int set_output(GemmProblem& q, float* out, int64_t ld_out, int64_t row_div, int6
   q.stride_hi = stride_hi;
   q.chunk_stride = chunk_stride;
   q.tma_store = 0;
-  const bool aligned = (row_div % 32 == 0) && (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  q.skip_store = (debug_flag_bits() & 16) ? 1 : 0;
+  const bool aligned = (row_div % 32 == 0) && (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
+                       !(debug_flag_bits() & 32);
   if (aligned && (nz_rows == 1 || nz_chunks == 1)) {
     const uint64_t nz = uint64_t(nz_rows > 1 ? nz_rows : nz_chunks);
     const uint64_t zp = uint64_t(nz_rows > 1 ? stride_hi : (nz_chunks > 1 ? chunk_stride : row_div * ld_out));
@@ -1387,7 +1442,7 @@ int set_output(GemmProblem& q, float* out, int64_t ld_out, int64_t row_div, int6
       int rc = make_map_f32_3d(&q.out_map, out, uint64_t(q.N), uint64_t(std::min<int64_t>(row_div, q.M)), nz,
                                uint64_t(ld_out), zp);
       if (rc) return rc;
-      q.tma_store = 1;
+      q.tma_store = (debug_flag_bits() & 64) ? 2 : 1;
     }
   }
   return DISCO_OK;
@@ -1464,10 +1519,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
     for (int d = 0; d < 2; ++d)
       if ((rc = make_map_blocked(&p.g_map[d], Gb + int64_t(d) * g.b * g.B, g.b, g.B, 32))) return rc;
   }
-  static const int debug_flags = [] {
-    const char* e = getenv("DISCO_DEBUG_FLAGS");
-    return e ? atoi(e) : 0;
-  }();
+  const int debug_flags = debug_flag_bits();
   p.debug_flags = debug_flags;
   const int64_t units =
       int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
@@ -1538,11 +1590,16 @@ int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform) {
   return DISCO_OK;
 }
 
+// f16 E -> G factors [2][groups][b], stored after the f32 m_g in DISCO_R_SCALE.
+uint4* scale16(void* ws, const Geometry& g) {
+  return reinterpret_cast<uint4*>(region<float>(ws, g, DISCO_R_SCALE) + 2 * int64_t(g.groups) * g.b);
+}
+
 // E operand of direction `dir` (estore): per-(row, group) scales and label-column values.
 void set_xform(GemmProblem& q, void* ws, const Geometry& g, int dir) {
   q.xform = g.estore;
   if (!g.estore) return;
-  q.xscale = region<float>(ws, g, DISCO_R_SCALE) + int64_t(dir) * g.groups * g.b;
+  q.xscale = reinterpret_cast<const __half*>(scale16(ws, g)) + int64_t(dir) * g.groups * g.b;
   q.xlabel = region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b + int64_t(dir) * g.b;
   q.xb = int(g.b);
   q.lab_off = int(int64_t(g.rank) * g.b);
@@ -1550,6 +1607,105 @@ void set_xform(GemmProblem& q, void* ws, const Geometry& g, int dir) {
 
 int elementwise_grid(int64_t n, int threads) {
   return int(std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, int64_t(sm_count()) * 16)));
+}
+
+
+cudaStream_t st_of(void* stream) { return static_cast<cudaStream_t>(stream); }
+
+// Cross GEMMs into p.prob[first], p.prob[first + 1]:
+//   X_g = G_{d'}^T . A_{d'} (local rows), g = image <- d' = t2i (1), g = text <- d' = i2t (0)
+int build_cross(GemmParams& p, int first, void* ws, const Geometry& g) {
+  const __half* G = region<__half>(ws, g, DISCO_R_G);
+  const __half* f16 = region<__half>(ws, g, DISCO_R_FEAT16);
+  const __half* I16 = f16;
+  const __half* T16 = f16 + g.B * g.Dp;
+  const int64_t Bc = g.B / g.nchunk;  // canonical chunk rows
+  const int cross_wide = g.wide;      // wide units read G once; otherwise chunks are paired
+  int rc;
+  for (int gi = 0; gi < 2; ++gi) {
+    GemmProblem& q = p.prob[first + gi];
+    const int dsrc = gi == 0 ? 1 : 0;
+    const __half* Gd = G + int64_t(dsrc) * g.b * g.ldG;
+    const __half* Ad = gi == 0 ? T16 : I16;  // image grad uses T_n, text grad uses I_n
+    if (g.g_blocked) {
+      if ((rc = make_map_blocked(&q.a_map, G + int64_t(dsrc) * g.b * g.B, g.b, g.B, 64))) return rc;
+      q.a_blocked = 1;
+    } else if ((rc = make_map(&q.a_map, false, Gd, g.B, g.b, g.ldG, 64, 64))) {  // MN-major G^T
+      return rc;
+    }
+    if ((rc = make_map(&q.b_map, false, Ad, g.Dp, g.B, g.Dp, 64, 64))) return rc;  // MN-major features
+    q.a_mn_major = 1;
+    q.b_mn_major = 1;
+    q.M = int(g.B);
+    q.N = int(g.Dp);
+    q.m_tiles = int((g.B + PAIR_M - 1) / PAIR_M);
+    q.n_tiles = cross_wide ? int(g.Dp / (2 * BN)) : int((g.Dp + BN - 1) / BN);
+    q.paired = !cross_wide && g.cpr >= 2;
+    q.k_chunks = g.np;  // units along K (pairs of canonical chunks when paired)
+    q.k_chunk_len = int(g.cpr > 1 ? Bc : g.b);
+    q.k_total = int(g.b);
+    q.a_k_off = 0;
+    q.b_k_off = int(int64_t(g.rank) * g.b);
+    q.a_row_off = 0;
+    set_xform(q, ws, g, dsrc);
+    if (g.np > 1) {  // canonical partials [2][np][B][Dp]
+      rc = set_output(q, region<float>(ws, g, DISCO_R_XPART) + int64_t(gi) * g.np * g.B * g.Dp, g.Dp, g.B, 0, 1,
+                      g.B * g.Dp, g.np);
+    } else {  // directly destination-major send slabs [N][2][b][Dp]
+      rc = set_output(q, region<float>(ws, g, DISCO_R_SEND) + int64_t(gi) * g.b * g.Dp, g.Dp, g.b, 2 * g.b * g.Dp,
+                      g.N, 0, 1);
+    }
+    if (rc) return rc;
+  }
+  return DISCO_OK;
+}
+
+// Sender-side tree over this rank's chunk partials into the destination-major slabs
+// (single rank: the owner combine reads the partials directly).
+int cross_presum(void* ws, const Geometry& g, cudaStream_t st) {
+  if (g.np > 1 && g.N > 1) {
+    const int64_t n = 2 * g.B * (g.Dp / 4);
+    presum_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_XPART), g.np, g.N,
+                                                           int(g.b), int(g.Dp), region<float4>(ws, g, DISCO_R_SEND));
+    count_launch();
+    CUDA_TRY(cudaGetLastError());
+  }
+  return DISCO_OK;
+}
+
+// Intra GEMMs into p.prob[first], p.prob[first + 1]: Y_image = G_i . T_g ; Y_text = G_t . I_g
+int build_intra(GemmParams& p, int first, void* ws, const Geometry& g) {
+  const __half* G = region<__half>(ws, g, DISCO_R_G);
+  const __half* f16 = region<__half>(ws, g, DISCO_R_FEAT16);
+  const __half* I16 = f16;
+  const __half* T16 = f16 + g.B * g.Dp;
+  int rc;
+  for (int gi = 0; gi < 2; ++gi) {
+    GemmProblem& q = p.prob[first + gi];
+    const __half* Gd = G + int64_t(gi) * g.b * g.ldG;
+    const __half* Cd = gi == 0 ? T16 : I16;
+    if (g.g_blocked) {
+      if ((rc = make_map_blocked(&q.a_map, G + int64_t(gi) * g.b * g.B, g.b, g.B, BM))) return rc;
+      q.a_blocked = 1;
+    } else if ((rc = make_map(&q.a_map, false, Gd, g.B, g.b, g.ldG, 64, BM))) {  // K-major G
+      return rc;
+    }
+    if ((rc = make_map(&q.b_map, false, Cd, g.Dp, g.B, g.Dp, 64, 64))) return rc;  // MN-major features
+    q.a_mn_major = 0;
+    q.b_mn_major = 1;
+    q.M = int(g.b);
+    q.N = int(g.Dp);
+    q.m_tiles = int((g.b + PAIR_M - 1) / PAIR_M);
+    q.n_tiles = g.wide ? int(g.Dp / (2 * BN)) : int((g.Dp + BN - 1) / BN);
+    q.k_chunks = g.ksplit;  // fixed K halves [0, B/2), [B/2, B): independent of N
+    q.k_chunk_len = int(g.B / g.ksplit);
+    q.k_total = int(g.B);
+    set_xform(q, ws, g, gi);
+    if ((rc = set_output(q, region<float>(ws, g, DISCO_R_INTRA) + int64_t(gi) * g.ksplit * g.b * g.Dp, g.Dp, g.b, 0,
+                         1, g.b * g.Dp, g.ksplit)))
+      return rc;
+  }
+  return DISCO_OK;
 }
 
 }  // namespace disco
@@ -1651,10 +1807,16 @@ int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, floa
   const int n = int(2 * g.b);
   stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(
       region<float2>(ws, g, DISCO_R_STATS), rows, g.nchunk, int(g.b), rows + 2 * g.b, rows + 4 * g.b,
-      region<float>(ws, g, DISCO_R_CE), g.estore ? region<float>(ws, g, DISCO_R_SCALE) : nullptr, g.groups,
-      region<Status>(ws, g, DISCO_R_STATUS));
+      region<float>(ws, g, DISCO_R_CE), region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
   CUDA_TRY(cudaGetLastError());
+  if (g.estore) {
+    const int64_t nv = 2 * int64_t(g.groups) * g.b / 8;
+    scale_kernel<<<elementwise_grid(nv, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_SCALE), rows + 2 * g.b,
+                                                           g.groups, int(g.b), scale16(ws, g));
+    count_launch();
+    CUDA_TRY(cudaGetLastError());
+  }
   return DISCO_OK;
 }
 
@@ -1672,101 +1834,38 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-
-  // cross GEMMs: X_g = G_{d'}^T . A_{d'} (local rows), g = image <- d' = t2i (1), g = text <- d' = i2t (0)
-  const __half* G = region<__half>(ws, g, DISCO_R_G);
-  const __half* f16 = region<__half>(ws, g, DISCO_R_FEAT16);
-  const __half* I16 = f16;
-  const __half* T16 = f16 + g.B * g.Dp;
   GemmParams p;
   memset(&p, 0, sizeof(p));
+  if ((rc = build_cross(p, 0, ws, g))) return rc;
   p.nprob = 2;
-  const int64_t Bc = g.B / g.nchunk;  // canonical chunk rows
-  const int cross_wide = g.wide;  // wide units read G once; otherwise chunks are paired
-  for (int gi = 0; gi < 2; ++gi) {
-    GemmProblem& q = p.prob[gi];
-    const int dsrc = gi == 0 ? 1 : 0;
-    const __half* Gd = G + int64_t(dsrc) * g.b * g.ldG;
-    const __half* Ad = gi == 0 ? T16 : I16;  // image grad uses T_n, text grad uses I_n
-    if (g.g_blocked) {
-      if ((rc = make_map_blocked(&q.a_map, G + int64_t(dsrc) * g.b * g.B, g.b, g.B, 64))) return rc;
-      q.a_blocked = 1;
-    } else if ((rc = make_map(&q.a_map, false, Gd, g.B, g.b, g.ldG, 64, 64))) {  // MN-major G^T
-      return rc;
-    }
-    if ((rc = make_map(&q.b_map, false, Ad, g.Dp, g.B, g.Dp, 64, 64))) return rc;  // MN-major features
-    q.a_mn_major = 1;
-    q.b_mn_major = 1;
-    q.M = int(g.B);
-    q.N = int(g.Dp);
-    q.m_tiles = int((g.B + PAIR_M - 1) / PAIR_M);
-    q.n_tiles = cross_wide ? int(g.Dp / (2 * BN)) : int((g.Dp + BN - 1) / BN);
-    q.paired = !cross_wide && g.cpr >= 2;
-    q.k_chunks = g.np;  // units along K (pairs of canonical chunks when paired)
-    q.k_chunk_len = int(g.cpr > 1 ? Bc : g.b);
-    q.k_total = int(g.b);
-    q.a_k_off = 0;
-    q.b_k_off = int(int64_t(g.rank) * g.b);
-    q.a_row_off = 0;
-    set_xform(q, ws, g, dsrc);
-    if (g.np > 1) {  // paired canonical partials [2][np][B][Dp]
-      rc = set_output(q, region<float>(ws, g, DISCO_R_XPART) + int64_t(gi) * g.np * g.B * g.Dp, g.Dp, g.B, 0, 1,
-                      g.B * g.Dp, g.np);
-    } else {  // directly destination-major send slabs [N][2][b][Dp]
-      rc = set_output(q, region<float>(ws, g, DISCO_R_SEND) + int64_t(gi) * g.b * g.Dp, g.Dp, g.b, 2 * g.b * g.Dp,
-                      world, 0, 1);
-    }
-    if (rc) return rc;
-  }
-  if ((rc = launch_gemm(p, st, cross_wide, g.estore))) return rc;
-  if (g.np > 1 && world > 1) {  // single rank: the owner combine reads the partials directly
-    const int64_t n = 2 * g.B * (g.Dp / 4);
-    presum_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_XPART), g.np, world,
-                                                           int(g.b), int(g.Dp), region<float4>(ws, g, DISCO_R_SEND));
-    count_launch();
-    CUDA_TRY(cudaGetLastError());
-  }
-  return DISCO_OK;
+  if ((rc = launch_gemm(p, st, g.wide, g.estore))) return rc;
+  return cross_presum(ws, g, st);
 }
 
 int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int rank, void* stream) {
   Geometry g;
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const __half* G = region<__half>(ws, g, DISCO_R_G);
-  const __half* f16 = region<__half>(ws, g, DISCO_R_FEAT16);
-  const __half* I16 = f16;
-  const __half* T16 = f16 + g.B * g.Dp;
   GemmParams p;
   memset(&p, 0, sizeof(p));
+  if ((rc = build_intra(p, 0, ws, g))) return rc;
   p.nprob = 2;
-  for (int gi = 0; gi < 2; ++gi) {  // Y_image = G_i . T_g ; Y_text = G_t . I_g
-    GemmProblem& q = p.prob[gi];
-    const __half* Gd = G + int64_t(gi) * g.b * g.ldG;
-    const __half* Cd = gi == 0 ? T16 : I16;
-    if (g.g_blocked) {
-      if ((rc = make_map_blocked(&q.a_map, G + int64_t(gi) * g.b * g.B, g.b, g.B, BM))) return rc;
-      q.a_blocked = 1;
-    } else if ((rc = make_map(&q.a_map, false, Gd, g.B, g.b, g.ldG, 64, BM))) {  // K-major G
-      return rc;
-    }
-    if ((rc = make_map(&q.b_map, false, Cd, g.Dp, g.B, g.Dp, 64, 64))) return rc;  // MN-major features
-    q.a_mn_major = 0;
-    q.b_mn_major = 1;
-    q.M = int(g.b);
-    q.N = int(g.Dp);
-    q.m_tiles = int((g.b + PAIR_M - 1) / PAIR_M);
-    q.n_tiles = g.wide ? int(g.Dp / (2 * BN)) : int((g.Dp + BN - 1) / BN);
-    q.k_chunks = g.ksplit;  // fixed K halves [0, B/2), [B/2, B): independent of N
-    q.k_chunk_len = int(g.B / g.ksplit);
-    q.k_total = int(g.B);
-    set_xform(q, ws, g, gi);
-    if ((rc = set_output(q, region<float>(ws, g, DISCO_R_INTRA) + int64_t(gi) * g.ksplit * g.b * g.Dp, g.Dp, g.b, 0,
-                         1, g.b * g.Dp, g.ksplit)))
-      return rc;
-  }
-  return launch_gemm(p, st, g.wide, g.estore);
+  return launch_gemm(p, st_of(stream), g.wide, g.estore);
+}
+
+int disco_b200_backward_fused(void* ws, int64_t B, int64_t D, int world, int rank, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  cudaStream_t st = st_of(stream);
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  if ((rc = build_intra(p, 0, ws, g))) return rc;  // list A: long units (K = B / ksplit)
+  if ((rc = build_cross(p, 2, ws, g))) return rc;  // list B: one canonical chunk of K per unit
+  p.nprob = 4;
+  p.split = 2;
+  if ((rc = launch_gemm(p, st, g.wide, g.estore))) return rc;
+  return cross_presum(ws, g, st);
 }
 
 int disco_b200_combine(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip, float* d_image,

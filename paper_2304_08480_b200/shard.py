@@ -330,11 +330,14 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         endpoint.all_gather_into(plan.gather, plan.pack)
     _lib.call("disco_b200_forward", *plan.args, t, st)
     _lib.call("disco_b200_backward_grad", *plan.args, t, st)
-    _lib.call("disco_b200_backward_cross", *plan.args, st)
-    work = endpoint.all_to_all_into(plan.recv, plan.send, async_op=True) if N > 1 else None
-    _lib.call("disco_b200_backward_intra", *plan.args, st)
-    if work is not None:
+    if N > 1:
+        # cross first, so the slab exchange overlaps the intra GEMM
+        _lib.call("disco_b200_backward_cross", *plan.args, st)
+        work = endpoint.all_to_all_into(plan.recv, plan.send, async_op=True)
+        _lib.call("disco_b200_backward_intra", *plan.args, st)
         work.wait()
+    else:
+        _lib.call("disco_b200_backward_fused", *plan.args, st)
     d_image = torch.empty((b, D), dtype=torch.float32, device=device)
     d_text = torch.empty((b, D), dtype=torch.float32, device=device)
     _lib.call("disco_b200_combine", *plan.args, t, int(bool(flip_cross_rank_sign)),

@@ -17,8 +17,9 @@ import os
 import subprocess
 
 KERNEL_KEYS = [  # order of the tensor-core launches within one step
-    ("logits_kernel<0>", "logits_fwd"),
-    ("logits_kernel<1>", "logits_grad"),
+    ("logits_kernel<2>", "logits_fwd"),   # forward + E store (canonical shapes)
+    ("logits_kernel<0>", "logits_fwd"),   # forward only (recompute path)
+    ("logits_kernel<1>", "logits_grad"),  # recompute path only
     ("gemm_kernel", "gemm_cross"),
     ("gemm_kernel", "gemm_intra"),
 ]
@@ -63,7 +64,7 @@ def summarize_rep(rep):
     out = {}
     seen = {}
     for r in rows:
-        name = r[h.index("Kernel Name")]
+        name = r[h.index("Kernel Name")].replace("(int)", "")
         for pat, key in KERNEL_KEYS:
             if pat in name:
                 n = seen.get(pat, 0)
