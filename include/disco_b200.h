@@ -136,6 +136,16 @@ int disco_b200_backward_fused(void* ws, int64_t B, int64_t D, int world, int ran
 int disco_b200_combine(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,
                        float* d_image, float* d_text, int64_t ld_out, void* stream);
 
+/* Row-block pipelining (single rank): backward GEMMs (intra + cross) restricted
+ * to output rows [row0, row1) (256-aligned, or row1 == b), and the owner combine
+ * of those rows.  Running block k's combine and device->host copy while block
+ * k+1's GEMMs run hides the gradient read-back; the union over blocks equals
+ * disco_b200_backward_fused + disco_b200_combine bit for bit. */
+int disco_b200_backward_rows(void* ws, int64_t B, int64_t D, int world, int rank, int64_t row0, int64_t row1,
+                             void* stream);
+int disco_b200_combine_rows(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip, int64_t row0,
+                            int64_t row1, float* d_image, float* d_text, int64_t ld_out, void* stream);
+
 /* Full-size per-rank contribution (LocalGradContribution, shard.py:61-80,
  * 153-162): t*0.5/b * (scatter(intra) + send slabs), B x D fp32 each. */
 int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,

@@ -47,6 +47,8 @@ SIGNATURES = {
     "disco_b200_backward_intra": [_vp, _i64, _i64, _int, _int, _vp],
     "disco_b200_backward_fused": [_vp, _i64, _i64, _int, _int, _vp],
     "disco_b200_combine": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _vp, _i64, _vp],
+    "disco_b200_backward_rows": [_vp, _i64, _i64, _int, _int, _i64, _i64, _vp],
+    "disco_b200_combine_rows": [_vp, _i64, _i64, _int, _int, _f32, _int, _i64, _i64, _vp, _vp, _i64, _vp],
     "disco_b200_contribution": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _vp, _i64, _vp],
     "disco_b200_loss": [_vp, _i64, _i64, _int, _int, _int, _vp],
 }

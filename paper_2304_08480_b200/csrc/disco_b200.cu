@@ -134,6 +134,7 @@ struct GemmProblem {
   int a_mn_major, b_mn_major;
   int M, N;               // valid output extents
   int m_tiles, n_tiles, k_chunks;  // m tiles of 256 rows (CTA pair), n tiles of 256 columns
+  int m_off;              // first m tile (row-block launches cover tiles [m_off, m_off + m_tiles))
   int k_chunk_len;        // elements of K per chunk (multiple of 64 unless k_chunks == 1)
   int k_total;            // total K extent
   int a_k_off, b_k_off;   // added to the K coordinate of MN-major operands
@@ -677,7 +678,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     nt = rem % q.n_tiles;
     rem /= q.n_tiles;
     kc = rem % q.k_chunks;
-    mt = rem / q.k_chunks;
+    mt = rem / q.k_chunks + q.m_off;
   };
   // canonical chunk index `c` -> [k0, k0 + nk*BK)
   auto k_range = [&](const GemmProblem& q, int c, int& k0, int& nk) {
@@ -1118,17 +1119,19 @@ __global__ void presum_kernel(const float4* xpart, int np, int N, int b, int Dp,
 // Owner combine: d_g[r] = s * (intra_g[r] + cross_g[r]) written b x D (ld_out), where
 //   cross = tree over the N received slabs recv[src][g][r] (negated for src != rank if flip), or,
 //   single rank with canonical chunks (xpart != null), tree over the np local paired partials.
+// Rows [row0, row0 + nrows) only (row-block pipelining); outputs are indexed by the absolute row.
 __global__ void combine_kernel(const float4* intra, int ksplit, const float4* recv, const float4* xpart, int np,
                                int N, int rank, int b, int Dp, int D, float s, int flip, float* d_image,
-                               float* d_text, int64_t ld_out, Status* status) {
+                               float* d_text, int64_t ld_out, int row0, int nrows, Status* status) {
   const int v4 = Dp / 4;
   const bool vec_out = (ld_out % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_image) | reinterpret_cast<uintptr_t>(d_text)) % 16 == 0);
   const int64_t per_g = int64_t(b) * v4;
-  const int64_t total = 2 * per_g;
+  const int64_t per_blk = int64_t(nrows) * v4;
+  const int64_t total = 2 * per_blk;
   bool bad = false;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int g = int(i / per_g);
-    const int64_t rem = i - g * per_g;
+  for (int64_t ii = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ii < total; ii += int64_t(gridDim.x) * blockDim.x) {
+    const int g = int(ii / per_blk);
+    const int64_t rem = (ii - g * per_blk) + int64_t(row0) * v4;
     const int r = int(rem / v4), vc = int(rem % v4);
     float4 cross;
     if (xpart) {
@@ -1614,7 +1617,7 @@ cudaStream_t st_of(void* stream) { return static_cast<cudaStream_t>(stream); }
 
 // Cross GEMMs into p.prob[first], p.prob[first + 1]:
 //   X_g = G_{d'}^T . A_{d'} (local rows), g = image <- d' = t2i (1), g = text <- d' = i2t (0)
-int build_cross(GemmParams& p, int first, void* ws, const Geometry& g) {
+int build_cross(GemmParams& p, int first, void* ws, const Geometry& g, int mt0 = 0, int mt1 = -1) {
   const __half* G = region<__half>(ws, g, DISCO_R_G);
   const __half* f16 = region<__half>(ws, g, DISCO_R_FEAT16);
   const __half* I16 = f16;
@@ -1639,6 +1642,8 @@ int build_cross(GemmParams& p, int first, void* ws, const Geometry& g) {
     q.M = int(g.B);
     q.N = int(g.Dp);
     q.m_tiles = int((g.B + PAIR_M - 1) / PAIR_M);
+    if (mt1 >= 0) q.m_tiles = std::min(q.m_tiles, mt1) - mt0;
+    q.m_off = mt0;
     q.n_tiles = cross_wide ? int(g.Dp / (2 * BN)) : int((g.Dp + BN - 1) / BN);
     q.paired = !cross_wide && g.cpr >= 2;
     q.k_chunks = g.np;  // units along K (pairs of canonical chunks when paired)
@@ -1673,8 +1678,22 @@ int cross_presum(void* ws, const Geometry& g, cudaStream_t st) {
   return DISCO_OK;
 }
 
+int launch_combine(void* ws, const Geometry& g, float t, int flip, int row0, int nrows, float* d_image, float* d_text,
+                   int64_t ld_out, cudaStream_t st) {
+  const float s = float(0.5 * double(t) / double(g.B));
+  const int64_t n = 2 * int64_t(nrows) * (g.Dp / 4);
+  if (n == 0) return DISCO_OK;
+  combine_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
+      region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float4>(ws, g, DISCO_R_RECV),
+      (g.N == 1 && g.np > 1) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, g.N, g.rank, int(g.b),
+      int(g.Dp), int(g.D), s, flip, d_image, d_text, ld_out, row0, nrows, region<Status>(ws, g, DISCO_R_STATUS));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
 // Intra GEMMs into p.prob[first], p.prob[first + 1]: Y_image = G_i . T_g ; Y_text = G_t . I_g
-int build_intra(GemmParams& p, int first, void* ws, const Geometry& g) {
+int build_intra(GemmParams& p, int first, void* ws, const Geometry& g, int mt0 = 0, int mt1 = -1) {
   const __half* G = region<__half>(ws, g, DISCO_R_G);
   const __half* f16 = region<__half>(ws, g, DISCO_R_FEAT16);
   const __half* I16 = f16;
@@ -1696,6 +1715,8 @@ int build_intra(GemmParams& p, int first, void* ws, const Geometry& g) {
     q.M = int(g.b);
     q.N = int(g.Dp);
     q.m_tiles = int((g.b + PAIR_M - 1) / PAIR_M);
+    if (mt1 >= 0) q.m_tiles = std::min(q.m_tiles, mt1) - mt0;
+    q.m_off = mt0;
     q.n_tiles = g.wide ? int(g.Dp / (2 * BN)) : int((g.Dp + BN - 1) / BN);
     q.k_chunks = g.ksplit;  // fixed K halves [0, B/2), [B/2, B): independent of N
     q.k_chunk_len = int(g.B / g.ksplit);
@@ -1875,15 +1896,37 @@ int disco_b200_combine(void* ws, int64_t B, int64_t D, int world, int rank, floa
   if (rc) return rc;
   if (ld_out < D) return fail(DISCO_SHAPE_ERROR, "output row stride smaller than D");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const float s = float(0.5 * double(t) / double(B));
-  const int64_t n = 2 * g.b * (g.Dp / 4);
-  combine_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
-      region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float4>(ws, g, DISCO_R_RECV),
-      (world == 1 && g.np > 1) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, world, rank, int(g.b),
-      int(g.Dp), int(D), s, flip, d_image, d_text, ld_out, region<Status>(ws, g, DISCO_R_STATUS));
-  count_launch();
-  CUDA_TRY(cudaGetLastError());
-  return DISCO_OK;
+  return launch_combine(ws, g, t, flip, 0, int(g.b), d_image, d_text, ld_out, st);
+}
+
+int disco_b200_combine_rows(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip, int64_t row0,
+                            int64_t row1, float* d_image, float* d_text, int64_t ld_out, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (ld_out < D) return fail(DISCO_SHAPE_ERROR, "output row stride smaller than D");
+  if (row0 < 0 || row1 > g.b || row0 > row1) return fail(DISCO_SHAPE_ERROR, "row range [%lld, %lld) outside [0, %lld)",
+                                                         (long long)row0, (long long)row1, (long long)g.b);
+  return launch_combine(ws, g, t, flip, int(row0), int(row1 - row0), d_image, d_text, ld_out, st_of(stream));
+}
+
+int disco_b200_backward_rows(void* ws, int64_t B, int64_t D, int world, int rank, int64_t row0, int64_t row1,
+                             void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (world != 1) return fail(DISCO_LAYOUT_ERROR, "row-block backward is single-rank only (N = %d)", world);
+  if (row0 < 0 || row1 > g.b || row0 >= row1 || row0 % PAIR_M != 0 || (row1 % PAIR_M != 0 && row1 != g.b))
+    return fail(DISCO_SHAPE_ERROR, "row block [%lld, %lld) must be 256-aligned inside [0, %lld)", (long long)row0,
+                (long long)row1, (long long)g.b);
+  const int mt0 = int(row0 / PAIR_M), mt1 = int((row1 + PAIR_M - 1) / PAIR_M);
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  if ((rc = build_intra(p, 0, ws, g, mt0, mt1))) return rc;
+  if ((rc = build_cross(p, 2, ws, g, mt0, mt1))) return rc;
+  p.nprob = 4;
+  p.split = 2;
+  return launch_gemm(p, st_of(stream), g.wide, g.estore);
 }
 
 int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,

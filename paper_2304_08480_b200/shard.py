@@ -136,6 +136,13 @@ class Plan:
         self.recv = view(_lib.R_RECV, torch.float32)
         self.status = view(_lib.R_STATUS, torch.uint8)[:16]
         self.status_host = torch.empty(16, dtype=torch.uint8, pin_memory=True)
+        self._copy_stream = None
+
+    def copy_stream(self) -> "torch.cuda.Stream":
+        """Side stream for the pipelined device->host gradient copies (created on first use)."""
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(self.device)
+        return self._copy_stream
 
     @property
     def args(self):
@@ -310,12 +317,29 @@ def _account_loss_scope(loss_counters, exchange_counters, b, B, D) -> None:
         loss_counters.release(2 * b * B)
 
 
-def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_sign: bool = False):
+def row_blocks(b: int):
+    """Output row blocks of the single-rank pipelined backward: quarters of the 256-row
+    tiles, the last quarter halved so the exposed device->host tail is short."""
+    tiles = (b + 255) // 256
+    if tiles < 8:
+        return [(0, b)]
+    q = tiles // 4
+    cuts = [0, q, 2 * q, 3 * q, 3 * q + (tiles - 3 * q) // 2, tiles]
+    return [(min(256 * lo, b), min(256 * hi, b)) for lo, hi in zip(cuts, cuts[1:]) if hi > lo]
+
+
+def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_sign: bool = False,
+                     host_out=None):
     """Launch one rank's DisCo fwd+bwd without any host synchronisation.
 
     Inputs must already be CUDA tensors (b x D).  Returns (d_image, d_text,
     plan); the global loss and the non-finite flags are read later with
     ``finish_status(plan)``.  ``disco_step`` is this plus that read-back.
+
+    ``host_out`` = (h_image, h_text) pinned host tensors (single rank): the
+    backward then runs in output row blocks and each block's gradients are
+    copied to the host on ``plan.copy_stream`` while the next block computes
+    (wait on that stream, or call ``finish_status``, before reading them).
     """
     N, n = endpoint.world_size, endpoint.rank
     b, D = local_I.shape
@@ -336,12 +360,27 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         work = endpoint.all_to_all_into(plan.recv, plan.send, async_op=True)
         _lib.call("disco_b200_backward_intra", *plan.args, st)
         work.wait()
-    else:
-        _lib.call("disco_b200_backward_fused", *plan.args, st)
     d_image = torch.empty((b, D), dtype=torch.float32, device=device)
     d_text = torch.empty((b, D), dtype=torch.float32, device=device)
-    _lib.call("disco_b200_combine", *plan.args, t, int(bool(flip_cross_rank_sign)),
-              d_image.data_ptr(), d_text.data_ptr(), D, st)
+    flip = int(bool(flip_cross_rank_sign))
+    if N == 1 and host_out is not None:
+        cs = plan.copy_stream()
+        cur = torch.cuda.current_stream(device)
+        h_image, h_text = host_out
+        for r0, r1 in row_blocks(b):
+            _lib.call("disco_b200_backward_rows", *plan.args, r0, r1, st)
+            _lib.call("disco_b200_combine_rows", *plan.args, t, flip, r0, r1,
+                      d_image.data_ptr(), d_text.data_ptr(), D, st)
+            cs.wait_stream(cur)
+            with torch.cuda.stream(cs):
+                h_image[r0:r1].copy_(d_image[r0:r1], non_blocking=True)
+                h_text[r0:r1].copy_(d_text[r0:r1], non_blocking=True)
+        d_image.record_stream(cs)
+        d_text.record_stream(cs)
+    else:
+        if N == 1:
+            _lib.call("disco_b200_backward_fused", *plan.args, st)
+        _lib.call("disco_b200_combine", *plan.args, t, flip, d_image.data_ptr(), d_text.data_ptr(), D, st)
     if N > 1:
         endpoint.all_gather_into(plan.ce_all, plan.ce)
     _lib.call("disco_b200_loss", *plan.args, 0, st)
@@ -350,6 +389,8 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
 
 def finish_status(plan: Plan) -> float:
     loss, flags = _read_status(plan)
+    if plan._copy_stream is not None:
+        plan._copy_stream.synchronize()
     _raise_on_flags(flags)
     return loss
 
@@ -384,9 +425,17 @@ def disco_step(endpoint, local_I, local_T, t: float, *, loss_counters: Counters 
     if T_dev.dtype != I_dev.dtype:
         T_dev = T_dev.to(I_dev.dtype)
     exchange_counters.alloc(2 * batch * dim)
+    host_out = None
+    if origin != "cuda" and endpoint.world_size == 1:  # pipelined read-back (row blocks)
+        shape = (layout.local_batch, dim)
+        host_out = (torch.empty(shape, dtype=torch.float32, pin_memory=True),
+                    torch.empty(shape, dtype=torch.float32, pin_memory=True))
     d_image, d_text, plan = disco_step_async(endpoint, I_dev, T_dev, t,
-                                             flip_cross_rank_sign=flip_cross_rank_sign)
-    h_image, h_text = _unstage_async(d_image, origin), _unstage_async(d_text, origin)
+                                             flip_cross_rank_sign=flip_cross_rank_sign, host_out=host_out)
+    if host_out is not None:
+        h_image, h_text = host_out
+    else:
+        h_image, h_text = _unstage_async(d_image, origin), _unstage_async(d_text, origin)
     loss = finish_status(plan)
     _account_loss_scope(loss_counters, exchange_counters, layout.local_batch, batch, dim)
     exchange_counters.alloc(batch * dim)

@@ -201,3 +201,19 @@ def test_large_index_space(release_plans):
     assert O.max_rel_error(di[rows].cpu().numpy(), ri) < TOL
     assert O.max_rel_error(dt[rows].cpu().numpy(), rt) < TOL
     assert abs(loss - rl[0]) / rl[0] < TOL
+
+
+@pytest.mark.parametrize("B,D", [(4096, 512), (3072, 256), (2048, 768)])
+def test_host_pipelined_readback_bitwise(B, D):
+    """Host inputs at N=1 take the row-block pipelined backward (disco_b200_backward_rows +
+    combine_rows, device->host copies overlapped); it must equal the device path bit for bit."""
+    I, T = O.synthetic_features(B, D, 3)
+    blocks = P.shard.row_blocks(B)
+    assert blocks[0][0] == 0 and blocks[-1][1] == B
+    dh_i, dh_t, lh = P.disco_step(None, I.astype(np.float32), T.astype(np.float32), 100.0)
+    dd_i, dd_t, ld = P.disco_step(None, dev(I), dev(T), 100.0)
+    assert isinstance(dh_i, np.ndarray) and dh_i.dtype == np.float32
+    assert lh == ld
+    assert np.array_equal(dh_i, dd_i.cpu().numpy()) and np.array_equal(dh_t, dd_t.cpu().numpy())
+    ri, rt, _ = O.clip_grad_full(O.bf16_round(I), O.bf16_round(T), 100.0)
+    assert O.max_rel_error(dh_i, ri) < TOL and O.max_rel_error(dh_t, rt) < TOL

@@ -20,9 +20,9 @@ KERNEL_KEYS = [  # order of the tensor-core launches within one step
     ("logits_kernel<2>", "logits_fwd"),   # forward + E store (canonical shapes)
     ("logits_kernel<0>", "logits_fwd"),   # forward only (recompute path)
     ("logits_kernel<1>", "logits_grad"),  # recompute path only
-    ("gemm_kernel", "gemm_cross"),
-    ("gemm_kernel", "gemm_intra"),
+    ("gemm_kernel", "gemm_backward"),     # single rank: intra + cross in one launch
 ]
+MULTI_RANK_GEMMS = [("gemm_kernel", "gemm_cross"), ("gemm_kernel", "gemm_intra")]
 METRICS = [
     "gpu__time_duration.sum",
     "dram__bytes_read.sum",
@@ -107,7 +107,10 @@ def main():
     ap.add_argument("--rep", required=True)
     ap.add_argument("--launches")
     ap.add_argument("--out", required=True)
+    ap.add_argument("--multi-rank", action="store_true", help="separate cross / intra GEMM launches (N > 1)")
     a = ap.parse_args()
+    if a.multi_rank:
+        KERNEL_KEYS[:] = [k for k in KERNEL_KEYS if k[0] != "gemm_kernel"] + MULTI_RANK_GEMMS
     os.makedirs(a.out, exist_ok=True)
     summ = summarize_rep(a.rep)
     with open(os.path.join(a.out, "ncu_summary.json"), "w") as f:
