@@ -64,11 +64,13 @@ enum disco_region {
   DISCO_R_SEND = 10,   /* f32  [N][2][b][Dp]      cross slabs by destination (all_to_all in) */
   DISCO_R_RECV = 11,   /* f32  [N][2][b][Dp]      cross slabs by source (all_to_all out)     */
   DISCO_R_INTRA = 12,  /* f32  [2][b][Dp]         intra-rank gradient terms                  */
-  DISCO_R_STATUS = 13, /* f64 loss, i32 flags      host-visible step status                   */
+  DISCO_R_STATUS = 13, /* f64 loss, i32 flags, f64 dL/dt   host-visible step status           */
   DISCO_R_SCALE = 14,  /* f32  [2][B/128][b]      group offsets m_g, then
                           f16  [2][B/128][b]      E -> G factors exp2(m_g - lse2) per row and
                           128-column group (canonical shapes; empty otherwise)                */
-  DISCO_R_COUNT = 15
+  DISCO_R_RDOT = 15,    /* f32  [b]               per-row <d_image, I_n> + <d_text, T_n>       */
+  DISCO_R_RDOT_ALL = 16, /* f32  [N][b]           all_gather of DISCO_R_RDOT (alias at N = 1)  */
+  DISCO_R_COUNT = 17
 };
 
 int disco_b200_abi_version(void);
@@ -155,6 +157,16 @@ int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank,
  * DISCO_R_CE when world == 1 or local_only) / (2 * rows) into DISCO_R_STATUS.
  * local_only=1 gives the rank's local_loss (shard.py:140-141). */
 int disco_b200_loss(void* ws, int64_t B, int64_t D, int world, int rank, int local_only, void* stream);
+
+/* Logit-scale gradient (the reference has none).
+ * The logits are bilinear in (I, T), so dL/dt = (<dL/dI, I> + <dL/dT, T>) / (2t)
+ * over the global batch.  _rows writes this rank's per-row terms (with the bf16
+ * features the loss used) into DISCO_R_RDOT; after the host all_gathers them into
+ * DISCO_R_RDOT_ALL (N > 1), _grad sums them in global-row order (f64, independent
+ * of N) and stores dL/dt in the status block (f64 at byte offset 16). */
+int disco_b200_logit_scale_rows(void* ws, int64_t B, int64_t D, int world, int rank, const float* d_image,
+                                const float* d_text, int64_t ld_out, void* stream);
+int disco_b200_logit_scale_grad(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
 
 #ifdef __cplusplus
 }

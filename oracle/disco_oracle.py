@@ -116,6 +116,29 @@ def clip_grad_full(I, T, t: float):
     return d_image, d_text, ((i2t + t2i) / 2.0, i2t, t2i)
 
 
+def dlogit_scale_full(I, T, t: float) -> float:
+    """dL/dt of clip_loss_full (oracle.py:108-127) w.r.t. the logit scale t, f64.
+
+    The reference computes no logit-scale gradient (a documented gap,
+    SPEC.md:243), so this is pinned by finite differences of clip_loss_full
+    (tests/test_oracle_golden.py), not by reference outputs.  With S = t*I@T.T
+    and G = dL/dS = (P_row - Y + P_col - Y) / (2B) (oracle.py:130-200):
+    dL/dt = sum(G * I@T.T).
+    """
+    I = np.asarray(I, dtype=np.float64)
+    T = np.asarray(T, dtype=np.float64)
+    B = I.shape[0]
+    S0 = I @ T.T
+    S = S0 * t
+    P1 = np.exp(S - S.max(axis=1, keepdims=True))
+    P1 /= P1.sum(axis=1, keepdims=True)
+    P2 = np.exp(S - S.max(axis=0, keepdims=True))
+    P2 /= P2.sum(axis=0, keepdims=True)
+    G = P1 + P2
+    G[np.arange(B), np.arange(B)] -= 2.0
+    return float((G * S0).sum() / (2.0 * B))
+
+
 def clip_stats_blocked(I, T, t: float, block: int = 2048):
     """Row/column softmax statistics of S = t*I@T.T without materialising S.
 

@@ -7,6 +7,7 @@ arguments and exceptions, computed by hand-written sm_100a kernels
 (tcgen05/TMEM/TMA) behind a C ABI, with NCCL collectives over NVLink.
 """
 
+from .autograd import DiscoCLIPLoss, DiscoLossFunction, disco_loss
 from .counters import Counters, tracking
 from .errors import (
     CollectiveContractError,
@@ -25,7 +26,9 @@ from .shard import (
     disco_step,
     disco_step_async,
     finish_status,
+    finish_status_with_dlogit,
     local_labels,
+    logit_scale_grad_async,
     local_loss_and_grads,
     shard_slice,
 )
@@ -38,6 +41,8 @@ __all__ = [
     "Counters",
     "DeadlockError",
     "DegenerateInputError",
+    "DiscoCLIPLoss",
+    "DiscoLossFunction",
     "DomainError",
     "LayoutError",
     "LocalEndpoint",
@@ -49,11 +54,14 @@ __all__ = [
     "ShardLayout",
     "SingleEndpoint",
     "TrainingDivergenceError",
+    "disco_loss",
     "disco_step",
     "disco_step_async",
     "finish_status",
+    "finish_status_with_dlogit",
     "local_labels",
     "local_loss_and_grads",
+    "logit_scale_grad_async",
     "run_ranks",
     "shard_slice",
     "tracking",

@@ -25,7 +25,7 @@ F32, BF16, F64, F16 = 0, 1, 2, 3
 
 # workspace regions (disco_region)
 R_PACK, R_GATHER, R_FEAT, R_FEAT16, R_STATS, R_ROWS, R_CE, R_CE_ALL, R_G, R_XPART, R_SEND, R_RECV, \
-    R_INTRA, R_STATUS, R_SCALE = range(15)
+    R_INTRA, R_STATUS, R_SCALE, R_RDOT, R_RDOT_ALL = range(17)
 
 _i64 = ctypes.c_int64
 _int = ctypes.c_int
@@ -51,6 +51,8 @@ SIGNATURES = {
     "disco_b200_combine_rows": [_vp, _i64, _i64, _int, _int, _f32, _int, _i64, _i64, _vp, _vp, _i64, _vp],
     "disco_b200_contribution": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _vp, _i64, _vp],
     "disco_b200_loss": [_vp, _i64, _i64, _int, _int, _int, _vp],
+    "disco_b200_logit_scale_rows": [_vp, _i64, _i64, _int, _int, _vp, _vp, _i64, _vp],
+    "disco_b200_logit_scale_grad": [_vp, _i64, _i64, _int, _int, _f32, _vp],
 }
 _RESTYPES = {"disco_b200_last_error": ctypes.c_char_p, "disco_b200_launch_count": _i64}
 

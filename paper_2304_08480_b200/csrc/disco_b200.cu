@@ -95,6 +95,7 @@ struct Status {
   double loss;
   int flags;
   int pad;
+  double dlogit;             // dL/d(logit scale), disco_b200_logit_scale_grad
   double loss_partial[128];  // loss_partial_kernel scratch (LOSS_BLOCKS)
 };
 
@@ -1232,6 +1233,54 @@ __global__ void loss_partial_kernel(const float* ce_all, int N, int b, double* p
   if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
 }
 
+// dL/dt per local row r: <d_image[r], I_n[r]> + <d_text[r], T_n[r]> with the bf16 features the loss
+// used (pack region [2][b][Dp]); one warp per row, fixed lane order, f64 accumulation.
+__global__ void rowdot_kernel(const float* d_image, const float* d_text, int64_t ld_out, const __nv_bfloat16* pack,
+                              int b, int D, int Dp, float* rdot) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= b) return;
+  const __nv_bfloat16* I = pack + int64_t(warp) * Dp;
+  const __nv_bfloat16* T = pack + (int64_t(b) + warp) * Dp;
+  const float* di = d_image + int64_t(warp) * ld_out;
+  const float* dt = d_text + int64_t(warp) * ld_out;
+  double acc = 0.0;
+  for (int c = lane; c < D; c += 32)
+    acc += double(di[c]) * double(__bfloat162float(I[c])) + double(dt[c]) * double(__bfloat162float(T[c]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) rdot[warp] = float(acc);
+}
+
+// Fixed-order f64 sum of n floats: LOSS_BLOCKS contiguous slices, then a tree (as the loss).
+__global__ void rowsum_partial_kernel(const float* x, int64_t n, double* partial) {
+  __shared__ double red[256];
+  const int64_t per = (n + LOSS_BLOCKS - 1) / LOSS_BLOCKS;
+  const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
+  double acc = 0.0;
+  for (int64_t f = lo + threadIdx.x; f < hi; f += blockDim.x) acc += double(x[f]);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void dlogit_final_kernel(const double* partial, double scale, Status* status) {
+  __shared__ double red[LOSS_BLOCKS];
+  red[threadIdx.x] = partial[threadIdx.x];
+  __syncthreads();
+  for (int w = LOSS_BLOCKS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    status->dlogit = red[0] * scale;
+    if (!isfinite(status->dlogit)) status->flags |= FLAG_GRAD_NONFINITE;
+  }
+}
+
 __global__ void loss_final_kernel(const double* partial, int64_t rows2, Status* status) {
   __shared__ double red[LOSS_BLOCKS];
   red[threadIdx.x] = partial[threadIdx.x];
@@ -1350,6 +1399,8 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   len[DISCO_R_RECV] = N > 1 ? N * 2 * b * Dp * 4 : 0;
   len[DISCO_R_INTRA] = 2 * int64_t(g->ksplit) * b * Dp * 4;
   len[DISCO_R_STATUS] = int64_t(sizeof(Status));
+  len[DISCO_R_RDOT] = b * 4;
+  len[DISCO_R_RDOT_ALL] = N > 1 ? N * b * 4 : 0;
   len[DISCO_R_SCALE] = g->estore ? 2 * int64_t(g->groups) * b * (4 + 2) : 0;  // f32 m_g, then f16 scales
   int64_t off = 0;
   for (int r = 0; r < DISCO_R_COUNT; ++r) {
@@ -1364,6 +1415,8 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
     g->len[DISCO_R_GATHER] = g->len[DISCO_R_PACK];
     g->off[DISCO_R_RECV] = g->off[DISCO_R_SEND];
     g->len[DISCO_R_RECV] = g->len[DISCO_R_SEND];
+    g->off[DISCO_R_RDOT_ALL] = g->off[DISCO_R_RDOT];
+    g->len[DISCO_R_RDOT_ALL] = g->len[DISCO_R_RDOT];
   }
   g->total = off;
   return DISCO_OK;
@@ -1958,6 +2011,36 @@ int disco_b200_loss(void* ws, int64_t B, int64_t D, int world, int rank, int loc
   loss_partial_kernel<<<LOSS_BLOCKS, 256, 0, st>>>(region<float>(ws, g, local ? DISCO_R_CE : DISCO_R_CE_ALL), nw,
                                                    int(g.b), status->loss_partial);
   loss_final_kernel<<<1, LOSS_BLOCKS, 0, st>>>(status->loss_partial, int64_t(2) * nw * g.b, status);
+  count_launch(2);
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_logit_scale_rows(void* ws, int64_t B, int64_t D, int world, int rank, const float* d_image,
+                                const float* d_text, int64_t ld_out, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (ld_out < D) return fail(DISCO_SHAPE_ERROR, "output row stride smaller than D");
+  const int64_t threads = g.b * 32;
+  rowdot_kernel<<<int((threads + 255) / 256), 256, 0, st_of(stream)>>>(
+      d_image, d_text, ld_out, region<__nv_bfloat16>(ws, g, DISCO_R_PACK), int(g.b), int(D), int(g.Dp),
+      region<float>(ws, g, DISCO_R_RDOT));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_logit_scale_grad(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
+  cudaStream_t st = st_of(stream);
+  Status* status = region<Status>(ws, g, DISCO_R_STATUS);
+  rowsum_partial_kernel<<<LOSS_BLOCKS, 256, 0, st>>>(region<float>(ws, g, DISCO_R_RDOT_ALL), g.B,
+                                                     status->loss_partial);
+  dlogit_final_kernel<<<1, LOSS_BLOCKS, 0, st>>>(status->loss_partial, 0.5 / double(t), status);
   count_launch(2);
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;

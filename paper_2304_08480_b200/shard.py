@@ -134,8 +134,10 @@ class Plan:
         self.ce_all = view(_lib.R_CE_ALL, torch.float32)
         self.send = view(_lib.R_SEND, torch.float32)
         self.recv = view(_lib.R_RECV, torch.float32)
-        self.status = view(_lib.R_STATUS, torch.uint8)[:16]
-        self.status_host = torch.empty(16, dtype=torch.uint8, pin_memory=True)
+        self.rdot = view(_lib.R_RDOT, torch.float32)
+        self.rdot_all = view(_lib.R_RDOT_ALL, torch.float32)
+        self.status = view(_lib.R_STATUS, torch.uint8)[:24]
+        self.status_host = torch.empty(24, dtype=torch.uint8, pin_memory=True)
         self._copy_stream = None
 
     def copy_stream(self) -> "torch.cuda.Stream":
@@ -221,12 +223,14 @@ def _stream_ptr(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def _read_status(plan: Plan):
+def _read_status(plan: Plan, with_dlogit: bool = False):
     plan.status_host.copy_(plan.status, non_blocking=True)
     torch.cuda.current_stream(plan.device).synchronize()
     raw = plan.status_host.numpy()
     loss = float(raw[:8].view(np.float64)[0])
     flags = int(raw[8:12].view(np.int32)[0])
+    if with_dlogit:
+        return loss, flags, float(raw[16:24].view(np.float64)[0])
     return loss, flags
 
 
@@ -393,6 +397,25 @@ def finish_status(plan: Plan) -> float:
         plan._copy_stream.synchronize()
     _raise_on_flags(flags)
     return loss
+
+
+def logit_scale_grad_async(endpoint, plan: Plan, d_image, d_text, t: float) -> None:
+    """Queue dL/dt after ``disco_step_async``: per-row
+    <d, features> terms, all_gather across ranks (N > 1), fixed-order sum.  Read it
+    with ``finish_status_with_dlogit``."""
+    st = _stream_ptr(plan.device)
+    _lib.call("disco_b200_logit_scale_rows", *plan.args, d_image.data_ptr(), d_text.data_ptr(),
+              d_image.stride(0), st)
+    if plan.world > 1:
+        endpoint.all_gather_into(plan.rdot_all, plan.rdot)
+    _lib.call("disco_b200_logit_scale_grad", *plan.args, t, st)
+
+
+def finish_status_with_dlogit(plan: Plan):
+    """(global loss, dL/dt) after ``logit_scale_grad_async``; raises on non-finite flags."""
+    loss, flags, dlogit = _read_status(plan, with_dlogit=True)
+    _raise_on_flags(flags)
+    return loss, dlogit
 
 
 def disco_step(endpoint, local_I, local_T, t: float, *, loss_counters: Counters | None = None,

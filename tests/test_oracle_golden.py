@@ -103,3 +103,23 @@ def test_bf16_round_is_round_to_nearest_even():
     ours = O.bf16_round(x)
     ref = torch.from_numpy(x).to(torch.bfloat16).to(torch.float32).numpy()
     assert ours.tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("t", [1.0, 14.2857, 100.0])
+@pytest.mark.parametrize("correlated", [False, True])
+def test_dlogit_scale_oracle_matches_finite_difference(t, correlated):
+    """oracle.dlogit_scale_full (the logit-scale gradient the reference lacks)
+    against a central difference of the reference-pinned clip_loss_full."""
+    I, T = O.synthetic_features(64, 16, 7, correlated=correlated, bf16=False)
+    h = 1e-5 * t
+    fd = (O.clip_loss_full(I, T, t + h)[0] - O.clip_loss_full(I, T, t - h)[0]) / (2 * h)
+    g = O.dlogit_scale_full(I, T, t)
+    assert abs(g - fd) <= 1e-6 * max(1.0, abs(fd)), (g, fd)
+
+
+def test_dlogit_scale_euler_identity():
+    """dL/dt = (<dL/dI, I> + <dL/dT, T>) / (2t) (the identity the device path uses)."""
+    I, T = O.synthetic_features(48, 8, 2, bf16=False)
+    t = 10.0
+    di, dt, _ = O.clip_grad_full(I, T, t)
+    assert abs(O.dlogit_scale_full(I, T, t) - ((di * I).sum() + (dt * T).sum()) / (2 * t)) < 1e-12
