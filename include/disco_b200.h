@@ -168,6 +168,15 @@ int disco_b200_logit_scale_rows(void* ws, int64_t B, int64_t D, int world, int r
                                 const float* d_text, int64_t ld_out, void* stream);
 int disco_b200_logit_scale_grad(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
 
+/* Tower side of the two-tower trainer (reference towers.py:148-157):
+ * row L2 normalisation of raw tower outputs (matrix.py:165-176) and its backward
+ * (matrix.py:178-195), fp32, one warp per row.  flags (device int, may be NULL):
+ * bit0 non-finite values, bit1 a row norm below 1e-12 (DegenerateInputError). */
+int disco_b200_l2norm_rows(const float* raw, int64_t ld_raw, int64_t rows, int64_t D, float* out, int64_t ld_out,
+                           float* norms, int* flags, void* stream);
+int disco_b200_l2norm_rows_backward(const float* raw, int64_t ld_raw, const float* grad, int64_t ld_grad, int64_t rows,
+                                    int64_t D, float* out, int64_t ld_out, int* flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

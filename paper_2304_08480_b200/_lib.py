@@ -53,6 +53,8 @@ SIGNATURES = {
     "disco_b200_loss": [_vp, _i64, _i64, _int, _int, _int, _vp],
     "disco_b200_logit_scale_rows": [_vp, _i64, _i64, _int, _int, _vp, _vp, _i64, _vp],
     "disco_b200_logit_scale_grad": [_vp, _i64, _i64, _int, _int, _f32, _vp],
+    "disco_b200_l2norm_rows": [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp],
+    "disco_b200_l2norm_rows_backward": [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp],
 }
 _RESTYPES = {"disco_b200_last_error": ctypes.c_char_p, "disco_b200_launch_count": _i64}
 

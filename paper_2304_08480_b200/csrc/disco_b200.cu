@@ -1251,6 +1251,65 @@ __global__ void rowdot_kernel(const float* d_image, const float* d_text, int64_t
   if (lane == 0) rdot[warp] = float(acc);
 }
 
+// Tower-side row normalisation (reference matrix.py:165-176, 178-195), one warp per row, fp32 I/O,
+// f64 norms.  flags (optional): bit0 non-finite input, bit1 row norm below 1e-12 (DegenerateInputError).
+constexpr double NORM_EPSILON = 1e-12;
+__global__ void l2norm_rows_kernel(const float* raw, int64_t ld_raw, int rows, int D, float* out, int64_t ld_out,
+                                   float* norms, int* flags) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* x = raw + int64_t(r) * ld_raw;
+  double ss = 0.0;
+  bool bad = false;
+  for (int c = lane; c < D; c += 32) {
+    const float v = x[c];
+    bad |= !isfinite(v);
+    ss += double(v) * double(v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const double n = sqrt(ss);
+  if (lane == 0) {
+    if (norms) norms[r] = float(n);
+    if (flags && (bad || !isfinite(n))) atomicOr(flags, 1);
+    if (flags && n < NORM_EPSILON) atomicOr(flags, 2);
+  }
+  const double inv = 1.0 / n;
+  float* y = out + int64_t(r) * ld_out;
+  for (int c = lane; c < D; c += 32) y[c] = float(double(x[c]) * inv);
+}
+
+// d_raw = (g - (u . g) u) / ||x||, u = x / ||x||  (the backward of l2norm_rows)
+__global__ void l2norm_rows_backward_kernel(const float* raw, int64_t ld_raw, const float* grad, int64_t ld_grad,
+                                            int rows, int D, float* out, int64_t ld_out, int* flags) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* x = raw + int64_t(r) * ld_raw;
+  const float* g = grad + int64_t(r) * ld_grad;
+  double ss = 0.0, xg = 0.0;
+  for (int c = lane; c < D; c += 32) {
+    ss += double(x[c]) * double(x[c]);
+    xg += double(x[c]) * double(g[c]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    xg += __shfl_xor_sync(0xffffffffu, xg, o);
+  }
+  const double n = sqrt(ss);
+  if (lane == 0 && flags && n < NORM_EPSILON) atomicOr(flags, 2);
+  const double inner = xg / n;  // u . g
+  bool bad = false;
+  float* y = out + int64_t(r) * ld_out;
+  for (int c = lane; c < D; c += 32) {
+    const double u = double(x[c]) / n;
+    const float v = float((double(g[c]) - inner * u) / n);
+    bad |= !isfinite(v);
+    y[c] = v;
+  }
+  if (flags && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1);
+}
+
 // Fixed-order f64 sum of n floats: LOSS_BLOCKS contiguous slices, then a tree (as the loss).
 __global__ void rowsum_partial_kernel(const float* x, int64_t n, double* partial) {
   __shared__ double red[256];
@@ -2042,6 +2101,29 @@ int disco_b200_logit_scale_grad(void* ws, int64_t B, int64_t D, int world, int r
                                                      status->loss_partial);
   dlogit_final_kernel<<<1, LOSS_BLOCKS, 0, st>>>(status->loss_partial, 0.5 / double(t), status);
   count_launch(2);
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_l2norm_rows(const float* raw, int64_t ld_raw, int64_t rows, int64_t D, float* out, int64_t ld_out,
+                           float* norms, int* flags, void* stream) {
+  if (rows < 0 || D < 1 || ld_raw < D || ld_out < D) return fail(DISCO_SHAPE_ERROR, "bad l2norm geometry");
+  if (rows == 0) return DISCO_OK;
+  l2norm_rows_kernel<<<int((rows * 32 + 255) / 256), 256, 0, st_of(stream)>>>(raw, ld_raw, int(rows), int(D), out,
+                                                                              ld_out, norms, flags);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_l2norm_rows_backward(const float* raw, int64_t ld_raw, const float* grad, int64_t ld_grad, int64_t rows,
+                                    int64_t D, float* out, int64_t ld_out, int* flags, void* stream) {
+  if (rows < 0 || D < 1 || ld_raw < D || ld_grad < D || ld_out < D)
+    return fail(DISCO_SHAPE_ERROR, "bad l2norm backward geometry");
+  if (rows == 0) return DISCO_OK;
+  l2norm_rows_backward_kernel<<<int((rows * 32 + 255) / 256), 256, 0, st_of(stream)>>>(
+      raw, ld_raw, grad, ld_grad, int(rows), int(D), out, ld_out, flags);
+  count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
 }

@@ -1,0 +1,71 @@
+"""GPU: the two-tower trainer and the measured footprint (row 3)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2304_08480_b200 import costs, towers
+from paper_2304_08480_b200.errors import DegenerateInputError
+
+pytestmark = pytest.mark.gpu
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_towers.npz"))
+
+
+def test_l2norm_kernels_match_reference_formulas():
+    rng = np.random.default_rng(0)
+    raw = rng.standard_normal((300, 77)) * 3.0
+    up = rng.standard_normal((300, 77))
+    x = torch.tensor(raw, dtype=torch.float32, device="cuda")
+    g = torch.tensor(up, dtype=torch.float32, device="cuda")
+    out, norms = towers.l2_normalize_rows(x)
+    xf = raw.astype(np.float32).astype(np.float64)
+    n = np.linalg.norm(xf, axis=1, keepdims=True)
+    assert np.abs(out.cpu().numpy() - xf / n).max() < 1e-6
+    assert np.abs(norms.cpu().numpy() - n[:, 0]).max() < 1e-5
+    d = towers.l2_normalize_rows_backward(x, g).cpu().numpy()
+    u = xf / n
+    gf = up.astype(np.float32).astype(np.float64)
+    ref = (gf - (u * gf).sum(1, keepdims=True) * u) / n
+    assert np.abs(d - ref).max() < 1e-6
+    with pytest.raises(DegenerateInputError):
+        towers.l2_normalize_rows(torch.zeros((4, 8), device="cuda"))
+
+
+def _run(mode, world, steps=50):
+    ds = towers.PairedDataset(G["ds_image"], G["ds_text"], 0)
+    p = towers.TowerParams(G["W0_image"], G["W0_text"], float(G["t"]))
+    cfg = towers.TrainConfig(global_batch=16, world_size=world, steps=steps, learning_rate=0.2, seed=0, mode=mode)
+    return np.array([loss for _, loss in towers.train_run(cfg, ds, p)]), p
+
+
+def test_naive_trajectory_tracks_reference_f64():
+    traj, p = _run("naive", 1)
+    ref = G["traj_naive"]
+    assert abs(traj[0] - ref[0]) / ref[0] < 1e-3          # README golden 16.915930208126888
+    # D = 4 features rounded to bf16 move each logit by ~t * 2^-9: ~1% drift over the first steps
+    assert np.all(np.abs(traj[:5] - ref[:5]) / ref[:5] < 2e-2)
+    assert traj[-1] < 0.2 * traj[0] and np.isfinite(traj).all()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_disco_and_naive_trajectories_coincide(world):
+    naive, pn = _run("naive", 1, steps=20)
+    disco, pd = _run("disco", world, steps=20)
+    assert np.abs(naive - disco).max() <= 1e-5 * np.abs(naive).max(), (naive, disco)
+    assert torch.allclose(pn.W_image, pd.W_image, rtol=1e-4, atol=1e-6)
+    assert torch.allclose(pn.W_text, pd.W_text, rtol=1e-4, atol=1e-6)
+
+
+def test_measured_footprint_scales_as_b_squared_over_n():
+    B, D = 8192, 256
+    reps = {N: costs.measured_footprint("disco", B, N, D) for N in (1, 2, 4, 8)}
+    naive = costs.measured_footprint("naive", B, 1, D)
+    for N, r in reps.items():
+        b = B // N
+        assert r.loss_elements == 2 * b * B and r.loss_flops == 4 * b * B * D
+        assert r.bytes >= 2 * 2 * b * B  # the f16 E blocks alone
+    assert reps[1].bytes > reps[2].bytes > reps[4].bytes > reps[8].bytes
+    assert reps[8].bytes < reps[1].bytes / 4
+    assert naive.loss_elements == B * B and naive.bytes >= 4 * B * B
