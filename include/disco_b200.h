@@ -65,15 +65,19 @@ enum disco_region {
   DISCO_R_RECV = 11,   /* f32  [N][2][b][Dp]      cross slabs by source (all_to_all out)     */
   DISCO_R_INTRA = 12,  /* f32  [2][b][Dp]         intra-rank gradient terms                  */
   DISCO_R_STATUS = 13, /* f64 loss, i32 flags, f64 dL/dt   host-visible step status           */
-  DISCO_R_SCALE = 14,  /* f32  [2][B/128][b]      group offsets m_g, then
-                          f16  [2][B/128][b]      E -> G factors exp2(m_g - lse2) per row and
-                          128-column group (canonical shapes; empty otherwise)                */
+  DISCO_R_SCALE = 14,  /* f32  [2][B/64][b]       group offsets m_g, then
+                          f16  [2][B/64][b]       E -> G factors exp2(m_g - lse2) per row and
+                          64-column group (canonical shapes; empty otherwise)                 */
   DISCO_R_RDOT = 15,    /* f32  [b]               per-row <d_image, I_n> + <d_text, T_n>       */
   DISCO_R_RDOT_ALL = 16, /* f32  [N][b]           all_gather of DISCO_R_RDOT (alias at N = 1)  */
   DISCO_R_COUNT = 17
 };
 
 int disco_b200_abi_version(void);
+
+/* Profiling experiments only (never needed for correct results): replaces the
+ * DISCO_DEBUG_FLAGS bits read at load time, returns the previous value. */
+int disco_b200_set_experiment_flags(int flags);
 const char* disco_b200_last_error(void);
 
 /* Number of CUDA kernels this library has launched in this process

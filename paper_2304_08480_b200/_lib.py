@@ -35,6 +35,7 @@ _f32 = ctypes.c_float
 # name -> argtypes (restype is int unless listed in _RESTYPES)
 SIGNATURES = {
     "disco_b200_abi_version": [],
+    "disco_b200_set_experiment_flags": [_int],
     "disco_b200_last_error": [],
     "disco_b200_launch_count": [],
     "disco_b200_workspace_bytes": [_i64, _i64, _int, _int, ctypes.POINTER(_i64)],

@@ -66,7 +66,7 @@ constexpr int NUM_EPI_WARPS = 8;
 // E-operand GEMMs add 4 transform warps (10-13) that rescale each A stage in smem (E -> G).
 constexpr int NUM_XF_WARPS = 4;
 constexpr int NUM_THREADS_XF = NUM_THREADS + 32 * NUM_XF_WARPS;
-constexpr int GROUP_COLS = 128;   // E offset granularity: one exp2 offset per (row, 128-column group)
+constexpr int GROUP_COLS = 64;    // E offset granularity: one exp2 offset per (row, 64-column group)
 constexpr int TMEM_COLS = 512;    // 2 accumulators of 128 lanes x 256 fp32 columns
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -77,14 +77,21 @@ struct SmemCtl {
   uint64_t tfull[2];       // both: accumulator ready (multicast commit)
   uint64_t tempty[2];      // leader: both CTAs' epilogues drained the accumulator
   uint64_t xfull[STAGES];  // leader: both CTAs' transform warps rescaled the stage (E-operand GEMMs)
+  uint64_t afull[8];       // leader: resident A slice k of the unit landed (logits kernel, Dp <= 512)
+  uint64_t aempty[8];      // both: the unit's last MMA on A slice k retired
   uint32_t tmem_base;
 };
 // Epilogue staging: 8 warps x STAGING_BUFS x (32 rows x 128 B), swizzled like TMA SWIZZLE_128B.
 constexpr int STAGING_TILE = 32 * 128;
 constexpr int STAGING_BUFS = 1;
 constexpr int STAGING_BYTES = NUM_EPI_WARPS * STAGING_BUFS * STAGING_TILE;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(TILE_RING_BYTES) + STAGING_BYTES + 256;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(TILE_RING_BYTES) + STAGING_BYTES + 512;
+// Logits kernel with a resident A block (Dp <= 512): A = 8 slices x 16 KiB, then a 4-stage B ring.
+constexpr int ARES_SLICES = 8;
+constexpr int ARES_B_STAGES = 4;
+static_assert(ARES_SLICES * A_STAGE_BYTES + ARES_B_STAGES * B_STAGE_BYTES == TILE_RING_BYTES, "A-resident layout");
 static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory limit");
+static_assert(sizeof(uint64_t) * 46 + 4 <= 512, "control block");
 
 // -------------------------------------------------------- status flag bits
 constexpr int FLAG_INPUT_NONFINITE = 1;
@@ -211,23 +218,33 @@ __device__ __forceinline__ uint8_t* smem_base(uint8_t* raw) {
 
 // Leader-side MMA issue for one unit: nk k-blocks of BK, 4 UMMAs per N tile each.
 // NB = 2: the same A stage feeds two N tiles into accumulators d_tmem and d_tmem + BN.
+// Called by the whole (leader) MMA warp: barrier waits and descriptor arithmetic are
+// warp-uniform (uniform registers), one elected lane issues the UMMAs and the commits.
+// Successive K=16 steps advance the descriptor start address by 32 B (K-major) or 2 KiB
+// (MN-major), i.e. by 2 or 128 in the descriptor's 16-byte units.
 template <int NB, bool XF = false>
 __device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<Ring<NB>::STAGES>& pipe, int nk,
                                          uint32_t d_tmem, uint32_t idesc, int a_mn, int b_mn) {
+  const uint64_t a_step = a_mn ? 128 : 2, b_step = b_mn ? 128 : 2;
   for (int kb = 0; kb < nk; ++kb) {
     ptx::mbar_wait(XF ? &ctl->xfull[pipe.stage] : &ctl->full[pipe.stage], pipe.phase);
     ptx::tc_fence_after();
     const uint32_t a_base = ptx::smem_u32(tiles + pipe.stage * Ring<NB>::STAGE_BYTES);
     const uint32_t b_base = a_base + A_STAGE_BYTES;
+    const uint64_t ad0 = operand_desc(a_base, a_mn, 0);
+    uint64_t bd0[NB];
 #pragma unroll
-    for (int kk = 0; kk < BK / 16; ++kk) {
-      const uint64_t ad = operand_desc(a_base, a_mn, kk);
+    for (int j = 0; j < NB; ++j) bd0[j] = operand_desc(b_base + j * B_STAGE_BYTES, b_mn, 0);
+    if (ptx::elect_one()) {
 #pragma unroll
-      for (int j = 0; j < NB; ++j)
-        ptx::umma_f16_pair(d_tmem + j * BN, ad, operand_desc(b_base + j * B_STAGE_BYTES, b_mn, kk), idesc,
-                           (kb | kk) != 0);
+      for (int kk = 0; kk < BK / 16; ++kk) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          ptx::umma_f16_pair(d_tmem + j * BN, ad0 + kk * a_step, bd0[j] + kk * b_step, idesc, (kb | kk) != 0);
+      }
+      ptx::umma_commit_pair(&ctl->empty[pipe.stage], 0x3);  // both CTAs' smem slots free
     }
-    ptx::umma_commit_pair(&ctl->empty[pipe.stage], 0x3);  // both CTAs' smem slots free
+    __syncwarp();
     pipe.advance();
   }
 }
@@ -280,6 +297,10 @@ __device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane
       ptx::mbar_init(&ctl->tempty[i], 2 * NUM_EPI_WARPS);  // every epilogue warp of both CTAs
     }
     for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&ctl->xfull[s], 2 * NUM_XF_WARPS);
+    for (int s = 0; s < ARES_SLICES; ++s) {
+      ptx::mbar_init(&ctl->afull[s], 1);
+      ptx::mbar_init(&ctl->aempty[s], 1);
+    }
     ptx::fence_barrier_init();
   }
   if (warp == 1) {
@@ -324,7 +345,11 @@ __device__ __forceinline__ void release_accumulator(SmemCtl* ctl, int buf, int l
 // so the logits are never recomputed.
 enum { KIND_FWD = 0, KIND_GRAD = 1, KIND_FWDE = 2 };
 
-template <int KIND>
+// ARES: the unit's A block (its 256 local rows x Dp, Dp <= 512) stays resident in smem for all
+// column tiles of the unit and only B streams through a 4-stage ring; A slice k of the next unit
+// is reloaded as soon as the unit's last tile has consumed it.  Halves the TMA fill traffic and
+// cuts smem traffic per MMA from ~128 to ~96 B/clk/SM (the narrow 256-column tile is smem-bound).
+template <int KIND, bool ARES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     logits_kernel(const __grid_constant__ LogitsParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -388,34 +413,84 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           ptx::tma_prefetch_2d(&p.b_map[dir], kb * BK, col0);
         }
       };
-      for (int u = pair; u < num_units; u += npairs) {
-        int dir, rt, ch, t0;
-        decode(u, dir, rt, ch, t0);
-        const int a_row = p.rank * p.b + rt * PAIR_M + crank * BM;
-        for (int ti = 0; ti < tiles_per_unit; ++ti) {
-          const int col0 = ch * p.chunk_cols + (t0 + ti) * BN + crank * (BN / 2);
-          for (int kb = 0; kb < nk; ++kb) {
-            uint32_t bar;
-            uint8_t* st = producer_acquire<1>(ctl, tiles, pipe, leader, bar);
-            ptx::tma_load_2d_pair(st, &p.a_map[dir], bar, kb * BK, a_row, ptx::kEvictLast);
-            ptx::tma_load_2d_pair(st + A_STAGE_BYTES, &p.b_map[dir], bar, kb * BK, col0, ptx::kEvictLast);
-            pipe.advance();
+      if constexpr (ARES) {
+        Pipe<ARES_B_STAGES> bp;
+        uint8_t* bring = tiles + ARES_SLICES * A_STAGE_BYTES;
+        uint32_t uphase = 0;
+        for (int u = pair; u < num_units; u += npairs, uphase ^= 1) {
+          int dir, rt, ch, t0;
+          decode(u, dir, rt, ch, t0);
+          const int a_row = p.rank * p.b + rt * PAIR_M + crank * BM;
+          for (int ti = 0; ti < tiles_per_unit; ++ti) {
+            const int col0 = ch * p.chunk_cols + (t0 + ti) * BN + crank * (BN / 2);
+            for (int kb = 0; kb < nk; ++kb) {
+              if (ti == 0) {  // this unit's A slice kb, once the previous unit released it
+                ptx::mbar_wait(&ctl->aempty[kb], uphase ^ 1);
+                if (leader) ptx::mbar_arrive_expect_tx(&ctl->afull[kb], 2 * A_STAGE_BYTES);
+                ptx::tma_load_2d_pair(tiles + kb * A_STAGE_BYTES, &p.a_map[dir], ptx::map_to_rank(&ctl->afull[kb], 0),
+                                      kb * BK, a_row, ptx::kEvictLast);
+              }
+              ptx::mbar_wait(&ctl->empty[bp.stage], bp.phase ^ 1);
+              if (leader) ptx::mbar_arrive_expect_tx(&ctl->full[bp.stage], 2 * B_STAGE_BYTES);
+              ptx::tma_load_2d_pair(bring + bp.stage * B_STAGE_BYTES, &p.b_map[dir],
+                                    ptx::map_to_rank(&ctl->full[bp.stage], 0), kb * BK, col0, ptx::kEvictLast);
+              bp.advance();
+            }
+          }
+        }
+      } else {
+        for (int u = pair; u < num_units; u += npairs) {
+          int dir, rt, ch, t0;
+          decode(u, dir, rt, ch, t0);
+          const int a_row = p.rank * p.b + rt * PAIR_M + crank * BM;
+          for (int ti = 0; ti < tiles_per_unit; ++ti) {
+            const int col0 = ch * p.chunk_cols + (t0 + ti) * BN + crank * (BN / 2);
+            for (int kb = 0; kb < nk; ++kb) {
+              uint32_t bar;
+              uint8_t* st = producer_acquire<1>(ctl, tiles, pipe, leader, bar);
+              ptx::tma_load_2d_pair(st, &p.a_map[dir], bar, kb * BK, a_row, ptx::kEvictLast);
+              ptx::tma_load_2d_pair(st + A_STAGE_BYTES, &p.b_map[dir], bar, kb * BK, col0, ptx::kEvictLast);
+              pipe.advance();
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader CTA)
+    if (leader) {  // ---------------- MMA issuer (leader CTA, whole warp; one elected lane issues)
       constexpr uint32_t idesc = ptx::instr_desc_f16(PAIR_M, BN, 1, 1, 0, 0);  // bf16 x bf16, both K-major
       Pipe pipe;
-      uint32_t it = 0;
-      for (int u = pair; u < num_units; u += npairs) {
+      Pipe<ARES_B_STAGES> bp;
+      uint8_t* bring = tiles + ARES_SLICES * A_STAGE_BYTES;
+      uint32_t it = 0, uphase = 0;
+      for (int u = pair; u < num_units; u += npairs, uphase ^= 1) {
         for (int ti = 0; ti < tiles_per_unit; ++ti, ++it) {
           const uint32_t buf = it & 1, use = it >> 1;
           ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
           ptx::tc_fence_after();
-          mma_tile<1>(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, 0, 0);
-          ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
+          const uint32_t d_tmem = ctl->tmem_base + buf * BN;
+          if constexpr (ARES) {
+            for (int kb = 0; kb < nk; ++kb) {
+              if (ti == 0) ptx::mbar_wait(&ctl->afull[kb], uphase);
+              ptx::mbar_wait(&ctl->full[bp.stage], bp.phase);
+              ptx::tc_fence_after();
+              const uint64_t ad0 = operand_desc(ptx::smem_u32(tiles + kb * A_STAGE_BYTES), 0, 0);
+              const uint64_t bd0 = operand_desc(ptx::smem_u32(bring + bp.stage * B_STAGE_BYTES), 0, 0);
+              if (ptx::elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk)
+                  ptx::umma_f16_pair(d_tmem, ad0 + 2 * kk, bd0 + 2 * kk, idesc, (kb | kk) != 0);
+                ptx::umma_commit_pair(&ctl->empty[bp.stage], 0x3);
+                if (ti == tiles_per_unit - 1) ptx::umma_commit_pair(&ctl->aempty[kb], 0x3);
+              }
+              __syncwarp();
+              bp.advance();
+            }
+          } else {
+            mma_tile<1>(ctl, tiles, pipe, nk, d_tmem, idesc, 0, 0);
+          }
+          if (ptx::elect_one()) ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
+          __syncwarp();
         }
       }
     }
@@ -496,25 +571,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
           }
         } else if (KIND == KIND_FWDE) {
-          // canonical chunks: this warp's 128 columns are entirely inside or past the chunk
+          // canonical chunks: this warp's 128 columns are entirely inside or past the chunk.
+          // One TMEM pass (TMEM reads are 64 B/clk/SM: a second pass would pace the tile at the
+          // MMA time): each 64-column group is loaded once, its max taken in registers, then
+          // E = exp2(y - m_g) packed to f16 and stored as one 32 x 64 slice.
           if (col0 < chunk_hi) {  // warp-uniform
-            float v[32];
-            float cm = -INFINITY;
+            const int li = label - col0;  // label column relative to this warp's 128 columns
 #pragma unroll 1
-            for (int j = 0; j < 4; ++j) {  // pass 1: group max
-              ptx::tmem_ld32(taddr + j * 32, v);
+            for (int j = 0; j < 2; ++j) {
+              float va[32], vb[32];
+              ptx::tmem_ld32(taddr + j * 64, va);
+              ptx::tmem_ld32(taddr + j * 64 + 32, vb);
+              float cm = fmaxf(va[0], vb[0]);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) cm = fmaxf(cm, v[i]);
-            }
-            const float mg = cm * p.tl2e;
-            float s0 = 0.f, s1 = 0.f;
-            const int li = label - col0;  // label column relative to the group
-#pragma unroll 1
-            for (int j = 0; j < 2; ++j) {  // pass 2: E, sum of the non-label terms, 64-column slices
+              for (int i = 1; i < 32; ++i) cm = fmaxf(cm, fmaxf(va[i], vb[i]));
+              const float mg = cm * p.tl2e;
+              float s0 = 0.f, s1 = 0.f;
               uint32_t h[32];
 #pragma unroll
               for (int half = 0; half < 2; ++half) {
-                ptx::tmem_ld32(taddr + j * 64 + half * 32, v);
+                const float* v = half ? vb : va;
                 const int lg = li - (j * 64 + half * 32);
                 if (unsigned(lg) >= 32u) {  // warp-uniform: labels of a warp's 32 rows share a 32-column group
 #pragma unroll
@@ -550,11 +626,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 if (rbase < p.b) ptx::tma_store_4d(&p.g_map[dir], tile, cb & 127, rbase & 127, cb >> 7, rbase >> 7);
                 ptx::bulk_commit();
               }
+              const float mnew = fmaxf(m2, mg);
+              l = l * ptx::ex2(m2 - mnew) + (s0 + s1) * ptx::ex2(mg - mnew);
+              m2 = mnew;
+              if (row_ok) p.mg[(int64_t(dir) * p.groups + cb / GROUP_COLS) * p.b + row] = mg;
             }
-            const float mnew = fmaxf(m2, mg);
-            l = l * ptx::ex2(m2 - mnew) + (s0 + s1) * ptx::ex2(mg - mnew);
-            m2 = mnew;
-            if (row_ok) p.mg[(int64_t(dir) * p.groups + col0 / GROUP_COLS) * p.b + row] = mg;
           }
         } else {
           // G = exp2(y - lse2) (label column: P_label - 1), f16, 64-column slices
@@ -720,7 +796,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader CTA)
+    if (leader) {  // ---------------- MMA issuer (leader CTA, whole warp; one elected lane issues)
       Pipe<RS> pipe;
       uint32_t it = 0;
       for (int u = pair; u < num_units; u += npairs) {
@@ -735,8 +811,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           ptx::mbar_wait(&ctl->tempty[1], ((it >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
           mma_tile<NB, XF>(ctl, tiles, pipe, nk, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major);
-          ptx::umma_commit_pair(&ctl->tfull[0], 0x3);
-          ptx::umma_commit_pair(&ctl->tfull[1], 0x3);
+          if (ptx::elect_one()) {
+            ptx::umma_commit_pair(&ctl->tfull[0], 0x3);
+            ptx::umma_commit_pair(&ctl->tfull[1], 0x3);
+          }
+          __syncwarp();
           it += 2;
         }
         if constexpr (NB == 1) {
@@ -747,7 +826,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
             ptx::tc_fence_after();
             mma_tile<1, XF>(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, q.a_mn_major, q.b_mn_major);
-            ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
+            if (ptx::elect_one()) ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
+            __syncwarp();
           }
         }
       }
@@ -768,9 +848,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       const int m0 = mt * PAIR_M + crank * BM;
       const int rowoff = q.a_mn_major ? (xt >> 6) * 8192 + (xt & 63) * 128 : xt * 128;
       const int sw = (rowoff >> 7) & 7;
-      // per-stage scale index: K-major: (k / 128) * xb + (m0 + xt); MN-major: (m0 / 128) * xb + k + xt % 64
+      // per-stage scale index (64-column groups): K-major: (k / 64) * xb + (m0 + xt);
+      // MN-major: ((m0 + 64 * (xt / 64)) / 64) * xb + k + xt % 64
       auto sidx = [&](int k) -> int64_t {
-        return q.a_mn_major ? int64_t(m0 >> 7) * q.xb + k + (xt & 63) : int64_t(k >> 7) * q.xb + m0 + xt;
+        return q.a_mn_major ? int64_t((m0 >> 6) + (xt >> 6)) * q.xb + k + (xt & 63) : int64_t(k >> 6) * q.xb + m0 + xt;
       };
       // rows past b (last pair tile when b / 128 is odd) were zero-filled by TMA: nothing to scale
       const bool active = q.xform && (q.a_mn_major || m0 + xt < q.xb);
@@ -1398,14 +1479,13 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 // DISCO_DEBUG_FLAGS (profiling experiments only): bit0 skip G stores (recompute GRAD), bit1 L2
 // persistence for the features in GRAD, bit4 skip GEMM output stores, bit5 GEMM epilogues store
-// with st.global instead of TMA.
-int debug_flag_bits() {
-  static const int bits = [] {
-    const char* e = getenv("DISCO_DEBUG_FLAGS");
-    return e ? atoi(e) : 0;
-  }();
-  return bits;
-}
+// with st.global instead of TMA, bit6 GEMM epilogues store via coalesced st.global rows, bit7
+// logits kernel keeps a resident A block (measured no faster, so off by default).
+std::atomic<int> g_debug_bits{[] {
+  const char* e = getenv("DISCO_DEBUG_FLAGS");
+  return e ? atoi(e) : 0;
+}()};
+int debug_flag_bits() { return g_debug_bits.load(std::memory_order_relaxed); }
 
 int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   if (world < 1) return fail(DISCO_LAYOUT_ERROR, "world size must be >= 1, got %d", world);
@@ -1599,6 +1679,15 @@ int prepare_kernel(K kernel) {
 // Persistent grid of CTA pairs: one pair per unit, at most one CTA per SM.
 int grid_for(int64_t units) { return 2 * int(std::min<int64_t>(units, sm_count() / 2)); }
 
+template <int KIND, bool ARES>
+int launch_logits_t(const LogitsParams& p, int64_t units, cudaStream_t st) {
+  int rc;
+  if ((rc = prepare_kernel(logits_kernel<KIND, ARES>))) return rc;
+  logits_kernel<KIND, ARES><<<grid_for(units), NUM_THREADS, SMEM_BYTES, st>>>(p);
+  count_launch();
+  return DISCO_OK;
+}
+
 int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t st) {
   LogitsParams p;
   memset(&p, 0, sizeof(p));
@@ -1638,16 +1727,15 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.debug_flags = debug_flags;
   const int64_t units =
       int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
+  const bool ares = g.Dp <= BK * ARES_SLICES && (debug_flags & 128);  // experiment: not faster on B200
   if (kind == KIND_FWD) {
-    if ((rc = prepare_kernel(logits_kernel<KIND_FWD>))) return rc;
-    logits_kernel<KIND_FWD><<<grid_for(units), NUM_THREADS, SMEM_BYTES, st>>>(p);
-    count_launch();
+    rc = ares ? launch_logits_t<KIND_FWD, true>(p, units, st) : launch_logits_t<KIND_FWD, false>(p, units, st);
+    if (rc) return rc;
   } else if (kind == KIND_FWDE) {
-    if ((rc = prepare_kernel(logits_kernel<KIND_FWDE>))) return rc;
-    logits_kernel<KIND_FWDE><<<grid_for(units), NUM_THREADS, SMEM_BYTES, st>>>(p);
-    count_launch();
+    rc = ares ? launch_logits_t<KIND_FWDE, true>(p, units, st) : launch_logits_t<KIND_FWDE, false>(p, units, st);
+    if (rc) return rc;
   } else {
-    if ((rc = prepare_kernel(logits_kernel<KIND_GRAD>))) return rc;
+    if ((rc = prepare_kernel(logits_kernel<KIND_GRAD, false>))) return rc;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid_for(units));
     cfg.blockDim = dim3(NUM_THREADS);
@@ -1673,7 +1761,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
       attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
       cfg.numAttrs = 1;
     }
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, logits_kernel<KIND_GRAD>, p));
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, logits_kernel<KIND_GRAD, false>, p));
     count_launch();
   }
   CUDA_TRY(cudaGetLastError());
@@ -1851,6 +1939,8 @@ using namespace disco;
 extern "C" {
 
 int disco_b200_abi_version(void) { return DISCO_B200_ABI_VERSION; }
+
+int disco_b200_set_experiment_flags(int flags) { return g_debug_bits.exchange(flags); }
 
 int64_t disco_b200_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 

@@ -1,0 +1,85 @@
+"""Same-process A/B timing of kernel variants (profiling experiments, not a bench value).
+
+Alternates experiment-flag settings (disco_b200_set_experiment_flags) rep by rep so every
+variant sees the same clocks / thermal state, and reports the median per-phase time.
+
+  python tools/ab_kernels.py --flags 0 128 --reps 15
+  python tools/ab_kernels.py --so-b /path/to/other/_disco_b200.so   (two builds, same ABI)
+"""
+import argparse
+import ctypes
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2304_08480_b200 as P  # noqa: E402
+from paper_2304_08480_b200 import _lib  # noqa: E402
+from paper_2304_08480_b200.shard import get_plan  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--batch", type=int, default=32768)
+ap.add_argument("--dim", type=int, default=512)
+ap.add_argument("--flags", type=int, nargs="+", default=[0])
+ap.add_argument("--so-b", default=None, help="second library build to alternate with")
+ap.add_argument("--reps", type=int, default=15)
+a = ap.parse_args()
+
+torch.cuda.set_device(0)
+dev = torch.device("cuda", 0)
+B, D, t = a.batch, a.dim, 100.0
+g = torch.Generator(device=dev)
+g.manual_seed(0)
+I = torch.nn.functional.normalize(torch.randn(B, D, device=dev, generator=g), dim=1).bfloat16()
+T = torch.nn.functional.normalize(torch.randn(B, D, device=dev, generator=g), dim=1).bfloat16()
+plan = get_plan(B, D, 1, 0, dev)
+st = torch.cuda.current_stream(dev)
+sp = st.cuda_stream
+di = torch.empty((B, D), dtype=torch.float32, device=dev)
+dt = torch.empty((B, D), dtype=torch.float32, device=dev)
+flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+libs = [("main", _lib.load())]
+if a.so_b:
+    lb = ctypes.CDLL(a.so_b)
+    for name, argtypes in _lib.SIGNATURES.items():
+        fn = getattr(lb, name, None)
+        if fn is None:  # older build: no experiment-flag hook
+            continue
+        fn.argtypes = argtypes
+        fn.restype = _lib._RESTYPES.get(name, ctypes.c_int)
+    libs.append(("b", lb))
+variants = [(ln, lib, f) for ln, lib in libs for f in a.flags]
+
+
+def run(lib, flags, ev):
+    if hasattr(lib, "disco_b200_set_experiment_flags"):
+        lib.disco_b200_set_experiment_flags(flags)
+    args = plan.args
+    assert lib.disco_b200_pack(*args, I.data_ptr(), T.data_ptr(), D, D, _lib.BF16, 1, sp) == 0
+    ev[0].record(st)
+    assert lib.disco_b200_forward(*args, t, sp) == 0
+    ev[1].record(st)
+    assert lib.disco_b200_backward_grad(*args, t, sp) == 0
+    assert lib.disco_b200_backward_fused(*args, sp) == 0
+    ev[2].record(st)
+    assert lib.disco_b200_combine(*args, t, 0, di.data_ptr(), dt.data_ptr(), D, sp) == 0
+    ev[3].record(st)
+
+
+times = {v[0] + ":" + str(v[2]): ([], [], []) for v in variants}
+for rep in range(a.reps + 2):
+    for ln, lib, f in variants:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        flush.zero_()
+        run(lib, f, ev)
+        torch.cuda.synchronize()
+        if rep >= 2:
+            k = ln + ":" + str(f)
+            for i in range(3):
+                times[k][i].append(ev[i].elapsed_time(ev[i + 1]))
+for k, (fw, bw, cb) in times.items():
+    print(f"{k:10s} forward {statistics.median(fw):.4f}  backward {statistics.median(bw):.4f}  "
+          f"combine {statistics.median(cb):.4f}  total {statistics.median(fw) + statistics.median(bw) + statistics.median(cb):.4f} ms")

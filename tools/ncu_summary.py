@@ -17,9 +17,9 @@ import os
 import subprocess
 
 KERNEL_KEYS = [  # order of the tensor-core launches within one step
-    ("logits_kernel<2>", "logits_fwd"),   # forward + E store (canonical shapes)
-    ("logits_kernel<0>", "logits_fwd"),   # forward only (recompute path)
-    ("logits_kernel<1>", "logits_grad"),  # recompute path only
+    ("logits_kernel<2", "logits_fwd"),    # forward + E store (canonical shapes)
+    ("logits_kernel<0", "logits_fwd"),    # forward only (recompute path)
+    ("logits_kernel<1", "logits_grad"),   # recompute path only
     ("gemm_kernel", "gemm_backward"),     # single rank: intra + cross in one launch
 ]
 MULTI_RANK_GEMMS = [("gemm_kernel", "gemm_cross"), ("gemm_kernel", "gemm_intra")]
