@@ -575,13 +575,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           // One TMEM pass (TMEM reads are 64 B/clk/SM: a second pass would pace the tile at the
           // MMA time): each 64-column group is loaded once, its max taken in registers, then
           // E = exp2(y - m_g) packed to f16 and stored as one 32 x 64 slice.
-          if (col0 < chunk_hi) {  // warp-uniform
+          if (col0 < chunk_hi && (p.debug_flags & 512)) {  // ablation: drain TMEM only
+            float va[32];
+#pragma unroll 1
+            for (int j = 0; j < 4; ++j) {
+              ptx::tmem_ld32(taddr + j * 32, va);
+              if (va[0] == 12345.678f) asm volatile("trap;");
+            }
+          } else if (col0 < chunk_hi) {  // warp-uniform
             const int li = label - col0;  // label column relative to this warp's 128 columns
 #pragma unroll 1
             for (int j = 0; j < 2; ++j) {
+              uint32_t ra[32], rb[32];  // both halves of the slice under one tcgen05.wait::ld
+              ptx::tmem_ld32_async(taddr + j * 64, ra);
+              ptx::tmem_ld32_async(taddr + j * 64 + 32, rb);
+              ptx::tmem_wait_ld_dep(ra, rb);
               float va[32], vb[32];
-              ptx::tmem_ld32(taddr + j * 64, va);
-              ptx::tmem_ld32(taddr + j * 64 + 32, vb);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                va[i] = __uint_as_float(ra[i]);
+                vb[i] = __uint_as_float(rb[i]);
+              }
               float cm = fmaxf(va[0], vb[0]);
 #pragma unroll
               for (int i = 1; i < 32; ++i) cm = fmaxf(cm, fmaxf(va[i], vb[i]));
@@ -623,7 +637,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               ptx::fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
-                if (rbase < p.b) ptx::tma_store_4d(&p.g_map[dir], tile, cb & 127, rbase & 127, cb >> 7, rbase >> 7);
+                if (rbase < p.b && !(p.debug_flags & 1))  // bit0 ablation: skip the E stores
+                  ptx::tma_store_4d(&p.g_map[dir], tile, cb & 127, rbase & 127, cb >> 7, rbase >> 7);
                 ptx::bulk_commit();
               }
               const float mnew = fmaxf(m2, mg);
@@ -992,6 +1007,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
   }
   kernel_epilogue(ctl, warp);
 }
+
+__global__ void __launch_bounds__(NUM_THREADS_XF, 1) cluster_probe_kernel() {}
 
 // =====================================================================
 // Small HBM-bound kernels
@@ -1477,7 +1494,8 @@ struct Geometry {
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// DISCO_DEBUG_FLAGS (profiling experiments only): bit0 skip G stores (recompute GRAD), bit1 L2
+// DISCO_DEBUG_FLAGS (profiling experiments only): bit0 skip G / E stores, bit9 FWDE epilogue only
+// drains TMEM (no math, no stores), bit1 L2
 // persistence for the features in GRAD, bit4 skip GEMM output stores, bit5 GEMM epilogues store
 // with st.global instead of TMA, bit6 GEMM epilogues store via coalesced st.global rows, bit7
 // logits kernel keeps a resident A block (measured no faster, so off by default).
@@ -1511,7 +1529,7 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   }
   g->chunk_cols = int(B / g->nchunk);
   g->g_blocked = (g->nchunk == 8 && g->b % 128 == 0) ? 1 : 0;
-  g->wide = (g->Dp % 512 == 0) ? 1 : 0;
+  g->wide = (g->Dp % 512 == 0 && !(debug_flag_bits() & 256)) ? 1 : 0;  // bit8: narrow-unit experiment
   // cross partials per rank: wide units keep one partial per canonical chunk (the first tree
   // level then runs in presum/combine); narrow units pair chunks in the two accumulators.
   g->np = g->wide ? g->cpr : (g->cpr >= 2 ? g->cpr / 2 : 1);
@@ -1679,11 +1697,39 @@ int prepare_kernel(K kernel) {
 // Persistent grid of CTA pairs: one pair per unit, at most one CTA per SM.
 int grid_for(int64_t units) { return 2 * int(std::min<int64_t>(units, sm_count() / 2)); }
 
+// Experiment (DISCO_DEBUG_FLAGS bit1): L2 persistence window over the bf16 feature operands while
+// the E / G write stream runs.
+int l2_window(cudaLaunchAttribute* attr, const void* base, size_t bytes) {
+  static int maxp = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(v));
+    return v;
+  }();
+  attr->id = cudaLaunchAttributeAccessPolicyWindow;
+  attr->val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  attr->val.accessPolicyWindow.num_bytes = bytes;
+  attr->val.accessPolicyWindow.hitRatio = std::min(1.0f, float(maxp) / float(bytes));
+  attr->val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr->val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  return 1;
+}
+
 template <int KIND, bool ARES>
-int launch_logits_t(const LogitsParams& p, int64_t units, cudaStream_t st) {
+int launch_logits_t(const LogitsParams& p, int64_t units, cudaStream_t st, const void* feat = nullptr,
+                    size_t feat_bytes = 0) {
   int rc;
   if ((rc = prepare_kernel(logits_kernel<KIND, ARES>))) return rc;
-  logits_kernel<KIND, ARES><<<grid_for(units), NUM_THREADS, SMEM_BYTES, st>>>(p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid_for(units));
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  cfg.attrs = attr;
+  cfg.numAttrs = (feat && (debug_flag_bits() & 2)) ? l2_window(&attr[0], feat, feat_bytes) : 0;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, logits_kernel<KIND, ARES>, p));
   count_launch();
   return DISCO_OK;
 }
@@ -1732,7 +1778,9 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
     rc = ares ? launch_logits_t<KIND_FWD, true>(p, units, st) : launch_logits_t<KIND_FWD, false>(p, units, st);
     if (rc) return rc;
   } else if (kind == KIND_FWDE) {
-    rc = ares ? launch_logits_t<KIND_FWDE, true>(p, units, st) : launch_logits_t<KIND_FWDE, false>(p, units, st);
+    const size_t fb = size_t(2) * g.B * g.Dp * 2;
+    rc = ares ? launch_logits_t<KIND_FWDE, true>(p, units, st, feat, fb)
+              : launch_logits_t<KIND_FWDE, false>(p, units, st, feat, fb);
     if (rc) return rc;
   } else {
     if ((rc = prepare_kernel(logits_kernel<KIND_GRAD, false>))) return rc;
@@ -1744,23 +1792,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
     cudaLaunchAttribute attr[1];
     cfg.attrs = attr;
     cfg.numAttrs = 0;
-    if (debug_flags & 2) {  // experiment: persist the bf16 feature operands in L2 during the G write stream
-      static int maxp = [] {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev);
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(v));
-        return v;
-      }();
-      const size_t bytes = size_t(2) * g.B * g.Dp * 2;
-      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-      attr[0].val.accessPolicyWindow.base_ptr = const_cast<__nv_bfloat16*>(feat);
-      attr[0].val.accessPolicyWindow.num_bytes = bytes;
-      attr[0].val.accessPolicyWindow.hitRatio = std::min(1.0f, float(maxp) / float(bytes));
-      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cfg.numAttrs = 1;
-    }
+    if (debug_flags & 2) cfg.numAttrs = l2_window(&attr[0], feat, size_t(2) * g.B * g.Dp * 2);
     CUDA_TRY(cudaLaunchKernelEx(&cfg, logits_kernel<KIND_GRAD, false>, p));
     count_launch();
   }
@@ -1941,6 +1973,26 @@ extern "C" {
 int disco_b200_abi_version(void) { return DISCO_B200_ABI_VERSION; }
 
 int disco_b200_set_experiment_flags(int flags) { return g_debug_bits.exchange(flags); }
+
+// Profiling helper: co-resident clusters of `cluster_size` CTAs for the backward GEMM's launch
+// shape (SMEM_BYTES per CTA, 1 CTA per SM).
+int disco_b200_max_active_clusters(int cluster_size, int* clusters) {
+  CUDA_TRY(cudaFuncSetAttribute(cluster_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
+  CUDA_TRY(cudaFuncSetAttribute(cluster_probe_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(cluster_size * 64));
+  cfg.blockDim = dim3(NUM_THREADS_XF);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(cluster_size);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveClusters(clusters, (void*)cluster_probe_kernel, &cfg));
+  return DISCO_OK;
+}
 
 int64_t disco_b200_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 

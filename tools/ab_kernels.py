@@ -35,6 +35,15 @@ g.manual_seed(0)
 I = torch.nn.functional.normalize(torch.randn(B, D, device=dev, generator=g), dim=1).bfloat16()
 T = torch.nn.functional.normalize(torch.randn(B, D, device=dev, generator=g), dim=1).bfloat16()
 plan = get_plan(B, D, 1, 0, dev)
+# experiments may change the geometry (e.g. bit8 narrow units): give the workspace the max size
+_need = 0
+for _f in a.flags:
+    _lib.load().disco_b200_set_experiment_flags(_f)
+    _need = max(_need, _lib.workspace_bytes(B, D, 1, 0))
+_lib.load().disco_b200_set_experiment_flags(0)
+if _need > plan.ws.numel():
+    plan.ws = torch.empty(_need, dtype=torch.uint8, device=dev)
+    plan.ptr = plan.ws.data_ptr()
 st = torch.cuda.current_stream(dev)
 sp = st.cuda_stream
 di = torch.empty((B, D), dtype=torch.float32, device=dev)
