@@ -105,6 +105,12 @@ int disco_b200_pack(void* ws, int64_t B, int64_t D, int world, int rank, const v
                     const void* local_T, int64_t ld_I, int64_t ld_T, int dtype, int clear_status,
                     void* stream);
 
+/* Rows [row0, row1) of disco_b200_pack (same layout, same non-finite flag); the
+ * host-buffer single-rank path packs each canonical chunk as its H2D copy lands. */
+int disco_b200_pack_rows(void* ws, int64_t B, int64_t D, int world, int rank, const void* local_I,
+                         const void* local_T, int64_t ld_I, int64_t ld_T, int dtype, int clear_status, int64_t row0,
+                         int64_t row1, void* stream);
+
 /* Forward: unpack the gathered features, fused logits GEMM + online
  * log-sum-exp + target extraction (shard.py:134-141, matrix.py:103-118),
  * fixed-order chunk combine -> per-row lse / ce / label gradient.
@@ -113,6 +119,16 @@ int disco_b200_pack(void* ws, int64_t B, int64_t D, int world, int rank, const v
  * 128-column group, and the combine turns m_g into exp2(m_g - lse2)
  * (DISCO_R_SCALE), so the backward needs no logit recompute. */
 int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
+
+/* Wavefront forward (single rank, canonical shapes with B % 2048 == 0; *waves = 0 otherwise):
+ * disco_b200_forward == forward_wave(0) ... forward_wave(waves - 1) + forward_finish, bit for bit.
+ * Wave k computes the logit units (row chunk, column chunk) with max(row chunk, column chunk) == k,
+ * i.e. exactly those that became computable when rows [k*B/8, (k+1)*B/8) of I and T landed, so
+ * the host->device copy of host features overlaps the logits GEMMs.  Waves may run on different
+ * streams (they write disjoint outputs); forward_finish must follow all of them. */
+int disco_b200_forward_waves(int64_t B, int64_t D, int world, int rank, int* waves);
+int disco_b200_forward_wave(void* ws, int64_t B, int64_t D, int world, int rank, float t, int wave, void* stream);
+int disco_b200_forward_finish(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
 
 /* Backward part 1: recompute the logit tiles (bit-identical to the forward)
  * -> G = softmax - onehot, unscaled, f16 (shard.py:143-146, matrix.py:131-144).

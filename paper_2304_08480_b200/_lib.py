@@ -42,7 +42,11 @@ SIGNATURES = {
     "disco_b200_ws_region": [_i64, _i64, _int, _int, _int, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
     "disco_b200_chunking": [_i64, _int, ctypes.POINTER(_int), ctypes.POINTER(_int)],
     "disco_b200_pack": [_vp, _i64, _i64, _int, _int, _vp, _vp, _i64, _i64, _int, _int, _vp],
+    "disco_b200_pack_rows": [_vp, _i64, _i64, _int, _int, _vp, _vp, _i64, _i64, _int, _int, _i64, _i64, _vp],
     "disco_b200_forward": [_vp, _i64, _i64, _int, _int, _f32, _vp],
+    "disco_b200_forward_waves": [_i64, _i64, _int, _int, ctypes.POINTER(_int)],
+    "disco_b200_forward_wave": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp],
+    "disco_b200_forward_finish": [_vp, _i64, _i64, _int, _int, _vp],
     "disco_b200_backward_grad": [_vp, _i64, _i64, _int, _int, _f32, _vp],
     "disco_b200_backward_cross": [_vp, _i64, _i64, _int, _int, _vp],
     "disco_b200_backward_intra": [_vp, _i64, _i64, _int, _int, _vp],
@@ -129,6 +133,13 @@ def chunking(B: int, world: int):
     nchunk, cpr = _int(), _int()
     call("disco_b200_chunking", B, world, ctypes.byref(nchunk), ctypes.byref(cpr))
     return nchunk.value, cpr.value
+
+
+def forward_waves(B: int, D: int, world: int, rank: int) -> int:
+    """Waves of the H2D-pipelined forward (0: shape not wavefront-capable)."""
+    out = _int()
+    call("disco_b200_forward_waves", B, D, world, rank, ctypes.byref(out))
+    return out.value
 
 
 def launch_count() -> int:

@@ -129,6 +129,10 @@ struct LogitsParams {
   // FWDE outputs: E = exp2(y - m_g) into the blocked G region, m_g per (dir, 128-column group, row)
   float* mg;            // [2][groups][b]
   int groups;           // B / 128
+  // wave >= 0 (single rank, H2D-pipelined forward): only the units whose row chunk or column
+  // chunk is `wave` and the other index <= wave, i.e. the units that became computable when
+  // canonical chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per chunk.
+  int wave, rt_per_chunk;
 };
 
 struct GemmProblem {
@@ -370,7 +374,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   kernel_prologue(ctl, warp, lane);
 
   constexpr bool CHUNK_UNITS = KIND != KIND_GRAD;  // unit = all tiles of one column chunk
-  const int per_dir = p.row_tiles * p.nchunk * (CHUNK_UNITS ? 1 : p.tiles_per_chunk);
+  const int wave = CHUNK_UNITS ? p.wave : -1;
+  const int per_dir = wave >= 0 ? p.rt_per_chunk * (2 * wave + 1)
+                                : p.row_tiles * p.nchunk * (CHUNK_UNITS ? 1 : p.tiles_per_chunk);
   const int num_units = 2 * per_dir;
   const int tiles_per_unit = CHUNK_UNITS ? p.tiles_per_chunk : 1;
   const int nk = p.Dp / BK;
@@ -378,7 +384,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   auto decode = [&](int u, int& dir, int& rt, int& ch, int& t0) {
     dir = u / per_dir;
     int rem = u - dir * per_dir;
-    if (CHUNK_UNITS) {
+    if (wave >= 0) {  // new row tiles x chunks [0, wave], then old row tiles x chunk `wave`
+      const int fresh = p.rt_per_chunk * (wave + 1);
+      if (rem < fresh) {
+        rt = wave * p.rt_per_chunk + rem / (wave + 1);
+        ch = rem % (wave + 1);
+      } else {
+        rt = rem - fresh;
+        ch = wave;
+      }
+      t0 = 0;
+    } else if (CHUNK_UNITS) {
       rt = rem / p.nchunk;
       ch = rem - rt * p.nchunk;
       t0 = 0;
@@ -1030,16 +1046,19 @@ __device__ __forceinline__ float load_as_float<__half>(const void* p, int64_t i)
 // One thread per 8 output elements (one 16-byte store); f64 inputs are rounded
 // directly f64 -> bf16 (a single rounding).
 // out16 (optional): also write the f16 copy (single rank: packed == gathered layout).
+// Rows [row0, row0 + nrows) of both matrices (the H2D-pipelined single-rank path packs one
+// canonical chunk at a time as it lands).
 template <typename T>
 __global__ void pack_kernel(const void* I, const void* Tm, int64_t ldI, int64_t ldT, int b, int D, int Dp,
-                            __nv_bfloat16* out, __half* out16, Status* status) {
+                            __nv_bfloat16* out, __half* out16, Status* status, int row0, int nrows) {
   const int v8 = Dp / 8;
-  const int64_t total = int64_t(2) * b * v8;
+  const int64_t total = int64_t(2) * nrows * v8;
   bool bad = false;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int c0 = int(i % v8) * 8;
-    const int64_t rr = i / v8;
-    const int dir = int(rr / b), r = int(rr % b);
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < total; j += int64_t(gridDim.x) * blockDim.x) {
+    const int c0 = int(j % v8) * 8;
+    const int64_t rr = j / v8;
+    const int dir = int(rr / nrows), r = row0 + int(rr % nrows);
+    const int64_t i = (int64_t(dir) * b + r) * v8 + c0 / 8;
     const void* src = dir ? Tm : I;
     const int64_t base = r * (dir ? ldT : ldI);
     __align__(16) __nv_bfloat16 o[8];
@@ -1734,7 +1753,7 @@ int launch_logits_t(const LogitsParams& p, int64_t units, cudaStream_t st, const
   return DISCO_OK;
 }
 
-int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t st) {
+int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t st, int wave = -1) {
   LogitsParams p;
   memset(&p, 0, sizeof(p));
   const __nv_bfloat16* feat = region<__nv_bfloat16>(ws, g, DISCO_R_FEAT);
@@ -1764,6 +1783,8 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.g_blocked = g.g_blocked;
   p.mg = region<float>(ws, g, DISCO_R_SCALE);
   p.groups = g.groups;
+  p.wave = wave;
+  p.rt_per_chunk = g.chunk_cols / PAIR_M;
   if (kind != KIND_FWD && g.g_blocked) {
     const __half* Gb = region<__half>(ws, g, DISCO_R_G);
     for (int d = 0; d < 2; ++d)
@@ -1771,8 +1792,8 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   }
   const int debug_flags = debug_flag_bits();
   p.debug_flags = debug_flags;
-  const int64_t units =
-      int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
+  const int64_t units = wave >= 0 ? int64_t(2) * p.rt_per_chunk * (2 * wave + 1)
+                                  : int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
   const bool ares = g.Dp <= BK * ARES_SLICES && (debug_flags & 128);  // experiment: not faster on B200
   if (kind == KIND_FWD) {
     rc = ares ? launch_logits_t<KIND_FWD, true>(p, units, st) : launch_logits_t<KIND_FWD, false>(p, units, st);
@@ -1961,6 +1982,25 @@ int build_intra(GemmParams& p, int first, void* ws, const Geometry& g, int mt0 =
   return DISCO_OK;
 }
 
+// stats combine (+ E -> G factors): after every logits unit of the forward has run.
+int forward_finish(void* ws, const Geometry& g, cudaStream_t st) {
+  float* rows = region<float>(ws, g, DISCO_R_ROWS);
+  const int n = int(2 * g.b);
+  stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(
+      region<float2>(ws, g, DISCO_R_STATS), rows, g.nchunk, int(g.b), rows + 2 * g.b, rows + 4 * g.b,
+      region<float>(ws, g, DISCO_R_CE), region<Status>(ws, g, DISCO_R_STATUS));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  if (g.estore) {
+    const int64_t nv = 2 * int64_t(g.groups) * g.b / 8;
+    scale_kernel<<<elementwise_grid(nv, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_SCALE), rows + 2 * g.b,
+                                                           g.groups, int(g.b), scale16(ws, g));
+    count_launch();
+    CUDA_TRY(cudaGetLastError());
+  }
+  return DISCO_OK;
+}
+
 }  // namespace disco
 
 // =====================================================================
@@ -2027,10 +2067,20 @@ int disco_b200_chunking(int64_t B, int world, int* nchunk, int* chunks_per_rank)
 
 int disco_b200_pack(void* ws, int64_t B, int64_t D, int world, int rank, const void* local_I, const void* local_T,
                     int64_t ld_I, int64_t ld_T, int dtype, int clear_status, void* stream) {
+  return disco_b200_pack_rows(ws, B, D, world, rank, local_I, local_T, ld_I, ld_T, dtype, clear_status, 0, B / world,
+                              stream);
+}
+
+int disco_b200_pack_rows(void* ws, int64_t B, int64_t D, int world, int rank, const void* local_I,
+                         const void* local_T, int64_t ld_I, int64_t ld_T, int dtype, int clear_status, int64_t row0,
+                         int64_t row1, void* stream) {
   Geometry g;
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   if (ld_I < D || ld_T < D) return fail(DISCO_SHAPE_ERROR, "row stride smaller than D");
+  if (row0 < 0 || row1 > g.b || row0 > row1)
+    return fail(DISCO_LAYOUT_ERROR, "pack rows [%lld, %lld) outside [0, %lld)", (long long)row0, (long long)row1,
+                (long long)g.b);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Status* status = region<Status>(ws, g, DISCO_R_STATUS);
   if (clear_status) {
@@ -2039,21 +2089,23 @@ int disco_b200_pack(void* ws, int64_t B, int64_t D, int world, int rank, const v
   }
   __nv_bfloat16* out = region<__nv_bfloat16>(ws, g, DISCO_R_PACK);
   __half* out16 = world == 1 ? region<__half>(ws, g, DISCO_R_FEAT16) : nullptr;  // PACK aliases FEAT
-  const int64_t n = 2 * g.b * (g.Dp / 8);
+  const int64_t n = 2 * (row1 - row0) * (g.Dp / 8);
   const int grid = elementwise_grid(n, 256);
+  const int r0 = int(row0), nr = int(row1 - row0);
+  if (nr == 0) return DISCO_OK;
   switch (dtype) {
     case DISCO_F32:
-      pack_kernel<float><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, out16, status);
+      pack_kernel<float><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, out16, status, r0, nr);
       break;
     case DISCO_BF16:
       pack_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out,
-                                                       out16, status);
+                                                       out16, status, r0, nr);
       break;
     case DISCO_F16:
-      pack_kernel<__half><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, out16, status);
+      pack_kernel<__half><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, out16, status, r0, nr);
       break;
     case DISCO_F64:
-      pack_kernel<double><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, out16, status);
+      pack_kernel<double><<<grid, 256, 0, st>>>(local_I, local_T, ld_I, ld_T, int(g.b), int(D), int(g.Dp), out, out16, status, r0, nr);
       break;
     default:
       return fail(DISCO_SHAPE_ERROR, "unsupported dtype code %d", dtype);
@@ -2078,22 +2130,35 @@ int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, floa
     CUDA_TRY(cudaGetLastError());
   }
   if ((rc = launch_logits(g.estore ? KIND_FWDE : KIND_FWD, ws, g, t, st))) return rc;
-  float* rows = region<float>(ws, g, DISCO_R_ROWS);
-  const int n = int(2 * g.b);
-  stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(
-      region<float2>(ws, g, DISCO_R_STATS), rows, g.nchunk, int(g.b), rows + 2 * g.b, rows + 4 * g.b,
-      region<float>(ws, g, DISCO_R_CE), region<Status>(ws, g, DISCO_R_STATUS));
-  count_launch();
-  CUDA_TRY(cudaGetLastError());
-  if (g.estore) {
-    const int64_t nv = 2 * int64_t(g.groups) * g.b / 8;
-    scale_kernel<<<elementwise_grid(nv, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_SCALE), rows + 2 * g.b,
-                                                           g.groups, int(g.b), scale16(ws, g));
-    count_launch();
-    CUDA_TRY(cudaGetLastError());
-  }
+  return forward_finish(ws, g, st);
+}
+
+int disco_b200_forward_waves(int64_t B, int64_t D, int world, int rank, int* waves) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  *waves = (world == 1 && g.estore && g.chunk_cols % PAIR_M == 0) ? g.nchunk : 0;
   return DISCO_OK;
 }
+
+int disco_b200_forward_wave(void* ws, int64_t B, int64_t D, int world, int rank, float t, int wave, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
+  if (!(world == 1 && g.estore && g.chunk_cols % PAIR_M == 0))
+    return fail(DISCO_LAYOUT_ERROR, "wavefront forward needs a single rank and B %% 2048 == 0");
+  if (wave < 0 || wave >= g.nchunk) return fail(DISCO_LAYOUT_ERROR, "wave %d outside [0, %d)", wave, g.nchunk);
+  return launch_logits(KIND_FWDE, ws, g, t, static_cast<cudaStream_t>(stream), wave);
+}
+
+int disco_b200_forward_finish(void* ws, int64_t B, int64_t D, int world, int rank, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  return forward_finish(ws, g, static_cast<cudaStream_t>(stream));
+}
+
 
 int disco_b200_backward_grad(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream) {
   Geometry g;

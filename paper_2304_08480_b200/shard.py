@@ -138,13 +138,23 @@ class Plan:
         self.rdot_all = view(_lib.R_RDOT_ALL, torch.float32)
         self.status = view(_lib.R_STATUS, torch.uint8)[:24]
         self.status_host = torch.empty(24, dtype=torch.uint8, pin_memory=True)
+        self.waves = _lib.forward_waves(B, D, world, rank)
         self._copy_stream = None
+        self._h2d_stream = None
+        self._wave_stream = None
 
     def copy_stream(self) -> "torch.cuda.Stream":
         """Side stream for the pipelined device->host gradient copies (created on first use)."""
         if self._copy_stream is None:
             self._copy_stream = torch.cuda.Stream(self.device)
         return self._copy_stream
+
+    def h2d_streams(self):
+        """(host->device copy stream, second compute stream) of the wavefront forward."""
+        if self._h2d_stream is None:
+            self._h2d_stream = torch.cuda.Stream(self.device)
+            self._wave_stream = torch.cuda.Stream(self.device)
+        return self._h2d_stream, self._wave_stream
 
     @property
     def args(self):
@@ -199,6 +209,25 @@ def _stage(x, device):
     if x.stride(1) != 1 or (x.shape[0] > 1 and x.stride(0) < x.shape[1]):
         x = x.contiguous()
     return x, origin
+
+
+def _on_host(x) -> bool:
+    return isinstance(x, np.ndarray) or (isinstance(x, torch.Tensor) and not x.is_cuda)
+
+
+def _host_tensor(x):
+    """(row-contiguous CPU tensor, origin) for the H2D-pipelined path; same checks as _stage."""
+    origin = "cpu"
+    if isinstance(x, np.ndarray):
+        origin = ("numpy", x.dtype)
+        if x.ndim != 2:
+            raise ShapeError(f"expected a 2-D matrix, got ndim={x.ndim}")
+        x = torch.from_numpy(np.ascontiguousarray(x))
+    if x.dim() != 2:
+        raise ShapeError(f"expected a 2-D matrix, got ndim={x.dim()}")
+    if x.dtype not in _TORCH_DTYPE_CODE:
+        x = x.to(torch.float32)
+    return x.contiguous(), origin
 
 
 def _unstage_async(t: torch.Tensor, origin):
@@ -332,13 +361,61 @@ def row_blocks(b: int):
     return [(min(256 * lo, b), min(256 * hi, b)) for lo, hi in zip(cuts, cuts[1:]) if hi > lo]
 
 
+def _pipelined_pack_forward(plan: Plan, I_host: torch.Tensor, T_host: torch.Tensor, t: float) -> None:
+    """Single rank, host features: H2D copy in canonical row chunks on a copy stream; as chunk k
+    lands its rows are packed and forward wave k runs (the logit units that chunk k completes),
+    alternating between two compute streams so one wave's tail overlaps the next.  Bit-identical
+    to pack + disco_b200_forward (the waves partition the units; every unit is unchanged)."""
+    device = plan.device
+    cur = torch.cuda.current_stream(device)
+    h2d, side = plan.h2d_streams()
+    b, D = I_host.shape
+    code = _TORCH_DTYPE_CODE[I_host.dtype]
+    I_dev = torch.empty(I_host.shape, dtype=I_host.dtype, device=device)
+    T_dev = torch.empty(T_host.shape, dtype=T_host.dtype, device=device)
+    # status reset before any wave can raise a flag, on the stream every other stream follows
+    _lib.call("disco_b200_pack_rows", *plan.args, I_dev.data_ptr(), T_dev.data_ptr(), D, D, code, 1, 0, 0,
+              cur.cuda_stream)
+    h2d.wait_stream(cur)
+    side.wait_stream(cur)
+    rows = b // plan.waves
+    landed = []
+    with torch.cuda.stream(h2d):
+        for k in range(plan.waves):
+            sl = slice(k * rows, (k + 1) * rows)
+            I_dev[sl].copy_(I_host[sl], non_blocking=True)
+            T_dev[sl].copy_(T_host[sl], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+            landed.append(ev)
+    streams = (cur, side)
+    for k in range(plan.waves):
+        s = streams[k % 2]
+        s.wait_event(landed[k])
+        _lib.call("disco_b200_pack_rows", *plan.args, I_dev.data_ptr(), T_dev.data_ptr(), D, D, code, 0,
+                  k * rows, (k + 1) * rows, s.cuda_stream)
+        _lib.call("disco_b200_forward_wave", *plan.args, t, k, s.cuda_stream)
+    cur.wait_stream(side)
+    for x in (I_dev, T_dev):
+        x.record_stream(h2d)
+        x.record_stream(side)
+    _lib.call("disco_b200_forward_finish", *plan.args, cur.cuda_stream)
+
+
+def host_pipelined(world: int, B: int, D: int, rank: int = 0) -> bool:
+    """True when disco_step_async overlaps the H2D copy of host features with the forward."""
+    return world == 1 and _lib.forward_waves(B, D, world, rank) > 0
+
+
 def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_sign: bool = False,
                      host_out=None):
     """Launch one rank's DisCo fwd+bwd without any host synchronisation.
 
-    Inputs must already be CUDA tensors (b x D).  Returns (d_image, d_text,
-    plan); the global loss and the non-finite flags are read later with
-    ``finish_status(plan)``.  ``disco_step`` is this plus that read-back.
+    Inputs are CUDA tensors (b x D), or, on a single rank with a wavefront-capable
+    shape (``host_pipelined``), CPU tensors (pinned for a fully asynchronous copy):
+    their H2D copy then overlaps the forward GEMMs chunk by chunk.  Returns
+    (d_image, d_text, plan); the global loss and the non-finite flags are read
+    later with ``finish_status(plan)``.  ``disco_step`` is this plus that read-back.
 
     ``host_out`` = (h_image, h_text) pinned host tensors (single rank): the
     backward then runs in output row blocks and each block's gradients are
@@ -348,15 +425,22 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
     N, n = endpoint.world_size, endpoint.rank
     b, D = local_I.shape
     B = b * N
-    device = local_I.device
+    on_host = not local_I.is_cuda
+    device = _default_device() if on_host else local_I.device
     plan = get_plan(B, D, N, n, device)
     st = _stream_ptr(device)
-    code = _TORCH_DTYPE_CODE[local_I.dtype]
-    _lib.call("disco_b200_pack", *plan.args, local_I.data_ptr(), local_T.data_ptr(),
-              local_I.stride(0), local_T.stride(0), code, 1, st)
-    if N > 1:
-        endpoint.all_gather_into(plan.gather, plan.pack)
-    _lib.call("disco_b200_forward", *plan.args, t, st)
+    if on_host:
+        if N != 1 or plan.waves == 0 or local_T.is_cuda:
+            raise ValueError("host (CPU) features need a single rank and a wavefront shape; "
+                             "stage them to the device first")
+        _pipelined_pack_forward(plan, local_I.contiguous(), local_T.contiguous(), t)
+    else:
+        code = _TORCH_DTYPE_CODE[local_I.dtype]
+        _lib.call("disco_b200_pack", *plan.args, local_I.data_ptr(), local_T.data_ptr(),
+                  local_I.stride(0), local_T.stride(0), code, 1, st)
+        if N > 1:
+            endpoint.all_gather_into(plan.gather, plan.pack)
+        _lib.call("disco_b200_forward", *plan.args, t, st)
     _lib.call("disco_b200_backward_grad", *plan.args, t, st)
     if N > 1:
         # cross first, so the slab exchange overlaps the intra GEMM
@@ -443,8 +527,12 @@ def disco_step(endpoint, local_I, local_T, t: float, *, loss_counters: Counters 
     t = _check_t(t)
     batch, dim = layout.global_batch, local_I.shape[1]
     device = _default_device()
-    I_dev, origin = _stage(local_I, device)
-    T_dev, _ = _stage(local_T, device)
+    if endpoint.world_size == 1 and host_pipelined(1, batch, dim) and _on_host(local_I) and _on_host(local_T):
+        I_dev, origin = _host_tensor(local_I)  # H2D happens inside, chunk by chunk
+        T_dev, _ = _host_tensor(local_T)
+    else:
+        I_dev, origin = _stage(local_I, device)
+        T_dev, _ = _stage(local_T, device)
     if T_dev.dtype != I_dev.dtype:
         T_dev = T_dev.to(I_dev.dtype)
     exchange_counters.alloc(2 * batch * dim)

@@ -217,3 +217,33 @@ def test_host_pipelined_readback_bitwise(B, D):
     assert np.array_equal(dh_i, dd_i.cpu().numpy()) and np.array_equal(dh_t, dd_t.cpu().numpy())
     ri, rt, _ = O.clip_grad_full(O.bf16_round(I), O.bf16_round(T), 100.0)
     assert O.max_rel_error(dh_i, ri) < TOL and O.max_rel_error(dh_t, rt) < TOL
+
+
+@pytest.mark.parametrize("B,D,dtype", [(32768, 512, torch.bfloat16), (8192, 1024, torch.float32),
+                                       (2048, 64, torch.float16)])
+def test_host_pipelined_forward_bitwise(B, D, dtype):
+    """Host features at N=1 with B % 2048 == 0 take the wavefront forward (chunked H2D on a copy
+    stream, disco_b200_pack_rows + forward_wave per landed chunk on two compute streams,
+    forward_finish); pinned torch inputs, outputs equal to the device path bit for bit."""
+    assert P.shard.host_pipelined(1, B, D)
+    I, T = O.synthetic_features(B, D, 4)
+    Ih = torch.from_numpy(I.astype(np.float32)).to(dtype).pin_memory()
+    Th = torch.from_numpy(T.astype(np.float32)).to(dtype).pin_memory()
+    for _ in range(2):  # second call reuses the plan, streams and pinned buffers
+        dh_i, dh_t, lh = P.disco_step(None, Ih, Th, 100.0)
+    dd_i, dd_t, ld = P.disco_step(None, Ih.cuda(), Th.cuda(), 100.0)
+    assert not dh_i.is_cuda and lh == ld
+    assert torch.equal(dh_i, dd_i.cpu()) and torch.equal(dh_t, dd_t.cpu())
+
+
+def test_host_pipelined_nonfinite_in_late_chunk():
+    """A NaN landing with the last H2D chunk is still flagged (the status reset is ordered before
+    every wave's pack on both compute streams)."""
+    B, D = 4096, 128
+    I, T = O.synthetic_features(B, D, 2)
+    T = T.astype(np.float32)
+    T[B - 3, 7] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        P.disco_step(None, I.astype(np.float32), T, 10.0)
+    di, dt, loss = P.disco_step(None, I.astype(np.float32), O.synthetic_features(B, D, 2)[1].astype(np.float32), 10.0)
+    assert np.isfinite(loss)

@@ -25,6 +25,7 @@ ap.add_argument("--dim", type=int, default=512)
 ap.add_argument("--flags", type=int, nargs="+", default=[0])
 ap.add_argument("--so-b", default=None, help="second library build to alternate with")
 ap.add_argument("--reps", type=int, default=15)
+ap.add_argument("--warm", type=float, default=3.0, help="seconds of untimed steps first (clocks ramp)")
 a = ap.parse_args()
 
 torch.cuda.set_device(0)
@@ -78,6 +79,11 @@ def run(lib, flags, ev):
     ev[3].record(st)
 
 
+import time as _time
+_t0 = _time.time()
+while _time.time() - _t0 < a.warm:
+    run(libs[0][1], a.flags[0], [torch.cuda.Event(enable_timing=True) for _ in range(4)])
+    torch.cuda.synchronize()
 times = {v[0] + ":" + str(v[2]): ([], [], []) for v in variants}
 for rep in range(a.reps + 2):
     for ln, lib, f in variants:
