@@ -168,6 +168,33 @@ int disco_b200_backward_rows(void* ws, int64_t B, int64_t D, int world, int rank
 int disco_b200_combine_rows(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip, int64_t row0,
                             int64_t row1, float* d_image, float* d_text, int64_t ld_out, void* stream);
 
+/* Peer transport: the cross-rank gradient exchange done by the backward GEMM
+ * itself over NVLink peer memory instead of an NCCL all_to_all + sender presum.
+ *
+ * Every rank owns one peer window (disco_b200_peer_alloc: cudaMalloc'd, IPC-exportable):
+ * u32 arrival flags [N], then two parity windows of [2][L][b][Dp] f32 slabs, L = N * (chunk
+ * partials per rank).  disco_b200_backward_peer runs the intra and cross GEMMs as one persistent
+ * launch; each cross tile's epilogue TMA-stores its fp32 chunk partial straight into the owning
+ * rank's window (leaf rank*np + k), so the transfer overlaps the GEMM tile by tile; a one-warp
+ * kernel then publishes `epoch` into every destination's flag slot [rank] (release, system
+ * scope).  disco_b200_combine_peer waits (acquire) until all N slots of this rank's window hold
+ * `epoch` (bounded by timeout_s: on expiry it sets status flag 8 instead of hanging), then runs
+ * the owner combine over the L leaves with the same fixed tree as disco_b200_combine, so the
+ * result is bit-identical to the all_to_all path and to N = 1.  Step s uses parity s & 1.
+ * Requires 2 <= N <= 8 and b % 128 == 0.  peer_bases: host array of the N ranks' window bases
+ * (this rank's own allocation at index rank, IPC-opened mappings of the others). */
+int disco_b200_peer_bytes(int64_t B, int64_t D, int world, int rank, int64_t* bytes);
+int disco_b200_peer_handle_bytes(void);
+int disco_b200_peer_alloc(int64_t bytes, void** ptr, void* ipc_handle);
+int disco_b200_peer_open(const void* ipc_handle, void** ptr);
+int disco_b200_peer_close(void* ptr);
+int disco_b200_peer_free(void* ptr);
+int disco_b200_backward_peer(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
+                             int parity, uint32_t epoch, void* stream);
+int disco_b200_combine_peer(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,
+                            const void* my_base, int parity, uint32_t epoch, double timeout_s, float* d_image,
+                            float* d_text, int64_t ld_out, void* stream);
+
 /* Full-size per-rank contribution (LocalGradContribution, shard.py:61-80,
  * 153-162): t*0.5/b * (scatter(intra) + send slabs), B x D fp32 each. */
 int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,

@@ -54,6 +54,16 @@ SIGNATURES = {
     "disco_b200_combine": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _vp, _i64, _vp],
     "disco_b200_backward_rows": [_vp, _i64, _i64, _int, _int, _i64, _i64, _vp],
     "disco_b200_combine_rows": [_vp, _i64, _i64, _int, _int, _f32, _int, _i64, _i64, _vp, _vp, _i64, _vp],
+    "disco_b200_peer_bytes": [_i64, _i64, _int, _int, ctypes.POINTER(_i64)],
+    "disco_b200_peer_handle_bytes": [],
+    "disco_b200_peer_alloc": [_i64, ctypes.POINTER(_vp), _vp],
+    "disco_b200_peer_open": [_vp, ctypes.POINTER(_vp)],
+    "disco_b200_peer_close": [_vp],
+    "disco_b200_peer_free": [_vp],
+    "disco_b200_backward_peer": [_vp, _i64, _i64, _int, _int, ctypes.POINTER(ctypes.c_uint64), _int,
+                                 ctypes.c_uint32, _vp],
+    "disco_b200_combine_peer": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _int, ctypes.c_uint32,
+                                ctypes.c_double, _vp, _vp, _i64, _vp],
     "disco_b200_contribution": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _vp, _i64, _vp],
     "disco_b200_loss": [_vp, _i64, _i64, _int, _int, _int, _vp],
     "disco_b200_logit_scale_rows": [_vp, _i64, _i64, _int, _int, _vp, _vp, _i64, _vp],

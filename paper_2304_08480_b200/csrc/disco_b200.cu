@@ -97,6 +97,7 @@ static_assert(sizeof(uint64_t) * 46 + 4 <= 512, "control block");
 constexpr int FLAG_INPUT_NONFINITE = 1;
 constexpr int FLAG_LOSS_NONFINITE = 2;
 constexpr int FLAG_GRAD_NONFINITE = 4;
+constexpr int FLAG_PEER_TIMEOUT = 8;  // peer transport: a peer's slabs never arrived (wait kernel gave up)
 
 struct Status {
   double loss;
@@ -141,6 +142,11 @@ struct GemmProblem {
   CUtensorMap out_map;    // 3-D fp32 store map {N, row_div, z}, box {32, 32, 1}
   int tma_store;          // 1: TMA stores through staging smem; 0: direct st.global
   int skip_store;         // profiling experiment (DISCO_DEBUG_FLAGS bit4): drain TMEM, store nothing
+  int ablate;             // profiling experiments: bit10 transform warps skip the rescale, bit11 no drain
+  // peer transport (N > 1): output rows of destination rank r = row / peer_b are TMA-stored straight
+  // into rank r's peer-mapped slab window through peer_map[r] (z = local partial index)
+  int peer, peer_b;
+  CUtensorMap peer_map[8];
   int paired;             // 1: unit = chunks (2kc, 2kc+1), summed in the epilogue
   int a_blocked;          // 1: A is a blocked G ([rows/128][cols/128][128][128], 4-D map)
   int a_mn_major, b_mn_major;
@@ -226,8 +232,8 @@ __device__ __forceinline__ uint8_t* smem_base(uint8_t* raw) {
 // warp-uniform (uniform registers), one elected lane issues the UMMAs and the commits.
 // Successive K=16 steps advance the descriptor start address by 32 B (K-major) or 2 KiB
 // (MN-major), i.e. by 2 or 128 in the descriptor's 16-byte units.
-template <int NB, bool XF = false>
-__device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<Ring<NB>::STAGES>& pipe, int nk,
+template <int NB, bool XF = false, int RS = Ring<NB>::STAGES>
+__device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>& pipe, int nk,
                                          uint32_t d_tmem, uint32_t idesc, int a_mn, int b_mn) {
   const uint64_t a_step = a_mn ? 128 : 2, b_step = b_mn ? 128 : 2;
   for (int kb = 0; kb < nk; ++kb) {
@@ -256,8 +262,8 @@ __device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<Ring
 // Producer side of one k-block: wait for the slot, arm the leader's barrier, load.
 // LOCAL (E-operand GEMMs): each CTA counts its own bytes on its own barrier, which its
 // transform warps wait on; otherwise the leader's barrier counts both CTAs' bytes.
-template <int NB, bool LOCAL = false>
-__device__ __forceinline__ uint8_t* producer_acquire(SmemCtl* ctl, uint8_t* tiles, Pipe<Ring<NB>::STAGES>& pipe,
+template <int NB, bool LOCAL = false, int RS = Ring<NB>::STAGES>
+__device__ __forceinline__ uint8_t* producer_acquire(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>& pipe,
                                                      bool leader, uint32_t& bar, uint32_t crank = 0) {
   ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
   if (LOCAL) {
@@ -748,15 +754,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 //   into the two TMEM buffers and summed in the epilogue ((c0 + c1): the first
 //   level of the fixed reduction tree).
 // =====================================================================
-template <int NB, bool XF>
+// SB = epilogue staging buffers per warp.  SB = 2 (wide units): the operand ring drops to 3
+// stages and the freed 48 KiB double-buffers the staging, so a warp fills one 4 KiB slice while
+// the TMA store of the previous one is still reading shared memory.
+template <int NB, bool XF, int SB = 1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF : NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ GemmParams p) {
-  constexpr int RS = Ring<NB>::STAGES;
+  constexpr int RS = SB == 2 ? 3 : Ring<NB>::STAGES;
   static_assert(NB == 1 || NB == 2, "one or two N tiles per unit");
+  static_assert(SB == 1 || (NB == 2 && RS * Ring<NB>::STAGE_BYTES + NUM_EPI_WARPS * SB * STAGING_TILE <=
+                                           TILE_RING_BYTES + STAGING_BYTES), "staging overlaps the control block");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
-  uint8_t* staging = tiles + TILE_RING_BYTES;
-  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(staging + STAGING_BYTES);
+  uint8_t* staging = tiles + (SB == 1 ? TILE_RING_BYTES : RS * Ring<NB>::STAGE_BYTES);
+  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + TILE_RING_BYTES + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int crank = int(ptx::cluster_ctarank());
   const bool leader = crank == 0;
@@ -766,7 +777,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     for (int i = 0; i < p.nprob; ++i) {
       ptx::prefetch_tmap(&p.prob[i].a_map);
       ptx::prefetch_tmap(&p.prob[i].b_map);
-      if (p.prob[i].tma_store) ptx::prefetch_tmap(&p.prob[i].out_map);
+      if (p.prob[i].tma_store && !p.prob[i].peer) ptx::prefetch_tmap(&p.prob[i].out_map);
+      for (int r = 0; r < (p.prob[i].peer ? p.prob[i].M / p.prob[i].peer_b : 0); ++r)
+        ptx::prefetch_tmap(&p.prob[i].peer_map[r]);
     }
   }
   kernel_prologue(ctl, warp, lane);
@@ -809,7 +822,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           k_range(q, kc * (1 + q.paired) + sub, k0, nk);
           for (int kb = 0; kb < nk; ++kb) {
             uint32_t bar;
-            uint8_t* st = producer_acquire<NB, XF>(ctl, tiles, pipe, leader, bar, crank);
+            uint8_t* st = producer_acquire<NB, XF, RS>(ctl, tiles, pipe, leader, bar, crank);
             const int k = k0 + kb * BK;
             if (q.a_blocked)
               load_blocked(&q.a_map, q.a_mn_major, st, bar, m0, k, BM, ptx::kEvictFirst);
@@ -841,7 +854,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           ptx::mbar_wait(&ctl->tempty[0], ((it >> 1) & 1) ^ 1);
           ptx::mbar_wait(&ctl->tempty[1], ((it >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
-          mma_tile<NB, XF>(ctl, tiles, pipe, nk, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major);
+          mma_tile<NB, XF, RS>(ctl, tiles, pipe, nk, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major);
           if (ptx::elect_one()) {
             ptx::umma_commit_pair(&ctl->tfull[0], 0x3);
             ptx::umma_commit_pair(&ctl->tfull[1], 0x3);
@@ -856,7 +869,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             const uint32_t buf = it & 1, use = it >> 1;
             ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
             ptx::tc_fence_after();
-            mma_tile<1, XF>(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, q.a_mn_major, q.b_mn_major);
+            mma_tile<1, XF, RS>(ctl, tiles, pipe, nk, ctl->tmem_base + buf * BN, idesc, q.a_mn_major, q.b_mn_major);
             if (ptx::elect_one()) ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
             __syncwarp();
           }
@@ -908,7 +921,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             const __half sc = sq[r];
             sq[r] = ld_scale(kb + XPF);
             ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
-            if (active) {
+            if (active && !(q.ablate & 1024)) {
               uint8_t* rowp = tiles + pipe.stage * Ring<NB>::STAGE_BYTES + rowoff;
               int lab_rel;
               float glab;
@@ -937,7 +950,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     const int ew = warp - 2;
     const int quad = warp & 3;
     const int chalf = ew >> 2;
-    uint8_t* tile = staging + ew * STAGING_BUFS * STAGING_TILE;
+    uint8_t* tile = staging + ew * SB * STAGING_TILE;
     uint32_t it = 0, gslice = 0;
     for (int u = pair; u < num_units; u += npairs) {
       int pi, mt, nt, kc;
@@ -959,7 +972,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       const int z = int(row0 / q.row_div) + kc;
       const int rlo = int(row0 % q.row_div);
 #pragma unroll 1
-      for (int jj = 0; jj < NB * (BN / 64); ++jj) {
+      for (int jj = 0; jj < ((q.ablate & 2048) ? 0 : NB * (BN / 64)); ++jj) {
         // NB = 2: slices 0..3 from accumulator 0 (columns [0,256)), 4..7 from accumulator 1
         const int j = jj % (BN / 64), acc = jj / (BN / 64);
         const int c0 = cbase + acc * BN + j * 32;
@@ -994,14 +1007,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           uint32_t w[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(v[i]);
-          uint8_t* stile = tile + (gslice % STAGING_BUFS) * STAGING_TILE;
-          if (lane == 0) ptx::bulk_wait_read<STAGING_BUFS - 1>();
+          uint8_t* stile = tile + (gslice % SB) * STAGING_TILE;
+          if (lane == 0) ptx::bulk_wait_read<SB - 1>();
           __syncwarp();
           ptx::st_swizzled_row(stile, lane, w);
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            if (row0 < q.M) ptx::tma_store_3d(&q.out_map, stile, c0, rlo, z);
+            if (q.peer) {  // NVLink push: this slice belongs to rank row0 / b
+              const int dest = row0 / q.peer_b;
+              if (row0 < q.M) ptx::tma_store_3d(&q.peer_map[dest], stile, c0, row0 - dest * q.peer_b, kc);
+            } else if (row0 < q.M) {
+              ptx::tma_store_3d(&q.out_map, stile, c0, rlo, z);
+            }
             ptx::bulk_commit();
           }
           ++gslice;
@@ -1238,9 +1256,12 @@ __global__ void presum_kernel(const float4* xpart, int np, int N, int b, int Dp,
 //   cross = tree over the N received slabs recv[src][g][r] (negated for src != rank if flip), or,
 //   single rank with canonical chunks (xpart != null), tree over the np local paired partials.
 // Rows [row0, row0 + nrows) only (row-block pipelining); outputs are indexed by the absolute row.
+// Peer transport: xpart = this rank's slab window [2][np leaves][b][Dp] (every source rank's chunk
+// partials, pushed by their cross GEMMs); leaves outside [own_lo, own_hi) came from other ranks.
 __global__ void combine_kernel(const float4* intra, int ksplit, const float4* recv, const float4* xpart, int np,
                                int N, int rank, int b, int Dp, int D, float s, int flip, float* d_image,
-                               float* d_text, int64_t ld_out, int row0, int nrows, Status* status) {
+                               float* d_text, int64_t ld_out, int row0, int nrows, Status* status, int own_lo = 0,
+                               int own_hi = 1 << 30) {
   const int v4 = Dp / 4;
   const bool vec_out = (ld_out % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_image) | reinterpret_cast<uintptr_t>(d_text)) % 16 == 0);
   const int64_t per_g = int64_t(b) * v4;
@@ -1254,7 +1275,10 @@ __global__ void combine_kernel(const float4* intra, int ksplit, const float4* re
     float4 cross;
     if (xpart) {
       const float4* src = xpart + (int64_t(g) * np) * per_g + rem;
-      cross = tree_sum(np, [&](int k) { return src[k * per_g]; });
+      cross = tree_sum(np, [&](int k) {
+        const float4 x = src[k * per_g];
+        return (flip && (k < own_lo || k >= own_hi)) ? f4neg(x) : x;
+      });
     } else {
       cross = tree_sum(N, [&](int src) {
         const float4 x = recv[((int64_t(src) * 2 + g) * b) * v4 + rem];
@@ -1321,6 +1345,45 @@ __global__ void contribution_kernel(const float4* intra, int ksplit, const float
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&status->flags, FLAG_GRAD_NONFINITE);
+}
+
+// ---------------------------------------------------------------- peer transport
+// Peer window of a rank (one cudaMalloc, IPC-exported): PEER_FLAG_BYTES of u32 arrival flags
+// (slot src = the epoch of the last step whose slabs source rank src pushed here), then two
+// parity windows of [2][L][b][Dp] f32 slabs (L = N * chunk partials per rank).  Step s writes
+// parity s & 1: a rank's push for step s + 1 can only start after its own combine of step s,
+// which waited for every peer's step-s arrival, so no window is overwritten while being read.
+constexpr int64_t PEER_FLAG_BYTES = 1024;
+struct PeerPtrs {
+  uint32_t* flag[8];  // &flags[rank] inside each destination's window
+};
+
+__global__ void peer_signal_kernel(PeerPtrs p, int n, uint32_t epoch) {
+  // the cross GEMM (previous kernel on this stream) completed its bulk stores; make them visible
+  // system-wide before the arrival flags
+  __threadfence_system();
+  const int r = threadIdx.x;
+  if (r < n) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.flag[r]), "r"(epoch) : "memory");
+}
+
+__global__ void peer_wait_kernel(const uint32_t* flags, int n, uint32_t epoch, Status* status,
+                                 unsigned long long timeout_ns) {
+  const int r = threadIdx.x;
+  if (r >= n) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
+    if (v == epoch) break;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {  // never hang the device: flag the step and let the host raise
+      atomicOr(&status->flags, FLAG_PEER_TIMEOUT);
+      break;
+    }
+    __nanosleep(256);
+  }
 }
 
 // Loss: sum of the [N][2][b] per-row ce in an order fixed by the global row
@@ -1665,6 +1728,7 @@ int set_output(GemmProblem& q, float* out, int64_t ld_out, int64_t row_div, int6
   q.chunk_stride = chunk_stride;
   q.tma_store = 0;
   q.skip_store = (debug_flag_bits() & 16) ? 1 : 0;
+  q.ablate = debug_flag_bits() & (1024 | 2048);
   const bool aligned = (row_div % 32 == 0) && (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                        !(debug_flag_bits() & 32);
   if (aligned && (nz_rows == 1 || nz_chunks == 1)) {
@@ -1823,11 +1887,11 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
 
 // wide = 1: every unit covers all N columns (n_tiles counts 512-column tiles), NB = 2 kernel.
 // xform = 1: A operands hold E (transform warps rescale to G in smem).
-template <int NB, bool XF>
+template <int NB, bool XF, int SB = 1>
 int launch_gemm_t(GemmParams& p, cudaStream_t st) {
   int rc;
-  if ((rc = prepare_kernel(gemm_kernel<NB, XF>))) return rc;
-  gemm_kernel<NB, XF><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS, SMEM_BYTES, st>>>(p);
+  if ((rc = prepare_kernel(gemm_kernel<NB, XF, SB>))) return rc;
+  gemm_kernel<NB, XF, SB><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS, SMEM_BYTES, st>>>(p);
   return DISCO_OK;
 }
 
@@ -1836,8 +1900,10 @@ int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform) {
   for (int i = 0; i < p.nprob; ++i)
     p.units[i + 1] = p.units[i] + p.prob[i].m_tiles * p.prob[i].n_tiles * p.prob[i].k_chunks;
   int rc;
+  const bool sb2 = debug_flag_bits() & 4096;  // experiment: 3-stage ring + double-buffered staging
   if (wide)
-    rc = xform ? launch_gemm_t<2, true>(p, st) : launch_gemm_t<2, false>(p, st);
+    rc = xform ? (sb2 ? launch_gemm_t<2, true, 2>(p, st) : launch_gemm_t<2, true>(p, st))
+               : (sb2 ? launch_gemm_t<2, false, 2>(p, st) : launch_gemm_t<2, false>(p, st));
   else
     rc = xform ? launch_gemm_t<1, true>(p, st) : launch_gemm_t<1, false>(p, st);
   if (rc) return rc;
@@ -1998,6 +2064,37 @@ int forward_finish(void* ws, const Geometry& g, cudaStream_t st) {
     count_launch();
     CUDA_TRY(cudaGetLastError());
   }
+  return DISCO_OK;
+}
+
+// ---------------------------------------------------------------- peer transport (host side)
+int64_t peer_leaves(const Geometry& g) { return int64_t(g.N) * g.np; }
+int64_t peer_window_bytes(const Geometry& g) { return round_up(2 * peer_leaves(g) * g.b * g.Dp * 4, 1024); }
+int64_t peer_total_bytes(const Geometry& g) { return PEER_FLAG_BYTES + 2 * peer_window_bytes(g); }
+float* peer_window(const void* base, const Geometry& g, int parity) {
+  return reinterpret_cast<float*>(const_cast<uint8_t*>(static_cast<const uint8_t*>(base)) + PEER_FLAG_BYTES +
+                                  int64_t(parity & 1) * peer_window_bytes(g));
+}
+int check_peer(const Geometry& g) {
+  if (g.N < 2 || g.N > 8) return fail(DISCO_LAYOUT_ERROR, "peer transport needs 2 <= world <= 8, got %d", g.N);
+  if (g.b % 128 != 0) return fail(DISCO_LAYOUT_ERROR, "peer transport needs b %% 128 == 0, got %lld", (long long)g.b);
+  return DISCO_OK;
+}
+
+// Cross problem `q` (gradient gi) pushes its chunk partials into every destination's window:
+// leaf (rank * np + kc) of [2][L][b][Dp], rows of destination r = output rows [r*b, (r+1)*b).
+int set_output_peer(GemmProblem& q, const uint64_t* bases, int parity, const Geometry& g, int gi) {
+  const int64_t L = peer_leaves(g);
+  for (int r = 0; r < g.N; ++r) {
+    const float* base = peer_window(reinterpret_cast<const void*>(bases[r]), g, parity) +
+                        ((int64_t(gi) * L + int64_t(g.rank) * g.np) * g.b) * g.Dp;
+    int rc = make_map_f32_3d(&q.peer_map[r], base, uint64_t(g.Dp), uint64_t(g.b), uint64_t(g.np), uint64_t(g.Dp),
+                             uint64_t(g.b * g.Dp));
+    if (rc) return rc;
+  }
+  q.peer = 1;
+  q.peer_b = int(g.b);
+  q.tma_store = 1;
   return DISCO_OK;
 }
 
@@ -2330,6 +2427,105 @@ int disco_b200_l2norm_rows_backward(const float* raw, int64_t ld_raw, const floa
   if (rows == 0) return DISCO_OK;
   l2norm_rows_backward_kernel<<<int((rows * 32 + 255) / 256), 256, 0, st_of(stream)>>>(
       raw, ld_raw, grad, ld_grad, int(rows), int(D), out, ld_out, flags);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+// ------------------------------------------------------------ peer transport
+int disco_b200_peer_bytes(int64_t B, int64_t D, int world, int rank, int64_t* bytes) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if ((rc = check_peer(g))) return rc;
+  *bytes = peer_total_bytes(g);
+  return DISCO_OK;
+}
+
+int disco_b200_peer_alloc(int64_t bytes, void** ptr, void* ipc_handle) {
+  if (bytes <= 0) return fail(DISCO_SHAPE_ERROR, "peer window size must be positive");
+  CUDA_TRY(cudaMalloc(ptr, size_t(bytes)));
+  CUDA_TRY(cudaMemset(*ptr, 0, size_t(PEER_FLAG_BYTES)));  // arrival flags start at epoch 0
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, *ptr);
+    if (e != cudaSuccess) {
+      cudaFree(*ptr);
+      *ptr = nullptr;
+      return fail(DISCO_CUDA_ERROR, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    }
+    memcpy(ipc_handle, &h, sizeof(h));
+  }
+  CUDA_TRY(cudaDeviceSynchronize());
+  return DISCO_OK;
+}
+
+int disco_b200_peer_handle_bytes(void) { return int(sizeof(cudaIpcMemHandle_t)); }
+
+int disco_b200_peer_open(const void* ipc_handle, void** ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return DISCO_OK;
+}
+
+int disco_b200_peer_close(void* ptr) {
+  CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return DISCO_OK;
+}
+
+int disco_b200_peer_free(void* ptr) {
+  CUDA_TRY(cudaFree(ptr));
+  return DISCO_OK;
+}
+
+int disco_b200_backward_peer(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
+                             int parity, uint32_t epoch, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if ((rc = check_peer(g))) return rc;
+  cudaStream_t st = st_of(stream);
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  if ((rc = build_intra(p, 0, ws, g))) return rc;  // list A: long units
+  if ((rc = build_cross(p, 2, ws, g))) return rc;  // list B: cross units, pushed to the owners
+  for (int gi = 0; gi < 2; ++gi)
+    if ((rc = set_output_peer(p.prob[2 + gi], peer_bases, parity, g, gi))) return rc;
+  p.nprob = 4;
+  p.split = 2;
+  if ((rc = launch_gemm(p, st, g.wide, g.estore))) return rc;
+  PeerPtrs pp;
+  memset(&pp, 0, sizeof(pp));
+  for (int r = 0; r < g.N; ++r)
+    pp.flag[r] = reinterpret_cast<uint32_t*>(peer_bases[r]) + rank;
+  peer_signal_kernel<<<1, 32, 0, st>>>(pp, g.N, epoch);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_combine_peer(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,
+                            const void* my_base, int parity, uint32_t epoch, double timeout_s, float* d_image,
+                            float* d_text, int64_t ld_out, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if ((rc = check_peer(g))) return rc;
+  if (ld_out < D) return fail(DISCO_SHAPE_ERROR, "output row stride smaller than D");
+  cudaStream_t st = st_of(stream);
+  Status* status = region<Status>(ws, g, DISCO_R_STATUS);
+  peer_wait_kernel<<<1, 32, 0, st>>>(static_cast<const uint32_t*>(my_base), g.N, epoch, status,
+                                     (unsigned long long)(timeout_s * 1e9));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  const float s = float(0.5 * double(t) / double(g.B));
+  const int64_t n = 2 * g.b * (g.Dp / 4);
+  const int L = int(peer_leaves(g));
+  combine_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
+      region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, nullptr,
+      reinterpret_cast<const float4*>(peer_window(my_base, g, parity)), L, g.N, g.rank, int(g.b), int(g.Dp),
+      int(g.D), s, flip, d_image, d_text, ld_out, 0, int(g.b), status, g.rank * g.np, (g.rank + 1) * g.np);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;

@@ -66,18 +66,39 @@ class _DoneWork:
 class ProcessGroupEndpoint:
     """One rank's handle over a torch.distributed process group."""
 
-    def __init__(self, group=None):
+    in_process = False
+
+    def __init__(self, group=None, peer=None):
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed is not initialized")
         self.group = group
         self.rank = dist.get_rank(group)
         self.world_size = dist.get_world_size(group)
+        self.peer = peer  # None: env DISCO_PEER decides (peer.enabled)
+        # gloo cannot move CUDA tensors: stage the device fast paths through host memory (tests)
+        self._host_staged = dist.get_backend(group) != "nccl"
+
+    def exchange(self, obj) -> list:
+        """All ranks' picklable objects, in rank order (peer-window handles)."""
+        out = [None] * self.world_size
+        dist.all_gather_object(out, obj, group=self.group)
+        return out
 
     # -- fast paths ------------------------------------------------------
     def all_gather_into(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        if self._host_staged and out.is_cuda:
+            h = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_gather_into_tensor(h, inp.cpu(), group=self.group)
+            out.copy_(h)
+            return
         dist.all_gather_into_tensor(out, inp, group=self.group)
 
     def all_to_all_into(self, out: torch.Tensor, inp: torch.Tensor, async_op: bool = False):
+        if self._host_staged and out.is_cuda:
+            h = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_to_all_single(h, inp.cpu(), group=self.group)
+            out.copy_(h)
+            return _DoneWork()
         work = dist.all_to_all_single(out, inp, group=self.group, async_op=async_op)
         return work if async_op else _DoneWork()
 
@@ -131,10 +152,11 @@ class _Round:
 class LocalGroup:
     """Rendezvous for ``world_size`` rank threads sharing one CUDA device."""
 
-    def __init__(self, world_size: int, timeout: float = DEFAULT_TIMEOUT):
+    def __init__(self, world_size: int, timeout: float = DEFAULT_TIMEOUT, peer=None):
         if world_size < 1:
             raise ValueError(f"world size must be >= 1, got {world_size}")
         self.world_size = world_size
+        self.peer = peer
         self.timeout = timeout
         self._cond = threading.Condition()
         self._round = None
@@ -216,9 +238,16 @@ def _done_event(device):
 class LocalEndpoint:
     """One simulated rank; owned by exactly one thread."""
 
+    in_process = True  # peer windows are shared as raw device pointers
+
     def __init__(self, group: LocalGroup, rank: int):
         self.group = group
         self.rank = rank
+        self.peer = group.peer
+
+    def exchange(self, obj) -> list:
+        """All ranks' objects, in rank order."""
+        return self.group.collective(self.rank, "exchange", obj, (), lambda slots: list(slots))
 
     @property
     def world_size(self) -> int:
@@ -329,13 +358,14 @@ class SingleEndpoint:
         return None
 
 
-def run_ranks(world_size: int, fn, *, device=None, timeout: float = DEFAULT_TIMEOUT) -> list:
+def run_ranks(world_size: int, fn, *, device=None, timeout: float = DEFAULT_TIMEOUT, peer=None,
+              own_streams: bool = False) -> list:
     """Run ``fn(endpoint)`` once per simulated rank (threads, one device); return results.
 
     Same contract as the reference's run_ranks (fabric.py:291-324): the first
     failing rank's exception is re-raised after all workers stop.
     """
-    group = LocalGroup(world_size, timeout=timeout)
+    group = LocalGroup(world_size, timeout=timeout, peer=peer)
     results = [None] * world_size
     errors = [None] * world_size
     dev = device if device is not None else (torch.cuda.current_device() if torch.cuda.is_available() else None)
@@ -344,7 +374,12 @@ def run_ranks(world_size: int, fn, *, device=None, timeout: float = DEFAULT_TIME
         try:
             if dev is not None:
                 torch.cuda.set_device(dev)
-            results[rank] = fn(group.endpoint(rank))
+            if own_streams:  # ranks progress independently (the peer transport waits on device flags)
+                with torch.cuda.stream(torch.cuda.Stream()):
+                    results[rank] = fn(group.endpoint(rank))
+                    torch.cuda.current_stream().synchronize()
+            else:
+                results[rank] = fn(group.endpoint(rank))
         except BaseException as exc:  # propagate to the caller, unblock peers
             errors[rank] = exc
             group.poison(exc)

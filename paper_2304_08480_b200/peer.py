@@ -1,0 +1,87 @@
+"""Peer transport: the cross-rank gradient exchange over NVLink peer memory.
+
+Replaces the reference's all_reduce(AVG) of the two B x D contributions + row slice
+(shard.py:199-208) -- realised on the default path as an NCCL all_to_all of fp32 slabs plus a
+fixed-order tree -- by pushes from inside the backward GEMM: each cross tile's epilogue
+TMA-stores its chunk partial straight into the owning rank's peer window, a one-warp kernel
+publishes an arrival epoch to every owner, and the owner's combine waits for all N epochs and
+sums the leaves in the same fixed tree (include/disco_b200.h, "Peer transport").  The result is
+bit-identical to the all_to_all path and to N = 1.
+
+Windows are one cudaMalloc per rank (disco_b200_peer_alloc).  Across processes the bases are
+shared as CUDA IPC handles through the endpoint's object exchange; simulated ranks (threads of
+one process, ``LocalGroup(peer=True)``) share raw device pointers.
+"""
+
+import ctypes
+import os
+
+from . import _lib
+
+# wait-kernel bound: a missing peer sets status flag 8 (CollectiveTimeoutError) instead of a hang
+PEER_TIMEOUT_S = float(os.environ.get("DISCO_PEER_TIMEOUT", "60"))
+
+
+def enabled(endpoint) -> bool:
+    """Peer transport on for this endpoint: ``endpoint.peer`` if set, else env DISCO_PEER=1."""
+    flag = getattr(endpoint, "peer", None)
+    if flag is None:
+        flag = os.environ.get("DISCO_PEER", "0") not in ("", "0")
+    return bool(flag) and endpoint.world_size > 1
+
+
+def supported(B: int, D: int, world: int, rank: int) -> bool:
+    if world < 2 or world > 8 or B % world or (B // world) % 128:
+        return False
+    return True
+
+
+class PeerWindow:
+    """This rank's peer window and the N window bases (index = rank) for one plan geometry."""
+
+    def __init__(self, endpoint, B: int, D: int, world: int, rank: int):
+        lib = _lib.load()
+        self.world, self.rank = world, rank
+        nbytes = ctypes.c_int64()
+        _lib.call("disco_b200_peer_bytes", B, D, world, rank, ctypes.byref(nbytes))
+        self.nbytes = nbytes.value
+        in_process = getattr(endpoint, "in_process", False)
+        handle = None if in_process else ctypes.create_string_buffer(lib.disco_b200_peer_handle_bytes())
+        ptr = ctypes.c_void_p()
+        _lib.call("disco_b200_peer_alloc", self.nbytes, ctypes.byref(ptr), handle)
+        self.base = ptr.value
+        self._opened = []
+        try:
+            if in_process:
+                bases = endpoint.exchange(self.base)
+            else:
+                handles = endpoint.exchange(bytes(handle.raw))
+                bases = []
+                for r, h in enumerate(handles):
+                    if r == rank:
+                        bases.append(self.base)
+                        continue
+                    p = ctypes.c_void_p()
+                    _lib.call("disco_b200_peer_open", ctypes.create_string_buffer(h, len(h)), ctypes.byref(p))
+                    self._opened.append(p.value)
+                    bases.append(p.value)
+        except BaseException:
+            self.close()
+            raise
+        self.bases = (ctypes.c_uint64 * world)(*bases)
+        self.epoch = 0
+        endpoint.barrier()  # every window's arrival flags are zeroed before any rank signals
+
+    def next_step(self):
+        """(epoch, parity) of the next step; every rank advances in lockstep."""
+        self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 1
+        return self.epoch, self.epoch & 1
+
+    def close(self) -> None:
+        lib = _lib.load()
+        for p in self._opened:
+            lib.disco_b200_peer_close(ctypes.c_void_p(p))
+        self._opened = []
+        if self.base:
+            lib.disco_b200_peer_free(ctypes.c_void_p(self.base))
+            self.base = None

@@ -34,8 +34,9 @@ import numpy as np
 import torch
 
 from . import _lib
+from . import peer as _peer
 from .counters import Counters, tracking
-from .errors import DomainError, LayoutError, ShapeError
+from .errors import CollectiveTimeoutError, DomainError, LayoutError, ShapeError
 from .fabric import SingleEndpoint
 
 
@@ -142,6 +143,24 @@ class Plan:
         self._copy_stream = None
         self._h2d_stream = None
         self._wave_stream = None
+        self._peer = None
+        self._peer_group = None
+
+    def peer_window(self, endpoint) -> "_peer.PeerWindow":
+        """This rank's peer-transport window (created, and exchanged with the peers, on first use)."""
+        group = getattr(endpoint, "group", None)
+        if self._peer is not None and self._peer_group is not group:  # a new group: new windows
+            self.close()
+        if self._peer is None:
+            self._peer = _peer.PeerWindow(endpoint, self.B, self.D, self.world, self.rank)
+            self._peer_group = group
+        return self._peer
+
+    def close(self) -> None:
+        if self._peer is not None:
+            torch.cuda.synchronize(self.device)
+            self._peer.close()
+            self._peer = None
 
     def copy_stream(self) -> "torch.cuda.Stream":
         """Side stream for the pipelined device->host gradient copies (created on first use)."""
@@ -150,10 +169,11 @@ class Plan:
         return self._copy_stream
 
     def h2d_streams(self):
-        """(host->device copy stream, second compute stream) of the wavefront forward."""
+        """(host->device copy stream, extra compute streams) of the wavefront forward: waves
+        rotate over the current stream and these, so a wave's tail overlaps the next ones."""
         if self._h2d_stream is None:
             self._h2d_stream = torch.cuda.Stream(self.device)
-            self._wave_stream = torch.cuda.Stream(self.device)
+            self._wave_stream = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
         return self._h2d_stream, self._wave_stream
 
     @property
@@ -176,6 +196,8 @@ def get_plan(B: int, D: int, world: int, rank: int, device: torch.device) -> Pla
 
 def clear_plans() -> None:
     with _plans_lock:
+        for plan in _plans.values():
+            plan.close()
         _plans.clear()
 
 
@@ -270,6 +292,9 @@ def _raise_on_flags(flags: int) -> None:
         raise ValueError("cross-entropy logits contains non-finite entries")
     if flags & 4:
         raise ValueError("gradient contribution contains non-finite entries")
+    if flags & 8:
+        raise CollectiveTimeoutError(
+            f"peer transport: gradient slabs did not arrive within {_peer.PEER_TIMEOUT_S:g}s")
 
 
 def _check_t(t) -> float:
@@ -350,14 +375,23 @@ def _account_loss_scope(loss_counters, exchange_counters, b, B, D) -> None:
         loss_counters.release(2 * b * B)
 
 
+# Fractions of the 256-row tiles per output row block of the pipelined backward: quarters, the
+# last one halved so the exposed device->host tail is short (measured best of several schedules
+# with tools/e2e_timeline.py --sweep: shorter blocks cost more GEMM efficiency than they hide).
+ROW_BLOCK_FRACTIONS = (0.25, 0.25, 0.25, 0.125, 0.125)
+
+
 def row_blocks(b: int):
-    """Output row blocks of the single-rank pipelined backward: quarters of the 256-row
-    tiles, the last quarter halved so the exposed device->host tail is short."""
+    """Output row blocks of the single-rank pipelined backward (ROW_BLOCK_FRACTIONS of the
+    256-row tiles; one block for small b)."""
     tiles = (b + 255) // 256
     if tiles < 8:
         return [(0, b)]
-    q = tiles // 4
-    cuts = [0, q, 2 * q, 3 * q, 3 * q + (tiles - 3 * q) // 2, tiles]
+    cuts, acc = [0], 0.0
+    for f in ROW_BLOCK_FRACTIONS[:-1]:
+        acc += f
+        cuts.append(max(cuts[-1] + 1, min(tiles - 1, round(acc * tiles))))
+    cuts.append(tiles)
     return [(min(256 * lo, b), min(256 * hi, b)) for lo, hi in zip(cuts, cuts[1:]) if hi > lo]
 
 
@@ -377,28 +411,28 @@ def _pipelined_pack_forward(plan: Plan, I_host: torch.Tensor, T_host: torch.Tens
     _lib.call("disco_b200_pack_rows", *plan.args, I_dev.data_ptr(), T_dev.data_ptr(), D, D, code, 1, 0, 0,
               cur.cuda_stream)
     h2d.wait_stream(cur)
-    side.wait_stream(cur)
+    for s in side:
+        s.wait_stream(cur)
     rows = b // plan.waves
-    landed = []
-    with torch.cuda.stream(h2d):
-        for k in range(plan.waves):
-            sl = slice(k * rows, (k + 1) * rows)
+    streams = (cur,) + side
+    for k in range(plan.waves):  # enqueue copy k, then its wave, so wave 0 launches early
+        sl = slice(k * rows, (k + 1) * rows)
+        with torch.cuda.stream(h2d):
             I_dev[sl].copy_(I_host[sl], non_blocking=True)
             T_dev[sl].copy_(T_host[sl], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(h2d)
-            landed.append(ev)
-    streams = (cur, side)
-    for k in range(plan.waves):
-        s = streams[k % 2]
-        s.wait_event(landed[k])
+        landed = torch.cuda.Event()
+        landed.record(h2d)
+        s = streams[k % len(streams)]
+        s.wait_event(landed)
         _lib.call("disco_b200_pack_rows", *plan.args, I_dev.data_ptr(), T_dev.data_ptr(), D, D, code, 0,
                   k * rows, (k + 1) * rows, s.cuda_stream)
         _lib.call("disco_b200_forward_wave", *plan.args, t, k, s.cuda_stream)
-    cur.wait_stream(side)
+    for s in side:
+        cur.wait_stream(s)
     for x in (I_dev, T_dev):
         x.record_stream(h2d)
-        x.record_stream(side)
+        for s in side:
+            x.record_stream(s)
     _lib.call("disco_b200_forward_finish", *plan.args, cur.cuda_stream)
 
 
@@ -442,7 +476,13 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
             endpoint.all_gather_into(plan.gather, plan.pack)
         _lib.call("disco_b200_forward", *plan.args, t, st)
     _lib.call("disco_b200_backward_grad", *plan.args, t, st)
-    if N > 1:
+    pw = None
+    if N > 1 and _peer.enabled(endpoint) and _peer.supported(B, D, N, n):
+        # peer transport: the fused backward GEMM pushes each cross tile to its owner over NVLink
+        pw = plan.peer_window(endpoint)
+        epoch, parity = pw.next_step()
+        _lib.call("disco_b200_backward_peer", *plan.args, pw.bases, parity, epoch, st)
+    elif N > 1:
         # cross first, so the slab exchange overlaps the intra GEMM
         _lib.call("disco_b200_backward_cross", *plan.args, st)
         work = endpoint.all_to_all_into(plan.recv, plan.send, async_op=True)
@@ -465,6 +505,9 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
                 h_text[r0:r1].copy_(d_text[r0:r1], non_blocking=True)
         d_image.record_stream(cs)
         d_text.record_stream(cs)
+    elif pw is not None:
+        _lib.call("disco_b200_combine_peer", *plan.args, t, flip, pw.base, parity, epoch, _peer.PEER_TIMEOUT_S,
+                  d_image.data_ptr(), d_text.data_ptr(), D, st)
     else:
         if N == 1:
             _lib.call("disco_b200_backward_fused", *plan.args, st)

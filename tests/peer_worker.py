@@ -1,0 +1,41 @@
+"""One rank of tests/test_gpu_peer.py::test_peer_two_processes_ipc (not collected by pytest).
+
+Both ranks share cuda:0; the process group is gloo (host plumbing: the feature all_gather and
+the per-row loss all_gather are staged through host memory), the gradient exchange is the peer
+transport over CUDA IPC-mapped windows.  Two steps, so both parity windows are used.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2304_08480_b200 as P  # noqa: E402
+
+
+def main(out_dir):
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ep = P.ProcessGroupEndpoint(peer=True)
+    I = np.load(os.path.join(out_dir, "I.npy"))
+    T = np.load(os.path.join(out_dir, "T.npy"))
+    b = I.shape[0] // world
+    Id = torch.from_numpy(I[rank * b:(rank + 1) * b]).cuda()
+    Td = torch.from_numpy(T[rank * b:(rank + 1) * b]).cuda()
+    for _ in range(2):
+        di, dt, loss = P.disco_step(ep, Id, Td, 100.0)
+    np.save(os.path.join(out_dir, f"di{rank}.npy"), di.cpu().numpy())
+    np.save(os.path.join(out_dir, f"dt{rank}.npy"), dt.cpu().numpy())
+    np.save(os.path.join(out_dir, f"loss{rank}.npy"), np.array(loss))
+    ep.barrier()
+    from paper_2304_08480_b200.shard import clear_plans
+    clear_plans()
+    ep.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
