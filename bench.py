@@ -297,8 +297,12 @@ def run_ours(args):
     value = B / (ms / 1e3)
 
     # ---- kernel breakdown: events around each C-ABI call (one tensor-core kernel each)
+    from paper_2304_08480_b200 import peer as peer_mod
+    use_peer = world > 1 and peer_mod.enabled(ep) and peer_mod.supported(B, D, world, rank)
     if world == 1:  # the step runs intra + cross as one fused launch
         names = ["pack", "forward", "backward_grad", "backward", "combine", "loss"]
+    elif use_peer:  # fused intra + cross GEMM pushing cross tiles to the owners over NVLink
+        names = ["pack", "all_gather", "forward", "backward_grad", "backward_peer", "combine_peer", "loss"]
     else:
         names = ["pack", "all_gather", "forward", "backward_grad", "backward_cross", "all_to_all",
                  "backward_intra", "combine", "loss"]
@@ -325,6 +329,12 @@ def run_ours(args):
         timed("forward", lambda: _lib.call("disco_b200_forward", *args_, t, sp))
         timed("backward_grad", lambda: _lib.call("disco_b200_backward_grad", *args_, t, sp))
         timed("backward", lambda: _lib.call("disco_b200_backward_fused", *args_, sp))
+        if use_peer:
+            pw = plan.peer_window(ep)
+            epoch, parity = pw.next_step()
+            timed("backward_peer", lambda: _lib.call("disco_b200_backward_peer", *args_, pw.bases, parity, epoch, sp))
+            timed("combine_peer", lambda: _lib.call("disco_b200_combine_peer", *args_, t, 0, pw.base, parity, epoch,
+                                                    peer_mod.PEER_TIMEOUT_S, di.data_ptr(), dt_.data_ptr(), D, sp))
         timed("backward_cross", lambda: _lib.call("disco_b200_backward_cross", *args_, sp))
         timed("all_to_all", lambda: ep.all_to_all_into(plan.recv, plan.send))
         timed("backward_intra", lambda: _lib.call("disco_b200_backward_intra", *args_, sp))
@@ -383,6 +393,8 @@ def run_ours(args):
         kernels["logits_grad"] = (phases["backward_grad"], "hbm", g_bytes, "GB/s", hbm)
     if world == 1:
         kernels["gemm_backward"] = (phases["backward"], "tensor", 2 * mm, "TFLOP/s", sustained)
+    elif use_peer:
+        kernels["gemm_backward_peer"] = (phases["backward_peer"], "tensor", 2 * mm, "TFLOP/s", sustained)
     else:
         kernels["gemm_cross"] = (phases["backward_cross"], "tensor", mm, "TFLOP/s", sustained)
         kernels["gemm_intra"] = (phases["backward_intra"], "tensor", mm, "TFLOP/s", sustained)
@@ -414,6 +426,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"B={B},D={D},t={TEMP} (BASELINE config {args.config})", "global_batch": B,
                    "local_batch": b, "dim": D, "parallelism": f"dp{world}",
+                   "exchange": ("none" if world == 1 else
+                                "peer (GEMM epilogue TMA pushes over NVLink)" if use_peer else "nccl all_to_all"),
                    "l2": "flushed between steps (512 MB write, outside timed events)"},
         "loss": loss,
         "peak_loss_mem_gb": loss_mem / 1e9,

@@ -152,7 +152,7 @@ class _Round:
 class LocalGroup:
     """Rendezvous for ``world_size`` rank threads sharing one CUDA device."""
 
-    def __init__(self, world_size: int, timeout: float = DEFAULT_TIMEOUT, peer=None):
+    def __init__(self, world_size: int, timeout: float = DEFAULT_TIMEOUT, peer: bool = False):
         if world_size < 1:
             raise ValueError(f"world size must be >= 1, got {world_size}")
         self.world_size = world_size
@@ -358,14 +358,17 @@ class SingleEndpoint:
         return None
 
 
-def run_ranks(world_size: int, fn, *, device=None, timeout: float = DEFAULT_TIMEOUT, peer=None,
+def run_ranks(world_size: int, fn, *, device=None, timeout: float = DEFAULT_TIMEOUT, peer: bool = False,
               own_streams: bool = False) -> list:
     """Run ``fn(endpoint)`` once per simulated rank (threads, one device); return results.
 
     Same contract as the reference's run_ranks (fabric.py:291-324): the first
-    failing rank's exception is re-raised after all workers stop.
+    failing rank's exception is re-raised after all workers stop.  ``peer=True`` routes the
+    gradient exchange through the peer transport (windows shared as device pointers); each rank
+    thread then runs on its own CUDA stream.
     """
     group = LocalGroup(world_size, timeout=timeout, peer=peer)
+    own_streams = own_streams or peer  # the peer transport's wait kernels need independent rank streams
     results = [None] * world_size
     errors = [None] * world_size
     dev = device if device is not None else (torch.cuda.current_device() if torch.cuda.is_available() else None)

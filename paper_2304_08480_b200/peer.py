@@ -23,10 +23,11 @@ PEER_TIMEOUT_S = float(os.environ.get("DISCO_PEER_TIMEOUT", "60"))
 
 
 def enabled(endpoint) -> bool:
-    """Peer transport on for this endpoint: ``endpoint.peer`` if set, else env DISCO_PEER=1."""
+    """Peer transport on for this endpoint: ``endpoint.peer`` if set, else env DISCO_PEER
+    (default on; DISCO_PEER=0 selects the NCCL all_to_all + sender presum exchange)."""
     flag = getattr(endpoint, "peer", None)
     if flag is None:
-        flag = os.environ.get("DISCO_PEER", "0") not in ("", "0")
+        flag = os.environ.get("DISCO_PEER", "1") not in ("", "0")
     return bool(flag) and endpoint.world_size > 1
 
 

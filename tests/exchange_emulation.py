@@ -46,8 +46,11 @@ def rows_blockwise(fn, n_rows, block=128):
     return np.concatenate([fn(slice(s, min(s + block, n_rows))) for s in range(0, n_rows, block)], axis=0)
 
 
-def local_phase(rank, N, I, T, t):
-    """Everything before the exchange on one rank: G blocks, intra terms, slabs, per-row ce."""
+def local_phase(rank, N, I, T, t, leaves=False):
+    """Everything before the exchange on one rank: G blocks, intra terms, slabs, per-row ce.
+
+    leaves=True (peer transport): instead of the presummed slabs, return the rank's chunk
+    partials (pair level applied) as [np][2][B][D] -- what the GEMM pushes to the owners."""
     B, D = I.shape
     b = B // N
     nch, cpr = chunking(B, N)
@@ -76,7 +79,7 @@ def local_phase(rank, N, I, T, t):
         ce.append(np.log(np.exp(S_loc - mx[:, None]).sum(axis=1)) + mx - S_loc[np.arange(b), lab])
     # gradient index g: image (0) <- intra G_i.T_g, cross G_t^T.T_n ; text (1) <- G_t.I_g, G_i^T.I_n
     intra = [rows_blockwise(lambda sl: G[0][sl] @ feats[1], b), rows_blockwise(lambda sl: G[1][sl] @ feats[0], b)]
-    slabs = []
+    slabs, leaf_parts = [], []
     for g in range(2):
         Gd, Ad = (G[1], feats[1]) if g == 0 else (G[0], feats[0])
         parts = []
@@ -86,7 +89,11 @@ def local_phase(rank, N, I, T, t):
             parts.append(Gd[r0:r1].T @ Ad[lo + r0:lo + r1])     # B x D, one canonical chunk
         if cpr >= 2:
             parts = [parts[2 * i] + parts[2 * i + 1] for i in range(cpr // 2)]
+        leaf_parts.append(parts)
         slabs.append(tree(parts))
+    if leaves:
+        lv = np.stack([np.stack([leaf_parts[g][k] for g in range(2)]) for k in range(len(leaf_parts[0]))])
+        return np.stack(intra), lv.astype(np.float32), np.stack(ce).astype(np.float32)
     send = np.stack([np.stack([slabs[g][dst * b:(dst + 1) * b] for g in range(2)]) for dst in range(N)])
     return np.stack(intra), send.astype(np.float32), np.stack(ce).astype(np.float32)
 
@@ -114,6 +121,24 @@ def run_single_process(N, I, T, t):
     for r in range(N):
         recv = np.stack([outs[src][1][r] for src in range(N)])
         grads.append(owner_phase(r, N, t, B, outs[r][0], recv))
+    d_image = np.concatenate([g[0] for g in grads])
+    d_text = np.concatenate([g[1] for g in grads])
+    loss = loss_from(np.stack([o[2] for o in outs]), N, b)
+    return d_image, d_text, loss
+
+
+def run_single_process_peer(N, I, T, t):
+    """Peer transport: every rank pushes its leaves (no sender presum) into the owners' windows
+    [2][L][b][D] (leaf src*np + k); the owner's tree runs over all L = N*np leaves."""
+    B = I.shape[0]
+    b = B // N
+    outs = [local_phase(r, N, I, T, t, leaves=True) for r in range(N)]
+    s = np.float32(0.5 * t / B)
+    grads = []
+    for r in range(N):
+        window = [[outs[src][1][k][g][r * b:(r + 1) * b] for src in range(N) for k in range(outs[src][1].shape[0])]
+                  for g in range(2)]
+        grads.append([(outs[r][0][g] + tree(window[g])) * s for g in range(2)])
     d_image = np.concatenate([g[0] for g in grads])
     d_text = np.concatenate([g[1] for g in grads])
     loss = loss_from(np.stack([o[2] for o in outs]), N, b)

@@ -94,3 +94,27 @@ def test_loss_memory_scales_as_b_squared_over_n():
 
 def test_launch_counter_starts_at_zero_without_gpu():
     assert _lib.launch_count() >= 0
+
+
+def test_peer_window_geometry():
+    """Peer window = flag block + two parity windows of [2][N*np][b][Dp] f32 (every source's leaves)."""
+    out = ctypes.c_int64()
+    lib = _lib.load()
+    assert lib.disco_b200_peer_handle_bytes() == 64
+    for B, D, N, leaves in [(32768, 512, 8, 8), (32768, 512, 2, 8), (65536, 768, 4, 4), (3072, 256, 3, 3)]:
+        _lib.call("disco_b200_peer_bytes", B, D, N, 0, ctypes.byref(out))
+        b, Dp = B // N, (D + 63) // 64 * 64
+        win = (2 * leaves * b * Dp * 4 + 1023) // 1024 * 1024
+        assert out.value == 1024 + 2 * win, (B, D, N)
+    with pytest.raises(LayoutError):  # nothing to exchange at N = 1
+        _lib.call("disco_b200_peer_bytes", 4096, 512, 1, 0, ctypes.byref(out))
+    with pytest.raises(LayoutError):  # b % 128 != 0
+        _lib.call("disco_b200_peer_bytes", 4096 + 64 * 2, 512, 2, 0, ctypes.byref(out))
+
+
+def test_wavefront_forward_availability():
+    """The H2D-pipelined forward needs a single rank and B % 2048 == 0 (256-row tiles per chunk)."""
+    assert _lib.forward_waves(32768, 512, 1, 0) == 8
+    assert _lib.forward_waves(2048, 64, 1, 0) == 8
+    assert _lib.forward_waves(3072, 512, 1, 0) == 0
+    assert _lib.forward_waves(32768, 512, 2, 0) == 0

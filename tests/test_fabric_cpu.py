@@ -97,6 +97,66 @@ def test_emulated_exchange_is_bitwise_invariant_across_world_sizes(problem):
         assert got[2] == base[2]
 
 
+def test_peer_transport_tree_is_bitwise_the_all_to_all_tree(problem):
+    """Peer transport order (leaves pushed un-presummed, owner tree over N*np leaves) equals the
+    all_to_all order (sender presum, owner tree over sources) bit for bit, at every N."""
+    I, T, t = problem
+    base = E.run_single_process(1, I, T, t)
+    for N in (2, 4, 8):
+        got = E.run_single_process_peer(N, I, T, t)
+        assert got[0].tobytes() == base[0].tobytes(), N
+        assert got[1].tobytes() == base[1].tobytes(), N
+    I2, T2 = O.synthetic_features(96, 8, 1)  # non-canonical chunking (N chunks)
+    for N in (2, 3):
+        a = E.run_single_process(N, I2, T2, t)
+        b = E.run_single_process_peer(N, I2, T2, t)
+        assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
+
+
+def _exchange_worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ep = P.ProcessGroupEndpoint(peer=True)
+        got = ep.exchange(bytes([rank]) * 64)  # a peer-window IPC handle is 64 opaque bytes
+        np.save(os.path.join(outdir, f"x{rank}.npy"), np.frombuffer(b"".join(got), dtype=np.uint8))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_handle_exchange(tmp_path):
+    world = 2
+    mp.start_processes(_exchange_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       start_method="spawn")
+    want = np.frombuffer(bytes([0]) * 64 + bytes([1]) * 64, dtype=np.uint8)
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"x{r}.npy"), want)
+
+
+def test_peer_transport_switch(monkeypatch):
+    from paper_2304_08480_b200 import peer
+
+    g = P.LocalGroup(2, peer=True)
+    assert peer.enabled(g.endpoint(0))
+    assert not peer.enabled(P.LocalGroup(2, peer=False).endpoint(1))
+    assert not peer.enabled(P.LocalGroup(1, peer=True).endpoint(0))  # nothing to exchange at N = 1
+    assert not peer.enabled(P.LocalGroup(4).endpoint(0))  # simulated ranks: opt-in
+
+    class PG:  # a process-group endpoint without an explicit choice follows DISCO_PEER
+        world_size, peer = 4, None
+
+    monkeypatch.delenv("DISCO_PEER", raising=False)
+    assert peer.enabled(PG())  # default: on
+    monkeypatch.setenv("DISCO_PEER", "0")
+    assert not peer.enabled(PG())
+    assert peer.supported(32768, 512, 8, 0) and peer.supported(2048, 256, 2, 1)
+    assert not peer.supported(32768, 512, 16, 0) and not peer.supported(1000, 512, 2, 0)
+    assert not peer.supported(4096, 64, 64, 0)
+    res = P.run_ranks(3, lambda ep: ep.exchange(ep.rank * 10))
+    assert res == [[0, 10, 20]] * 3
+
+
 def test_local_group_threads_on_cpu_tensors():
     def fn(ep):
         x = torch.full((1, 2), float(ep.rank))
