@@ -345,6 +345,7 @@ def run_ours(args):
         for n in names:
             acc[n] += ev[n][0].elapsed_time(ev[n][1]) / reps
     phases = {n: round(v, 4) for n, v in acc.items()}
+    kernel_mhz = _lib.clock_probe(plan)  # SM clock the last timed launches actually ran at
 
     # ---- e2e through the public API with host buffers ---------------------
     e2e = None
@@ -445,7 +446,8 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": dict(clk.summary(), in_kernel_mhz=kernel_mhz,
+                       in_kernel_note="clock64 / globaltimer stamps of CTA 0 (NVML reports the target clock)"),
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -215,6 +215,11 @@ int disco_b200_logit_scale_rows(void* ws, int64_t B, int64_t D, int world, int r
                                 const float* d_text, int64_t ld_out, void* stream);
 int disco_b200_logit_scale_grad(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
 
+/* Profiling aid (synchronous): the SM clock in MHz at which CTA 0 of the last logits kernel
+ * (mhz[0]) and of the last backward GEMM (mhz[1]) ran, from clock64 / globaltimer stamps the
+ * kernels write into the status block; 0 if not run.  Shows the power-capped effective clock. */
+int disco_b200_clock_probe(void* ws, int64_t B, int64_t D, int world, int rank, double* mhz);
+
 /* Tower side of the two-tower trainer (reference towers.py:148-157):
  * row L2 normalisation of raw tower outputs (matrix.py:165-176) and its backward
  * (matrix.py:178-195), fp32, one warp per row.  flags (device int, may be NULL):

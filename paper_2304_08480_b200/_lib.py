@@ -64,6 +64,7 @@ SIGNATURES = {
                                  ctypes.c_uint32, _vp],
     "disco_b200_combine_peer": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _int, ctypes.c_uint32,
                                 ctypes.c_double, _vp, _vp, _i64, _vp],
+    "disco_b200_clock_probe": [_vp, _i64, _i64, _int, _int, ctypes.POINTER(ctypes.c_double)],
     "disco_b200_contribution": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _vp, _i64, _vp],
     "disco_b200_loss": [_vp, _i64, _i64, _int, _int, _int, _vp],
     "disco_b200_logit_scale_rows": [_vp, _i64, _i64, _int, _int, _vp, _vp, _i64, _vp],
@@ -150,6 +151,13 @@ def forward_waves(B: int, D: int, world: int, rank: int) -> int:
     out = _int()
     call("disco_b200_forward_waves", B, D, world, rank, ctypes.byref(out))
     return out.value
+
+
+def clock_probe(plan) -> dict:
+    """SM clock (MHz) the last logits kernel / backward GEMM ran at (CTA 0 stamps)."""
+    out = (ctypes.c_double * 2)()
+    call("disco_b200_clock_probe", *plan.args, out)
+    return {"logits_fwd": round(out[0], 1), "gemm_backward": round(out[1], 1)}
 
 
 def launch_count() -> int:

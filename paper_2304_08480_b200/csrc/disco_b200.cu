@@ -105,6 +105,9 @@ struct Status {
   int pad;
   double dlogit;             // dL/d(logit scale), disco_b200_logit_scale_grad
   double loss_partial[128];  // loss_partial_kernel scratch (LOSS_BLOCKS)
+  // clock probe (CTA 0 of the tensor-core kernels): {SM clock64, globaltimer ns} at entry and exit,
+  // [0..3] logits kernel, [4..7] backward GEMM -> the SM clock the kernel actually ran at
+  unsigned long long probe[8];
 };
 
 // ----------------------------------------------------------- kernel params
@@ -134,6 +137,7 @@ struct LogitsParams {
   // chunk is `wave` and the other index <= wave, i.e. the units that became computable when
   // canonical chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per chunk.
   int wave, rt_per_chunk;
+  unsigned long long* probe;  // Status::probe (may be null)
 };
 
 struct GemmProblem {
@@ -178,6 +182,7 @@ struct GemmParams {
   // proportion to their unit counts (Bresenham), so pairs walking the unit sequence with a
   // stride of #pairs see A and B units in different phases (spreads the accumulator drains).
   int split;
+  unsigned long long* probe;  // Status::probe + 4 (may be null)
 };
 
 // --------------------------------------------------------- shared helpers
@@ -296,6 +301,16 @@ __device__ __forceinline__ void xform_row(uint8_t* rowp, int sw, __half sc, int 
     *reinterpret_cast<__half*>(rowp + ((((lab_rel >> 3) ^ sw)) << 4) + (lab_rel & 7) * 2) = __float2half_rn(glab);
 }
 
+// Clock probe: CTA 0, thread 0 records {clock64, globaltimer} at slot [at, at + 1].
+__device__ __forceinline__ void probe_mark(unsigned long long* probe, int at) {
+  if (probe && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    probe[at] = clock64();
+    probe[at + 1] = t;
+  }
+}
+
 __device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane) {
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {  // the NB=2 ring uses the first Ring<2>::STAGES
@@ -377,6 +392,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       ptx::prefetch_tmap(&p.b_map[d]);
     }
   }
+  probe_mark(p.probe, 0);
   kernel_prologue(ctl, warp, lane);
 
   constexpr bool CHUNK_UNITS = KIND != KIND_GRAD;  // unit = all tiles of one column chunk
@@ -745,6 +761,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (KIND != KIND_FWD && lane == 0) ptx::bulk_wait_all();  // drain any bulk stores
   }
   kernel_epilogue(ctl, warp);
+  probe_mark(p.probe, 2);
 }
 
 // =====================================================================
@@ -782,6 +799,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
         ptx::prefetch_tmap(&p.prob[i].peer_map[r]);
     }
   }
+  probe_mark(p.probe, 0);
   kernel_prologue(ctl, warp, lane);
 
   const int num_units = p.units[p.nprob];
@@ -1040,6 +1058,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     if (lane == 0) ptx::bulk_wait_all();
   }
   kernel_epilogue(ctl, warp);
+  probe_mark(p.probe, 2);
 }
 
 __global__ void __launch_bounds__(NUM_THREADS_XF, 1) cluster_probe_kernel() {}
@@ -1666,6 +1685,10 @@ T* region(void* ws, const Geometry& g, int r) {
   return reinterpret_cast<T*>(static_cast<uint8_t*>(ws) + g.off[r]);
 }
 
+unsigned long long* probe_slot(void* ws, const Geometry& g, int at) {
+  return reinterpret_cast<unsigned long long*>(region<uint8_t>(ws, g, DISCO_R_STATUS) + offsetof(Status, probe)) + at;
+}
+
 // ------------------------------------------------------------ tensor maps
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1849,6 +1872,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.groups = g.groups;
   p.wave = wave;
   p.rt_per_chunk = g.chunk_cols / PAIR_M;
+  p.probe = probe_slot(ws, g, 0);
   if (kind != KIND_FWD && g.g_blocked) {
     const __half* Gb = region<__half>(ws, g, DISCO_R_G);
     for (int d = 0; d < 2; ++d)
@@ -1937,6 +1961,7 @@ cudaStream_t st_of(void* stream) { return static_cast<cudaStream_t>(stream); }
 // Cross GEMMs into p.prob[first], p.prob[first + 1]:
 //   X_g = G_{d'}^T . A_{d'} (local rows), g = image <- d' = t2i (1), g = text <- d' = i2t (0)
 int build_cross(GemmParams& p, int first, void* ws, const Geometry& g, int mt0 = 0, int mt1 = -1) {
+  p.probe = probe_slot(ws, g, 4);
   const __half* G = region<__half>(ws, g, DISCO_R_G);
   const __half* f16 = region<__half>(ws, g, DISCO_R_FEAT16);
   const __half* I16 = f16;
@@ -2013,6 +2038,7 @@ int launch_combine(void* ws, const Geometry& g, float t, int flip, int row0, int
 
 // Intra GEMMs into p.prob[first], p.prob[first + 1]: Y_image = G_i . T_g ; Y_text = G_t . I_g
 int build_intra(GemmParams& p, int first, void* ws, const Geometry& g, int mt0 = 0, int mt1 = -1) {
+  p.probe = probe_slot(ws, g, 4);
   const __half* G = region<__half>(ws, g, DISCO_R_G);
   const __half* f16 = region<__half>(ws, g, DISCO_R_FEAT16);
   const __half* I16 = f16;
@@ -2528,6 +2554,22 @@ int disco_b200_combine_peer(void* ws, int64_t B, int64_t D, int world, int rank,
       int(g.D), s, flip, d_image, d_text, ld_out, 0, int(g.b), status, g.rank * g.np, (g.rank + 1) * g.np);
   count_launch();
   CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+// Clock probe readout (synchronous; profiling aid): the SM clock, in MHz, at which CTA 0 of the
+// last logits kernel and of the last backward GEMM ran (clock64 cycles / globaltimer ns), 0 if
+// the kernel has not run.
+int disco_b200_clock_probe(void* ws, int64_t B, int64_t D, int world, int rank, double* mhz) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  unsigned long long pr[8];
+  CUDA_TRY(cudaMemcpy(pr, probe_slot(ws, g, 0), sizeof(pr), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 2; ++k) {
+    const unsigned long long* q = pr + 4 * k;
+    mhz[k] = (q[3] > q[1] && q[2] > q[0]) ? double(q[2] - q[0]) / double(q[3] - q[1]) * 1e3 : 0.0;
+  }
   return DISCO_OK;
 }
 

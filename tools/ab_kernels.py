@@ -85,6 +85,7 @@ while _time.time() - _t0 < a.warm:
     run(libs[0][1], a.flags[0], [torch.cuda.Event(enable_timing=True) for _ in range(4)])
     torch.cuda.synchronize()
 times = {v[0] + ":" + str(v[2]): ([], [], []) for v in variants}
+mhz = {}
 for rep in range(a.reps + 2):
     for ln, lib, f in variants:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -95,6 +96,9 @@ for rep in range(a.reps + 2):
             k = ln + ":" + str(f)
             for i in range(3):
                 times[k][i].append(ev[i].elapsed_time(ev[i + 1]))
+            mhz.setdefault(k, []).append(_lib.clock_probe(plan))
 for k, (fw, bw, cb) in times.items():
     print(f"{k:10s} forward {statistics.median(fw):.4f}  backward {statistics.median(bw):.4f}  "
-          f"combine {statistics.median(cb):.4f}  total {statistics.median(fw) + statistics.median(bw) + statistics.median(cb):.4f} ms")
+          f"combine {statistics.median(cb):.4f}  total {statistics.median(fw) + statistics.median(bw) + statistics.median(cb):.4f} ms"
+          f"  SM MHz fwd {statistics.median(m['logits_fwd'] for m in mhz[k]):.0f} "
+          f"bwd {statistics.median(m['gemm_backward'] for m in mhz[k]):.0f}")
