@@ -219,6 +219,8 @@ int disco_b200_logit_scale_grad(void* ws, int64_t B, int64_t D, int world, int r
  * (mhz[0]) and of the last backward GEMM (mhz[1]) ran, from clock64 / globaltimer stamps the
  * kernels write into the status block; 0 if not run.  Shows the power-capped effective clock. */
 int disco_b200_clock_probe(void* ws, int64_t B, int64_t D, int world, int rank, double* mhz);
+/*   mhz must hold 3 doubles: mhz[2] = mean cycles the backward GEMM's epilogue held its
+ *   accumulators per unit (TMEM drain + stores) since the previous readout. */
 
 /* Tower side of the two-tower trainer (reference towers.py:148-157):
  * row L2 normalisation of raw tower outputs (matrix.py:165-176) and its backward

@@ -155,9 +155,9 @@ def forward_waves(B: int, D: int, world: int, rank: int) -> int:
 
 def clock_probe(plan) -> dict:
     """SM clock (MHz) the last logits kernel / backward GEMM ran at (CTA 0 stamps)."""
-    out = (ctypes.c_double * 2)()
+    out = (ctypes.c_double * 3)()
     call("disco_b200_clock_probe", *plan.args, out)
-    return {"logits_fwd": round(out[0], 1), "gemm_backward": round(out[1], 1)}
+    return {"logits_fwd": round(out[0], 1), "gemm_backward": round(out[1], 1), "drain_cycles_per_unit": round(out[2])}
 
 
 def launch_count() -> int:

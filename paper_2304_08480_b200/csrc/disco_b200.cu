@@ -108,6 +108,9 @@ struct Status {
   // clock probe (CTA 0 of the tensor-core kernels): {SM clock64, globaltimer ns} at entry and exit,
   // [0..3] logits kernel, [4..7] backward GEMM -> the SM clock the kernel actually ran at
   unsigned long long probe[8];
+  // drain probe (backward GEMM, epilogue warp 2 of every leader CTA): sum over units of the
+  // cycles from "accumulators full" to "accumulators released", and the unit count
+  unsigned long long drain[2];
 };
 
 // ----------------------------------------------------------- kernel params
@@ -117,6 +120,7 @@ struct LogitsParams {
   CUtensorMap a_map[2];  // dir 0: I_g, dir 1: T_g   box {64, 128}
   CUtensorMap b_map[2];  // dir 0: T_g, dir 1: I_g   box {64, 128} (each CTA loads its half of N)
   CUtensorMap g_map[2];  // blocked-G store maps (4-D), box {64, 32, 1, 1}
+  CUtensorMap e_map[2];  // FWDE: blocked-E store maps, half slices: box {32, 32, 1, 1}, 64-byte swizzle
   int B, b, Dp, rank;
   int nchunk, chunk_cols, tiles_per_chunk, row_tiles;  // row_tiles counts 256-row pair tiles
   float tl2e;  // t * log2(e)
@@ -539,6 +543,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int r_in_tile = crank * BM + quad * 32 + lane;
     uint8_t* tile = staging + ew * STAGING_BUFS * STAGING_TILE;
     uint32_t it = 0, gslice = 0;
+    // FWDE E-store pipeline state: one pending (written, not yet stored) 32 x 32 half slice
+    bool epend = false;
+    int ebuf = 0, epend_buf = 0, epend_cb = 0, epend_rb = 0, epend_dir = 0;
+    auto e_flush = [&]() {
+      if (!epend) return;
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (epend_rb < p.b && !(p.debug_flags & 1))  // bit0 ablation: skip the E stores
+          ptx::tma_store_4d(&p.e_map[epend_dir], tile + epend_buf * (STAGING_TILE / 2), epend_cb & 127,
+                            epend_rb & 127, epend_cb >> 7, epend_rb >> 7);
+        ptx::bulk_commit();
+      }
+      epend = false;
+    };
     for (int u = pair; u < num_units; u += npairs) {
       int dir, rt, ch, t0;
       decode(u, dir, rt, ch, t0);
@@ -622,21 +641,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
           } else if (col0 < chunk_hi) {  // warp-uniform
             const int li = label - col0;  // label column relative to this warp's 128 columns
-#pragma unroll 1
+            uint32_t ra[32], rb[32];  // both halves of a slice under one tcgen05.wait::ld
+            ptx::tmem_ld32_async(taddr, ra);
+            ptx::tmem_ld32_async(taddr + 32, rb);
+            ptx::tmem_wait_ld_dep(ra, rb);
+#pragma unroll
             for (int j = 0; j < 2; ++j) {
-              uint32_t ra[32], rb[32];  // both halves of the slice under one tcgen05.wait::ld
-              ptx::tmem_ld32_async(taddr + j * 64, ra);
-              ptx::tmem_ld32_async(taddr + j * 64 + 32, rb);
-              ptx::tmem_wait_ld_dep(ra, rb);
               float va[32], vb[32];
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 va[i] = __uint_as_float(ra[i]);
                 vb[i] = __uint_as_float(rb[i]);
               }
-              float cm = fmaxf(va[0], vb[0]);
+              if (j == 0) {  // slice 1's TMEM loads fly while slice 0 is computed
+                ptx::tmem_ld32_async(taddr + 64, ra);
+                ptx::tmem_ld32_async(taddr + 96, rb);
+              }
+              float mx[32];  // max over the 64 columns as a depth-6 tree
 #pragma unroll
-              for (int i = 1; i < 32; ++i) cm = fmaxf(cm, fmaxf(va[i], vb[i]));
+              for (int i = 0; i < 32; ++i) mx[i] = fmaxf(va[i], vb[i]);
+#pragma unroll
+              for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+                for (int i = 0; i < w; ++i) mx[i] = fmaxf(mx[i], mx[i + w]);
+              const float cm = mx[0];
               const float mg = cm * p.tl2e;
               float s0 = 0.f, s1 = 0.f;
               uint32_t h[32];
@@ -666,23 +694,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                   }
                   has_t = true;
                 }
+                // Half-slice store pipeline: this half goes into staging half-buffer `ebuf`; the
+                // previous half, written one compute phase ago, is fenced and TMA-stored first, so
+                // neither the STS -> fence.proxy.async latency nor the TMA read is exposed.
+                const int rbase = rt * PAIR_M + crank * BM + quad * 32;
+                if (p.debug_flags & 131072) {  // bit17 ablation: E math only (no STS, no store)
+                  if (h[half * 16] == 0x7fff1234u) asm volatile("trap;");
+                  continue;
+                }
+                e_flush();  // fence + store the pending half (its STS completed during this half's math)
+                uint8_t* hb = tile + ebuf * (STAGING_TILE / 2);
+                if (lane == 0) ptx::bulk_wait_read<1>();  // this buffer's previous store has read smem
+                __syncwarp();
+                ptx::st_swizzled_row64(hb, lane, h + half * 16);
+                epend = true;
+                epend_buf = ebuf;
+                epend_cb = col0 + j * 64 + half * 32;
+                epend_rb = rbase;
+                epend_dir = dir;
+                ebuf ^= 1;
               }
               const int cb = col0 + j * 64;
-              const int rbase = rt * PAIR_M + crank * BM + quad * 32;
-              if (lane == 0) ptx::bulk_wait_read<0>();
-              __syncwarp();
-              ptx::st_swizzled_row(tile, lane, h);
-              ptx::fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                if (rbase < p.b && !(p.debug_flags & 1))  // bit0 ablation: skip the E stores
-                  ptx::tma_store_4d(&p.g_map[dir], tile, cb & 127, rbase & 127, cb >> 7, rbase >> 7);
-                ptx::bulk_commit();
-              }
               const float mnew = fmaxf(m2, mg);
               l = l * ptx::ex2(m2 - mnew) + (s0 + s1) * ptx::ex2(mg - mnew);
               m2 = mnew;
               if (row_ok) p.mg[(int64_t(dir) * p.groups + cb / GROUP_COLS) * p.b + row] = mg;
+              if (j == 0) ptx::tmem_wait_ld_dep(ra, rb);
             }
           }
         } else {
@@ -758,6 +795,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (has_t) p.target[dir * p.b + row] = yt;
       }
     }
+    if (KIND == KIND_FWDE) e_flush();
     if (KIND != KIND_FWD && lane == 0) ptx::bulk_wait_all();  // drain any bulk stores
   }
   kernel_epilogue(ctl, warp);
@@ -771,19 +809,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 //   into the two TMEM buffers and summed in the epilogue ((c0 + c1): the first
 //   level of the fixed reduction tree).
 // =====================================================================
-// SB = epilogue staging buffers per warp.  SB = 2 (wide units): the operand ring drops to 3
-// stages and the freed 48 KiB double-buffers the staging, so a warp fills one 4 KiB slice while
-// the TMA store of the previous one is still reading shared memory.
-template <int NB, bool XF, int SB = 1>
+template <int NB, bool XF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF : NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ GemmParams p) {
-  constexpr int RS = SB == 2 ? 3 : Ring<NB>::STAGES;
+  constexpr int RS = Ring<NB>::STAGES;
   static_assert(NB == 1 || NB == 2, "one or two N tiles per unit");
-  static_assert(SB == 1 || (NB == 2 && RS * Ring<NB>::STAGE_BYTES + NUM_EPI_WARPS * SB * STAGING_TILE <=
-                                           TILE_RING_BYTES + STAGING_BYTES), "staging overlaps the control block");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
-  uint8_t* staging = tiles + (SB == 1 ? TILE_RING_BYTES : RS * Ring<NB>::STAGE_BYTES);
+  uint8_t* staging = tiles + TILE_RING_BYTES;
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + TILE_RING_BYTES + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int crank = int(ptx::cluster_ctarank());
@@ -968,7 +1001,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     const int ew = warp - 2;
     const int quad = warp & 3;
     const int chalf = ew >> 2;
-    uint8_t* tile = staging + ew * SB * STAGING_TILE;
+    uint8_t* tile = staging + ew * STAGING_BUFS * STAGING_TILE;
     uint32_t it = 0, gslice = 0;
     for (int u = pair; u < num_units; u += npairs) {
       int pi, mt, nt, kc;
@@ -979,6 +1012,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       ptx::mbar_wait(&ctl->tfull[buf0], (it >> 1) & 1);
       if (two) ptx::mbar_wait(&ctl->tfull[buf1], ((it + 1) >> 1) & 1);
       ptx::tc_fence_after();
+      const long long drain_t0 = clock64();
       const int row0 = mt * PAIR_M + crank * BM + quad * 32;  // first row of this warp's 32-row slab
       const int row = row0 + lane;
       const uint32_t lane_base = ctl->tmem_base + (uint32_t(quad * 32) << 16) + chalf * (BN / 2);
@@ -1025,13 +1059,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           uint32_t w[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(v[i]);
-          uint8_t* stile = tile + (gslice % SB) * STAGING_TILE;
-          if (lane == 0) ptx::bulk_wait_read<SB - 1>();
+          uint8_t* stile = tile + (gslice % STAGING_BUFS) * STAGING_TILE;
+          if (lane == 0) ptx::bulk_wait_read<STAGING_BUFS - 1>();
           __syncwarp();
           ptx::st_swizzled_row(stile, lane, w);
           ptx::fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && !(q.ablate & 32768)) {  // bit15 ablation: stage but never store
             if (q.peer) {  // NVLink push: this slice belongs to rank row0 / b
               const int dest = row0 / q.peer_b;
               if (row0 < q.M) ptx::tma_store_3d(&q.peer_map[dest], stile, c0, row0 - dest * q.peer_b, kc);
@@ -1053,6 +1087,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       }
       release_accumulator(ctl, buf0, lane);
       if (two) release_accumulator(ctl, buf1, lane);
+      if (p.probe && ew == 0 && lane == 0 && leader) {
+        atomicAdd(p.probe + 4, (unsigned long long)(clock64() - drain_t0));  // Status::drain follows probe
+        atomicAdd(p.probe + 5, 1ull);
+      }
       it += two ? 2 : 1;
     }
     if (lane == 0) ptx::bulk_wait_all();
@@ -1751,7 +1789,7 @@ int set_output(GemmProblem& q, float* out, int64_t ld_out, int64_t row_div, int6
   q.chunk_stride = chunk_stride;
   q.tma_store = 0;
   q.skip_store = (debug_flag_bits() & 16) ? 1 : 0;
-  q.ablate = debug_flag_bits() & (1024 | 2048);
+  q.ablate = debug_flag_bits() & (1024 | 2048 | 32768);
   const bool aligned = (row_div % 32 == 0) && (ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                        !(debug_flag_bits() & 32);
   if (aligned && (nz_rows == 1 || nz_chunks == 1)) {
@@ -1768,16 +1806,17 @@ int set_output(GemmProblem& q, float* out, int64_t ld_out, int64_t row_div, int6
 }
 
 // 4-D f16 map over a blocked G: [rows/128][cols/128][128][128], box {64, box_rows, 1, 1}.
-int make_map_blocked(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+int make_map_blocked(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                     uint32_t box_cols = 64) {
   auto fn = encode_fn();
   if (!fn) return fail(DISCO_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[4] = {128, 128, cols / 128, rows / 128};
   cuuint64_t strides[3] = {256, 32768, (cols / 128) * 32768};
-  cuuint32_t box[4] = {64, box_rows, 1, 1};
+  cuuint32_t box[4] = {box_cols, box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DISCO_CUDA_ERROR, "cuTensorMapEncodeTiled(blocked G) failed (%d)", int(r));
   return DISCO_OK;
 }
@@ -1877,6 +1916,8 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
     const __half* Gb = region<__half>(ws, g, DISCO_R_G);
     for (int d = 0; d < 2; ++d)
       if ((rc = make_map_blocked(&p.g_map[d], Gb + int64_t(d) * g.b * g.B, g.b, g.B, 32))) return rc;
+    for (int d = 0; d < 2; ++d)
+      if ((rc = make_map_blocked(&p.e_map[d], Gb + int64_t(d) * g.b * g.B, g.b, g.B, 32, 32))) return rc;
   }
   const int debug_flags = debug_flag_bits();
   p.debug_flags = debug_flags;
@@ -1911,11 +1952,11 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
 
 // wide = 1: every unit covers all N columns (n_tiles counts 512-column tiles), NB = 2 kernel.
 // xform = 1: A operands hold E (transform warps rescale to G in smem).
-template <int NB, bool XF, int SB = 1>
+template <int NB, bool XF>
 int launch_gemm_t(GemmParams& p, cudaStream_t st) {
   int rc;
-  if ((rc = prepare_kernel(gemm_kernel<NB, XF, SB>))) return rc;
-  gemm_kernel<NB, XF, SB><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS, SMEM_BYTES, st>>>(p);
+  if ((rc = prepare_kernel(gemm_kernel<NB, XF>))) return rc;
+  gemm_kernel<NB, XF><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS, SMEM_BYTES, st>>>(p);
   return DISCO_OK;
 }
 
@@ -1924,10 +1965,8 @@ int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform) {
   for (int i = 0; i < p.nprob; ++i)
     p.units[i + 1] = p.units[i] + p.prob[i].m_tiles * p.prob[i].n_tiles * p.prob[i].k_chunks;
   int rc;
-  const bool sb2 = debug_flag_bits() & 4096;  // experiment: 3-stage ring + double-buffered staging
   if (wide)
-    rc = xform ? (sb2 ? launch_gemm_t<2, true, 2>(p, st) : launch_gemm_t<2, true>(p, st))
-               : (sb2 ? launch_gemm_t<2, false, 2>(p, st) : launch_gemm_t<2, false>(p, st));
+    rc = xform ? launch_gemm_t<2, true>(p, st) : launch_gemm_t<2, false>(p, st);
   else
     rc = xform ? launch_gemm_t<1, true>(p, st) : launch_gemm_t<1, false>(p, st);
   if (rc) return rc;
@@ -2564,12 +2603,15 @@ int disco_b200_clock_probe(void* ws, int64_t B, int64_t D, int world, int rank, 
   Geometry g;
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
-  unsigned long long pr[8];
+  unsigned long long pr[10];
   CUDA_TRY(cudaMemcpy(pr, probe_slot(ws, g, 0), sizeof(pr), cudaMemcpyDeviceToHost));
   for (int k = 0; k < 2; ++k) {
     const unsigned long long* q = pr + 4 * k;
     mhz[k] = (q[3] > q[1] && q[2] > q[0]) ? double(q[2] - q[0]) / double(q[3] - q[1]) * 1e3 : 0.0;
   }
+  // mhz[2]: mean accumulator drain (cycles per backward unit) since the last readout
+  mhz[2] = pr[9] ? double(pr[8]) / double(pr[9]) : 0.0;
+  CUDA_TRY(cudaMemset(probe_slot(ws, g, 8), 0, 2 * sizeof(unsigned long long)));
   return DISCO_OK;
 }
 

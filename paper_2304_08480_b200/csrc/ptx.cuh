@@ -195,6 +195,17 @@ __device__ __forceinline__ void st_swizzled_row(uint8_t* tile, int r, const uint
   }
 }
 
+// One 64-byte row (16 words) of a 32-row staging tile in the TMA SWIZZLE_64B layout: 16-byte
+// chunk q of row r sits at physical chunk q ^ ((r >> 1) & 3) (bank-conflict-free per quarter warp).
+__device__ __forceinline__ void st_swizzled_row64(uint8_t* tile, int r, const uint32_t* w) {
+  uint8_t* row = tile + r * 64;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 v = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    *reinterpret_cast<uint4*>(row + ((q ^ ((r >> 1) & 3)) << 4)) = v;
+  }
+}
+
 // Coalesced write-out of a 32-row x 128-byte swizzled staging tile with plain
 // LSU stores: each warp instruction stores 4 complete 128-byte rows.
 // dst(row) returns the global address of row `row` (nullptr = skip the row).

@@ -101,4 +101,5 @@ for k, (fw, bw, cb) in times.items():
     print(f"{k:10s} forward {statistics.median(fw):.4f}  backward {statistics.median(bw):.4f}  "
           f"combine {statistics.median(cb):.4f}  total {statistics.median(fw) + statistics.median(bw) + statistics.median(cb):.4f} ms"
           f"  SM MHz fwd {statistics.median(m['logits_fwd'] for m in mhz[k]):.0f} "
-          f"bwd {statistics.median(m['gemm_backward'] for m in mhz[k]):.0f}")
+          f"bwd {statistics.median(m['gemm_backward'] for m in mhz[k]):.0f} "
+          f"drain {statistics.median(m['drain_cycles_per_unit'] for m in mhz[k]):.0f} cyc/unit")
