@@ -55,7 +55,7 @@ enum disco_region {
   DISCO_R_GATHER = 1,  /* bf16 [N][2][b][Dp]      all_gather output                          */
   DISCO_R_FEAT = 2,    /* bf16 [2][B][Dp]         gathered I_g, T_g (forward GEMM operands)  */
   DISCO_R_FEAT16 = 3,  /* f16  [2][B][Dp]         gathered I_g, T_g (backward GEMM operands) */
-  DISCO_R_STATS = 4,   /* f32  [2][nchunk][b][2]  per column-chunk (max, sum-exp) partials   */
+  DISCO_R_STATS = 4,   /* f32x2 [2][nchunk*ssub][2][b] (max, sum-exp) per column sub-chunk and half */
   DISCO_R_ROWS = 5,    /* f32  [4][2][b]          target logit, lse, label gradient, spare   */
   DISCO_R_CE = 6,      /* f32  [2][b]             per-row cross-entropy (loss all_gather in) */
   DISCO_R_CE_ALL = 7,  /* f32  [N][2][b]          loss all_gather output                     */

@@ -39,6 +39,8 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <algorithm>
+#include <vector>
 
 #include "disco_b200.h"
 #include "ptx.cuh"
@@ -141,6 +143,7 @@ struct LogitsParams {
   // chunk is `wave` and the other index <= wave, i.e. the units that became computable when
   // canonical chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per chunk.
   int wave, rt_per_chunk;
+  int ssub;  // sub-chunks per canonical chunk (nchunk / chunk_cols above are per sub-chunk)
   unsigned long long* probe;  // Status::probe (may be null)
 };
 
@@ -178,6 +181,8 @@ struct GemmProblem {
   int lab_off;            // rank * b: global column of local row 0's positive pair
 };
 constexpr int MAX_PROBLEMS = 4;
+constexpr int MAX_SCHED_PAIRS = 80;
+constexpr int MAX_SCHED_UNITS = 4096;
 struct GemmParams {
   GemmProblem prob[MAX_PROBLEMS];
   int nprob;
@@ -187,6 +192,11 @@ struct GemmParams {
   // stride of #pairs see A and B units in different phases (spreads the accumulator drains).
   int split;
   unsigned long long* probe;  // Status::probe + 4 (may be null)
+  // Static longest-processing-time schedule (host-computed): pair i runs the unit sequence
+  // indices sched[sched_off[i] .. sched_off[i + 1]) in order; sched_n == 0: round-robin.
+  int sched_n;
+  uint16_t sched_off[MAX_SCHED_PAIRS + 1];
+  uint16_t sched[MAX_SCHED_UNITS];
 };
 
 // --------------------------------------------------------- shared helpers
@@ -401,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   constexpr bool CHUNK_UNITS = KIND != KIND_GRAD;  // unit = all tiles of one column chunk
   const int wave = CHUNK_UNITS ? p.wave : -1;
-  const int per_dir = wave >= 0 ? p.rt_per_chunk * (2 * wave + 1)
+  const int per_dir = wave >= 0 ? p.rt_per_chunk * (2 * wave + 1) * p.ssub
                                 : p.row_tiles * p.nchunk * (CHUNK_UNITS ? 1 : p.tiles_per_chunk);
   const int num_units = 2 * per_dir;
   const int tiles_per_unit = CHUNK_UNITS ? p.tiles_per_chunk : 1;
@@ -411,13 +421,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     dir = u / per_dir;
     int rem = u - dir * per_dir;
     if (wave >= 0) {  // new row tiles x chunks [0, wave], then old row tiles x chunk `wave`
-      const int fresh = p.rt_per_chunk * (wave + 1);
+      const int nsw = p.ssub * (wave + 1);  // sub-chunks of chunks [0, wave]
+      const int fresh = p.rt_per_chunk * nsw;
       if (rem < fresh) {
-        rt = wave * p.rt_per_chunk + rem / (wave + 1);
-        ch = rem % (wave + 1);
+        rt = wave * p.rt_per_chunk + rem / nsw;
+        ch = rem % nsw;
       } else {
-        rt = rem - fresh;
-        ch = wave;
+        rem -= fresh;
+        rt = rem / p.ssub;
+        ch = wave * p.ssub + rem % p.ssub;
       }
       t0 = 0;
     } else if (CHUNK_UNITS) {
@@ -836,6 +848,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
   kernel_prologue(ctl, warp, lane);
 
   const int num_units = p.units[p.nprob];
+  // this pair's sequence of unit indices: the static schedule, or round-robin over pairs
+  const int my_units = p.sched_n ? int(p.sched_off[pair + 1]) - int(p.sched_off[pair])
+                                 : (num_units - pair + npairs - 1) / npairs;
+  auto unit_at = [&](int k) -> int { return p.sched_n ? int(p.sched[p.sched_off[pair] + k]) : pair + k * npairs; };
   // unit -> (problem, mt, nt, kc); nt fastest so pairs sharing an A tile run together.
   auto decode = [&](int u, int& pi, int& mt, int& nt, int& kc) {
     if (p.split > 0) {
@@ -862,7 +878,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       Pipe<RS> pipe;
-      for (int u = pair; u < num_units; u += npairs) {
+      for (int uk = 0; uk < my_units; ++uk) {
+        const int u = unit_at(uk);
         int pi, mt, nt, kc;
         decode(u, pi, mt, nt, kc);
         const GemmProblem& q = p.prob[pi];
@@ -894,7 +911,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     if (leader) {  // ---------------- MMA issuer (leader CTA, whole warp; one elected lane issues)
       Pipe<RS> pipe;
       uint32_t it = 0;
-      for (int u = pair; u < num_units; u += npairs) {
+      for (int uk = 0; uk < my_units; ++uk) {
+        const int u = unit_at(uk);
         int pi, mt, nt, kc;
         decode(u, pi, mt, nt, kc);
         const GemmProblem& q = p.prob[pi];
@@ -936,7 +954,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     const int xt = threadIdx.x - 32 * (2 + NUM_EPI_WARPS);
     const uint32_t xbar = 0;  // transform completion is counted on the leader's xfull barriers
     Pipe<RS> pipe;
-    for (int u = pair; u < num_units; u += npairs) {
+    for (int uk = 0; uk < my_units; ++uk) {
+        const int u = unit_at(uk);
       int pi, mt, nt, kc;
       decode(u, pi, mt, nt, kc);
       const GemmProblem& q = p.prob[pi];
@@ -1003,7 +1022,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     const int chalf = ew >> 2;
     uint8_t* tile = staging + ew * STAGING_BUFS * STAGING_TILE;
     uint32_t it = 0, gslice = 0;
-    for (int u = pair; u < num_units; u += npairs) {
+    for (int uk = 0; uk < my_units; ++uk) {
+        const int u = unit_at(uk);
       int pi, mt, nt, kc;
       decode(u, pi, mt, nt, kc);
       const GemmProblem& q = p.prob[pi];
@@ -1199,17 +1219,23 @@ __global__ void unpack_kernel(const uint4* gathered, int N, int b, int Dp, uint4
 // canonical chunks: balanced tree ((0+1)+(2+3))+((4+5)+(6+7)); non-canonical
 // chunkings: ascending order.
 //   lse2 (log2 domain), ce = -log softmax[label], glabel = P_label - 1 = -(sum_{j!=label} P_j).
-__global__ void stats_combine_kernel(const float2* stats, const float* target, int nchunk, int b, float* lse2_out,
-                                     float* glabel_out, float* ce_out, Status* status) {
+// ssub: stats sub-chunks per canonical chunk (the forward's units cover one sub-chunk); a chunk's
+// sum is the fixed tree over its (sub-chunk, column half) partials.
+__global__ void stats_combine_kernel(const float2* stats, const float* target, int nchunk, int ssub, int b,
+                                     float* lse2_out, float* glabel_out, float* ce_out, Status* status) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 2 * b) return;
   const int dir = i / b, r = i % b;
-  auto at = [&](int c, int h) { return stats[((int64_t(dir) * nchunk + c) * 2 + h) * b + r]; };
+  const int nsc = nchunk * ssub;
+  auto at = [&](int sc, int h) { return stats[((int64_t(dir) * nsc + sc) * 2 + h) * b + r]; };
   float m = -INFINITY;
-  for (int c = 0; c < nchunk; ++c) m = fmaxf(m, fmaxf(at(c, 0).x, at(c, 1).x));
-  auto chunk_sum = [&](int c) {
-    const float2 s0 = at(c, 0), s1 = at(c, 1);
+  for (int sc = 0; sc < nsc; ++sc) m = fmaxf(m, fmaxf(at(sc, 0).x, at(sc, 1).x));
+  auto sub_sum = [&](int sc) {
+    const float2 s0 = at(sc, 0), s1 = at(sc, 1);
     return s0.y * ptx::ex2(s0.x - m) + s1.y * ptx::ex2(s1.x - m);
+  };
+  auto chunk_sum = [&](int c) {
+    return ssub == 2 ? sub_sum(2 * c) + sub_sum(2 * c + 1) : sub_sum(c);
   };
   float lo;
   if (nchunk == 8) {
@@ -1619,6 +1645,7 @@ struct Geometry {
   int64_t B, D, Dp, b, ldG;
   int N, rank;
   int nchunk, cpr;        // canonical chunks, chunks per rank
+  int ssub;               // forward stats sub-chunks per chunk (2: logits units of half a chunk)
   int np;                 // cross partials per rank after pairing chunks in the GEMM epilogue
   int g_blocked;          // G in 128 x 128 blocks (canonical chunking: b and B multiples of 128)
   int wide;               // Dp % 512 == 0: GEMM units cover all of D (two accumulators, G read once)
@@ -1667,6 +1694,9 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
     g->cpr = 1;
   }
   g->chunk_cols = int(B / g->nchunk);
+  // half-chunk logits units when a half chunk is whole 256-column tiles: twice the units, so
+  // small local batches (N = 8) fill the 74 CTA pairs in whole waves
+  g->ssub = (g->nchunk == 8 && g->chunk_cols % (2 * BN) == 0 && !(debug_flag_bits() & 524288)) ? 2 : 1;
   g->g_blocked = (g->nchunk == 8 && g->b % 128 == 0) ? 1 : 0;
   g->wide = (g->Dp % 512 == 0 && !(debug_flag_bits() & 256)) ? 1 : 0;  // bit8: narrow-unit experiment
   // cross partials per rank: wide units keep one partial per canonical chunk (the first tree
@@ -1685,7 +1715,7 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   len[DISCO_R_GATHER] = N > 1 ? N * 2 * b * Dp * 2 : 0;
   len[DISCO_R_FEAT] = 2 * B * Dp * 2;
   len[DISCO_R_FEAT16] = 2 * B * Dp * 2;
-  len[DISCO_R_STATS] = 2 * int64_t(g->nchunk) * 2 * b * 8;
+  len[DISCO_R_STATS] = 2 * int64_t(g->nchunk) * g->ssub * 2 * b * 8;
   len[DISCO_R_ROWS] = 4 * 2 * b * 4;
   len[DISCO_R_CE] = 2 * b * 4;
   len[DISCO_R_CE_ALL] = N * 2 * b * 4;
@@ -1894,9 +1924,10 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.b = int(g.b);
   p.Dp = int(g.Dp);
   p.rank = g.rank;
-  p.nchunk = g.nchunk;
-  p.chunk_cols = g.chunk_cols;
-  p.tiles_per_chunk = (g.chunk_cols + BN - 1) / BN;
+  p.nchunk = g.nchunk * g.ssub;  // the kernel's "chunks" are the stats sub-chunks
+  p.chunk_cols = g.chunk_cols / g.ssub;
+  p.ssub = g.ssub;
+  p.tiles_per_chunk = (p.chunk_cols + BN - 1) / BN;
   p.row_tiles = int((g.b + PAIR_M - 1) / PAIR_M);
   p.tl2e = t * LOG2E;
   float* rows = region<float>(ws, g, DISCO_R_ROWS);
@@ -1921,7 +1952,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   }
   const int debug_flags = debug_flag_bits();
   p.debug_flags = debug_flags;
-  const int64_t units = wave >= 0 ? int64_t(2) * p.rt_per_chunk * (2 * wave + 1)
+  const int64_t units = wave >= 0 ? int64_t(2) * p.rt_per_chunk * (2 * wave + 1) * p.ssub
                                   : int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
   const bool ares = g.Dp <= BK * ARES_SLICES && (debug_flags & 128);  // experiment: not faster on B200
   if (kind == KIND_FWD) {
@@ -1960,10 +1991,59 @@ int launch_gemm_t(GemmParams& p, cudaStream_t st) {
   return DISCO_OK;
 }
 
+// Static LPT schedule: unit cost = its K extent + a fixed drain cost (the accumulator drain
+// stalls the MMA for ~10k cycles per unit, about 640 rows of K at the wide MMA rate); units
+// are assigned longest first to the least-loaded pair, then each pair runs its units in
+// sequence order (which keeps the intra / cross interleave and the L2 locality).  Balances the
+// 4:1 intra / cross unit lengths that round-robin leaves ragged, e.g. at N = 8.
+void build_schedule(GemmParams& p, int npairs) {
+  const int n = p.units[p.nprob];
+  p.sched_n = 0;
+  if (n > MAX_SCHED_UNITS || npairs > MAX_SCHED_PAIRS || npairs < 1) return;
+  std::vector<std::pair<int64_t, int>> cost(n);
+  for (int s = 0; s < n; ++s) {
+    int u = s;
+    if (p.split > 0) {
+      const int64_t nA = p.units[p.split];
+      const int64_t cA = int64_t(s) * nA / n, cA1 = int64_t(s + 1) * nA / n;
+      u = cA1 > cA ? int(cA) : int(nA + s - cA1);
+    }
+    int pi = 0;
+    while (pi + 1 < p.nprob && u >= p.units[pi + 1]) ++pi;
+    const GemmProblem& q = p.prob[pi];
+    const int kc = ((u - p.units[pi]) / q.n_tiles) % q.k_chunks;
+    int64_t klen = 0;
+    for (int sub = 0; sub <= q.paired; ++sub) {
+      const int64_t k0 = int64_t(kc * (1 + q.paired) + sub) * q.k_chunk_len;
+      klen += std::max<int64_t>(0, std::min<int64_t>(q.k_chunk_len, q.k_total - k0));
+    }
+    cost[s] = {klen + 640, s};
+  }
+  std::stable_sort(cost.begin(), cost.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+  std::vector<int64_t> load(npairs, 0);
+  std::vector<std::vector<int>> lists(npairs);
+  for (const auto& c : cost) {
+    int best = 0;
+    for (int i = 1; i < npairs; ++i)
+      if (load[i] < load[best]) best = i;
+    load[best] += c.first;
+    lists[best].push_back(c.second);
+  }
+  int off = 0;
+  for (int i = 0; i < npairs; ++i) {
+    std::sort(lists[i].begin(), lists[i].end());
+    p.sched_off[i] = uint16_t(off);
+    for (int s : lists[i]) p.sched[off++] = uint16_t(s);
+  }
+  p.sched_off[npairs] = uint16_t(off);
+  p.sched_n = n;
+}
+
 int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform) {
   p.units[0] = 0;
   for (int i = 0; i < p.nprob; ++i)
     p.units[i + 1] = p.units[i] + p.prob[i].m_tiles * p.prob[i].n_tiles * p.prob[i].k_chunks;
+  if (!(debug_flag_bits() & 262144)) build_schedule(p, grid_for(p.units[p.nprob]) / 2);  // bit18: round-robin
   int rc;
   if (wide)
     rc = xform ? launch_gemm_t<2, true>(p, st) : launch_gemm_t<2, false>(p, st);
@@ -2118,7 +2198,7 @@ int forward_finish(void* ws, const Geometry& g, cudaStream_t st) {
   float* rows = region<float>(ws, g, DISCO_R_ROWS);
   const int n = int(2 * g.b);
   stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(
-      region<float2>(ws, g, DISCO_R_STATS), rows, g.nchunk, int(g.b), rows + 2 * g.b, rows + 4 * g.b,
+      region<float2>(ws, g, DISCO_R_STATS), rows, g.nchunk, g.ssub, int(g.b), rows + 2 * g.b, rows + 4 * g.b,
       region<float>(ws, g, DISCO_R_CE), region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
   CUDA_TRY(cudaGetLastError());
