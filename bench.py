@@ -284,8 +284,14 @@ def run_ours(args):
             step()
             ends[i].record(st)
         torch.cuda.synchronize()
-    barrier()
     launches = _lib.launch_count() - launches0
+    # NVML's throttle reasons lag a ~50 ms burst: keep sampling over the same work for
+    # another ~0.5 s (untimed) so a power cap that shaped the timed steps is reported
+    with ClockSampler(local_rank) as clk_after:
+        for _ in range(max(20, 100 // max(1, args.steps))):
+            step()
+        torch.cuda.synchronize()
+    barrier()
     loss = P.finish_status(plan)
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms = statistics.mean(step_ms)
@@ -447,7 +453,10 @@ def run_ours(args):
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": dict(clk.summary(), in_kernel_mhz=kernel_mhz,
-                       in_kernel_note="clock64 / globaltimer stamps of CTA 0 (NVML reports the target clock)"),
+                       reasons_sustained=clk_after.summary().get("reasons"),
+                       in_kernel_note="SM clock the tensor-core kernels actually ran at (clock64 / globaltimer "
+                                      "stamps of CTA 0); below NVML's sm_mhz because the 1000 W cap "
+                                      "(sw_power_cap) paces tensor-bound work, see reasons_sustained"),
     }
     print(json.dumps(line), flush=True)
     if world > 1:
