@@ -22,6 +22,7 @@ ap.add_argument("--batch", type=int, default=32768)
 ap.add_argument("--dim", type=int, default=512)
 ap.add_argument("--out", default="gpurun_out/e2e_trace.json")
 ap.add_argument("--sweep", action="store_true", help="time row-block schedules (CUDA events), no trace")
+ap.add_argument("--device", action="store_true", help="device-resident inputs (bench value path) instead of host")
 a = ap.parse_args()
 
 torch.cuda.set_device(0)
@@ -29,8 +30,8 @@ g = torch.Generator(device="cuda")
 g.manual_seed(0)
 I = torch.nn.functional.normalize(torch.randn(a.batch, a.dim, device="cuda", generator=g), dim=1)
 T = torch.nn.functional.normalize(torch.randn(a.batch, a.dim, device="cuda", generator=g), dim=1)
-I_h = I.bfloat16().cpu().pin_memory()
-T_h = T.bfloat16().cpu().pin_memory()
+I_h = I.bfloat16() if a.device else I.bfloat16().cpu().pin_memory()
+T_h = T.bfloat16() if a.device else T.bfloat16().cpu().pin_memory()
 for _ in range(3):
     P.disco_step(None, I_h, T_h, 100.0)
 torch.cuda.synchronize()

@@ -43,6 +43,8 @@ for N, flags in [(N, f) for N in a.worlds for f in a.flags]:
     _lib.load().disco_b200_set_experiment_flags(flags)
     clear_plans()
     torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats(dev)
+    mem0 = torch.cuda.memory_allocated(dev)
     b = B // N
     plan = get_plan(B, D, N, 0, dev)
     g = torch.Generator(device=dev)
@@ -98,7 +100,7 @@ for N, flags in [(N, f) for N in a.worlds for f in a.flags]:
     med = {k: round(statistics.median(v), 4) for k, v in acc.items()}
     flops = 12.0 * b * B * D
     mhz = _lib.clock_probe(plan)
-    out[f"{N}:{flags}"] = {"ms": med, "rank_tflops": round(flops / (med["step"] / 1e3) / 1e12, 1),
+    out[f"{N}:{flags}"] = {"peak_rank_mem_gb": round((torch.cuda.max_memory_allocated(dev) - mem0) / 1e9, 2), "ms": med, "rank_tflops": round(flops / (med["step"] / 1e3) / 1e12, 1),
               "projected_samples_per_s": round(B / (med["step"] / 1e3)), "in_kernel_mhz": mhz}
     o = out[f"{N}:{flags}"]
     print(f"N={N} flags={flags}: step {med['step']:.3f} ms/rank  {o['rank_tflops']} TF/s/rank  "
