@@ -1351,15 +1351,18 @@ __global__ void combine_kernel(const float4* intra, int ksplit, const float4* re
   const int64_t per_blk = int64_t(nrows) * v4;
   const int64_t total = 2 * per_blk;
   bool bad = false;
+  // 32-bit index math (total < 2^31 for every supported shape); partials are read once: __ldcs
+  const unsigned pb = unsigned(per_blk), uv4 = unsigned(v4);
   for (int64_t ii = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ii < total; ii += int64_t(gridDim.x) * blockDim.x) {
-    const int g = int(ii / per_blk);
-    const int64_t rem = (ii - g * per_blk) + int64_t(row0) * v4;
-    const int r = int(rem / v4), vc = int(rem % v4);
+    const unsigned iu = unsigned(ii);
+    const int g = int(iu / pb);
+    const int64_t rem = int64_t(iu - unsigned(g) * pb) + int64_t(row0) * v4;
+    const int r = int(unsigned(rem) / uv4), vc = int(unsigned(rem) % uv4);
     float4 cross;
     if (xpart) {
       const float4* src = xpart + (int64_t(g) * np) * per_g + rem;
       cross = tree_sum(np, [&](int k) {
-        const float4 x = src[k * per_g];
+        const float4 x = __ldcs(src + k * per_g);
         return (flip && (k < own_lo || k >= own_hi)) ? f4neg(x) : x;
       });
     } else {
@@ -1369,7 +1372,7 @@ __global__ void combine_kernel(const float4* intra, int ksplit, const float4* re
       });
     }
     const float4* ib = intra + (int64_t(g) * ksplit) * per_g + rem;  // intra K-split partials, fixed order
-    const float4 yi = ksplit == 2 ? f4add(ib[0], ib[per_g]) : ib[0];
+    const float4 yi = ksplit == 2 ? f4add(__ldcs(ib), __ldcs(ib + per_g)) : __ldcs(ib);
     const float4 t = f4add(yi, cross);
     const float4 o = make_float4(t.x * s, t.y * s, t.z * s, t.w * s);
     float* out = (g == 0 ? d_image : d_text) + int64_t(r) * ld_out;
