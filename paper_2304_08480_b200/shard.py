@@ -17,14 +17,17 @@ through the endpoint.  There is no CPU fallback.
 
 Dataflow of ``disco_step`` on rank n (b = B/N):
   pack (bf16)  -> all_gather [N][2][b][Dp]   (shard.py:190-191)
-  forward      : fused logits GEMM + online LSE + CE (shard.py:134-141)
-  backward_grad : recompute logits -> f16 G = softmax - onehot (shard.py:143-146)
-  backward_cross: G^T . local feats per canonical chunk, destination-major slabs
-                 (shard.py:149, 151)
-  all_to_all of the slabs (async, overlaps)  \\  replace all_reduce(AVG) +
-  backward_intra: G . gathered feats          /   row slice (shard.py:199-208)
-  combine      : s * (intra + fixed-tree sum of received slabs)
-  all_gather of per-row ce -> fixed-order f64 loss (shard.py:205)
+  forward      : fused logits GEMM + online LSE + CE, stores E = exp2(y - group max) in f16
+                 (shard.py:134-141); host inputs at N = 1: chunked H2D + logit wavefronts
+  backward_grad : no-op for canonical shapes (G = softmax - onehot is formed from E inside the
+                 backward GEMMs' shared-memory stages); otherwise recompute (shard.py:143-146)
+  backward     : intra G . gathered feats and cross G^T . local feats per canonical chunk in one
+                 persistent launch (shard.py:149-152); at N > 1 the cross tiles are pushed into
+                 the owners' peer windows by the GEMM epilogue (peer transport), or presummed
+                 and exchanged with an NCCL all_to_all (DISCO_PEER=0)      \\  replace
+  combine      : s * (intra + fixed-tree sum of the chunk partials)         /  all_reduce(AVG)
+                 (host outputs at N = 1: row blocks with overlapped D2H)       + row slice
+  all_gather of per-row ce -> fixed-order f64 loss (shard.py:205)              (shard.py:199-208)
 """
 
 from dataclasses import dataclass
