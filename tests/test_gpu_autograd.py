@@ -53,7 +53,11 @@ def test_bf16_features_get_bf16_grads_and_chain_rule():
     assert abs(log_scale.grad.item() - rs) <= TOL * abs(rs)
 
 
-def test_dlogit_bitwise_identical_across_world_sizes():
+@pytest.mark.parametrize("peer", [False, True])
+def test_dlogit_bitwise_identical_across_world_sizes(peer):
+    """Loss, dL/dt and both feature gradients through autograd are the same bytes at N = 1, 2, 4, 8,
+    with the NCCL-style exchange and with the peer transport (windows shared between the rank
+    threads, one stream per rank)."""
     B, D, t = 2048, 64, 100.0
     I, T = _feats(B, D, 9)
     Id = torch.tensor(I, dtype=torch.float32, device="cuda")
@@ -71,7 +75,7 @@ def test_dlogit_bitwise_identical_across_world_sizes():
             loss.backward()
             return loss.item(), s.grad.item(), Ir.grad, Tr.grad
 
-        res = P.run_ranks(N, fn)
+        res = P.run_ranks(N, fn, peer=peer and N > 1)
         assert len({r[0] for r in res}) == 1 and len({r[1] for r in res}) == 1
         results[N] = (res[0][0], res[0][1], torch.cat([r[2] for r in res]).cpu(), torch.cat([r[3] for r in res]).cpu())
     base = results[1]

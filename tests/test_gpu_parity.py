@@ -220,7 +220,7 @@ def test_host_pipelined_readback_bitwise(B, D):
 
 
 @pytest.mark.parametrize("B,D,dtype", [(32768, 512, torch.bfloat16), (8192, 1024, torch.float32),
-                                       (2048, 64, torch.float16)])
+                                       (2048, 64, torch.float16), (4096, 200, torch.float64)])
 def test_host_pipelined_forward_bitwise(B, D, dtype):
     """Host features at N=1 with B % 2048 == 0 take the wavefront forward (chunked H2D on a copy
     stream, disco_b200_pack_rows + forward_wave per landed chunk on two compute streams,
