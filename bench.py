@@ -222,6 +222,11 @@ def run_ours(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # DISCO_BENCH_SHARE_GPU=1 (code-path check only, numbers meaningless): every rank on cuda:0,
+    # gloo for the host plumbing -- exercises the N > 1 bench path on a one-GPU box
+    share = os.environ.get("DISCO_BENCH_SHARE_GPU", "0") == "1"
+    if share:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     device = torch.device("cuda", local_rank)
 
@@ -230,7 +235,10 @@ def run_ours(args):
     from paper_2304_08480_b200.shard import get_plan
 
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
         ep = P.ProcessGroupEndpoint()
     else:
         ep = P.SingleEndpoint()
@@ -414,7 +422,8 @@ def run_ours(args):
     # the forward also streams the f16 E blocks out (canonical shapes): its HBM side
     table["logits_fwd"]["e_write_gbs"] = None if recompute else g_bytes / (phases["forward"] / 1e3) / 1e9
     dom = max(table, key=lambda k: table[k]["ms"])
-    traffic = load_traffic().get(dom)
+    # ncu DRAM bytes per launch were captured at the headline workload (B=32K, D=512, N=1)
+    traffic = load_traffic().get(dom) if (B, D, world) == (B_GLOBAL, DIM, 1) else None
     step_tflops = 12.0 * b * B * D / (ms / 1e3) / 1e12
     d = table[dom]
 
