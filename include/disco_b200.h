@@ -60,7 +60,7 @@ enum disco_region {
   DISCO_R_CE = 6,      /* f32  [2][b]             per-row cross-entropy (loss all_gather in) */
   DISCO_R_CE_ALL = 7,  /* f32  [N][2][b]          loss all_gather output                     */
   DISCO_R_G = 8,       /* f16  [2][b][ldG]        softmax-minus-one-hot blocks (unscaled)    */
-  DISCO_R_XPART = 9,   /* f32  [2][cpr][B][Dp]    cross partials per canonical row chunk     */
+  DISCO_R_XPART = 9,   /* f32  [2][B][cpr][Dp]    cross partials per canonical row chunk     */
   DISCO_R_SEND = 10,   /* f32  [N][2][b][Dp]      cross slabs by destination (all_to_all in) */
   DISCO_R_RECV = 11,   /* f32  [N][2][b][Dp]      cross slabs by source (all_to_all out)     */
   DISCO_R_INTRA = 12,  /* f32  [2][b][Dp]         intra-rank gradient terms                  */

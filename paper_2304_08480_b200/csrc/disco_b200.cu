@@ -1317,7 +1317,7 @@ __device__ __forceinline__ float4 tree_sum(int n, Get get) {
 }
 
 // Sender-side tree over this rank's np paired-chunk partials:
-//   xpart [2][np][B][Dp] -> send [N][2][b][Dp] (destination-major). float4 per thread.
+//   xpart [2][B][np][Dp] (leaf-interleaved) -> send [N][2][b][Dp] (destination-major).
 __global__ void presum_kernel(const float4* xpart, int np, int N, int b, int Dp, float4* send) {
   const int v4 = Dp / 4;
   const int64_t B = int64_t(N) * b;
@@ -1328,8 +1328,8 @@ __global__ void presum_kernel(const float4* xpart, int np, int N, int b, int Dp,
     const int64_t rem = i - g * per_g;
     const int64_t c = rem / v4;
     const int vc = int(rem % v4);
-    const float4* src = xpart + (int64_t(g) * np) * per_g + rem;
-    const float4 acc = tree_sum(np, [&](int k) { return src[k * per_g]; });
+    const float4* src = xpart + ((int64_t(g) * B + c) * np) * v4 + vc;
+    const float4 acc = tree_sum(np, [&](int k) { return __ldcs(src + k * v4); });
     const int64_t dest = c / b, r = c % b;
     send[((dest * 2 + g) * b + r) * v4 + vc] = acc;
   }
@@ -1344,7 +1344,7 @@ __global__ void presum_kernel(const float4* xpart, int np, int N, int b, int Dp,
 __global__ void combine_kernel(const float4* intra, int ksplit, const float4* recv, const float4* xpart, int np,
                                int N, int rank, int b, int Dp, int D, float s, int flip, float* d_image,
                                float* d_text, int64_t ld_out, int row0, int nrows, Status* status, int own_lo = 0,
-                               int own_hi = 1 << 30) {
+                               int own_hi = 1 << 30, int interleaved = 0) {
   const int v4 = Dp / 4;
   const bool vec_out = (ld_out % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_image) | reinterpret_cast<uintptr_t>(d_text)) % 16 == 0);
   const int64_t per_g = int64_t(b) * v4;
@@ -1359,10 +1359,11 @@ __global__ void combine_kernel(const float4* intra, int ksplit, const float4* re
     const int64_t rem = int64_t(iu - unsigned(g) * pb) + int64_t(row0) * v4;
     const int r = int(unsigned(rem) / uv4), vc = int(unsigned(rem) % uv4);
     float4 cross;
-    if (xpart) {
-      const float4* src = xpart + (int64_t(g) * np) * per_g + rem;
+    if (xpart) {  // leaves [2][np][b][Dp] (peer windows) or leaf-interleaved [2][b][np][Dp] (local partials)
+      const int64_t ls = interleaved ? v4 : per_g;
+      const float4* src = xpart + (int64_t(g) * np) * per_g + (interleaved ? int64_t(r) * np * v4 + vc : rem);
       cross = tree_sum(np, [&](int k) {
-        const float4 x = __ldcs(src + k * per_g);
+        const float4 x = __ldcs(src + k * ls);
         return (flip && (k < own_lo || k >= own_hi)) ? f4neg(x) : x;
       });
     } else {
@@ -1408,8 +1409,8 @@ __global__ void contribution_kernel(const float4* intra, int ksplit, const float
     const int64_t dest = c / b, r = c % b;
     float4 x;
     if (xpart) {
-      const float4* src = xpart + (int64_t(g) * np) * per_g + rem;
-      x = tree_sum(np, [&](int k) { return src[k * per_g]; });
+      const float4* src = xpart + ((int64_t(g) * B + c) * np) * v4 + vc;
+      x = tree_sum(np, [&](int k) { return src[k * v4]; });
     } else {
       x = send[((dest * 2 + g) * b + r) * v4 + vc];
     }
@@ -2120,8 +2121,9 @@ int build_cross(GemmParams& p, int first, void* ws, const Geometry& g, int mt0 =
     q.a_row_off = 0;
     set_xform(q, ws, g, dsrc);
     if (g.np > 1) {  // canonical partials [2][np][B][Dp]
-      rc = set_output(q, region<float>(ws, g, DISCO_R_XPART) + int64_t(gi) * g.np * g.B * g.Dp, g.Dp, g.B, 0, 1,
-                      g.B * g.Dp, g.np);
+      // leaf-interleaved partials [2][B][np][Dp]: the combine's np loads of an element share a DRAM page
+      rc = set_output(q, region<float>(ws, g, DISCO_R_XPART) + int64_t(gi) * g.np * g.B * g.Dp, g.np * g.Dp, g.B, 0, 1,
+                      g.Dp, g.np);
     } else {  // directly destination-major send slabs [N][2][b][Dp]
       rc = set_output(q, region<float>(ws, g, DISCO_R_SEND) + int64_t(gi) * g.b * g.Dp, g.Dp, g.b, 2 * g.b * g.Dp,
                       g.N, 0, 1);
@@ -2152,7 +2154,8 @@ int launch_combine(void* ws, const Geometry& g, float t, int flip, int row0, int
   combine_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
       region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float4>(ws, g, DISCO_R_RECV),
       (g.N == 1 && g.np > 1) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, g.N, g.rank, int(g.b),
-      int(g.Dp), int(g.D), s, flip, d_image, d_text, ld_out, row0, nrows, region<Status>(ws, g, DISCO_R_STATUS));
+      int(g.Dp), int(g.D), s, flip, d_image, d_text, ld_out, row0, nrows, region<Status>(ws, g, DISCO_R_STATUS), 0,
+      1 << 30, 1);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
