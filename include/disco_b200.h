@@ -63,7 +63,7 @@ enum disco_region {
   DISCO_R_XPART = 9,   /* f32  [2][B][cpr][Dp]    cross partials per canonical row chunk     */
   DISCO_R_SEND = 10,   /* f32  [N][2][b][Dp]      cross slabs by destination (all_to_all in) */
   DISCO_R_RECV = 11,   /* f32  [N][2][b][Dp]      cross slabs by source (all_to_all out)     */
-  DISCO_R_INTRA = 12,  /* f32  [2][b][Dp]         intra-rank gradient terms                  */
+  DISCO_R_INTRA = 12,  /* f32  [2][ksplit][b][Dp] intra-rank gradient terms (K-split halves) */
   DISCO_R_STATUS = 13, /* f64 loss, i32 flags, f64 dL/dt   host-visible step status           */
   DISCO_R_SCALE = 14,  /* f32  [2][B/64][b]       group offsets m_g, then
                           f16  [2][B/64][b]       E -> G factors exp2(m_g - lse2) per row and
