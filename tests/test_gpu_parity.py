@@ -247,3 +247,21 @@ def test_host_pipelined_nonfinite_in_late_chunk():
         P.disco_step(None, I.astype(np.float32), T, 10.0)
     di, dt, loss = P.disco_step(None, I.astype(np.float32), O.synthetic_features(B, D, 2)[1].astype(np.float32), 10.0)
     assert np.isfinite(loss)
+
+
+def test_config_e_bitwise_and_sampled_oracle(release_plans):
+    """BASELINE config E (B=16384, D=1024: the non-distributed CLIP loss on one GPU): N=1 equals
+    N=8 simulated ranks bit for bit, and the f64 oracle on sampled rows within 1e-3."""
+    B, D, t = 16384, 1024, 100.0
+    I, T = O.synthetic_features(B, D, 12)
+    d8 = run_sim(I, T, 8, t)
+    from paper_2304_08480_b200.shard import clear_plans
+    clear_plans()
+    di, dt, loss = P.disco_step(None, dev(I), dev(T), t)
+    di, dt = di.cpu().numpy(), dt.cpu().numpy()
+    assert di.tobytes() == d8[0].tobytes() and dt.tobytes() == d8[1].tobytes() and loss == d8[2][0]
+    rows = np.linspace(0, B - 1, 48).astype(np.int64)
+    ri, rt, rl = O.clip_grad_rows(I, T, t, rows)
+    assert O.max_rel_error(di[rows], ri) < TOL
+    assert O.max_rel_error(dt[rows], rt) < TOL
+    assert abs(loss - rl[0]) / rl[0] < TOL
