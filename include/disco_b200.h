@@ -122,9 +122,10 @@ int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, floa
 
 /* Wavefront forward (single rank, canonical shapes with B % 2048 == 0; *waves = 0 otherwise):
  * disco_b200_forward == forward_wave(0) ... forward_wave(waves - 1) + forward_finish, bit for bit.
- * Wave k computes the logit units (row chunk, column chunk) with max(row chunk, column chunk) == k,
- * i.e. exactly those that became computable when rows [k*B/8, (k+1)*B/8) of I and T landed, so
- * the host->device copy of host features overlaps the logits GEMMs.  Waves may run on different
+ * With W = *waves (16 when B % 4096 == 0, else 8) and rows split in W equal chunks, wave k
+ * computes the logit units (row chunk, column chunk) with max(row chunk, column chunk) == k, i.e.
+ * exactly those that became computable when rows [k*B/W, (k+1)*B/W) of I and T landed, so the
+ * host->device copy of host features overlaps the logits GEMMs.  Waves may run on different
  * streams (they write disjoint outputs); forward_finish must follow all of them. */
 int disco_b200_forward_waves(int64_t B, int64_t D, int world, int rank, int* waves);
 int disco_b200_forward_wave(void* ws, int64_t B, int64_t D, int world, int rank, float t, int wave, void* stream);

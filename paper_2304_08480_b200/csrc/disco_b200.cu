@@ -141,9 +141,8 @@ struct LogitsParams {
   int groups;           // B / 128
   // wave >= 0 (single rank, H2D-pipelined forward): only the units whose row chunk or column
   // chunk is `wave` and the other index <= wave, i.e. the units that became computable when
-  // canonical chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per chunk.
+  // (stats sub-)chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per (sub-)chunk.
   int wave, rt_per_chunk;
-  int ssub;  // sub-chunks per canonical chunk (nchunk / chunk_cols above are per sub-chunk)
   unsigned long long* probe;  // Status::probe (may be null)
 };
 
@@ -411,7 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   constexpr bool CHUNK_UNITS = KIND != KIND_GRAD;  // unit = all tiles of one column chunk
   const int wave = CHUNK_UNITS ? p.wave : -1;
-  const int per_dir = wave >= 0 ? p.rt_per_chunk * (2 * wave + 1) * p.ssub
+  const int per_dir = wave >= 0 ? p.rt_per_chunk * (2 * wave + 1)
                                 : p.row_tiles * p.nchunk * (CHUNK_UNITS ? 1 : p.tiles_per_chunk);
   const int num_units = 2 * per_dir;
   const int tiles_per_unit = CHUNK_UNITS ? p.tiles_per_chunk : 1;
@@ -421,15 +420,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     dir = u / per_dir;
     int rem = u - dir * per_dir;
     if (wave >= 0) {  // new row tiles x chunks [0, wave], then old row tiles x chunk `wave`
-      const int nsw = p.ssub * (wave + 1);  // sub-chunks of chunks [0, wave]
-      const int fresh = p.rt_per_chunk * nsw;
+      const int fresh = p.rt_per_chunk * (wave + 1);
       if (rem < fresh) {
-        rt = wave * p.rt_per_chunk + rem / nsw;
-        ch = rem % nsw;
+        rt = wave * p.rt_per_chunk + rem / (wave + 1);
+        ch = rem % (wave + 1);
       } else {
-        rem -= fresh;
-        rt = rem / p.ssub;
-        ch = wave * p.ssub + rem % p.ssub;
+        rt = rem - fresh;
+        ch = wave;
       }
       t0 = 0;
     } else if (CHUNK_UNITS) {
@@ -1930,7 +1927,6 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.rank = g.rank;
   p.nchunk = g.nchunk * g.ssub;  // the kernel's "chunks" are the stats sub-chunks
   p.chunk_cols = g.chunk_cols / g.ssub;
-  p.ssub = g.ssub;
   p.tiles_per_chunk = (p.chunk_cols + BN - 1) / BN;
   p.row_tiles = int((g.b + PAIR_M - 1) / PAIR_M);
   p.tl2e = t * LOG2E;
@@ -1945,7 +1941,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.mg = region<float>(ws, g, DISCO_R_SCALE);
   p.groups = g.groups;
   p.wave = wave;
-  p.rt_per_chunk = g.chunk_cols / PAIR_M;
+  p.rt_per_chunk = p.chunk_cols / PAIR_M;  // waves are (sub-)chunks: rows and columns land together
   p.probe = probe_slot(ws, g, 0);
   if (kind != KIND_FWD && g.g_blocked) {
     const __half* Gb = region<__half>(ws, g, DISCO_R_G);
@@ -1956,7 +1952,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   }
   const int debug_flags = debug_flag_bits();
   p.debug_flags = debug_flags;
-  const int64_t units = wave >= 0 ? int64_t(2) * p.rt_per_chunk * (2 * wave + 1) * p.ssub
+  const int64_t units = wave >= 0 ? int64_t(2) * p.rt_per_chunk * (2 * wave + 1)
                                   : int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
   const bool ares = g.Dp <= BK * ARES_SLICES && (debug_flags & 128);  // experiment: not faster on B200
   if (kind == KIND_FWD) {
@@ -2385,7 +2381,9 @@ int disco_b200_forward_waves(int64_t B, int64_t D, int world, int rank, int* wav
   Geometry g;
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
-  *waves = (world == 1 && g.estore && g.chunk_cols % PAIR_M == 0) ? g.nchunk : 0;
+  // one wave per stats sub-chunk (16 at B % 4096 == 0): the work left after the last H2D chunk
+  // lands is (2W - 1) / W^2 of the forward
+  *waves = (world == 1 && g.estore && (g.chunk_cols / g.ssub) % PAIR_M == 0) ? g.nchunk * g.ssub : 0;
   return DISCO_OK;
 }
 
@@ -2394,9 +2392,10 @@ int disco_b200_forward_wave(void* ws, int64_t B, int64_t D, int world, int rank,
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
-  if (!(world == 1 && g.estore && g.chunk_cols % PAIR_M == 0))
+  if (!(world == 1 && g.estore && (g.chunk_cols / g.ssub) % PAIR_M == 0))
     return fail(DISCO_LAYOUT_ERROR, "wavefront forward needs a single rank and B %% 2048 == 0");
-  if (wave < 0 || wave >= g.nchunk) return fail(DISCO_LAYOUT_ERROR, "wave %d outside [0, %d)", wave, g.nchunk);
+  const int nw = g.nchunk * g.ssub;
+  if (wave < 0 || wave >= nw) return fail(DISCO_LAYOUT_ERROR, "wave %d outside [0, %d)", wave, nw);
   return launch_logits(KIND_FWDE, ws, g, t, static_cast<cudaStream_t>(stream), wave);
 }
 

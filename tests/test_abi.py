@@ -113,8 +113,10 @@ def test_peer_window_geometry():
 
 
 def test_wavefront_forward_availability():
-    """The H2D-pipelined forward needs a single rank and B % 2048 == 0 (256-row tiles per chunk)."""
-    assert _lib.forward_waves(32768, 512, 1, 0) == 8
+    """The H2D-pipelined forward needs a single rank and B % 2048 == 0 (whole 256-row tiles per
+    wave); waves follow the stats sub-chunks (16 when B % 4096 == 0)."""
+    assert _lib.forward_waves(32768, 512, 1, 0) == 16
+    assert _lib.forward_waves(4096, 512, 1, 0) == 16
     assert _lib.forward_waves(2048, 64, 1, 0) == 8
     assert _lib.forward_waves(3072, 512, 1, 0) == 0
     assert _lib.forward_waves(32768, 512, 2, 0) == 0
