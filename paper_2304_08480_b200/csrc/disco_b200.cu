@@ -1110,7 +1110,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       }
       it += two ? 2 : 1;
     }
-    if (lane == 0) ptx::bulk_wait_all();
+    if (lane == 0) {
+      ptx::bulk_wait_all();
+      bool any_peer = false;
+      for (int i = 0; i < p.nprob; ++i) any_peer |= p.prob[i].peer != 0;
+      if (any_peer) {  // pushed tiles are complete; order them before the arrival flags (next kernel)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence_system();
+      }
+    }
   }
   kernel_epilogue(ctl, warp);
   probe_mark(p.probe, 2);
