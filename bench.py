@@ -315,8 +315,8 @@ def run_ours(args):
     use_peer = world > 1 and peer_mod.enabled(ep) and peer_mod.supported(B, D, world, rank)
     if world == 1:  # the step runs intra + cross as one fused launch
         names = ["pack", "forward", "backward_grad", "backward", "combine", "loss"]
-    elif use_peer:  # fused intra + cross GEMM pushing cross tiles to the owners over NVLink
-        names = ["pack", "all_gather", "forward", "backward_grad", "backward_peer", "combine_peer", "loss"]
+    elif use_peer:  # peer all-gather (fused unpack), fused intra + cross GEMM pushing cross tiles to the owners
+        names = ["pack", "peer_gather", "forward", "backward_grad", "backward_peer", "combine_peer", "loss"]
     else:
         names = ["pack", "all_gather", "forward", "backward_grad", "backward_cross", "all_to_all",
                  "backward_intra", "combine", "loss"]
@@ -340,12 +340,18 @@ def run_ours(args):
         barrier()
         timed("pack", lambda: _lib.call("disco_b200_pack", *args_, I.data_ptr(), T.data_ptr(), D, D, _lib.BF16, 1, sp))
         timed("all_gather", lambda: ep.all_gather_into(plan.gather, plan.pack))
-        timed("forward", lambda: _lib.call("disco_b200_forward", *args_, t, sp))
-        timed("backward_grad", lambda: _lib.call("disco_b200_backward_grad", *args_, t, sp))
-        timed("backward", lambda: _lib.call("disco_b200_backward_fused", *args_, sp))
         if use_peer:
             pw = plan.peer_window(ep)
             epoch, parity = pw.next_step()
+            timed("peer_gather", lambda: (_lib.call("disco_b200_peer_publish", *args_, pw.bases, parity, epoch, sp),
+                                          _lib.call("disco_b200_peer_gather", *args_, pw.bases, parity, epoch,
+                                                    peer_mod.PEER_TIMEOUT_S, sp)))
+            timed("forward", lambda: _lib.call("disco_b200_forward_gathered", *args_, t, sp))
+        else:
+            timed("forward", lambda: _lib.call("disco_b200_forward", *args_, t, sp))
+        timed("backward_grad", lambda: _lib.call("disco_b200_backward_grad", *args_, t, sp))
+        timed("backward", lambda: _lib.call("disco_b200_backward_fused", *args_, sp))
+        if use_peer:
             timed("backward_peer", lambda: _lib.call("disco_b200_backward_peer", *args_, pw.bases, parity, epoch, sp))
             timed("combine_peer", lambda: _lib.call("disco_b200_combine_peer", *args_, t, 0, pw.base, parity, epoch,
                                                     peer_mod.PEER_TIMEOUT_S, di.data_ptr(), dt_.data_ptr(), D, sp))

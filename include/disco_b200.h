@@ -173,8 +173,9 @@ int disco_b200_combine_rows(void* ws, int64_t B, int64_t D, int world, int rank,
  * itself over NVLink peer memory instead of an NCCL all_to_all + sender presum.
  *
  * Every rank owns one peer window (disco_b200_peer_alloc: cudaMalloc'd, IPC-exportable):
- * u32 arrival flags [N], then two parity windows of [2][L][b][Dp] f32 slabs, L = N * (chunk
- * partials per rank).  disco_b200_backward_peer runs the intra and cross GEMMs as one persistent
+ * u32 arrival flags (slab slots [0, N), pack-ready slots [64, 64 + N)), then two parity windows
+ * of [2][L][b][Dp] f32 slabs, L = N * (chunk partials per rank), then two parity areas of
+ * [2][b][Dp] bf16 published rows.  disco_b200_backward_peer runs the intra and cross GEMMs as one persistent
  * launch; each cross tile's epilogue TMA-stores its fp32 chunk partial straight into the owning
  * rank's window (leaf rank*np + k), so the transfer overlaps the GEMM tile by tile; a one-warp
  * kernel then publishes `epoch` into every destination's flag slot [rank] (release, system
@@ -190,6 +191,17 @@ int disco_b200_peer_alloc(int64_t bytes, void** ptr, void* ipc_handle);
 int disco_b200_peer_open(const void* ipc_handle, void** ptr);
 int disco_b200_peer_close(void* ptr);
 int disco_b200_peer_free(void* ptr);
+/* Peer all-gather (replaces the NCCL all_gather + unpack at N > 1): publish copies this rank's
+ * packed rows (DISCO_R_PACK, written by disco_b200_pack) into its window's parity pack area and
+ * raises `epoch` in every window's pack-ready slot [rank]; gather waits (bounded, status flag 8)
+ * for all N pack-ready slots, then reads every rank's packed rows straight from its window
+ * (NVLink loads) into the forward (bf16) and backward (f16) operand layouts.  Follow it with
+ * disco_b200_forward_gathered (the forward without its unpack step). */
+int disco_b200_peer_publish(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
+                            int parity, uint32_t epoch, void* stream);
+int disco_b200_peer_gather(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
+                           int parity, uint32_t epoch, double timeout_s, void* stream);
+int disco_b200_forward_gathered(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
 int disco_b200_backward_peer(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
                              int parity, uint32_t epoch, void* stream);
 int disco_b200_combine_peer(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,

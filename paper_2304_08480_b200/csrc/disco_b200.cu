@@ -1478,6 +1478,35 @@ __global__ void peer_wait_kernel(const uint32_t* flags, int n, uint32_t epoch, S
   }
 }
 
+// Peer all-gather fused with the unpack: rank r's packed rows are read straight from its peer
+// window (NVLink loads) into the forward operands (bf16) and backward operands (f16).
+constexpr int PEER_PACK_FLAG0 = 64;  // u32 slot of the pack-ready flags in the flag block
+struct PeerSrc {
+  const uint4* pack[8];  // each rank's published [2][b][Dp] bf16 rows (this step's parity)
+};
+__global__ void peer_gather_unpack_kernel(PeerSrc src, int N, int b, int Dp, uint4* feat, uint4* feat16) {
+  const int vec_per_row = Dp / 8;
+  const int64_t per_rank = int64_t(2) * b * vec_per_row;
+  const int64_t total = int64_t(N) * per_rank;
+  const int64_t B = int64_t(N) * b;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int n = int(i / per_rank);
+    const int64_t j = i - n * per_rank;
+    const int vc = int(j % vec_per_row);
+    const int64_t rr = j / vec_per_row;
+    const int r = int(rr % b), dir = int(rr / b);
+    const uint4 x = src.pack[n][j];
+    const int64_t o = (dir * B + int64_t(n) * b + r) * vec_per_row + vc;
+    feat[o] = x;
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
+    uint4 y;
+    __half2* hy = reinterpret_cast<__half2*>(&y);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hy[k] = __float22half2_rn(__bfloat1622float2(h[k]));
+    feat16[o] = y;
+  }
+}
+
 // Loss: sum of the [N][2][b] per-row ce in an order fixed by the global row
 // index (independent of N), in f64, / (2 * N * b).  Stage 1: LOSS_BLOCKS
 // blocks each reduce a fixed contiguous slice of the flat index f = dir*B + g;
@@ -2225,7 +2254,15 @@ int forward_finish(void* ws, const Geometry& g, cudaStream_t st) {
 // ---------------------------------------------------------------- peer transport (host side)
 int64_t peer_leaves(const Geometry& g) { return int64_t(g.N) * g.np; }
 int64_t peer_window_bytes(const Geometry& g) { return round_up(2 * peer_leaves(g) * g.b * g.Dp * 4, 1024); }
-int64_t peer_total_bytes(const Geometry& g) { return PEER_FLAG_BYTES + 2 * peer_window_bytes(g); }
+int64_t peer_pack_bytes(const Geometry& g) { return round_up(2 * g.b * g.Dp * 2, 1024); }
+int64_t peer_total_bytes(const Geometry& g) {
+  return PEER_FLAG_BYTES + 2 * peer_window_bytes(g) + 2 * peer_pack_bytes(g);
+}
+// published packed rows of a rank, [2][b][Dp] bf16, parity window after the two slab windows
+uint8_t* peer_pack(const void* base, const Geometry& g, int parity) {
+  return const_cast<uint8_t*>(static_cast<const uint8_t*>(base)) + PEER_FLAG_BYTES + 2 * peer_window_bytes(g) +
+         int64_t(parity & 1) * peer_pack_bytes(g);
+}
 float* peer_window(const void* base, const Geometry& g, int parity) {
   return reinterpret_cast<float*>(const_cast<uint8_t*>(static_cast<const uint8_t*>(base)) + PEER_FLAG_BYTES +
                                   int64_t(parity & 1) * peer_window_bytes(g));
@@ -2367,13 +2404,23 @@ int disco_b200_pack_rows(void* ws, int64_t B, int64_t D, int world, int rank, co
   return DISCO_OK;
 }
 
+static int forward_impl(void* ws, int64_t B, int64_t D, int world, int rank, float t, bool unpack, void* stream);
+
 int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream) {
+  return forward_impl(ws, B, D, world, rank, t, true, stream);
+}
+
+int disco_b200_forward_gathered(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream) {
+  return forward_impl(ws, B, D, world, rank, t, false, stream);
+}
+
+static int forward_impl(void* ws, int64_t B, int64_t D, int world, int rank, float t, bool unpack, void* stream) {
   Geometry g;
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (world > 1) {  // single rank: pack already wrote FEAT / FEAT16
+  if (world > 1 && unpack) {  // single rank: pack already wrote FEAT / FEAT16; peer gather: fused
     const int64_t nvec = int64_t(world) * 2 * g.b * (g.Dp / 8);
     unpack_kernel<<<elementwise_grid(nvec, 256), 256, 0, st>>>(
         region<uint4>(ws, g, DISCO_R_GATHER), world, int(g.b), int(g.Dp), region<uint4>(ws, g, DISCO_R_FEAT),
@@ -2658,6 +2705,48 @@ int disco_b200_backward_peer(void* ws, int64_t B, int64_t D, int world, int rank
   for (int r = 0; r < g.N; ++r)
     pp.flag[r] = reinterpret_cast<uint32_t*>(peer_bases[r]) + rank;
   peer_signal_kernel<<<1, 32, 0, st>>>(pp, g.N, epoch);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_peer_publish(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
+                            int parity, uint32_t epoch, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if ((rc = check_peer(g))) return rc;
+  cudaStream_t st = st_of(stream);
+  CUDA_TRY(cudaMemcpyAsync(peer_pack(reinterpret_cast<const void*>(peer_bases[rank]), g, parity),
+                           region<uint8_t>(ws, g, DISCO_R_PACK), size_t(2 * g.b * g.Dp * 2), cudaMemcpyDeviceToDevice,
+                           st));
+  PeerPtrs pp;
+  memset(&pp, 0, sizeof(pp));
+  for (int r = 0; r < g.N; ++r)
+    pp.flag[r] = reinterpret_cast<uint32_t*>(peer_bases[r]) + PEER_PACK_FLAG0 + rank;
+  peer_signal_kernel<<<1, 32, 0, st>>>(pp, g.N, epoch);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_peer_gather(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
+                           int parity, uint32_t epoch, double timeout_s, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if ((rc = check_peer(g))) return rc;
+  cudaStream_t st = st_of(stream);
+  peer_wait_kernel<<<1, 32, 0, st>>>(reinterpret_cast<const uint32_t*>(peer_bases[rank]) + PEER_PACK_FLAG0, g.N,
+                                     epoch, region<Status>(ws, g, DISCO_R_STATUS), (unsigned long long)(timeout_s * 1e9));
+  count_launch();
+  PeerSrc src;
+  memset(&src, 0, sizeof(src));
+  for (int r = 0; r < g.N; ++r)
+    src.pack[r] = reinterpret_cast<const uint4*>(peer_pack(reinterpret_cast<const void*>(peer_bases[r]), g, parity));
+  const int64_t nvec = int64_t(g.N) * 2 * g.b * (g.Dp / 8);
+  peer_gather_unpack_kernel<<<elementwise_grid(nvec, 256), 256, 0, st>>>(
+      src, g.N, int(g.b), int(g.Dp), region<uint4>(ws, g, DISCO_R_FEAT), region<uint4>(ws, g, DISCO_R_FEAT16));
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;

@@ -466,6 +466,7 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
     device = _default_device() if on_host else local_I.device
     plan = get_plan(B, D, N, n, device)
     st = _stream_ptr(device)
+    pw = None  # peer window of this step (N > 1 with the peer transport)
     if on_host:
         if N != 1 or plan.waves == 0 or local_T.is_cuda:
             raise ValueError("host (CPU) features need a single rank and a wavefront shape; "
@@ -475,15 +476,21 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         code = _TORCH_DTYPE_CODE[local_I.dtype]
         _lib.call("disco_b200_pack", *plan.args, local_I.data_ptr(), local_T.data_ptr(),
                   local_I.stride(0), local_T.stride(0), code, 1, st)
-        if N > 1:
-            endpoint.all_gather_into(plan.gather, plan.pack)
-        _lib.call("disco_b200_forward", *plan.args, t, st)
+        if N > 1 and _peer.enabled(endpoint) and _peer.supported(B, D, N, n):
+            # peer transport: every rank reads the others' packed rows from their NVLink-mapped
+            # windows straight into its operand layouts (all_gather + unpack in one kernel)
+            pw = plan.peer_window(endpoint)
+            epoch, parity = pw.next_step()
+            _lib.call("disco_b200_peer_publish", *plan.args, pw.bases, parity, epoch, st)
+            _lib.call("disco_b200_peer_gather", *plan.args, pw.bases, parity, epoch, _peer.PEER_TIMEOUT_S, st)
+            _lib.call("disco_b200_forward_gathered", *plan.args, t, st)
+        else:
+            if N > 1:
+                endpoint.all_gather_into(plan.gather, plan.pack)
+            _lib.call("disco_b200_forward", *plan.args, t, st)
     _lib.call("disco_b200_backward_grad", *plan.args, t, st)
-    pw = None
-    if N > 1 and _peer.enabled(endpoint) and _peer.supported(B, D, N, n):
-        # peer transport: the fused backward GEMM pushes each cross tile to its owner over NVLink
-        pw = plan.peer_window(endpoint)
-        epoch, parity = pw.next_step()
+    if pw is not None:
+        # the fused backward GEMM pushes each cross tile to its owner over NVLink
         _lib.call("disco_b200_backward_peer", *plan.args, pw.bases, parity, epoch, st)
     elif N > 1:
         # cross first, so the slab exchange overlaps the intra GEMM

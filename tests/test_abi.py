@@ -97,7 +97,8 @@ def test_launch_counter_starts_at_zero_without_gpu():
 
 
 def test_peer_window_geometry():
-    """Peer window = flag block + two parity windows of [2][N*np][b][Dp] f32 (every source's leaves)."""
+    """Peer window = flag block + two parity windows of [2][N*np][b][Dp] f32 (every source's leaves)
+    + two parity areas of this rank's published [2][b][Dp] bf16 rows (the peer all-gather)."""
     out = ctypes.c_int64()
     lib = _lib.load()
     assert lib.disco_b200_peer_handle_bytes() == 64
@@ -105,7 +106,8 @@ def test_peer_window_geometry():
         _lib.call("disco_b200_peer_bytes", B, D, N, 0, ctypes.byref(out))
         b, Dp = B // N, (D + 63) // 64 * 64
         win = (2 * leaves * b * Dp * 4 + 1023) // 1024 * 1024
-        assert out.value == 1024 + 2 * win, (B, D, N)
+        pack = (2 * b * Dp * 2 + 1023) // 1024 * 1024
+        assert out.value == 1024 + 2 * win + 2 * pack, (B, D, N)
     with pytest.raises(LayoutError):  # nothing to exchange at N = 1
         _lib.call("disco_b200_peer_bytes", 4096, 512, 1, 0, ctypes.byref(out))
     with pytest.raises(LayoutError):  # b % 128 != 0
