@@ -359,8 +359,11 @@ def run_ours(args):
         timed("all_to_all", lambda: ep.all_to_all_into(plan.recv, plan.send))
         timed("backward_intra", lambda: _lib.call("disco_b200_backward_intra", *args_, sp))
         timed("combine", lambda: _lib.call("disco_b200_combine", *args_, t, 0, di.data_ptr(), dt_.data_ptr(), D, sp))
-        timed("loss", lambda: (world > 1 and ep.all_gather_into(plan.ce_all, plan.ce),
-                               _lib.call("disco_b200_loss", *args_, 0, sp)))
+        if use_peer:  # the ce rode with the slabs into this rank's window
+            timed("loss", lambda: _lib.call("disco_b200_loss_peer", *args_, pw.base, parity, sp))
+        else:
+            timed("loss", lambda: (world > 1 and ep.all_gather_into(plan.ce_all, plan.ce),
+                                   _lib.call("disco_b200_loss", *args_, 0, sp)))
         torch.cuda.synchronize()
         for n in names:
             acc[n] += ev[n][0].elapsed_time(ev[n][1]) / reps

@@ -175,7 +175,7 @@ int disco_b200_combine_rows(void* ws, int64_t B, int64_t D, int world, int rank,
  * Every rank owns one peer window (disco_b200_peer_alloc: cudaMalloc'd, IPC-exportable):
  * u32 arrival flags (slab slots [0, N), pack-ready slots [64, 64 + N)), then two parity windows
  * of [2][L][b][Dp] f32 slabs, L = N * (chunk partials per rank), then two parity areas of
- * [2][b][Dp] bf16 published rows.  disco_b200_backward_peer runs the intra and cross GEMMs as one persistent
+ * [2][b][Dp] bf16 published rows, then two parity areas of [N][2][b] f32 per-row ce.  disco_b200_backward_peer runs the intra and cross GEMMs as one persistent
  * launch; each cross tile's epilogue TMA-stores its fp32 chunk partial straight into the owning
  * rank's window (leaf rank*np + k), so the transfer overlaps the GEMM tile by tile; a one-warp
  * kernel then publishes `epoch` into every destination's flag slot [rank] (release, system
@@ -204,6 +204,12 @@ int disco_b200_peer_gather(void* ws, int64_t B, int64_t D, int world, int rank, 
 int disco_b200_forward_gathered(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
 int disco_b200_backward_peer(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
                              int parity, uint32_t epoch, void* stream);
+/* Loss at N > 1 with the peer transport: disco_b200_backward_peer also pushes the rank's per-row
+ * ce into every window's parity ce area ([N][2][b] f32, covered by the same arrival epoch), so
+ * after disco_b200_combine_peer the loss needs no collective: same fixed-order f64 sum as
+ * disco_b200_loss over the gathered ce. */
+int disco_b200_loss_peer(void* ws, int64_t B, int64_t D, int world, int rank, const void* my_base, int parity,
+                         void* stream);
 int disco_b200_combine_peer(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,
                             const void* my_base, int parity, uint32_t epoch, double timeout_s, float* d_image,
                             float* d_text, int64_t ld_out, void* stream);

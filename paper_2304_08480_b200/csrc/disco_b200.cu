@@ -1507,6 +1507,17 @@ __global__ void peer_gather_unpack_kernel(PeerSrc src, int N, int b, int Dp, uin
   }
 }
 
+// Per-row ce of this rank ([2][b]) into every rank's window ce area, slot `rank` of [N][2][b].
+struct PeerDst {
+  float* ce[8];
+};
+__global__ void peer_ce_push_kernel(const float4* ce, int n4, PeerDst dst, int N) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    const float4 v = ce[i];
+    for (int r = 0; r < N; ++r) reinterpret_cast<float4*>(dst.ce[r])[i] = v;
+  }
+}
+
 // Loss: sum of the [N][2][b] per-row ce in an order fixed by the global row
 // index (independent of N), in f64, / (2 * N * b).  Stage 1: LOSS_BLOCKS
 // blocks each reduce a fixed contiguous slice of the flat index f = dir*B + g;
@@ -2255,8 +2266,15 @@ int forward_finish(void* ws, const Geometry& g, cudaStream_t st) {
 int64_t peer_leaves(const Geometry& g) { return int64_t(g.N) * g.np; }
 int64_t peer_window_bytes(const Geometry& g) { return round_up(2 * peer_leaves(g) * g.b * g.Dp * 4, 1024); }
 int64_t peer_pack_bytes(const Geometry& g) { return round_up(2 * g.b * g.Dp * 2, 1024); }
+int64_t peer_ce_bytes(const Geometry& g) { return round_up(int64_t(g.N) * 2 * g.b * 4, 1024); }
 int64_t peer_total_bytes(const Geometry& g) {
-  return PEER_FLAG_BYTES + 2 * peer_window_bytes(g) + 2 * peer_pack_bytes(g);
+  return PEER_FLAG_BYTES + 2 * peer_window_bytes(g) + 2 * peer_pack_bytes(g) + 2 * peer_ce_bytes(g);
+}
+// every rank's per-row ce, [N][2][b] f32, parity area after the two pack areas
+float* peer_ce(const void* base, const Geometry& g, int parity) {
+  return reinterpret_cast<float*>(const_cast<uint8_t*>(static_cast<const uint8_t*>(base)) + PEER_FLAG_BYTES +
+                                  2 * peer_window_bytes(g) + 2 * peer_pack_bytes(g) +
+                                  int64_t(parity & 1) * peer_ce_bytes(g));
 }
 // published packed rows of a rank, [2][b][Dp] bf16, parity window after the two slab windows
 uint8_t* peer_pack(const void* base, const Geometry& g, int parity) {
@@ -2568,6 +2586,22 @@ int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank,
   return DISCO_OK;
 }
 
+int disco_b200_loss_peer(void* ws, int64_t B, int64_t D, int world, int rank, const void* my_base, int parity,
+                         void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if ((rc = check_peer(g))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Status* status = region<Status>(ws, g, DISCO_R_STATUS);
+  loss_partial_kernel<<<LOSS_BLOCKS, 256, 0, st>>>(peer_ce(my_base, g, parity), world, int(g.b),
+                                                   status->loss_partial);
+  loss_final_kernel<<<1, LOSS_BLOCKS, 0, st>>>(status->loss_partial, int64_t(2) * world * g.b, status);
+  count_launch(2);
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
 int disco_b200_loss(void* ws, int64_t B, int64_t D, int world, int rank, int local_only, void* stream) {
   Geometry g;
   int rc = make_geometry(B, D, world, rank, &g);
@@ -2700,6 +2734,15 @@ int disco_b200_backward_peer(void* ws, int64_t B, int64_t D, int world, int rank
   p.nprob = 4;
   p.split = 2;
   if ((rc = launch_gemm(p, st, g.wide, g.estore))) return rc;
+  // the rank's per-row ce rides with the slabs: the owners' combine wait covers it too
+  PeerDst pd;
+  memset(&pd, 0, sizeof(pd));
+  for (int r = 0; r < g.N; ++r)
+    pd.ce[r] = peer_ce(reinterpret_cast<const void*>(peer_bases[r]), g, parity) + int64_t(rank) * 2 * g.b;
+  const int n4 = int(2 * g.b / 4);
+  peer_ce_push_kernel<<<std::max(1, std::min(n4 / 256 + 1, 64)), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_CE), n4,
+                                                                               pd, g.N);
+  count_launch();
   PeerPtrs pp;
   memset(&pp, 0, sizeof(pp));
   for (int r = 0; r < g.N; ++r)

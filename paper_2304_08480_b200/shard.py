@@ -522,9 +522,12 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         if N == 1:
             _lib.call("disco_b200_backward_fused", *plan.args, st)
         _lib.call("disco_b200_combine", *plan.args, t, flip, d_image.data_ptr(), d_text.data_ptr(), D, st)
-    if N > 1:
-        endpoint.all_gather_into(plan.ce_all, plan.ce)
-    _lib.call("disco_b200_loss", *plan.args, 0, st)
+    if pw is not None:  # every rank's ce arrived with its slabs (covered by the combine's wait)
+        _lib.call("disco_b200_loss_peer", *plan.args, pw.base, parity, st)
+    else:
+        if N > 1:
+            endpoint.all_gather_into(plan.ce_all, plan.ce)
+        _lib.call("disco_b200_loss", *plan.args, 0, st)
     return d_image, d_text, plan
 
 

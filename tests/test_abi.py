@@ -107,7 +107,8 @@ def test_peer_window_geometry():
         b, Dp = B // N, (D + 63) // 64 * 64
         win = (2 * leaves * b * Dp * 4 + 1023) // 1024 * 1024
         pack = (2 * b * Dp * 2 + 1023) // 1024 * 1024
-        assert out.value == 1024 + 2 * win + 2 * pack, (B, D, N)
+        ce = (N * 2 * b * 4 + 1023) // 1024 * 1024
+        assert out.value == 1024 + 2 * win + 2 * pack + 2 * ce, (B, D, N)
     with pytest.raises(LayoutError):  # nothing to exchange at N = 1
         _lib.call("disco_b200_peer_bytes", 4096, 512, 1, 0, ctypes.byref(out))
     with pytest.raises(LayoutError):  # b % 128 != 0
