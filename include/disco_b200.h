@@ -131,6 +131,25 @@ int disco_b200_forward_waves(int64_t B, int64_t D, int world, int rank, int* wav
 int disco_b200_forward_wave(void* ws, int64_t B, int64_t D, int world, int rank, float t, int wave, void* stream);
 int disco_b200_forward_finish(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
 
+/* Streamed forward (host bf16 features, single rank, wavefront shape, D % 64 == 0): the caller
+ * copies chunk k's rows of I and T straight into DISCO_R_FEAT on a copy stream and then calls
+ * disco_b200_signal_wave(k, epoch) on that stream (cuStreamWriteValue32: no SM, ordered after
+ * the copies).  disco_b200_forward_streamed launches ONE persistent logits kernel over all
+ * waves in order whose producers wait for each wave's flag (bounded by timeout_s: status flag
+ * 16 instead of a hang), then derives the f16 operands and the non-finite flag, then the stats.
+ * Bit-identical to pack + disco_b200_forward; no per-wave launch tails.  Use a fresh epoch per
+ * step; the flags live in DISCO_R_STATUS, which the caller zeroes once when allocating. */
+int disco_b200_forward_streamed(void* ws, int64_t B, int64_t D, int world, int rank, float t, uint32_t epoch,
+                                double timeout_s, void* stream);
+int disco_b200_signal_wave(void* ws, int64_t B, int64_t D, int world, int rank, int wave, uint32_t epoch,
+                           void* stream);
+/* All of a step's chunk copies (pinned host bf16 [b][D] I and T -> DISCO_R_FEAT) and wave signals
+ * enqueued on copy_stream in one call.  Enqueue them BEFORE launching disco_b200_forward_streamed:
+ * streams may share a hardware queue, and a copy queued behind the spinning kernel could only run
+ * after it (the producers' bounded wait then expires); copies first can at worst serialise. */
+int disco_b200_h2d_streamed(void* ws, int64_t B, int64_t D, int world, int rank, const void* host_I,
+                            const void* host_T, uint32_t epoch, void* copy_stream);
+
 /* Backward part 1: recompute the logit tiles (bit-identical to the forward)
  * -> G = softmax - onehot, unscaled, f16 (shard.py:143-146, matrix.py:131-144).
  * Canonical shapes: no-op (G = E * scale, label column P_label - 1, is formed

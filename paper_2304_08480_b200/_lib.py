@@ -46,6 +46,9 @@ SIGNATURES = {
     "disco_b200_forward": [_vp, _i64, _i64, _int, _int, _f32, _vp],
     "disco_b200_forward_waves": [_i64, _i64, _int, _int, ctypes.POINTER(_int)],
     "disco_b200_forward_wave": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp],
+    "disco_b200_forward_streamed": [_vp, _i64, _i64, _int, _int, _f32, ctypes.c_uint32, ctypes.c_double, _vp],
+    "disco_b200_h2d_streamed": [_vp, _i64, _i64, _int, _int, _vp, _vp, ctypes.c_uint32, _vp],
+    "disco_b200_signal_wave": [_vp, _i64, _i64, _int, _int, _int, ctypes.c_uint32, _vp],
     "disco_b200_forward_finish": [_vp, _i64, _i64, _int, _int, _vp],
     "disco_b200_backward_grad": [_vp, _i64, _i64, _int, _int, _f32, _vp],
     "disco_b200_backward_cross": [_vp, _i64, _i64, _int, _int, _vp],

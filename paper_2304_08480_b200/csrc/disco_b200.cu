@@ -100,6 +100,7 @@ constexpr int FLAG_INPUT_NONFINITE = 1;
 constexpr int FLAG_LOSS_NONFINITE = 2;
 constexpr int FLAG_GRAD_NONFINITE = 4;
 constexpr int FLAG_PEER_TIMEOUT = 8;  // peer transport: a peer's slabs never arrived (wait kernel gave up)
+constexpr int FLAG_H2D_TIMEOUT = 16;  // streamed forward: an H2D chunk never landed
 
 struct Status {
   double loss;
@@ -113,6 +114,9 @@ struct Status {
   // drain probe (backward GEMM, epilogue warp 2 of every leader CTA): sum over units of the
   // cycles from "accumulators full" to "accumulators released", and the unit count
   unsigned long long drain[2];
+  // streamed forward (host inputs): wave k's rows landed in FEAT once wave_flags[k] >= the step's
+  // epoch; written by the copy stream (cuStreamWriteValue32), polled by the logits producers
+  unsigned int wave_flags[32];
 };
 
 // ----------------------------------------------------------- kernel params
@@ -143,6 +147,13 @@ struct LogitsParams {
   // chunk is `wave` and the other index <= wave, i.e. the units that became computable when
   // (stats sub-)chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per (sub-)chunk.
   int wave, rt_per_chunk;
+  // streamed (wave == -2): one persistent launch over all waves in order; the producers wait for
+  // wave_flags[k] >= epoch before loading wave k's tiles
+  const unsigned int* wave_flags;
+  unsigned int epoch;
+  int nwaves;
+  unsigned long long timeout_ns;
+  int* status_flags;
   unsigned long long* probe;  // Status::probe (may be null)
 };
 
@@ -410,23 +421,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   constexpr bool CHUNK_UNITS = KIND != KIND_GRAD;  // unit = all tiles of one column chunk
   const int wave = CHUNK_UNITS ? p.wave : -1;
+  const bool streamed = wave == -2;
   const int per_dir = wave >= 0 ? p.rt_per_chunk * (2 * wave + 1)
                                 : p.row_tiles * p.nchunk * (CHUNK_UNITS ? 1 : p.tiles_per_chunk);
-  const int num_units = 2 * per_dir;
+  const int num_units = streamed ? 2 * p.rt_per_chunk * p.nwaves * p.nwaves : 2 * per_dir;
+  // streamed: unit u belongs to wave k with 2 R k^2 <= u < 2 R (k+1)^2 (wave k holds 2 R (2k+1))
+  auto wave_of = [&](int u) {
+    int k = int(sqrtf(float(u) / float(2 * p.rt_per_chunk)));
+    while (k > 0 && 2 * p.rt_per_chunk * k * k > u) --k;
+    while (2 * p.rt_per_chunk * (k + 1) * (k + 1) <= u) ++k;
+    return k;
+  };
   const int tiles_per_unit = CHUNK_UNITS ? p.tiles_per_chunk : 1;
   const int nk = p.Dp / BK;
 
   auto decode = [&](int u, int& dir, int& rt, int& ch, int& t0) {
-    dir = u / per_dir;
-    int rem = u - dir * per_dir;
-    if (wave >= 0) {  // new row tiles x chunks [0, wave], then old row tiles x chunk `wave`
-      const int fresh = p.rt_per_chunk * (wave + 1);
+    int wv = wave, pd = per_dir;
+    if (streamed) {
+      wv = wave_of(u);
+      u -= 2 * p.rt_per_chunk * wv * wv;
+      pd = p.rt_per_chunk * (2 * wv + 1);
+    }
+    dir = u / pd;
+    int rem = u - dir * pd;
+    if (wv >= 0) {  // new row tiles x chunks [0, wave], then old row tiles x chunk `wave`
+      const int fresh = p.rt_per_chunk * (wv + 1);
       if (rem < fresh) {
-        rt = wave * p.rt_per_chunk + rem / (wave + 1);
-        ch = rem % (wave + 1);
+        rt = wv * p.rt_per_chunk + rem / (wv + 1);
+        ch = rem % (wv + 1);
       } else {
         rt = rem - fresh;
-        ch = wave;
+        ch = wv;
       }
       t0 = 0;
     } else if (CHUNK_UNITS) {
@@ -490,9 +515,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           }
         }
       } else {
+        unsigned int landed = 0;  // streamed: waves known to have landed
         for (int u = pair; u < num_units; u += npairs) {
           int dir, rt, ch, t0;
           decode(u, dir, rt, ch, t0);
+          if (streamed) {
+            const int k = wave_of(u);
+            if (k >= int(landed)) {
+              unsigned long long t_start;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+              while (true) {
+                unsigned int v;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.wave_flags + k) : "memory");
+                if (int(v - p.epoch) >= 0) break;  // epoch-relative: wraps safely
+                unsigned long long t_now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+                if (t_now - t_start > p.timeout_ns) {  // never hang: flag it, compute garbage, host raises
+                  atomicOr(p.status_flags, FLAG_H2D_TIMEOUT);
+                  break;
+                }
+                __nanosleep(128);
+              }
+              asm volatile("fence.proxy.async.global;" ::: "memory");  // the TMA loads below see the rows
+              landed = unsigned(k) + 1;
+            }
+          }
           const int a_row = p.rank * p.b + rt * PAIR_M + crank * BM;
           for (int ti = 0; ti < tiles_per_unit; ++ti) {
             const int col0 = ch * p.chunk_cols + (t0 + ti) * BN + crank * (BN / 2);
@@ -1219,6 +1266,26 @@ __global__ void unpack_kernel(const uint4* gathered, int N, int b, int Dp, uint4
   }
 }
 
+// Streamed forward: the H2D copies wrote the bf16 operands (FEAT) directly; derive the f16
+// backward operands and raise the non-finite input flag (the pack's other two jobs).
+__global__ void feat16_kernel(const uint4* feat, uint4* feat16, int64_t n, Status* status) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint4 x = feat[i];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
+    uint4 y;
+    __half2* hy = reinterpret_cast<__half2*>(&y);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __bfloat1622float2(h[k]);
+      bad |= !(isfinite(f.x) && isfinite(f.y));
+      hy[k] = __float22half2_rn(f);
+    }
+    feat16[i] = y;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&status->flags, FLAG_INPUT_NONFINITE);
+}
+
 // Per (dir,row): fixed-order combine of the (column chunk, column half)
 // (max, sum-exp) partials.  Within a chunk: half 0 + half 1; across the 8
 // canonical chunks: balanced tree ((0+1)+(2+3))+((4+5)+(6+7)); non-canonical
@@ -1806,6 +1873,21 @@ unsigned long long* probe_slot(void* ws, const Geometry& g, int at) {
   return reinterpret_cast<unsigned long long*>(region<uint8_t>(ws, g, DISCO_R_STATUS) + offsetof(Status, probe)) + at;
 }
 
+// cuStreamWriteValue32 (driver API, no SM involved): the copy stream's "chunk landed" signal.
+using PFN_writeValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_writeValue32 write_value_fn() {
+  static PFN_writeValue32 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_writeValue32>(ptr);
+  });
+  return fn;
+}
+
 // ------------------------------------------------------------ tensor maps
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1958,7 +2040,8 @@ int launch_logits_t(const LogitsParams& p, int64_t units, cudaStream_t st, const
   return DISCO_OK;
 }
 
-int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t st, int wave = -1) {
+int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t st, int wave = -1,
+                  unsigned int epoch = 0, double timeout_s = 0.0) {
   LogitsParams p;
   memset(&p, 0, sizeof(p));
   const __nv_bfloat16* feat = region<__nv_bfloat16>(ws, g, DISCO_R_FEAT);
@@ -1989,6 +2072,8 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.mg = region<float>(ws, g, DISCO_R_SCALE);
   p.groups = g.groups;
   p.wave = wave;
+  p.epoch = epoch;
+  p.timeout_ns = (unsigned long long)(timeout_s * 1e9);
   p.rt_per_chunk = p.chunk_cols / PAIR_M;  // waves are (sub-)chunks: rows and columns land together
   p.probe = probe_slot(ws, g, 0);
   if (kind != KIND_FWD && g.g_blocked) {
@@ -2000,9 +2085,16 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   }
   const int debug_flags = debug_flag_bits();
   p.debug_flags = debug_flags;
-  const int64_t units = wave >= 0 ? int64_t(2) * p.rt_per_chunk * (2 * wave + 1)
+  if (wave == -2) {
+    Status* stt = region<Status>(ws, g, DISCO_R_STATUS);
+    p.wave_flags = stt->wave_flags;
+    p.status_flags = &stt->flags;
+    p.nwaves = g.nchunk * g.ssub;
+  }
+  const int64_t units = wave == -2 ? int64_t(2) * p.rt_per_chunk * p.nwaves * p.nwaves
+                      : wave >= 0 ? int64_t(2) * p.rt_per_chunk * (2 * wave + 1)
                                   : int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
-  const bool ares = g.Dp <= BK * ARES_SLICES && (debug_flags & 128);  // experiment: not faster on B200
+  const bool ares = g.Dp <= BK * ARES_SLICES && (debug_flags & 128) && wave != -2;  // experiment: not faster
   if (kind == KIND_FWD) {
     rc = ares ? launch_logits_t<KIND_FWD, true>(p, units, st) : launch_logits_t<KIND_FWD, false>(p, units, st);
     if (rc) return rc;
@@ -2470,6 +2562,65 @@ int disco_b200_forward_wave(void* ws, int64_t B, int64_t D, int world, int rank,
   const int nw = g.nchunk * g.ssub;
   if (wave < 0 || wave >= nw) return fail(DISCO_LAYOUT_ERROR, "wave %d outside [0, %d)", wave, nw);
   return launch_logits(KIND_FWDE, ws, g, t, static_cast<cudaStream_t>(stream), wave);
+}
+
+int disco_b200_forward_streamed(void* ws, int64_t B, int64_t D, int world, int rank, float t, uint32_t epoch,
+                                double timeout_s, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
+  if (!(world == 1 && g.estore && (g.chunk_cols / g.ssub) % PAIR_M == 0 && g.D == g.Dp))
+    return fail(DISCO_LAYOUT_ERROR, "streamed forward needs a single rank, B %% 2048 == 0 and D %% 64 == 0");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((rc = launch_logits(KIND_FWDE, ws, g, t, st, -2, epoch, timeout_s))) return rc;
+  const int64_t n = 2 * g.B * g.Dp / 8;
+  feat16_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(region<uint4>(ws, g, DISCO_R_FEAT),
+                                                         region<uint4>(ws, g, DISCO_R_FEAT16), n,
+                                                         region<Status>(ws, g, DISCO_R_STATUS));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return forward_finish(ws, g, st);
+}
+
+int disco_b200_h2d_streamed(void* ws, int64_t B, int64_t D, int world, int rank, const void* host_I,
+                            const void* host_T, uint32_t epoch, void* copy_stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (!(world == 1 && g.estore && (g.chunk_cols / g.ssub) % PAIR_M == 0 && g.D == g.Dp))
+    return fail(DISCO_LAYOUT_ERROR, "streamed forward needs a single rank, B %% 2048 == 0 and D %% 64 == 0");
+  auto fn = write_value_fn();
+  if (!fn) return fail(DISCO_CUDA_ERROR, "cuStreamWriteValue32 unavailable");
+  const int waves = g.nchunk * g.ssub;
+  const int64_t rows = g.b / waves, row_bytes = g.Dp * 2;
+  uint8_t* feat = region<uint8_t>(ws, g, DISCO_R_FEAT);
+  Status* stt = region<Status>(ws, g, DISCO_R_STATUS);
+  cudaStream_t st = static_cast<cudaStream_t>(copy_stream);
+  for (int k = 0; k < waves; ++k) {
+    const int64_t off = k * rows * row_bytes, n = rows * row_bytes;
+    CUDA_TRY(cudaMemcpyAsync(feat + off, static_cast<const uint8_t*>(host_I) + off, size_t(n),
+                             cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(feat + g.B * row_bytes + off, static_cast<const uint8_t*>(host_T) + off, size_t(n),
+                             cudaMemcpyHostToDevice, st));
+    CUresult r = fn(static_cast<CUstream>(copy_stream), reinterpret_cast<CUdeviceptr>(&stt->wave_flags[k]), epoch, 0);
+    if (r != CUDA_SUCCESS) return fail(DISCO_CUDA_ERROR, "cuStreamWriteValue32 failed (%d)", int(r));
+  }
+  return DISCO_OK;
+}
+
+int disco_b200_signal_wave(void* ws, int64_t B, int64_t D, int world, int rank, int wave, uint32_t epoch,
+                           void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (wave < 0 || wave >= 32) return fail(DISCO_LAYOUT_ERROR, "wave %d outside [0, 32)", wave);
+  auto fn = write_value_fn();
+  if (!fn) return fail(DISCO_CUDA_ERROR, "cuStreamWriteValue32 unavailable");
+  Status* stt = region<Status>(ws, g, DISCO_R_STATUS);
+  CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(&stt->wave_flags[wave]), epoch, 0);
+  if (r != CUDA_SUCCESS) return fail(DISCO_CUDA_ERROR, "cuStreamWriteValue32 failed (%d)", int(r));
+  return DISCO_OK;
 }
 
 int disco_b200_forward_finish(void* ws, int64_t B, int64_t D, int world, int rank, void* stream) {

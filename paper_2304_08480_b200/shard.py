@@ -140,7 +140,11 @@ class Plan:
         self.recv = view(_lib.R_RECV, torch.float32)
         self.rdot = view(_lib.R_RDOT, torch.float32)
         self.rdot_all = view(_lib.R_RDOT_ALL, torch.float32)
-        self.status = view(_lib.R_STATUS, torch.uint8)[:24]
+        status_all = view(_lib.R_STATUS, torch.uint8)
+        status_all.zero_()  # the streamed forward's wave flags start below every epoch
+        self.status = status_all[:24]
+        self.feat = view(_lib.R_FEAT, torch.bfloat16).view(2, B, self.Dp)
+        self.h2d_epoch = 0
         self.status_host = torch.empty(24, dtype=torch.uint8, pin_memory=True)
         self.waves = _lib.forward_waves(B, D, world, rank)
         self._copy_stream = None
@@ -295,6 +299,8 @@ def _raise_on_flags(flags: int) -> None:
         raise ValueError("cross-entropy logits contains non-finite entries")
     if flags & 4:
         raise ValueError("gradient contribution contains non-finite entries")
+    if flags & 16:
+        raise RuntimeError("streamed forward: a host->device chunk never landed (wave flag timeout)")
     if flags & 8:
         raise CollectiveTimeoutError(
             f"peer transport: gradient slabs did not arrive within {_peer.PEER_TIMEOUT_S:g}s")
@@ -439,6 +445,34 @@ def _pipelined_pack_forward(plan: Plan, I_host: torch.Tensor, T_host: torch.Tens
     _lib.call("disco_b200_forward_finish", *plan.args, cur.cuda_stream)
 
 
+# host bf16 features with D % 64 == 0: one persistent, flag-gated logits launch (streamed forward)
+STREAMED_FORWARD = True
+H2D_TIMEOUT_S = 30.0
+
+
+def _streamed_forward(plan: Plan, I_host: torch.Tensor, T_host: torch.Tensor, t: float) -> None:
+    """Single rank, host bf16 features: chunk k's rows are copied straight into the forward
+    operands (DISCO_R_FEAT) on a copy stream, each followed by a stream write of the wave flag;
+    ONE persistent logits kernel walks the waves in order, its producers waiting on each flag.
+    Bit-identical to pack + disco_b200_forward."""
+    device = plan.device
+    cur = torch.cuda.current_stream(device)
+    h2d, _ = plan.h2d_streams()
+    b, D = I_host.shape
+    feat = plan.feat
+    # status reset, ordered before everything of this step (no rows are packed: 0..0)
+    _lib.call("disco_b200_pack_rows", *plan.args, feat.data_ptr(), feat.data_ptr(), D, D, _lib.BF16, 1, 0, 0,
+              cur.cuda_stream)
+    h2d.wait_stream(cur)  # the previous step is done with FEAT
+    plan.h2d_epoch = (plan.h2d_epoch + 1) & 0x7FFFFFFF or 1
+    epoch = plan.h2d_epoch
+    # every copy and wave signal is enqueued (one native call) BEFORE the kernel that waits on them
+    _lib.call("disco_b200_h2d_streamed", *plan.args, I_host.data_ptr(), T_host.data_ptr(), epoch, h2d.cuda_stream)
+    plan.h2d_keepalive = (I_host, T_host)  # raw-pointer copies: keep the host rows alive past this step
+    _lib.call("disco_b200_forward_streamed", *plan.args, t, epoch, H2D_TIMEOUT_S, cur.cuda_stream)
+    cur.wait_stream(h2d)
+
+
 def host_pipelined(world: int, B: int, D: int, rank: int = 0) -> bool:
     """True when disco_step_async overlaps the H2D copy of host features with the forward."""
     return world == 1 and _lib.forward_waves(B, D, world, rank) > 0
@@ -471,7 +505,12 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         if N != 1 or plan.waves == 0 or local_T.is_cuda:
             raise ValueError("host (CPU) features need a single rank and a wavefront shape; "
                              "stage them to the device first")
-        _pipelined_pack_forward(plan, local_I.contiguous(), local_T.contiguous(), t)
+        if (STREAMED_FORWARD and local_I.dtype == torch.bfloat16 and local_T.dtype == torch.bfloat16
+                and D == plan.Dp and local_I.is_contiguous() and local_T.is_contiguous()
+                and local_I.is_pinned() and local_T.is_pinned()):
+            _streamed_forward(plan, local_I.contiguous(), local_T.contiguous(), t)
+        else:
+            _pipelined_pack_forward(plan, local_I.contiguous(), local_T.contiguous(), t)
     else:
         code = _TORCH_DTYPE_CODE[local_I.dtype]
         _lib.call("disco_b200_pack", *plan.args, local_I.data_ptr(), local_T.data_ptr(),

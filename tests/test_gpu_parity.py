@@ -265,3 +265,25 @@ def test_config_e_bitwise_and_sampled_oracle(release_plans):
     assert O.max_rel_error(di[rows], ri) < TOL
     assert O.max_rel_error(dt[rows], rt) < TOL
     assert abs(loss - rl[0]) / rl[0] < TOL
+
+
+def test_streamed_forward_missing_chunk_times_out():
+    """The streamed forward's producers never wait unboundedly: a wave flag that is never raised
+    sets status flag 16 and the host raises instead of the GPU hanging."""
+    from paper_2304_08480_b200 import _lib
+    from paper_2304_08480_b200.shard import get_plan
+    B, D = 4096, 128
+    plan = get_plan(B, D, 1, 0, torch.device("cuda", 0))
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("disco_b200_pack_rows", *plan.args, plan.feat.data_ptr(), plan.feat.data_ptr(), D, D, _lib.BF16, 1,
+              0, 0, st)
+    _lib.call("disco_b200_forward_streamed", *plan.args, 10.0, 0x7FFF0000, 0.2, st)  # epoch never signalled
+    with pytest.raises(RuntimeError, match="never landed"):
+        P.finish_status(plan)
+    # the plan stays usable: a normal host-buffer step afterwards is correct
+    I, T = O.synthetic_features(B, D, 13)
+    Ih = torch.from_numpy(I.astype(np.float32)).bfloat16().pin_memory()
+    Th = torch.from_numpy(T.astype(np.float32)).bfloat16().pin_memory()
+    dh_i, dh_t, lh = P.disco_step(None, Ih, Th, 10.0)
+    dd_i, dd_t, ld = P.disco_step(None, Ih.cuda(), Th.cuda(), 10.0)
+    assert torch.equal(dh_i, dd_i.cpu()) and torch.equal(dh_t, dd_t.cpu()) and lh == ld
