@@ -1776,11 +1776,15 @@ struct Geometry {
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// DISCO_DEBUG_FLAGS (profiling experiments only): bit0 skip G / E stores, bit9 FWDE epilogue only
-// drains TMEM (no math, no stores), bit1 L2
-// persistence for the features in GRAD, bit4 skip GEMM output stores, bit5 GEMM epilogues store
-// with st.global instead of TMA, bit6 GEMM epilogues store via coalesced st.global rows, bit7
-// logits kernel keeps a resident A block (measured no faster, so off by default).
+// DISCO_DEBUG_FLAGS / disco_b200_set_experiment_flags (profiling experiments and ablations only;
+// tools/ab_kernels.py, tools/flag_parity.py).  Ablations produce wrong results on purpose.
+//   bit0  (1)       skip the G / E TMA stores              bit1  (2)       L2 persistence window (GRAD)
+//   bit4  (16)      GEMM: drain TMEM, store nothing        bit5  (32)      GEMM: st.global epilogue
+//   bit6  (64)      GEMM: coalesced st.global rows         bit7  (128)     logits: A-resident ring
+//   bit8  (256)     narrow (256-column) GEMM units         bit9  (512)     FWDE: drain TMEM only
+//   bit10 (1024)    transform warps skip the rescale       bit11 (2048)    GEMM: no accumulator drain
+//   bit15 (32768)   GEMM: stage but never TMA-store        bit17 (131072)  FWDE: E math only, no stores
+//   bit18 (262144)  GEMM: round-robin instead of LPT       bit19 (524288)  whole-chunk logits units
 std::atomic<int> g_debug_bits{[] {
   const char* e = getenv("DISCO_DEBUG_FLAGS");
   return e ? atoi(e) : 0;
