@@ -221,6 +221,19 @@ int disco_b200_peer_publish(void* ws, int64_t B, int64_t D, int world, int rank,
 int disco_b200_peer_gather(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
                            int parity, uint32_t epoch, double timeout_s, void* stream);
 int disco_b200_forward_gathered(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
+/* Streamed alternative (all-gather overlapped with the logits GEMM, canonical shapes): after
+ * disco_b200_peer_publish, peer_gather_streamed enqueues on a copy stream, for k = 0..N-1 and
+ * src = (rank + k) % N, a cuStreamWaitValue32 on src's pack-ready slot (no SM), the copy of src's
+ * rows (NVLink, copy engine) into the forward operands, and a stream write of wave flag k;
+ * forward_peer_streamed (enqueued after it on the compute stream) is ONE persistent logits
+ * launch whose producers take the column waves in that order, waiting on each flag (bounded:
+ * status flag 16), then derives the f16 operands and the statistics.  Results are bit-identical
+ * to the other gather paths.  Not for ranks sharing a GPU inside one process (the spinning
+ * kernel can hold the SMs another rank's pack needs). */
+int disco_b200_peer_gather_streamed(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
+                                    int parity, uint32_t epoch, void* copy_stream);
+int disco_b200_forward_peer_streamed(void* ws, int64_t B, int64_t D, int world, int rank, float t, uint32_t epoch,
+                                     double timeout_s, void* stream);
 int disco_b200_backward_peer(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
                              int parity, uint32_t epoch, void* stream);
 /* Loss at N > 1 with the peer transport: disco_b200_backward_peer also pushes the rank's per-row

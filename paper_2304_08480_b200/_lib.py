@@ -68,6 +68,9 @@ SIGNATURES = {
     "disco_b200_peer_gather": [_vp, _i64, _i64, _int, _int, ctypes.POINTER(ctypes.c_uint64), _int, ctypes.c_uint32,
                                ctypes.c_double, _vp],
     "disco_b200_forward_gathered": [_vp, _i64, _i64, _int, _int, _f32, _vp],
+    "disco_b200_peer_gather_streamed": [_vp, _i64, _i64, _int, _int, ctypes.POINTER(ctypes.c_uint64), _int,
+                                        ctypes.c_uint32, _vp],
+    "disco_b200_forward_peer_streamed": [_vp, _i64, _i64, _int, _int, _f32, ctypes.c_uint32, ctypes.c_double, _vp],
     "disco_b200_backward_peer": [_vp, _i64, _i64, _int, _int, ctypes.POINTER(ctypes.c_uint64), _int,
                                  ctypes.c_uint32, _vp],
     "disco_b200_loss_peer": [_vp, _i64, _i64, _int, _int, _vp, _int, _vp],

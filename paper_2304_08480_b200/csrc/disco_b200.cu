@@ -421,12 +421,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   constexpr bool CHUNK_UNITS = KIND != KIND_GRAD;  // unit = all tiles of one column chunk
   const int wave = CHUNK_UNITS ? p.wave : -1;
-  const bool streamed = wave == -2;
+  // streamed modes: -2 = H2D row/column wavefront (single rank), -3 = peer column waves (N > 1:
+  // wave k = the columns of source rank (rank + k) % N, all local row tiles)
+  const bool streamed = wave == -2 || wave == -3;
+  const bool colwaves = wave == -3;
+  const int spr = colwaves ? p.nchunk / p.nwaves : 1;          // sub-chunks per source rank
+  const int per_cwave = 2 * p.row_tiles * spr;                  // units per column wave
   const int per_dir = wave >= 0 ? p.rt_per_chunk * (2 * wave + 1)
                                 : p.row_tiles * p.nchunk * (CHUNK_UNITS ? 1 : p.tiles_per_chunk);
-  const int num_units = streamed ? 2 * p.rt_per_chunk * p.nwaves * p.nwaves : 2 * per_dir;
-  // streamed: unit u belongs to wave k with 2 R k^2 <= u < 2 R (k+1)^2 (wave k holds 2 R (2k+1))
+  const int num_units = colwaves ? per_cwave * p.nwaves
+                                 : streamed ? 2 * p.rt_per_chunk * p.nwaves * p.nwaves : 2 * per_dir;
+  // -2: unit u belongs to wave k with 2 R k^2 <= u < 2 R (k+1)^2 (wave k holds 2 R (2k+1))
   auto wave_of = [&](int u) {
+    if (colwaves) return u / per_cwave;
     int k = int(sqrtf(float(u) / float(2 * p.rt_per_chunk)));
     while (k > 0 && 2 * p.rt_per_chunk * k * k > u) --k;
     while (2 * p.rt_per_chunk * (k + 1) * (k + 1) <= u) ++k;
@@ -436,6 +443,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const int nk = p.Dp / BK;
 
   auto decode = [&](int u, int& dir, int& rt, int& ch, int& t0) {
+    if (colwaves) {
+      const int k = u / per_cwave;
+      int rem = u - k * per_cwave;
+      dir = rem / (p.row_tiles * spr);
+      rem -= dir * p.row_tiles * spr;
+      rt = rem / spr;
+      ch = ((p.rank + k) % p.nwaves) * spr + rem % spr;
+      t0 = 0;
+      return;
+    }
     int wv = wave, pd = per_dir;
     if (streamed) {
       wv = wave_of(u);
@@ -1892,6 +1909,21 @@ PFN_writeValue32 write_value_fn() {
   return fn;
 }
 
+// cuStreamWaitValue32: a copy stream waits for a peer's published flag without any SM.
+using PFN_waitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_waitValue32 wait_value_fn() {
+  static PFN_waitValue32 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_waitValue32>(ptr);
+  });
+  return fn;
+}
+
 // ------------------------------------------------------------ tensor maps
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -2089,16 +2121,17 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   }
   const int debug_flags = debug_flag_bits();
   p.debug_flags = debug_flags;
-  if (wave == -2) {
+  if (wave == -2 || wave == -3) {
     Status* stt = region<Status>(ws, g, DISCO_R_STATUS);
     p.wave_flags = stt->wave_flags;
     p.status_flags = &stt->flags;
-    p.nwaves = g.nchunk * g.ssub;
+    p.nwaves = wave == -2 ? g.nchunk * g.ssub : g.N;
   }
-  const int64_t units = wave == -2 ? int64_t(2) * p.rt_per_chunk * p.nwaves * p.nwaves
+  const int64_t units = wave == -3 ? int64_t(2) * p.row_tiles * p.nchunk
+                      : wave == -2 ? int64_t(2) * p.rt_per_chunk * p.nwaves * p.nwaves
                       : wave >= 0 ? int64_t(2) * p.rt_per_chunk * (2 * wave + 1)
                                   : int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
-  const bool ares = g.Dp <= BK * ARES_SLICES && (debug_flags & 128) && wave != -2;  // experiment: not faster
+  const bool ares = g.Dp <= BK * ARES_SLICES && (debug_flags & 128) && wave > -2;  // experiment: not faster
   if (kind == KIND_FWD) {
     rc = ares ? launch_logits_t<KIND_FWD, true>(p, units, st) : launch_logits_t<KIND_FWD, false>(p, units, st);
     if (rc) return rc;
@@ -2948,6 +2981,60 @@ int disco_b200_peer_gather(void* ws, int64_t B, int64_t D, int world, int rank, 
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
+}
+
+int disco_b200_peer_gather_streamed(void* ws, int64_t B, int64_t D, int world, int rank, const uint64_t* peer_bases,
+                                    int parity, uint32_t epoch, void* copy_stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if ((rc = check_peer(g))) return rc;
+  if (!(g.estore && (g.nchunk * g.ssub) % g.N == 0))
+    return fail(DISCO_LAYOUT_ERROR, "streamed peer gather needs canonical chunks");
+  auto wfn = write_value_fn();
+  auto wait = wait_value_fn();
+  if (!wfn || !wait) return fail(DISCO_CUDA_ERROR, "stream memory operations unavailable");
+  cudaStream_t st = static_cast<cudaStream_t>(copy_stream);
+  const int64_t rank_bytes = g.b * g.Dp * 2;  // one direction of one rank's rows
+  uint8_t* feat = region<uint8_t>(ws, g, DISCO_R_FEAT);
+  Status* stt = region<Status>(ws, g, DISCO_R_STATUS);
+  const uint32_t* my_flags = reinterpret_cast<const uint32_t*>(peer_bases[rank]) + PEER_PACK_FLAG0;
+  for (int k = 0; k < g.N; ++k) {
+    const int src = (rank + k) % g.N;
+    const uint8_t* from = src == rank ? region<uint8_t>(ws, g, DISCO_R_PACK)
+                                      : peer_pack(reinterpret_cast<const void*>(peer_bases[src]), g, parity);
+    if (src != rank) {  // wait (copy engine, no SM) until that rank published this step's rows
+      CUresult r = wait(static_cast<CUstream>(copy_stream), reinterpret_cast<CUdeviceptr>(my_flags + src), epoch,
+                        0 /* CU_STREAM_WAIT_VALUE_GEQ */);
+      if (r != CUDA_SUCCESS) return fail(DISCO_CUDA_ERROR, "cuStreamWaitValue32 failed (%d)", int(r));
+    }
+    for (int d = 0; d < 2; ++d)
+      CUDA_TRY(cudaMemcpyAsync(feat + (int64_t(d) * g.B + int64_t(src) * g.b) * g.Dp * 2, from + d * rank_bytes,
+                               size_t(rank_bytes), cudaMemcpyDeviceToDevice, st));
+    CUresult r = wfn(static_cast<CUstream>(copy_stream), reinterpret_cast<CUdeviceptr>(&stt->wave_flags[k]), epoch, 0);
+    if (r != CUDA_SUCCESS) return fail(DISCO_CUDA_ERROR, "cuStreamWriteValue32 failed (%d)", int(r));
+  }
+  return DISCO_OK;
+}
+
+int disco_b200_forward_peer_streamed(void* ws, int64_t B, int64_t D, int world, int rank, float t, uint32_t epoch,
+                                     double timeout_s, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if ((rc = check_peer(g))) return rc;
+  if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
+  if (!(g.estore && (g.nchunk * g.ssub) % g.N == 0))
+    return fail(DISCO_LAYOUT_ERROR, "streamed peer forward needs canonical chunks");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((rc = launch_logits(KIND_FWDE, ws, g, t, st, -3, epoch, timeout_s))) return rc;
+  const int64_t n = 2 * g.B * g.Dp / 8;
+  feat16_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(region<uint4>(ws, g, DISCO_R_FEAT),
+                                                         region<uint4>(ws, g, DISCO_R_FEAT16), n,
+                                                         region<Status>(ws, g, DISCO_R_STATUS));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return forward_finish(ws, g, st);
 }
 
 int disco_b200_combine_peer(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,

@@ -31,6 +31,17 @@ def enabled(endpoint) -> bool:
     return bool(flag) and endpoint.world_size > 1
 
 
+def streamed_gather(endpoint, B: int, world: int) -> bool:
+    """The all-gather overlapped with the logits GEMM (copy-engine pulls + flag-gated persistent
+    kernel).  Opt-in (DISCO_PEER_STREAMED=1) and one process per GPU only: when ranks share a GPU
+    (threads of one process, or the two-process single-GPU check) one rank's spinning kernel can
+    hold the SMs the other rank's publish needs -- measured to time out at B=8192 on one GPU; with
+    a GPU per rank that cannot happen, but the path is not yet validated on NVLink."""
+    if getattr(endpoint, "in_process", False) or os.environ.get("DISCO_PEER_STREAMED", "0") in ("", "0"):
+        return False
+    return B % 1024 == 0 and 8 % world == 0  # canonical chunks
+
+
 def supported(B: int, D: int, world: int, rank: int) -> bool:
     if world < 2 or world > 8 or B % world or (B // world) % 128:
         return False

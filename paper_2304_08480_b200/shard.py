@@ -148,6 +148,7 @@ class Plan:
         self.status_host = torch.empty(24, dtype=torch.uint8, pin_memory=True)
         self.waves = _lib.forward_waves(B, D, world, rank)
         self._copy_stream = None
+        self._gather_stream = None
         self._h2d_stream = None
         self._wave_stream = None
         self._peer = None
@@ -168,6 +169,12 @@ class Plan:
             torch.cuda.synchronize(self.device)
             self._peer.close()
             self._peer = None
+
+    def gather_stream(self) -> "torch.cuda.Stream":
+        """Copy stream of the streamed peer all-gather (N > 1)."""
+        if self._gather_stream is None:
+            self._gather_stream = torch.cuda.Stream(self.device)
+        return self._gather_stream
 
     def copy_stream(self) -> "torch.cuda.Stream":
         """Side stream for the pipelined device->host gradient copies (created on first use)."""
@@ -521,8 +528,18 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
             pw = plan.peer_window(endpoint)
             epoch, parity = pw.next_step()
             _lib.call("disco_b200_peer_publish", *plan.args, pw.bases, parity, epoch, st)
-            _lib.call("disco_b200_peer_gather", *plan.args, pw.bases, parity, epoch, _peer.PEER_TIMEOUT_S, st)
-            _lib.call("disco_b200_forward_gathered", *plan.args, t, st)
+            if _peer.streamed_gather(endpoint, B, N):
+                # copy-engine pulls gated by the peers' pack-ready flags, enqueued BEFORE the one
+                # persistent logits launch that consumes them column wave by column wave
+                cur = torch.cuda.current_stream(device)
+                gs = plan.gather_stream()
+                gs.wait_stream(cur)
+                _lib.call("disco_b200_peer_gather_streamed", *plan.args, pw.bases, parity, epoch, gs.cuda_stream)
+                _lib.call("disco_b200_forward_peer_streamed", *plan.args, t, epoch, _peer.PEER_TIMEOUT_S, st)
+                cur.wait_stream(gs)
+            else:
+                _lib.call("disco_b200_peer_gather", *plan.args, pw.bases, parity, epoch, _peer.PEER_TIMEOUT_S, st)
+                _lib.call("disco_b200_forward_gathered", *plan.args, t, st)
         else:
             if N > 1:
                 endpoint.all_gather_into(plan.gather, plan.pack)

@@ -111,14 +111,18 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_peer_two_processes_ipc(tmp_path):
-    """Two processes, one GPU, gloo + CUDA IPC windows: bitwise equal to N = 1."""
+@pytest.mark.parametrize("streamed", ["0", "1"])
+def test_peer_two_processes_ipc(tmp_path, streamed):
+    """Two processes, one GPU, gloo + CUDA IPC windows: bitwise equal to N = 1, with the kernel
+    all-gather and (small B, where the shared GPU's time slicing lets both ranks publish before
+    either spins for long) the streamed copy-engine all-gather."""
     B, D = 2048, 256
     I, T = O.synthetic_features(B, D, 11)
     np.save(tmp_path / "I.npy", I.astype(np.float32))
     np.save(tmp_path / "T.npy", T.astype(np.float32))
     port = _free_port()
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2",
+               DISCO_PEER_STREAMED=streamed, DISCO_PEER_TIMEOUT="30")
     procs = []
     for r in range(2):
         e = dict(env, RANK=str(r))
