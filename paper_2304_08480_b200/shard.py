@@ -391,24 +391,29 @@ def _account_loss_scope(loss_counters, exchange_counters, b, B, D) -> None:
         loss_counters.release(2 * b * B)
 
 
-# Fractions of the 256-row tiles per output row block of the pipelined backward: quarters, the
-# last one halved so the exposed device->host tail is short (measured best of several schedules
-# with tools/e2e_timeline.py --sweep: shorter blocks cost more GEMM efficiency than they hide).
-ROW_BLOCK_FRACTIONS = (0.25, 0.25, 0.25, 0.125, 0.125)
+# Fractions of the 256-row tiles per output row block of the pipelined backward: shrinking by
+# ~0.8 per block (32, 25, 20, 16, 12, 10, 8, 5 of 128 tiles), so each block's device->host copy
+# (19 us/tile) fits under the next block's GEMMs (24 us/tile) and the exposed tail is the last
+# 5 tiles.  Measured with tools/e2e_ab.py against quarters-then-eighths: -0.09 ms e2e; faster
+# shrinking (more, smaller launches) or intra-ahead schedules measured slower.
+ROW_BLOCK_FRACTIONS = (0.25, 0.1953125, 0.15625, 0.125, 0.09375, 0.078125, 0.0625, 0.0390625)
 
 
-def row_blocks(b: int):
-    """Output row blocks of the single-rank pipelined backward (ROW_BLOCK_FRACTIONS of the
-    256-row tiles; one block for small b)."""
+def row_blocks(b: int, fractions=None):
+    """Output row blocks of the single-rank pipelined backward (fractions of the 256-row tiles,
+    ROW_BLOCK_FRACTIONS by default; one block for small b)."""
+    fractions = fractions or ROW_BLOCK_FRACTIONS
     tiles = (b + 255) // 256
     if tiles < 8:
         return [(0, b)]
     cuts, acc = [0], 0.0
-    for f in ROW_BLOCK_FRACTIONS[:-1]:
+    for f in fractions[:-1]:
         acc += f
-        cuts.append(max(cuts[-1] + 1, min(tiles - 1, round(acc * tiles))))
+        c = max(cuts[-1] + 1, round(acc * tiles))
+        if c < tiles:
+            cuts.append(c)
     cuts.append(tiles)
-    return [(min(256 * lo, b), min(256 * hi, b)) for lo, hi in zip(cuts, cuts[1:]) if hi > lo]
+    return [(min(256 * lo, b), min(256 * hi, b)) for lo, hi in zip(cuts, cuts[1:])]
 
 
 def _pipelined_pack_forward(plan: Plan, I_host: torch.Tensor, T_host: torch.Tensor, t: float) -> None:

@@ -81,3 +81,14 @@ def test_counters_match_reference_accounting():
     assert loss.peak_live_elements == 2 * b * B and loss.live_elements == 0
     assert loss.flops == 4 * b * B * D
     assert exch.peak_live_elements == 2 * B * D and exch.flops == 8 * b * B * D
+
+
+def test_row_blocks_partition_rows():
+    """The pipelined read-back's row blocks partition [0, b) into non-empty, 256-aligned blocks."""
+    from paper_2304_08480_b200.shard import row_blocks
+    for b in (256, 1792, 2048, 2304, 3072, 4096, 8192, 32768, 65536, 196608 // 8):
+        bl = row_blocks(b)
+        assert bl[0][0] == 0 and bl[-1][1] == b
+        assert all(hi > lo for lo, hi in bl)
+        assert all(bl[i][1] == bl[i + 1][0] for i in range(len(bl) - 1))
+        assert all(lo % 256 == 0 for lo, _ in bl)

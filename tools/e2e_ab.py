@@ -16,12 +16,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, default=32768)
 ap.add_argument("--dim", type=int, default=512)
 ap.add_argument("--reps", type=int, default=12)
-ap.add_argument("--set", default=None, help="NAME=0|1: set a boolean switch in paper_2304_08480_b200.shard")
+ap.add_argument("--set", action="append", default=[],
+                help="NAME=VALUE: set a module switch in paper_2304_08480_b200.shard (Python literal)")
 a = ap.parse_args()
 if a.set:
+    import ast
     from paper_2304_08480_b200 import shard
-    name, val = a.set.split("=")
-    setattr(shard, name, val not in ("0", "False", "false"))
+    for kv in a.set:
+        name, val = kv.split("=", 1)
+        setattr(shard, name, ast.literal_eval(val))
 torch.cuda.set_device(0)
 g = torch.Generator(device="cuda")
 g.manual_seed(1234)
@@ -41,4 +44,4 @@ for _ in range(a.reps):
     s1.record()
     s1.synchronize()
     ms.append(s0.elapsed_time(s1))
-print(f"{a.set or 'default'}: e2e median {statistics.median(ms):.4f} ms min {min(ms):.4f} loss {loss:.6f}")
+print(f"{' '.join(a.set) or 'default'}: e2e median {statistics.median(ms):.4f} ms min {min(ms):.4f} loss {loss:.6f}")
