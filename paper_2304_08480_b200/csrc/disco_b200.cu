@@ -1218,10 +1218,11 @@ __global__ void pack_kernel(const void* I, const void* Tm, int64_t ldI, int64_t 
   const int v8 = Dp / 8;
   const int64_t total = int64_t(2) * nrows * v8;
   bool bad = false;
+  const unsigned uv8 = unsigned(v8), unr = unsigned(nrows);  // total < 2^31: 32-bit index math
   for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < total; j += int64_t(gridDim.x) * blockDim.x) {
-    const int c0 = int(j % v8) * 8;
-    const int64_t rr = j / v8;
-    const int dir = int(rr / nrows), r = row0 + int(rr % nrows);
+    const unsigned ju = unsigned(j), rr = ju / uv8;
+    const int c0 = int(ju - rr * uv8) * 8;
+    const int dir = int(rr / unr), r = row0 + int(rr - unsigned(dir) * unr);
     const int64_t i = (int64_t(dir) * b + r) * v8 + c0 / 8;
     const void* src = dir ? Tm : I;
     const int64_t base = r * (dir ? ldT : ldI);
