@@ -116,7 +116,7 @@ int disco_b200_pack_rows(void* ws, int64_t B, int64_t D, int world, int rank, co
  * fixed-order chunk combine -> per-row lse / ce / label gradient.
  * Canonical shapes (B % 1024 == 0, N | 8): the same epilogue also stores
  * E = exp2(t*log2(e)*s - m_g) (f16, DISCO_R_G) with m_g the row max over its
- * 128-column group, and the combine turns m_g into exp2(m_g - lse2)
+ * 64-column group, and the combine turns m_g into exp2(m_g - lse2)
  * (DISCO_R_SCALE), so the backward needs no logit recompute. */
 int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream);
 

@@ -10,14 +10,19 @@
 //   d_g   = t * 0.5 / B * (Y_g + sum_over_ranks X_g)
 //
 // Kernels
-//   logits_kernel<FWD>  : tcgen05 bf16 GEMM tiles of S with a fused online
-//                         (max, sum-exp) + target epilogue; S never hits HBM.
-//   logits_kernel<GRAD> : same tiles recomputed, epilogue writes f16 G.
-//   gemm_kernel         : grouped f16 GEMM (K-major or MN-major operands via
-//                         the UMMA descriptor major bits; no transposes),
-//                         fp32 tiles into partial / slab buffers.
-//   small kernels       : pack, unpack, stats combine, chunk presum, owner
-//                         combine, contribution, loss.
+//   logits_kernel<FWDE> : tcgen05 bf16 GEMM tiles of S with a fused online (max, sum-exp) +
+//                         target epilogue that also stores E = exp2(y - group max) in f16
+//                         (canonical shapes); S never hits HBM.  Variants: one launch, H2D
+//                         wavefronts, flag-gated persistent (streamed) over waves.
+//   logits_kernel<FWD>  : statistics only; logits_kernel<GRAD>: tiles recomputed -> f16 G
+//                         (non-canonical shapes).
+//   gemm_kernel         : grouped f16 GEMM (K-major or MN-major operands via the UMMA
+//                         descriptor major bits; no transposes), E -> G rescaled in shared memory
+//                         by transform warps, fp32 tiles into partial / slab buffers or, with the
+//                         peer transport, straight into the owning rank's window; static LPT
+//                         schedule over CTA pairs.
+//   small kernels       : pack, unpack / peer gather-unpack, stats combine, E -> G factors,
+//                         presum, owner combine, contribution, loss, peer signal / wait, towers.
 // All tensor-core kernels run on CTA pairs (cluster of 2, cta_group::2):
 //   TMA (SWIZZLE_128B; each CTA loads its 128 A rows and its 128-column half of
 //   B, completion counted on the leader's barrier) -> 6-stage smem ring ->
@@ -140,9 +145,9 @@ struct LogitsParams {
   int64_t ldG;
   int g_blocked;        // 1: G stored as [2][b/128][B/128][128][128] (contiguous 32 KiB blocks)
   int debug_flags;      // DISCO_DEBUG_FLAGS (profiling experiments only): bit0 skip G stores
-  // FWDE outputs: E = exp2(y - m_g) into the blocked G region, m_g per (dir, 128-column group, row)
+  // FWDE outputs: E = exp2(y - m_g) into the blocked G region, m_g per (dir, 64-column group, row)
   float* mg;            // [2][groups][b]
-  int groups;           // B / 128
+  int groups;           // B / 64 (GROUP_COLS)
   // wave >= 0 (single rank, H2D-pipelined forward): only the units whose row chunk or column
   // chunk is `wave` and the other index <= wave, i.e. the units that became computable when
   // (stats sub-)chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per (sub-)chunk.
@@ -389,7 +394,7 @@ __device__ __forceinline__ void release_accumulator(SmemCtl* ctl, int buf, int l
 // (w - 2) / 4 of this CTA's 128 x 256 accumulator.
 // =====================================================================
 // FWDE (canonical shapes): the forward epilogue also stores E = exp2(y - m_g), f16, where
-// m_g is the max of the row over its 128-column group, plus m_g itself.  The backward
+// m_g is the max of the row over its 64-column group, plus m_g itself.  The backward
 // GEMMs turn E into G = E * exp2(m_g - lse2) (label column: P_label - 1) in shared memory,
 // so the logits are never recomputed.
 enum { KIND_FWD = 0, KIND_GRAD = 1, KIND_FWDE = 2 };
@@ -1351,7 +1356,7 @@ __global__ void stats_combine_kernel(const float2* stats, const float* target, i
 }
 
 // E path: m_g [2][groups][b] (f32, log2 domain) -> sc [2][groups][b] = exp2(m_g - lse2[dir][r]) as f16,
-// the E -> G factor of every (row, 128-column group).  8 elements per thread (b % 8 == 0).
+// the E -> G factor of every (row, 64-column group).  8 elements per thread (b % 8 == 0).
 __global__ void scale_kernel(const float4* mg, const float* lse2, int groups, int b, uint4* sc) {
   const int64_t per_dir = int64_t(groups) * b / 8;
   const int64_t total = 2 * per_dir;
@@ -1785,7 +1790,7 @@ struct Geometry {
   int wide;               // Dp % 512 == 0: GEMM units cover all of D (two accumulators, G read once)
   int ksplit;             // intra K split (fixed function of B, D): partials [2][ksplit][b][Dp]
   int estore;             // forward stores E + group offsets; backward GEMMs rescale E -> G (no recompute)
-  int groups;             // B / 128 column groups (E offsets)
+  int groups;             // B / 64 column groups (E offsets)
   int chunk_cols;         // B / nchunk
   int64_t off[DISCO_R_COUNT];
   int64_t len[DISCO_R_COUNT];
