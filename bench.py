@@ -293,12 +293,6 @@ def run_ours(args):
             ends[i].record(st)
         torch.cuda.synchronize()
     launches = _lib.launch_count() - launches0
-    # NVML's throttle reasons lag a ~50 ms burst: keep sampling over the same work for
-    # another ~0.5 s (untimed) so a power cap that shaped the timed steps is reported
-    with ClockSampler(local_rank) as clk_after:
-        for _ in range(max(20, 100 // max(1, args.steps))):
-            step()
-        torch.cuda.synchronize()
     barrier()
     loss = P.finish_status(plan)
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -400,6 +394,14 @@ def run_ours(args):
                "h2d_bytes_per_step": int(I_h.numel() * I_h.element_size() * 2),
                "d2h_bytes_per_step": out_bytes,
                "ms_per_step": em}
+
+    # NVML's throttle reasons lag a ~50 ms burst: sample over ~0.5 s more of the same work (untimed,
+    # after every measurement) so a power cap that shaped the timed steps is reported
+    with ClockSampler(local_rank) as clk_after:
+        for _ in range(max(20, 100 // max(1, args.steps))):
+            step()
+        torch.cuda.synchronize()
+    P.finish_status(plan)
 
     if rank != 0:
         if world > 1:
