@@ -148,6 +148,8 @@ struct LogitsParams {
   // FWDE outputs: E = exp2(y - m_g) into the blocked G region, m_g per (dir, 64-column group, row)
   float* mg;            // [2][groups][b]
   int groups;           // B / 64 (GROUP_COLS)
+  // SYM (N = 1): dir-1 statistics per (64-row group of S_0, column): sum of E_1 without the label
+  float* ssum;          // [groups][B]
   // wave >= 0 (single rank, H2D-pipelined forward): only the units whose row chunk or column
   // chunk is `wave` and the other index <= wave, i.e. the units that became computable when
   // (stats sub-)chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per (sub-)chunk.
@@ -330,6 +332,50 @@ __device__ __forceinline__ void xform_row(uint8_t* rowp, int sw, __half sc, int 
     *reinterpret_cast<__half*>(rowp + ((((lab_rel >> 3) ^ sw)) << 4) + (lab_rel & 7) * 2) = __float2half_rn(glab);
 }
 
+// Symmetric single-rank forward (SYM, N = 1): S_1 = S_0^T, so one GEMM tile of S_0 feeds both
+// directions.  lane_scatter reduces a warp's 32 x 32 block down its rows: lane L ends with the
+// max / sum over the 32 lanes of column L (31 shuffles in a fixed butterfly, deterministic).
+template <bool MAX>
+__device__ __forceinline__ float lane_scatter(const float* v, int lane) {
+  float a[16];
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float keep = hi ? v[i + 16] : v[i], send = hi ? v[i] : v[i + 16];
+      const float got = __shfl_xor_sync(0xffffffffu, send, 16);
+      a[i] = MAX ? fmaxf(keep, got) : keep + got;
+    }
+  }
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1) {
+    const bool hi = lane & w;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float keep = hi ? a[i + w] : a[i], send = hi ? a[i] : a[i + w];
+      const float got = __shfl_xor_sync(0xffffffffu, send, w);
+      a[i] = MAX ? fmaxf(keep, got) : keep + got;
+    }
+  }
+  return a[0];
+}
+
+// A warp's 32 x 32 f16 block stored transposed into a 32-row x 64-byte SWIZZLE_64B staging tile:
+// lane r holds w[k] = (row r; columns 2k, 2k+1), tile row c receives column c of all 32 lanes.
+// A 2 x 2 exchange inside lane pairs forms (row 2m, row 2m + 1) words, so each STS is 32-bit and
+// one instruction fills two whole tile rows (bank-conflict-free).
+__device__ __forceinline__ void st_transposed_64(uint8_t* tile, int lane, const uint32_t* w) {
+  const int odd = lane & 1, m = lane >> 1;
+  const uint32_t sel = odd ? 0x3276u : 0x5410u;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const uint32_t o = __shfl_xor_sync(0xffffffffu, w[k], 1);
+    const uint32_t x = __byte_perm(w[k], o, sel);
+    const int c = 2 * k + odd;
+    *reinterpret_cast<uint32_t*>(tile + c * 64 + (((m >> 2) ^ ((c >> 1) & 3)) << 4) + (m & 3) * 4) = x;
+  }
+}
+
 // Clock probe: CTA 0, thread 0 records {clock64, globaltimer} at slot [at, at + 1].
 __device__ __forceinline__ void probe_mark(unsigned long long* probe, int at) {
   if (probe && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -403,13 +449,26 @@ enum { KIND_FWD = 0, KIND_GRAD = 1, KIND_FWDE = 2 };
 // column tiles of the unit and only B streams through a 4-stage ring; A slice k of the next unit
 // is reloaded as soon as the unit's last tile has consumed it.  Halves the TMA fill traffic and
 // cuts smem traffic per MMA from ~128 to ~96 B/clk/SM (the narrow 256-column tile is smem-bound).
-template <int KIND, bool ARES>
+// SYM (FWDE, N = 1): units cover direction 0 only; each epilogue warp also emits the t2i E block
+// of its 32 x 32 half slices (column maxima over the 64-row group shared with the partner warp
+// through shared memory, E_1 stored transposed) and the dir-1 group sums.  5-stage ring so that
+// three staging half-buffers per warp fit.
+constexpr int SYM_STAGES = 5;
+constexpr int SYM_EBUFS = 3;
+static_assert(SYM_STAGES * STAGE_BYTES + NUM_EPI_WARPS * (SYM_EBUFS * STAGING_TILE / 2 + 256) <=
+                  TILE_RING_BYTES + STAGING_BYTES, "SYM smem layout");
+template <int KIND, bool ARES, bool SYM = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     logits_kernel(const __grid_constant__ LogitsParams p) {
+  static_assert(!SYM || (KIND == KIND_FWDE && !ARES), "SYM is a FWDE variant");
+  constexpr int LRS = SYM ? SYM_STAGES : Ring<1>::STAGES;  // operand ring stages
+  constexpr int EBUFS = SYM ? SYM_EBUFS : 2;                // E staging half-buffers per warp
+  constexpr int NDIR = SYM ? 1 : 2;                         // directions walked by the units
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
-  uint8_t* staging = tiles + TILE_RING_BYTES;
-  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(staging + STAGING_BYTES);
+  uint8_t* staging = tiles + LRS * STAGE_BYTES;
+  float* xbuf = reinterpret_cast<float*>(staging + NUM_EPI_WARPS * EBUFS * (STAGING_TILE / 2));  // SYM: [8][64]
+  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + TILE_RING_BYTES + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int crank = int(ptx::cluster_ctarank());
   const bool leader = crank == 0;
@@ -435,13 +494,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const int per_dir = wave >= 0 ? p.rt_per_chunk * (2 * wave + 1)
                                 : p.row_tiles * p.nchunk * (CHUNK_UNITS ? 1 : p.tiles_per_chunk);
   const int num_units = colwaves ? per_cwave * p.nwaves
-                                 : streamed ? 2 * p.rt_per_chunk * p.nwaves * p.nwaves : 2 * per_dir;
-  // -2: unit u belongs to wave k with 2 R k^2 <= u < 2 R (k+1)^2 (wave k holds 2 R (2k+1))
+                                 : streamed ? NDIR * p.rt_per_chunk * p.nwaves * p.nwaves : NDIR * per_dir;
+  // -2: unit u belongs to wave k with 2 R k^2 <= u < 2 R (k+1)^2 (wave k holds 2 R (2k+1));
+  // SYM: R k^2 <= u < R (k+1)^2
   auto wave_of = [&](int u) {
     if (colwaves) return u / per_cwave;
-    int k = int(sqrtf(float(u) / float(2 * p.rt_per_chunk)));
-    while (k > 0 && 2 * p.rt_per_chunk * k * k > u) --k;
-    while (2 * p.rt_per_chunk * (k + 1) * (k + 1) <= u) ++k;
+    int k = int(sqrtf(float(u) / float(NDIR * p.rt_per_chunk)));
+    while (k > 0 && NDIR * p.rt_per_chunk * k * k > u) --k;
+    while (NDIR * p.rt_per_chunk * (k + 1) * (k + 1) <= u) ++k;
     return k;
   };
   const int tiles_per_unit = CHUNK_UNITS ? p.tiles_per_chunk : 1;
@@ -461,7 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int wv = wave, pd = per_dir;
     if (streamed) {
       wv = wave_of(u);
-      u -= 2 * p.rt_per_chunk * wv * wv;
+      u -= NDIR * p.rt_per_chunk * wv * wv;
       pd = p.rt_per_chunk * (2 * wv + 1);
     }
     dir = u / pd;
@@ -491,7 +551,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
-      Pipe pipe;
+      Pipe<LRS> pipe;
       // L2 prefetch of the operands of the tile after the current one: the G
       // write stream (GRAD) evicts feature lines, and a demand miss behind the
       // DRAM write queue is longer than the smem ring can cover.
@@ -567,7 +627,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const int col0 = ch * p.chunk_cols + (t0 + ti) * BN + crank * (BN / 2);
             for (int kb = 0; kb < nk; ++kb) {
               uint32_t bar;
-              uint8_t* st = producer_acquire<1>(ctl, tiles, pipe, leader, bar);
+              uint8_t* st = producer_acquire<1, false, LRS>(ctl, tiles, pipe, leader, bar);
               ptx::tma_load_2d_pair(st, &p.a_map[dir], bar, kb * BK, a_row, ptx::kEvictLast);
               ptx::tma_load_2d_pair(st + A_STAGE_BYTES, &p.b_map[dir], bar, kb * BK, col0, ptx::kEvictLast);
               pipe.advance();
@@ -579,7 +639,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     if (leader) {  // ---------------- MMA issuer (leader CTA, whole warp; one elected lane issues)
       constexpr uint32_t idesc = ptx::instr_desc_f16(PAIR_M, BN, 1, 1, 0, 0);  // bf16 x bf16, both K-major
-      Pipe pipe;
+      Pipe<LRS> pipe;
       Pipe<ARES_B_STAGES> bp;
       uint8_t* bring = tiles + ARES_SLICES * A_STAGE_BYTES;
       uint32_t it = 0, uphase = 0;
@@ -607,7 +667,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               bp.advance();
             }
           } else {
-            mma_tile<1>(ctl, tiles, pipe, nk, d_tmem, idesc, 0, 0);
+            mma_tile<1, false, LRS>(ctl, tiles, pipe, nk, d_tmem, idesc, 0, 0);
           }
           if (ptx::elect_one()) ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
           __syncwarp();
@@ -619,7 +679,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int quad = warp & 3;
     const int chalf = ew >> 2;  // column half of the 256-wide tile
     const int r_in_tile = crank * BM + quad * 32 + lane;
-    uint8_t* tile = staging + ew * STAGING_BUFS * STAGING_TILE;
+    uint8_t* tile = staging + ew * EBUFS * (STAGING_TILE / 2);
     uint32_t it = 0, gslice = 0;
     // FWDE E-store pipeline state: one pending (written, not yet stored) 32 x 32 half slice
     bool epend = false;
@@ -629,12 +689,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (epend_rb < p.b && !(p.debug_flags & 1))  // bit0 ablation: skip the E stores
+        if (epend_rb < (epend_dir && SYM ? p.B : p.b) && !(p.debug_flags & 1))  // bit0 ablation: skip E stores
           ptx::tma_store_4d(&p.e_map[epend_dir], tile + epend_buf * (STAGING_TILE / 2), epend_cb & 127,
                             epend_rb & 127, epend_cb >> 7, epend_rb >> 7);
         ptx::bulk_commit();
       }
       epend = false;
+    };
+    // Stage one 32 x 32 half slice (written by `write` into a free staging half-buffer) as the new
+    // pending store at (column cb, row rb) of direction d's E; the previous pending one is issued.
+    auto e_push = [&](auto&& write, int cb, int rb, int d) {
+      e_flush();  // fence + store the pending half (its STS completed during this half's math)
+      uint8_t* hb = tile + ebuf * (STAGING_TILE / 2);
+      if (lane == 0) ptx::bulk_wait_read<EBUFS - 1>();  // this buffer's previous store has read smem
+      __syncwarp();
+      write(hb);
+      epend = true;
+      epend_buf = ebuf;
+      epend_cb = cb;
+      epend_rb = rb;
+      epend_dir = d;
+      ebuf = ebuf + 1 == EBUFS ? 0 : ebuf + 1;
     };
     for (int u = pair; u < num_units; u += npairs) {
       int dir, rt, ch, t0;
@@ -731,7 +806,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 va[i] = __uint_as_float(ra[i]);
                 vb[i] = __uint_as_float(rb[i]);
               }
-              if (j == 0) {  // slice 1's TMEM loads fly while slice 0 is computed
+              if (j == 0 && !SYM) {  // slice 1's TMEM loads fly while slice 0 is computed
                 ptx::tmem_ld32_async(taddr + 64, ra);
                 ptx::tmem_ld32_async(taddr + 96, rb);
               }
@@ -780,24 +855,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                   if (h[half * 16] == 0x7fff1234u) asm volatile("trap;");
                   continue;
                 }
-                e_flush();  // fence + store the pending half (its STS completed during this half's math)
-                uint8_t* hb = tile + ebuf * (STAGING_TILE / 2);
-                if (lane == 0) ptx::bulk_wait_read<1>();  // this buffer's previous store has read smem
-                __syncwarp();
-                ptx::st_swizzled_row64(hb, lane, h + half * 16);
-                epend = true;
-                epend_buf = ebuf;
-                epend_cb = col0 + j * 64 + half * 32;
-                epend_rb = rbase;
-                epend_dir = dir;
-                ebuf ^= 1;
+                const int hcb = col0 + j * 64 + half * 32;
+                e_push([&](uint8_t* hb) { ptx::st_swizzled_row64(hb, lane, h + half * 16); }, hcb, rbase, dir);
+                if constexpr (SYM) {
+                  // t2i half slice: rows hcb.. of S_1 = columns of this block, columns rbase.. .
+                  // m_1 = max over the 64-row group (this warp + partner warp ew ^ 1, same columns).
+                  float* xb = xbuf + ew * 64;
+                  const float* xo = xbuf + (ew ^ 1) * 64;
+                  const int pbar = 1 + (ew >> 1);
+                  xb[lane] = lane_scatter<true>(v, lane);
+                  ptx::named_bar_sync(pbar, 64);
+                  float e1[32];
+#pragma unroll
+                  for (int q = 0; q < 8; ++q) {
+                    const float4 a4 = reinterpret_cast<const float4*>(xb)[q];
+                    const float4 o4 = reinterpret_cast<const float4*>(xo)[q];
+                    e1[4 * q + 0] = ptx::ex2(fmaf(v[4 * q + 0], p.tl2e, -(fmaxf(a4.x, o4.x) * p.tl2e)));
+                    e1[4 * q + 1] = ptx::ex2(fmaf(v[4 * q + 1], p.tl2e, -(fmaxf(a4.y, o4.y) * p.tl2e)));
+                    e1[4 * q + 2] = ptx::ex2(fmaf(v[4 * q + 2], p.tl2e, -(fmaxf(a4.z, o4.z) * p.tl2e)));
+                    e1[4 * q + 3] = ptx::ex2(fmaf(v[4 * q + 3], p.tl2e, -(fmaxf(a4.w, o4.w) * p.tl2e)));
+                  }
+                  const float m1 = fmaxf(xb[lane], xo[lane]) * p.tl2e;  // column hcb + lane's offset
+                  uint32_t h1[16];
+#pragma unroll
+                  for (int k = 0; k < 16; ++k) {
+                    __half2 hh = __floats2half2_rn(e1[2 * k], e1[2 * k + 1]);
+                    h1[k] = *reinterpret_cast<uint32_t*>(&hh);
+                  }
+                  if (hcb == rbase) {  // warp-uniform: the diagonal (labels) is element (lane, lane)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) e1[i] = i == lane ? 0.f : e1[i];
+                  }
+                  const float cs = lane_scatter<false>(e1, lane);
+                  e_push([&](uint8_t* hb) { st_transposed_64(hb, lane, h1); }, rbase, hcb, 1);
+                  xb[32 + lane] = cs;
+                  ptx::named_bar_sync(pbar, 64);
+                  if (!(quad & 1)) {  // the group's lower warp: fixed order (rows 0-31) + (rows 32-63)
+                    const int64_t at = int64_t(rbase >> 6) * p.B + hcb + lane;
+                    p.mg[int64_t(p.groups) * p.b + at] = m1;
+                    p.ssum[at] = xb[32 + lane] + xo[32 + lane];
+                  }
+                }
               }
               const int cb = col0 + j * 64;
               const float mnew = fmaxf(m2, mg);
               l = l * ptx::ex2(m2 - mnew) + (s0 + s1) * ptx::ex2(mg - mnew);
               m2 = mnew;
               if (row_ok) p.mg[(int64_t(dir) * p.groups + cb / GROUP_COLS) * p.b + row] = mg;
-              if (j == 0) ptx::tmem_wait_ld_dep(ra, rb);
+              if (j == 0) {
+                if (SYM) {  // registers: SYM loads slice 1 only after slice 0 (168-register cap)
+                  ptx::tmem_ld32_async(taddr + 64, ra);
+                  ptx::tmem_ld32_async(taddr + 96, rb);
+                }
+                ptx::tmem_wait_ld_dep(ra, rb);
+              }
             }
           }
         } else {
@@ -870,7 +981,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
       if (KIND != KIND_GRAD && row_ok) {
         p.stats[((int64_t(dir) * p.nchunk + ch) * 2 + chalf) * p.b + row] = make_float2(m2, l);
-        if (has_t) p.target[dir * p.b + row] = yt;
+        if (has_t) {
+          p.target[dir * p.b + row] = yt;
+          if (SYM) p.target[p.b + row] = yt;  // S_1[r, r] = S_0[r, r]
+        }
       }
     }
     if (KIND == KIND_FWDE) e_flush();
@@ -1316,10 +1430,25 @@ __global__ void feat16_kernel(const uint4* feat, uint4* feat16, int64_t n, Statu
 //   lse2 (log2 domain), ce = -log softmax[label], glabel = P_label - 1 = -(sum_{j!=label} P_j).
 // ssub: stats sub-chunks per canonical chunk (the forward's units cover one sub-chunk); a chunk's
 // sum is the fixed tree over its (sub-chunk, column half) partials.
-__global__ void stats_combine_kernel(const float2* stats, const float* target, int nchunk, int ssub, int b,
+// Shared tail: (m, lo = sum of non-label terms relative to m, target yt) -> lse2, glabel, ce of row i.
+__device__ __forceinline__ void finish_row(int i, float m, float lo, float yt, float* lse2_out, float* glabel_out,
+                                           float* ce_out, Status* status) {
+  const float et = ptx::ex2(yt - m);
+  const float lall = lo + et;
+  const float lse2 = m + log2f(lall);
+  const float dlt = m - yt;  // >= 0
+  const float ce = dlt < 64.f ? log1pf(lo * exp2f(dlt)) : dlt * LN2 + logf(lall);
+  lse2_out[i] = lse2;
+  glabel_out[i] = -lo / lall;
+  ce_out[i] = ce;
+  if (!isfinite(ce) || !isfinite(lse2)) atomicOr(&status->flags, FLAG_LOSS_NONFINITE);
+}
+
+// ndir = 1: direction 0 only (the symmetric single-rank forward combines direction 1 separately).
+__global__ void stats_combine_kernel(const float2* stats, const float* target, int nchunk, int ssub, int b, int ndir,
                                      float* lse2_out, float* glabel_out, float* ce_out, Status* status) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 2 * b) return;
+  if (i >= ndir * b) return;
   const int dir = i / b, r = i % b;
   const int nsc = nchunk * ssub;
   auto at = [&](int sc, int h) { return stats[((int64_t(dir) * nsc + sc) * 2 + h) * b + r]; };
@@ -1342,17 +1471,27 @@ __global__ void stats_combine_kernel(const float2* stats, const float* target, i
     lo = 0.f;
     for (int c = 0; c < nchunk; ++c) lo += chunk_sum(c);
   }
-  const float yt = target[i];
-  const float et = ptx::ex2(yt - m);
-  const float lall = lo + et;
-  const float lse2 = m + log2f(lall);
-  const float dlt = m - yt;  // >= 0
-  const float ce = dlt < 64.f ? log1pf(lo * exp2f(dlt)) : dlt * LN2 + logf(lall);
-  lse2_out[i] = lse2;
-  glabel_out[i] = -lo / lall;
-  ce_out[i] = ce;
+  finish_row(i, m, lo, target[i], lse2_out, glabel_out, ce_out, status);
+}
 
-  if (!isfinite(ce) || !isfinite(lse2)) atomicOr(&status->flags, FLAG_LOSS_NONFINITE);
+// SYM (N = 1), direction 1: row c of S_1 is column c of S_0; the forward left one (max, sum) pair
+// per (64-row group, column) -- m_1 in the dir-1 half of m_g, the label-free sum in ssum.
+// Online combine in ascending group order (deterministic).
+__global__ void stats_sym_kernel(const float* mg1, const float* ssum, const float* target, int groups, int B,
+                                 float* lse2_out, float* glabel_out, float* ce_out, Status* status) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= B) return;
+  float m = -INFINITY, lo = 0.f;
+  for (int g = 0; g < groups; ++g) {
+    const float mg = mg1[int64_t(g) * B + c], sg = ssum[int64_t(g) * B + c];
+    if (mg > m) {
+      lo = lo * ptx::ex2(m - mg) + sg;
+      m = mg;
+    } else {
+      lo += sg * ptx::ex2(mg - m);
+    }
+  }
+  finish_row(B + c, m, lo, target[B + c], lse2_out, glabel_out, ce_out, status);
 }
 
 // E path: m_g [2][groups][b] (f32, log2 domain) -> sc [2][groups][b] = exp2(m_g - lse2[dir][r]) as f16,
@@ -1790,6 +1929,7 @@ struct Geometry {
   int wide;               // Dp % 512 == 0: GEMM units cover all of D (two accumulators, G read once)
   int ksplit;             // intra K split (fixed function of B, D): partials [2][ksplit][b][Dp]
   int estore;             // forward stores E + group offsets; backward GEMMs rescale E -> G (no recompute)
+  int sym;                // N = 1 + estore: one GEMM of S_0 feeds both directions (S_1 = S_0^T)
   int groups;             // B / 64 column groups (E offsets)
   int chunk_cols;         // B / nchunk
   int64_t off[DISCO_R_COUNT];
@@ -1851,6 +1991,12 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
     return e && atoi(e) != 0;
   }();
   g->estore = (g->g_blocked && !no_estore) ? 1 : 0;
+  // DISCO_SYMMETRIC=1 (read per call; experiment, off by default): the symmetric single-rank
+  // forward.  Correct (tools/sym_ab.py, test_symmetric_forward_vs_oracle) but measured slower: the
+  // t2i column statistics cost ~2x the i2t epilogue in issue slots and MUFU, more than the halved
+  // MMA saves.  Not bitwise equal to N > 1 (t2i sums in another order).
+  const char* sym_env = getenv("DISCO_SYMMETRIC");
+  g->sym = (world == 1 && g->estore && sym_env && atoi(sym_env) == 1) ? 1 : 0;
   g->groups = int(B / GROUP_COLS);
   const int64_t b = g->b, Dp = g->Dp, N = world;
   int64_t len[DISCO_R_COUNT];
@@ -1858,7 +2004,10 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   len[DISCO_R_GATHER] = N > 1 ? N * 2 * b * Dp * 2 : 0;
   len[DISCO_R_FEAT] = 2 * B * Dp * 2;
   len[DISCO_R_FEAT16] = 2 * B * Dp * 2;
-  len[DISCO_R_STATS] = 2 * int64_t(g->nchunk) * g->ssub * 2 * b * 8;
+  // + (N = 1, estore) the symmetric forward's dir-1 group sums [groups][B] f32 (allocated whether or
+  // not DISCO_SYMMETRIC selects the path, so the workspace size does not depend on it)
+  len[DISCO_R_STATS] = 2 * int64_t(g->nchunk) * g->ssub * 2 * b * 8 +
+                       (N == 1 && g->estore ? int64_t(g->groups) * B * 4 : 0);
   len[DISCO_R_ROWS] = 4 * 2 * b * 4;
   len[DISCO_R_CE] = 2 * b * 4;
   len[DISCO_R_CE_ALL] = N * 2 * b * 4;
@@ -2064,11 +2213,11 @@ int l2_window(cudaLaunchAttribute* attr, const void* base, size_t bytes) {
   return 1;
 }
 
-template <int KIND, bool ARES>
+template <int KIND, bool ARES, bool SYM = false>
 int launch_logits_t(const LogitsParams& p, int64_t units, cudaStream_t st, const void* feat = nullptr,
                     size_t feat_bytes = 0) {
   int rc;
-  if ((rc = prepare_kernel(logits_kernel<KIND, ARES>))) return rc;
+  if ((rc = prepare_kernel(logits_kernel<KIND, ARES, SYM>))) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid_for(units));
   cfg.blockDim = dim3(NUM_THREADS);
@@ -2077,7 +2226,7 @@ int launch_logits_t(const LogitsParams& p, int64_t units, cudaStream_t st, const
   cudaLaunchAttribute attr[1];
   cfg.attrs = attr;
   cfg.numAttrs = (feat && (debug_flag_bits() & 2)) ? l2_window(&attr[0], feat, feat_bytes) : 0;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, logits_kernel<KIND, ARES>, p));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, logits_kernel<KIND, ARES, SYM>, p));
   count_launch();
   return DISCO_OK;
 }
@@ -2113,6 +2262,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.g_blocked = g.g_blocked;
   p.mg = region<float>(ws, g, DISCO_R_SCALE);
   p.groups = g.groups;
+  p.ssum = reinterpret_cast<float*>(p.stats + 2 * int64_t(g.nchunk) * g.ssub * 2 * g.b);
   p.wave = wave;
   p.epoch = epoch;
   p.timeout_ns = (unsigned long long)(timeout_s * 1e9);
@@ -2133,18 +2283,21 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
     p.status_flags = &stt->flags;
     p.nwaves = wave == -2 ? g.nchunk * g.ssub : g.N;
   }
+  const bool sym = g.sym && kind == KIND_FWDE && wave != -3;
+  const int64_t ndir = sym ? 1 : 2;
   const int64_t units = wave == -3 ? int64_t(2) * p.row_tiles * p.nchunk
-                      : wave == -2 ? int64_t(2) * p.rt_per_chunk * p.nwaves * p.nwaves
-                      : wave >= 0 ? int64_t(2) * p.rt_per_chunk * (2 * wave + 1)
-                                  : int64_t(2) * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
+                      : wave == -2 ? ndir * p.rt_per_chunk * p.nwaves * p.nwaves
+                      : wave >= 0 ? ndir * p.rt_per_chunk * (2 * wave + 1)
+                                  : ndir * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
   const bool ares = g.Dp <= BK * ARES_SLICES && (debug_flags & 128) && wave > -2;  // experiment: not faster
   if (kind == KIND_FWD) {
     rc = ares ? launch_logits_t<KIND_FWD, true>(p, units, st) : launch_logits_t<KIND_FWD, false>(p, units, st);
     if (rc) return rc;
   } else if (kind == KIND_FWDE) {
     const size_t fb = size_t(2) * g.B * g.Dp * 2;
-    rc = ares ? launch_logits_t<KIND_FWDE, true>(p, units, st, feat, fb)
-              : launch_logits_t<KIND_FWDE, false>(p, units, st, feat, fb);
+    rc = sym    ? launch_logits_t<KIND_FWDE, false, true>(p, units, st, feat, fb)
+         : ares ? launch_logits_t<KIND_FWDE, true>(p, units, st, feat, fb)
+                : launch_logits_t<KIND_FWDE, false>(p, units, st, feat, fb);
     if (rc) return rc;
   } else {
     if ((rc = prepare_kernel(logits_kernel<KIND_GRAD, false>))) return rc;
@@ -2381,12 +2534,22 @@ int build_intra(GemmParams& p, int first, void* ws, const Geometry& g, int mt0 =
 // stats combine (+ E -> G factors): after every logits unit of the forward has run.
 int forward_finish(void* ws, const Geometry& g, cudaStream_t st) {
   float* rows = region<float>(ws, g, DISCO_R_ROWS);
-  const int n = int(2 * g.b);
-  stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(
-      region<float2>(ws, g, DISCO_R_STATS), rows, g.nchunk, g.ssub, int(g.b), rows + 2 * g.b, rows + 4 * g.b,
-      region<float>(ws, g, DISCO_R_CE), region<Status>(ws, g, DISCO_R_STATUS));
+  const int ndir = g.sym ? 1 : 2;
+  const int n = int(ndir * g.b);
+  float2* stats = region<float2>(ws, g, DISCO_R_STATS);
+  stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(stats, rows, g.nchunk, g.ssub, int(g.b), ndir,
+                                                        rows + 2 * g.b, rows + 4 * g.b, region<float>(ws, g, DISCO_R_CE),
+                                                        region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
   CUDA_TRY(cudaGetLastError());
+  if (g.sym) {
+    stats_sym_kernel<<<int((g.B + 255) / 256), 256, 0, st>>>(
+        region<float>(ws, g, DISCO_R_SCALE) + int64_t(g.groups) * g.b,
+        reinterpret_cast<float*>(stats + 2 * int64_t(g.nchunk) * g.ssub * 2 * g.b), rows, g.groups, int(g.B),
+        rows + 2 * g.b, rows + 4 * g.b, region<float>(ws, g, DISCO_R_CE), region<Status>(ws, g, DISCO_R_STATUS));
+    count_launch();
+    CUDA_TRY(cudaGetLastError());
+  }
   if (g.estore) {
     const int64_t nv = 2 * int64_t(g.groups) * g.b / 8;
     scale_kernel<<<elementwise_grid(nv, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_SCALE), rows + 2 * g.b,

@@ -287,3 +287,24 @@ def test_streamed_forward_missing_chunk_times_out():
     dh_i, dh_t, lh = P.disco_step(None, Ih, Th, 10.0)
     dd_i, dd_t, ld = P.disco_step(None, Ih.cuda(), Th.cuda(), 10.0)
     assert torch.equal(dh_i, dd_i.cpu()) and torch.equal(dh_t, dd_t.cpu()) and lh == ld
+
+
+@pytest.mark.parametrize("B,D", [(2048, 512), (8192, 256)])
+def test_symmetric_forward_vs_oracle(B, D, monkeypatch):
+    """DISCO_SYMMETRIC=1 (experiment, off by default): one GEMM of S_0 feeds both directions
+    (S_1 = S_0^T; t2i column statistics reduced across lanes in the epilogue).  Within the
+    contract tolerance of the f64 oracle and of the two-GEMM path, on the device path, the host
+    wavefront path (f32 host inputs) and the streamed path (pinned bf16 host inputs)."""
+    I, T = O.synthetic_features(B, D, 7)
+    bi, bt, bl = (x.cpu().numpy() if torch.is_tensor(x) else x for x in P.disco_step(None, dev(I), dev(T), 100.0))
+    monkeypatch.setenv("DISCO_SYMMETRIC", "1")
+    di, dt, loss = P.disco_step(None, dev(I), dev(T), 100.0)
+    di, dt = di.cpu().numpy(), dt.cpu().numpy()
+    assert max(errors(di, dt, loss, I, T, 100.0)) < TOL
+    assert O.max_rel_error(di, bi) < 1e-3 and O.max_rel_error(dt, bt) < 1e-3 and abs(loss - bl) / bl < 1e-6
+    hi, ht, hl = P.disco_step(None, I.astype(np.float32), T.astype(np.float32), 100.0)
+    assert np.array_equal(hi, di) and np.array_equal(ht, dt) and hl == loss
+    Ih = torch.from_numpy(I.astype(np.float32)).bfloat16().pin_memory()
+    Th = torch.from_numpy(T.astype(np.float32)).bfloat16().pin_memory()
+    si, stt, sl = P.disco_step(None, Ih, Th, 100.0)
+    assert torch.equal(si, torch.from_numpy(di)) and torch.equal(stt, torch.from_numpy(dt)) and sl == loss
