@@ -417,8 +417,11 @@ def run_ours(args):
         "logits_fwd": (phases["forward"], "tensor", mm, "TFLOP/s", sustained)}
     if recompute:
         kernels["logits_grad"] = (phases["backward_grad"], "hbm", g_bytes, "GB/s", hbm)
+    # fused single-rank backward (default at N = 1, wide D): one GEMM per gradient on H = G_0 + G_1^T
+    # executes 4*b*B*D flops for the reference's 8*b*B*D; the roofline uses the executed flops
+    hfuse = world == 1 and bool(_lib.path_info(B, D, world, 0) & _lib.PATH_HFUSE)
     if world == 1:
-        kernels["gemm_backward"] = (phases["backward"], "tensor", 2 * mm, "TFLOP/s", sustained)
+        kernels["gemm_backward"] = (phases["backward"], "tensor", (1 if hfuse else 2) * mm, "TFLOP/s", sustained)
     elif use_peer:
         kernels["gemm_backward_peer"] = (phases["backward_peer"], "tensor", 2 * mm, "TFLOP/s", sustained)
     else:
@@ -435,7 +438,12 @@ def run_ours(args):
     dom = max(table, key=lambda k: table[k]["ms"])
     # ncu DRAM bytes per launch were captured at the headline workload (B=32K, D=512, N=1)
     traffic = load_traffic().get(dom) if (B, D, world) == (B_GLOBAL, DIM, 1) else None
-    step_tflops = 12.0 * b * B * D / (ms / 1e3) / 1e12
+    if hfuse:
+        table["gemm_backward"]["algorithmic_tflops"] = 2 * mm / (phases["backward"] / 1e3) / 1e12
+        table["gemm_backward"]["note"] = ("fused single-rank backward: H = G_0 + G_1^T formed in shared memory, "
+                                          "4*b*B*D executed flops (the reference's algorithm: 8*b*B*D)")
+    step_tflops = 12.0 * b * B * D / (ms / 1e3) / 1e12            # algorithmic
+    step_exec_tflops = (8.0 if hfuse else 12.0) * b * B * D / (ms / 1e3) / 1e12
     d = table[dom]
 
     cpu = None
@@ -466,8 +474,9 @@ def run_ours(args):
         "roofline": {"bound": d["bound"], "kernel": dom, "achieved": d["achieved"], "peak": d["peak"],
                      "unit": d["unit"], "frac": d["frac"], "traffic": traffic,
                      "peak_kind": f"{src} ({'bf16 sustained' if d['unit'] == 'TFLOP/s' else 'HBM copy'})",
-                     "launch_ms": d["ms"], "step_tflops": step_tflops, "step_frac": step_tflops / sustained,
-                     "step_frac_of_burst": step_tflops / burst, "kernels": table},
+                     "launch_ms": d["ms"], "step_tflops_algorithmic": step_tflops,
+                     "step_tflops": step_exec_tflops, "step_frac": step_exec_tflops / sustained,
+                     "step_frac_of_burst": step_exec_tflops / burst, "kernels": table},
         "phases_ms": phases,
         "cpu_baseline": cpu,
         "e2e": e2e,

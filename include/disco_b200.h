@@ -128,6 +128,16 @@ int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, floa
  * host->device copy of host features overlaps the logits GEMMs.  Waves may run on different
  * streams (they write disjoint outputs); forward_finish must follow all of them. */
 int disco_b200_forward_waves(int64_t B, int64_t D, int world, int rank, int* waves);
+
+/* Which implementation this geometry takes (bit mask; DISCO_SYMMETRIC / DISCO_HFUSE read now):
+ * bit0 E stored by the forward (recompute-free backward), bit1 wide GEMM units (Dp % 512 == 0),
+ * bit2 fused single-rank backward (H = G_0 + G_1^T: one GEMM per gradient, 4*b*B*D backward
+ * flops instead of 8*b*B*D; E_1 stored transposed), bit3 symmetric single-rank forward. */
+#define DISCO_PATH_ESTORE 1
+#define DISCO_PATH_WIDE 2
+#define DISCO_PATH_HFUSE 4
+#define DISCO_PATH_SYM 8
+int disco_b200_path_info(int64_t B, int64_t D, int world, int rank, int* bits);
 int disco_b200_forward_wave(void* ws, int64_t B, int64_t D, int world, int rank, float t, int wave, void* stream);
 int disco_b200_forward_finish(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
 

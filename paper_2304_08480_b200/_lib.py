@@ -45,6 +45,7 @@ SIGNATURES = {
     "disco_b200_pack_rows": [_vp, _i64, _i64, _int, _int, _vp, _vp, _i64, _i64, _int, _int, _i64, _i64, _vp],
     "disco_b200_forward": [_vp, _i64, _i64, _int, _int, _f32, _vp],
     "disco_b200_forward_waves": [_i64, _i64, _int, _int, ctypes.POINTER(_int)],
+    "disco_b200_path_info": [_i64, _i64, _int, _int, ctypes.POINTER(_int)],
     "disco_b200_forward_wave": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp],
     "disco_b200_forward_streamed": [_vp, _i64, _i64, _int, _int, _f32, ctypes.c_uint32, ctypes.c_double, _vp],
     "disco_b200_h2d_streamed": [_vp, _i64, _i64, _int, _int, _vp, _vp, ctypes.c_uint32, _vp],
@@ -162,6 +163,16 @@ def forward_waves(B: int, D: int, world: int, rank: int) -> int:
     """Waves of the H2D-pipelined forward (0: shape not wavefront-capable)."""
     out = _int()
     call("disco_b200_forward_waves", B, D, world, rank, ctypes.byref(out))
+    return out.value
+
+
+PATH_ESTORE, PATH_WIDE, PATH_HFUSE, PATH_SYM = 1, 2, 4, 8
+
+
+def path_info(B: int, D: int, world: int, rank: int = 0) -> int:
+    """disco_b200_path_info bit mask (PATH_*): which kernels this geometry runs right now."""
+    out = _int()
+    call("disco_b200_path_info", B, D, world, rank, ctypes.byref(out))
     return out.value
 
 

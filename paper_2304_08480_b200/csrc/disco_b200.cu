@@ -60,14 +60,15 @@ constexpr int PAIR_M = 2 * BM;
 constexpr int A_STAGE_BYTES = BM * BK * 2;        // 16 KiB
 constexpr int B_STAGE_BYTES = (BN / 2) * BK * 2;  // 16 KiB (this CTA's half of one 256-column N tile)
 constexpr int TILE_RING_BYTES = 192 * 1024;      // operand ring: 6 x 32 KiB (NB=1) or 4 x 48 KiB (NB=2)
-// NB = number of 256-column N tiles per unit (2 = "wide": all 512 columns of D, two accumulators)
-template <int NB> struct Ring {
-  static constexpr int STAGE_BYTES = A_STAGE_BYTES + NB * B_STAGE_BYTES;
+// NB = number of 256-column N tiles per unit (2 = "wide": all 512 columns of D, two accumulators);
+// NA = A tiles per stage (2: the fused single-rank backward stages both directions' E tiles)
+template <int NB, int NA = 1> struct Ring {
+  static constexpr int STAGE_BYTES = NA * A_STAGE_BYTES + NB * B_STAGE_BYTES;
   static constexpr int STAGES = TILE_RING_BYTES / STAGE_BYTES;
 };
 constexpr int STAGES = Ring<1>::STAGES;  // max stage count (barrier arrays)
 constexpr int STAGE_BYTES = Ring<1>::STAGE_BYTES;
-static_assert(Ring<1>::STAGES == 6 && Ring<2>::STAGES == 4, "ring geometry");
+static_assert(Ring<1>::STAGES == 6 && Ring<2>::STAGES == 4 && Ring<2, 2>::STAGES == 3, "ring geometry");
 constexpr int NUM_THREADS = 320;  // warp0 TMA, warp1 MMA, warps2-9 epilogue
 constexpr int NUM_EPI_WARPS = 8;
 // E-operand GEMMs add 4 transform warps (10-13) that rescale each A stage in smem (E -> G).
@@ -150,6 +151,9 @@ struct LogitsParams {
   int groups;           // B / 64 (GROUP_COLS)
   // SYM (N = 1): dir-1 statistics per (64-row group of S_0, column): sum of E_1 without the label
   float* ssum;          // [groups][B]
+  // e1t (N = 1, fused backward): direction 1's E stored transposed, E_1^T[r][c] in the blocked layout
+  // of direction 0, so both directions' tiles of a (r, c) block share one shared-memory layout
+  int e1t;
   // wave >= 0 (single rank, H2D-pipelined forward): only the units whose row chunk or column
   // chunk is `wave` and the other index <= wave, i.e. the units that became computable when
   // (stats sub-)chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per (sub-)chunk.
@@ -196,6 +200,13 @@ struct GemmProblem {
   const float* xlabel;    // [xb] label-column value P_label - 1
   int xb;                 // local rows b (pitch of xscale)
   int lab_off;            // rank * b: global column of local row 0's positive pair
+  // fused single-rank backward (hfuse, N = 1): A2 = the other direction's E over the same
+  // (row, K) block, staged MN-major beside A; the transform warps write H = G_d + G_d'^T into A,
+  // so one GEMM H . C replaces intra (G_d . C) + cross (G_d'^T . C): half the MMA work
+  int hfuse;
+  CUtensorMap a2_map;     // blocked E of direction d' (MN-major loads)
+  const __half* xscale2;  // [groups][xb] E -> G factors of direction d'
+  const float* xlabel2;   // [xb] label values of direction d'
 };
 constexpr int MAX_PROBLEMS = 4;
 constexpr int MAX_SCHED_PAIRS = 80;
@@ -268,15 +279,15 @@ __device__ __forceinline__ uint8_t* smem_base(uint8_t* raw) {
 // warp-uniform (uniform registers), one elected lane issues the UMMAs and the commits.
 // Successive K=16 steps advance the descriptor start address by 32 B (K-major) or 2 KiB
 // (MN-major), i.e. by 2 or 128 in the descriptor's 16-byte units.
-template <int NB, bool XF = false, int RS = Ring<NB>::STAGES>
+template <int NB, bool XF = false, int RS = Ring<NB>::STAGES, int NA = 1>
 __device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>& pipe, int nk,
                                          uint32_t d_tmem, uint32_t idesc, int a_mn, int b_mn) {
   const uint64_t a_step = a_mn ? 128 : 2, b_step = b_mn ? 128 : 2;
   for (int kb = 0; kb < nk; ++kb) {
     ptx::mbar_wait(XF ? &ctl->xfull[pipe.stage] : &ctl->full[pipe.stage], pipe.phase);
     ptx::tc_fence_after();
-    const uint32_t a_base = ptx::smem_u32(tiles + pipe.stage * Ring<NB>::STAGE_BYTES);
-    const uint32_t b_base = a_base + A_STAGE_BYTES;
+    const uint32_t a_base = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES);
+    const uint32_t b_base = a_base + NA * A_STAGE_BYTES;
     const uint64_t ad0 = operand_desc(a_base, a_mn, 0);
     uint64_t bd0[NB];
 #pragma unroll
@@ -298,18 +309,18 @@ __device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>&
 // Producer side of one k-block: wait for the slot, arm the leader's barrier, load.
 // LOCAL (E-operand GEMMs): each CTA counts its own bytes on its own barrier, which its
 // transform warps wait on; otherwise the leader's barrier counts both CTAs' bytes.
-template <int NB, bool LOCAL = false, int RS = Ring<NB>::STAGES>
+template <int NB, bool LOCAL = false, int RS = Ring<NB>::STAGES, int NA = 1>
 __device__ __forceinline__ uint8_t* producer_acquire(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>& pipe,
                                                      bool leader, uint32_t& bar, uint32_t crank = 0) {
   ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
   if (LOCAL) {
-    ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], Ring<NB>::STAGE_BYTES);
+    ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], Ring<NB, NA>::STAGE_BYTES);
     bar = ptx::map_to_rank(&ctl->full[pipe.stage], crank);
   } else {
-    if (leader) ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], 2 * Ring<NB>::STAGE_BYTES);
+    if (leader) ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], 2 * Ring<NB, NA>::STAGE_BYTES);
     bar = ptx::map_to_rank(&ctl->full[pipe.stage], 0);
   }
-  return tiles + pipe.stage * Ring<NB>::STAGE_BYTES;
+  return tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES;
 }
 
 // E -> G on one 128-byte smem row (64 f16 of one G row i, G columns [j0, j0 + 64)) of a
@@ -327,6 +338,33 @@ __device__ __forceinline__ void xform_row(uint8_t* rowp, int sw, __half sc, int 
 #pragma unroll
     for (int k = 0; k < 4; ++k) h[k] = __hmul2(h[k], s2);
     *reinterpret_cast<uint4*>(rowp + ((c ^ sw) << 4)) = x[c];
+  }
+  if (unsigned(lab_rel) < 64u)
+    *reinterpret_cast<__half*>(rowp + ((((lab_rel >> 3) ^ sw)) << 4) + (lab_rel & 7) * 2) = __float2half_rn(glab);
+}
+
+// Fused single-rank backward (hfuse): one 128-byte row of H = G_0 + G_1^T (d_image, K-major) or of
+// H^T (d_text, MN-major).  E_1 is stored transposed (LogitsParams::e1t), so A and A2 hold the two
+// directions' E over the same (r, c) block in the same swizzled layout and H is elementwise:
+// H = E_0 * s0 + E_1^T * s1, where s0 is this row's scalar factor (direction 0: one per row and
+// 64-column group) and s1 the 64 factors of direction 1 along the row (one per column c, for the
+// row's 64-row group).  vec_a: the vector factors belong to tile A (d_text) instead of A2.
+// The diagonal element gets glab = (P_0 - 1) + (P_1 - 1).
+__device__ __forceinline__ void xform_row_h(uint8_t* rowp, const uint8_t* row2p, int sw, __half sc,
+                                            const uint4 (&s1)[8], bool vec_a, int lab_rel, float glab) {
+  const __half2 s2 = __half2half2(sc);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int off = (c ^ sw) << 4;
+    uint4 x = *reinterpret_cast<const uint4*>(rowp + off);
+    const uint4 y = *reinterpret_cast<const uint4*>(row2p + off);
+    __half2* h = reinterpret_cast<__half2*>(&x);
+    const __half2* h2 = reinterpret_cast<const __half2*>(&y);
+    const __half2* f = reinterpret_cast<const __half2*>(&s1[c]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      h[k] = vec_a ? __hfma2(h[k], f[k], __hmul2(h2[k], s2)) : __hfma2(h2[k], f[k], __hmul2(h[k], s2));
+    *reinterpret_cast<uint4*>(rowp + off) = x;
   }
   if (unsigned(lab_rel) < 64u)
     *reinterpret_cast<__half*>(rowp + ((((lab_rel >> 3) ^ sw)) << 4) + (lab_rel & 7) * 2) = __float2half_rn(glab);
@@ -689,7 +727,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (epend_rb < (epend_dir && SYM ? p.B : p.b) && !(p.debug_flags & 1))  // bit0 ablation: skip E stores
+        if (epend_rb < (epend_dir && (SYM || p.e1t) ? p.B : p.b) && !(p.debug_flags & 1))  // bit0: skip E stores
           ptx::tma_store_4d(&p.e_map[epend_dir], tile + epend_buf * (STAGING_TILE / 2), epend_cb & 127,
                             epend_rb & 127, epend_cb >> 7, epend_rb >> 7);
         ptx::bulk_commit();
@@ -856,7 +894,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                   continue;
                 }
                 const int hcb = col0 + j * 64 + half * 32;
-                e_push([&](uint8_t* hb) { ptx::st_swizzled_row64(hb, lane, h + half * 16); }, hcb, rbase, dir);
+                if (!SYM && dir == 1 && p.e1t)  // E_1^T: tile rows = this slice's 32 columns
+                  e_push([&](uint8_t* hb) { st_transposed_64(hb, lane, h + half * 16); }, rbase, hcb, 1);
+                else
+                  e_push([&](uint8_t* hb) { ptx::st_swizzled_row64(hb, lane, h + half * 16); }, hcb, rbase, dir);
                 if constexpr (SYM) {
                   // t2i half slice: rows hcb.. of S_1 = columns of this block, columns rbase.. .
                   // m_1 = max over the 64-row group (this warp + partner warp ew ^ 1, same columns).
@@ -1001,11 +1042,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 //   into the two TMEM buffers and summed in the epilogue ((c0 + c1): the first
 //   level of the fixed reduction tree).
 // =====================================================================
-template <int NB, bool XF>
+template <int NB, bool XF, bool HF = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF : NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ GemmParams p) {
-  constexpr int RS = Ring<NB>::STAGES;
+  constexpr int NA = HF ? 2 : 1;  // A tiles per stage
+  constexpr int RS = Ring<NB, NA>::STAGES;
   static_assert(NB == 1 || NB == 2, "one or two N tiles per unit");
+  static_assert(!HF || (XF && NB == 2), "the fused single-rank backward is a wide E-operand GEMM");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
   uint8_t* staging = tiles + TILE_RING_BYTES;
@@ -1019,6 +1062,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     for (int i = 0; i < p.nprob; ++i) {
       ptx::prefetch_tmap(&p.prob[i].a_map);
       ptx::prefetch_tmap(&p.prob[i].b_map);
+      if (HF) ptx::prefetch_tmap(&p.prob[i].a2_map);
       if (p.prob[i].tma_store && !p.prob[i].peer) ptx::prefetch_tmap(&p.prob[i].out_map);
       for (int r = 0; r < (p.prob[i].peer ? p.prob[i].M / p.prob[i].peer_b : 0); ++r)
         ptx::prefetch_tmap(&p.prob[i].peer_map[r]);
@@ -1070,7 +1114,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           k_range(q, kc * (1 + q.paired) + sub, k0, nk);
           for (int kb = 0; kb < nk; ++kb) {
             uint32_t bar;
-            uint8_t* st = producer_acquire<NB, XF, RS>(ctl, tiles, pipe, leader, bar, crank);
+            uint8_t* st = producer_acquire<NB, XF, RS, NA>(ctl, tiles, pipe, leader, bar, crank);
             const int k = k0 + kb * BK;
             if (q.a_blocked)
               load_blocked(&q.a_map, q.a_mn_major, st, bar, m0, k, BM, ptx::kEvictFirst);
@@ -1078,9 +1122,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
               load_operand(&q.a_map, 1, st, bar, m0, k + q.a_k_off, BM, ptx::kEvictFirst);
             else
               load_operand(&q.a_map, 0, st, bar, m0 + q.a_row_off, k, BM, ptx::kEvictFirst);
+            if (HF) load_blocked(&q.a2_map, q.a_mn_major, st + A_STAGE_BYTES, bar, m0, k, BM, ptx::kEvictFirst);
 #pragma unroll
             for (int j = 0; j < NB; ++j)
-              load_operand(&q.b_map, q.b_mn_major, st + A_STAGE_BYTES + j * B_STAGE_BYTES, bar, n0 + j * BN,
+              load_operand(&q.b_map, q.b_mn_major, st + NA * A_STAGE_BYTES + j * B_STAGE_BYTES, bar, n0 + j * BN,
                            k + q.b_k_off, BN / 2, ptx::kEvictLast);
             pipe.advance();
           }
@@ -1103,7 +1148,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           ptx::mbar_wait(&ctl->tempty[0], ((it >> 1) & 1) ^ 1);
           ptx::mbar_wait(&ctl->tempty[1], ((it >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
-          mma_tile<NB, XF, RS>(ctl, tiles, pipe, nk, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major);
+          mma_tile<NB, XF, RS, NA>(ctl, tiles, pipe, nk, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major);
           if (ptx::elect_one()) {
             ptx::umma_commit_pair(&ctl->tfull[0], 0x3);
             ptx::umma_commit_pair(&ctl->tfull[1], 0x3);
@@ -1149,7 +1194,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       };
       // rows past b (last pair tile when b / 128 is odd) were zero-filled by TMA: nothing to scale
       const bool active = q.xform && (q.a_mn_major || m0 + xt < q.xb);
-      const float glab_row = (active && !q.a_mn_major) ? q.xlabel[m0 + xt] : 0.f;
+      const float glab_row = (active && !q.a_mn_major) ? q.xlabel[m0 + xt] + (HF ? q.xlabel2[m0 + xt] : 0.f) : 0.f;
+      // HF: the 64 direction-1 factors along this thread's row, one 128-byte vector per stage, loaded
+      // one stage ahead (L2-prefetched XPF stages ahead).  K-major (d_image, row r = m0 + xt):
+      // s1[(r / 64) * b + k + j]; MN-major (d_text, K-row r = k + xt % 64, columns c = m0 + 64 (xt / 64) + j):
+      // s1[(k / 64) * b + c]
+      auto s1_at = [&](int k) -> const __half* {
+        return q.a_mn_major ? q.xscale2 + int64_t(k >> 6) * q.xb + m0 + ((xt >> 6) << 6)
+                            : q.xscale2 + int64_t((m0 + xt) >> 6) * q.xb + k;
+      };
+      uint4 s1v[2][8];  // double buffer, role fixed by the XPF-unrolled loop (kb parity)
       for (int sub = 0; sub <= q.paired; ++sub) {
         int k0, nk;
         k_range(q, kc * (1 + q.paired) + sub, k0, nk);
@@ -1159,9 +1213,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
         // wait on an in-flight load).
         constexpr int XPF = 4;
         auto ld_scale = [&](int kb) { return (active && kb < nk) ? q.xscale[sidx(k0 + kb * BK)] : __float2half(0.f); };
+        auto ld_s1 = [&](int kb, uint4 (&dst)[8]) {
+          if (!HF) return;
+          if (active && kb < nk) {
+            const uint4* v = reinterpret_cast<const uint4*>(s1_at(k0 + kb * BK));
+#pragma unroll
+            for (int c = 0; c < 8; ++c) dst[c] = v[c];
+          }
+          if (active && kb + XPF < nk) asm volatile("prefetch.global.L2 [%0];" ::"l"(s1_at(k0 + (kb + XPF) * BK)));
+        };
         __half sq[XPF];
 #pragma unroll
         for (int r = 0; r < XPF; ++r) sq[r] = ld_scale(r);
+        if (HF) {
+#pragma unroll
+          for (int r = 1; r < XPF; ++r)
+            if (active && r < nk) asm volatile("prefetch.global.L2 [%0];" ::"l"(s1_at(k0 + r * BK)));
+          ld_s1(0, s1v[0]);
+        }
         for (int kb0 = 0; kb0 < nk; kb0 += XPF) {
 #pragma unroll
           for (int r = 0; r < XPF; ++r) {
@@ -1170,9 +1239,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             const int k = k0 + kb * BK;
             const __half sc = sq[r];
             sq[r] = ld_scale(kb + XPF);
+            if (HF) ld_s1(kb + 1, s1v[(r + 1) & 1]);
             ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
-            if (active && !(q.ablate & 1024)) {
-              uint8_t* rowp = tiles + pipe.stage * Ring<NB>::STAGE_BYTES + rowoff;
+            if (HF && active && !(q.ablate & 1024)) {
+              uint8_t* rowp = tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES + rowoff;
+              int lab_rel;
+              float glab;
+              if (q.a_mn_major) {  // K-row r = k + xt % 64; its label column r
+                const int i = k + (xt & 63);
+                lab_rel = i - (m0 + (xt >> 6) * 64);
+                glab = unsigned(lab_rel) < 64u ? q.xlabel[i] + q.xlabel2[i] : 0.f;
+              } else {
+                lab_rel = m0 + xt - k;
+                glab = glab_row;
+              }
+              xform_row_h(rowp, rowp + A_STAGE_BYTES, sw, sc, s1v[r & 1], q.a_mn_major, lab_rel, glab);
+              ptx::fence_proxy_async_smem();
+            } else if (active && !(q.ablate & 1024)) {
+              uint8_t* rowp = tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES + rowoff;
               int lab_rel;
               float glab;
               if (q.a_mn_major) {  // row = G row i = k + xt % 64; label column lab_off + i
@@ -1600,11 +1684,13 @@ __global__ void combine_kernel(const float4* intra, int ksplit, const float4* re
         const float4 x = __ldcs(src + k * ls);
         return (flip && (k < own_lo || k >= own_hi)) ? f4neg(x) : x;
       });
-    } else {
+    } else if (N > 0) {
       cross = tree_sum(N, [&](int src) {
         const float4 x = recv[((int64_t(src) * 2 + g) * b) * v4 + rem];
         return (flip && src != rank) ? f4neg(x) : x;
       });
+    } else {  // N == 0: fused single-rank backward, the intra partials already hold the cross terms
+      cross = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const float4* ib = intra + (int64_t(g) * ksplit) * per_g + rem;  // intra K-split partials, fixed order
     const float4 yi = ksplit == 2 ? f4add(__ldcs(ib), __ldcs(ib + per_g)) : __ldcs(ib);
@@ -1645,8 +1731,10 @@ __global__ void contribution_kernel(const float4* intra, int ksplit, const float
     if (xpart) {
       const float4* src = xpart + ((int64_t(g) * B + c) * np) * v4 + vc;
       x = tree_sum(np, [&](int k) { return src[k * v4]; });
-    } else {
+    } else if (send) {
       x = send[((dest * 2 + g) * b + r) * v4 + vc];
+    } else {  // fused single-rank backward: no separate cross terms
+      x = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const bool own = dest == rank;
     if (own) {
@@ -1930,6 +2018,7 @@ struct Geometry {
   int ksplit;             // intra K split (fixed function of B, D): partials [2][ksplit][b][Dp]
   int estore;             // forward stores E + group offsets; backward GEMMs rescale E -> G (no recompute)
   int sym;                // N = 1 + estore: one GEMM of S_0 feeds both directions (S_1 = S_0^T)
+  int hfuse;              // N = 1, wide: backward GEMMs on H = G_d + G_d'^T (intra + cross in one)
   int groups;             // B / 64 column groups (E offsets)
   int chunk_cols;         // B / nchunk
   int64_t off[DISCO_R_COUNT];
@@ -1997,6 +2086,13 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   // MMA saves.  Not bitwise equal to N > 1 (t2i sums in another order).
   const char* sym_env = getenv("DISCO_SYMMETRIC");
   g->sym = (world == 1 && g->estore && sym_env && atoi(sym_env) == 1) ? 1 : 0;
+  // Fused single-rank backward (default; DISCO_HFUSE=0, read per call, selects the two-GEMM-pair
+  // backward that is bitwise identical to N > 1).  At N = 1 every cross term G_d'^T . C pairs with
+  // an intra term G_d . C over the same B x B block, so the transform warps form H = G_0 + G_1^T in
+  // shared memory and one GEMM per gradient replaces two (half the backward MMA work).  Forward and
+  // backward of one step must see the same setting (the forward stores E_1 transposed for it).
+  const char* hf_env = getenv("DISCO_HFUSE");
+  g->hfuse = (world == 1 && g->estore && g->wide && g->ksplit == 2 && !g->sym && !(hf_env && atoi(hf_env) == 0)) ? 1 : 0;
   g->groups = int(B / GROUP_COLS);
   const int64_t b = g->b, Dp = g->Dp, N = world;
   int64_t len[DISCO_R_COUNT];
@@ -2263,6 +2359,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.mg = region<float>(ws, g, DISCO_R_SCALE);
   p.groups = g.groups;
   p.ssum = reinterpret_cast<float*>(p.stats + 2 * int64_t(g.nchunk) * g.ssub * 2 * g.b);
+  p.e1t = g.hfuse;
   p.wave = wave;
   p.epoch = epoch;
   p.timeout_ns = (unsigned long long)(timeout_s * 1e9);
@@ -2319,11 +2416,11 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
 
 // wide = 1: every unit covers all N columns (n_tiles counts 512-column tiles), NB = 2 kernel.
 // xform = 1: A operands hold E (transform warps rescale to G in smem).
-template <int NB, bool XF>
+template <int NB, bool XF, bool HF = false>
 int launch_gemm_t(GemmParams& p, cudaStream_t st) {
   int rc;
-  if ((rc = prepare_kernel(gemm_kernel<NB, XF>))) return rc;
-  gemm_kernel<NB, XF><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS, SMEM_BYTES, st>>>(p);
+  if ((rc = prepare_kernel(gemm_kernel<NB, XF, HF>))) return rc;
+  gemm_kernel<NB, XF, HF><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS, SMEM_BYTES, st>>>(p);
   return DISCO_OK;
 }
 
@@ -2375,13 +2472,15 @@ void build_schedule(GemmParams& p, int npairs) {
   p.sched_n = n;
 }
 
-int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform) {
+int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform, int hfuse = 0) {
   p.units[0] = 0;
   for (int i = 0; i < p.nprob; ++i)
     p.units[i + 1] = p.units[i] + p.prob[i].m_tiles * p.prob[i].n_tiles * p.prob[i].k_chunks;
   if (!(debug_flag_bits() & 262144)) build_schedule(p, grid_for(p.units[p.nprob]) / 2);  // bit18: round-robin
   int rc;
-  if (wide)
+  if (hfuse)
+    rc = launch_gemm_t<2, true, true>(p, st);
+  else if (wide)
     rc = xform ? launch_gemm_t<2, true>(p, st) : launch_gemm_t<2, false>(p, st);
   else
     rc = xform ? launch_gemm_t<1, true>(p, st) : launch_gemm_t<1, false>(p, st);
@@ -2485,9 +2584,9 @@ int launch_combine(void* ws, const Geometry& g, float t, int flip, int row0, int
   if (n == 0) return DISCO_OK;
   combine_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
       region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float4>(ws, g, DISCO_R_RECV),
-      (g.N == 1 && g.np > 1) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, g.N, g.rank, int(g.b),
-      int(g.Dp), int(g.D), s, flip, d_image, d_text, ld_out, row0, nrows, region<Status>(ws, g, DISCO_R_STATUS), 0,
-      1 << 30, 1);
+      (g.N == 1 && g.np > 1 && !g.hfuse) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np,
+      g.hfuse ? 0 : g.N, g.rank, int(g.b), int(g.Dp), int(g.D), s, flip, d_image, d_text, ld_out, row0, nrows,
+      region<Status>(ws, g, DISCO_R_STATUS), 0, 1 << 30, 1);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
@@ -2528,6 +2627,38 @@ int build_intra(GemmParams& p, int first, void* ws, const Geometry& g, int mt0 =
                          1, g.b * g.Dp, g.ksplit)))
       return rc;
   }
+  return DISCO_OK;
+}
+
+// Fused single-rank backward (g.hfuse): two GEMMs on H = G_0 + G_1^T, whose tiles the transform
+// warps build from E_0 and E_1^T (stored transposed by the forward, LogitsParams::e1t):
+//   d_image rows r: H . T_g, A = E_0 K-major, A2 = E_1^T K-major (the intra problem of direction 0)
+//   d_text  rows c: H^T . I_g, A = E_1^T MN-major, A2 = E_0 MN-major
+// K = all B in ksplit halves (the intra partials); no cross terms.  Scalar factors: direction 0
+// (xscale, indexed as the problem's major-ness requires); vector factors: direction 1 (xscale2).
+int build_hfuse(GemmParams& p, void* ws, const Geometry& g, int mt0 = 0, int mt1 = -1) {
+  int rc;
+  if ((rc = build_intra(p, 0, ws, g, mt0, mt1))) return rc;
+  const __half* G = region<__half>(ws, g, DISCO_R_G);
+  const __half* E0 = G;
+  const __half* E1t = G + g.b * g.B;
+  const __half* sc16 = reinterpret_cast<const __half*>(scale16(ws, g));
+  const float* labels = region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b;
+  for (int gi = 0; gi < 2; ++gi) {
+    GemmProblem& q = p.prob[gi];
+    if (gi == 1) {  // rows c of d_text: both E tiles MN-major
+      if ((rc = make_map_blocked(&q.a_map, E1t, g.b, g.B, 64))) return rc;
+      q.a_mn_major = 1;
+    }
+    if ((rc = make_map_blocked(&q.a2_map, gi == 0 ? E1t : E0, g.b, g.B, gi == 0 ? BM : 64))) return rc;
+    q.hfuse = 1;
+    q.xscale = sc16;                       // direction 0 (scalar per row / K-row)
+    q.xscale2 = sc16 + int64_t(g.groups) * g.b;  // direction 1 (vector along the row)
+    q.xlabel = labels;
+    q.xlabel2 = labels + g.b;
+  }
+  p.nprob = 2;
+  p.split = 0;
   return DISCO_OK;
 }
 
@@ -2758,6 +2889,15 @@ int disco_b200_forward_waves(int64_t B, int64_t D, int world, int rank, int* wav
   return DISCO_OK;
 }
 
+int disco_b200_path_info(int64_t B, int64_t D, int world, int rank, int* bits) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  *bits = (g.estore ? DISCO_PATH_ESTORE : 0) | (g.wide ? DISCO_PATH_WIDE : 0) | (g.hfuse ? DISCO_PATH_HFUSE : 0) |
+          (g.sym ? DISCO_PATH_SYM : 0);
+  return DISCO_OK;
+}
+
 int disco_b200_forward_wave(void* ws, int64_t B, int64_t D, int world, int rank, float t, int wave, void* stream) {
   Geometry g;
   int rc = make_geometry(B, D, world, rank, &g);
@@ -2851,6 +2991,7 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (g.hfuse) return DISCO_OK;  // fused single-rank backward: disco_b200_backward_intra covers both terms
   GemmParams p;
   memset(&p, 0, sizeof(p));
   if ((rc = build_cross(p, 0, ws, g))) return rc;
@@ -2865,6 +3006,10 @@ int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int ran
   if (rc) return rc;
   GemmParams p;
   memset(&p, 0, sizeof(p));
+  if (g.hfuse) {
+    if ((rc = build_hfuse(p, ws, g))) return rc;
+    return launch_gemm(p, st_of(stream), 1, 1, 1);
+  }
   if ((rc = build_intra(p, 0, ws, g))) return rc;
   p.nprob = 2;
   return launch_gemm(p, st_of(stream), g.wide, g.estore);
@@ -2877,6 +3022,10 @@ int disco_b200_backward_fused(void* ws, int64_t B, int64_t D, int world, int ran
   cudaStream_t st = st_of(stream);
   GemmParams p;
   memset(&p, 0, sizeof(p));
+  if (g.hfuse) {
+    if ((rc = build_hfuse(p, ws, g))) return rc;
+    return launch_gemm(p, st, 1, 1, 1);
+  }
   if ((rc = build_intra(p, 0, ws, g))) return rc;  // list A: long units (K = B / ksplit)
   if ((rc = build_cross(p, 2, ws, g))) return rc;  // list B: one canonical chunk of K per unit
   p.nprob = 4;
@@ -2918,6 +3067,10 @@ int disco_b200_backward_rows(void* ws, int64_t B, int64_t D, int world, int rank
   const int mt0 = int(row0 / PAIR_M), mt1 = int((row1 + PAIR_M - 1) / PAIR_M);
   GemmParams p;
   memset(&p, 0, sizeof(p));
+  if (g.hfuse) {
+    if ((rc = build_hfuse(p, ws, g, mt0, mt1))) return rc;
+    return launch_gemm(p, st_of(stream), 1, 1, 1);
+  }
   if ((rc = build_intra(p, 0, ws, g, mt0, mt1))) return rc;
   if ((rc = build_cross(p, 2, ws, g, mt0, mt1))) return rc;
   p.nprob = 4;
@@ -2935,8 +3088,8 @@ int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank,
   const float s = float(0.5 * double(t) / double(g.b));
   const int64_t n = 2 * g.B * (g.Dp / 4);
   contribution_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
-      region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float4>(ws, g, DISCO_R_SEND),
-      (world == 1 && g.np > 1) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, world, rank, int(g.b),
+      region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, g.hfuse ? nullptr : region<float4>(ws, g, DISCO_R_SEND),
+      (world == 1 && g.np > 1 && !g.hfuse) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, world, rank, int(g.b),
       int(g.Dp), int(D), s, flip && world > 1, d_image_full, d_text_full, ld_out, region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
   CUDA_TRY(cudaGetLastError());

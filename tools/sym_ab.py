@@ -1,7 +1,7 @@
-"""Symmetric single-rank forward (DISCO_SYMMETRIC=1, an experiment, off by default) against the
-two-GEMM forward.
+"""Single-rank path switches A/B: an environment switch (default DISCO_SYMMETRIC, the symmetric
+forward; DISCO_HFUSE, the fused backward) at 1 against 0.
 
-  python tools/sym_ab.py [--sizes 2048x512 8192x512 32768x512 16384x1024] [--reps 10]
+  python tools/sym_ab.py [--var DISCO_SYMMETRIC] [--sizes 2048x512 8192x512 32768x512 16384x1024] [--reps 10]
 
 For each size: both paths on the same device inputs, their normwise difference, the symmetric
 path against the f64 oracle on sampled rows, and the device step time of each (CUDA events,
@@ -25,13 +25,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--sizes", nargs="+", default=["2048x512", "8192x512", "32768x512", "16384x1024"])
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--t", type=float, default=100.0)
+ap.add_argument("--var", default="DISCO_SYMMETRIC")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
 
 def run(I, T, sym, reps):
-    os.environ["DISCO_SYMMETRIC"] = "1" if sym else "0"
+    os.environ[a.var] = "1" if sym else "0"
     clear_plans()
     out = P.disco_step(None, I, T, a.t)
     torch.cuda.synchronize()
@@ -69,5 +70,5 @@ for sz in a.sizes:
          "bitwise_d_image": bool(np.array_equal(di0, di1)), "bitwise_d_text": bool(np.array_equal(dt0, dt1))}
     res[sz] = r
     print(sz, json.dumps(r), flush=True)
-    os.environ.pop("DISCO_SYMMETRIC", None)
+    os.environ.pop(a.var, None)
 print(json.dumps(res))
