@@ -151,9 +151,6 @@ struct LogitsParams {
   int groups;           // B / 64 (GROUP_COLS)
   // SYM (N = 1): dir-1 statistics per (64-row group of S_0, column): sum of E_1 without the label
   float* ssum;          // [groups][B]
-  // e1t (N = 1, fused backward): direction 1's E stored transposed, E_1^T[r][c] in the blocked layout
-  // of direction 0, so both directions' tiles of a (r, c) block share one shared-memory layout
-  int e1t;
   // wave >= 0 (single rank, H2D-pipelined forward): only the units whose row chunk or column
   // chunk is `wave` and the other index <= wave, i.e. the units that became computable when
   // (stats sub-)chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per (sub-)chunk.
@@ -338,33 +335,6 @@ __device__ __forceinline__ void xform_row(uint8_t* rowp, int sw, __half sc, int 
 #pragma unroll
     for (int k = 0; k < 4; ++k) h[k] = __hmul2(h[k], s2);
     *reinterpret_cast<uint4*>(rowp + ((c ^ sw) << 4)) = x[c];
-  }
-  if (unsigned(lab_rel) < 64u)
-    *reinterpret_cast<__half*>(rowp + ((((lab_rel >> 3) ^ sw)) << 4) + (lab_rel & 7) * 2) = __float2half_rn(glab);
-}
-
-// Fused single-rank backward (hfuse): one 128-byte row of H = G_0 + G_1^T (d_image, K-major) or of
-// H^T (d_text, MN-major).  E_1 is stored transposed (LogitsParams::e1t), so A and A2 hold the two
-// directions' E over the same (r, c) block in the same swizzled layout and H is elementwise:
-// H = E_0 * s0 + E_1^T * s1, where s0 is this row's scalar factor (direction 0: one per row and
-// 64-column group) and s1 the 64 factors of direction 1 along the row (one per column c, for the
-// row's 64-row group).  vec_a: the vector factors belong to tile A (d_text) instead of A2.
-// The diagonal element gets glab = (P_0 - 1) + (P_1 - 1).
-__device__ __forceinline__ void xform_row_h(uint8_t* rowp, const uint8_t* row2p, int sw, __half sc,
-                                            const uint4 (&s1)[8], bool vec_a, int lab_rel, float glab) {
-  const __half2 s2 = __half2half2(sc);
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int off = (c ^ sw) << 4;
-    uint4 x = *reinterpret_cast<const uint4*>(rowp + off);
-    const uint4 y = *reinterpret_cast<const uint4*>(row2p + off);
-    __half2* h = reinterpret_cast<__half2*>(&x);
-    const __half2* h2 = reinterpret_cast<const __half2*>(&y);
-    const __half2* f = reinterpret_cast<const __half2*>(&s1[c]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      h[k] = vec_a ? __hfma2(h[k], f[k], __hmul2(h2[k], s2)) : __hfma2(h2[k], f[k], __hmul2(h[k], s2));
-    *reinterpret_cast<uint4*>(rowp + off) = x;
   }
   if (unsigned(lab_rel) < 64u)
     *reinterpret_cast<__half*>(rowp + ((((lab_rel >> 3) ^ sw)) << 4) + (lab_rel & 7) * 2) = __float2half_rn(glab);
@@ -727,7 +697,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (epend_rb < (epend_dir && (SYM || p.e1t) ? p.B : p.b) && !(p.debug_flags & 1))  // bit0: skip E stores
+        if (epend_rb < (epend_dir && SYM ? p.B : p.b) && !(p.debug_flags & 1))  // bit0 ablation: skip E stores
           ptx::tma_store_4d(&p.e_map[epend_dir], tile + epend_buf * (STAGING_TILE / 2), epend_cb & 127,
                             epend_rb & 127, epend_cb >> 7, epend_rb >> 7);
         ptx::bulk_commit();
@@ -894,10 +864,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                   continue;
                 }
                 const int hcb = col0 + j * 64 + half * 32;
-                if (!SYM && dir == 1 && p.e1t)  // E_1^T: tile rows = this slice's 32 columns
-                  e_push([&](uint8_t* hb) { st_transposed_64(hb, lane, h + half * 16); }, rbase, hcb, 1);
-                else
-                  e_push([&](uint8_t* hb) { ptx::st_swizzled_row64(hb, lane, h + half * 16); }, hcb, rbase, dir);
+                e_push([&](uint8_t* hb) { ptx::st_swizzled_row64(hb, lane, h + half * 16); }, hcb, rbase, dir);
                 if constexpr (SYM) {
                   // t2i half slice: rows hcb.. of S_1 = columns of this block, columns rbase.. .
                   // m_1 = max over the 64-row group (this warp + partner warp ew ^ 1, same columns).
@@ -1122,7 +1089,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
               load_operand(&q.a_map, 1, st, bar, m0, k + q.a_k_off, BM, ptx::kEvictFirst);
             else
               load_operand(&q.a_map, 0, st, bar, m0 + q.a_row_off, k, BM, ptx::kEvictFirst);
-            if (HF) load_blocked(&q.a2_map, q.a_mn_major, st + A_STAGE_BYTES, bar, m0, k, BM, ptx::kEvictFirst);
+            if (HF) load_blocked(&q.a2_map, 1, st + A_STAGE_BYTES, bar, m0, k, BM, ptx::kEvictFirst);
 #pragma unroll
             for (int j = 0; j < NB; ++j)
               load_operand(&q.b_map, q.b_mn_major, st + NA * A_STAGE_BYTES + j * B_STAGE_BYTES, bar, n0 + j * BN,
@@ -1170,6 +1137,111 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
         }
       }
     }
+  } else if (XF && HF && warp >= 2 + NUM_EPI_WARPS) {  // ---------- transform warps 10..13 (fused)
+    // Fused single-rank backward: the stage holds A = E_d (K-major, rows = output rows) and A2 =
+    // E_d' over the same block (MN-major: K-rows = E_d' rows).  Warp xw builds rows
+    // [32 xw, 32 xw + 32) of H = G_d + G_d'^T in place of A as 8 blocks of 16 x 16: ldmatrix.x4
+    // fragments of E_d, ldmatrix.x4.trans fragments of E_d' (the transpose lands in the same
+    // fragment positions), H = E_d * s (row factor) + E_d'^T * s' (column factor), stmatrix.x4.
+    // Lane 8j + i addresses row i of matrix j (j & 1: rows +8, j >> 1: columns +8); thread t holds
+    // (row t / 4 (+8), columns 2 (t % 4) + {0, 1} (+8)).
+    const int xw = (threadIdx.x - 32 * (2 + NUM_EPI_WARPS)) >> 5;
+    const int mj = lane >> 3, mi = lane & 7;
+    const int tr = lane >> 2, tc = 2 * (lane & 3);
+    Pipe<RS> pipe;
+    for (int uk = 0; uk < my_units; ++uk) {
+      const int u = unit_at(uk);
+      int pi, mt, nt, kc;
+      decode(u, pi, mt, nt, kc);
+      const GemmProblem& q = p.prob[pi];
+      const int m0 = mt * PAIR_M + crank * BM;
+      const int wr0 = m0 + 32 * xw;  // first output row of this warp
+      const __half* s1base = q.xscale2 + int64_t(wr0 >> 6) * q.xb;  // E_d' factors of the rows' 64-group
+      float glab[4];  // label values of this thread's 4 rows (16 rb + 8 h + t / 4)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = wr0 + 16 * (j >> 1) + 8 * (j & 1) + tr;
+        glab[j] = q.xlabel[r] + q.xlabel2[r];
+      }
+      int k0, nk;
+      k_range(q, kc, k0, nk);
+      // per-stage factors, loaded one stage ahead into a double buffer whose role is fixed by the
+      // stage parity (XPF-unrolled loop); L2 prefetches run XPF stages ahead
+      constexpr int XPF = 4;
+      __half s0v[2][4];
+      uint32_t s1v[2][8];
+      auto ld_scales = [&](int kb, __half (&s0)[4], uint32_t (&s1)[8]) {
+        if (kb >= nk) return;
+        const int k = k0 + kb * BK;
+        const __half* s0p = q.xscale + int64_t(k >> 6) * q.xb + wr0 + tr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s0[j] = s0p[16 * (j >> 1) + 8 * (j & 1)];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) s1[c] = *reinterpret_cast<const uint32_t*>(s1base + k + 8 * c + tc);
+        if (lane == 0 && kb + XPF < nk) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(q.xscale + int64_t((k >> 6) + XPF) * q.xb + wr0));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(s1base + k + XPF * BK));
+        }
+      };
+      if (lane == 0)
+        for (int r = 1; r < XPF && r < nk; ++r) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(q.xscale + int64_t(((k0 + r * BK) >> 6)) * q.xb + wr0));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(s1base + k0 + r * BK));
+        }
+      ld_scales(0, s0v[0], s1v[0]);
+      for (int kb0 = 0; kb0 < nk; kb0 += XPF) {
+#pragma unroll
+        for (int r = 0; r < XPF; ++r) {
+          const int kb = kb0 + r;
+          if (kb >= nk) break;
+          const int k = k0 + kb * BK;
+          ld_scales(kb + 1, s0v[(r + 1) & 1], s1v[(r + 1) & 1]);
+          ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
+          if (!(q.ablate & 1024)) {
+            const uint32_t abase = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES);
+            const uint32_t a2base = abase + A_STAGE_BYTES;
+            // labels: global column lab_off + row; this stage holds columns [k, k + 64)
+            const int dl = q.lab_off + wr0 - k;  // label column of the warp's row 0, stage-relative
+            const bool diag = dl > -32 && dl < 64;
+#pragma unroll
+            for (int rb = 0; rb < 2; ++rb) {
+#pragma unroll
+              for (int cb = 0; cb < 4; ++cb) {
+                const int row = 32 * xw + 16 * rb + 8 * (mj & 1) + mi;  // A-tile row this lane addresses
+                const int ch = 2 * cb + (mj >> 1);                       // its 16-byte chunk (8 columns)
+                const uint32_t aaddr = abase + row * 128 + ((ch ^ (row & 7)) << 4);
+                const int R = 32 * xw + 16 * rb + 8 * (mj & 1);          // matrix's first row
+                const int c = 8 * ch + mi;                               // A2 K-row (E_d' row) addressed
+                const uint32_t baddr = a2base + (R >> 6) * 8192 + c * 128 + ((((R & 63) >> 3) ^ (c & 7)) << 4);
+                uint32_t e0[4], e1[4], hv[4];
+                ptx::ldmatrix_x4(e0, aaddr);
+                ptx::ldmatrix_x4_trans(e1, baddr);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const __half2 sr = __half2half2(s0v[r & 1][2 * rb + (j & 1)]);
+                  const __half2 sc = *reinterpret_cast<const __half2*>(&s1v[r & 1][2 * cb + (j >> 1)]);
+                  __half2 h = __hfma2(*reinterpret_cast<const __half2*>(&e1[j]), sc,
+                                      __hmul2(*reinterpret_cast<const __half2*>(&e0[j]), sr));
+                  if (diag) {  // warp-uniform; element (row, col) is a label iff col == dl + row
+                    const int rr = 16 * rb + 8 * (j & 1) + tr;            // warp-relative row
+                    const int cc = 16 * cb + 8 * (j >> 1) + tc;           // stage-relative column
+                    const __half gl = __float2half_rn(glab[2 * rb + (j & 1)]);
+                    if (cc == dl + rr) h.x = gl;
+                    if (cc + 1 == dl + rr) h.y = gl;
+                  }
+                  hv[j] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                ptx::stmatrix_x4(aaddr, hv);
+              }
+            }
+            ptx::fence_proxy_async_smem();
+          }
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(ptx::map_to_rank(&ctl->xfull[pipe.stage], 0));
+          pipe.advance();
+        }
+      }
+    }
   } else if (XF && warp >= 2 + NUM_EPI_WARPS) {  // ---------------- transform warps 10..13
     // Thread xt owns one 128-byte row of this CTA's A stage:
     //   K-major A (intra, G rows = M): row xt = G row m0 + xt, G columns [k, k + 64);
@@ -1194,16 +1266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       };
       // rows past b (last pair tile when b / 128 is odd) were zero-filled by TMA: nothing to scale
       const bool active = q.xform && (q.a_mn_major || m0 + xt < q.xb);
-      const float glab_row = (active && !q.a_mn_major) ? q.xlabel[m0 + xt] + (HF ? q.xlabel2[m0 + xt] : 0.f) : 0.f;
-      // HF: the 64 direction-1 factors along this thread's row, one 128-byte vector per stage, loaded
-      // one stage ahead (L2-prefetched XPF stages ahead).  K-major (d_image, row r = m0 + xt):
-      // s1[(r / 64) * b + k + j]; MN-major (d_text, K-row r = k + xt % 64, columns c = m0 + 64 (xt / 64) + j):
-      // s1[(k / 64) * b + c]
-      auto s1_at = [&](int k) -> const __half* {
-        return q.a_mn_major ? q.xscale2 + int64_t(k >> 6) * q.xb + m0 + ((xt >> 6) << 6)
-                            : q.xscale2 + int64_t((m0 + xt) >> 6) * q.xb + k;
-      };
-      uint4 s1v[2][8];  // double buffer, role fixed by the XPF-unrolled loop (kb parity)
+      const float glab_row = (active && !q.a_mn_major) ? q.xlabel[m0 + xt] : 0.f;
       for (int sub = 0; sub <= q.paired; ++sub) {
         int k0, nk;
         k_range(q, kc * (1 + q.paired) + sub, k0, nk);
@@ -1213,24 +1276,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
         // wait on an in-flight load).
         constexpr int XPF = 4;
         auto ld_scale = [&](int kb) { return (active && kb < nk) ? q.xscale[sidx(k0 + kb * BK)] : __float2half(0.f); };
-        auto ld_s1 = [&](int kb, uint4 (&dst)[8]) {
-          if (!HF) return;
-          if (active && kb < nk) {
-            const uint4* v = reinterpret_cast<const uint4*>(s1_at(k0 + kb * BK));
-#pragma unroll
-            for (int c = 0; c < 8; ++c) dst[c] = v[c];
-          }
-          if (active && kb + XPF < nk) asm volatile("prefetch.global.L2 [%0];" ::"l"(s1_at(k0 + (kb + XPF) * BK)));
-        };
         __half sq[XPF];
 #pragma unroll
         for (int r = 0; r < XPF; ++r) sq[r] = ld_scale(r);
-        if (HF) {
-#pragma unroll
-          for (int r = 1; r < XPF; ++r)
-            if (active && r < nk) asm volatile("prefetch.global.L2 [%0];" ::"l"(s1_at(k0 + r * BK)));
-          ld_s1(0, s1v[0]);
-        }
         for (int kb0 = 0; kb0 < nk; kb0 += XPF) {
 #pragma unroll
           for (int r = 0; r < XPF; ++r) {
@@ -1239,23 +1287,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             const int k = k0 + kb * BK;
             const __half sc = sq[r];
             sq[r] = ld_scale(kb + XPF);
-            if (HF) ld_s1(kb + 1, s1v[(r + 1) & 1]);
             ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
-            if (HF && active && !(q.ablate & 1024)) {
-              uint8_t* rowp = tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES + rowoff;
-              int lab_rel;
-              float glab;
-              if (q.a_mn_major) {  // K-row r = k + xt % 64; its label column r
-                const int i = k + (xt & 63);
-                lab_rel = i - (m0 + (xt >> 6) * 64);
-                glab = unsigned(lab_rel) < 64u ? q.xlabel[i] + q.xlabel2[i] : 0.f;
-              } else {
-                lab_rel = m0 + xt - k;
-                glab = glab_row;
-              }
-              xform_row_h(rowp, rowp + A_STAGE_BYTES, sw, sc, s1v[r & 1], q.a_mn_major, lab_rel, glab);
-              ptx::fence_proxy_async_smem();
-            } else if (active && !(q.ablate & 1024)) {
+            if (active && !(q.ablate & 1024)) {
               uint8_t* rowp = tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES + rowoff;
               int lab_rel;
               float glab;
@@ -2359,7 +2392,6 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.mg = region<float>(ws, g, DISCO_R_SCALE);
   p.groups = g.groups;
   p.ssum = reinterpret_cast<float*>(p.stats + 2 * int64_t(g.nchunk) * g.ssub * 2 * g.b);
-  p.e1t = g.hfuse;
   p.wave = wave;
   p.epoch = epoch;
   p.timeout_ns = (unsigned long long)(timeout_s * 1e9);
@@ -2630,32 +2662,26 @@ int build_intra(GemmParams& p, int first, void* ws, const Geometry& g, int mt0 =
   return DISCO_OK;
 }
 
-// Fused single-rank backward (g.hfuse): two GEMMs on H = G_0 + G_1^T, whose tiles the transform
-// warps build from E_0 and E_1^T (stored transposed by the forward, LogitsParams::e1t):
-//   d_image rows r: H . T_g, A = E_0 K-major, A2 = E_1^T K-major (the intra problem of direction 0)
-//   d_text  rows c: H^T . I_g, A = E_1^T MN-major, A2 = E_0 MN-major
-// K = all B in ksplit halves (the intra partials); no cross terms.  Scalar factors: direction 0
-// (xscale, indexed as the problem's major-ness requires); vector factors: direction 1 (xscale2).
+// Fused single-rank backward (g.hfuse): two GEMMs, one per gradient, on H_d = G_d + G_d'^T:
+//   d_image rows r: H_0 . T_g, A = E_0 (K-major), A2 = E_1 (MN-major: its K-rows are E_1 rows)
+//   d_text  rows c: H_1 . I_g, A = E_1 (K-major), A2 = E_0 (MN-major)
+// i.e. the intra problems with the other direction's E as a second A operand; the transform
+// warps form H_d tile by tile (ldmatrix / ldmatrix.trans / stmatrix).  K = all B in ksplit halves
+// (the intra partials); no cross terms.  Factors: xscale = direction d (one per row and K-group),
+// xscale2 = direction d' (one per K column for the rows' 64-group).
 int build_hfuse(GemmParams& p, void* ws, const Geometry& g, int mt0 = 0, int mt1 = -1) {
   int rc;
   if ((rc = build_intra(p, 0, ws, g, mt0, mt1))) return rc;
   const __half* G = region<__half>(ws, g, DISCO_R_G);
-  const __half* E0 = G;
-  const __half* E1t = G + g.b * g.B;
   const __half* sc16 = reinterpret_cast<const __half*>(scale16(ws, g));
   const float* labels = region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b;
   for (int gi = 0; gi < 2; ++gi) {
     GemmProblem& q = p.prob[gi];
-    if (gi == 1) {  // rows c of d_text: both E tiles MN-major
-      if ((rc = make_map_blocked(&q.a_map, E1t, g.b, g.B, 64))) return rc;
-      q.a_mn_major = 1;
-    }
-    if ((rc = make_map_blocked(&q.a2_map, gi == 0 ? E1t : E0, g.b, g.B, gi == 0 ? BM : 64))) return rc;
+    const int d2 = 1 - gi;
+    if ((rc = make_map_blocked(&q.a2_map, G + int64_t(d2) * g.b * g.B, g.b, g.B, 64))) return rc;
     q.hfuse = 1;
-    q.xscale = sc16;                       // direction 0 (scalar per row / K-row)
-    q.xscale2 = sc16 + int64_t(g.groups) * g.b;  // direction 1 (vector along the row)
-    q.xlabel = labels;
-    q.xlabel2 = labels + g.b;
+    q.xscale2 = sc16 + int64_t(d2) * g.groups * g.b;
+    q.xlabel2 = labels + int64_t(d2) * g.b;
   }
   p.nprob = 2;
   p.split = 0;
