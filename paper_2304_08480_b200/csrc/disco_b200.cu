@@ -99,6 +99,12 @@ constexpr int ARES_SLICES = 8;
 constexpr int ARES_B_STAGES = 4;
 static_assert(ARES_SLICES * A_STAGE_BYTES + ARES_B_STAGES * B_STAGE_BYTES == TILE_RING_BYTES, "A-resident layout");
 static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory limit");
+// Fused single-rank backward: per ring stage, the stage's E -> G factors land by bulk copy beside
+// the tiles (after the control block): 128 row factors of direction d (256 B) + the direction-d'
+// factor vectors of the CTA's two 64-row groups (2 x 128 B).
+constexpr int HF_SCALE_BYTES = 512;
+constexpr size_t SMEM_BYTES_HF = SMEM_BYTES + 3 * HF_SCALE_BYTES;
+static_assert(SMEM_BYTES_HF <= 232448, "fused backward smem");
 static_assert(sizeof(uint64_t) * 46 + 4 <= 512, "control block");
 
 // -------------------------------------------------------- status flag bits
@@ -308,10 +314,11 @@ __device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>&
 // transform warps wait on; otherwise the leader's barrier counts both CTAs' bytes.
 template <int NB, bool LOCAL = false, int RS = Ring<NB>::STAGES, int NA = 1>
 __device__ __forceinline__ uint8_t* producer_acquire(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>& pipe,
-                                                     bool leader, uint32_t& bar, uint32_t crank = 0) {
+                                                     bool leader, uint32_t& bar, uint32_t crank = 0,
+                                                     uint32_t extra_bytes = 0) {
   ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
   if (LOCAL) {
-    ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], Ring<NB, NA>::STAGE_BYTES);
+    ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], Ring<NB, NA>::STAGE_BYTES + extra_bytes);
     bar = ptx::map_to_rank(&ctl->full[pipe.stage], crank);
   } else {
     if (leader) ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], 2 * Ring<NB, NA>::STAGE_BYTES);
@@ -1020,6 +1027,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
   uint8_t* tiles = smem_base(smem_raw);
   uint8_t* staging = tiles + TILE_RING_BYTES;
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + TILE_RING_BYTES + STAGING_BYTES);
+  uint8_t* hf_scales = reinterpret_cast<uint8_t*>(ctl) + 512;  // HF: [RS][HF_SCALE_BYTES]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int crank = int(ptx::cluster_ctarank());
   const bool leader = crank == 0;
@@ -1081,7 +1089,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           k_range(q, kc * (1 + q.paired) + sub, k0, nk);
           for (int kb = 0; kb < nk; ++kb) {
             uint32_t bar;
-            uint8_t* st = producer_acquire<NB, XF, RS, NA>(ctl, tiles, pipe, leader, bar, crank);
+            uint8_t* st = producer_acquire<NB, XF, RS, NA>(ctl, tiles, pipe, leader, bar, crank,
+                                                           HF ? HF_SCALE_BYTES : 0);
             const int k = k0 + kb * BK;
             if (q.a_blocked)
               load_blocked(&q.a_map, q.a_mn_major, st, bar, m0, k, BM, ptx::kEvictFirst);
@@ -1089,7 +1098,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
               load_operand(&q.a_map, 1, st, bar, m0, k + q.a_k_off, BM, ptx::kEvictFirst);
             else
               load_operand(&q.a_map, 0, st, bar, m0 + q.a_row_off, k, BM, ptx::kEvictFirst);
-            if (HF) load_blocked(&q.a2_map, 1, st + A_STAGE_BYTES, bar, m0, k, BM, ptx::kEvictFirst);
+            if (HF) {
+              load_blocked(&q.a2_map, 1, st + A_STAGE_BYTES, bar, m0, k, BM, ptx::kEvictFirst);
+              // the stage's factors: direction d rows [m0, m0 + 128) at K-group k / 64, and the
+              // direction-d' vectors (columns [k, k + 64)) of the two 64-row groups
+              const uint32_t sd = ptx::smem_u32(hf_scales + pipe.stage * HF_SCALE_BYTES);
+              ptx::bulk_g2s(sd, q.xscale + int64_t(k >> 6) * q.xb + m0, 256, bar);
+              ptx::bulk_g2s(sd + 256, q.xscale2 + int64_t(m0 >> 6) * q.xb + k, 128, bar);
+              ptx::bulk_g2s(sd + 384, q.xscale2 + int64_t((m0 >> 6) + 1) * q.xb + k, 128, bar);
+            }
 #pragma unroll
             for (int j = 0; j < NB; ++j)
               load_operand(&q.b_map, q.b_mn_major, st + NA * A_STAGE_BYTES + j * B_STAGE_BYTES, bar, n0 + j * BN,
@@ -1156,7 +1173,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       const GemmProblem& q = p.prob[pi];
       const int m0 = mt * PAIR_M + crank * BM;
       const int wr0 = m0 + 32 * xw;  // first output row of this warp
-      const __half* s1base = q.xscale2 + int64_t(wr0 >> 6) * q.xb;  // E_d' factors of the rows' 64-group
       float glab[4];  // label values of this thread's 4 rows (16 rb + 8 h + t / 4)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -1165,81 +1181,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       }
       int k0, nk;
       k_range(q, kc, k0, nk);
-      // per-stage factors, loaded one stage ahead into a double buffer whose role is fixed by the
-      // stage parity (XPF-unrolled loop); L2 prefetches run XPF stages ahead
-      constexpr int XPF = 4;
-      __half s0v[2][4];
-      uint32_t s1v[2][8];
-      auto ld_scales = [&](int kb, __half (&s0)[4], uint32_t (&s1)[8]) {
-        if (kb >= nk) return;
+      for (int kb = 0; kb < nk; ++kb) {
         const int k = k0 + kb * BK;
-        const __half* s0p = q.xscale + int64_t(k >> 6) * q.xb + wr0 + tr;
+        ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
+        if (!(q.ablate & 1024)) {
+          const uint32_t abase = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES);
+          const uint32_t a2base = abase + A_STAGE_BYTES;
+          // the stage's factors (bulk-copied by the producer with the tiles)
+          const uint8_t* sd = hf_scales + pipe.stage * HF_SCALE_BYTES;
+          __half s0[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) s0[j] = s0p[16 * (j >> 1) + 8 * (j & 1)];
+          for (int j = 0; j < 4; ++j)
+            s0[j] = reinterpret_cast<const __half*>(sd)[32 * xw + 16 * (j >> 1) + 8 * (j & 1) + tr];
+          uint32_t s1[8];
+          const uint32_t* s1p = reinterpret_cast<const uint32_t*>(sd + 256 + (xw >> 1) * 128 + tc * 2);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) s1[c] = *reinterpret_cast<const uint32_t*>(s1base + k + 8 * c + tc);
-        if (lane == 0 && kb + XPF < nk) {
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(q.xscale + int64_t((k >> 6) + XPF) * q.xb + wr0));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(s1base + k + XPF * BK));
-        }
-      };
-      if (lane == 0)
-        for (int r = 1; r < XPF && r < nk; ++r) {
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(q.xscale + int64_t(((k0 + r * BK) >> 6)) * q.xb + wr0));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(s1base + k0 + r * BK));
-        }
-      ld_scales(0, s0v[0], s1v[0]);
-      for (int kb0 = 0; kb0 < nk; kb0 += XPF) {
+          for (int c = 0; c < 8; ++c) s1[c] = s1p[4 * c];
+          // labels: global column lab_off + row; this stage holds columns [k, k + 64)
+          const int dl = q.lab_off + wr0 - k;  // label column of the warp's row 0, stage-relative
+          const bool diag = dl > -32 && dl < 64;
 #pragma unroll
-        for (int r = 0; r < XPF; ++r) {
-          const int kb = kb0 + r;
-          if (kb >= nk) break;
-          const int k = k0 + kb * BK;
-          ld_scales(kb + 1, s0v[(r + 1) & 1], s1v[(r + 1) & 1]);
-          ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
-          if (!(q.ablate & 1024)) {
-            const uint32_t abase = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES);
-            const uint32_t a2base = abase + A_STAGE_BYTES;
-            // labels: global column lab_off + row; this stage holds columns [k, k + 64)
-            const int dl = q.lab_off + wr0 - k;  // label column of the warp's row 0, stage-relative
-            const bool diag = dl > -32 && dl < 64;
+          for (int rb = 0; rb < 2; ++rb) {
 #pragma unroll
-            for (int rb = 0; rb < 2; ++rb) {
+            for (int cb = 0; cb < 4; ++cb) {
+              const int row = 32 * xw + 16 * rb + 8 * (mj & 1) + mi;  // A-tile row this lane addresses
+              const int ch = 2 * cb + (mj >> 1);                       // its 16-byte chunk (8 columns)
+              const uint32_t aaddr = abase + row * 128 + ((ch ^ (row & 7)) << 4);
+              const int R = 32 * xw + 16 * rb + 8 * (mj & 1);          // matrix's first row
+              const int c = 8 * ch + mi;                               // A2 K-row (E_d' row) addressed
+              const uint32_t baddr = a2base + (R >> 6) * 8192 + c * 128 + ((((R & 63) >> 3) ^ (c & 7)) << 4);
+              uint32_t e0[4], e1[4], hv[4];
+              ptx::ldmatrix_x4(e0, aaddr);
+              ptx::ldmatrix_x4_trans(e1, baddr);
 #pragma unroll
-              for (int cb = 0; cb < 4; ++cb) {
-                const int row = 32 * xw + 16 * rb + 8 * (mj & 1) + mi;  // A-tile row this lane addresses
-                const int ch = 2 * cb + (mj >> 1);                       // its 16-byte chunk (8 columns)
-                const uint32_t aaddr = abase + row * 128 + ((ch ^ (row & 7)) << 4);
-                const int R = 32 * xw + 16 * rb + 8 * (mj & 1);          // matrix's first row
-                const int c = 8 * ch + mi;                               // A2 K-row (E_d' row) addressed
-                const uint32_t baddr = a2base + (R >> 6) * 8192 + c * 128 + ((((R & 63) >> 3) ^ (c & 7)) << 4);
-                uint32_t e0[4], e1[4], hv[4];
-                ptx::ldmatrix_x4(e0, aaddr);
-                ptx::ldmatrix_x4_trans(e1, baddr);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  const __half2 sr = __half2half2(s0v[r & 1][2 * rb + (j & 1)]);
-                  const __half2 sc = *reinterpret_cast<const __half2*>(&s1v[r & 1][2 * cb + (j >> 1)]);
-                  __half2 h = __hfma2(*reinterpret_cast<const __half2*>(&e1[j]), sc,
-                                      __hmul2(*reinterpret_cast<const __half2*>(&e0[j]), sr));
-                  if (diag) {  // warp-uniform; element (row, col) is a label iff col == dl + row
-                    const int rr = 16 * rb + 8 * (j & 1) + tr;            // warp-relative row
-                    const int cc = 16 * cb + 8 * (j >> 1) + tc;           // stage-relative column
-                    const __half gl = __float2half_rn(glab[2 * rb + (j & 1)]);
-                    if (cc == dl + rr) h.x = gl;
-                    if (cc + 1 == dl + rr) h.y = gl;
-                  }
-                  hv[j] = *reinterpret_cast<uint32_t*>(&h);
+              for (int j = 0; j < 4; ++j) {
+                const __half2 sr = __half2half2(s0[2 * rb + (j & 1)]);
+                const __half2 sc = *reinterpret_cast<const __half2*>(&s1[2 * cb + (j >> 1)]);
+                __half2 h = __hfma2(*reinterpret_cast<const __half2*>(&e1[j]), sc,
+                                    __hmul2(*reinterpret_cast<const __half2*>(&e0[j]), sr));
+                if (diag) {  // warp-uniform; element (row, col) is a label iff col == dl + row
+                  const int rr = 16 * rb + 8 * (j & 1) + tr;            // warp-relative row
+                  const int cc = 16 * cb + 8 * (j >> 1) + tc;           // stage-relative column
+                  const __half gl = __float2half_rn(glab[2 * rb + (j & 1)]);
+                  if (cc == dl + rr) h.x = gl;
+                  if (cc + 1 == dl + rr) h.y = gl;
                 }
-                ptx::stmatrix_x4(aaddr, hv);
+                hv[j] = *reinterpret_cast<uint32_t*>(&h);
               }
+              ptx::stmatrix_x4(aaddr, hv);
             }
-            ptx::fence_proxy_async_smem();
           }
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive_cluster(ptx::map_to_rank(&ctl->xfull[pipe.stage], 0));
-          pipe.advance();
+          ptx::fence_proxy_async_smem();
         }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(ptx::map_to_rank(&ctl->xfull[pipe.stage], 0));
+        pipe.advance();
       }
     }
   } else if (XF && warp >= 2 + NUM_EPI_WARPS) {  // ---------------- transform warps 10..13
@@ -2314,9 +2310,9 @@ int sm_count() {
 }
 
 template <typename K>
-int prepare_kernel(K kernel) {
+int prepare_kernel(K kernel, size_t smem = SMEM_BYTES) {
   // Per-device attribute; cheap enough to set on every launch.
-  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   return DISCO_OK;
 }
 
@@ -2451,8 +2447,9 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
 template <int NB, bool XF, bool HF = false>
 int launch_gemm_t(GemmParams& p, cudaStream_t st) {
   int rc;
-  if ((rc = prepare_kernel(gemm_kernel<NB, XF, HF>))) return rc;
-  gemm_kernel<NB, XF, HF><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS, SMEM_BYTES, st>>>(p);
+  if ((rc = prepare_kernel(gemm_kernel<NB, XF, HF>, HF ? SMEM_BYTES_HF : SMEM_BYTES))) return rc;
+  gemm_kernel<NB, XF, HF><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS,
+                            HF ? SMEM_BYTES_HF : SMEM_BYTES, st>>>(p);
   return DISCO_OK;
 }
 
