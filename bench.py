@@ -438,6 +438,8 @@ def run_ours(args):
     dom = max(table, key=lambda k: table[k]["ms"])
     # ncu DRAM bytes per launch were captured at the headline workload (B=32K, D=512, N=1)
     traffic = load_traffic().get(dom) if (B, D, world) == (B_GLOBAL, DIM, 1) else None
+    if world == 1 and not recompute:  # the backward streams both E blocks twice (d_image and d_text GEMMs)
+        table["gemm_backward"]["e_read_gbs"] = 2 * g_bytes / (phases["backward"] / 1e3) / 1e9
     if hfuse:
         table["gemm_backward"]["algorithmic_tflops"] = 2 * mm / (phases["backward"] / 1e3) / 1e12
         table["gemm_backward"]["note"] = ("fused single-rank backward: H = G_0 + G_1^T formed in shared memory, "
