@@ -178,7 +178,14 @@ int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int ran
 /* Backward parts 2 + 3 in one persistent launch (single rank, where no slab
  * exchange has to overlap the intra GEMM): the intra and cross units are
  * interleaved in proportion to their counts.  Same outputs as
- * disco_b200_backward_cross followed by disco_b200_backward_intra. */
+ * disco_b200_backward_cross followed by disco_b200_backward_intra.
+ *
+ * Fused single-rank backward (DISCO_PATH_HFUSE, disco_b200_path_info; default at N = 1 for
+ * Dp % 512 == 0 and B >= 4096, off with DISCO_HFUSE=0): every cross term pairs with an intra
+ * term over the same block, so backward_fused / backward_rows / backward_intra run one GEMM per
+ * gradient on H = G_d + G_d'^T (formed in shared memory) into DISCO_R_INTRA, backward_cross is a
+ * no-op, and combine / combine_rows / contribution read no cross partials.  Within 1e-3 of the
+ * f64 oracle like every path, but not bitwise equal to N > 1 (one more f16 rounding). */
 int disco_b200_backward_fused(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
 
 /* Owner combine after the slab exchange (replaces all_reduce(AVG) +
