@@ -147,6 +147,7 @@ class Plan:
         self.h2d_epoch = 0
         self.status_host = torch.empty(24, dtype=torch.uint8, pin_memory=True)
         self.waves = _lib.forward_waves(B, D, world, rank)
+        self.pairs = torch.cuda.get_device_properties(device).multi_processor_count // 2  # persistent CTA pairs
         self._copy_stream = None
         self._gather_stream = None
         self._h2d_stream = None
@@ -399,6 +400,18 @@ def _account_loss_scope(loss_counters, exchange_counters, b, B, D) -> None:
 ROW_BLOCK_FRACTIONS = (0.25, 0.1953125, 0.15625, 0.125, 0.09375, 0.078125, 0.0625, 0.0390625)
 
 
+def fused_row_blocks(b: int, pairs: int, units_per_tile: int = 4):
+    """Row blocks for the fused single-rank backward (disco_b200_path_info PATH_HFUSE): its units
+    are long (a K half of all B columns) and only ``units_per_tile`` per 256-row tile, so every
+    block is one whole wave of the ``pairs`` CTA pairs.  A wave's gradients (~19 MB at D = 512)
+    are produced faster than PCIe drains them, so the device->host copy never waits after the
+    first block: the step is bounded by the copy (tools/e2e_timeline.py)."""
+    tiles = (b + 255) // 256
+    w1 = max(1, pairs // units_per_tile)  # tiles per wave
+    cuts = list(range(0, tiles, w1)) + [tiles]
+    return [(min(256 * lo, b), min(256 * hi, b)) for lo, hi in zip(cuts, cuts[1:])]
+
+
 def row_blocks(b: int, fractions=None):
     """Output row blocks of the single-rank pipelined backward (fractions of the 256-row tiles,
     ROW_BLOCK_FRACTIONS by default; one block for small b)."""
@@ -566,7 +579,9 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         cs = plan.copy_stream()
         cur = torch.cuda.current_stream(device)
         h_image, h_text = host_out
-        for r0, r1 in row_blocks(b):
+        blocks = (fused_row_blocks(b, plan.pairs) if _lib.path_info(B, D, N, n) & _lib.PATH_HFUSE
+                  else row_blocks(b))
+        for r0, r1 in blocks:
             _lib.call("disco_b200_backward_rows", *plan.args, r0, r1, st)
             _lib.call("disco_b200_combine_rows", *plan.args, t, flip, r0, r1,
                       d_image.data_ptr(), d_text.data_ptr(), D, st)

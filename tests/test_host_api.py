@@ -92,3 +92,16 @@ def test_row_blocks_partition_rows():
         assert all(hi > lo for lo, hi in bl)
         assert all(bl[i][1] == bl[i + 1][0] for i in range(len(bl) - 1))
         assert all(lo % 256 == 0 for lo, _ in bl)
+
+
+def test_fused_row_blocks_whole_waves():
+    """Fused single-rank backward row blocks: one wave of 74 CTA pairs (4 units per 256-row tile)
+    each; a partition of [0, b) on 256-row boundaries."""
+    from paper_2304_08480_b200.shard import fused_row_blocks
+    bl = fused_row_blocks(32768, 74)
+    assert [(hi - lo) // 256 for lo, hi in bl] == [18] * 7 + [2]
+    for b in (4096, 8192, 16384, 32768, 65536, 12288):
+        bl = fused_row_blocks(b, 74)
+        assert bl[0][0] == 0 and bl[-1][1] == b
+        assert all(lo < hi and lo % 256 == 0 for lo, hi in bl)
+        assert all(bl[i][1] == bl[i + 1][0] for i in range(len(bl) - 1))
