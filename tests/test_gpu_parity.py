@@ -317,7 +317,7 @@ def test_symmetric_forward_vs_oracle(B, D, monkeypatch):
     assert torch.equal(si, torch.from_numpy(di)) and torch.equal(stt, torch.from_numpy(dt)) and sl == loss
 
 
-@pytest.mark.parametrize("B,D", [(4096, 512), (8192, 1024)])
+@pytest.mark.parametrize("B,D", [(4096, 512), (8192, 1024), (5120, 500), (4096, 1000)])
 def test_fused_backward_vs_oracle(B, D, monkeypatch):
     """Default single-rank backward (wide D, B >= 4096): one GEMM per gradient on
     H = G_0 + G_1^T built in shared memory from E_0 and the transposed E_1.  Within the contract
