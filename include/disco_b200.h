@@ -180,8 +180,8 @@ int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int ran
  * interleaved in proportion to their counts.  Same outputs as
  * disco_b200_backward_cross followed by disco_b200_backward_intra.
  *
- * Fused single-rank backward (DISCO_PATH_HFUSE, disco_b200_path_info; default at N = 1 for
- * Dp % 512 == 0 and B >= 4096, off with DISCO_HFUSE=0): every cross term pairs with an intra
+ * Fused single-rank backward (DISCO_PATH_HFUSE, disco_b200_path_info; opt-in with DISCO_HFUSE=1,
+ * at N = 1 for Dp % 512 == 0 and B >= 4096): every cross term pairs with an intra
  * term over the same block, so backward_fused / backward_rows / backward_intra run one GEMM per
  * gradient on H = G_d + G_d'^T (formed in shared memory) into DISCO_R_INTRA, backward_cross is a
  * no-op, and combine / combine_rows / contribution read no cross partials.  Within 1e-3 of the

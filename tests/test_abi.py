@@ -126,20 +126,20 @@ def test_wavefront_forward_availability():
 
 
 def test_path_info_reports_the_fused_single_rank_backward(monkeypatch):
-    """Geometry only (no GPU): the fused single-rank backward is the default for wide canonical
-    shapes at N = 1, never at N > 1 or narrow D, and DISCO_HFUSE=0 (read per call) switches it off."""
+    """Geometry only (no GPU): the fused single-rank backward is opt-in (DISCO_HFUSE=1, read per
+    call) -- the default keeps N = 1 bit-for-bit equal to N > 1 -- and applies only to wide
+    canonical shapes at N = 1."""
     from paper_2304_08480_b200 import _lib
     monkeypatch.delenv("DISCO_HFUSE", raising=False)
     monkeypatch.delenv("DISCO_SYMMETRIC", raising=False)
     bits = _lib.path_info(32768, 512, 1)
-    assert bits & _lib.PATH_ESTORE and bits & _lib.PATH_WIDE and bits & _lib.PATH_HFUSE
+    assert bits & _lib.PATH_ESTORE and bits & _lib.PATH_WIDE and not bits & _lib.PATH_HFUSE
+    monkeypatch.setenv("DISCO_HFUSE", "1")
+    assert _lib.path_info(32768, 512, 1) & _lib.PATH_HFUSE
     assert not _lib.path_info(32768, 512, 2) & _lib.PATH_HFUSE
     assert not _lib.path_info(65536, 768, 1) & _lib.PATH_HFUSE          # D = 768: not wide
     assert not _lib.path_info(2048, 512, 1) & _lib.PATH_HFUSE           # B < 4096: no K split
     assert _lib.path_info(16384, 1024, 1) & _lib.PATH_HFUSE             # config E
-    monkeypatch.setenv("DISCO_HFUSE", "0")
-    assert not _lib.path_info(32768, 512, 1) & _lib.PATH_HFUSE
-    monkeypatch.delenv("DISCO_HFUSE")
     monkeypatch.setenv("DISCO_SYMMETRIC", "1")  # the symmetric forward excludes it
     bits = _lib.path_info(32768, 512, 1)
     assert bits & _lib.PATH_SYM and not bits & _lib.PATH_HFUSE

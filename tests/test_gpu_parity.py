@@ -95,8 +95,8 @@ def test_single_gpu_vs_oracle(B, D):
 
 
 def test_bitwise_identical_across_world_sizes(monkeypatch):
-    """N-invariance of the canonical two-GEMM-pair path; at N = 1 the default fused backward
-    (H = G_0 + G_1^T, test_fused_backward_*) rounds differently, so it is switched off here."""
+    """N-invariance of the default (two-GEMM-pair) path; the opt-in fused single-rank backward
+    (DISCO_HFUSE=1, test_fused_backward_*) rounds differently, so it is pinned off here."""
     monkeypatch.setenv("DISCO_HFUSE", "0")
     B, D, t = 8192, 512, 100.0
     I, T = O.synthetic_features(B, D, 2)
@@ -254,8 +254,8 @@ def test_host_pipelined_nonfinite_in_late_chunk():
 
 def test_config_e_bitwise_and_sampled_oracle(release_plans, monkeypatch):
     """BASELINE config E (B=16384, D=1024: the non-distributed CLIP loss on one GPU): the
-    two-GEMM-pair path at N=1 equals N=8 simulated ranks bit for bit; it and the default fused
-    backward match the f64 oracle on sampled rows within 1e-3."""
+    default path at N=1 equals N=8 simulated ranks bit for bit; it and the opt-in fused backward
+    match the f64 oracle on sampled rows within 1e-3."""
     B, D, t = 16384, 1024, 100.0
     I, T = O.synthetic_features(B, D, 12)
     d8 = run_sim(I, T, 8, t)
@@ -319,15 +319,16 @@ def test_symmetric_forward_vs_oracle(B, D, monkeypatch):
 
 @pytest.mark.parametrize("B,D", [(4096, 512), (8192, 1024), (5120, 500), (4096, 1000)])
 def test_fused_backward_vs_oracle(B, D, monkeypatch):
-    """Default single-rank backward (wide D, B >= 4096): one GEMM per gradient on
-    H = G_0 + G_1^T built in shared memory from E_0 and the transposed E_1.  Within the contract
-    tolerance of the f64 oracle and of the two-GEMM-pair path; the host row-block path and the
-    contribution path (local_loss_and_grads) give the same bytes; repeat runs are bitwise equal."""
+    """Opt-in fused single-rank backward (DISCO_HFUSE=1; wide D, B >= 4096): one GEMM per
+    gradient on H = G_0 + G_1^T built in shared memory from E_0 and E_1 (ldmatrix / .trans).
+    Within the contract tolerance of the f64 oracle and of the default (N-invariant) path; the
+    host row-block path and the contribution path (local_loss_and_grads) give the same bytes;
+    repeat runs are bitwise equal."""
     I, T = O.synthetic_features(B, D, 21)
-    monkeypatch.setenv("DISCO_HFUSE", "0")
+    monkeypatch.delenv("DISCO_HFUSE", raising=False)
     bi, bt, bl = P.disco_step(None, dev(I), dev(T), 100.0)
     bi, bt = bi.cpu().numpy(), bt.cpu().numpy()
-    monkeypatch.delenv("DISCO_HFUSE")
+    monkeypatch.setenv("DISCO_HFUSE", "1")
     di, dt, loss = P.disco_step(None, dev(I), dev(T), 100.0)
     di, dt = di.cpu().numpy(), dt.cpu().numpy()
     assert not np.array_equal(di, bi)  # the fused path really ran (different rounding)

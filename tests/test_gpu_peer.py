@@ -51,7 +51,7 @@ def sim(I, T, N, t, peer, steps=1, **kw):
 
 @pytest.mark.parametrize("B,D", [(4096, 512), (2048, 768), (3072, 256)])
 def test_peer_matches_all_to_all_and_single_rank(B, D, monkeypatch):
-    monkeypatch.setenv("DISCO_HFUSE", "0")  # N = 1 reference: the N-invariant two-GEMM-pair backward
+    monkeypatch.setenv("DISCO_HFUSE", "0")  # N = 1 reference: the N-invariant path (the default; pinned)
     I, T = O.synthetic_features(B, D, 7)
     di1, dt1, l1 = P.disco_step(None, dev(I), dev(T), 100.0)
     di1, dt1 = di1.cpu().numpy(), dt1.cpu().numpy()
