@@ -188,6 +188,7 @@ struct GemmProblem {
   int M, N;               // valid output extents
   int m_tiles, n_tiles, k_chunks;  // m tiles of 256 rows (CTA pair), n tiles of 256 columns
   int m_off;              // first m tile (row-block launches cover tiles [m_off, m_off + m_tiles))
+  int n_off;              // first output column (split-width launches: [0, 512k) wide, the rest narrow)
   int k_chunk_len;        // elements of K per chunk (multiple of 64 unless k_chunks == 1)
   int k_total;            // total K extent
   int a_k_off, b_k_off;   // added to the K coordinate of MN-major operands
@@ -1083,7 +1084,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
         decode(u, pi, mt, nt, kc);
         const GemmProblem& q = p.prob[pi];
         const int m0 = mt * PAIR_M + crank * BM;
-        const int n0 = nt * NB * BN + crank * (BN / 2);
+        const int n0 = nt * NB * BN + crank * (BN / 2) + q.n_off;
         for (int sub = 0; sub <= q.paired; ++sub) {
           int k0, nk;
           k_range(q, kc * (1 + q.paired) + sub, k0, nk);
@@ -1330,7 +1331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       const int row = row0 + lane;
       const uint32_t lane_base = ctl->tmem_base + (uint32_t(quad * 32) << 16) + chalf * (BN / 2);
       const uint32_t ta0 = lane_base + buf0 * BN, ta1 = lane_base + buf1 * BN;
-      const int cbase = nt * NB * BN + chalf * (BN / 2);
+      const int cbase = nt * NB * BN + chalf * (BN / 2) + q.n_off;
       float* orow = nullptr;
       if (!q.tma_store && row < q.M)
         orow = q.out + kc * q.chunk_stride + (row / q.row_div) * q.stride_hi + (row % q.row_div) * q.ld_out;
@@ -2044,6 +2045,7 @@ struct Geometry {
   int np;                 // cross partials per rank after pairing chunks in the GEMM epilogue
   int g_blocked;          // G in 128 x 128 blocks (canonical chunking: b and B multiples of 128)
   int wide;               // Dp % 512 == 0: GEMM units cover all of D (two accumulators, G read once)
+  int wsplit;             // Dp > 512, Dp % 512 != 0: wide units for the first 512k columns + narrow rest
   int ksplit;             // intra K split (fixed function of B, D): partials [2][ksplit][b][Dp]
   int estore;             // forward stores E + group offsets; backward GEMMs rescale E -> G (no recompute)
   int sym;                // N = 1 + estore: one GEMM of S_0 feeds both directions (S_1 = S_0^T)
@@ -2102,8 +2104,13 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   g->wide = (g->Dp % 512 == 0 && !(debug_flag_bits() & 256)) ? 1 : 0;  // bit8: narrow-unit experiment
   // cross partials per rank: wide units keep one partial per canonical chunk (the first tree
   // level then runs in presum/combine); narrow units pair chunks in the two accumulators.
-  g->np = g->wide ? g->cpr : (g->cpr >= 2 ? g->cpr / 2 : 1);
-  g->ksplit = (g->wide && B % 128 == 0 && B >= 4096) ? 2 : 1;
+  // split width (Dp > 512, not a multiple of 512, e.g. D = 768): columns [0, 512 floor(Dp/512)) run
+  // as wide units and the rest as narrow unpaired units, in two launches with the wide partial
+  // structure (one partial per canonical chunk, two K halves), so E is read twice per GEMM
+  // instead of once per 256 columns
+  g->wsplit = (!g->wide && g->Dp > 512 && !(debug_flag_bits() & 256) && !(debug_flag_bits() & 1048576)) ? 1 : 0;
+  g->np = (g->wide || g->wsplit) ? g->cpr : (g->cpr >= 2 ? g->cpr / 2 : 1);
+  g->ksplit = ((g->wide || g->wsplit) && B % 128 == 0 && B >= 4096) ? 2 : 1;
   static const bool no_estore = [] {  // DISCO_RECOMPUTE=1: A/B switch to the recompute (GRAD) path
     const char* e = getenv("DISCO_RECOMPUTE");
     return e && atoi(e) != 0;
@@ -2501,7 +2508,29 @@ void build_schedule(GemmParams& p, int npairs) {
   p.sched_n = n;
 }
 
-int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform, int hfuse = 0) {
+int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform, int hfuse = 0);
+
+// Split-width backward (g.wsplit): the same problems twice -- wide units over columns
+// [0, wcols), then narrow unpaired units over [wcols, Dp) -- with identical K decompositions, so
+// every output partial is formed exactly as a wide (or narrow) unit alone would form it.
+int launch_backward(GemmParams& p, cudaStream_t st, const Geometry& g) {
+  if (!g.wsplit) return launch_gemm(p, st, g.wide, g.estore);
+  const int wcols = int(g.Dp / 512) * 512;
+  GemmParams q = p;
+  for (int i = 0; i < p.nprob; ++i) {
+    p.prob[i].n_tiles = wcols / (2 * BN);
+    p.prob[i].n_off = 0;
+    p.prob[i].paired = 0;
+    q.prob[i].n_tiles = int((g.Dp - wcols + BN - 1) / BN);
+    q.prob[i].n_off = wcols;
+    q.prob[i].paired = 0;
+  }
+  int rc;
+  if ((rc = launch_gemm(p, st, 1, g.estore))) return rc;
+  return launch_gemm(q, st, 0, g.estore);
+}
+
+int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform, int hfuse) {
   p.units[0] = 0;
   for (int i = 0; i < p.nprob; ++i)
     p.units[i + 1] = p.units[i] + p.prob[i].m_tiles * p.prob[i].n_tiles * p.prob[i].k_chunks;
@@ -2550,7 +2579,7 @@ int build_cross(GemmParams& p, int first, void* ws, const Geometry& g, int mt0 =
   const __half* I16 = f16;
   const __half* T16 = f16 + g.B * g.Dp;
   const int64_t Bc = g.B / g.nchunk;  // canonical chunk rows
-  const int cross_wide = g.wide;      // wide units read G once; otherwise chunks are paired
+  const int cross_wide = g.wide || g.wsplit;  // wide / split units: one partial per chunk; else pairs
   int rc;
   for (int gi = 0; gi < 2; ++gi) {
     GemmProblem& q = p.prob[first + gi];
@@ -3019,7 +3048,7 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
   memset(&p, 0, sizeof(p));
   if ((rc = build_cross(p, 0, ws, g))) return rc;
   p.nprob = 2;
-  if ((rc = launch_gemm(p, st, g.wide, g.estore))) return rc;
+  if ((rc = launch_backward(p, st, g))) return rc;
   return cross_presum(ws, g, st);
 }
 
@@ -3035,7 +3064,7 @@ int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int ran
   }
   if ((rc = build_intra(p, 0, ws, g))) return rc;
   p.nprob = 2;
-  return launch_gemm(p, st_of(stream), g.wide, g.estore);
+  return launch_backward(p, st_of(stream), g);
 }
 
 int disco_b200_backward_fused(void* ws, int64_t B, int64_t D, int world, int rank, void* stream) {
@@ -3053,7 +3082,7 @@ int disco_b200_backward_fused(void* ws, int64_t B, int64_t D, int world, int ran
   if ((rc = build_cross(p, 2, ws, g))) return rc;  // list B: one canonical chunk of K per unit
   p.nprob = 4;
   p.split = 2;
-  if ((rc = launch_gemm(p, st, g.wide, g.estore))) return rc;
+  if ((rc = launch_backward(p, st, g))) return rc;
   return cross_presum(ws, g, st);
 }
 
@@ -3098,7 +3127,7 @@ int disco_b200_backward_rows(void* ws, int64_t B, int64_t D, int world, int rank
   if ((rc = build_cross(p, 2, ws, g, mt0, mt1))) return rc;
   p.nprob = 4;
   p.split = 2;
-  return launch_gemm(p, st_of(stream), g.wide, g.estore);
+  return launch_backward(p, st_of(stream), g);
 }
 
 int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,
@@ -3266,7 +3295,7 @@ int disco_b200_backward_peer(void* ws, int64_t B, int64_t D, int world, int rank
     if ((rc = set_output_peer(p.prob[2 + gi], peer_bases, parity, g, gi))) return rc;
   p.nprob = 4;
   p.split = 2;
-  if ((rc = launch_gemm(p, st, g.wide, g.estore))) return rc;
+  if ((rc = launch_backward(p, st, g))) return rc;
   // the rank's per-row ce rides with the slabs: the owners' combine wait covers it too
   PeerDst pd;
   memset(&pd, 0, sizeof(pd));

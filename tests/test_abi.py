@@ -102,7 +102,8 @@ def test_peer_window_geometry():
     out = ctypes.c_int64()
     lib = _lib.load()
     assert lib.disco_b200_peer_handle_bytes() == 64
-    for B, D, N, leaves in [(32768, 512, 8, 8), (32768, 512, 2, 8), (65536, 768, 4, 4), (3072, 256, 3, 3)]:
+    # D = 768 (split width: wide + narrow launches) keeps one leaf per canonical chunk like D = 512
+    for B, D, N, leaves in [(32768, 512, 8, 8), (32768, 512, 2, 8), (65536, 768, 4, 8), (3072, 256, 3, 3)]:
         _lib.call("disco_b200_peer_bytes", B, D, N, 0, ctypes.byref(out))
         b, Dp = B // N, (D + 63) // 64 * 64
         win = (2 * leaves * b * Dp * 4 + 1023) // 1024 * 1024
