@@ -2117,7 +2117,7 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   }();
   g->estore = (g->g_blocked && !no_estore) ? 1 : 0;
   // DISCO_SYMMETRIC=1 (read per call; experiment, off by default): the symmetric single-rank
-  // forward.  Correct (tools/sym_ab.py, test_symmetric_forward_vs_oracle) but measured slower: the
+  // forward.  Correct (tools/env_ab.py, test_symmetric_forward_vs_oracle) but measured slower: the
   // t2i column statistics cost ~2x the i2t epilogue in issue slots and MUFU, more than the halved
   // MMA saves.  Not bitwise equal to N > 1 (t2i sums in another order).
   const char* sym_env = getenv("DISCO_SYMMETRIC");

@@ -1,7 +1,7 @@
 """Single-rank path switches A/B: an environment switch (default DISCO_SYMMETRIC, the symmetric
 forward; DISCO_HFUSE, the fused backward) at 1 against 0.
 
-  python tools/sym_ab.py [--var DISCO_SYMMETRIC] [--sizes 2048x512 8192x512 32768x512 16384x1024] [--reps 10]
+  python tools/env_ab.py [--var DISCO_SYMMETRIC] [--sizes 2048x512 8192x512 32768x512 16384x1024] [--reps 10]
 
 For each size: both paths on the same device inputs, their normwise difference, the symmetric
 path against the f64 oracle on sampled rows, and the device step time of each (CUDA events,
@@ -61,11 +61,11 @@ for sz in a.sizes:
     Ib, Tb = O.bf16_round(I), O.bf16_round(T)
     rows = np.linspace(0, B - 1, 24).astype(np.int64)
     ri, rt, rl = O.clip_grad_rows(Ib, Tb, a.t, rows)
-    r = {"ms_two_gemm": round(ms0, 4), "ms_sym": round(ms1, 4),
-         "sym_vs_two_gemm": [float(O.max_rel_error(di1, di0)), float(O.max_rel_error(dt1, dt0)), abs(l1 - l0) / abs(l0)],
-         "sym_vs_oracle": [float(O.max_rel_error(di1[rows], ri)), float(O.max_rel_error(dt1[rows], rt)),
+    r = {"ms_off": round(ms0, 4), "ms_on": round(ms1, 4),
+         "on_vs_off": [float(O.max_rel_error(di1, di0)), float(O.max_rel_error(dt1, dt0)), abs(l1 - l0) / abs(l0)],
+         "on_vs_oracle": [float(O.max_rel_error(di1[rows], ri)), float(O.max_rel_error(dt1[rows], rt)),
                            abs(l1 - rl[0]) / rl[0]],
-         "two_gemm_vs_oracle": [float(O.max_rel_error(di0[rows], ri)), float(O.max_rel_error(dt0[rows], rt)),
+         "off_vs_oracle": [float(O.max_rel_error(di0[rows], ri)), float(O.max_rel_error(dt0[rows], rt)),
                                 abs(l0 - rl[0]) / rl[0]],
          "bitwise_d_image": bool(np.array_equal(di0, di1)), "bitwise_d_text": bool(np.array_equal(dt0, dt1))}
     res[sz] = r
