@@ -103,7 +103,7 @@ static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory li
 // the tiles (after the control block): 128 row factors of direction d (256 B) + the direction-d'
 // factor vectors of the CTA's two 64-row groups (2 x 128 B).
 constexpr int HF_SCALE_BYTES = 512;
-constexpr size_t SMEM_BYTES_HF = SMEM_BYTES + 3 * HF_SCALE_BYTES;
+constexpr size_t SMEM_BYTES_HF = SMEM_BYTES + size_t(Ring<2, 2>::STAGES) * HF_SCALE_BYTES;
 static_assert(SMEM_BYTES_HF <= 232448, "fused backward smem");
 static_assert(sizeof(uint64_t) * 46 + 4 <= 512, "control block");
 
@@ -1028,7 +1028,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
   uint8_t* tiles = smem_base(smem_raw);
   uint8_t* staging = tiles + TILE_RING_BYTES;
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + TILE_RING_BYTES + STAGING_BYTES);
-  uint8_t* hf_scales = reinterpret_cast<uint8_t*>(ctl) + 512;  // HF: [RS][HF_SCALE_BYTES]
+  uint8_t* hf_scales = reinterpret_cast<uint8_t*>(ctl) + 512;  // HF: [RS][HF_SCALE_BYTES] (SMEM_BYTES_HF)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int crank = int(ptx::cluster_ctarank());
   const bool leader = crank == 0;
