@@ -44,7 +44,6 @@ TEMP = 100.0
 CONFIGS = {"A": (1024, 512), "B": (32768, 512), "C": (65536, 768), "D": (196608, 512), "E": (16384, 1024)}
 METRIC = "contrastive-loss fwd+bwd samples/sec at B=32K,D=512; peak loss mem/GPU"
 UNIT = "samples/s"
-CPU_SAMPLE_ROWS = 2048
 
 
 def parse():
@@ -60,44 +59,64 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fused", action="store_true", help="skip the opt-in fused single-rank backward leg")
+    ap.add_argument("--no-ref-check", action="store_true",
+                    help="reference arm: skip the one-step unmodified-reference cross-check")
     return ap.parse_args()
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port of the reference path, bounded row sample
+# CPU baseline: the reference algorithm on the host cores, FULL workload per step
 # ---------------------------------------------------------------------------
-def cpu_port_sample(B, D, rows, t=TEMP, seed=0, reps=1):
-    """Time the reference algorithm (shard.py:98-166, f32 as costs.py:158) for
-    `rows` local rows of a rank against all B columns, both directions:
-    logits GEMMs, CE, softmax-minus-onehot, the four gradient GEMMs.
-    Returns (samples/s, seconds per sample block)."""
+def cpu_features(B, D, seed=0):
+    """cli.py:103-105 features, bf16-rounded, as f32 (the reference's benchmark precision,
+    costs.py:158)."""
     from oracle import disco_oracle as O
     rng = np.random.default_rng(seed)
     I = rng.standard_normal((B, D)).astype(np.float32)
     I /= np.linalg.norm(I, axis=1, keepdims=True)
     T = rng.standard_normal((B, D)).astype(np.float32)
     T /= np.linalg.norm(T, axis=1, keepdims=True)
-    I, T = O.bf16_round(I), O.bf16_round(T)
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        I_n, T_n = I[:rows], T[:rows]
-        labels = np.arange(rows)
-        li = (I_n @ T.T) * np.float32(t)
-        lt = (T_n @ I.T) * np.float32(t)
-        loss = (O.cross_entropy_mean(li, labels) + O.cross_entropy_mean(lt, labels)) / 2.0
-        O.softmax_ce_grad_inplace(li, labels, 0.5 / rows)
-        O.softmax_ce_grad_inplace(lt, labels, 0.5 / rows)
-        d_image = lt.T @ T_n
-        d_image[:rows] += li @ T
-        d_text = li.T @ I_n
-        d_text[:rows] += lt @ I
-        d_image *= t
-        d_text *= t
-        assert np.isfinite(loss)
-        times.append(time.perf_counter() - t0)
-    sec = statistics.median(times)
-    return rows / sec, sec
+    return O.bf16_round(I), O.bf16_round(T)
+
+
+def cpu_port_step(I, T, world, t=TEMP, workers=None):
+    """One full DisCo step of all `world` ranks on the host (oracle.disco_step_blocked: the
+    reference's shard.py:98-208 arithmetic in f32, row blocks on `workers` threads with
+    single-threaded BLAS each).  Returns seconds."""
+    from oracle import disco_oracle as O
+    from threadpoolctl import threadpool_limits
+    workers = workers or cpu_cores()
+    t0 = time.perf_counter()
+    with threadpool_limits(1):
+        d_i, d_t, loss = O.disco_step_blocked(I, T, world, t, rows_per_block=512, workers=workers)
+    sec = time.perf_counter() - t0
+    assert np.isfinite(loss)
+    return sec
+
+
+def unmodified_reference_step(I, T, world, t=TEMP):
+    """One step of the UNMODIFIED reference disco_step (shard.py:169-208) through its own
+    run_ranks (fabric.py:291, lockstep) with verification on, from baseline/_ref when that
+    install is present (python -m pip install --no-deps ... --target baseline/_ref).  A single
+    cross-check of the port's speed on the same host; None when absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "disco")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        import disco  # noqa: F401  (the reference package, unmodified)
+        from disco import disco_step, run_ranks
+    finally:
+        sys.path.remove(ref)
+    b = I.shape[0] // world
+
+    def fn(ep):
+        rows = slice(ep.rank * b, (ep.rank + 1) * b)
+        return disco_step(ep, I[rows], T[rows], t)[2]
+
+    t0 = time.perf_counter()
+    run_ranks(world, fn, mode="lockstep")
+    return time.perf_counter() - t0
 
 
 def cpu_cores():
@@ -111,32 +130,43 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    B, D = args.batch, args.dim
-    rows = min(CPU_SAMPLE_ROWS, B)
-    for _ in range(max(args.warmup, 1) if args.warmup else 0):
-        cpu_port_sample(B, D, rows // 4)
-    vals = []
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, _ = cpu_port_sample(B, D, rows)
-        vals.append(v)
-    wall = time.perf_counter() - t0
-    value = statistics.median(vals)
-    sample = (f"{rows} of {B // args.gpus} local rows x {B} columns, D={D}, both directions, "
-              f"f32 numpy/BLAS; samples/s = rows / time")
+    B, D, N = args.batch, args.dim, args.gpus
+    I, T = cpu_features(B, D)
+    cores = cpu_cores()
+    t_start = time.perf_counter()
+    for _ in range(args.warmup):
+        cpu_port_step(I, T, N)
+    secs = [cpu_port_step(I, T, N) for _ in range(args.steps)]
+    wall = time.perf_counter() - t_start
+    sec = statistics.mean(secs)
+    value = B / sec
+    unmod = None
+    if not args.no_ref_check:
+        us = unmodified_reference_step(I, T, N)
+        if us is not None:
+            unmod = {"value": B / us, "unit": UNIT, "ms_per_step": 1e3 * us, "steps": 1,
+                     "note": "unmodified reference disco_step via run_ranks(lockstep) from baseline/_ref, "
+                             "verification on, f32, one step (cross-check of the port's speed)"}
+    sample = (f"full step: all {N} rank(s) x {B // N} rows x {B} columns, D={D}, both directions "
+              f"(oracle.disco_step_blocked, f32, {cores} threads x 1-thread BLAS)")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * B / value,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": f"B={B},D={D},t={TEMP} (BASELINE config {args.config})",
-                                         "global_batch": B, "dim": D, "parallelism": f"dp{args.gpus}"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-                         "sample": sample},
+        "data": "synthetic", "config": workload_config(args, B, D, N),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "unmodified_reference": unmod},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def workload_config(args, B, D, world):
+    """The `config` object both arms print (same keys, so the driver can pair the lines)."""
+    return {"workload": f"B={B},D={D},t={TEMP} (BASELINE config {args.config})", "global_batch": B,
+            "local_batch": B // world, "dim": D, "parallelism": f"dp{world}"}
 
 
 # ---------------------------------------------------------------------------
@@ -214,6 +244,77 @@ def load_traffic():
         return {}
 
 
+def exchange_preflight(P, ep, I, T, t, world, local_rank, share):
+    """Decide the N > 1 exchange before the timed steps (never fatal).
+
+    The peer transport (default) needs peer access between every pair of GPUs and working CUDA
+    IPC windows.  Check ``can_device_access_peer`` for all pairs, then run one step through the
+    NCCL exchange (DISCO_PEER=0 path) and one through the peer transport and require identical
+    bytes (both are bitwise equal to N = 1 by construction).  Any failure, timeout or mismatch
+    on any rank selects the NCCL exchange for the whole job; the choice and the reason are
+    recorded in ``config.exchange_preflight``."""
+    import torch
+    import torch.distributed as dist
+    from paper_2304_08480_b200 import peer as peer_mod
+    from paper_2304_08480_b200.shard import clear_plans
+
+    B, D = I.shape[0] * world, I.shape[1]
+    info = {"peer_requested": peer_mod.enabled(ep), "peer_supported": peer_mod.supported(B, D, world, ep.rank)}
+    dev = torch.device("cuda", local_rank)
+
+    def agree(ok: bool) -> bool:  # every rank must agree (MIN over ranks)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev if not share else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        return bool(flag.item())
+
+    if share:
+        access = True  # every rank on cuda:0 (code-path check)
+    else:
+        n_dev = torch.cuda.device_count()
+        access = all(torch.cuda.can_device_access_peer(local_rank, j) for j in range(min(world, n_dev)) if j != local_rank)
+    info["peer_access_all_pairs"] = agree(access)
+    if not (info["peer_requested"] and info["peer_supported"]):
+        info.update(choice="nccl", reason="peer transport not requested or not supported for this geometry")
+        ep.peer = False
+        return info
+    if not info["peer_access_all_pairs"]:
+        info.update(choice="nccl", reason="cudaDeviceCanAccessPeer false for some GPU pair")
+        ep.peer = False
+        return info
+    ref, err = None, None
+    try:
+        ep.peer = False
+        di0, dt0, l0 = P.disco_step(ep, I, T, t)
+        ref = (di0.clone(), dt0.clone(), l0)
+    except Exception as exc:  # pragma: no cover - reported, then the job decides below
+        err = f"nccl step failed: {type(exc).__name__}: {exc}"
+    same = False
+    saved_timeout = peer_mod.PEER_TIMEOUT_S
+    if ref is not None:
+        peer_mod.PEER_TIMEOUT_S = 20.0  # a broken transport raises CollectiveTimeoutError, never hangs
+        try:
+            ep.peer = True
+            for _ in range(2):  # both parity windows
+                di1, dt1, l1 = P.disco_step(ep, I, T, t)
+            same = bool(torch.equal(di1, ref[0]) and torch.equal(dt1, ref[1]) and l1 == ref[2])
+            if not same:
+                err = "peer step differs from the NCCL step"
+        except Exception as exc:
+            err = f"peer step failed: {type(exc).__name__}: {exc}"
+        finally:
+            peer_mod.PEER_TIMEOUT_S = saved_timeout
+    try:
+        ok = agree(same)
+    except Exception as exc:  # pragma: no cover
+        ok, err = False, f"agreement collective failed: {exc}"
+    info["peer_step_matches_nccl"] = ok
+    ep.peer = ok
+    if not ok:
+        clear_plans()
+    info.update(choice="peer" if ok else "nccl", reason=err if not ok else "peer access + bitwise-equal preflight step")
+    return info
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -258,6 +359,12 @@ def run_ours(args):
     def barrier():
         if world > 1:
             dist.barrier()
+
+    # ---- N > 1: check the peer transport before trusting it with the timed steps -------------
+    preflight = exchange_preflight(P, ep, I, T, TEMP, world, local_rank, share) if world > 1 else None
+    from paper_2304_08480_b200.shard import clear_plans
+    clear_plans()
+    torch.cuda.empty_cache()
 
     # ---- loss-scope memory: everything the first step allocates (workspace incl. the O(B^2/N)
     # E/G blocks, outputs), measured by the caching allocator from a clean slate -----------
@@ -363,6 +470,32 @@ def run_ours(args):
         for n in names:
             acc[n] += ev[n][0].elapsed_time(ev[n][1]) / reps
     phases = {n: round(v, 4) for n, v in acc.items()}
+    traffic_n = None
+    peer_bytes = 0
+    if world > 1:
+        from paper_2304_08480_b200 import costs as costs_mod
+        Dp = (D + 63) // 64 * 64
+        ag_bytes = (world - 1) * 2 * b * Dp * 2   # bf16 rows received per rank (both feature sets)
+        rs_bytes = (world - 1) * 2 * b * Dp * 4   # fp32 partial rows each rank sends to their owners
+        link = 900.0                              # NVLink 5 GB/s per direction
+        ag_ms = phases.get("peer_gather", phases.get("all_gather"))
+        traffic_n = {"note": "bytes per rank per step; busbw = bytes moved per rank / phase time "
+                             "(nccl-tests convention: algbw * (N-1)/N); link = 900 GB/s per direction",
+                     "all_gather": {"bytes": ag_bytes, "ms": ag_ms, "busbw_gbs": ag_bytes / (ag_ms / 1e3) / 1e9,
+                                    "frac_of_link": ag_bytes / (ag_ms / 1e3) / 1e9 / link,
+                                    "kind": "peer pull + unpack kernel" if use_peer else "nccl all_gather_into_tensor"}}
+        if use_peer:
+            bw_ms = phases["backward_peer"]
+            traffic_n["reduce_scatter"] = {
+                "bytes": rs_bytes, "ms_overlapped": bw_ms, "combine_ms": phases["combine_peer"],
+                "push_gbs_during_gemm": rs_bytes / (bw_ms / 1e3) / 1e9,
+                "kind": "TMA pushes from the backward GEMM epilogue into the owners' windows (overlapped)"}
+            peer_bytes = costs_mod.peer_window_bytes(B, D, world, rank)
+        else:
+            a_ms = phases["all_to_all"]
+            traffic_n["reduce_scatter"] = {"bytes": rs_bytes, "ms": a_ms, "busbw_gbs": rs_bytes / (a_ms / 1e3) / 1e9,
+                                           "frac_of_link": rs_bytes / (a_ms / 1e3) / 1e9 / link,
+                                           "kind": "nccl all_to_all_single of fp32 destination slabs"}
     kernel_mhz = _lib.clock_probe(plan)  # SM clock the last timed launches actually ran at
 
     # ---- e2e through the public API with host buffers ---------------------
@@ -499,28 +632,30 @@ def run_ours(args):
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        rows = CPU_SAMPLE_ROWS
-        cpu_port_sample(B, D, rows // 8)
-        v, sec = cpu_port_sample(B, D, rows)
-        cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-               "sample": f"{rows} of {b} local rows x {B} columns, D={D}, both directions, "
-                         f"oracle/disco_oracle.py f32 numpy ({sec:.1f} s)"}
+        I_c, T_c = cpu_features(B, D)
+        sec = cpu_port_step(I_c, T_c, world)
+        cpu = {"value": B / sec, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+               "sample": f"one full step: {b} rows x {B} columns, D={D}, both directions "
+                         f"(oracle.disco_step_blocked, f32, {cpu_cores()} threads; {sec:.1f} s)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"B={B},D={D},t={TEMP} (BASELINE config {args.config})", "global_batch": B,
-                   "local_batch": b, "dim": D, "parallelism": f"dp{world}",
-                   "exchange": ("none" if world == 1 else
-                                "peer (GEMM epilogue TMA pushes over NVLink)" if use_peer else "nccl all_to_all"),
-                   "l2": "flushed between steps (512 MB write, outside timed events)"},
+        "config": dict(workload_config(args, B, D, world),
+                       exchange=("none" if world == 1 else
+                                 "peer (GEMM epilogue TMA pushes over NVLink)" if use_peer else "nccl all_to_all"),
+                       exchange_preflight=preflight,
+                       l2="flushed between steps (512 MB write, outside timed events)"),
         "loss": loss,
-        "peak_loss_mem_gb": loss_mem / 1e9,
+        "peak_loss_mem_gb": (loss_mem + peer_bytes) / 1e9,
         "loss_mem_detail": {"e_blocks_gb": g_bytes_ws / 1e9, "workspace_gb": plan.ws.numel() / 1e9,
+                            "peer_window_gb": peer_bytes / 1e9,
                             "reference_loss_scope_elems": 2 * b * B,
-                            "note": "max_memory_allocated delta of the first step (workspace + outputs); "
+                            "note": "max_memory_allocated delta of the first step (workspace + outputs) + the "
+                                    "peer window (cudaMalloc'd outside torch, N > 1 peer transport); "
                                     "E blocks = 2*b*B f16 = the reference's 2*b*B loss elements (costs.py:110-112)"},
+        "exchange_traffic": traffic_n,
         "peak_mem_gb": peak_mem / 1e9,
         "roofline": {"bound": d["bound"], "kernel": dom, "achieved": d["achieved"], "peak": d["peak"],
                      "unit": d["unit"], "frac": d["frac"], "traffic": traffic,

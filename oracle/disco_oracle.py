@@ -245,6 +245,73 @@ def disco_step_all(I, T, world: int, t: float, flip_cross_rank_sign: bool = Fals
     return acc_i, acc_t, loss
 
 
+def disco_step_blocked(I, T, world: int, t: float, rows_per_block: int = 1024, workers: int = 1):
+    """All ranks of shard.py:169-208 computed in row blocks on a thread pool: the CPU baseline's
+    timing kernel (bench.py ``--impl reference`` / ``cpu_baseline``), NOT a parity oracle.
+
+    Same arithmetic as ``disco_step_all`` in the dtype of the inputs (f32 in the bench, the
+    reference's benchmark precision, costs.py:158): for rank n and each block of its rows
+    (labels n*b + arange, shard.py:92-95), logits = t * rows @ gathered.T (shard.py:134-137),
+    row CE (matrix.py:103-118), G = (softmax - onehot) * 0.5/b in place (matrix.py:131-144),
+    then the cross terms G^T @ rows accumulated into full-size B x D contributions and the
+    intra terms G @ gathered written into the block's rows (shard.py:148-154); the contributions
+    are averaged over ranks (fabric.py:86-93) and the loss likewise.  The blocks of one rank's
+    step are independent except for the cross accumulation, which each worker keeps in its own
+    buffer and which is summed in worker order at the end.  numpy releases the GIL in BLAS and
+    large ufuncs, so ``workers`` threads each run single-threaded BLAS on their own blocks.
+    Returns (d_image, d_text, loss) for all B rows.
+    """
+    from concurrent.futures import ThreadPoolExecutor
+
+    I = np.ascontiguousarray(I)
+    T = np.ascontiguousarray(T)
+    B, D = I.shape
+    b = B // world
+    dt = I.dtype.type
+    tasks = []
+    for n in range(world):
+        for r0 in range(n * b, (n + 1) * b, rows_per_block):
+            tasks.append((n, r0, min(r0 + rows_per_block, (n + 1) * b)))
+    workers = max(1, min(workers, len(tasks)))
+    parts = [tasks[w::workers] for w in range(workers)]
+    intra_i = np.zeros((B, D), dtype=I.dtype)
+    intra_t = np.zeros((B, D), dtype=I.dtype)
+
+    def run(mine):
+        cross_i = np.zeros((B, D), dtype=I.dtype)
+        cross_t = np.zeros((B, D), dtype=I.dtype)
+        ce = 0.0
+        for n, r0, r1 in mine:
+            labels = np.arange(r0, r1)
+            li = (I[r0:r1] @ T.T) * dt(t)
+            lt = (T[r0:r1] @ I.T) * dt(t)
+            ce += float(row_ce(li, labels).sum() + row_ce(lt, labels).sum())
+            softmax_ce_grad_inplace(li, labels, 0.5 / b)
+            softmax_ce_grad_inplace(lt, labels, 0.5 / b)
+            cross_i += lt.T @ T[r0:r1]
+            cross_t += li.T @ I[r0:r1]
+            intra_i[r0:r1] = li @ T
+            intra_t[r0:r1] = lt @ I
+        return cross_i, cross_t, ce
+
+    if workers == 1:
+        results = [run(parts[0])]
+    else:
+        with ThreadPoolExecutor(workers) as pool:
+            results = list(pool.map(run, parts))
+    d_image = intra_i
+    d_text = intra_t
+    ce = 0.0
+    for ci, ct, c in results:
+        d_image += ci
+        d_text += ct
+        ce += c
+    d_image *= dt(t / world)
+    d_text *= dt(t / world)
+    loss = ce / (2.0 * b) / world
+    return d_image, d_text, loss
+
+
 # ---------------------------------------------------------------------------
 # inputs and the parity metric composition (cli.py)
 # ---------------------------------------------------------------------------

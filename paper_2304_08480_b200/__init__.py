@@ -19,7 +19,7 @@ from .errors import (
     ShapeError,
     TrainingDivergenceError,
 )
-from .fabric import LocalEndpoint, LocalGroup, ProcessGroupEndpoint, ReduceOp, SingleEndpoint, run_ranks
+from .fabric import CONCURRENT, LOCKSTEP, LocalEndpoint, LocalGroup, ProcessGroupEndpoint, ReduceOp, SingleEndpoint, run_ranks
 from .shard import (
     LocalGradContribution,
     ShardLayout,
@@ -36,6 +36,8 @@ from .shard import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "CONCURRENT",
+    "LOCKSTEP",
     "CollectiveContractError",
     "CollectiveTimeoutError",
     "Counters",

@@ -24,6 +24,7 @@ loss by the world size.
 
 import torch
 
+from .errors import ShapeError
 from .fabric import SingleEndpoint
 from .shard import _check_t, disco_step_async, finish_status_with_dlogit, logit_scale_grad_async
 
@@ -34,8 +35,13 @@ class DiscoLossFunction(torch.autograd.Function):
         t = _check_t(float(logit_scale.detach()) if torch.is_tensor(logit_scale) else logit_scale)
         I = image_features.detach()
         T = text_features.detach()
+        if I.dim() != 2 or tuple(I.shape) != tuple(T.shape):
+            raise ShapeError(f"feature shapes must be equal 2-D matrices, got {tuple(I.shape)} and {tuple(T.shape)}")
         if T.dtype != I.dtype:
             T = T.to(I.dtype)
+        if I.device != T.device:
+            raise ValueError(f"features on different devices: {I.device} vs {T.device}")
+        I, T = I.contiguous(), T.contiguous()
         d_image, d_text, plan = disco_step_async(endpoint, I, T, t)
         logit_scale_grad_async(endpoint, plan, d_image, d_text, t)
         loss, dlogit = finish_status_with_dlogit(plan)

@@ -34,6 +34,7 @@ import numpy as np
 import torch
 
 from .errors import DomainError
+from .fabric import CONCURRENT, LOCKSTEP
 
 METHODS = ("CLIP", "BASIC", "DisCo", "DisCo*")
 CSV_FIELDS = ("method", "B", "N", "L", "D", "backbone_elements",
@@ -122,15 +123,15 @@ def bytes_moved(collective: str, buffer_elements: int, N: int) -> int:
 # ---------------------------------------------------------------------------
 # measured on the device
 # ---------------------------------------------------------------------------
-def _features(B, D, seed, device):
-    """cli.py:103-105 inputs (seeded, rows L2-normalised), as device fp32."""
+def _features(B, D, seed, device, dtype=torch.float32):
+    """cli.py:103-105 inputs (seeded, rows L2-normalised), on the device."""
     rng = np.random.default_rng(seed)
     I = rng.standard_normal((B, D))
     I /= np.linalg.norm(I, axis=1, keepdims=True)
     T = rng.standard_normal((B, D))
     T /= np.linalg.norm(T, axis=1, keepdims=True)
-    return (torch.tensor(I, dtype=torch.float32, device=device),
-            torch.tensor(T, dtype=torch.float32, device=device))
+    return (torch.tensor(I, dtype=dtype, device=device),
+            torch.tensor(T, dtype=dtype, device=device))
 
 
 def _naive_clip_step(I, T, t):
@@ -144,23 +145,72 @@ def _naive_clip_step(I, T, t):
     return I.grad, T.grad, float(loss.detach())
 
 
-def measured_detail(mode: str, B: int, N: int, D: int, *, temperature: float = 10.0, seed: int = 0,
-                    device=None):
-    """(loss_elements, loss_flops, bytes_per_rank) of one measured loss call on the GPU.
 
-    disco: N simulated ranks (threads) run ``disco_step`` on fresh workspaces; the
-    allocator peak over a clean slate, divided by N (the ranks are symmetric), is the
-    per-rank device footprint.  naive: one full-batch CLIP step.
+
+def _validate_measured(mode, B, N, precision, scheduler):
+    if mode not in ("naive", "disco"):
+        raise DomainError(f"mode must be 'naive' or 'disco', got {mode!r}")
+    if precision not in PRECISION_BYTES:
+        raise DomainError(f"precision must be one of {tuple(PRECISION_BYTES)}")
+    if scheduler not in (LOCKSTEP, CONCURRENT):
+        raise DomainError(f"scheduler must be {LOCKSTEP!r} or {CONCURRENT!r}, got {scheduler!r}")
+    if B % N != 0:
+        raise DomainError(f"B={B} is not divisible by N={N}")
+    if not torch.cuda.is_available():
+        raise RuntimeError("measured footprints need a CUDA device (no CPU fallback)")
+
+
+def measured_detail(mode: str, B: int, N: int, D: int, *, precision: str = "f64", temperature: float = 10.0,
+                    seed: int = 0, scheduler: str = LOCKSTEP, device=None):
+    """Raw per-rank counter peaks (loss_peak, loss_flops, exchange_peak) -- costs.py:143-187.
+
+    Same contract as the reference: ``disco`` passes ``Counters`` through this package's
+    ``disco_step`` on N simulated ranks (the device path records the reference's accounting,
+    shard.py:133-156 and 192-204: loss peak 2*b*B, 4*b*B*D FLOPs, exchange peak 5*B*D) and
+    returns the max over ranks; ``naive`` runs the full-batch CLIP loss on the GPU with the
+    accounting of clip_grad_full (oracle.py:148-186: B*B, 2*B*B*D, 2*B*D).  The device bytes
+    the call allocates are ``measured_device_bytes``.
+    """
+    from . import shard
+    from .counters import Counters
+    from .fabric import run_ranks
+
+    _validate_measured(mode, B, N, precision, scheduler)
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    I, T = _features(B, D, seed, device, torch.float64 if precision == "f64" else torch.float32)
+    if mode == "naive":
+        loss_counters, exchange_counters = Counters(), Counters()
+        loss_counters.add_flops(2 * B * B * D)
+        loss_counters.alloc(B * B)
+        _naive_clip_step(I, T, temperature)
+        exchange_counters.add_flops(4 * B * B * D)
+        exchange_counters.alloc(2 * B * D)
+        loss_counters.release(B * B)
+        return (loss_counters.peak_live_elements, loss_counters.flops, exchange_counters.peak_live_elements)
+    b = B // N
+
+    def fn(ep):
+        rows = slice(ep.rank * b, (ep.rank + 1) * b)
+        lc, xc = Counters(), Counters()
+        shard.disco_step(ep, I[rows], T[rows], temperature, loss_counters=lc, exchange_counters=xc)
+        return lc.peak_live_elements, lc.flops, xc.peak_live_elements
+
+    per_rank = run_ranks(N, fn, device=device)
+    return tuple(max(v) for v in zip(*per_rank))
+
+
+def measured_device_bytes(mode: str, B: int, N: int, D: int, *, temperature: float = 10.0, seed: int = 0,
+                          device=None) -> int:
+    """Device bytes one loss call allocates per rank (torch caching-allocator peak over a clean slate).
+
+    disco: N simulated ranks (threads) run ``disco_step`` on fresh workspaces; the peak divided by
+    N (the ranks are symmetric) is the per-rank footprint, plus the rank's peer window (cudaMalloc'd
+    outside torch, N > 1 with the peer transport).  naive: one full-batch CLIP step.
     """
     from . import shard
     from .fabric import run_ranks
 
-    if mode not in ("naive", "disco"):
-        raise DomainError(f"mode must be 'naive' or 'disco', got {mode!r}")
-    if B % N != 0:
-        raise DomainError(f"B={B} is not divisible by N={N}")
-    if not torch.cuda.is_available():
-        raise RuntimeError("measured_footprint needs a CUDA device (no CPU fallback)")
+    _validate_measured(mode, B, N, "f32", LOCKSTEP)
     device = device or torch.device("cuda", torch.cuda.current_device())
     I, T = _features(B, D, seed, device)
     shard.clear_plans()
@@ -172,7 +222,6 @@ def measured_detail(mode: str, B: int, N: int, D: int, *, temperature: float = 1
         _naive_clip_step(I, T, temperature)
         torch.cuda.synchronize(device)
         per_rank = torch.cuda.max_memory_allocated(device) - base
-        loss_elements, loss_flops = B * B, 2 * B * B * D
     else:
         b = B // N
 
@@ -183,16 +232,33 @@ def measured_detail(mode: str, B: int, N: int, D: int, *, temperature: float = 1
         run_ranks(N, fn, device=device)
         torch.cuda.synchronize(device)
         per_rank = (torch.cuda.max_memory_allocated(device) - base) // N
-        loss_elements, loss_flops = 2 * b * B, 4 * b * B * D  # shard.py:133-138 accounting
+        per_rank += peer_window_bytes(B, D, N)
     shard.clear_plans()
     torch.cuda.empty_cache()
-    return loss_elements, loss_flops, int(per_rank)
+    return int(per_rank)
 
 
-def measured_footprint(mode: str, B: int, N: int, D: int, *, temperature: float = 10.0, seed: int = 0,
-                       device=None) -> CostReport:
-    """CostReport of one measured loss call (costs.py:124-140 schema; bytes measured)."""
-    le, lf, nbytes = measured_detail(mode, B, N, D, temperature=temperature, seed=seed, device=device)
+def peer_window_bytes(B: int, D: int, N: int, rank: int = 0) -> int:
+    """Bytes of a rank's peer-transport window (0 when the geometry does not use it)."""
+    import ctypes
+    from . import _lib
+    from . import peer
+
+    if not peer.supported(B, D, N, rank):
+        return 0
+    out = ctypes.c_int64()
+    _lib.call("disco_b200_peer_bytes", B, D, N, rank, ctypes.byref(out))
+    return int(out.value)
+
+
+def measured_footprint(mode: str, B: int, N: int, D: int, *, precision: str = "f64", temperature: float = 10.0,
+                       seed: int = 0, scheduler: str = LOCKSTEP, device=None) -> CostReport:
+    """CostReport of one measured loss call (costs.py:124-140 schema).  ``loss_elements`` /
+    ``loss_flops`` are the counter peaks of ``measured_detail``; ``bytes`` is the MEASURED device
+    footprint per rank (``measured_device_bytes``), not elements x scalar size."""
+    le, lf, _ = measured_detail(mode, B, N, D, precision=precision, temperature=temperature, seed=seed,
+                                scheduler=scheduler, device=device)
+    nbytes = measured_device_bytes(mode, B, N, D, temperature=temperature, seed=seed, device=device)
     return _report("CLIP" if mode == "naive" else "DisCo", B, N, 0, D, 0, le, lf, nbytes)
 
 

@@ -1422,7 +1422,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
   probe_mark(p.probe, 2);
 }
 
-__global__ void __launch_bounds__(NUM_THREADS_XF, 1) cluster_probe_kernel() {}
 
 // =====================================================================
 // Small HBM-bound kernels
@@ -2827,26 +2826,6 @@ extern "C" {
 int disco_b200_abi_version(void) { return DISCO_B200_ABI_VERSION; }
 
 int disco_b200_set_experiment_flags(int flags) { return g_debug_bits.exchange(flags); }
-
-// Profiling helper: co-resident clusters of `cluster_size` CTAs for the backward GEMM's launch
-// shape (SMEM_BYTES per CTA, 1 CTA per SM).
-int disco_b200_max_active_clusters(int cluster_size, int* clusters) {
-  CUDA_TRY(cudaFuncSetAttribute(cluster_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
-  CUDA_TRY(cudaFuncSetAttribute(cluster_probe_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(cluster_size * 64));
-  cfg.blockDim = dim3(NUM_THREADS_XF);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = unsigned(cluster_size);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CUDA_TRY(cudaOccupancyMaxActiveClusters(clusters, (void*)cluster_probe_kernel, &cfg));
-  return DISCO_OK;
-}
 
 int64_t disco_b200_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 

@@ -35,6 +35,7 @@ import torch.distributed as dist
 from .errors import CollectiveContractError, CollectiveTimeoutError
 
 DEFAULT_TIMEOUT = 300.0
+LOCKSTEP, CONCURRENT = "lockstep", "concurrent"  # reference scheduler names (fabric.py); ranks run as threads
 
 
 class ReduceOp(enum.Enum):

@@ -31,6 +31,7 @@ Dataflow of ``disco_step`` on rank n (b = B/N):
 """
 
 from dataclasses import dataclass
+import os
 import threading
 
 import numpy as np
@@ -152,8 +153,12 @@ class Plan:
         self._gather_stream = None
         self._h2d_stream = None
         self._wave_stream = None
+        self._pack_stream = None
         self._peer = None
         self._peer_group = None
+        self.last_event = None   # end of the last enqueued use (cross-stream ordering, _enter)
+        self.last_stream = None
+        self.used = 0
 
     def peer_window(self, endpoint) -> "_peer.PeerWindow":
         """This rank's peer-transport window (created, and exchanged with the peers, on first use)."""
@@ -183,6 +188,12 @@ class Plan:
             self._copy_stream = torch.cuda.Stream(self.device)
         return self._copy_stream
 
+    def pack_stream(self) -> "torch.cuda.Stream":
+        """Stream of the wavefront forward's per-chunk packs (all in order on one stream)."""
+        if self._pack_stream is None:
+            self._pack_stream = torch.cuda.Stream(self.device)
+        return self._pack_stream
+
     def h2d_streams(self):
         """(host->device copy stream, extra compute streams) of the wavefront forward: waves
         rotate over the current stream and these, so a wave's tail overlaps the next ones."""
@@ -196,24 +207,72 @@ class Plan:
         return (self.ptr, self.B, self.D, self.world, self.rank)
 
 
+# Plans are cached per (geometry, device, workspace size) -- not per thread, so fresh rank threads
+# (run_ranks, a user's verify loop) reuse the workspace of the same rank/geometry.  The workspace
+# size is part of the key because it follows the geometry the library computes right now.  The
+# cache is bounded in bytes (least recently used plans are released first) and a plan used from
+# a different stream than its last user first waits for that user's work (``_enter``).
 _plans = {}
 _plans_lock = threading.Lock()
+_plan_clock = [0]
+
+
+def _cache_cap(device: torch.device) -> int:
+    env = os.environ.get("DISCO_PLAN_CACHE_BYTES")
+    if env:
+        return int(float(env))
+    return int(0.6 * torch.cuda.get_device_properties(device).total_memory)
+
+
+def _release(plan: Plan) -> None:
+    if plan.last_event is not None:
+        plan.last_event.synchronize()
+    plan.close()
 
 
 def get_plan(B: int, D: int, world: int, rank: int, device: torch.device) -> Plan:
-    key = (B, D, world, rank, device.index, threading.get_ident())
+    nbytes = _lib.workspace_bytes(B, D, world, rank)
+    key = (B, D, world, rank, device.index, nbytes)
     with _plans_lock:
+        _plan_clock[0] += 1
         plan = _plans.get(key)
         if plan is None:
+            cap = _cache_cap(device)
+            held = sum(p.ws.numel() for k, p in _plans.items() if k[4] == device.index)
+            for k in sorted((k for k in _plans if k[4] == device.index), key=lambda k: _plans[k].used):
+                if held + nbytes <= cap:
+                    break
+                victim = _plans.pop(k)
+                held -= victim.ws.numel()
+                _release(victim)
             plan = _plans[key] = Plan(B, D, world, rank, device)
+        plan.used = _plan_clock[0]
         return plan
+
+
+def cached_plans() -> int:
+    """Number of cached workspaces (tests: the cache must not grow with rank threads)."""
+    with _plans_lock:
+        return len(_plans)
 
 
 def clear_plans() -> None:
     with _plans_lock:
         for plan in _plans.values():
-            plan.close()
+            _release(plan)
         _plans.clear()
+
+
+def _enter(plan: Plan, stream) -> None:
+    """Order this use of the plan's workspace after its previous user's work on another stream."""
+    if plan.last_event is not None and plan.last_stream != stream.cuda_stream:
+        stream.wait_event(plan.last_event)
+
+
+def _leave(plan: Plan, stream) -> None:
+    ev = torch.cuda.Event()
+    ev.record(stream)
+    plan.last_event, plan.last_stream = ev, stream.cuda_stream
 
 
 # ---------------------------------------------------------------------------
@@ -352,7 +411,9 @@ def local_loss_and_grads(layout: ShardLayout, I_gathered, T_gathered, t: float, 
     N, B, D, n = layout.world_size, layout.global_batch, Ig.shape[1], layout.rank
     b = layout.local_batch
     plan = get_plan(B, D, N, n, device)
-    st = _stream_ptr(device)
+    cur_stream = torch.cuda.current_stream(device)
+    _enter(plan, cur_stream)
+    st = cur_stream.cuda_stream
     code = _TORCH_DTYPE_CODE[Ig.dtype]
     if Tg.dtype != Ig.dtype:
         Tg = Tg.to(Ig.dtype)
@@ -372,6 +433,7 @@ def local_loss_and_grads(layout: ShardLayout, I_gathered, T_gathered, t: float, 
     _lib.call("disco_b200_contribution", *plan.args, t, int(bool(flip_cross_rank_sign)),
               d_image.data_ptr(), d_text.data_ptr(), D, st)
     _lib.call("disco_b200_loss", *plan.args, 1, st)
+    _leave(plan, cur_stream)
     h_image, h_text = _unstage_async(d_image, origin), _unstage_async(d_text, origin)
     loss, flags = _read_status(plan)
     _raise_on_flags(flags)
@@ -449,6 +511,8 @@ def _pipelined_pack_forward(plan: Plan, I_host: torch.Tensor, T_host: torch.Tens
         s.wait_stream(cur)
     rows = b // plan.waves
     streams = (cur,) + side
+    pack = plan.pack_stream()
+    pack.wait_stream(cur)
     for k in range(plan.waves):  # enqueue copy k, then its wave, so wave 0 launches early
         sl = slice(k * rows, (k + 1) * rows)
         with torch.cuda.stream(h2d):
@@ -456,16 +520,21 @@ def _pipelined_pack_forward(plan: Plan, I_host: torch.Tensor, T_host: torch.Tens
             T_dev[sl].copy_(T_host[sl], non_blocking=True)
         landed = torch.cuda.Event()
         landed.record(h2d)
-        s = streams[k % len(streams)]
-        s.wait_event(landed)
+        # wave k reads the packed rows of chunks 0..k: every pack runs in order on ONE stream, so
+        # the event after pack k covers all earlier packs (waves rotate over three streams)
+        pack.wait_event(landed)
         _lib.call("disco_b200_pack_rows", *plan.args, I_dev.data_ptr(), T_dev.data_ptr(), D, D, code, 0,
-                  k * rows, (k + 1) * rows, s.cuda_stream)
+                  k * rows, (k + 1) * rows, pack.cuda_stream)
+        packed = torch.cuda.Event()
+        packed.record(pack)
+        s = streams[k % len(streams)]
+        s.wait_event(packed)
         _lib.call("disco_b200_forward_wave", *plan.args, t, k, s.cuda_stream)
-    for s in side:
+    for s in side + (pack,):
         cur.wait_stream(s)
     for x in (I_dev, T_dev):
         x.record_stream(h2d)
-        for s in side:
+        for s in side + (pack,):
             x.record_stream(s)
     _lib.call("disco_b200_forward_finish", *plan.args, cur.cuda_stream)
 
@@ -519,12 +588,15 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
     (wait on that stream, or call ``finish_status``, before reading them).
     """
     N, n = endpoint.world_size, endpoint.rank
+    _check_step_inputs(local_I, local_T)
     b, D = local_I.shape
     B = b * N
     on_host = not local_I.is_cuda
     device = _default_device() if on_host else local_I.device
     plan = get_plan(B, D, N, n, device)
-    st = _stream_ptr(device)
+    cur_stream = torch.cuda.current_stream(device)
+    _enter(plan, cur_stream)
+    st = cur_stream.cuda_stream
     pw = None  # peer window of this step (N > 1 with the peer transport)
     if on_host:
         if N != 1 or plan.waves == 0 or local_T.is_cuda:
@@ -604,7 +676,36 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         if N > 1:
             endpoint.all_gather_into(plan.ce_all, plan.ce)
         _lib.call("disco_b200_loss", *plan.args, 0, st)
+    _leave(plan, cur_stream)
     return d_image, d_text, plan
+
+
+def _check_step_inputs(local_I, local_T) -> None:
+    """What the kernels assume of ``disco_step_async``'s inputs (the checks ``disco_step`` gets
+    from ``_stage``): tensors, 2-D, equal shapes and dtypes, a supported dtype, unit column
+    stride with rows at least D apart, both on the same device.  Raises ShapeError / TypeError
+    before any launch, so a bad view cannot make a kernel read out of bounds."""
+    for x in (local_I, local_T):
+        if not isinstance(x, torch.Tensor):
+            raise TypeError(f"disco_step_async takes torch tensors, got {type(x)!r}")
+        if x.dim() != 2:
+            raise ShapeError(f"expected a 2-D matrix, got ndim={x.dim()}")
+    if tuple(local_I.shape) != tuple(local_T.shape):
+        raise ShapeError(
+            f"local feature shapes disagree: {tuple(local_I.shape)} vs {tuple(local_T.shape)}")
+    if local_I.dtype != local_T.dtype:
+        raise TypeError(f"feature dtypes disagree: {local_I.dtype} vs {local_T.dtype}")
+    if local_I.dtype not in _TORCH_DTYPE_CODE:
+        raise TypeError(f"unsupported feature dtype {local_I.dtype} (f32, bf16, f16, f64)")
+    if local_I.device != local_T.device:
+        raise ValueError(f"features on different devices: {local_I.device} vs {local_T.device}")
+    if local_I.shape[0] == 0 or local_I.shape[1] == 0:
+        raise ShapeError(f"empty feature matrix {tuple(local_I.shape)}")
+    for x in (local_I, local_T):
+        if x.stride(1) != 1 or (x.shape[0] > 1 and x.stride(0) < x.shape[1]):
+            raise ShapeError(
+                f"features need unit column stride and row stride >= D (got strides {tuple(x.stride())}); "
+                "pass .contiguous()")
 
 
 def finish_status(plan: Plan) -> float:

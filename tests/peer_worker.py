@@ -1,8 +1,12 @@
-"""One rank of tests/test_gpu_peer.py::test_peer_two_processes_ipc (not collected by pytest).
+"""One rank of the two-process tests in tests/test_gpu_peer.py (not collected by pytest).
 
-Both ranks share cuda:0; the process group is gloo (host plumbing: the feature all_gather and
-the per-row loss all_gather are staged through host memory), the gradient exchange is the peer
-transport over CUDA IPC-mapped windows.  Two steps, so both parity windows are used.
+Both ranks share cuda:0; the process group is gloo.  argv[2] selects the exchange:
+  peer  -- the gradient exchange is the peer transport over CUDA IPC-mapped windows;
+  nccl  -- DISCO_PEER=0: the exchange the NCCL path runs (ProcessGroupEndpoint.all_gather_into,
+           all_to_all_into, the per-row ce all_gather) with the real device kernels, the
+           collectives staged through host memory (gloo cannot move CUDA tensors; two ranks on
+           one GPU cannot form an NCCL communicator).
+Two steps, so both parity windows are used.
 """
 import os
 import sys
@@ -15,11 +19,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2304_08480_b200 as P  # noqa: E402
 
 
-def main(out_dir):
+def main(out_dir, mode="peer"):
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    ep = P.ProcessGroupEndpoint(peer=True)
+    ep = P.ProcessGroupEndpoint(peer=(mode == "peer"))
     I = np.load(os.path.join(out_dir, "I.npy"))
     T = np.load(os.path.join(out_dir, "T.npy"))
     b = I.shape[0] // world
@@ -38,4 +42,4 @@ def main(out_dir):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "peer")

@@ -38,6 +38,15 @@ def test_every_header_symbol_is_exported_and_bound():
     assert set(_lib.SIGNATURES) == set(syms)
 
 
+def test_every_export_is_declared_in_the_header():
+    """export -> header: the library exports no disco_b200_* entry point the header does not declare."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if line.split() and line.split()[-1].startswith("disco_b200_")}
+    assert exported, "no disco_b200_* exports found"
+    assert exported == set(declared_symbols()), exported ^ set(declared_symbols())
+
+
 def test_layout_validation_matches_shard_layout():
     # ShardLayout rules (shard.py:38-49) enforced by the C side too
     with pytest.raises(LayoutError, match="not divisible"):

@@ -112,22 +112,25 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("streamed", ["0", "1"])
-def test_peer_two_processes_ipc(tmp_path, streamed):
-    """Two processes, one GPU, gloo + CUDA IPC windows: bitwise equal to N = 1, with the kernel
-    all-gather and (small B, where the shared GPU's time slicing lets both ranks publish before
-    either spins for long) the streamed copy-engine all-gather."""
+@pytest.mark.parametrize("mode,streamed", [("peer", "0"), ("peer", "1"), ("nccl", "0")])
+def test_peer_two_processes_ipc(tmp_path, mode, streamed):
+    """Two processes, one GPU, gloo: bitwise equal to N = 1.  ``peer``: CUDA IPC windows, with the
+    kernel all-gather and (small B, where the shared GPU's time slicing lets both ranks publish
+    before either spins for long) the streamed copy-engine all-gather.  ``nccl``: DISCO_PEER=0, the
+    ProcessGroupEndpoint all_gather / all_to_all exchange (shard.py:190-205 replaced by
+    fabric.py all_gather_into + all_to_all_into) driving the real kernels, host-staged."""
     B, D = 2048, 256
     I, T = O.synthetic_features(B, D, 11)
     np.save(tmp_path / "I.npy", I.astype(np.float32))
     np.save(tmp_path / "T.npy", T.astype(np.float32))
     port = _free_port()
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2",
-               DISCO_PEER_STREAMED=streamed, DISCO_PEER_TIMEOUT="30")
+               DISCO_PEER_STREAMED=streamed, DISCO_PEER_TIMEOUT="30", DISCO_PEER="0" if mode == "nccl" else "1")
     procs = []
     for r in range(2):
         e = dict(env, RANK=str(r))
-        procs.append(subprocess.Popen([sys.executable, os.path.join(HERE, "peer_worker.py"), str(tmp_path)], env=e))
+        procs.append(subprocess.Popen([sys.executable, os.path.join(HERE, "peer_worker.py"), str(tmp_path), mode],
+                                      env=e))
     rcs = []
     for p in procs:
         try:

@@ -123,3 +123,16 @@ def test_dlogit_scale_euler_identity():
     t = 10.0
     di, dt, _ = O.clip_grad_full(I, T, t)
     assert abs(O.dlogit_scale_full(I, T, t) - ((di * I).sum() + (dt * T).sum()) / (2 * t)) < 1e-12
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_blocked_timing_port_equals_the_oracle_step(world):
+    """oracle.disco_step_blocked (the CPU baseline's timing kernel) computes the same step as
+    disco_step_all (itself pinned to the reference above), for any blocking and thread count."""
+    I, T = O.synthetic_features(64, 8, 3)
+    ref = O.disco_step_all(I, T, world, 10.0)
+    for rows, workers in ((5, 3), (64, 1), (7, 8)):
+        got = O.disco_step_blocked(I, T, world, 10.0, rows_per_block=rows, workers=workers)
+        assert O.max_rel_error(got[0], ref[0]) < 1e-12
+        assert O.max_rel_error(got[1], ref[1]) < 1e-12
+        assert abs(got[2] - ref[2]) < 1e-12 * abs(ref[2])
