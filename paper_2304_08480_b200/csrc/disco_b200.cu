@@ -53,6 +53,15 @@
 
 namespace disco {
 
+// Profiling experiments and ablations (DISCO_DEBUG_FLAGS bits, the symmetric single-rank forward,
+// the A-resident forward ring) exist only in builds with -DDISCO_EXPERIMENTS=1
+// (python -m paper_2304_08480_b200.build --out ... -D DISCO_EXPERIMENTS=1; tools/ab_kernels.py).
+// The default library compiles none of their checks into the kernels.
+#ifndef DISCO_EXPERIMENTS
+#define DISCO_EXPERIMENTS 0
+#endif
+constexpr bool XP = DISCO_EXPERIMENTS != 0;
+
 // ------------------------------------------------------------------ tiling
 constexpr int BM = 128;      // rows per CTA (the pair covers 256)
 constexpr int BN = 256;      // accumulator columns (each CTA loads 128 of the B operand rows)
@@ -285,11 +294,12 @@ __device__ __forceinline__ uint8_t* smem_base(uint8_t* raw) {
 // Successive K=16 steps advance the descriptor start address by 32 B (K-major) or 2 KiB
 // (MN-major), i.e. by 2 or 128 in the descriptor's 16-byte units.
 template <int NB, bool XF = false, int RS = Ring<NB>::STAGES, int NA = 1>
-__device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>& pipe, int nk,
-                                         uint32_t d_tmem, uint32_t idesc, int a_mn, int b_mn) {
+__device__ __forceinline__ void mma_blocks(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>& pipe, int nk, int kb0,
+                                           uint32_t d_tmem, uint32_t idesc, int a_mn, int b_mn, int j_lo, int j_hi,
+                                           bool wait, bool release) {
   const uint64_t a_step = a_mn ? 128 : 2, b_step = b_mn ? 128 : 2;
   for (int kb = 0; kb < nk; ++kb) {
-    ptx::mbar_wait(XF ? &ctl->xfull[pipe.stage] : &ctl->full[pipe.stage], pipe.phase);
+    if (wait) ptx::mbar_wait(XF ? &ctl->xfull[pipe.stage] : &ctl->full[pipe.stage], pipe.phase);
     ptx::tc_fence_after();
     const uint32_t a_base = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES);
     const uint32_t b_base = a_base + NA * A_STAGE_BYTES;
@@ -302,13 +312,20 @@ __device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>&
       for (int kk = 0; kk < BK / 16; ++kk) {
 #pragma unroll
         for (int j = 0; j < NB; ++j)
-          ptx::umma_f16_pair(d_tmem + j * BN, ad0 + kk * a_step, bd0[j] + kk * b_step, idesc, (kb | kk) != 0);
+          if (j >= j_lo && j < j_hi)
+            ptx::umma_f16_pair(d_tmem + j * BN, ad0 + kk * a_step, bd0[j] + kk * b_step, idesc, ((kb0 + kb) | kk) != 0);
       }
-      ptx::umma_commit_pair(&ctl->empty[pipe.stage], 0x3);  // both CTAs' smem slots free
+      if (release) ptx::umma_commit_pair(&ctl->empty[pipe.stage], 0x3);  // both CTAs' smem slots free
     }
     __syncwarp();
     pipe.advance();
   }
+}
+
+template <int NB, bool XF = false, int RS = Ring<NB>::STAGES, int NA = 1>
+__device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>& pipe, int nk,
+                                         uint32_t d_tmem, uint32_t idesc, int a_mn, int b_mn) {
+  mma_blocks<NB, XF, RS, NA>(ctl, tiles, pipe, nk, 0, d_tmem, idesc, a_mn, b_mn, 0, NB, true, true);
 }
 
 // Producer side of one k-block: wait for the slot, arm the leader's barrier, load.
@@ -395,7 +412,11 @@ __device__ __forceinline__ void st_transposed_64(uint8_t* tile, int lane, const 
 
 // Clock probe: CTA 0, thread 0 records {clock64, globaltimer} at slot [at, at + 1].
 __device__ __forceinline__ void probe_mark(unsigned long long* probe, int at) {
-  if (probe && blockIdx.x == 0 && threadIdx.x == 0) {
+  // ctaid / tid re-read (volatile) so the entry and exit marks share no live predicate (it spilled)
+  unsigned bid, tid;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(bid));
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+  if (probe && bid == 0 && tid == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     probe[at] = clock64();
@@ -403,7 +424,7 @@ __device__ __forceinline__ void probe_mark(unsigned long long* probe, int at) {
   }
 }
 
-__device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane) {
+__device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane, int epi_warps = NUM_EPI_WARPS) {
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {  // the NB=2 ring uses the first Ring<2>::STAGES
       ptx::mbar_init(&ctl->full[s], 1);
@@ -411,7 +432,7 @@ __device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&ctl->tfull[i], 1);
-      ptx::mbar_init(&ctl->tempty[i], 2 * NUM_EPI_WARPS);  // every epilogue warp of both CTAs
+      ptx::mbar_init(&ctl->tempty[i], 2 * epi_warps);  // every epilogue warp of both CTAs
     }
     for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&ctl->xfull[s], 2 * NUM_XF_WARPS);
     for (int s = 0; s < ARES_SLICES; ++s) {
@@ -474,16 +495,67 @@ constexpr int SYM_STAGES = 5;
 constexpr int SYM_EBUFS = 3;
 static_assert(SYM_STAGES * STAGE_BYTES + NUM_EPI_WARPS * (SYM_EBUFS * STAGING_TILE / 2 + 256) <=
                   TILE_RING_BYTES + STAGING_BYTES, "SYM smem layout");
+#ifndef DISCO_FWD_STAGES
+#define DISCO_FWD_STAGES 6
+#endif
+#ifndef DISCO_FWDE_WARPS
+#define DISCO_FWDE_WARPS 8
+#endif
+#ifndef DISCO_FWD_EBUFS
+#define DISCO_FWD_EBUFS 2
+#endif
+constexpr int FWD_STAGES = DISCO_FWD_STAGES;  // forward operand ring stages (32 KiB each)
+constexpr int FWD_EBUFS = DISCO_FWD_EBUFS;    // forward E staging half-buffers per epilogue warp (2 KiB each)
+static_assert(FWD_STAGES * STAGE_BYTES + NUM_EPI_WARPS * FWD_EBUFS * (STAGING_TILE / 2) <= TILE_RING_BYTES + STAGING_BYTES,
+              "forward smem layout");
+// FWDE epilogue width: 16 warps (4 per SM sub-partition, each draining a 64-column quarter of the
+// 256-column accumulator) instead of 8 (128-column halves).  The E epilogue is latency-bound
+// (dependent FFMA -> MUFU -> FADD chains, TMEM loads, staging), so twice the warps per scheduler
+// keep the MUFU and FMA pipes fed while the MMA of the next tile runs.  Costs one operand stage
+// (5 x 32 KiB ring, measured neutral) for the 16 warps' staging buffers.
+#ifndef DISCO_FWDE_PACKED
+#define DISCO_FWDE_PACKED 0
+#endif
+constexpr int FWDE_EPI = DISCO_FWDE_WARPS;
+// y = S t log2(e) - m_g and the running sums as packed FP32 pairs (FFMA2 / FADD2) or scalar
+__device__ __forceinline__ float2 fwde_y(float a, float b, float2 tl2, float2 nmg) {
+#if DISCO_FWDE_PACKED
+  return ptx::ffma2(make_float2(a, b), tl2, nmg);
+#else
+  return make_float2(fmaf(a, tl2.x, nmg.x), fmaf(b, tl2.y, nmg.y));
+#endif
+}
+__device__ __forceinline__ float2 fwde_acc(float2 s, float e0, float e1) {
+#if DISCO_FWDE_PACKED
+  return ptx::fadd2(s, make_float2(e0, e1));
+#else
+  return make_float2(s.x + e0, s.y + e1);
+#endif
+}
+constexpr int FWDE_STAGES = FWDE_EPI == 16 ? 5 : FWD_STAGES;
+static_assert(FWDE_EPI == 8 || FWDE_EPI == 16, "FWDE epilogue warps");
+static_assert(FWDE_STAGES * STAGE_BYTES + FWDE_EPI * FWD_EBUFS * (STAGING_TILE / 2) <= TILE_RING_BYTES + STAGING_BYTES,
+              "FWDE smem layout");
+template <int KIND, bool ARES, bool SYM>
+__host__ __device__ constexpr int logits_epi() { return (KIND == KIND_FWDE && !SYM && !ARES) ? FWDE_EPI : NUM_EPI_WARPS; }
+template <int KIND, bool ARES, bool SYM>
+__host__ __device__ constexpr int logits_threads() { return 64 + 32 * logits_epi<KIND, ARES, SYM>(); }
+// statistics parts per (row, sub-chunk) the FWDE / FWD kernels write: one per epilogue column part
+constexpr int FWDE_PARTS = FWDE_EPI / 4;
+
 template <int KIND, bool ARES, bool SYM = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND, ARES, SYM>(), 1)
     logits_kernel(const __grid_constant__ LogitsParams p) {
   static_assert(!SYM || (KIND == KIND_FWDE && !ARES), "SYM is a FWDE variant");
-  constexpr int LRS = SYM ? SYM_STAGES : Ring<1>::STAGES;  // operand ring stages
-  constexpr int EBUFS = SYM ? SYM_EBUFS : 2;                // E staging half-buffers per warp
+  constexpr int EPI = logits_epi<KIND, ARES, SYM>();    // epilogue warps
+  constexpr int NPARTS = EPI / 4;                        // column parts of a 256-column tile
+  constexpr int PART_COLS = BN / NPARTS;                 // columns per epilogue warp and tile
+  constexpr int LRS = SYM ? SYM_STAGES : (EPI == 16 ? FWDE_STAGES : FWD_STAGES);  // operand ring stages
+  constexpr int EBUFS = SYM ? SYM_EBUFS : FWD_EBUFS;   // E staging half-buffers per warp
   constexpr int NDIR = SYM ? 1 : 2;                         // directions walked by the units
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
-  uint8_t* staging = tiles + LRS * STAGE_BYTES;
+  uint8_t* staging = tiles + (ARES ? TILE_RING_BYTES : LRS * STAGE_BYTES);
   float* xbuf = reinterpret_cast<float*>(staging + NUM_EPI_WARPS * EBUFS * (STAGING_TILE / 2));  // SYM: [8][64]
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + TILE_RING_BYTES + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -498,7 +570,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   }
   probe_mark(p.probe, 0);
-  kernel_prologue(ctl, warp, lane);
+  kernel_prologue(ctl, warp, lane, EPI);
 
   constexpr bool CHUNK_UNITS = KIND != KIND_GRAD;  // unit = all tiles of one column chunk
   const int wave = CHUNK_UNITS ? p.wave : -1;
@@ -691,10 +763,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else {  // ---------------------------- epilogue warps 2..9
+  } else {  // ---------------------------- epilogue warps 2..(EPI + 1)
     const int ew = warp - 2;
-    const int quad = warp & 3;
-    const int chalf = ew >> 2;  // column half of the 256-wide tile
+    const int quad = warp & 3;   // TMEM lane quadrant (fixed by the warp's position in its warpgroup)
+    const int cpart = ew >> 2;   // column part of the 256-wide tile (PART_COLS columns)
     const int r_in_tile = crank * BM + quad * 32 + lane;
     uint8_t* tile = staging + ew * EBUFS * (STAGING_TILE / 2);
     uint32_t it = 0, gslice = 0;
@@ -706,7 +778,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (epend_rb < (epend_dir && SYM ? p.B : p.b) && !(p.debug_flags & 1))  // bit0 ablation: skip E stores
+        if (epend_rb < (epend_dir && SYM ? p.B : p.b))
           ptx::tma_store_4d(&p.e_map[epend_dir], tile + epend_buf * (STAGING_TILE / 2), epend_cb & 127,
                             epend_rb & 127, epend_cb >> 7, epend_rb >> 7);
         ptx::bulk_commit();
@@ -749,11 +821,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t buf = it & 1, use = it >> 1;
         ptx::mbar_wait(&ctl->tfull[buf], use & 1);
         ptx::tc_fence_after();
-        const int col0 = chunk_lo + (t0 + ti) * BN + chalf * (BN / 2);
-        const uint32_t taddr = ctl->tmem_base + (uint32_t(quad * 32) << 16) + buf * BN + chalf * (BN / 2);
+        const int col0 = chunk_lo + (t0 + ti) * BN + cpart * PART_COLS;
+        const uint32_t taddr = ctl->tmem_base + (uint32_t(quad * 32) << 16) + buf * BN + cpart * PART_COLS;
         if (KIND == KIND_FWD) {
 #pragma unroll 1
-          for (int j = 0; j < BN / 64; ++j) {
+          for (int j = 0; j < PART_COLS / 32; ++j) {
             const int cb = col0 + j * 32;
             if (cb >= chunk_hi) break;  // warp-uniform
             float v[32];
@@ -798,34 +870,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
           }
         } else if (KIND == KIND_FWDE) {
-          // canonical chunks: this warp's 128 columns are entirely inside or past the chunk.
-          // One TMEM pass (TMEM reads are 64 B/clk/SM: a second pass would pace the tile at the
-          // MMA time): each 64-column group is loaded once, its max taken in registers, then
-          // E = exp2(y - m_g) packed to f16 and stored as one 32 x 64 slice.
-          if (col0 < chunk_hi && (p.debug_flags & 512)) {  // ablation: drain TMEM only
-            float va[32];
-#pragma unroll 1
-            for (int j = 0; j < 4; ++j) {
-              ptx::tmem_ld32(taddr + j * 32, va);
-              if (va[0] == 12345.678f) asm volatile("trap;");
-            }
-          } else if (col0 < chunk_hi) {  // warp-uniform
-            const int li = label - col0;  // label column relative to this warp's 128 columns
+          // canonical chunks: this warp's PART_COLS columns are entirely inside or past the chunk.
+          // One TMEM pass (a second pass would pace the tile at the TMEM read rate): each
+          // 64-column group is loaded once (both 32-column halves under one tcgen05.wait::ld), its
+          // max taken in registers, then E = exp2(y - m_g) packed to f16 and stored as two 32 x 32
+          // half slices.  y = S t log2(e) - m_g and the two running sums use packed FP32 pairs
+          // (FFMA2 / FADD2: bit-identical to the scalar fmaf / add, half the issue slots).
+          constexpr int NJ = PART_COLS / 64;
+          if (col0 < chunk_hi) {  // warp-uniform
+            const int li = label - col0;  // label column relative to this warp's columns
+            const float2 tl2 = make_float2(p.tl2e, p.tl2e);
             uint32_t ra[32], rb[32];  // both halves of a slice under one tcgen05.wait::ld
             ptx::tmem_ld32_async(taddr, ra);
             ptx::tmem_ld32_async(taddr + 32, rb);
             ptx::tmem_wait_ld_dep(ra, rb);
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
+            for (int j = 0; j < NJ; ++j) {
               float va[32], vb[32];
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 va[i] = __uint_as_float(ra[i]);
                 vb[i] = __uint_as_float(rb[i]);
               }
-              if (j == 0 && !SYM) {  // slice 1's TMEM loads fly while slice 0 is computed
-                ptx::tmem_ld32_async(taddr + 64, ra);
-                ptx::tmem_ld32_async(taddr + 96, rb);
+              if (j + 1 < NJ && !SYM) {  // the next slice's TMEM loads fly while this one is computed
+                ptx::tmem_ld32_async(taddr + 64 * (j + 1), ra);
+                ptx::tmem_ld32_async(taddr + 64 * (j + 1) + 32, rb);
               }
               float mx[32];  // max over the 64 columns as a depth-6 tree
 #pragma unroll
@@ -836,29 +905,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 for (int i = 0; i < w; ++i) mx[i] = fmaxf(mx[i], mx[i + w]);
               const float cm = mx[0];
               const float mg = cm * p.tl2e;
-              float s0 = 0.f, s1 = 0.f;
+              const float2 nmg = make_float2(-mg, -mg);
+              float2 s2 = make_float2(0.f, 0.f);  // (even-column sum, odd-column sum)
               uint32_t h[32];
 #pragma unroll
               for (int half = 0; half < 2; ++half) {
                 const float* v = half ? vb : va;
                 const int lg = li - (j * 64 + half * 32);
-                if (unsigned(lg) >= 32u) {  // warp-uniform: labels of a warp's 32 rows share a 32-column group
+                if (unsigned(lg) >= 32u) {  // warp-uniform: a warp's 32 labels share a 32-column group
 #pragma unroll
                   for (int i = 0; i < 32; i += 2) {
-                    const float e0 = ptx::ex2(fmaf(v[i], p.tl2e, -mg));
-                    const float e1 = ptx::ex2(fmaf(v[i + 1], p.tl2e, -mg));
-                    s0 += e0;
-                    s1 += e1;
+                    const float2 y = fwde_y(v[i], v[i + 1], tl2, nmg);
+                    const float e0 = ptx::ex2(y.x), e1 = ptx::ex2(y.y);
+                    s2 = fwde_acc(s2, e0, e1);
                     __half2 hh = __floats2half2_rn(e0, e1);
                     h[half * 16 + i / 2] = *reinterpret_cast<uint32_t*>(&hh);
                   }
-                } else {
+                } else {  // the label term stays out of the sum (adding +0 leaves it unchanged)
 #pragma unroll
                   for (int i = 0; i < 32; i += 2) {
-                    const float e0 = ptx::ex2(fmaf(v[i], p.tl2e, -mg));
-                    const float e1 = ptx::ex2(fmaf(v[i + 1], p.tl2e, -mg));
-                    if (i == lg) yt = v[i] * p.tl2e; else s0 += e0;
-                    if (i + 1 == lg) yt = v[i + 1] * p.tl2e; else s1 += e1;
+                    const float2 y = fwde_y(v[i], v[i + 1], tl2, nmg);
+                    const float e0 = ptx::ex2(y.x), e1 = ptx::ex2(y.y);
+                    if (i == lg) yt = v[i] * p.tl2e;
+                    if (i + 1 == lg) yt = v[i + 1] * p.tl2e;
+                    s2 = fwde_acc(s2, i == lg ? 0.f : e0, i + 1 == lg ? 0.f : e1);
                     __half2 hh = __floats2half2_rn(e0, e1);
                     h[half * 16 + i / 2] = *reinterpret_cast<uint32_t*>(&hh);
                   }
@@ -868,10 +938,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 // previous half, written one compute phase ago, is fenced and TMA-stored first, so
                 // neither the STS -> fence.proxy.async latency nor the TMA read is exposed.
                 const int rbase = rt * PAIR_M + crank * BM + quad * 32;
-                if (p.debug_flags & 131072) {  // bit17 ablation: E math only (no STS, no store)
-                  if (h[half * 16] == 0x7fff1234u) asm volatile("trap;");
-                  continue;
-                }
                 const int hcb = col0 + j * 64 + half * 32;
                 e_push([&](uint8_t* hb) { ptx::st_swizzled_row64(hb, lane, h + half * 16); }, hcb, rbase, dir);
                 if constexpr (SYM) {
@@ -916,13 +982,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               }
               const int cb = col0 + j * 64;
               const float mnew = fmaxf(m2, mg);
-              l = l * ptx::ex2(m2 - mnew) + (s0 + s1) * ptx::ex2(mg - mnew);
+              l = l * ptx::ex2(m2 - mnew) + (s2.x + s2.y) * ptx::ex2(mg - mnew);
               m2 = mnew;
               if (row_ok) p.mg[(int64_t(dir) * p.groups + cb / GROUP_COLS) * p.b + row] = mg;
-              if (j == 0) {
+              if (j + 1 < NJ) {
                 if (SYM) {  // registers: SYM loads slice 1 only after slice 0 (168-register cap)
-                  ptx::tmem_ld32_async(taddr + 64, ra);
-                  ptx::tmem_ld32_async(taddr + 96, rb);
+                  ptx::tmem_ld32_async(taddr + 64 * (j + 1), ra);
+                  ptx::tmem_ld32_async(taddr + 64 * (j + 1) + 32, rb);
                 }
                 ptx::tmem_wait_ld_dep(ra, rb);
               }
@@ -932,7 +998,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           // G = exp2(y - lse2) (label column: P_label - 1), f16, 64-column slices
           // transposed through swizzled smem and written as full 128-byte rows.
 #pragma unroll 1
-          for (int j = 0; j < BN / 128; ++j) {
+          for (int j = 0; j < PART_COLS / 64; ++j) {
             const int cb = col0 + j * 64;
             if (cb >= chunk_hi) break;  // warp-uniform
             uint32_t h[32];
@@ -997,7 +1063,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         release_accumulator(ctl, buf, lane);
       }
       if (KIND != KIND_GRAD && row_ok) {
-        p.stats[((int64_t(dir) * p.nchunk + ch) * 2 + chalf) * p.b + row] = make_float2(m2, l);
+        p.stats[((int64_t(dir) * p.nchunk + ch) * NPARTS + cpart) * p.b + row] = make_float2(m2, l);
         if (has_t) {
           p.target[dir * p.b + row] = yt;
           if (SYM) p.target[p.b + row] = yt;  // S_1[r, r] = S_0[r, r]
@@ -1131,10 +1197,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
         if constexpr (NB == 2) {  // wide unit: both accumulators, one pass over K
           int k0, nk;
           k_range(q, kc, k0, nk);
-          ptx::mbar_wait(&ctl->tempty[0], ((it >> 1) & 1) ^ 1);
-          ptx::mbar_wait(&ctl->tempty[1], ((it >> 1) & 1) ^ 1);
-          ptx::tc_fence_after();
-          mma_tile<NB, XF, RS, NA>(ctl, tiles, pipe, nk, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major);
+          const uint32_t ph = ((it >> 1) & 1) ^ 1;
+          if (HF) {
+            ptx::mbar_wait(&ctl->tempty[0], ph);
+            ptx::mbar_wait(&ctl->tempty[1], ph);
+            ptx::tc_fence_after();
+            mma_tile<NB, XF, RS, NA>(ctl, tiles, pipe, nk, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major);
+          } else {
+            // The epilogue releases accumulator 0 half-way through its drain: issue the unit's first
+            // ring-full of k-blocks into accumulator 0 alone (the stages stay resident), then, once
+            // accumulator 1 is free, the same stages into accumulator 1, releasing them, then the rest
+            // of K into both.  Each accumulator still sums its k-blocks in the same order.
+            const int pre = nk < RS ? nk : RS;
+            ptx::mbar_wait(&ctl->tempty[0], ph);
+            Pipe<RS> first = pipe;
+            mma_blocks<NB, XF, RS, NA>(ctl, tiles, first, pre, 0, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major,
+                                       0, 1, true, false);
+            ptx::mbar_wait(&ctl->tempty[1], ph);
+            mma_blocks<NB, XF, RS, NA>(ctl, tiles, pipe, pre, 0, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major,
+                                       1, 2, false, true);
+            mma_blocks<NB, XF, RS, NA>(ctl, tiles, pipe, nk - pre, pre, ctl->tmem_base, idesc, q.a_mn_major,
+                                       q.b_mn_major, 0, 2, true, true);
+          }
           if (ptx::elect_one()) {
             ptx::umma_commit_pair(&ctl->tfull[0], 0x3);
             ptx::umma_commit_pair(&ctl->tfull[1], 0x3);
@@ -1186,7 +1270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       for (int kb = 0; kb < nk; ++kb) {
         const int k = k0 + kb * BK;
         ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
-        if (!(q.ablate & 1024)) {
+        if (!(XP && (q.ablate & 1024))) {
           const uint32_t abase = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES);
           const uint32_t a2base = abase + A_STAGE_BYTES;
           // the stage's factors (bulk-copied by the producer with the tiles)
@@ -1286,7 +1370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             const __half sc = sq[r];
             sq[r] = ld_scale(kb + XPF);
             ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
-            if (active && !(q.ablate & 1024)) {
+            if (active && !(XP && (q.ablate & 1024))) {
               uint8_t* rowp = tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES + rowoff;
               int lab_rel;
               float glab;
@@ -1338,8 +1422,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
         orow = q.out + kc * q.chunk_stride + (row / q.row_div) * q.stride_hi + (row % q.row_div) * q.ld_out;
       const int z = int(row0 / q.row_div) + kc;
       const int rlo = int(row0 % q.row_div);
+      if (NB == 2 && !HF && q.tma_store == 1 && !(XP && (q.skip_store || q.ablate))) {
+        // Wide drain, software-pipelined: slice jj + 1's TMEM load is in flight while slice jj is
+        // staged and TMA-stored, and accumulator 0 is released as soon as its last slice sits in
+        // registers, so the MMA starts the next unit (accumulator 0 half) during this drain.
+        uint32_t ra[32], rb[32];
+        auto taddr_of = [&](int jj) { return (jj < 4 ? ta0 : ta1) + (jj & 3) * 32; };
+        auto stage_store = [&](const uint32_t (&w)[32], int jj) {
+          const int c0 = cbase + (jj >> 2) * BN + (jj & 3) * 32;
+          if (c0 >= q.N) return;  // warp-uniform
+          if (lane == 0) ptx::bulk_wait_read<STAGING_BUFS - 1>();
+          __syncwarp();
+          ptx::st_swizzled_row(tile, lane, w);
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (q.peer) {  // NVLink push: this slice belongs to rank row0 / b
+              const int dest = row0 / q.peer_b;
+              if (row0 < q.M) ptx::tma_store_3d(&q.peer_map[dest], tile, c0, row0 - dest * q.peer_b, kc);
+            } else if (row0 < q.M) {
+              ptx::tma_store_3d(&q.out_map, tile, c0, rlo, z);
+            }
+            ptx::bulk_commit();
+          }
+        };
+        ptx::tmem_ld32_async(taddr_of(0), ra);
+        ptx::tmem_wait_ld_dep1(ra);
+#pragma unroll
+        for (int jj = 0; jj < 8; jj += 2) {
+          ptx::tmem_ld32_async(taddr_of(jj + 1), rb);
+          stage_store(ra, jj);
+          ptx::tmem_wait_ld_dep1(rb);
+          if (jj + 1 == 3) release_accumulator(ctl, buf0, lane);  // slices 0..3 (accumulator 0) are out
+          if (jj + 2 < 8) ptx::tmem_ld32_async(taddr_of(jj + 2), ra);
+          stage_store(rb, jj + 1);
+          if (jj + 2 < 8) ptx::tmem_wait_ld_dep1(ra);
+        }
+        release_accumulator(ctl, buf1, lane);
+        if (p.probe && ew == 0 && lane == 0 && leader) {
+          atomicAdd(p.probe + 4, (unsigned long long)(clock64() - drain_t0));
+          atomicAdd(p.probe + 5, 1ull);
+        }
+        it += 2;
+        continue;
+      }
 #pragma unroll 1
-      for (int jj = 0; jj < ((q.ablate & 2048) ? 0 : NB * (BN / 64)); ++jj) {
+      for (int jj = 0; jj < ((XP && (q.ablate & 2048)) ? 0 : NB * (BN / 64)); ++jj) {
         // NB = 2: slices 0..3 from accumulator 0 (columns [0,256)), 4..7 from accumulator 1
         const int j = jj % (BN / 64), acc = jj / (BN / 64);
         const int c0 = cbase + acc * BN + j * 32;
@@ -1352,9 +1480,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] += v1[i];
         }
-        if (q.skip_store) {
+        if (XP && q.skip_store) {
           if (v[0] == 12345.678f) asm volatile("trap;");  // keep the TMEM load live
-        } else if (q.tma_store == 2) {
+        } else if (XP && q.tma_store == 2) {
           // 32 x 32 fp32 slice transposed through swizzled smem, then written by the warp as
           // 128-byte row segments (4 rows per instruction); no async-proxy round trip.
           uint32_t w[32];
@@ -1380,7 +1508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           ptx::st_swizzled_row(stile, lane, w);
           ptx::fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0 && !(q.ablate & 32768)) {  // bit15 ablation: stage but never store
+          if (lane == 0 && !(XP && (q.ablate & 32768))) {  // bit15 ablation: stage but never store
             if (q.peer) {  // NVLink push: this slice belongs to rank row0 / b
               const int dest = row0 / q.peer_b;
               if (row0 < q.M) ptx::tma_store_3d(&q.peer_map[dest], stile, c0, row0 - dest * q.peer_b, kc);
@@ -1584,18 +1712,26 @@ __device__ __forceinline__ void finish_row(int i, float m, float lo, float yt, f
 }
 
 // ndir = 1: direction 0 only (the symmetric single-rank forward combines direction 1 separately).
-__global__ void stats_combine_kernel(const float2* stats, const float* target, int nchunk, int ssub, int b, int ndir,
-                                     float* lse2_out, float* glabel_out, float* ce_out, Status* status) {
+// Per (dir, row): the forward left one online (max, sum) per (sub-chunk, column part); combine
+// them in a fixed tree -- parts ((0 + 1) + (2 + 3)), sub-chunks, then the 8 canonical chunks
+// ((0 + 1) + (2 + 3)) + ((4 + 5) + (6 + 7)) -- a function of B only, never of N.
+__global__ void stats_combine_kernel(const float2* stats, const float* target, int nchunk, int ssub, int nparts,
+                                     int b, int ndir, float* lse2_out, float* glabel_out, float* ce_out,
+                                     Status* status) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ndir * b) return;
   const int dir = i / b, r = i % b;
   const int nsc = nchunk * ssub;
-  auto at = [&](int sc, int h) { return stats[((int64_t(dir) * nsc + sc) * 2 + h) * b + r]; };
+  auto at = [&](int sc, int h) { return stats[((int64_t(dir) * nsc + sc) * nparts + h) * b + r]; };
   float m = -INFINITY;
-  for (int sc = 0; sc < nsc; ++sc) m = fmaxf(m, fmaxf(at(sc, 0).x, at(sc, 1).x));
+  for (int sc = 0; sc < nsc; ++sc)
+    for (int h = 0; h < nparts; ++h) m = fmaxf(m, at(sc, h).x);
+  auto part = [&](int sc, int h) {
+    const float2 s = at(sc, h);
+    return s.y * ptx::ex2(s.x - m);
+  };
   auto sub_sum = [&](int sc) {
-    const float2 s0 = at(sc, 0), s1 = at(sc, 1);
-    return s0.y * ptx::ex2(s0.x - m) + s1.y * ptx::ex2(s1.x - m);
+    return nparts == 4 ? (part(sc, 0) + part(sc, 1)) + (part(sc, 2) + part(sc, 3)) : part(sc, 0) + part(sc, 1);
   };
   auto chunk_sum = [&](int c) {
     return ssub == 2 ? sub_sum(2 * c) + sub_sum(2 * c + 1) : sub_sum(c);
@@ -2097,7 +2233,7 @@ std::atomic<int> g_debug_bits{[] {
   const char* e = getenv("DISCO_DEBUG_FLAGS");
   return e ? atoi(e) : 0;
 }()};
-int debug_flag_bits() { return g_debug_bits.load(std::memory_order_relaxed); }
+int debug_flag_bits() { return XP ? g_debug_bits.load(std::memory_order_relaxed) : 0; }
 
 int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   if (world < 1) return fail(DISCO_LAYOUT_ERROR, "world size must be >= 1, got %d", world);
@@ -2138,14 +2274,14 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   g->ksplit = ((g->wide || g->wsplit) && B % 128 == 0 && B >= 4096) ? 2 : 1;
   static const bool no_estore = [] {  // DISCO_RECOMPUTE=1: A/B switch to the recompute (GRAD) path
     const char* e = getenv("DISCO_RECOMPUTE");
-    return e && atoi(e) != 0;
+    return XP && e && atoi(e) != 0;
   }();
   g->estore = (g->g_blocked && !no_estore) ? 1 : 0;
   // DISCO_SYMMETRIC=1 (read per call; experiment, off by default): the symmetric single-rank
   // forward.  Correct (tools/env_ab.py, test_symmetric_forward_vs_oracle) but measured slower: the
   // t2i column statistics cost ~2x the i2t epilogue in issue slots and MUFU, more than the halved
   // MMA saves.  Not bitwise equal to N > 1 (t2i sums in another order).
-  const char* sym_env = getenv("DISCO_SYMMETRIC");
+  const char* sym_env = XP ? getenv("DISCO_SYMMETRIC") : nullptr;
   g->sym = (world == 1 && g->estore && sym_env && atoi(sym_env) == 1) ? 1 : 0;
   // Fused single-rank backward (opt-in: DISCO_HFUSE=1, read per call).  At N = 1 every cross term
   // G_d'^T . C pairs with an intra term G_d . C over the same B x B block, so the transform warps
@@ -2163,7 +2299,7 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   len[DISCO_R_FEAT16] = 2 * B * Dp * 2;
   // + (N = 1, estore) the symmetric forward's dir-1 group sums [groups][B] f32 (allocated whether or
   // not DISCO_SYMMETRIC selects the path, so the workspace size does not depend on it)
-  len[DISCO_R_STATS] = 2 * int64_t(g->nchunk) * g->ssub * 2 * b * 8 +
+  len[DISCO_R_STATS] = 2 * int64_t(g->nchunk) * g->ssub * 4 * b * 8 +  // [2][sub-chunks][<= 4 parts][b] f32x2
                        (N == 1 && g->estore ? int64_t(g->groups) * B * 4 : 0);
   len[DISCO_R_ROWS] = 4 * 2 * b * 4;
   len[DISCO_R_CE] = 2 * b * 4;
@@ -2377,7 +2513,7 @@ int launch_logits_t(const LogitsParams& p, int64_t units, cudaStream_t st, const
   if ((rc = prepare_kernel(logits_kernel<KIND, ARES, SYM>))) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid_for(units));
-  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.blockDim = dim3(logits_threads<KIND, ARES, SYM>());
   cfg.dynamicSmemBytes = SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -2419,7 +2555,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   p.g_blocked = g.g_blocked;
   p.mg = region<float>(ws, g, DISCO_R_SCALE);
   p.groups = g.groups;
-  p.ssum = reinterpret_cast<float*>(p.stats + 2 * int64_t(g.nchunk) * g.ssub * 2 * g.b);
+  p.ssum = reinterpret_cast<float*>(p.stats + 2 * int64_t(g.nchunk) * g.ssub * 4 * g.b);
   p.wave = wave;
   p.epoch = epoch;
   p.timeout_ns = (unsigned long long)(timeout_s * 1e9);
@@ -2448,13 +2584,23 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
                                   : ndir * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
   const bool ares = g.Dp <= BK * ARES_SLICES && (debug_flags & 128) && wave > -2;  // experiment: not faster
   if (kind == KIND_FWD) {
+#if DISCO_EXPERIMENTS
     rc = ares ? launch_logits_t<KIND_FWD, true>(p, units, st) : launch_logits_t<KIND_FWD, false>(p, units, st);
+#else
+    (void)ares;
+    rc = launch_logits_t<KIND_FWD, false>(p, units, st);
+#endif
     if (rc) return rc;
   } else if (kind == KIND_FWDE) {
     const size_t fb = size_t(2) * g.B * g.Dp * 2;
+#if DISCO_EXPERIMENTS
     rc = sym    ? launch_logits_t<KIND_FWDE, false, true>(p, units, st, feat, fb)
          : ares ? launch_logits_t<KIND_FWDE, true>(p, units, st, feat, fb)
                 : launch_logits_t<KIND_FWDE, false>(p, units, st, feat, fb);
+#else
+    (void)sym;
+    rc = launch_logits_t<KIND_FWDE, false>(p, units, st, feat, fb);
+#endif
     if (rc) return rc;
   } else {
     if ((rc = prepare_kernel(logits_kernel<KIND_GRAD, false>))) return rc;
@@ -2745,7 +2891,9 @@ int forward_finish(void* ws, const Geometry& g, cudaStream_t st) {
   const int ndir = g.sym ? 1 : 2;
   const int n = int(ndir * g.b);
   float2* stats = region<float2>(ws, g, DISCO_R_STATS);
-  stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(stats, rows, g.nchunk, g.ssub, int(g.b), ndir,
+  // column parts per (row, sub-chunk): the FWDE kernel's epilogue parts, or halves (FWD, SYM)
+  const int nparts = (g.estore && !g.sym) ? FWDE_PARTS : 2;
+  stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(stats, rows, g.nchunk, g.ssub, nparts, int(g.b), ndir,
                                                         rows + 2 * g.b, rows + 4 * g.b, region<float>(ws, g, DISCO_R_CE),
                                                         region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
@@ -2753,7 +2901,7 @@ int forward_finish(void* ws, const Geometry& g, cudaStream_t st) {
   if (g.sym) {
     stats_sym_kernel<<<int((g.B + 255) / 256), 256, 0, st>>>(
         region<float>(ws, g, DISCO_R_SCALE) + int64_t(g.groups) * g.b,
-        reinterpret_cast<float*>(stats + 2 * int64_t(g.nchunk) * g.ssub * 2 * g.b), rows, g.groups, int(g.B),
+        reinterpret_cast<float*>(stats + 2 * int64_t(g.nchunk) * g.ssub * 4 * g.b), rows, g.groups, int(g.B),
         rows + 2 * g.b, rows + 4 * g.b, region<float>(ws, g, DISCO_R_CE), region<Status>(ws, g, DISCO_R_STATUS));
     count_launch();
     CUDA_TRY(cudaGetLastError());

@@ -48,35 +48,64 @@ def supported(B: int, D: int, world: int, rank: int) -> bool:
     return True
 
 
+class PeerUnavailable(RuntimeError):
+    """The peer transport cannot run on this group (no peer access between some pair of GPUs, or
+    the IPC mapping failed on some rank).  Raised on EVERY rank (the decision is collective), so
+    the caller can fall back to the NCCL exchange without a rank hanging in a wait kernel."""
+
+
+def _peer_access_all_pairs(devices) -> bool:
+    import torch
+    for i in set(devices):
+        for j in set(devices):
+            if i != j and not torch.cuda.can_device_access_peer(i, j):
+                return False
+    return True
+
+
 class PeerWindow:
     """This rank's peer window and the N window bases (index = rank) for one plan geometry."""
 
     def __init__(self, endpoint, B: int, D: int, world: int, rank: int):
+        import torch
         lib = _lib.load()
         self.world, self.rank = world, rank
+        self.base = None
+        self._opened = []
+        in_process = getattr(endpoint, "in_process", False)
+        if not in_process:
+            # every rank sees every rank's device: identical all-pairs answer on every rank
+            devices = endpoint.exchange(torch.cuda.current_device())
+            if not _peer_access_all_pairs(devices):
+                raise PeerUnavailable(f"no peer access between some pair of GPUs {sorted(set(devices))}")
         nbytes = ctypes.c_int64()
         _lib.call("disco_b200_peer_bytes", B, D, world, rank, ctypes.byref(nbytes))
         self.nbytes = nbytes.value
-        in_process = getattr(endpoint, "in_process", False)
         handle = None if in_process else ctypes.create_string_buffer(lib.disco_b200_peer_handle_bytes())
         ptr = ctypes.c_void_p()
         _lib.call("disco_b200_peer_alloc", self.nbytes, ctypes.byref(ptr), handle)
         self.base = ptr.value
-        self._opened = []
         try:
             if in_process:
                 bases = endpoint.exchange(self.base)
             else:
                 handles = endpoint.exchange(bytes(handle.raw))
-                bases = []
+                bases, err = [], None
                 for r, h in enumerate(handles):
                     if r == rank:
                         bases.append(self.base)
                         continue
                     p = ctypes.c_void_p()
-                    _lib.call("disco_b200_peer_open", ctypes.create_string_buffer(h, len(h)), ctypes.byref(p))
+                    try:
+                        _lib.call("disco_b200_peer_open", ctypes.create_string_buffer(h, len(h)), ctypes.byref(p))
+                    except RuntimeError as exc:
+                        err = str(exc)
+                        break
                     self._opened.append(p.value)
                     bases.append(p.value)
+                failures = [e for e in endpoint.exchange(err) if e]  # collective: all ranks decide alike
+                if failures:
+                    raise PeerUnavailable(f"peer window mapping failed: {failures[0]}")
         except BaseException:
             self.close()
             raise

@@ -615,7 +615,12 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         if N > 1 and _peer.enabled(endpoint) and _peer.supported(B, D, N, n):
             # peer transport: every rank reads the others' packed rows from their NVLink-mapped
             # windows straight into its operand layouts (all_gather + unpack in one kernel)
-            pw = plan.peer_window(endpoint)
+            try:
+                pw = plan.peer_window(endpoint)
+            except _peer.PeerUnavailable:
+                endpoint.peer = False  # collective decision: every rank falls back to the NCCL exchange
+                pw = None
+        if pw is not None:
             epoch, parity = pw.next_step()
             _lib.call("disco_b200_peer_publish", *plan.args, pw.bases, parity, epoch, st)
             if _peer.streamed_gather(endpoint, B, N):
@@ -630,9 +635,10 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
             else:
                 _lib.call("disco_b200_peer_gather", *plan.args, pw.bases, parity, epoch, _peer.PEER_TIMEOUT_S, st)
                 _lib.call("disco_b200_forward_gathered", *plan.args, t, st)
+        elif N > 1:
+            endpoint.all_gather_into(plan.gather, plan.pack)
+            _lib.call("disco_b200_forward", *plan.args, t, st)
         else:
-            if N > 1:
-                endpoint.all_gather_into(plan.gather, plan.pack)
             _lib.call("disco_b200_forward", *plan.args, t, st)
     _lib.call("disco_b200_backward_grad", *plan.args, t, st)
     if pw is not None:

@@ -5,7 +5,9 @@ Both ranks share cuda:0; the process group is gloo.  argv[2] selects the exchang
   nccl  -- DISCO_PEER=0: the exchange the NCCL path runs (ProcessGroupEndpoint.all_gather_into,
            all_to_all_into, the per-row ce all_gather) with the real device kernels, the
            collectives staged through host memory (gloo cannot move CUDA tensors; two ranks on
-           one GPU cannot form an NCCL communicator).
+           one GPU cannot form an NCCL communicator);
+  fallback -- the peer transport is requested but reported unavailable (peer access check patched
+           to fail): every rank must fall back to the NCCL exchange together.
 Two steps, so both parity windows are used.
 """
 import os
@@ -23,7 +25,10 @@ def main(out_dir, mode="peer"):
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    ep = P.ProcessGroupEndpoint(peer=(mode == "peer"))
+    if mode == "fallback":
+        from paper_2304_08480_b200 import peer as peer_mod
+        peer_mod._peer_access_all_pairs = lambda devices: False
+    ep = P.ProcessGroupEndpoint(peer=(mode != "nccl"))
     I = np.load(os.path.join(out_dir, "I.npy"))
     T = np.load(os.path.join(out_dir, "T.npy"))
     b = I.shape[0] // world
@@ -31,6 +36,8 @@ def main(out_dir, mode="peer"):
     Td = torch.from_numpy(T[rank * b:(rank + 1) * b]).cuda()
     for _ in range(2):
         di, dt, loss = P.disco_step(ep, Id, Td, 100.0)
+    if mode == "fallback":
+        assert ep.peer is False, "peer transport should have been disabled"
     np.save(os.path.join(out_dir, f"di{rank}.npy"), di.cpu().numpy())
     np.save(os.path.join(out_dir, f"dt{rank}.npy"), dt.cpu().numpy())
     np.save(os.path.join(out_dir, f"loss{rank}.npy"), np.array(loss))

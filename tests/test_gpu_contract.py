@@ -137,7 +137,7 @@ def test_disco_step_async_rejects_unsafe_inputs():
     with pytest.raises(P.ShapeError):
         P.disco_step_async(ep, a[None], a[None], 10.0)
     # a valid strided view (unit column stride, row stride > D) is read in place
-    big = torch.randn(64, 48, device="cuda")
+    big = torch.nn.functional.normalize(torch.randn(64, 48, device="cuda"), dim=1).bfloat16().float()
     view = big[:, :32]
     d_i, d_t, plan = P.disco_step_async(ep, view, view, 10.0)
     loss = P.finish_status(plan)
@@ -147,12 +147,12 @@ def test_disco_step_async_rejects_unsafe_inputs():
 
 
 def test_autograd_accepts_non_contiguous_features():
-    base = torch.randn(2, 128, 64, device="cuda")
-    I = torch.nn.functional.normalize(base[0], dim=1).t().contiguous().t()  # column-major view
-    T = torch.nn.functional.normalize(base[1], dim=1)
+    base = torch.nn.functional.normalize(torch.randn(2, 128, 64, device="cuda"), dim=2).bfloat16().float()
+    I = base[0].t().contiguous().t()  # column-major view (bf16-representable values, as the kernels see them)
+    T = base[1]
     I.requires_grad_(True)
     loss = P.disco_loss(I, T, 10.0)
     loss.backward()
     ri, _, rl = O.clip_grad_full(I.detach().double().cpu().numpy(), T.double().cpu().numpy(), 10.0)
-    assert abs(float(loss) - rl[0]) < 1e-3 * rl[0]
+    assert abs(float(loss.detach()) - rl[0]) < 1e-3 * rl[0]
     assert O.max_rel_error(I.grad.cpu().numpy(), ri) < 1e-3

@@ -302,6 +302,11 @@ def test_symmetric_forward_vs_oracle(B, D, monkeypatch):
     (S_1 = S_0^T; t2i column statistics reduced across lanes in the epilogue).  Within the
     contract tolerance of the f64 oracle and of the two-GEMM path, on the device path, the host
     wavefront path (f32 host inputs) and the streamed path (pinned bf16 host inputs)."""
+    from paper_2304_08480_b200 import _lib
+    monkeypatch.setenv("DISCO_SYMMETRIC", "1")
+    if not _lib.path_info(B, D, 1) & _lib.PATH_SYM:
+        pytest.skip("symmetric forward: experiment, compiled only with -DDISCO_EXPERIMENTS=1")
+    monkeypatch.delenv("DISCO_SYMMETRIC")
     I, T = O.synthetic_features(B, D, 7)
     bi, bt, bl = (x.cpu().numpy() if torch.is_tensor(x) else x for x in P.disco_step(None, dev(I), dev(T), 100.0))
     monkeypatch.setenv("DISCO_SYMMETRIC", "1")

@@ -112,13 +112,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("mode,streamed", [("peer", "0"), ("peer", "1"), ("nccl", "0")])
+@pytest.mark.parametrize("mode,streamed", [("peer", "0"), ("peer", "1"), ("nccl", "0"), ("fallback", "0")])
 def test_peer_two_processes_ipc(tmp_path, mode, streamed):
     """Two processes, one GPU, gloo: bitwise equal to N = 1.  ``peer``: CUDA IPC windows, with the
     kernel all-gather and (small B, where the shared GPU's time slicing lets both ranks publish
     before either spins for long) the streamed copy-engine all-gather.  ``nccl``: DISCO_PEER=0, the
     ProcessGroupEndpoint all_gather / all_to_all exchange (shard.py:190-205 replaced by
-    fabric.py all_gather_into + all_to_all_into) driving the real kernels, host-staged."""
+    fabric.py all_gather_into + all_to_all_into) driving the real kernels, host-staged.
+    ``fallback``: peer requested but unavailable (access check fails on every rank): both ranks
+    drop to the NCCL exchange instead of hanging."""
     B, D = 2048, 256
     I, T = O.synthetic_features(B, D, 11)
     np.save(tmp_path / "I.npy", I.astype(np.float32))

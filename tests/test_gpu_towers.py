@@ -67,5 +67,9 @@ def test_measured_footprint_scales_as_b_squared_over_n():
         assert r.loss_elements == 2 * b * B and r.loss_flops == 4 * b * B * D
         assert r.bytes >= 2 * 2 * b * B  # the f16 E blocks alone
     assert reps[1].bytes > reps[2].bytes > reps[4].bytes > reps[8].bytes
-    assert reps[8].bytes < reps[1].bytes / 4
+    # the O(B^2/N) workspace falls faster than 1/4 from N = 1 to 8; the peer-transport window
+    # (counted in bytes since round 2: cudaMalloc'd outside torch) is O(B*D) fp32 slabs on top
+    win8 = costs.peer_window_bytes(B, D, 8)
+    assert win8 > 0
+    assert reps[8].bytes - win8 < reps[1].bytes / 4
     assert naive.loss_elements == B * B and naive.bytes >= 4 * B * B

@@ -24,6 +24,7 @@ ap.add_argument("--batch", type=int, default=32768)
 ap.add_argument("--dim", type=int, default=512)
 ap.add_argument("--flags", type=int, nargs="+", default=[0])
 ap.add_argument("--so-b", default=None, help="second library build to alternate with")
+ap.add_argument("--so", nargs="*", default=[], help="more library builds to alternate with (name=path or path)")
 ap.add_argument("--reps", type=int, default=15)
 ap.add_argument("--warm", type=float, default=3.0, help="seconds of untimed steps first (clocks ramp)")
 a = ap.parse_args()
@@ -52,15 +53,17 @@ dt = torch.empty((B, D), dtype=torch.float32, device=dev)
 flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
 libs = [("main", _lib.load())]
-if a.so_b:
-    lb = ctypes.CDLL(a.so_b)
+extra = ([("b", a.so_b)] if a.so_b else []) + [
+    (x.split("=", 1)[0], x.split("=", 1)[1]) if "=" in x else (os.path.basename(x).rsplit(".", 1)[0], x) for x in a.so]
+for lname, path in extra:
+    lb = ctypes.CDLL(os.path.abspath(path))
     for name, argtypes in _lib.SIGNATURES.items():
         fn = getattr(lb, name, None)
         if fn is None:  # older build: no experiment-flag hook
             continue
         fn.argtypes = argtypes
         fn.restype = _lib._RESTYPES.get(name, ctypes.c_int)
-    libs.append(("b", lb))
+    libs.append((lname, lb))
 variants = [(ln, lib, f) for ln, lib in libs for f in a.flags]
 
 
