@@ -20,8 +20,11 @@ Printed on rank 0, one JSON line:
             (CUDA events on the launching stream) against the measured bf16
             peak (MEASURED_PEAKS.json); step-level fraction alongside.
   cpu_baseline  the oracle port of the reference path (oracle/disco_oracle.py,
-            numpy f32, all host cores) on a bounded row sample (rank 0, N=1 only).
-``--impl reference`` times that CPU port alone as the reference arm.
+            numpy f32, all host cores), one full step (rank 0, N=1 only).
+  exchange_backward  (N=1) the same step with DISCO_BACKWARD=exchange: intra + cross
+            GEMMs, the reference's dataflow; `value` is the default dual backward.
+``--impl reference`` times that CPU port (full steps) as the reference arm, plus one
+step of the unmodified reference disco_step from baseline/_ref when installed.
 """
 
 import argparse
@@ -58,7 +61,8 @@ def parse():
                     help="BASELINE.json config letter (SURVEY 8.0); --batch/--dim override")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-fused", action="store_true", help="skip the opt-in fused single-rank backward leg")
+    ap.add_argument("--no-exchange-leg", "--no-fused", dest="no_exchange_leg", action="store_true",
+                    help="skip the exchange-backward comparison leg (N = 1)")
     ap.add_argument("--no-ref-check", action="store_true",
                     help="reference arm: skip the one-step unmodified-reference cross-check")
     return ap.parse_args()
@@ -315,6 +319,76 @@ def exchange_preflight(P, ep, I, T, t, world, local_rank, share):
     return info
 
 
+def phase_breakdown(P, _lib, peer_mod, ep, plan, names, I, T, t, st, flush, barrier, use_peer, dual, reps=5):
+    """Mean ms of each C-ABI phase of one step (CUDA events around each call on the launch stream,
+    L2 flushed before every rep); `names` selects the phases of the path being measured."""
+    import torch
+    B, D, world = plan.B, plan.D, plan.world
+    b = B // world
+    args_ = plan.args
+    sp = st.cuda_stream
+    dev = plan.device
+    ev = {n: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for n in names}
+    acc = {n: 0.0 for n in names}
+    di = torch.empty((b, D), dtype=torch.float32, device=dev)
+    dt_ = torch.empty((b, D), dtype=torch.float32, device=dev)
+
+    def timed(name, fn):
+        if name not in ev:
+            return
+        ev[name][0].record(st)
+        fn()
+        ev[name][1].record(st)
+
+    for _ in range(reps):
+        flush.zero_()
+        barrier()
+        timed("pack", lambda: _lib.call("disco_b200_pack", *args_, I.data_ptr(), T.data_ptr(), D, D, _lib.BF16, 1, sp))
+        timed("all_gather", lambda: ep.all_gather_into(plan.gather, plan.pack))
+        pw = parity = epoch = None
+        if use_peer:
+            pw = plan.peer_window(ep)
+            epoch, parity = pw.next_step()
+            timed("peer_gather", lambda: (_lib.call("disco_b200_peer_publish", *args_, pw.bases, parity, epoch, sp),
+                                          _lib.call("disco_b200_peer_gather", *args_, pw.bases, parity, epoch,
+                                                    peer_mod.PEER_TIMEOUT_S, sp)))
+            timed("forward", lambda: _lib.call("disco_b200_forward_gathered", *args_, t, sp))
+        else:
+            timed("forward", lambda: _lib.call("disco_b200_forward", *args_, t, sp))
+        if dual:
+            timed("stats_exchange", lambda: ep.all_gather_into(plan.xall, plan.xchg))
+            timed("dual_prep", lambda: _lib.call("disco_b200_dual_prep", *args_, 0, sp))
+            timed("backward", lambda: _lib.call("disco_b200_backward_dual", *args_, 0, b, sp))
+            timed("combine", lambda: _lib.call("disco_b200_combine_dual", *args_, t, 0, b, di.data_ptr(),
+                                               dt_.data_ptr(), D, sp))
+            timed("fixup", lambda: _lib.call("disco_b200_dual_fixup", *args_, t, 0, di.data_ptr(), dt_.data_ptr(),
+                                             D, sp))
+            timed("loss", lambda: _lib.call("disco_b200_loss", *args_, 2, sp))
+        else:
+            timed("backward_grad", lambda: _lib.call("disco_b200_backward_grad", *args_, t, sp))
+            timed("backward", lambda: _lib.call("disco_b200_backward_fused", *args_, sp))
+            if use_peer:
+                timed("backward_peer", lambda: _lib.call("disco_b200_backward_peer", *args_, pw.bases, parity, epoch,
+                                                         sp))
+                timed("combine_peer", lambda: _lib.call("disco_b200_combine_peer", *args_, t, 0, pw.base, parity,
+                                                        epoch, peer_mod.PEER_TIMEOUT_S, di.data_ptr(), dt_.data_ptr(),
+                                                        D, sp))
+            timed("backward_cross", lambda: _lib.call("disco_b200_backward_cross", *args_, sp))
+            timed("all_to_all", lambda: ep.all_to_all_into(plan.recv, plan.send))
+            timed("backward_intra", lambda: _lib.call("disco_b200_backward_intra", *args_, sp))
+            timed("combine", lambda: _lib.call("disco_b200_combine", *args_, t, 0, di.data_ptr(), dt_.data_ptr(), D,
+                                               sp))
+            if use_peer:  # the ce rode with the slabs into this rank's window
+                timed("loss", lambda: _lib.call("disco_b200_loss_peer", *args_, pw.base, parity, sp))
+            else:
+                timed("loss", lambda: (world > 1 and ep.all_gather_into(plan.ce_all, plan.ce),
+                                       _lib.call("disco_b200_loss", *args_, 0, sp)))
+        torch.cuda.synchronize()
+        for n in names:
+            acc[n] += ev[n][0].elapsed_time(ev[n][1]) / reps
+    return {n: round(v, 4) for n, v in acc.items()}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -415,68 +489,23 @@ def run_ours(args):
     # ---- kernel breakdown: events around each C-ABI call (one tensor-core kernel each)
     from paper_2304_08480_b200 import peer as peer_mod
     use_peer = world > 1 and peer_mod.enabled(ep) and peer_mod.supported(B, D, world, rank)
-    if world == 1:  # the step runs intra + cross as one fused launch
-        names = ["pack", "forward", "backward_grad", "backward", "combine", "loss"]
-    elif use_peer:  # peer all-gather (fused unpack), fused intra + cross GEMM pushing cross tiles to the owners
-        names = ["pack", "peer_gather", "forward", "backward_grad", "backward_peer", "combine_peer", "loss"]
+    dual = bool(_lib.path_info(B, D, world, rank) & _lib.PATH_DUAL)
+    names = ["pack"] + (["peer_gather"] if use_peer else ["all_gather"] if world > 1 else []) + ["forward"]
+    if dual:  # the default: statistics exchange, one GEMM per gradient over the rank's own E block
+        names += (["stats_exchange"] if world > 1 else []) + ["dual_prep", "backward", "combine", "fixup", "loss"]
+    elif world == 1:  # exchange backward, intra + cross as one launch
+        names += ["backward_grad", "backward", "combine", "loss"]
+    elif use_peer:  # fused intra + cross GEMM pushing cross tiles to the owners
+        names += ["backward_grad", "backward_peer", "combine_peer", "loss"]
     else:
-        names = ["pack", "all_gather", "forward", "backward_grad", "backward_cross", "all_to_all",
-                 "backward_intra", "combine", "loss"]
-    ev = {n: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for n in names}
-    args_ = plan.args
-    sp = st.cuda_stream
-    reps = 5
-    acc = {n: 0.0 for n in names}
-    di = torch.empty((b, D), dtype=torch.float32, device=device)
-    dt_ = torch.empty((b, D), dtype=torch.float32, device=device)
-
-    def timed(name, fn):
-        if name not in ev:
-            return
-        ev[name][0].record(st)
-        fn()
-        ev[name][1].record(st)
-
-    for _ in range(reps):
-        flush.zero_()
-        barrier()
-        timed("pack", lambda: _lib.call("disco_b200_pack", *args_, I.data_ptr(), T.data_ptr(), D, D, _lib.BF16, 1, sp))
-        timed("all_gather", lambda: ep.all_gather_into(plan.gather, plan.pack))
-        if use_peer:
-            pw = plan.peer_window(ep)
-            epoch, parity = pw.next_step()
-            timed("peer_gather", lambda: (_lib.call("disco_b200_peer_publish", *args_, pw.bases, parity, epoch, sp),
-                                          _lib.call("disco_b200_peer_gather", *args_, pw.bases, parity, epoch,
-                                                    peer_mod.PEER_TIMEOUT_S, sp)))
-            timed("forward", lambda: _lib.call("disco_b200_forward_gathered", *args_, t, sp))
-        else:
-            timed("forward", lambda: _lib.call("disco_b200_forward", *args_, t, sp))
-        timed("backward_grad", lambda: _lib.call("disco_b200_backward_grad", *args_, t, sp))
-        timed("backward", lambda: _lib.call("disco_b200_backward_fused", *args_, sp))
-        if use_peer:
-            timed("backward_peer", lambda: _lib.call("disco_b200_backward_peer", *args_, pw.bases, parity, epoch, sp))
-            timed("combine_peer", lambda: _lib.call("disco_b200_combine_peer", *args_, t, 0, pw.base, parity, epoch,
-                                                    peer_mod.PEER_TIMEOUT_S, di.data_ptr(), dt_.data_ptr(), D, sp))
-        timed("backward_cross", lambda: _lib.call("disco_b200_backward_cross", *args_, sp))
-        timed("all_to_all", lambda: ep.all_to_all_into(plan.recv, plan.send))
-        timed("backward_intra", lambda: _lib.call("disco_b200_backward_intra", *args_, sp))
-        timed("combine", lambda: _lib.call("disco_b200_combine", *args_, t, 0, di.data_ptr(), dt_.data_ptr(), D, sp))
-        if use_peer:  # the ce rode with the slabs into this rank's window
-            timed("loss", lambda: _lib.call("disco_b200_loss_peer", *args_, pw.base, parity, sp))
-        else:
-            timed("loss", lambda: (world > 1 and ep.all_gather_into(plan.ce_all, plan.ce),
-                                   _lib.call("disco_b200_loss", *args_, 0, sp)))
-        torch.cuda.synchronize()
-        for n in names:
-            acc[n] += ev[n][0].elapsed_time(ev[n][1]) / reps
-    phases = {n: round(v, 4) for n, v in acc.items()}
+        names += ["backward_grad", "backward_cross", "all_to_all", "backward_intra", "combine", "loss"]
+    phases = phase_breakdown(P, _lib, peer_mod, ep, plan, names, I, T, t, st, flush, barrier, use_peer, dual)
     traffic_n = None
     peer_bytes = 0
     if world > 1:
         from paper_2304_08480_b200 import costs as costs_mod
         Dp = (D + 63) // 64 * 64
         ag_bytes = (world - 1) * 2 * b * Dp * 2   # bf16 rows received per rank (both feature sets)
-        rs_bytes = (world - 1) * 2 * b * Dp * 4   # fp32 partial rows each rank sends to their owners
         link = 900.0                              # NVLink 5 GB/s per direction
         ag_ms = phases.get("peer_gather", phases.get("all_gather"))
         traffic_n = {"note": "bytes per rank per step; busbw = bytes moved per rank / phase time "
@@ -484,18 +513,27 @@ def run_ours(args):
                      "all_gather": {"bytes": ag_bytes, "ms": ag_ms, "busbw_gbs": ag_bytes / (ag_ms / 1e3) / 1e9,
                                     "frac_of_link": ag_bytes / (ag_ms / 1e3) / 1e9 / link,
                                     "kind": "peer pull + unpack kernel" if use_peer else "nccl all_gather_into_tensor"}}
-        if use_peer:
+        if dual:
+            sx_bytes = (world - 1) * 4 * b * 4
+            traffic_n["stats_exchange"] = {
+                "bytes": sx_bytes, "ms": phases["stats_exchange"],
+                "kind": "nccl all_gather of the 4 b per-row statistics (lse2, ce); the dual backward "
+                        "needs no gradient reduce-scatter"}
+        elif use_peer:
+            rs_bytes = (world - 1) * 2 * b * Dp * 4   # fp32 partial rows each rank sends to their owners
             bw_ms = phases["backward_peer"]
             traffic_n["reduce_scatter"] = {
                 "bytes": rs_bytes, "ms_overlapped": bw_ms, "combine_ms": phases["combine_peer"],
                 "push_gbs_during_gemm": rs_bytes / (bw_ms / 1e3) / 1e9,
                 "kind": "TMA pushes from the backward GEMM epilogue into the owners' windows (overlapped)"}
-            peer_bytes = costs_mod.peer_window_bytes(B, D, world, rank)
         else:
+            rs_bytes = (world - 1) * 2 * b * Dp * 4
             a_ms = phases["all_to_all"]
             traffic_n["reduce_scatter"] = {"bytes": rs_bytes, "ms": a_ms, "busbw_gbs": rs_bytes / (a_ms / 1e3) / 1e9,
                                            "frac_of_link": rs_bytes / (a_ms / 1e3) / 1e9 / link,
                                            "kind": "nccl all_to_all_single of fp32 destination slabs"}
+        if use_peer:
+            peer_bytes = costs_mod.peer_window_bytes(B, D, world, rank)
     kernel_mhz = _lib.clock_probe(plan)  # SM clock the last timed launches actually ran at
 
     # ---- e2e through the public API with host buffers ---------------------
@@ -530,52 +568,40 @@ def run_ours(args):
 
     e2e = None if args.no_e2e else measure_e2e()
 
-    # ---- the opt-in fused single-rank backward (DISCO_HFUSE=1), same workload --------
-    # One GEMM per gradient on H = G_0 + G_1^T (half the backward flops); within 1e-3 of the
-    # oracle but not bit-for-bit equal to N > 1, so the default (the line's `value`) is the
-    # N-invariant path the north star asks for.  Measured here the same way, for comparison.
-    fused = None
-    if world == 1 and not args.no_fused:
-        saved = os.environ.get("DISCO_HFUSE")
-        os.environ["DISCO_HFUSE"] = "1"
+    # ---- the exchange backward (DISCO_BACKWARD=exchange), same workload, for comparison -----
+    # Intra + cross GEMMs (8*b*B*D backward flops) and, at N > 1, the gradient reduce-scatter: the
+    # reference's dataflow (shard.py:148-154, 199-208).  The line's `value` is the dual backward.
+    exchange = None
+    if world == 1 and dual and not args.no_exchange_leg:
+        saved = os.environ.get("DISCO_BACKWARD")
+        os.environ["DISCO_BACKWARD"] = "exchange"
         try:
-            if _lib.path_info(B, D, world, rank) & _lib.PATH_HFUSE:
-                for _ in range(args.warmup):
-                    step()
-                torch.cuda.synchronize()
-                f0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-                f1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-                for i in range(args.steps):
-                    flush.zero_()
-                    f0[i].record(st)
-                    step()
-                    f1[i].record(st)
-                torch.cuda.synchronize()
-                fms = statistics.mean(a.elapsed_time(z) for a, z in zip(f0, f1))
-                f_loss = P.finish_status(plan)
-                bw = []
-                for _ in range(5):  # the fused backward GEMM alone (its forward state is current)
-                    flush.zero_()
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record(st)
-                    _lib.call("disco_b200_backward_fused", *plan.args, st.cuda_stream)
-                    e1.record(st)
-                    torch.cuda.synchronize()
-                    bw.append(e0.elapsed_time(e1))
-                bms = statistics.mean(bw)
-                fused = {"value": B / (fms / 1e3), "unit": UNIT, "ms_per_step": fms, "loss": f_loss,
-                         "backward_ms": bms,
-                         "backward_tflops_executed": 4.0 * b * B * D / (bms / 1e3) / 1e12,
-                         "backward_frac_executed": 4.0 * b * B * D / (bms / 1e3) / 1e12 / load_peaks()[1],
-                         "e2e": None if args.no_e2e else measure_e2e(),
-                         "note": "DISCO_HFUSE=1: single-rank backward as one GEMM per gradient on "
-                                 "H = G_0 + G_1^T (4*b*B*D executed flops); within 1e-3 of the oracle, "
-                                 "not bitwise equal to N > 1"}
+            for _ in range(args.warmup):
+                step()
+            torch.cuda.synchronize()
+            f0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            f1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            for i in range(args.steps):
+                flush.zero_()
+                f0[i].record(st)
+                step()
+                f1[i].record(st)
+            torch.cuda.synchronize()
+            fms = statistics.mean(a.elapsed_time(z) for a, z in zip(f0, f1))
+            x_loss = P.finish_status(plan)
+            xph = phase_breakdown(P, _lib, peer_mod, ep, plan, ["pack", "forward", "backward_grad", "backward",
+                                                                 "combine", "loss"],
+                                  I, T, t, st, flush, barrier, False, False)
+            exchange = {"value": B / (fms / 1e3), "unit": UNIT, "ms_per_step": fms, "loss": x_loss,
+                        "phases_ms": xph,
+                        "backward_tflops": 8.0 * b * B * D / (xph["backward"] / 1e3) / 1e12,
+                        "note": "DISCO_BACKWARD=exchange: intra + cross GEMMs (8*b*B*D backward flops), "
+                                "the reference's dataflow; also bitwise N-invariant"}
         finally:
             if saved is None:
-                os.environ.pop("DISCO_HFUSE", None)
+                os.environ.pop("DISCO_BACKWARD", None)
             else:
-                os.environ["DISCO_HFUSE"] = saved
+                os.environ["DISCO_BACKWARD"] = saved
 
     # NVML's throttle reasons lag a ~50 ms burst: sample over ~0.5 s more of the same work (untimed,
     # after every measurement) so a power cap that shaped the timed steps is reported
@@ -594,16 +620,15 @@ def run_ours(args):
     burst, sustained, hbm, src = load_peaks()
     mm = 4.0 * b * B * D           # 2 directions x 2*b*B*D (12*b*B*D per step)
     g_bytes = 2.0 * b * B * 2       # f16 E / G blocks (a6 output, both directions)
-    recompute = phases["backward_grad"] > 0.1  # non-canonical shapes recompute the logits
+    recompute = phases.get("backward_grad", 0.0) > 0.1  # non-canonical shapes recompute the logits
     kernels = {  # name: (ms, bound, algorithmic work per launch, unit, peak)
         "logits_fwd": (phases["forward"], "tensor", mm, "TFLOP/s", sustained)}
     if recompute:
         kernels["logits_grad"] = (phases["backward_grad"], "hbm", g_bytes, "GB/s", hbm)
-    # fused single-rank backward (default at N = 1, wide D): one GEMM per gradient on H = G_0 + G_1^T
-    # executes 4*b*B*D flops for the reference's 8*b*B*D; the roofline uses the executed flops
-    hfuse = world == 1 and bool(_lib.path_info(B, D, world, 0) & _lib.PATH_HFUSE)
-    if world == 1:
-        kernels["gemm_backward"] = (phases["backward"], "tensor", (1 if hfuse else 2) * mm, "TFLOP/s", sustained)
+    # dual backward: one GEMM per gradient on H = G_d + G_d'^T, 4*b*B*D executed flops for the
+    # reference's 8*b*B*D; the roofline uses the executed flops
+    if dual or world == 1:
+        kernels["gemm_backward"] = (phases["backward"], "tensor", (1 if dual else 2) * mm, "TFLOP/s", sustained)
     elif use_peer:
         kernels["gemm_backward_peer"] = (phases["backward_peer"], "tensor", 2 * mm, "TFLOP/s", sustained)
     else:
@@ -617,17 +642,22 @@ def run_ours(args):
                     "frac_of_burst": ach / burst if unit == "TFLOP/s" else None}
     # the forward also streams the f16 E blocks out (canonical shapes): its HBM side
     table["logits_fwd"]["e_write_gbs"] = None if recompute else g_bytes / (phases["forward"] / 1e3) / 1e9
-    dom = max(table, key=lambda k: table[k]["ms"])
+    if "combine" in phases and dual:  # reads the K-half partials + label rows, writes the fp32 gradients
+        cb = 2 * b * D * 4 * 2 + 2 * b * D * 4 + 2 * b * D * 2
+        table["combine_dual"] = {"ms": phases["combine"], "bound": "hbm", "achieved": cb / (phases["combine"] / 1e3) / 1e9,
+                                 "peak": hbm, "unit": "GB/s", "frac": cb / (phases["combine"] / 1e3) / 1e9 / hbm,
+                                 "bytes": cb}
+    dom = max((k for k in table if table[k]["unit"] == "TFLOP/s"), key=lambda k: table[k]["ms"])
     # ncu DRAM bytes per launch were captured at the headline workload (B=32K, D=512, N=1)
     traffic = load_traffic().get(dom) if (B, D, world) == (B_GLOBAL, DIM, 1) else None
-    if world == 1 and not recompute:  # the backward streams both E blocks twice (d_image and d_text GEMMs)
-        table["gemm_backward"]["e_read_gbs"] = 2 * g_bytes / (phases["backward"] / 1e3) / 1e9
-    if hfuse:
+    if "gemm_backward" in table and not recompute:  # E read once per gradient GEMM (dual) or twice
+        table["gemm_backward"]["e_read_gbs"] = (1 if dual else 2) * g_bytes / (phases["backward"] / 1e3) / 1e9
+    if dual:
         table["gemm_backward"]["algorithmic_tflops"] = 2 * mm / (phases["backward"] / 1e3) / 1e12
-        table["gemm_backward"]["note"] = ("fused single-rank backward: H = G_0 + G_1^T formed in shared memory, "
-                                          "4*b*B*D executed flops (the reference's algorithm: 8*b*B*D)")
+        table["gemm_backward"]["note"] = ("dual backward: H = G_d + G_d'^T formed in shared memory from the rank's own "
+                                          "E block, 4*b*B*D executed flops (the reference's algorithm: 8*b*B*D)")
     step_tflops = 12.0 * b * B * D / (ms / 1e3) / 1e12            # algorithmic
-    step_exec_tflops = (8.0 if hfuse else 12.0) * b * B * D / (ms / 1e3) / 1e12
+    step_exec_tflops = (8.0 if dual else 12.0) * b * B * D / (ms / 1e3) / 1e12
     d = table[dom]
 
     cpu = None
@@ -643,7 +673,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": dict(workload_config(args, B, D, world),
+                       backward="dual (rank-local H = G_d + G_d'^T GEMMs)" if dual else "exchange (intra + cross GEMMs)",
                        exchange=("none" if world == 1 else
+                                 ("peer all-gather + nccl stats all_gather" if use_peer else
+                                  "nccl all_gather (features, stats)") if dual else
                                  "peer (GEMM epilogue TMA pushes over NVLink)" if use_peer else "nccl all_to_all"),
                        exchange_preflight=preflight,
                        l2="flushed between steps (512 MB write, outside timed events)"),
@@ -666,7 +699,7 @@ def run_ours(args):
         "phases_ms": phases,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "fused_single_rank": fused,
+        "exchange_backward": exchange,
         "gpu_launches": launches,
         "clocks": dict(clk.summary(), in_kernel_mhz=kernel_mhz,
                        reasons_sustained=clk_after.summary().get("reasons"),

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define DISCO_B200_ABI_VERSION 2
+#define DISCO_B200_ABI_VERSION 3
 
 enum disco_status {
   DISCO_OK = 0,
@@ -56,8 +56,9 @@ enum disco_region {
   DISCO_R_FEAT = 2,    /* bf16 [2][B][Dp]         gathered I_g, T_g (forward GEMM operands)  */
   DISCO_R_FEAT16 = 3,  /* f16  [2][B][Dp]         gathered I_g, T_g (backward GEMM operands) */
   DISCO_R_STATS = 4,   /* f32x2 [2][nchunk*ssub][2][b] (max, sum-exp) per column sub-chunk and half */
-  DISCO_R_ROWS = 5,    /* f32  [4][2][b]          target logit, lse, label gradient, spare   */
-  DISCO_R_CE = 6,      /* f32  [2][b]             per-row cross-entropy (loss all_gather in) */
+  DISCO_R_ROWS = 5,    /* f32  [4][2][b]          target logit, spare, label gradient, spare */
+  DISCO_R_CE = 6,      /* f32  [2][b]             per-row cross-entropy (loss all_gather in);
+                          the second half of DISCO_R_XCHG                                     */
   DISCO_R_CE_ALL = 7,  /* f32  [N][2][b]          loss all_gather output                     */
   DISCO_R_G = 8,       /* f16  [2][b][ldG]        softmax-minus-one-hot blocks (unscaled)    */
   DISCO_R_XPART = 9,   /* f32  [2][B][cpr][Dp]    cross partials per canonical row chunk     */
@@ -70,7 +71,12 @@ enum disco_region {
                           64-column group (canonical shapes; empty otherwise)                 */
   DISCO_R_RDOT = 15,    /* f32  [b]               per-row <d_image, I_n> + <d_text, T_n>       */
   DISCO_R_RDOT_ALL = 16, /* f32  [N][b]           all_gather of DISCO_R_RDOT (alias at N = 1)  */
-  DISCO_R_COUNT = 17
+  DISCO_R_XCHG = 17,   /* f32  [4][b]             lse2 (i2t, t2i) then ce (i2t, t2i) of this rank's
+                          rows: the dual backward's all_gather input                          */
+  DISCO_R_XALL = 18,   /* f32  [N][4][b]          all_gather of DISCO_R_XCHG (alias at N = 1)  */
+  DISCO_R_QCOL = 19,   /* f32  [2][B] column factors q_c, then f32x2 [2][B/64] (Q_g, min lse2) */
+  DISCO_R_FIX = 20,    /* i32  [2][ksplit][b]     rows queued for disco_b200_dual_fixup        */
+  DISCO_R_COUNT = 21
 };
 
 int disco_b200_abi_version(void);
@@ -129,14 +135,15 @@ int disco_b200_forward(void* ws, int64_t B, int64_t D, int world, int rank, floa
  * streams (they write disjoint outputs); forward_finish must follow all of them. */
 int disco_b200_forward_waves(int64_t B, int64_t D, int world, int rank, int* waves);
 
-/* Which implementation this geometry takes (bit mask; DISCO_SYMMETRIC / DISCO_HFUSE read now):
+/* Which implementation this geometry takes (bit mask; DISCO_BACKWARD is read now):
  * bit0 E stored by the forward (recompute-free backward), bit1 wide GEMM units (Dp % 512 == 0),
- * bit2 fused single-rank backward (H = G_0 + G_1^T: one GEMM per gradient, 4*b*B*D backward
- * flops instead of 8*b*B*D; E_1 stored transposed), bit3 symmetric single-rank forward. */
+ * bit2 dual backward for disco_step (every N; DISCO_BACKWARD=exchange turns it off): one GEMM per
+ * gradient over the rank's own E block on H = G_d + G_d'^T, 4*b*B*D backward flops instead of
+ * 8*b*B*D, no gradient reduce-scatter (disco_b200_dual_prep / _backward_dual / _combine_dual /
+ * _dual_fixup below). */
 #define DISCO_PATH_ESTORE 1
 #define DISCO_PATH_WIDE 2
-#define DISCO_PATH_HFUSE 4
-#define DISCO_PATH_SYM 8
+#define DISCO_PATH_DUAL 4
 int disco_b200_path_info(int64_t B, int64_t D, int world, int rank, int* bits);
 int disco_b200_forward_wave(void* ws, int64_t B, int64_t D, int world, int rank, float t, int wave, void* stream);
 int disco_b200_forward_finish(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
@@ -178,14 +185,7 @@ int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int ran
 /* Backward parts 2 + 3 in one persistent launch (single rank, where no slab
  * exchange has to overlap the intra GEMM): the intra and cross units are
  * interleaved in proportion to their counts.  Same outputs as
- * disco_b200_backward_cross followed by disco_b200_backward_intra.
- *
- * Fused single-rank backward (DISCO_PATH_HFUSE, disco_b200_path_info; opt-in with DISCO_HFUSE=1,
- * at N = 1 for Dp % 512 == 0 and B >= 4096): every cross term pairs with an intra
- * term over the same block, so backward_fused / backward_rows / backward_intra run one GEMM per
- * gradient on H = G_d + G_d'^T (formed in shared memory) into DISCO_R_INTRA, backward_cross is a
- * no-op, and combine / combine_rows / contribution read no cross partials.  Within 1e-3 of the
- * f64 oracle like every path, but not bitwise equal to N > 1 (one more f16 rounding). */
+ * disco_b200_backward_cross followed by disco_b200_backward_intra. */
 int disco_b200_backward_fused(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
 
 /* Owner combine after the slab exchange (replaces all_reduce(AVG) +
@@ -268,9 +268,33 @@ int disco_b200_combine_peer(void* ws, int64_t B, int64_t D, int world, int rank,
 int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,
                             float* d_image_full, float* d_text_full, int64_t ld_out, void* stream);
 
+/* Dual backward (DISCO_PATH_DUAL; disco_step's backward for canonical shapes at every N).
+ * The gradient of rank n's rows needs, besides its own softmax rows G_d[r, :], the other
+ * direction's softmax at column r of every row c, G_d'[c, r] = exp2(y[r, c] - lse2_d'[c]) --
+ * a logit rank n already holds in its own E block.  So after the forward (whose per-row lse2 and
+ * ce land in DISCO_R_XCHG) the ranks all_gather DISCO_R_XCHG into DISCO_R_XALL (4 b floats per
+ * rank; nothing to do at N = 1), and then:
+ *   dual_prep      column factors from the gathered statistics (flip != 0: the flip hook's sign
+ *                  on columns outside this rank's rows, shard.py:158-162);
+ *   backward_dual  one GEMM per gradient, H'_d = 2^14 (G_d + G_d'^T) formed in shared memory
+ *                  from E, rows [row0, row1) (256-aligned or row1 == b) into DISCO_R_INTRA;
+ *   combine_dual   d = 0.5 t / B (2^-14 (K halves) + label term in fp32) for rows [row0, row1);
+ *   dual_fixup     exact fp32 recompute of the rows whose E range could not carry a column term
+ *                  (queued by backward_dual; the count is Status offset 12; normally none).
+ * Together they replace the reference's all_reduce(AVG) + slice (shard.py:199-208) with results
+ * bitwise independent of N (every reduction is a fixed function of B). */
+int disco_b200_dual_prep(void* ws, int64_t B, int64_t D, int world, int rank, int flip, void* stream);
+int disco_b200_backward_dual(void* ws, int64_t B, int64_t D, int world, int rank, int64_t row0, int64_t row1,
+                             void* stream);
+int disco_b200_combine_dual(void* ws, int64_t B, int64_t D, int world, int rank, float t, int64_t row0, int64_t row1,
+                            float* d_image, float* d_text, int64_t ld_out, void* stream);
+int disco_b200_dual_fixup(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip, float* d_image,
+                          float* d_text, int64_t ld_out, void* stream);
+
 /* Loss: fixed-order f64 sum of the gathered per-row ce (DISCO_R_CE_ALL, or
- * DISCO_R_CE when world == 1 or local_only) / (2 * rows) into DISCO_R_STATUS.
- * local_only=1 gives the rank's local_loss (shard.py:140-141). */
+ * DISCO_R_CE when world == 1 or local_only == 1) / (2 * rows) into DISCO_R_STATUS.
+ * local_only=1 gives the rank's local_loss (shard.py:140-141); local_only=2 reads every rank's ce
+ * from the dual backward's gathered statistics (DISCO_R_XALL). */
 int disco_b200_loss(void* ws, int64_t B, int64_t D, int world, int rank, int local_only, void* stream);
 
 /* Logit-scale gradient (the reference has none).

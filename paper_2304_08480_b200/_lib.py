@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_disco_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "disco_b200.h")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # status codes (disco_status)
 OK, SHAPE, LAYOUT, DOMAIN, NONFINITE, CUDA = 0, 1, 2, 3, 4, 5
@@ -25,7 +25,7 @@ F32, BF16, F64, F16 = 0, 1, 2, 3
 
 # workspace regions (disco_region)
 R_PACK, R_GATHER, R_FEAT, R_FEAT16, R_STATS, R_ROWS, R_CE, R_CE_ALL, R_G, R_XPART, R_SEND, R_RECV, \
-    R_INTRA, R_STATUS, R_SCALE, R_RDOT, R_RDOT_ALL = range(17)
+    R_INTRA, R_STATUS, R_SCALE, R_RDOT, R_RDOT_ALL, R_XCHG, R_XALL, R_QCOL, R_FIX = range(21)
 
 _i64 = ctypes.c_int64
 _int = ctypes.c_int
@@ -82,6 +82,10 @@ SIGNATURES = {
     "disco_b200_loss": [_vp, _i64, _i64, _int, _int, _int, _vp],
     "disco_b200_logit_scale_rows": [_vp, _i64, _i64, _int, _int, _vp, _vp, _i64, _vp],
     "disco_b200_logit_scale_grad": [_vp, _i64, _i64, _int, _int, _f32, _vp],
+    "disco_b200_dual_prep": [_vp, _i64, _i64, _int, _int, _int, _vp],
+    "disco_b200_backward_dual": [_vp, _i64, _i64, _int, _int, _i64, _i64, _vp],
+    "disco_b200_combine_dual": [_vp, _i64, _i64, _int, _int, _f32, _i64, _i64, _vp, _vp, _i64, _vp],
+    "disco_b200_dual_fixup": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _vp, _i64, _vp],
     "disco_b200_l2norm_rows": [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp],
     "disco_b200_l2norm_rows_backward": [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp],
 }
@@ -166,7 +170,7 @@ def forward_waves(B: int, D: int, world: int, rank: int) -> int:
     return out.value
 
 
-PATH_ESTORE, PATH_WIDE, PATH_HFUSE, PATH_SYM = 1, 2, 4, 8
+PATH_ESTORE, PATH_WIDE, PATH_DUAL = 1, 2, 4
 
 
 def path_info(B: int, D: int, world: int, rank: int = 0) -> int:

@@ -85,6 +85,12 @@ constexpr int NUM_EPI_WARPS = 8;
 constexpr int NUM_XF_WARPS = 4;
 constexpr int NUM_THREADS_XF = NUM_THREADS + 32 * NUM_XF_WARPS;
 constexpr int GROUP_COLS = 64;    // E offset granularity: one exp2 offset per (row, 64-column group)
+// The forward stores E = exp2(y - m_g + E_HEADROOM) (m_g: the row's group max without the label),
+// values in (0, 2^15].  E-operand GEMMs therefore see scaled operands: the two-GEMM (exchange)
+// backward forms 2^15 G, the dual backward 2^14 H (H <= 2); the combines undo the power of two.
+constexpr float E_HEADROOM = 15.f;
+constexpr float G_EXCHANGE_SCALE = 32768.f;  // 2^E_HEADROOM
+constexpr float H_DUAL_LOG2 = 14.f;
 constexpr int TMEM_COLS = 512;    // 2 accumulators of 128 lanes x 256 fp32 columns
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -109,12 +115,15 @@ constexpr int ARES_SLICES = 8;
 constexpr int ARES_B_STAGES = 4;
 static_assert(ARES_SLICES * A_STAGE_BYTES + ARES_B_STAGES * B_STAGE_BYTES == TILE_RING_BYTES, "A-resident layout");
 static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory limit");
-// Fused single-rank backward: per ring stage, the stage's E -> G factors land by bulk copy beside
-// the tiles (after the control block): 128 row factors of direction d (256 B) + the direction-d'
-// factor vectors of the CTA's two 64-row groups (2 x 128 B).
-constexpr int HF_SCALE_BYTES = 512;
-constexpr size_t SMEM_BYTES_HF = SMEM_BYTES + size_t(Ring<2, 2>::STAGES) * HF_SCALE_BYTES;
-static_assert(SMEM_BYTES_HF <= 232448, "fused backward smem");
+// Dual backward (E-operand GEMMs, xform = 2): per ring stage, the q factors of the stage's 64 K
+// columns (256 B) land by bulk copy beside the tiles, after the control block.
+constexpr int DUAL_Q_BYTES = 64 * 4;
+constexpr size_t SMEM_BYTES_XF = SMEM_BYTES + size_t(STAGES) * DUAL_Q_BYTES;
+static_assert(SMEM_BYTES_XF <= 232448, "E-operand GEMM smem");
+// A row is fixed up (recomputed exactly, dual_fixup_kernel) when one of its groups' maxima exceeds
+// the smallest column LSE of the group by more than this (log2 units): only then can an E entry
+// below the f16 normal range (29 binades under m_g) carry >= 2^-12 of a column's softmax mass.
+constexpr float DUAL_SAFE_SPAN = 17.f;
 static_assert(sizeof(uint64_t) * 46 + 4 <= 512, "control block");
 
 // -------------------------------------------------------- status flag bits
@@ -127,7 +136,7 @@ constexpr int FLAG_H2D_TIMEOUT = 16;  // streamed forward: an H2D chunk never la
 struct Status {
   double loss;
   int flags;
-  int pad;
+  int fix_count;             // dual backward: rows queued for the exact recompute (DISCO_R_FIX)
   double dlogit;             // dL/d(logit scale), disco_b200_logit_scale_grad
   double loss_partial[128];  // loss_partial_kernel scratch (LOSS_BLOCKS)
   // clock probe (CTA 0 of the tensor-core kernels): {SM clock64, globaltimer ns} at entry and exit,
@@ -165,8 +174,6 @@ struct LogitsParams {
   // FWDE outputs: E = exp2(y - m_g) into the blocked G region, m_g per (dir, 64-column group, row)
   float* mg;            // [2][groups][b]
   int groups;           // B / 64 (GROUP_COLS)
-  // SYM (N = 1): dir-1 statistics per (64-row group of S_0, column): sum of E_1 without the label
-  float* ssum;          // [groups][B]
   // wave >= 0 (single rank, H2D-pipelined forward): only the units whose row chunk or column
   // chunk is `wave` and the other index <= wave, i.e. the units that became computable when
   // (stats sub-)chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per (sub-)chunk.
@@ -214,13 +221,16 @@ struct GemmProblem {
   const float* xlabel;    // [xb] label-column value P_label - 1
   int xb;                 // local rows b (pitch of xscale)
   int lab_off;            // rank * b: global column of local row 0's positive pair
-  // fused single-rank backward (hfuse, N = 1): A2 = the other direction's E over the same
-  // (row, K) block, staged MN-major beside A; the transform warps write H = G_d + G_d'^T into A,
-  // so one GEMM H . C replaces intra (G_d . C) + cross (G_d'^T . C): half the MMA work
-  int hfuse;
-  CUtensorMap a2_map;     // blocked E of direction d' (MN-major loads)
-  const __half* xscale2;  // [groups][xb] E -> G factors of direction d'
-  const float* xlabel2;   // [xb] label values of direction d'
+  // dual backward (xform = 2, K-major E rows of direction d): the transform warps write
+  // H' = 2^14 (G_d + G_d'^T) = E (a_r + p_r q_c) over the rank's own E block, with
+  // a_r = exp2(m_g - 1 - lse2_d[r]), p_r = exp2(m_g - 1 - Q_g), q_c = exp2(Q_g - lse2_d'[c]) (< 2^100)
+  const float* xmg;       // [groups][xb] group maxima m_g of direction d (f32)
+  const float* xlse;      // [xb] lse2 of direction d (this rank's rows)
+  const float* xq;        // [B] q_c (bulk-copied per stage; sign -1 under the flip hook)
+  const float2* xgm;      // [groups] (Q_g, smallest column lse2 of the group or -inf)
+  int* fix_list;          // rows needing the exact recompute: fix_tag + row
+  int* fix_count;
+  int fix_tag, fix_cap;
 };
 constexpr int MAX_PROBLEMS = 4;
 constexpr int MAX_SCHED_PAIRS = 80;
@@ -346,68 +356,25 @@ __device__ __forceinline__ uint8_t* producer_acquire(SmemCtl* ctl, uint8_t* tile
   return tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES;
 }
 
-// E -> G on one 128-byte smem row (64 f16 of one G row i, G columns [j0, j0 + 64)) of a
-// SWIZZLE_128B operand stage: multiply by the f16 factor sc (HMUL2); the label column
-// (j == lab) gets P_label - 1.  Logical 16-byte chunk c sits at physical c ^ (row & 7);
+// E -> 2^15 G on one 128-byte smem row (64 f16 of one G row i, G columns [j0, j0 + 64)) of a
+// SWIZZLE_128B operand stage: multiply by the f16 factor sc = exp2(m_g - lse2) (HMUL2; E carries
+// the 2^15 headroom); the label column (j == lab) gets 2^15 (P_label - 1).  Logical 16-byte chunk c sits at physical c ^ (row & 7);
 // walking physical chunks in lane order keeps the 8 rows of a quarter-warp on distinct banks.
-__device__ __forceinline__ void xform_row(uint8_t* rowp, int sw, __half sc, int lab_rel, float glab) {
+__device__ __forceinline__ void xform_row(uint32_t rowp, int sw, __half sc, int lab_rel, float glab) {
   const __half2 s2 = __half2half2(sc);  // packed f16 multiply: 4 HMUL2 per 16-byte chunk
   uint4 x[8];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) x[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ sw) << 4));
+  for (int c = 0; c < 8; ++c) x[c] = ptx::lds128(rowp + ((c ^ sw) << 4));
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     __half2* h = reinterpret_cast<__half2*>(&x[c]);
 #pragma unroll
     for (int k = 0; k < 4; ++k) h[k] = __hmul2(h[k], s2);
-    *reinterpret_cast<uint4*>(rowp + ((c ^ sw) << 4)) = x[c];
+    ptx::sts128(rowp + ((c ^ sw) << 4), x[c]);
   }
   if (unsigned(lab_rel) < 64u)
-    *reinterpret_cast<__half*>(rowp + ((((lab_rel >> 3) ^ sw)) << 4) + (lab_rel & 7) * 2) = __float2half_rn(glab);
-}
-
-// Symmetric single-rank forward (SYM, N = 1): S_1 = S_0^T, so one GEMM tile of S_0 feeds both
-// directions.  lane_scatter reduces a warp's 32 x 32 block down its rows: lane L ends with the
-// max / sum over the 32 lanes of column L (31 shuffles in a fixed butterfly, deterministic).
-template <bool MAX>
-__device__ __forceinline__ float lane_scatter(const float* v, int lane) {
-  float a[16];
-  {
-    const bool hi = lane & 16;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float keep = hi ? v[i + 16] : v[i], send = hi ? v[i] : v[i + 16];
-      const float got = __shfl_xor_sync(0xffffffffu, send, 16);
-      a[i] = MAX ? fmaxf(keep, got) : keep + got;
-    }
-  }
-#pragma unroll
-  for (int w = 8; w >= 1; w >>= 1) {
-    const bool hi = lane & w;
-#pragma unroll
-    for (int i = 0; i < w; ++i) {
-      const float keep = hi ? a[i + w] : a[i], send = hi ? a[i] : a[i + w];
-      const float got = __shfl_xor_sync(0xffffffffu, send, w);
-      a[i] = MAX ? fmaxf(keep, got) : keep + got;
-    }
-  }
-  return a[0];
-}
-
-// A warp's 32 x 32 f16 block stored transposed into a 32-row x 64-byte SWIZZLE_64B staging tile:
-// lane r holds w[k] = (row r; columns 2k, 2k+1), tile row c receives column c of all 32 lanes.
-// A 2 x 2 exchange inside lane pairs forms (row 2m, row 2m + 1) words, so each STS is 32-bit and
-// one instruction fills two whole tile rows (bank-conflict-free).
-__device__ __forceinline__ void st_transposed_64(uint8_t* tile, int lane, const uint32_t* w) {
-  const int odd = lane & 1, m = lane >> 1;
-  const uint32_t sel = odd ? 0x3276u : 0x5410u;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const uint32_t o = __shfl_xor_sync(0xffffffffu, w[k], 1);
-    const uint32_t x = __byte_perm(w[k], o, sel);
-    const int c = 2 * k + odd;
-    *reinterpret_cast<uint32_t*>(tile + c * 64 + (((m >> 2) ^ ((c >> 1) & 3)) << 4) + (m & 3) * 4) = x;
-  }
+    ptx::sts16(rowp + (((lab_rel >> 3) ^ sw) << 4) + (lab_rel & 7) * 2,
+               __half_as_ushort(__float2half_rn(glab * G_EXCHANGE_SCALE)));
 }
 
 // Clock probe: CTA 0, thread 0 records {clock64, globaltimer} at slot [at, at + 1].
@@ -487,14 +454,6 @@ enum { KIND_FWD = 0, KIND_GRAD = 1, KIND_FWDE = 2 };
 // column tiles of the unit and only B streams through a 4-stage ring; A slice k of the next unit
 // is reloaded as soon as the unit's last tile has consumed it.  Halves the TMA fill traffic and
 // cuts smem traffic per MMA from ~128 to ~96 B/clk/SM (the narrow 256-column tile is smem-bound).
-// SYM (FWDE, N = 1): units cover direction 0 only; each epilogue warp also emits the t2i E block
-// of its 32 x 32 half slices (column maxima over the 64-row group shared with the partner warp
-// through shared memory, E_1 stored transposed) and the dir-1 group sums.  5-stage ring so that
-// three staging half-buffers per warp fit.
-constexpr int SYM_STAGES = 5;
-constexpr int SYM_EBUFS = 3;
-static_assert(SYM_STAGES * STAGE_BYTES + NUM_EPI_WARPS * (SYM_EBUFS * STAGING_TILE / 2 + 256) <=
-                  TILE_RING_BYTES + STAGING_BYTES, "SYM smem layout");
 #ifndef DISCO_FWD_STAGES
 #define DISCO_FWD_STAGES 6
 #endif
@@ -536,27 +495,25 @@ constexpr int FWDE_STAGES = FWDE_EPI == 16 ? 5 : FWD_STAGES;
 static_assert(FWDE_EPI == 8 || FWDE_EPI == 16, "FWDE epilogue warps");
 static_assert(FWDE_STAGES * STAGE_BYTES + FWDE_EPI * FWD_EBUFS * (STAGING_TILE / 2) <= TILE_RING_BYTES + STAGING_BYTES,
               "FWDE smem layout");
-template <int KIND, bool ARES, bool SYM>
-__host__ __device__ constexpr int logits_epi() { return (KIND == KIND_FWDE && !SYM && !ARES) ? FWDE_EPI : NUM_EPI_WARPS; }
-template <int KIND, bool ARES, bool SYM>
-__host__ __device__ constexpr int logits_threads() { return 64 + 32 * logits_epi<KIND, ARES, SYM>(); }
+template <int KIND, bool ARES>
+__host__ __device__ constexpr int logits_epi() { return (KIND == KIND_FWDE && !ARES) ? FWDE_EPI : NUM_EPI_WARPS; }
+template <int KIND, bool ARES>
+__host__ __device__ constexpr int logits_threads() { return 64 + 32 * logits_epi<KIND, ARES>(); }
 // statistics parts per (row, sub-chunk) the FWDE / FWD kernels write: one per epilogue column part
 constexpr int FWDE_PARTS = FWDE_EPI / 4;
 
-template <int KIND, bool ARES, bool SYM = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND, ARES, SYM>(), 1)
+template <int KIND, bool ARES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND, ARES>(), 1)
     logits_kernel(const __grid_constant__ LogitsParams p) {
-  static_assert(!SYM || (KIND == KIND_FWDE && !ARES), "SYM is a FWDE variant");
-  constexpr int EPI = logits_epi<KIND, ARES, SYM>();    // epilogue warps
+  constexpr int EPI = logits_epi<KIND, ARES>();          // epilogue warps
   constexpr int NPARTS = EPI / 4;                        // column parts of a 256-column tile
   constexpr int PART_COLS = BN / NPARTS;                 // columns per epilogue warp and tile
-  constexpr int LRS = SYM ? SYM_STAGES : (EPI == 16 ? FWDE_STAGES : FWD_STAGES);  // operand ring stages
-  constexpr int EBUFS = SYM ? SYM_EBUFS : FWD_EBUFS;   // E staging half-buffers per warp
-  constexpr int NDIR = SYM ? 1 : 2;                         // directions walked by the units
+  constexpr int LRS = EPI == 16 ? FWDE_STAGES : FWD_STAGES;  // operand ring stages
+  constexpr int EBUFS = FWD_EBUFS;                           // E staging half-buffers per warp
+  constexpr int NDIR = 2;                                    // directions walked by the units
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
   uint8_t* staging = tiles + (ARES ? TILE_RING_BYTES : LRS * STAGE_BYTES);
-  float* xbuf = reinterpret_cast<float*>(staging + NUM_EPI_WARPS * EBUFS * (STAGING_TILE / 2));  // SYM: [8][64]
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + TILE_RING_BYTES + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int crank = int(ptx::cluster_ctarank());
@@ -585,7 +542,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
   const int num_units = colwaves ? per_cwave * p.nwaves
                                  : streamed ? NDIR * p.rt_per_chunk * p.nwaves * p.nwaves : NDIR * per_dir;
   // -2: unit u belongs to wave k with 2 R k^2 <= u < 2 R (k+1)^2 (wave k holds 2 R (2k+1));
-  // SYM: R k^2 <= u < R (k+1)^2
   auto wave_of = [&](int u) {
     if (colwaves) return u / per_cwave;
     int k = int(sqrtf(float(u) / float(NDIR * p.rt_per_chunk)));
@@ -778,7 +734,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (epend_rb < (epend_dir && SYM ? p.B : p.b))
+        if (epend_rb < p.b)
           ptx::tma_store_4d(&p.e_map[epend_dir], tile + epend_buf * (STAGING_TILE / 2), epend_cb & 127,
                             epend_rb & 127, epend_cb >> 7, epend_rb >> 7);
         ptx::bulk_commit();
@@ -892,9 +848,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
                 va[i] = __uint_as_float(ra[i]);
                 vb[i] = __uint_as_float(rb[i]);
               }
-              if (j + 1 < NJ && !SYM) {  // the next slice's TMEM loads fly while this one is computed
+              if (j + 1 < NJ) {  // the next slice's TMEM loads fly while this one is computed
                 ptx::tmem_ld32_async(taddr + 64 * (j + 1), ra);
                 ptx::tmem_ld32_async(taddr + 64 * (j + 1) + 32, rb);
+              }
+              // The label column leaves the group max, the sum and E: its logit goes to yt and the
+              // element becomes -inf (so E = 0 there).  li - 64 j = lane + 32 m (labels and columns
+              // are 32-aligned), so "this group holds the warp's labels" is warp-uniform and lane
+              // L's label is element L of half m.
+              const int lj = li - j * 64;
+              if (unsigned(lj) < 32u) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (i == lane) {
+                    yt = va[i] * p.tl2e;
+                    va[i] = -INFINITY;
+                  }
+                has_t = true;
+              } else if (unsigned(lj - 32) < 32u) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (i == lane) {
+                    yt = vb[i] * p.tl2e;
+                    vb[i] = -INFINITY;
+                  }
+                has_t = true;
               }
               float mx[32];  // max over the 64 columns as a depth-6 tree
 #pragma unroll
@@ -904,35 +882,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
 #pragma unroll
                 for (int i = 0; i < w; ++i) mx[i] = fmaxf(mx[i], mx[i + w]);
               const float cm = mx[0];
-              const float mg = cm * p.tl2e;
-              const float2 nmg = make_float2(-mg, -mg);
-              float2 s2 = make_float2(0.f, 0.f);  // (even-column sum, odd-column sum)
+              const float mg = cm * p.tl2e;  // group max of y, label excluded
+              // E = exp2(y - mg + E_HEADROOM) in (0, 2^15]: the headroom keeps entries down to 29
+              // binades below the group max normal in f16, which the dual backward's column term
+              // needs (it rescales the row-offset E by the column statistics)
+              const float2 nmg = make_float2(E_HEADROOM - mg, E_HEADROOM - mg);
+              float2 s2 = make_float2(0.f, 0.f);  // (even-column sum, odd-column sum), label excluded
               uint32_t h[32];
 #pragma unroll
               for (int half = 0; half < 2; ++half) {
                 const float* v = half ? vb : va;
-                const int lg = li - (j * 64 + half * 32);
-                if (unsigned(lg) >= 32u) {  // warp-uniform: a warp's 32 labels share a 32-column group
 #pragma unroll
-                  for (int i = 0; i < 32; i += 2) {
-                    const float2 y = fwde_y(v[i], v[i + 1], tl2, nmg);
-                    const float e0 = ptx::ex2(y.x), e1 = ptx::ex2(y.y);
-                    s2 = fwde_acc(s2, e0, e1);
-                    __half2 hh = __floats2half2_rn(e0, e1);
-                    h[half * 16 + i / 2] = *reinterpret_cast<uint32_t*>(&hh);
-                  }
-                } else {  // the label term stays out of the sum (adding +0 leaves it unchanged)
-#pragma unroll
-                  for (int i = 0; i < 32; i += 2) {
-                    const float2 y = fwde_y(v[i], v[i + 1], tl2, nmg);
-                    const float e0 = ptx::ex2(y.x), e1 = ptx::ex2(y.y);
-                    if (i == lg) yt = v[i] * p.tl2e;
-                    if (i + 1 == lg) yt = v[i + 1] * p.tl2e;
-                    s2 = fwde_acc(s2, i == lg ? 0.f : e0, i + 1 == lg ? 0.f : e1);
-                    __half2 hh = __floats2half2_rn(e0, e1);
-                    h[half * 16 + i / 2] = *reinterpret_cast<uint32_t*>(&hh);
-                  }
-                  has_t = true;
+                for (int i = 0; i < 32; i += 2) {  // the label element is -inf: E = 0, out of the sum
+                  const float2 y = fwde_y(v[i], v[i + 1], tl2, nmg);
+                  const float e0 = ptx::ex2(y.x), e1 = ptx::ex2(y.y);
+                  s2 = fwde_acc(s2, e0, e1);
+                  __half2 hh = __floats2half2_rn(e0, e1);
+                  h[half * 16 + i / 2] = *reinterpret_cast<uint32_t*>(&hh);
                 }
                 // Half-slice store pipeline: this half goes into staging half-buffer `ebuf`; the
                 // previous half, written one compute phase ago, is fenced and TMA-stored first, so
@@ -940,58 +906,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
                 const int rbase = rt * PAIR_M + crank * BM + quad * 32;
                 const int hcb = col0 + j * 64 + half * 32;
                 e_push([&](uint8_t* hb) { ptx::st_swizzled_row64(hb, lane, h + half * 16); }, hcb, rbase, dir);
-                if constexpr (SYM) {
-                  // t2i half slice: rows hcb.. of S_1 = columns of this block, columns rbase.. .
-                  // m_1 = max over the 64-row group (this warp + partner warp ew ^ 1, same columns).
-                  float* xb = xbuf + ew * 64;
-                  const float* xo = xbuf + (ew ^ 1) * 64;
-                  const int pbar = 1 + (ew >> 1);
-                  xb[lane] = lane_scatter<true>(v, lane);
-                  ptx::named_bar_sync(pbar, 64);
-                  float e1[32];
-#pragma unroll
-                  for (int q = 0; q < 8; ++q) {
-                    const float4 a4 = reinterpret_cast<const float4*>(xb)[q];
-                    const float4 o4 = reinterpret_cast<const float4*>(xo)[q];
-                    e1[4 * q + 0] = ptx::ex2(fmaf(v[4 * q + 0], p.tl2e, -(fmaxf(a4.x, o4.x) * p.tl2e)));
-                    e1[4 * q + 1] = ptx::ex2(fmaf(v[4 * q + 1], p.tl2e, -(fmaxf(a4.y, o4.y) * p.tl2e)));
-                    e1[4 * q + 2] = ptx::ex2(fmaf(v[4 * q + 2], p.tl2e, -(fmaxf(a4.z, o4.z) * p.tl2e)));
-                    e1[4 * q + 3] = ptx::ex2(fmaf(v[4 * q + 3], p.tl2e, -(fmaxf(a4.w, o4.w) * p.tl2e)));
-                  }
-                  const float m1 = fmaxf(xb[lane], xo[lane]) * p.tl2e;  // column hcb + lane's offset
-                  uint32_t h1[16];
-#pragma unroll
-                  for (int k = 0; k < 16; ++k) {
-                    __half2 hh = __floats2half2_rn(e1[2 * k], e1[2 * k + 1]);
-                    h1[k] = *reinterpret_cast<uint32_t*>(&hh);
-                  }
-                  if (hcb == rbase) {  // warp-uniform: the diagonal (labels) is element (lane, lane)
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) e1[i] = i == lane ? 0.f : e1[i];
-                  }
-                  const float cs = lane_scatter<false>(e1, lane);
-                  e_push([&](uint8_t* hb) { st_transposed_64(hb, lane, h1); }, rbase, hcb, 1);
-                  xb[32 + lane] = cs;
-                  ptx::named_bar_sync(pbar, 64);
-                  if (!(quad & 1)) {  // the group's lower warp: fixed order (rows 0-31) + (rows 32-63)
-                    const int64_t at = int64_t(rbase >> 6) * p.B + hcb + lane;
-                    p.mg[int64_t(p.groups) * p.b + at] = m1;
-                    p.ssum[at] = xb[32 + lane] + xo[32 + lane];
-                  }
-                }
               }
               const int cb = col0 + j * 64;
               const float mnew = fmaxf(m2, mg);
-              l = l * ptx::ex2(m2 - mnew) + (s2.x + s2.y) * ptx::ex2(mg - mnew);
+              l = l * ptx::ex2(m2 - mnew) + (s2.x + s2.y) * ptx::ex2(mg - E_HEADROOM - mnew);
               m2 = mnew;
               if (row_ok) p.mg[(int64_t(dir) * p.groups + cb / GROUP_COLS) * p.b + row] = mg;
-              if (j + 1 < NJ) {
-                if (SYM) {  // registers: SYM loads slice 1 only after slice 0 (168-register cap)
-                  ptx::tmem_ld32_async(taddr + 64 * (j + 1), ra);
-                  ptx::tmem_ld32_async(taddr + 64 * (j + 1) + 32, rb);
-                }
-                ptx::tmem_wait_ld_dep(ra, rb);
-              }
+              if (j + 1 < NJ) ptx::tmem_wait_ld_dep(ra, rb);
             }
           }
         } else {
@@ -1066,7 +987,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
         p.stats[((int64_t(dir) * p.nchunk + ch) * NPARTS + cpart) * p.b + row] = make_float2(m2, l);
         if (has_t) {
           p.target[dir * p.b + row] = yt;
-          if (SYM) p.target[p.b + row] = yt;  // S_1[r, r] = S_0[r, r]
         }
       }
     }
@@ -1084,18 +1004,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
 //   into the two TMEM buffers and summed in the epilogue ((c0 + c1): the first
 //   level of the fixed reduction tree).
 // =====================================================================
-template <int NB, bool XF, bool HF = false>
+template <int NB, bool XF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF : NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ GemmParams p) {
-  constexpr int NA = HF ? 2 : 1;  // A tiles per stage
+  constexpr int NA = 1;  // A tiles per stage
   constexpr int RS = Ring<NB, NA>::STAGES;
   static_assert(NB == 1 || NB == 2, "one or two N tiles per unit");
-  static_assert(!HF || (XF && NB == 2), "the fused single-rank backward is a wide E-operand GEMM");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
   uint8_t* staging = tiles + TILE_RING_BYTES;
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + TILE_RING_BYTES + STAGING_BYTES);
-  uint8_t* hf_scales = reinterpret_cast<uint8_t*>(ctl) + 512;  // HF: [RS][HF_SCALE_BYTES] (SMEM_BYTES_HF)
+  uint8_t* qrec = reinterpret_cast<uint8_t*>(ctl) + 512;  // dual: [RS][DUAL_Q_BYTES] (SMEM_BYTES_XF)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int crank = int(ptx::cluster_ctarank());
   const bool leader = crank == 0;
@@ -1105,7 +1024,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     for (int i = 0; i < p.nprob; ++i) {
       ptx::prefetch_tmap(&p.prob[i].a_map);
       ptx::prefetch_tmap(&p.prob[i].b_map);
-      if (HF) ptx::prefetch_tmap(&p.prob[i].a2_map);
       if (p.prob[i].tma_store && !p.prob[i].peer) ptx::prefetch_tmap(&p.prob[i].out_map);
       for (int r = 0; r < (p.prob[i].peer ? p.prob[i].M / p.prob[i].peer_b : 0); ++r)
         ptx::prefetch_tmap(&p.prob[i].peer_map[r]);
@@ -1157,8 +1075,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           k_range(q, kc * (1 + q.paired) + sub, k0, nk);
           for (int kb = 0; kb < nk; ++kb) {
             uint32_t bar;
+            const bool dual = XF && q.xform == 2;
             uint8_t* st = producer_acquire<NB, XF, RS, NA>(ctl, tiles, pipe, leader, bar, crank,
-                                                           HF ? HF_SCALE_BYTES : 0);
+                                                           dual ? DUAL_Q_BYTES : 0);
             const int k = k0 + kb * BK;
             if (q.a_blocked)
               load_blocked(&q.a_map, q.a_mn_major, st, bar, m0, k, BM, ptx::kEvictFirst);
@@ -1166,15 +1085,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
               load_operand(&q.a_map, 1, st, bar, m0, k + q.a_k_off, BM, ptx::kEvictFirst);
             else
               load_operand(&q.a_map, 0, st, bar, m0 + q.a_row_off, k, BM, ptx::kEvictFirst);
-            if (HF) {
-              load_blocked(&q.a2_map, 1, st + A_STAGE_BYTES, bar, m0, k, BM, ptx::kEvictFirst);
-              // the stage's factors: direction d rows [m0, m0 + 128) at K-group k / 64, and the
-              // direction-d' vectors (columns [k, k + 64)) of the two 64-row groups
-              const uint32_t sd = ptx::smem_u32(hf_scales + pipe.stage * HF_SCALE_BYTES);
-              ptx::bulk_g2s(sd, q.xscale + int64_t(k >> 6) * q.xb + m0, 256, bar);
-              ptx::bulk_g2s(sd + 256, q.xscale2 + int64_t(m0 >> 6) * q.xb + k, 128, bar);
-              ptx::bulk_g2s(sd + 384, q.xscale2 + int64_t((m0 >> 6) + 1) * q.xb + k, 128, bar);
-            }
+            if (dual)  // the stage's 64 column factors q_c
+              ptx::bulk_g2s(ptx::smem_u32(qrec + pipe.stage * DUAL_Q_BYTES), q.xq + k, DUAL_Q_BYTES, bar);
 #pragma unroll
             for (int j = 0; j < NB; ++j)
               load_operand(&q.b_map, q.b_mn_major, st + NA * A_STAGE_BYTES + j * B_STAGE_BYTES, bar, n0 + j * BN,
@@ -1198,12 +1110,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           int k0, nk;
           k_range(q, kc, k0, nk);
           const uint32_t ph = ((it >> 1) & 1) ^ 1;
-          if (HF) {
-            ptx::mbar_wait(&ctl->tempty[0], ph);
-            ptx::mbar_wait(&ctl->tempty[1], ph);
-            ptx::tc_fence_after();
-            mma_tile<NB, XF, RS, NA>(ctl, tiles, pipe, nk, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major);
-          } else {
+          {
             // The epilogue releases accumulator 0 half-way through its drain: issue the unit's first
             // ring-full of k-blocks into accumulator 0 alone (the stages stay resident), then, once
             // accumulator 1 is free, the same stages into accumulator 1, releasing them, then the rest
@@ -1240,90 +1147,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
         }
       }
     }
-  } else if (XF && HF && warp >= 2 + NUM_EPI_WARPS) {  // ---------- transform warps 10..13 (fused)
-    // Fused single-rank backward: the stage holds A = E_d (K-major, rows = output rows) and A2 =
-    // E_d' over the same block (MN-major: K-rows = E_d' rows).  Warp xw builds rows
-    // [32 xw, 32 xw + 32) of H = G_d + G_d'^T in place of A as 8 blocks of 16 x 16: ldmatrix.x4
-    // fragments of E_d, ldmatrix.x4.trans fragments of E_d' (the transpose lands in the same
-    // fragment positions), H = E_d * s (row factor) + E_d'^T * s' (column factor), stmatrix.x4.
-    // Lane 8j + i addresses row i of matrix j (j & 1: rows +8, j >> 1: columns +8); thread t holds
-    // (row t / 4 (+8), columns 2 (t % 4) + {0, 1} (+8)).
-    const int xw = (threadIdx.x - 32 * (2 + NUM_EPI_WARPS)) >> 5;
-    const int mj = lane >> 3, mi = lane & 7;
-    const int tr = lane >> 2, tc = 2 * (lane & 3);
-    Pipe<RS> pipe;
-    for (int uk = 0; uk < my_units; ++uk) {
-      const int u = unit_at(uk);
-      int pi, mt, nt, kc;
-      decode(u, pi, mt, nt, kc);
-      const GemmProblem& q = p.prob[pi];
-      const int m0 = mt * PAIR_M + crank * BM;
-      const int wr0 = m0 + 32 * xw;  // first output row of this warp
-      float glab[4];  // label values of this thread's 4 rows (16 rb + 8 h + t / 4)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = wr0 + 16 * (j >> 1) + 8 * (j & 1) + tr;
-        glab[j] = q.xlabel[r] + q.xlabel2[r];
-      }
-      int k0, nk;
-      k_range(q, kc, k0, nk);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int k = k0 + kb * BK;
-        ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
-        if (!(XP && (q.ablate & 1024))) {
-          const uint32_t abase = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES);
-          const uint32_t a2base = abase + A_STAGE_BYTES;
-          // the stage's factors (bulk-copied by the producer with the tiles)
-          const uint8_t* sd = hf_scales + pipe.stage * HF_SCALE_BYTES;
-          __half s0[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            s0[j] = reinterpret_cast<const __half*>(sd)[32 * xw + 16 * (j >> 1) + 8 * (j & 1) + tr];
-          uint32_t s1[8];
-          const uint32_t* s1p = reinterpret_cast<const uint32_t*>(sd + 256 + (xw >> 1) * 128 + tc * 2);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) s1[c] = s1p[4 * c];
-          // labels: global column lab_off + row; this stage holds columns [k, k + 64)
-          const int dl = q.lab_off + wr0 - k;  // label column of the warp's row 0, stage-relative
-          const bool diag = dl > -32 && dl < 64;
-#pragma unroll
-          for (int rb = 0; rb < 2; ++rb) {
-#pragma unroll
-            for (int cb = 0; cb < 4; ++cb) {
-              const int row = 32 * xw + 16 * rb + 8 * (mj & 1) + mi;  // A-tile row this lane addresses
-              const int ch = 2 * cb + (mj >> 1);                       // its 16-byte chunk (8 columns)
-              const uint32_t aaddr = abase + row * 128 + ((ch ^ (row & 7)) << 4);
-              const int R = 32 * xw + 16 * rb + 8 * (mj & 1);          // matrix's first row
-              const int c = 8 * ch + mi;                               // A2 K-row (E_d' row) addressed
-              const uint32_t baddr = a2base + (R >> 6) * 8192 + c * 128 + ((((R & 63) >> 3) ^ (c & 7)) << 4);
-              uint32_t e0[4], e1[4], hv[4];
-              ptx::ldmatrix_x4(e0, aaddr);
-              ptx::ldmatrix_x4_trans(e1, baddr);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const __half2 sr = __half2half2(s0[2 * rb + (j & 1)]);
-                const __half2 sc = *reinterpret_cast<const __half2*>(&s1[2 * cb + (j >> 1)]);
-                __half2 h = __hfma2(*reinterpret_cast<const __half2*>(&e1[j]), sc,
-                                    __hmul2(*reinterpret_cast<const __half2*>(&e0[j]), sr));
-                if (diag) {  // warp-uniform; element (row, col) is a label iff col == dl + row
-                  const int rr = 16 * rb + 8 * (j & 1) + tr;            // warp-relative row
-                  const int cc = 16 * cb + 8 * (j >> 1) + tc;           // stage-relative column
-                  const __half gl = __float2half_rn(glab[2 * rb + (j & 1)]);
-                  if (cc == dl + rr) h.x = gl;
-                  if (cc + 1 == dl + rr) h.y = gl;
-                }
-                hv[j] = *reinterpret_cast<uint32_t*>(&h);
-              }
-              ptx::stmatrix_x4(aaddr, hv);
-            }
-          }
-          ptx::fence_proxy_async_smem();
-        }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(ptx::map_to_rank(&ctl->xfull[pipe.stage], 0));
-        pipe.advance();
-      }
-    }
   } else if (XF && warp >= 2 + NUM_EPI_WARPS) {  // ---------------- transform warps 10..13
     // Thread xt owns one 128-byte row of this CTA's A stage:
     //   K-major A (intra, G rows = M): row xt = G row m0 + xt, G columns [k, k + 64);
@@ -1339,6 +1162,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       decode(u, pi, mt, nt, kc);
       const GemmProblem& q = p.prob[pi];
       const int m0 = mt * PAIR_M + crank * BM;
+      if (q.xform == 2) {
+        // Dual backward: thread xt owns row r = m0 + xt of this direction's E block (K-major) and
+        // rewrites each 64-column stage to H' = E (a_r + p_r q_c) in fp32 (one f16 rounding).  The
+        // label column is zeroed (its fp32 value is added by the combine).  The row's group
+        // maxima and the group metadata run XPF stages ahead.
+        const int r = m0 + xt;
+        const bool act = r < q.xb;  // rows past b were zero-filled by TMA: nothing to transform
+        const float lse_r = act ? q.xlse[r] : 0.f;
+        const int sw = xt & 7;
+        int k0, nk;
+        k_range(q, kc, k0, nk);
+        constexpr int XPF = 4;
+        auto ld_mg = [&](int kb) { return (act && kb < nk) ? q.xmg[int64_t((k0 + kb * BK) >> 6) * q.xb + r] : 0.f; };
+        auto ld_gm = [&](int kb) { return kb < nk ? q.xgm[(k0 + kb * BK) >> 6] : make_float2(0.f, 0.f); };
+        float mq[XPF];
+        float2 gq[XPF];
+#pragma unroll
+        for (int i = 0; i < XPF; ++i) {
+          mq[i] = ld_mg(i);
+          gq[i] = ld_gm(i);
+        }
+        bool unsafe = false;
+        for (int kb0 = 0; kb0 < nk; kb0 += XPF) {
+#pragma unroll
+          for (int i = 0; i < XPF; ++i) {
+            const int kb = kb0 + i;
+            if (kb >= nk) break;
+            const int k = k0 + kb * BK;
+            const float mg = mq[i];
+            const float2 gm = gq[i];
+            mq[i] = ld_mg(kb + XPF);
+            gq[i] = ld_gm(kb + XPF);
+            ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
+            if (act) {
+              unsafe |= mg - gm.y > DUAL_SAFE_SPAN;
+              const float a = ptx::ex2(mg + (H_DUAL_LOG2 - E_HEADROOM) - lse_r), pr = ptx::ex2(mg + (H_DUAL_LOG2 - E_HEADROOM) - gm.x);
+              const float2 a2 = make_float2(a, a), p2 = make_float2(pr, pr);
+              const uint32_t rowp = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES + xt * 128);
+              const uint32_t qs = ptx::smem_u32(qrec + pipe.stage * DUAL_Q_BYTES);
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                uint4 x = ptx::lds128(rowp + ((c ^ sw) << 4));
+                const float4 q0 = ptx::lds128f(qs + 32 * c), q1 = ptx::lds128f(qs + 32 * c + 16);
+                const float2 qv[4] = {make_float2(q0.x, q0.y), make_float2(q0.z, q0.w), make_float2(q1.x, q1.y),
+                                      make_float2(q1.z, q1.w)};
+                __half2* h = reinterpret_cast<__half2*>(&x);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  h[e] = __float22half2_rn(ptx::fmul2(__half22float2(h[e]), ptx::ffma2(p2, qv[e], a2)));
+                ptx::sts128(rowp + ((c ^ sw) << 4), x);
+              }
+              const int lab_rel = q.lab_off + r - k;
+              if (unsigned(lab_rel) < 64u) ptx::sts16(rowp + (((lab_rel >> 3) ^ sw) << 4) + (lab_rel & 7) * 2, 0);
+              ptx::fence_proxy_async_smem();
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(ptx::map_to_rank(&ctl->xfull[pipe.stage], 0));
+            pipe.advance();
+          }
+        }
+        if (unsafe) {
+          const int slot = atomicAdd(q.fix_count, 1);
+          if (slot < q.fix_cap) q.fix_list[slot] = q.fix_tag + r;
+        }
+        continue;
+      }
       const int rowoff = q.a_mn_major ? (xt >> 6) * 8192 + (xt & 63) * 128 : xt * 128;
       const int sw = (rowoff >> 7) & 7;
       // per-stage scale index (64-column groups): K-major: (k / 64) * xb + (m0 + xt);
@@ -1371,7 +1260,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             sq[r] = ld_scale(kb + XPF);
             ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
             if (active && !(XP && (q.ablate & 1024))) {
-              uint8_t* rowp = tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES + rowoff;
+              const uint32_t rowp = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES + rowoff);
               int lab_rel;
               float glab;
               if (q.a_mn_major) {  // row = G row i = k + xt % 64; label column lab_off + i
@@ -1422,7 +1311,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
         orow = q.out + kc * q.chunk_stride + (row / q.row_div) * q.stride_hi + (row % q.row_div) * q.ld_out;
       const int z = int(row0 / q.row_div) + kc;
       const int rlo = int(row0 % q.row_div);
-      if (NB == 2 && !HF && q.tma_store == 1 && !(XP && (q.skip_store || q.ablate))) {
+      if (NB == 2 && q.tma_store == 1 && !(XP && (q.skip_store || q.ablate))) {
         // Wide drain, software-pipelined: slice jj + 1's TMEM load is in flight while slice jj is
         // staged and TMA-stored, and accumulator 0 is released as soon as its last slice sits in
         // registers, so the MMA starts the next unit (accumulator 0 half) during this drain.
@@ -1644,6 +1533,7 @@ __global__ void pack_kernel(const void* I, const void* Tm, int64_t ldI, int64_t 
 __global__ void clear_status_kernel(Status* s) {
   s->loss = 0.0;
   s->flags = 0;
+  s->fix_count = 0;
 }
 
 // gathered [N][2][b][Dp] bf16 -> feat [2][B][Dp] bf16 and feat16 [2][B][Dp] f16. 8 elements per thread.
@@ -1698,15 +1588,18 @@ __global__ void feat16_kernel(const uint4* feat, uint4* feat16, int64_t n, Statu
 // ssub: stats sub-chunks per canonical chunk (the forward's units cover one sub-chunk); a chunk's
 // sum is the fixed tree over its (sub-chunk, column half) partials.
 // Shared tail: (m, lo = sum of non-label terms relative to m, target yt) -> lse2, glabel, ce of row i.
+// m is the max over the non-label columns (the E offsets exclude the label), so the target may
+// exceed it: the row total is taken relative to M = max(m, yt).
 __device__ __forceinline__ void finish_row(int i, float m, float lo, float yt, float* lse2_out, float* glabel_out,
                                            float* ce_out, Status* status) {
-  const float et = ptx::ex2(yt - m);
-  const float lall = lo + et;
-  const float lse2 = m + log2f(lall);
-  const float dlt = m - yt;  // >= 0
-  const float ce = dlt < 64.f ? log1pf(lo * exp2f(dlt)) : dlt * LN2 + logf(lall);
+  const float M = fmaxf(m, yt);
+  const float lom = lo * ptx::ex2(m - M);  // non-label mass relative to M
+  const float lall = lom + ptx::ex2(yt - M);
+  const float lse2 = M + log2f(lall);
+  const float dlt = m - yt;  // ce = ln(1 + lo 2^(m - yt))
+  const float ce = dlt < 64.f ? log1pf(lo * exp2f(dlt)) : dlt * LN2 + logf(lo + exp2f(-dlt));
   lse2_out[i] = lse2;
-  glabel_out[i] = -lo / lall;
+  glabel_out[i] = -lom / lall;
   ce_out[i] = ce;
   if (!isfinite(ce) || !isfinite(lse2)) atomicOr(&status->flags, FLAG_LOSS_NONFINITE);
 }
@@ -1747,26 +1640,6 @@ __global__ void stats_combine_kernel(const float2* stats, const float* target, i
     for (int c = 0; c < nchunk; ++c) lo += chunk_sum(c);
   }
   finish_row(i, m, lo, target[i], lse2_out, glabel_out, ce_out, status);
-}
-
-// SYM (N = 1), direction 1: row c of S_1 is column c of S_0; the forward left one (max, sum) pair
-// per (64-row group, column) -- m_1 in the dir-1 half of m_g, the label-free sum in ssum.
-// Online combine in ascending group order (deterministic).
-__global__ void stats_sym_kernel(const float* mg1, const float* ssum, const float* target, int groups, int B,
-                                 float* lse2_out, float* glabel_out, float* ce_out, Status* status) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= B) return;
-  float m = -INFINITY, lo = 0.f;
-  for (int g = 0; g < groups; ++g) {
-    const float mg = mg1[int64_t(g) * B + c], sg = ssum[int64_t(g) * B + c];
-    if (mg > m) {
-      lo = lo * ptx::ex2(m - mg) + sg;
-      m = mg;
-    } else {
-      lo += sg * ptx::ex2(mg - m);
-    }
-  }
-  finish_row(B + c, m, lo, target[B + c], lse2_out, glabel_out, ce_out, status);
 }
 
 // E path: m_g [2][groups][b] (f32, log2 domain) -> sc [2][groups][b] = exp2(m_g - lse2[dir][r]) as f16,
@@ -1958,6 +1831,167 @@ struct PeerPtrs {
   uint32_t* flag[8];  // &flags[rank] inside each destination's window
 };
 
+// =====================================================================
+// Dual backward (DISCO_PATH_DUAL).  Rank n's rows r need, besides their own softmax G_d[r, :],
+// the other direction's softmax at column r of every row c: G_d'[c, r] = exp2(y[r, c] - lse2_d'[c])
+// with y[r, c] the logit rank n already has in its own E block.  So each gradient is one GEMM
+// over the rank's own block, H_d = G_d + G_d'^T (shard.py:148-154 summed over all ranks), and the
+// only exchange after the forward is the B column statistics -- no gradient reduce-scatter.
+// =====================================================================
+// Per column direction e (the lse2 the H_d columns use: e = 1 - d) and 64-column group g:
+// Q_g = max lse2_e over the group, q_c = exp2(min(Q_g - lse2_e[c], 100)) (negated for columns
+// outside this rank's rows under the flip hook), and the group's smallest lse2_e, or -inf when the
+// group's spread exceeds 96 (p_r q_c would leave the f32 range: every row goes to the fixup).
+// xall: [N][4][b] gathered (lse2_0, lse2_1, ce_0, ce_1); outputs for d: q [2][B], gm [2][groups].
+__global__ void dual_prep_kernel(const float* xall, int b, int groups, int rank, int flip, float* q, float2* gm) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= 2 * groups) return;
+  const int d = w / groups, g = w % groups, e = 1 - d;
+  const int64_t B = int64_t(groups) * 64;
+  float L[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t c = int64_t(g) * 64 + h * 32 + lane;
+    L[h] = xall[((c / b) * 4 + e) * b + c % b];
+  }
+  float mx = fmaxf(L[0], L[1]), mn = fminf(L[0], L[1]);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t c = int64_t(g) * 64 + h * 32 + lane;
+    const bool other = c < int64_t(rank) * b || c >= int64_t(rank + 1) * b;
+    const float v = exp2f(fminf(mx - L[h], 100.f));
+    q[int64_t(d) * B + c] = (flip && other) ? -v : v;
+  }
+  if (lane == 0) gm[int64_t(d) * groups + g] = make_float2(mx, mx - mn > 96.f ? -INFINITY : mn);
+}
+
+// d[r] = s (2^-14 (K-half partials, fixed order) + lab_r F_label(r)) for rows [row0, row0 + nrows):
+// the dual GEMM left 2^14 H with the label column zeroed; lab_r = (P_i2t - 1) + (P_t2i - 1) of row r
+// (fp32, both directions are this rank's) times the label row's features (d_image: T_n[r],
+// d_text: I_n[r], the packed bf16 rows the GEMMs used).
+__global__ void combine_dual_kernel(const float4* intra, int ksplit, const float* glabel, const __nv_bfloat16* pack,
+                                    int b, int Dp, int D, float s, float* d_image, float* d_text, int64_t ld_out,
+                                    int row0, int nrows, Status* status) {
+  const int v4 = Dp / 4;
+  const bool vec_out = (ld_out % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_image) | reinterpret_cast<uintptr_t>(d_text)) % 16 == 0);
+  const int64_t per_g = int64_t(b) * v4;
+  const unsigned pb = unsigned(int64_t(nrows) * v4), uv4 = unsigned(v4);
+  const int64_t total = 2 * int64_t(pb);
+  bool bad = false;
+  for (int64_t ii = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ii < total; ii += int64_t(gridDim.x) * blockDim.x) {
+    const unsigned iu = unsigned(ii);
+    const int g = int(iu / pb);
+    const int64_t rem = int64_t(iu - unsigned(g) * pb) + int64_t(row0) * v4;
+    const int r = int(unsigned(rem) / uv4), vc = int(unsigned(rem) % uv4);
+    const float4* ib = intra + (int64_t(g) * ksplit) * per_g + rem;
+    const float4 y = ksplit == 2 ? f4add(__ldcs(ib), __ldcs(ib + per_g)) : __ldcs(ib);
+    const float lab = glabel[r] + glabel[b + r];
+    // label row features: the other direction's packed row r (d_image pairs with T_n, d_text with I_n)
+    const uint2 fr = *reinterpret_cast<const uint2*>(pack + (int64_t(1 - g) * b + r) * Dp + vc * 4);
+    const float2 f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&fr.x));
+    const float2 f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&fr.y));
+    static_assert(H_DUAL_LOG2 == 14.f, "combine scale");
+    constexpr float inv = 1.f / 16384.f;  // 2^-H_DUAL_LOG2
+    const float4 o = make_float4(fmaf(lab, f01.x, y.x * inv) * s, fmaf(lab, f01.y, y.y * inv) * s,
+                                 fmaf(lab, f23.x, y.z * inv) * s, fmaf(lab, f23.y, y.w * inv) * s);
+    float* out = (g == 0 ? d_image : d_text) + int64_t(r) * ld_out;
+    const int c = vc * 4;
+    bad |= !(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w));
+    if (c + 4 <= D && vec_out) {
+      __stcs(reinterpret_cast<float4*>(out + c), o);
+    } else {
+      const float ov[4] = {o.x, o.y, o.z, o.w};
+      for (int k = 0; k < 4 && c + k < D; ++k) out[c + k] = ov[k];
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&status->flags, FLAG_GRAD_NONFINITE);
+}
+
+// Exact recompute of the rows the dual transform flagged (E range too narrow for a column term;
+// never seen with the synthetic features of the tests and bench at D >= 64): one CTA per queued
+// (direction, row) at a time, all in fp32 from the bf16 features -- y = t log2(e) <A_r, C_c>,
+// H = exp2(y - lse2_d[r]) + sign_c exp2(y - lse2_d'[c]), label (P_d - 1) + (P_d' - 1) -- then
+// d[r] = s sum_c H_c C_c, columns in ascending order (a function of the row only: N-invariant).
+constexpr int FIX_THREADS = 256;
+constexpr int FIX_COLS = 256;   // columns per chunk (one per thread in the dot phase)
+constexpr int FIX_MAX_DP = 2048;
+__global__ void __launch_bounds__(FIX_THREADS) dual_fixup_kernel(
+    const __nv_bfloat16* feat, const float* xall, const float* glabel, const int* list, const Status* status,
+    int cap, int B, int b, int Dp, int D, int rank, float tl2e, float s, int flip, float* d_image, float* d_text,
+    int64_t ld_out) {
+  __shared__ float arow[FIX_MAX_DP];
+  __shared__ float hs[FIX_COLS];
+  const int n = min(status->fix_count, cap);
+  constexpr int PER = FIX_MAX_DP / FIX_THREADS;
+  for (int e = blockIdx.x; e < n; e += gridDim.x) {
+    const int tag = list[e];
+    const int d = tag / b, r = tag % b, dp = 1 - d;
+    const __nv_bfloat16* A = feat + (int64_t(d) * B + int64_t(rank) * b + r) * Dp;
+    const __nv_bfloat16* C = feat + int64_t(dp) * B * Dp;
+    __syncthreads();
+    for (int k = threadIdx.x; k < Dp; k += FIX_THREADS) arow[k] = __bfloat162float(A[k]);
+    const float lse_r = xall[(int64_t(rank) * 4 + d) * b + r];
+    const float lab = glabel[r] + glabel[b + r];
+    const int64_t label = int64_t(rank) * b + r;
+    float acc[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) acc[k] = 0.f;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < B; c0 += FIX_COLS) {
+      {
+        const int64_t c = c0 + threadIdx.x;
+        float h = 0.f;
+        if (c < B) {
+          const uint4* cr = reinterpret_cast<const uint4*>(C + c * Dp);
+          float dot = 0.f;
+          for (int k8 = 0; k8 < Dp / 8; ++k8) {
+            const uint4 v = cr[k8];
+            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 f = __bfloat1622float2(hv[j]);
+              dot = fmaf(arow[8 * k8 + 2 * j], f.x, dot);
+              dot = fmaf(arow[8 * k8 + 2 * j + 1], f.y, dot);
+            }
+          }
+          if (c == label) {
+            h = lab;
+          } else {
+            const float y = dot * tl2e;
+            const float lc = xall[((c / b) * 4 + dp) * b + c % b];
+            const bool other = c < int64_t(rank) * b || c >= int64_t(rank + 1) * b;
+            h = exp2f(y - lse_r) + ((flip && other) ? -1.f : 1.f) * exp2f(y - lc);
+          }
+        }
+        hs[threadIdx.x] = h;
+      }
+      __syncthreads();
+      const int nc = B - c0 < FIX_COLS ? int(B - c0) : FIX_COLS;
+      for (int j = 0; j < nc; ++j) {
+        const float h = hs[j];
+        const __nv_bfloat16* cr = C + (c0 + j) * Dp;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int dim = threadIdx.x + k * FIX_THREADS;
+          if (dim < Dp) acc[k] = fmaf(h, __bfloat162float(cr[dim]), acc[k]);
+        }
+      }
+      __syncthreads();
+    }
+    float* out = (d == 0 ? d_image : d_text) + int64_t(r) * ld_out;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int dim = threadIdx.x + k * FIX_THREADS;
+      if (dim < D) out[dim] = acc[k] * s;
+    }
+  }
+}
+
 __global__ void peer_signal_kernel(PeerPtrs p, int n, uint32_t epoch) {
   // the cross GEMM (previous kernel on this stream) completed its bulk stores; make them visible
   // system-wide before the arrival flags
@@ -2031,7 +2065,9 @@ __global__ void peer_ce_push_kernel(const float4* ce, int n4, PeerDst dst, int N
 // blocks each reduce a fixed contiguous slice of the flat index f = dir*B + g;
 // stage 2: one warp adds the block partials in a fixed tree.
 constexpr int LOSS_BLOCKS = 128;
-__global__ void loss_partial_kernel(const float* ce_all, int N, int b, double* partial) {
+// ce_all: per rank `rs` row vectors of b floats, the two ce directions at vectors dir_off, dir_off + 1
+// ([N][2][b] ce gathers: rs = 2, dir_off = 0; [N][4][b] dual exchange: rs = 4, dir_off = 2).
+__global__ void loss_partial_kernel(const float* ce_all, int N, int b, double* partial, int rs = 2, int dir_off = 0) {
   __shared__ double red[256];
   const int64_t B = int64_t(N) * b;
   const int64_t n2 = 2 * B;
@@ -2042,7 +2078,7 @@ __global__ void loss_partial_kernel(const float* ce_all, int N, int b, double* p
     const int dir = int(f / B);
     const int64_t gidx = f - dir * B;
     const int64_t n = gidx / b, r = gidx % b;
-    acc += double(ce_all[(n * 2 + dir) * b + r]);
+    acc += double(ce_all[(n * rs + dir_off + dir) * b + r]);
   }
   red[threadIdx.x] = acc;
   __syncthreads();
@@ -2209,8 +2245,7 @@ struct Geometry {
   int wsplit;             // Dp > 512, Dp % 512 != 0: wide units for the first 512k columns + narrow rest
   int ksplit;             // intra K split (fixed function of B, D): partials [2][ksplit][b][Dp]
   int estore;             // forward stores E + group offsets; backward GEMMs rescale E -> G (no recompute)
-  int sym;                // N = 1 + estore: one GEMM of S_0 feeds both directions (S_1 = S_0^T)
-  int hfuse;              // N = 1, wide: backward GEMMs on H = G_d + G_d'^T (intra + cross in one)
+  int dual;               // disco_step's backward is the dual one (rank-local H = G_d + G_d'^T GEMMs)
   int groups;             // B / 64 column groups (E offsets)
   int chunk_cols;         // B / nchunk
   int64_t off[DISCO_R_COUNT];
@@ -2277,19 +2312,14 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
     return XP && e && atoi(e) != 0;
   }();
   g->estore = (g->g_blocked && !no_estore) ? 1 : 0;
-  // DISCO_SYMMETRIC=1 (read per call; experiment, off by default): the symmetric single-rank
-  // forward.  Correct (tools/env_ab.py, test_symmetric_forward_vs_oracle) but measured slower: the
-  // t2i column statistics cost ~2x the i2t epilogue in issue slots and MUFU, more than the halved
-  // MMA saves.  Not bitwise equal to N > 1 (t2i sums in another order).
-  const char* sym_env = XP ? getenv("DISCO_SYMMETRIC") : nullptr;
-  g->sym = (world == 1 && g->estore && sym_env && atoi(sym_env) == 1) ? 1 : 0;
-  // Fused single-rank backward (opt-in: DISCO_HFUSE=1, read per call).  At N = 1 every cross term
-  // G_d'^T . C pairs with an intra term G_d . C over the same B x B block, so the transform warps
-  // form H = G_0 + G_1^T in shared memory and one GEMM per gradient replaces two (half the backward
-  // MMA work).  Off by default: H adds an f16 rounding, so results are within 1e-3 of the oracle
-  // but not bit-for-bit equal to N > 1, which the default path guarantees.
-  const char* hf_env = getenv("DISCO_HFUSE");
-  g->hfuse = (world == 1 && g->estore && g->wide && g->ksplit == 2 && !g->sym && hf_env && atoi(hf_env) == 1) ? 1 : 0;
+  // Dual backward (default wherever E is stored, Dp <= 2048): after the forward every rank
+  // all_gathers the 4 b row statistics, and each gradient is ONE GEMM over the rank's own E block,
+  // H_d = G_d + G_d'^T -- half the backward MMA work of the exchange backward and no gradient
+  // reduce-scatter, bitwise equal at every N.  DISCO_BACKWARD=exchange (read per call) selects the
+  // two-GEMM exchange backward (intra + cross GEMMs, reduce-scatter), the form local_loss_and_grads
+  // always uses because its contract is the full-size per-rank contribution.
+  const char* bw = getenv("DISCO_BACKWARD");
+  g->dual = (g->estore && g->Dp <= FIX_MAX_DP && !(bw && strcmp(bw, "exchange") == 0)) ? 1 : 0;
   g->groups = int(B / GROUP_COLS);
   const int64_t b = g->b, Dp = g->Dp, N = world;
   int64_t len[DISCO_R_COUNT];
@@ -2297,12 +2327,9 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   len[DISCO_R_GATHER] = N > 1 ? N * 2 * b * Dp * 2 : 0;
   len[DISCO_R_FEAT] = 2 * B * Dp * 2;
   len[DISCO_R_FEAT16] = 2 * B * Dp * 2;
-  // + (N = 1, estore) the symmetric forward's dir-1 group sums [groups][B] f32 (allocated whether or
-  // not DISCO_SYMMETRIC selects the path, so the workspace size does not depend on it)
-  len[DISCO_R_STATS] = 2 * int64_t(g->nchunk) * g->ssub * 4 * b * 8 +  // [2][sub-chunks][<= 4 parts][b] f32x2
-                       (N == 1 && g->estore ? int64_t(g->groups) * B * 4 : 0);
+  len[DISCO_R_STATS] = 2 * int64_t(g->nchunk) * g->ssub * 4 * b * 8;  // [2][sub-chunks][<= 4 parts][b] f32x2
   len[DISCO_R_ROWS] = 4 * 2 * b * 4;
-  len[DISCO_R_CE] = 2 * b * 4;
+  len[DISCO_R_CE] = 0;  // alias into DISCO_R_XCHG (below)
   len[DISCO_R_CE_ALL] = N * 2 * b * 4;
   len[DISCO_R_G] = 2 * b * g->ldG * 2;
   len[DISCO_R_XPART] = g->np > 1 ? 2 * int64_t(g->np) * B * Dp * 4 : 0;
@@ -2313,14 +2340,23 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   len[DISCO_R_RDOT] = b * 4;
   len[DISCO_R_RDOT_ALL] = N > 1 ? N * b * 4 : 0;
   len[DISCO_R_SCALE] = g->estore ? 2 * int64_t(g->groups) * b * (4 + 2) : 0;  // f32 m_g, then f16 scales
+  len[DISCO_R_XCHG] = 4 * b * 4;
+  len[DISCO_R_XALL] = N > 1 ? N * 4 * b * 4 : 0;
+  len[DISCO_R_QCOL] = g->estore ? 2 * B * 4 + 2 * int64_t(g->groups) * 8 : 0;
+  len[DISCO_R_FIX] = g->estore ? 2 * int64_t(g->ksplit) * b * 4 : 0;
   int64_t off = 0;
   for (int r = 0; r < DISCO_R_COUNT; ++r) {
     g->off[r] = off;
     g->len[r] = len[r];
     off += round_up(len[r], 1024);
   }
+  // the per-row lse2 and ce live in the exchange vector: DISCO_R_CE is its ce half
+  g->off[DISCO_R_CE] = g->off[DISCO_R_XCHG] + 2 * b * 4;
+  g->len[DISCO_R_CE] = 2 * b * 4;
   // aliases for the single-rank case: packed == gathered == forward operand layout
   if (N == 1) {
+    g->off[DISCO_R_XALL] = g->off[DISCO_R_XCHG];
+    g->len[DISCO_R_XALL] = g->len[DISCO_R_XCHG];
     g->off[DISCO_R_PACK] = g->off[DISCO_R_FEAT];
     g->off[DISCO_R_GATHER] = g->off[DISCO_R_PACK];
     g->len[DISCO_R_GATHER] = g->len[DISCO_R_PACK];
@@ -2337,6 +2373,9 @@ template <typename T>
 T* region(void* ws, const Geometry& g, int r) {
   return reinterpret_cast<T*>(static_cast<uint8_t*>(ws) + g.off[r]);
 }
+
+// this rank's per-row lse2 [2][b] (first half of the exchange vector DISCO_R_XCHG)
+float* lse2_of(void* ws, const Geometry& g) { return region<float>(ws, g, DISCO_R_XCHG); }
 
 unsigned long long* probe_slot(void* ws, const Geometry& g, int at) {
   return reinterpret_cast<unsigned long long*>(region<uint8_t>(ws, g, DISCO_R_STATUS) + offsetof(Status, probe)) + at;
@@ -2506,20 +2545,20 @@ int l2_window(cudaLaunchAttribute* attr, const void* base, size_t bytes) {
   return 1;
 }
 
-template <int KIND, bool ARES, bool SYM = false>
+template <int KIND, bool ARES>
 int launch_logits_t(const LogitsParams& p, int64_t units, cudaStream_t st, const void* feat = nullptr,
                     size_t feat_bytes = 0) {
   int rc;
-  if ((rc = prepare_kernel(logits_kernel<KIND, ARES, SYM>))) return rc;
+  if ((rc = prepare_kernel(logits_kernel<KIND, ARES>))) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid_for(units));
-  cfg.blockDim = dim3(logits_threads<KIND, ARES, SYM>());
+  cfg.blockDim = dim3(logits_threads<KIND, ARES>());
   cfg.dynamicSmemBytes = SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   cfg.attrs = attr;
   cfg.numAttrs = (feat && (debug_flag_bits() & 2)) ? l2_window(&attr[0], feat, feat_bytes) : 0;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, logits_kernel<KIND, ARES, SYM>, p));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, logits_kernel<KIND, ARES>, p));
   count_launch();
   return DISCO_OK;
 }
@@ -2548,14 +2587,13 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   float* rows = region<float>(ws, g, DISCO_R_ROWS);
   p.stats = region<float2>(ws, g, DISCO_R_STATS);
   p.target = rows;
-  p.lse2 = rows + 2 * g.b;
+  p.lse2 = lse2_of(ws, g);
   p.glabel = rows + 4 * g.b;
   p.G = region<__half>(ws, g, DISCO_R_G);
   p.ldG = g.ldG;
   p.g_blocked = g.g_blocked;
   p.mg = region<float>(ws, g, DISCO_R_SCALE);
   p.groups = g.groups;
-  p.ssum = reinterpret_cast<float*>(p.stats + 2 * int64_t(g.nchunk) * g.ssub * 4 * g.b);
   p.wave = wave;
   p.epoch = epoch;
   p.timeout_ns = (unsigned long long)(timeout_s * 1e9);
@@ -2576,8 +2614,7 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
     p.status_flags = &stt->flags;
     p.nwaves = wave == -2 ? g.nchunk * g.ssub : g.N;
   }
-  const bool sym = g.sym && kind == KIND_FWDE && wave != -3;
-  const int64_t ndir = sym ? 1 : 2;
+  const int64_t ndir = 2;
   const int64_t units = wave == -3 ? int64_t(2) * p.row_tiles * p.nchunk
                       : wave == -2 ? ndir * p.rt_per_chunk * p.nwaves * p.nwaves
                       : wave >= 0 ? ndir * p.rt_per_chunk * (2 * wave + 1)
@@ -2594,11 +2631,9 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   } else if (kind == KIND_FWDE) {
     const size_t fb = size_t(2) * g.B * g.Dp * 2;
 #if DISCO_EXPERIMENTS
-    rc = sym    ? launch_logits_t<KIND_FWDE, false, true>(p, units, st, feat, fb)
-         : ares ? launch_logits_t<KIND_FWDE, true>(p, units, st, feat, fb)
-                : launch_logits_t<KIND_FWDE, false>(p, units, st, feat, fb);
+    rc = ares ? launch_logits_t<KIND_FWDE, true>(p, units, st, feat, fb)
+              : launch_logits_t<KIND_FWDE, false>(p, units, st, feat, fb);
 #else
-    (void)sym;
     rc = launch_logits_t<KIND_FWDE, false>(p, units, st, feat, fb);
 #endif
     if (rc) return rc;
@@ -2622,12 +2657,12 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
 
 // wide = 1: every unit covers all N columns (n_tiles counts 512-column tiles), NB = 2 kernel.
 // xform = 1: A operands hold E (transform warps rescale to G in smem).
-template <int NB, bool XF, bool HF = false>
+template <int NB, bool XF>
 int launch_gemm_t(GemmParams& p, cudaStream_t st) {
   int rc;
-  if ((rc = prepare_kernel(gemm_kernel<NB, XF, HF>, HF ? SMEM_BYTES_HF : SMEM_BYTES))) return rc;
-  gemm_kernel<NB, XF, HF><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS,
-                            HF ? SMEM_BYTES_HF : SMEM_BYTES, st>>>(p);
+  const size_t smem = XF ? SMEM_BYTES_XF : SMEM_BYTES;
+  if ((rc = prepare_kernel(gemm_kernel<NB, XF>, smem))) return rc;
+  gemm_kernel<NB, XF><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS, smem, st>>>(p);
   return DISCO_OK;
 }
 
@@ -2679,7 +2714,7 @@ void build_schedule(GemmParams& p, int npairs) {
   p.sched_n = n;
 }
 
-int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform, int hfuse = 0);
+int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform);
 
 // Split-width backward (g.wsplit): the same problems twice -- wide units over columns
 // [0, wcols), then narrow unpaired units over [wcols, Dp) -- with identical K decompositions, so
@@ -2701,15 +2736,13 @@ int launch_backward(GemmParams& p, cudaStream_t st, const Geometry& g) {
   return launch_gemm(q, st, 0, g.estore);
 }
 
-int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform, int hfuse) {
+int launch_gemm(GemmParams& p, cudaStream_t st, int wide, int xform) {
   p.units[0] = 0;
   for (int i = 0; i < p.nprob; ++i)
     p.units[i + 1] = p.units[i] + p.prob[i].m_tiles * p.prob[i].n_tiles * p.prob[i].k_chunks;
   if (!(debug_flag_bits() & 262144)) build_schedule(p, grid_for(p.units[p.nprob]) / 2);  // bit18: round-robin
   int rc;
-  if (hfuse)
-    rc = launch_gemm_t<2, true, true>(p, st);
-  else if (wide)
+  if (wide)
     rc = xform ? launch_gemm_t<2, true>(p, st) : launch_gemm_t<2, false>(p, st);
   else
     rc = xform ? launch_gemm_t<1, true>(p, st) : launch_gemm_t<1, false>(p, st);
@@ -2806,15 +2839,20 @@ int cross_presum(void* ws, const Geometry& g, cudaStream_t st) {
   return DISCO_OK;
 }
 
+// Scale of the exchange backward's GEMM outputs: 0.5 t / B (reference loss scale, shard.py:143-146),
+// times 2^-15 when the GEMMs ran on E (the forward's headroom: they formed 2^15 G).
+float exchange_scale(const Geometry& g, float t, double rows) {
+  return float(0.5 * double(t) / rows * (g.estore ? 1.0 / G_EXCHANGE_SCALE : 1.0));
+}
+
 int launch_combine(void* ws, const Geometry& g, float t, int flip, int row0, int nrows, float* d_image, float* d_text,
                    int64_t ld_out, cudaStream_t st) {
-  const float s = float(0.5 * double(t) / double(g.B));
+  const float s = exchange_scale(g, t, double(g.B));
   const int64_t n = 2 * int64_t(nrows) * (g.Dp / 4);
   if (n == 0) return DISCO_OK;
   combine_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
       region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float4>(ws, g, DISCO_R_RECV),
-      (g.N == 1 && g.np > 1 && !g.hfuse) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np,
-      g.hfuse ? 0 : g.N, g.rank, int(g.b), int(g.Dp), int(g.D), s, flip, d_image, d_text, ld_out, row0, nrows,
+      (g.N == 1 && g.np > 1) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, g.N, g.rank, int(g.b), int(g.Dp), int(g.D), s, flip, d_image, d_text, ld_out, row0, nrows,
       region<Status>(ws, g, DISCO_R_STATUS), 0, 1 << 30, 1);
   count_launch();
   CUDA_TRY(cudaGetLastError());
@@ -2859,60 +2897,56 @@ int build_intra(GemmParams& p, int first, void* ws, const Geometry& g, int mt0 =
   return DISCO_OK;
 }
 
-// Fused single-rank backward (g.hfuse): two GEMMs, one per gradient, on H_d = G_d + G_d'^T:
-//   d_image rows r: H_0 . T_g, A = E_0 (K-major), A2 = E_1 (MN-major: its K-rows are E_1 rows)
-//   d_text  rows c: H_1 . I_g, A = E_1 (K-major), A2 = E_0 (MN-major)
-// i.e. the intra problems with the other direction's E as a second A operand; the transform
-// warps form H_d tile by tile (ldmatrix / ldmatrix.trans / stmatrix).  K = all B in ksplit halves
-// (the intra partials); no cross terms.  Factors: xscale = direction d (one per row and K-group),
-// xscale2 = direction d' (one per K column for the rows' 64-group).
-int build_hfuse(GemmParams& p, void* ws, const Geometry& g, int mt0 = 0, int mt1 = -1) {
+// Dual GEMMs (g.dual): the intra problems (rows [mt0, mt1) of 256) with the dual transform:
+//   d_image rows r: H'_0 . T_g, A = E_0 rows;  d_text rows r: H'_1 . I_g, A = E_1 rows
+// K = all B columns in g.ksplit fixed halves (DISCO_R_INTRA partials), combined by combine_dual.
+int build_dual(GemmParams& p, void* ws, const Geometry& g, int mt0 = 0, int mt1 = -1) {
   int rc;
   if ((rc = build_intra(p, 0, ws, g, mt0, mt1))) return rc;
-  const __half* G = region<__half>(ws, g, DISCO_R_G);
-  const __half* sc16 = reinterpret_cast<const __half*>(scale16(ws, g));
-  const float* labels = region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b;
-  for (int gi = 0; gi < 2; ++gi) {
-    GemmProblem& q = p.prob[gi];
-    const int d2 = 1 - gi;
-    if ((rc = make_map_blocked(&q.a2_map, G + int64_t(d2) * g.b * g.B, g.b, g.B, 64))) return rc;
-    q.hfuse = 1;
-    q.xscale2 = sc16 + int64_t(d2) * g.groups * g.b;
-    q.xlabel2 = labels + int64_t(d2) * g.b;
+  const float* mg = region<float>(ws, g, DISCO_R_SCALE);
+  float* qcol = region<float>(ws, g, DISCO_R_QCOL);
+  const float2* gm = reinterpret_cast<const float2*>(qcol + 2 * g.B);
+  Status* status = region<Status>(ws, g, DISCO_R_STATUS);
+  for (int d = 0; d < 2; ++d) {
+    GemmProblem& q = p.prob[d];
+    q.xform = 2;
+    q.xmg = mg + int64_t(d) * g.groups * g.b;
+    q.xlse = lse2_of(ws, g) + int64_t(d) * g.b;
+    q.xq = qcol + int64_t(d) * g.B;
+    q.xgm = gm + int64_t(d) * g.groups;
+    q.fix_list = region<int>(ws, g, DISCO_R_FIX);
+    q.fix_count = &status->fix_count;
+    q.fix_tag = int(int64_t(d) * g.b);
+    q.fix_cap = int(2 * g.ksplit * g.b);
   }
   p.nprob = 2;
   p.split = 0;
   return DISCO_OK;
 }
 
-// stats combine (+ E -> G factors): after every logits unit of the forward has run.
+// stats combine: after every logits unit of the forward has run.  lse2 and ce land in the
+// exchange vector (DISCO_R_XCHG), the label gradients in DISCO_R_ROWS.
 int forward_finish(void* ws, const Geometry& g, cudaStream_t st) {
   float* rows = region<float>(ws, g, DISCO_R_ROWS);
-  const int ndir = g.sym ? 1 : 2;
-  const int n = int(ndir * g.b);
-  float2* stats = region<float2>(ws, g, DISCO_R_STATS);
-  // column parts per (row, sub-chunk): the FWDE kernel's epilogue parts, or halves (FWD, SYM)
-  const int nparts = (g.estore && !g.sym) ? FWDE_PARTS : 2;
-  stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(stats, rows, g.nchunk, g.ssub, nparts, int(g.b), ndir,
-                                                        rows + 2 * g.b, rows + 4 * g.b, region<float>(ws, g, DISCO_R_CE),
+  const int n = int(2 * g.b);
+  // column parts per (row, sub-chunk): the FWDE kernel's epilogue parts, or halves (FWD)
+  const int nparts = g.estore ? FWDE_PARTS : 2;
+  stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(region<float2>(ws, g, DISCO_R_STATS), rows, g.nchunk, g.ssub,
+                                                        nparts, int(g.b), 2, lse2_of(ws, g), rows + 4 * g.b,
+                                                        region<float>(ws, g, DISCO_R_CE),
                                                         region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
   CUDA_TRY(cudaGetLastError());
-  if (g.sym) {
-    stats_sym_kernel<<<int((g.B + 255) / 256), 256, 0, st>>>(
-        region<float>(ws, g, DISCO_R_SCALE) + int64_t(g.groups) * g.b,
-        reinterpret_cast<float*>(stats + 2 * int64_t(g.nchunk) * g.ssub * 4 * g.b), rows, g.groups, int(g.B),
-        rows + 2 * g.b, rows + 4 * g.b, region<float>(ws, g, DISCO_R_CE), region<Status>(ws, g, DISCO_R_STATUS));
-    count_launch();
-    CUDA_TRY(cudaGetLastError());
-  }
-  if (g.estore) {
-    const int64_t nv = 2 * int64_t(g.groups) * g.b / 8;
-    scale_kernel<<<elementwise_grid(nv, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_SCALE), rows + 2 * g.b,
-                                                           g.groups, int(g.b), scale16(ws, g));
-    count_launch();
-    CUDA_TRY(cudaGetLastError());
-  }
+  return DISCO_OK;
+}
+
+// E -> G factors of the exchange backward (legacy transform): exp2(m_g - lse2) as f16.
+int exchange_scales(void* ws, const Geometry& g, cudaStream_t st) {
+  const int64_t nv = 2 * int64_t(g.groups) * g.b / 8;
+  scale_kernel<<<elementwise_grid(nv, 256), 256, 0, st>>>(region<float4>(ws, g, DISCO_R_SCALE), lse2_of(ws, g),
+                                                         g.groups, int(g.b), scale16(ws, g));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
 }
 
@@ -3103,8 +3137,7 @@ int disco_b200_path_info(int64_t B, int64_t D, int world, int rank, int* bits) {
   Geometry g;
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
-  *bits = (g.estore ? DISCO_PATH_ESTORE : 0) | (g.wide ? DISCO_PATH_WIDE : 0) | (g.hfuse ? DISCO_PATH_HFUSE : 0) |
-          (g.sym ? DISCO_PATH_SYM : 0);
+  *bits = (g.estore ? DISCO_PATH_ESTORE : 0) | (g.wide ? DISCO_PATH_WIDE : 0) | (g.dual ? DISCO_PATH_DUAL : 0);
   return DISCO_OK;
 }
 
@@ -3192,7 +3225,8 @@ int disco_b200_backward_grad(void* ws, int64_t B, int64_t D, int world, int rank
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
-  if (g.estore) return DISCO_OK;  // the forward already stored E; the backward GEMMs finish G in smem
+  // E path: the forward already stored E; the backward GEMMs finish G in smem with these factors
+  if (g.estore) return exchange_scales(ws, g, static_cast<cudaStream_t>(stream));
   return launch_logits(KIND_GRAD, ws, g, t, static_cast<cudaStream_t>(stream));
 }
 
@@ -3201,7 +3235,6 @@ int disco_b200_backward_cross(void* ws, int64_t B, int64_t D, int world, int ran
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (g.hfuse) return DISCO_OK;  // fused single-rank backward: disco_b200_backward_intra covers both terms
   GemmParams p;
   memset(&p, 0, sizeof(p));
   if ((rc = build_cross(p, 0, ws, g))) return rc;
@@ -3216,10 +3249,6 @@ int disco_b200_backward_intra(void* ws, int64_t B, int64_t D, int world, int ran
   if (rc) return rc;
   GemmParams p;
   memset(&p, 0, sizeof(p));
-  if (g.hfuse) {
-    if ((rc = build_hfuse(p, ws, g))) return rc;
-    return launch_gemm(p, st_of(stream), 1, 1, 1);
-  }
   if ((rc = build_intra(p, 0, ws, g))) return rc;
   p.nprob = 2;
   return launch_backward(p, st_of(stream), g);
@@ -3232,10 +3261,6 @@ int disco_b200_backward_fused(void* ws, int64_t B, int64_t D, int world, int ran
   cudaStream_t st = st_of(stream);
   GemmParams p;
   memset(&p, 0, sizeof(p));
-  if (g.hfuse) {
-    if ((rc = build_hfuse(p, ws, g))) return rc;
-    return launch_gemm(p, st, 1, 1, 1);
-  }
   if ((rc = build_intra(p, 0, ws, g))) return rc;  // list A: long units (K = B / ksplit)
   if ((rc = build_cross(p, 2, ws, g))) return rc;  // list B: one canonical chunk of K per unit
   p.nprob = 4;
@@ -3277,10 +3302,6 @@ int disco_b200_backward_rows(void* ws, int64_t B, int64_t D, int world, int rank
   const int mt0 = int(row0 / PAIR_M), mt1 = int((row1 + PAIR_M - 1) / PAIR_M);
   GemmParams p;
   memset(&p, 0, sizeof(p));
-  if (g.hfuse) {
-    if ((rc = build_hfuse(p, ws, g, mt0, mt1))) return rc;
-    return launch_gemm(p, st_of(stream), 1, 1, 1);
-  }
   if ((rc = build_intra(p, 0, ws, g, mt0, mt1))) return rc;
   if ((rc = build_cross(p, 2, ws, g, mt0, mt1))) return rc;
   p.nprob = 4;
@@ -3295,11 +3316,11 @@ int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank,
   if (rc) return rc;
   if (ld_out < D) return fail(DISCO_SHAPE_ERROR, "output row stride smaller than D");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const float s = float(0.5 * double(t) / double(g.b));
+  const float s = exchange_scale(g, t, double(g.b));
   const int64_t n = 2 * g.B * (g.Dp / 4);
   contribution_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(
-      region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, g.hfuse ? nullptr : region<float4>(ws, g, DISCO_R_SEND),
-      (world == 1 && g.np > 1 && !g.hfuse) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, world, rank, int(g.b),
+      region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float4>(ws, g, DISCO_R_SEND),
+      (world == 1 && g.np > 1) ? region<float4>(ws, g, DISCO_R_XPART) : nullptr, g.np, world, rank, int(g.b),
       int(g.Dp), int(D), s, flip && world > 1, d_image_full, d_text_full, ld_out, region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();
   CUDA_TRY(cudaGetLastError());
@@ -3327,11 +3348,16 @@ int disco_b200_loss(void* ws, int64_t B, int64_t D, int world, int rank, int loc
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool local = local_only || world == 1;
+  const bool local = local_only == 1 || world == 1;
+  const bool xall = local_only == 2 && !local;  // dual backward: ce of every rank in DISCO_R_XALL
   Status* status = region<Status>(ws, g, DISCO_R_STATUS);
   const int nw = local ? 1 : world;
-  loss_partial_kernel<<<LOSS_BLOCKS, 256, 0, st>>>(region<float>(ws, g, local ? DISCO_R_CE : DISCO_R_CE_ALL), nw,
-                                                   int(g.b), status->loss_partial);
+  if (xall)
+    loss_partial_kernel<<<LOSS_BLOCKS, 256, 0, st>>>(region<float>(ws, g, DISCO_R_XALL), nw, int(g.b),
+                                                     status->loss_partial, 4, 2);
+  else
+    loss_partial_kernel<<<LOSS_BLOCKS, 256, 0, st>>>(region<float>(ws, g, local ? DISCO_R_CE : DISCO_R_CE_ALL), nw,
+                                                     int(g.b), status->loss_partial);
   loss_final_kernel<<<1, LOSS_BLOCKS, 0, st>>>(status->loss_partial, int64_t(2) * nw * g.b, status);
   count_launch(2);
   CUDA_TRY(cudaGetLastError());
@@ -3386,6 +3412,79 @@ int disco_b200_l2norm_rows_backward(const float* raw, int64_t ld_raw, const floa
   if (rows == 0) return DISCO_OK;
   l2norm_rows_backward_kernel<<<int((rows * 32 + 255) / 256), 256, 0, st_of(stream)>>>(
       raw, ld_raw, grad, ld_grad, int(rows), int(D), out, ld_out, flags);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+// ------------------------------------------------------------ dual backward
+static int dual_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
+  int rc = make_geometry(B, D, world, rank, g);
+  if (rc) return rc;
+  if (!g->dual)
+    return fail(DISCO_LAYOUT_ERROR, "dual backward not available for B=%lld D=%lld N=%d (disco_b200_path_info)",
+                (long long)B, (long long)D, world);
+  return DISCO_OK;
+}
+
+int disco_b200_dual_prep(void* ws, int64_t B, int64_t D, int world, int rank, int flip, void* stream) {
+  Geometry g;
+  int rc = dual_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  float* qcol = region<float>(ws, g, DISCO_R_QCOL);
+  const int warps = 2 * g.groups;
+  dual_prep_kernel<<<(warps * 32 + 255) / 256, 256, 0, st_of(stream)>>>(
+      region<float>(ws, g, DISCO_R_XALL), int(g.b), g.groups, rank, flip && world > 1, qcol,
+      reinterpret_cast<float2*>(qcol + 2 * g.B));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_backward_dual(void* ws, int64_t B, int64_t D, int world, int rank, int64_t row0, int64_t row1,
+                             void* stream) {
+  Geometry g;
+  int rc = dual_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (row0 < 0 || row1 > g.b || row0 >= row1 || row0 % PAIR_M != 0 || (row1 % PAIR_M != 0 && row1 != g.b))
+    return fail(DISCO_SHAPE_ERROR, "row block [%lld, %lld) must be 256-aligned inside [0, %lld)", (long long)row0,
+                (long long)row1, (long long)g.b);
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  if ((rc = build_dual(p, ws, g, int(row0 / PAIR_M), int((row1 + PAIR_M - 1) / PAIR_M)))) return rc;
+  return launch_backward(p, st_of(stream), g);
+}
+
+int disco_b200_combine_dual(void* ws, int64_t B, int64_t D, int world, int rank, float t, int64_t row0, int64_t row1,
+                            float* d_image, float* d_text, int64_t ld_out, void* stream) {
+  Geometry g;
+  int rc = dual_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (ld_out < D) return fail(DISCO_SHAPE_ERROR, "output row stride smaller than D");
+  if (row0 < 0 || row1 > g.b || row0 > row1) return fail(DISCO_SHAPE_ERROR, "row range [%lld, %lld) outside [0, %lld)",
+                                                         (long long)row0, (long long)row1, (long long)g.b);
+  const int64_t n = 2 * (row1 - row0) * (g.Dp / 4);
+  if (n == 0) return DISCO_OK;
+  combine_dual_kernel<<<elementwise_grid(n, 256), 256, 0, st_of(stream)>>>(
+      region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b,
+      region<__nv_bfloat16>(ws, g, DISCO_R_PACK), int(g.b), int(g.Dp), int(D), float(0.5 * double(t) / double(g.B)),
+      d_image, d_text, ld_out, int(row0), int(row1 - row0), region<Status>(ws, g, DISCO_R_STATUS));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+
+int disco_b200_dual_fixup(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip, float* d_image,
+                          float* d_text, int64_t ld_out, void* stream) {
+  Geometry g;
+  int rc = dual_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (ld_out < D) return fail(DISCO_SHAPE_ERROR, "output row stride smaller than D");
+  dual_fixup_kernel<<<sm_count(), FIX_THREADS, 0, st_of(stream)>>>(
+      region<__nv_bfloat16>(ws, g, DISCO_R_FEAT), region<float>(ws, g, DISCO_R_XALL),
+      region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b, region<int>(ws, g, DISCO_R_FIX), region<Status>(ws, g, DISCO_R_STATUS),
+      int(2 * g.ksplit * g.b), int(g.B), int(g.b), int(g.Dp), int(D), rank, t * LOG2E,
+      float(0.5 * double(t) / double(g.B)), flip && world > 1, d_image, d_text, ld_out);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
@@ -3583,7 +3682,7 @@ int disco_b200_combine_peer(void* ws, int64_t B, int64_t D, int world, int rank,
                                      (unsigned long long)(timeout_s * 1e9));
   count_launch();
   CUDA_TRY(cudaGetLastError());
-  const float s = float(0.5 * double(t) / double(g.B));
+  const float s = exchange_scale(g, t, double(g.B));
   const int64_t n = 2 * g.b * (g.Dp / 4);
   const int L = int(peer_leaves(g));
   combine_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(

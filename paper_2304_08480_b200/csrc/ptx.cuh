@@ -192,26 +192,41 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Explicit shared-memory accesses by 32-bit shared address (generic pointers into smem compile to
+// LD.E / ST.E with a generic-to-shared window check); volatile + memory clobber keep them ordered
+// after the mbarrier waits that publish the TMA data.
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 lds128f(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void sts16(uint32_t a, unsigned short v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
+}
+
 // Write one 128-byte row segment (8 x 16 B) of a 32-row staging tile laid out
 // with the TMA SWIZZLE_128B pattern (16-byte chunk q of row r lands at q ^ (r & 7)).
 __device__ __forceinline__ void st_swizzled_row(uint8_t* tile, int r, const uint32_t (&w)[32]) {
-  uint8_t* row = tile + r * 128;
+  const uint32_t row = smem_u32(tile) + r * 128;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    uint4 v = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-    *reinterpret_cast<uint4*>(row + ((q ^ (r & 7)) << 4)) = v;
-  }
+  for (int q = 0; q < 8; ++q) sts128(row + ((q ^ (r & 7)) << 4), make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
 }
 
 // One 64-byte row (16 words) of a 32-row staging tile in the TMA SWIZZLE_64B layout: 16-byte
 // chunk q of row r sits at physical chunk q ^ ((r >> 1) & 3) (bank-conflict-free per quarter warp).
 __device__ __forceinline__ void st_swizzled_row64(uint8_t* tile, int r, const uint32_t* w) {
-  uint8_t* row = tile + r * 64;
+  const uint32_t row = smem_u32(tile) + r * 64;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint4 v = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-    *reinterpret_cast<uint4*>(row + ((q ^ ((r >> 1) & 3)) << 4)) = v;
-  }
+  for (int q = 0; q < 4; ++q)
+    sts128(row + ((q ^ ((r >> 1) & 3)) << 4), make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
 }
 
 // Coalesced write-out of a 32-row x 128-byte swizzled staging tile with plain
@@ -437,6 +452,12 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   unsigned long long r;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(r);
+}
+
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
   return f2_from(r);
 }
 

@@ -141,6 +141,10 @@ class Plan:
         self.recv = view(_lib.R_RECV, torch.float32)
         self.rdot = view(_lib.R_RDOT, torch.float32)
         self.rdot_all = view(_lib.R_RDOT_ALL, torch.float32)
+        self.xchg = view(_lib.R_XCHG, torch.float32)  # dual backward: this rank's 4 b row statistics
+        self.xall = view(_lib.R_XALL, torch.float32)  # ... all_gathered (alias at N = 1)
+        self.pending_host = None  # (d_image, d_text, h_image, h_text) of a row-block step (dual fixup refresh)
+        self.fixed_rows = 0       # rows the last step's dual fixup recomputed (set by the status read)
         status_all = view(_lib.R_STATUS, torch.uint8)
         status_all.zero_()  # the streamed forward's wave flags start below every epoch
         self.status = status_all[:24]
@@ -354,6 +358,7 @@ def _read_status(plan: Plan, with_dlogit: bool = False):
     raw = plan.status_host.numpy()
     loss = float(raw[:8].view(np.float64)[0])
     flags = int(raw[8:12].view(np.int32)[0])
+    plan.fixed_rows = int(raw[12:16].view(np.int32)[0])  # dual backward rows recomputed exactly
     if with_dlogit:
         return loss, flags, float(raw[16:24].view(np.float64)[0])
     return loss, flags
@@ -463,7 +468,7 @@ ROW_BLOCK_FRACTIONS = (0.25, 0.1953125, 0.15625, 0.125, 0.09375, 0.078125, 0.062
 
 
 def fused_row_blocks(b: int, pairs: int, units_per_tile: int = 4):
-    """Row blocks for the fused single-rank backward (disco_b200_path_info PATH_HFUSE): its units
+    """Row blocks for the single-rank dual backward (disco_b200_path_info PATH_DUAL): its units
     are long (a K half of all B columns) and only ``units_per_tile`` per 256-row tile, so every
     block is one whole wave of the ``pairs`` CTA pairs.  A wave's gradients (~19 MB at D = 512)
     are produced faster than PCIe drains them, so the device->host copy never waits after the
@@ -640,6 +645,56 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
             _lib.call("disco_b200_forward", *plan.args, t, st)
         else:
             _lib.call("disco_b200_forward", *plan.args, t, st)
+    d_image = torch.empty((b, D), dtype=torch.float32, device=device)
+    d_text = torch.empty((b, D), dtype=torch.float32, device=device)
+    flip = int(bool(flip_cross_rank_sign))
+    if _lib.path_info(B, D, N, n) & _lib.PATH_DUAL:
+        _dual_backward(endpoint, plan, t, flip, d_image, d_text, host_out)
+    else:
+        _exchange_backward(endpoint, plan, t, flip, d_image, d_text, host_out, pw,
+                           parity if pw is not None else 0, epoch if pw is not None else 0)
+    _leave(plan, cur_stream)
+    return d_image, d_text, plan
+
+
+def _dual_backward(endpoint, plan: Plan, t: float, flip: int, d_image, d_text, host_out) -> None:
+    """The dual backward (disco_b200_path_info PATH_DUAL): all_gather the 4 b row statistics, then
+    one GEMM per gradient over the rank's own E block (H = G_d + G_d'^T), the combine with the
+    fp32 label term, the exact recompute of any flagged rows, and the loss from the gathered ce.
+    Replaces the reference's all_reduce(AVG) + slice (shard.py:199-208): no gradient exchange."""
+    device, b, D, N = plan.device, plan.b, plan.D, plan.world
+    st = torch.cuda.current_stream(device).cuda_stream
+    if N > 1:
+        endpoint.all_gather_into(plan.xall, plan.xchg)
+    _lib.call("disco_b200_dual_prep", *plan.args, flip, st)
+    if N == 1 and host_out is not None:
+        cs = plan.copy_stream()
+        cur = torch.cuda.current_stream(device)
+        h_image, h_text = host_out
+        for r0, r1 in fused_row_blocks(b, plan.pairs):
+            _lib.call("disco_b200_backward_dual", *plan.args, r0, r1, st)
+            _lib.call("disco_b200_combine_dual", *plan.args, t, r0, r1, d_image.data_ptr(), d_text.data_ptr(), D, st)
+            cs.wait_stream(cur)
+            with torch.cuda.stream(cs):
+                h_image[r0:r1].copy_(d_image[r0:r1], non_blocking=True)
+                h_text[r0:r1].copy_(d_text[r0:r1], non_blocking=True)
+        d_image.record_stream(cs)
+        d_text.record_stream(cs)
+        plan.pending_host = (d_image, d_text, h_image, h_text)
+    else:
+        _lib.call("disco_b200_backward_dual", *plan.args, 0, b, st)
+        _lib.call("disco_b200_combine_dual", *plan.args, t, 0, b, d_image.data_ptr(), d_text.data_ptr(), D, st)
+    _lib.call("disco_b200_dual_fixup", *plan.args, t, flip, d_image.data_ptr(), d_text.data_ptr(), D, st)
+    _lib.call("disco_b200_loss", *plan.args, 2, st)
+
+
+def _exchange_backward(endpoint, plan: Plan, t: float, flip: int, d_image, d_text, host_out, pw, parity: int,
+                       epoch: int) -> None:
+    """The exchange backward (DISCO_BACKWARD=exchange, or shapes without stored E): intra and
+    cross GEMMs, then the reference's all_reduce(AVG) + slice as a reduce-scatter -- over the peer
+    transport (cross tiles pushed from the GEMM epilogue) or an NCCL all_to_all."""
+    device, b, D, N = plan.device, plan.b, plan.D, plan.world
+    st = torch.cuda.current_stream(device).cuda_stream
     _lib.call("disco_b200_backward_grad", *plan.args, t, st)
     if pw is not None:
         # the fused backward GEMM pushes each cross tile to its owner over NVLink
@@ -650,16 +705,11 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         work = endpoint.all_to_all_into(plan.recv, plan.send, async_op=True)
         _lib.call("disco_b200_backward_intra", *plan.args, st)
         work.wait()
-    d_image = torch.empty((b, D), dtype=torch.float32, device=device)
-    d_text = torch.empty((b, D), dtype=torch.float32, device=device)
-    flip = int(bool(flip_cross_rank_sign))
     if N == 1 and host_out is not None:
         cs = plan.copy_stream()
         cur = torch.cuda.current_stream(device)
         h_image, h_text = host_out
-        blocks = (fused_row_blocks(b, plan.pairs) if _lib.path_info(B, D, N, n) & _lib.PATH_HFUSE
-                  else row_blocks(b))
-        for r0, r1 in blocks:
+        for r0, r1 in row_blocks(b):
             _lib.call("disco_b200_backward_rows", *plan.args, r0, r1, st)
             _lib.call("disco_b200_combine_rows", *plan.args, t, flip, r0, r1,
                       d_image.data_ptr(), d_text.data_ptr(), D, st)
@@ -682,8 +732,6 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         if N > 1:
             endpoint.all_gather_into(plan.ce_all, plan.ce)
         _lib.call("disco_b200_loss", *plan.args, 0, st)
-    _leave(plan, cur_stream)
-    return d_image, d_text, plan
 
 
 def _check_step_inputs(local_I, local_T) -> None:
@@ -718,8 +766,19 @@ def finish_status(plan: Plan) -> float:
     loss, flags = _read_status(plan)
     if plan._copy_stream is not None:
         plan._copy_stream.synchronize()
+    _refresh_host_rows(plan)
     _raise_on_flags(flags)
     return loss
+
+
+def _refresh_host_rows(plan: Plan) -> None:
+    """Row-block steps copy each block to the host as soon as it is combined; rows the dual
+    fixup recomputed afterwards (plan.fixed_rows > 0, normally none) are copied again here."""
+    pending, plan.pending_host = plan.pending_host, None
+    if pending is not None and plan.fixed_rows > 0:
+        d_image, d_text, h_image, h_text = pending
+        h_image.copy_(d_image)
+        h_text.copy_(d_text)
 
 
 def logit_scale_grad_async(endpoint, plan: Plan, d_image, d_text, t: float) -> None:

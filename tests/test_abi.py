@@ -135,23 +135,21 @@ def test_wavefront_forward_availability():
     assert _lib.forward_waves(32768, 512, 2, 0) == 0
 
 
-def test_path_info_reports_the_fused_single_rank_backward(monkeypatch):
-    """Geometry only (no GPU): the fused single-rank backward is opt-in (DISCO_HFUSE=1, read per
-    call) -- the default keeps N = 1 bit-for-bit equal to N > 1 -- and applies only to wide
-    canonical shapes at N = 1."""
+def test_path_info_reports_the_dual_backward(monkeypatch):
+    """Geometry only (no GPU): disco_step's backward is the dual one (rank-local H = G_d + G_d'^T
+    GEMMs, no gradient reduce-scatter) wherever the forward stores E (B % 1024 == 0, N | 8), at
+    every world size; DISCO_BACKWARD=exchange (read per call) selects the exchange backward."""
     from paper_2304_08480_b200 import _lib
-    monkeypatch.delenv("DISCO_HFUSE", raising=False)
-    monkeypatch.delenv("DISCO_SYMMETRIC", raising=False)
+    monkeypatch.delenv("DISCO_BACKWARD", raising=False)
+    for B, D, N in [(32768, 512, 1), (32768, 512, 8), (65536, 768, 8), (16384, 1024, 1), (1024, 16, 2),
+                    (196608, 512, 8)]:
+        bits = _lib.path_info(B, D, N)
+        assert bits & _lib.PATH_ESTORE and bits & _lib.PATH_DUAL, (B, D, N)
+    assert _lib.path_info(32768, 512, 1) & _lib.PATH_WIDE
+    assert not _lib.path_info(65536, 768, 8) & _lib.PATH_WIDE
+    for B, D, N in [(1000, 100, 1), (96, 24, 3), (3072, 512, 3)]:  # no stored E: recompute + exchange
+        assert not _lib.path_info(B, D, N) & (_lib.PATH_ESTORE | _lib.PATH_DUAL), (B, D, N)
+    assert not _lib.path_info(4096, 4096, 1) & _lib.PATH_DUAL  # Dp > 2048: the fixup's row limit
+    monkeypatch.setenv("DISCO_BACKWARD", "exchange")
     bits = _lib.path_info(32768, 512, 1)
-    assert bits & _lib.PATH_ESTORE and bits & _lib.PATH_WIDE and not bits & _lib.PATH_HFUSE
-    monkeypatch.setenv("DISCO_HFUSE", "1")
-    assert _lib.path_info(32768, 512, 1) & _lib.PATH_HFUSE
-    assert not _lib.path_info(32768, 512, 2) & _lib.PATH_HFUSE
-    assert not _lib.path_info(65536, 768, 1) & _lib.PATH_HFUSE          # D = 768: not wide
-    assert not _lib.path_info(2048, 512, 1) & _lib.PATH_HFUSE           # B < 4096: no K split
-    assert _lib.path_info(16384, 1024, 1) & _lib.PATH_HFUSE             # config E
-    # the symmetric forward is a profiling experiment compiled only into -DDISCO_EXPERIMENTS=1
-    # builds: the default library ignores DISCO_SYMMETRIC
-    monkeypatch.setenv("DISCO_SYMMETRIC", "1")
-    bits = _lib.path_info(32768, 512, 1)
-    assert not bits & _lib.PATH_SYM and bits & _lib.PATH_HFUSE
+    assert bits & _lib.PATH_ESTORE and not bits & _lib.PATH_DUAL

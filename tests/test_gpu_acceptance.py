@@ -109,12 +109,11 @@ def _run_sim(Id, Td, world, t, peer=False):
             [r[2] for r in res])
 
 
-@pytest.mark.parametrize("peer", [False, True], ids=["all_to_all", "peer"])
+@pytest.mark.parametrize("peer", [False, True], ids=["nccl", "peer"])
 def test_headline_shape_bitwise_across_world_sizes(release_plans, monkeypatch, peer):
     """B = 32768, D = 512 (BASELINE config B): N = 2, 4, 8 simulated ranks reproduce N = 1 bit for
-    bit (the default, N-invariant backward), through the all_to_all exchange and through the peer
-    transport; N = 1 is checked against the f64 oracle on sampled rows."""
-    monkeypatch.setenv("DISCO_HFUSE", "0")
+    bit (the default dual backward), with the endpoint all_gather and with the peer all-gather;
+    N = 1 is checked against the f64 oracle on sampled rows."""
     monkeypatch.setenv("DISCO_PEER_TIMEOUT", "30")
     B, D, t = 32768, 512, 100.0
     I, T = O.synthetic_features(B, D, 7)

@@ -94,10 +94,10 @@ def test_single_gpu_vs_oracle(B, D):
     assert max(e) < TOL, e
 
 
-def test_bitwise_identical_across_world_sizes(monkeypatch):
-    """N-invariance of the default (two-GEMM-pair) path; the opt-in fused single-rank backward
-    (DISCO_HFUSE=1, test_fused_backward_*) rounds differently, so it is pinned off here."""
-    monkeypatch.setenv("DISCO_HFUSE", "0")
+@pytest.mark.parametrize("backward", ["dual", "exchange"])
+def test_bitwise_identical_across_world_sizes(monkeypatch, backward):
+    """N-invariance of both backwards (the default dual one and DISCO_BACKWARD=exchange)."""
+    monkeypatch.setenv("DISCO_BACKWARD", backward)
     B, D, t = 8192, 512, 100.0
     I, T = O.synthetic_features(B, D, 2)
     base = None
@@ -254,8 +254,8 @@ def test_host_pipelined_nonfinite_in_late_chunk():
 
 def test_config_e_bitwise_and_sampled_oracle(release_plans, monkeypatch):
     """BASELINE config E (B=16384, D=1024: the non-distributed CLIP loss on one GPU): the
-    default path at N=1 equals N=8 simulated ranks bit for bit; it and the opt-in fused backward
-    match the f64 oracle on sampled rows within 1e-3."""
+    default (dual) path at N=1 equals N=8 simulated ranks bit for bit; it and the exchange
+    backward match the f64 oracle on sampled rows within 1e-3."""
     B, D, t = 16384, 1024, 100.0
     I, T = O.synthetic_features(B, D, 12)
     d8 = run_sim(I, T, 8, t)
@@ -263,11 +263,11 @@ def test_config_e_bitwise_and_sampled_oracle(release_plans, monkeypatch):
     clear_plans()
     rows = np.linspace(0, B - 1, 48).astype(np.int64)
     ri, rt, rl = O.clip_grad_rows(I, T, t, rows)
-    for hfuse in ("0", "1"):
-        monkeypatch.setenv("DISCO_HFUSE", hfuse)
+    for backward in ("dual", "exchange"):
+        monkeypatch.setenv("DISCO_BACKWARD", backward)
         di, dt, loss = P.disco_step(None, dev(I), dev(T), t)
         di, dt = di.cpu().numpy(), dt.cpu().numpy()
-        if hfuse == "0":
+        if backward == "dual":
             assert di.tobytes() == d8[0].tobytes() and dt.tobytes() == d8[1].tobytes() and loss == d8[2][0]
         assert O.max_rel_error(di[rows], ri) < TOL
         assert O.max_rel_error(dt[rows], rt) < TOL
@@ -296,54 +296,29 @@ def test_streamed_forward_missing_chunk_times_out():
     assert torch.equal(dh_i, dd_i.cpu()) and torch.equal(dh_t, dd_t.cpu()) and lh == ld
 
 
-@pytest.mark.parametrize("B,D", [(2048, 512), (8192, 256)])
-def test_symmetric_forward_vs_oracle(B, D, monkeypatch):
-    """DISCO_SYMMETRIC=1 (experiment, off by default): one GEMM of S_0 feeds both directions
-    (S_1 = S_0^T; t2i column statistics reduced across lanes in the epilogue).  Within the
-    contract tolerance of the f64 oracle and of the two-GEMM path, on the device path, the host
-    wavefront path (f32 host inputs) and the streamed path (pinned bf16 host inputs)."""
-    from paper_2304_08480_b200 import _lib
-    monkeypatch.setenv("DISCO_SYMMETRIC", "1")
-    if not _lib.path_info(B, D, 1) & _lib.PATH_SYM:
-        pytest.skip("symmetric forward: experiment, compiled only with -DDISCO_EXPERIMENTS=1")
-    monkeypatch.delenv("DISCO_SYMMETRIC")
-    I, T = O.synthetic_features(B, D, 7)
-    bi, bt, bl = (x.cpu().numpy() if torch.is_tensor(x) else x for x in P.disco_step(None, dev(I), dev(T), 100.0))
-    monkeypatch.setenv("DISCO_SYMMETRIC", "1")
-    di, dt, loss = P.disco_step(None, dev(I), dev(T), 100.0)
-    di, dt = di.cpu().numpy(), dt.cpu().numpy()
-    assert max(errors(di, dt, loss, I, T, 100.0)) < TOL
-    assert O.max_rel_error(di, bi) < 1e-3 and O.max_rel_error(dt, bt) < 1e-3 and abs(loss - bl) / bl < 1e-6
-    hi, ht, hl = P.disco_step(None, I.astype(np.float32), T.astype(np.float32), 100.0)
-    assert np.array_equal(hi, di) and np.array_equal(ht, dt) and hl == loss
-    Ih = torch.from_numpy(I.astype(np.float32)).bfloat16().pin_memory()
-    Th = torch.from_numpy(T.astype(np.float32)).bfloat16().pin_memory()
-    si, stt, sl = P.disco_step(None, Ih, Th, 100.0)
-    assert torch.equal(si, torch.from_numpy(di)) and torch.equal(stt, torch.from_numpy(dt)) and sl == loss
-
-
 @pytest.mark.parametrize("B,D", [(4096, 512), (8192, 1024), (5120, 500), (4096, 1000)])
-def test_fused_backward_vs_oracle(B, D, monkeypatch):
-    """Opt-in fused single-rank backward (DISCO_HFUSE=1; wide D, B >= 4096): one GEMM per
-    gradient on H = G_0 + G_1^T built in shared memory from E_0 and E_1 (ldmatrix / .trans).
-    Within the contract tolerance of the f64 oracle and of the default (N-invariant) path; the
-    host row-block path and the contribution path (local_loss_and_grads) give the same bytes;
-    repeat runs are bitwise equal."""
+def test_dual_and_exchange_backwards_vs_oracle(B, D, monkeypatch):
+    """The dual backward (default; one GEMM per gradient on H = G_d + G_d'^T over the rank's own
+    E block) and the exchange backward (DISCO_BACKWARD=exchange; intra + cross GEMMs) are both
+    within the contract tolerance of the f64 oracle and of each other; the host row-block path
+    gives the device path's bytes; local_loss_and_grads (always the exchange form) equals the
+    exchange step at N = 1; repeat runs are bitwise equal."""
     I, T = O.synthetic_features(B, D, 21)
-    monkeypatch.delenv("DISCO_HFUSE", raising=False)
+    monkeypatch.setenv("DISCO_BACKWARD", "exchange")
     bi, bt, bl = P.disco_step(None, dev(I), dev(T), 100.0)
     bi, bt = bi.cpu().numpy(), bt.cpu().numpy()
-    monkeypatch.setenv("DISCO_HFUSE", "1")
-    di, dt, loss = P.disco_step(None, dev(I), dev(T), 100.0)
-    di, dt = di.cpu().numpy(), dt.cpu().numpy()
-    assert not np.array_equal(di, bi)  # the fused path really ran (different rounding)
-    assert max(errors(di, dt, loss, I, T, 100.0)) < TOL
-    assert O.max_rel_error(di, bi) < 1e-3 and O.max_rel_error(dt, bt) < 1e-3 and abs(loss - bl) / bl < 1e-6
-    hi, ht, hl = P.disco_step(None, I.astype(np.float32), T.astype(np.float32), 100.0)
-    assert np.array_equal(hi, di) and np.array_equal(ht, dt) and hl == loss
+    assert max(errors(bi, bt, bl, I, T, 100.0)) < TOL
     c = P.local_loss_and_grads(P.ShardLayout(world_size=1, global_batch=B, rank=0), I.astype(np.float32),
                                T.astype(np.float32), 100.0)
-    assert np.array_equal(np.asarray(c.d_image_full, dtype=np.float32), di)
-    assert np.array_equal(np.asarray(c.d_text_full, dtype=np.float32), dt)
+    assert np.array_equal(np.asarray(c.d_image_full, dtype=np.float32), bi)
+    assert np.array_equal(np.asarray(c.d_text_full, dtype=np.float32), bt)
+    monkeypatch.delenv("DISCO_BACKWARD")
+    di, dt, loss = P.disco_step(None, dev(I), dev(T), 100.0)
+    di, dt = di.cpu().numpy(), dt.cpu().numpy()
+    assert not np.array_equal(di, bi)  # the dual path really ran (different rounding)
+    assert max(errors(di, dt, loss, I, T, 100.0)) < TOL
+    assert O.max_rel_error(di, bi) < 1e-3 and O.max_rel_error(dt, bt) < 1e-3 and loss == bl
+    hi, ht, hl = P.disco_step(None, I.astype(np.float32), T.astype(np.float32), 100.0)
+    assert np.array_equal(hi, di) and np.array_equal(ht, dt) and hl == loss
     ri, rt, rl = P.disco_step(None, dev(I), dev(T), 100.0)
     assert np.array_equal(ri.cpu().numpy(), di) and np.array_equal(rt.cpu().numpy(), dt) and rl == loss

@@ -1,6 +1,8 @@
 """GPU: the peer transport against the all_to_all path and N = 1.
 
-The backward GEMM pushes every cross tile into the owner's peer window (TMA stores through
+Both backwards run over it: the default dual backward (the peer all-gather of the packed rows,
+then only the row statistics are exchanged) and the exchange backward (DISCO_BACKWARD=exchange),
+whose backward GEMM pushes every cross tile into the owner's peer window (TMA stores through
 per-destination tensor maps), a one-warp kernel publishes an arrival epoch, and the owner's
 combine waits for all N epochs.  Results must be bit-identical to the NCCL-style path (same
 fixed tree, evaluated at the owner), to N = 1, and must stay so across steps (the two parity
@@ -49,9 +51,10 @@ def sim(I, T, N, t, peer, steps=1, **kw):
     return di, dt, [r[2] for r in res]
 
 
+@pytest.mark.parametrize("backward", ["dual", "exchange"])
 @pytest.mark.parametrize("B,D", [(4096, 512), (2048, 768), (3072, 256)])
-def test_peer_matches_all_to_all_and_single_rank(B, D, monkeypatch):
-    monkeypatch.setenv("DISCO_HFUSE", "0")  # N = 1 reference: the N-invariant path (the default; pinned)
+def test_peer_matches_all_to_all_and_single_rank(B, D, monkeypatch, backward):
+    monkeypatch.setenv("DISCO_BACKWARD", backward)
     I, T = O.synthetic_features(B, D, 7)
     di1, dt1, l1 = P.disco_step(None, dev(I), dev(T), 100.0)
     di1, dt1 = di1.cpu().numpy(), dt1.cpu().numpy()
@@ -69,7 +72,9 @@ def test_peer_matches_all_to_all_and_single_rank(B, D, monkeypatch):
     assert O.max_rel_error(di1, ri) < 1e-3 and O.max_rel_error(dt1, rt) < 1e-3
 
 
-def test_peer_sign_flip_matches_all_to_all():
+@pytest.mark.parametrize("backward", ["dual", "exchange"])
+def test_peer_sign_flip_matches_all_to_all(monkeypatch, backward):
+    monkeypatch.setenv("DISCO_BACKWARD", backward)
     B, D = 2048, 256
     I, T = O.synthetic_features(B, D, 8)
     pi, pt, _ = sim(I, T, 2, 10.0, peer=True, flip_cross_rank_sign=True)
@@ -90,6 +95,7 @@ def test_peer_missing_rank_times_out_instead_of_hanging(monkeypatch):
     from paper_2304_08480_b200.shard import get_plan
 
     monkeypatch.setattr(peer_mod, "PEER_TIMEOUT_S", 0.5)
+    monkeypatch.setenv("DISCO_BACKWARD", "exchange")
     B, D = 2048, 256
     I, T = O.synthetic_features(B, D, 9)
     Id, Td = dev(I), dev(T)
@@ -112,8 +118,10 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("mode,streamed", [("peer", "0"), ("peer", "1"), ("nccl", "0"), ("fallback", "0")])
-def test_peer_two_processes_ipc(tmp_path, mode, streamed):
+@pytest.mark.parametrize("mode,streamed,backward", [("peer", "0", "dual"), ("peer", "1", "dual"), ("nccl", "0", "dual"),
+                                                    ("fallback", "0", "dual"), ("peer", "0", "exchange"),
+                                                    ("nccl", "0", "exchange")])
+def test_peer_two_processes_ipc(tmp_path, monkeypatch, mode, streamed, backward):
     """Two processes, one GPU, gloo: bitwise equal to N = 1.  ``peer``: CUDA IPC windows, with the
     kernel all-gather and (small B, where the shared GPU's time slicing lets both ranks publish
     before either spins for long) the streamed copy-engine all-gather.  ``nccl``: DISCO_PEER=0, the
@@ -127,7 +135,8 @@ def test_peer_two_processes_ipc(tmp_path, mode, streamed):
     np.save(tmp_path / "T.npy", T.astype(np.float32))
     port = _free_port()
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2",
-               DISCO_PEER_STREAMED=streamed, DISCO_PEER_TIMEOUT="30", DISCO_PEER="0" if mode == "nccl" else "1")
+               DISCO_PEER_STREAMED=streamed, DISCO_PEER_TIMEOUT="30", DISCO_PEER="0" if mode == "nccl" else "1",
+               DISCO_BACKWARD=backward)
     procs = []
     for r in range(2):
         e = dict(env, RANK=str(r))
@@ -141,6 +150,7 @@ def test_peer_two_processes_ipc(tmp_path, mode, streamed):
             p.kill()
             rcs.append("timeout")
     assert rcs == [0, 0], rcs
+    monkeypatch.setenv("DISCO_BACKWARD", backward)
     di1, dt1, l1 = P.disco_step(None, dev(I), dev(T), 100.0)
     got_i = np.concatenate([np.load(tmp_path / f"di{r}.npy") for r in range(2)])
     got_t = np.concatenate([np.load(tmp_path / f"dt{r}.npy") for r in range(2)])

@@ -83,23 +83,40 @@ def summarize_rep(rep):
     return out
 
 
-def launches_md(path):
+def launches_md(path, hbm_gbs=None):
+    """Launch list of one step from an ncu metrics CSV (one row per kernel x metric): duration and,
+    when captured, DRAM bytes -> achieved GB/s per launch (the HBM side of the elementwise tails)."""
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h = rows[hi]
-    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    lines = ["| # | kernel | time (us) |", "|---|---|---|"]
-    total = 0.0
-    n = 0
+    ii, ki, mi, vi, ui = h.index("ID"), h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), \
+        h.index("Metric Unit")
+    launches = {}
+    order = []
     for r in rows[hi + 1:]:
         if "disco" not in r[ki]:
             continue
-        t = float(r[vi].replace(",", "")) * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[ui], 1.0)
-        lines.append(f"| {n} | `{r[ki][:70]}` | {t:.1f} |")
+        if r[ii] not in launches:
+            launches[r[ii]] = {"name": r[ki]}
+            order.append(r[ii])
+        launches[r[ii]][r[mi]] = float(r[vi].replace(",", "")) * UNIT_SCALE.get(r[ui], 1.0)
+    lines = ["| # | kernel | time (us) | DRAM read (MB) | DRAM write (MB) | GB/s |", "|---|---|---|---|---|---|"]
+    total = 0.0
+    table = []
+    for n, key in enumerate(order):
+        L = launches[key]
+        t = L.get("gpu__time_duration.sum", 0.0)
+        rd, wr = L.get("dram__bytes_read.sum"), L.get("dram__bytes_write.sum")
+        gbs = (rd + wr) / t / 1e9 if (rd is not None and wr is not None and t > 0) else None
+        lines.append(f"| {n} | `{L['name'][:70]}` | {t * 1e6:.1f} | "
+                     f"{'' if rd is None else f'{rd / 1e6:.1f}'} | {'' if wr is None else f'{wr / 1e6:.1f}'} | "
+                     f"{'' if gbs is None else f'{gbs:.0f}'} |")
+        table.append({"kernel": L["name"][:90], "us": t * 1e6, "dram_read_mb": None if rd is None else rd / 1e6,
+                      "dram_write_mb": None if wr is None else wr / 1e6, "gbs": gbs,
+                      "frac_of_hbm": (gbs / hbm_gbs) if (gbs and hbm_gbs) else None})
         total += t
-        n += 1
-    lines.append(f"| | total ({n} disco launches) | {total:.1f} |")
-    return "\n".join(lines)
+    lines.append(f"| | total ({len(order)} disco launches) | {total * 1e6:.1f} | | | |")
+    return "\n".join(lines), table
 
 
 def main():
@@ -119,10 +136,22 @@ def main():
     with open(os.path.join(root, "ncu_summary.json"), "w") as f:
         json.dump({k: v["dram_bytes_per_launch"] for k, v in summ.items()}, f, indent=1)
     if a.launches:
+        hbm = None
+        peaks = os.path.join(os.path.dirname(root), "MEASURED_PEAKS.json")
+        if os.path.exists(peaks):
+            try:
+                pk = json.load(open(peaks))
+                hbm = pk.get("hbm_copy_gbs") or pk.get("hbm_gbs")
+            except Exception:
+                hbm = None
+        md, table = launches_md(a.launches, hbm or 6650.0)
         with open(os.path.join(a.out, "launches.md"), "w") as f:
-            f.write("Serialised launch list (ncu --metrics gpu__time_duration.sum --clock-control none), "
-                    "cold caches: compare shares, not absolutes.\n\n")
-            f.write(launches_md(a.launches) + "\n")
+            f.write("Serialised launch list of one step (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+                    "dram__bytes_write.sum --clock-control none), cold caches: compare shares, not absolutes. "
+                    "GB/s = DRAM bytes / launch time (the HBM side of the tails).\n\n")
+            f.write(md + "\n")
+        with open(os.path.join(a.out, "launches.json"), "w") as f:
+            json.dump({"hbm_peak_gbs": hbm or 6650.0, "launches": table}, f, indent=1)
     for k, v in summ.items():
         print(f"{k:12s} {v['gpu__time_duration.sum'] * 1e3:8.3f} ms  dram {v['dram_bytes_per_launch'] / 1e9:6.2f} GB  "
               f"tensor {v['sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed']:5.1f}%  "
