@@ -122,8 +122,9 @@ constexpr size_t SMEM_BYTES_XF = SMEM_BYTES + size_t(STAGES) * DUAL_Q_BYTES;
 static_assert(SMEM_BYTES_XF <= 232448, "E-operand GEMM smem");
 // A row is fixed up (recomputed exactly, dual_fixup_kernel) when one of its groups' maxima exceeds
 // the smallest column LSE of the group by more than this (log2 units): only then can an E entry
-// below the f16 normal range (29 binades under m_g) carry >= 2^-12 of a column's softmax mass.
-constexpr float DUAL_SAFE_SPAN = 17.f;
+// below the f16 normal range (29 binades under m_g) carry >= 2^-13 of a column's softmax mass,
+// and only then can the f16 factor a_r + p_r q_c exceed 2^15.
+constexpr float DUAL_SAFE_SPAN = 16.f;
 static_assert(sizeof(uint64_t) * 46 + 4 <= 512, "control block");
 
 // -------------------------------------------------------- status flag bits
@@ -1164,18 +1165,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
       const int m0 = mt * PAIR_M + crank * BM;
       if (q.xform == 2) {
         // Dual backward: thread xt owns row r = m0 + xt of this direction's E block (K-major) and
-        // rewrites each 64-column stage to H' = E (a_r + p_r q_c) in fp32 (one f16 rounding).  The
-        // label column is zeroed (its fp32 value is added by the combine).  The row's group
-        // maxima and the group metadata run XPF stages ahead.
+        // rewrites each 64-column stage to H' = E f with f = a_r + p_r q_c formed in fp32 (FFMA2)
+        // and rounded once to f16 (saturating: only rows the fixup recomputes can exceed the
+        // range), the product by HMUL2 -- the exchange backward's roundings.  The label column is
+        // zeroed (the combine adds its fp32 value).  All 8 E chunks are loaded before any math and
+        // the column factors one chunk ahead; the row's group maxima and the group metadata run
+        // XPF stages ahead.
         const int r = m0 + xt;
         const bool act = r < q.xb;  // rows past b were zero-filled by TMA: nothing to transform
         const float lse_r = act ? q.xlse[r] : 0.f;
+        const float* xmg_r = q.xmg + r;
+        const float2* xgm = q.xgm;
+        const int64_t xb = q.xb;
+        const int lab_base = q.lab_off + r;
         const int sw = xt & 7;
         int k0, nk;
         k_range(q, kc, k0, nk);
-        constexpr int XPF = 4;
-        auto ld_mg = [&](int kb) { return (act && kb < nk) ? q.xmg[int64_t((k0 + kb * BK) >> 6) * q.xb + r] : 0.f; };
-        auto ld_gm = [&](int kb) { return kb < nk ? q.xgm[(k0 + kb * BK) >> 6] : make_float2(0.f, 0.f); };
+        constexpr int XPF = 6;
+        auto ld_mg = [&](int kb) { return (act && kb < nk) ? xmg_r[int64_t((k0 + kb * BK) >> 6) * xb] : 0.f; };
+        auto ld_gm = [&](int kb) { return kb < nk ? xgm[(k0 + kb * BK) >> 6] : make_float2(0.f, 0.f); };
         float mq[XPF];
         float2 gq[XPF];
 #pragma unroll
@@ -1197,23 +1205,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
             if (act) {
               unsafe |= mg - gm.y > DUAL_SAFE_SPAN;
-              const float a = ptx::ex2(mg + (H_DUAL_LOG2 - E_HEADROOM) - lse_r), pr = ptx::ex2(mg + (H_DUAL_LOG2 - E_HEADROOM) - gm.x);
+              const float a = ptx::ex2(mg + (H_DUAL_LOG2 - E_HEADROOM) - lse_r);
+              const float pr = ptx::ex2(mg + (H_DUAL_LOG2 - E_HEADROOM) - gm.x);
               const float2 a2 = make_float2(a, a), p2 = make_float2(pr, pr);
               const uint32_t rowp = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES + xt * 128);
               const uint32_t qs = ptx::smem_u32(qrec + pipe.stage * DUAL_Q_BYTES);
+              uint4 x[8];
+#pragma unroll
+              for (int c = 0; c < 8; ++c) x[c] = ptx::lds128(rowp + ((c ^ sw) << 4));
+              float4 q0 = ptx::lds128f(qs), q1 = ptx::lds128f(qs + 16);
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
-                uint4 x = ptx::lds128(rowp + ((c ^ sw) << 4));
-                const float4 q0 = ptx::lds128f(qs + 32 * c), q1 = ptx::lds128f(qs + 32 * c + 16);
+                float4 n0, n1;
+                if (c < 7) {
+                  n0 = ptx::lds128f(qs + 32 * (c + 1));
+                  n1 = ptx::lds128f(qs + 32 * (c + 1) + 16);
+                }
                 const float2 qv[4] = {make_float2(q0.x, q0.y), make_float2(q0.z, q0.w), make_float2(q1.x, q1.y),
                                       make_float2(q1.z, q1.w)};
-                __half2* h = reinterpret_cast<__half2*>(&x);
+                __half2* h = reinterpret_cast<__half2*>(&x[c]);
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  h[e] = __float22half2_rn(ptx::fmul2(__half22float2(h[e]), ptx::ffma2(p2, qv[e], a2)));
-                ptx::sts128(rowp + ((c ^ sw) << 4), x);
+                for (int e = 0; e < 4; ++e) {
+                  const uint32_t f = ptx::f2_to_h2_satfinite(ptx::ffma2(p2, qv[e], a2));
+                  h[e] = __hmul2(h[e], *reinterpret_cast<const __half2*>(&f));
+                }
+                ptx::sts128(rowp + ((c ^ sw) << 4), x[c]);
+                if (c < 7) {
+                  q0 = n0;
+                  q1 = n1;
+                }
               }
-              const int lab_rel = q.lab_off + r - k;
+              const int lab_rel = lab_base - k;
               if (unsigned(lab_rel) < 64u) ptx::sts16(rowp + (((lab_rel >> 3) ^ sw) << 4) + (lab_rel & 7) * 2, 0);
               ptx::fence_proxy_async_smem();
             }

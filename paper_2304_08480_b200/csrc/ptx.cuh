@@ -455,6 +455,12 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return f2_from(r);
 }
 
+// (lo, hi) f32 -> f16x2, saturating to +-65504 instead of overflowing to inf
+__device__ __forceinline__ uint32_t f2_to_h2_satfinite(float2 v) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(v.y), "f"(v.x));
+  return r;
+}
 __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   unsigned long long r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));

@@ -27,6 +27,7 @@ ap.add_argument("--so-b", default=None, help="second library build to alternate 
 ap.add_argument("--so", nargs="*", default=[], help="more library builds to alternate with (name=path or path)")
 ap.add_argument("--reps", type=int, default=15)
 ap.add_argument("--warm", type=float, default=3.0, help="seconds of untimed steps first (clocks ramp)")
+ap.add_argument("--exchange", action="store_true", help="time the exchange backward instead of the dual one")
 a = ap.parse_args()
 
 torch.cuda.set_device(0)
@@ -75,10 +76,16 @@ def run(lib, flags, ev):
     ev[0].record(st)
     assert lib.disco_b200_forward(*args, t, sp) == 0
     ev[1].record(st)
-    assert lib.disco_b200_backward_grad(*args, t, sp) == 0
-    assert lib.disco_b200_backward_fused(*args, sp) == 0
-    ev[2].record(st)
-    assert lib.disco_b200_combine(*args, t, 0, di.data_ptr(), dt.data_ptr(), D, sp) == 0
+    if a.exchange:
+        assert lib.disco_b200_backward_grad(*args, t, sp) == 0
+        assert lib.disco_b200_backward_fused(*args, sp) == 0
+        ev[2].record(st)
+        assert lib.disco_b200_combine(*args, t, 0, di.data_ptr(), dt.data_ptr(), D, sp) == 0
+    else:
+        assert lib.disco_b200_dual_prep(*args, 0, sp) == 0
+        assert lib.disco_b200_backward_dual(*args, 0, B, sp) == 0
+        ev[2].record(st)
+        assert lib.disco_b200_combine_dual(*args, t, 0, B, di.data_ptr(), dt.data_ptr(), D, sp) == 0
     ev[3].record(st)
 
 
@@ -101,7 +108,10 @@ for rep in range(a.reps + 2):
                 times[k][i].append(ev[i].elapsed_time(ev[i + 1]))
             mhz.setdefault(k, []).append(_lib.clock_probe(plan))
 for k, (fw, bw, cb) in times.items():
-    print(f"{k:10s} forward {statistics.median(fw):.4f}  backward {statistics.median(bw):.4f}  "
+    mf = statistics.median(m['logits_fwd'] for m in mhz[k])
+    mb = statistics.median(m['gemm_backward'] for m in mhz[k])
+    print(f"{k:10s} cycles(k) fwd {statistics.median(fw) * mf:.0f} bwd {statistics.median(bw) * mb:.0f}   "
+          f"forward {statistics.median(fw):.4f}  backward {statistics.median(bw):.4f}  "
           f"combine {statistics.median(cb):.4f}  total {statistics.median(fw) + statistics.median(bw) + statistics.median(cb):.4f} ms"
           f"  SM MHz fwd {statistics.median(m['logits_fwd'] for m in mhz[k]):.0f} "
           f"bwd {statistics.median(m['gemm_backward'] for m in mhz[k]):.0f} "
