@@ -48,6 +48,26 @@ def supported(B: int, D: int, world: int, rank: int) -> bool:
     return True
 
 
+def in_process_fence(endpoint, stream) -> None:
+    """Simulated ranks (threads sharing ONE GPU, ``endpoint.in_process``): order every rank's
+    signalled work before any rank's wait kernel, so a wait kernel never spins.
+
+    On one shared device a spinning wait kernel can deadlock against a peer thread's allocation:
+    a device/pinned-memory allocation implicitly serialises the streams, so a publish enqueued
+    after another thread's ``cudaMalloc`` waits for the spinning kernel that waits for it (seen as
+    a 60 s wait timeout with garbage operands on a CPU-contended box).  Each rank records an event
+    after its signal, the events are exchanged through the host rendezvous and every rank's stream
+    waits on all of them: the wait kernels still read the device flags (the protocol is unchanged)
+    but find them already raised.  Processes with a GPU each never take this path."""
+    if not getattr(endpoint, "in_process", False):
+        return
+    import torch
+    ev = torch.cuda.Event()
+    ev.record(stream)
+    for e in endpoint.exchange(ev):
+        stream.wait_event(e)
+
+
 class PeerUnavailable(RuntimeError):
     """The peer transport cannot run on this group (no peer access between some pair of GPUs, or
     the IPC mapping failed on some rank).  Raised on EVERY rank (the decision is collective), so

@@ -628,6 +628,7 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         if pw is not None:
             epoch, parity = pw.next_step()
             _lib.call("disco_b200_peer_publish", *plan.args, pw.bases, parity, epoch, st)
+            _peer.in_process_fence(endpoint, cur_stream)
             if _peer.streamed_gather(endpoint, B, N):
                 # copy-engine pulls gated by the peers' pack-ready flags, enqueued BEFORE the one
                 # persistent logits launch that consumes them column wave by column wave
@@ -699,6 +700,7 @@ def _exchange_backward(endpoint, plan: Plan, t: float, flip: int, d_image, d_tex
     if pw is not None:
         # the fused backward GEMM pushes each cross tile to its owner over NVLink
         _lib.call("disco_b200_backward_peer", *plan.args, pw.bases, parity, epoch, st)
+        _peer.in_process_fence(endpoint, torch.cuda.current_stream(device))
     elif N > 1:
         # cross first, so the slab exchange overlaps the intra GEMM
         _lib.call("disco_b200_backward_cross", *plan.args, st)
