@@ -456,7 +456,13 @@ enum { KIND_FWD = 0, KIND_GRAD = 1, KIND_FWDE = 2 };
 // is reloaded as soon as the unit's last tile has consumed it.  Halves the TMA fill traffic and
 // cuts smem traffic per MMA from ~128 to ~96 B/clk/SM (the narrow 256-column tile is smem-bound).
 #ifndef DISCO_FWD_STAGES
-#define DISCO_FWD_STAGES 6
+#define DISCO_FWD_STAGES 5  // 5 x 32 KiB: same-process A/B 2-3% fewer cycles than 6, 4 and 3 much slower
+#endif
+#ifndef DISCO_ESTORE_POLICY
+#define DISCO_ESTORE_POLICY ptx::kEvictFirst  // L2 policy of the forward's E stores
+#endif
+#ifndef DISCO_FWD_NOESTORE
+#define DISCO_FWD_NOESTORE 0
 #endif
 #ifndef DISCO_FWDE_WARPS
 #define DISCO_FWDE_WARPS 8
@@ -496,6 +502,14 @@ constexpr int FWDE_STAGES = FWDE_EPI == 16 ? 5 : FWD_STAGES;
 static_assert(FWDE_EPI == 8 || FWDE_EPI == 16, "FWDE epilogue warps");
 static_assert(FWDE_STAGES * STAGE_BYTES + FWDE_EPI * FWD_EBUFS * (STAGING_TILE / 2) <= TILE_RING_BYTES + STAGING_BYTES,
               "FWDE smem layout");
+#ifndef DISCO_WAITPROBE
+#define DISCO_WAITPROBE 0
+#endif
+#if DISCO_WAITPROBE
+// profiling build only: logits kernel barrier-wait cycles {MMA full, MMA tempty, MMA total, MMA
+// threads, epilogue tfull by warp quadrant x4}, read by disco_b200_waitprobe
+__device__ unsigned long long g_waitprobe[8];
+#endif
 template <int KIND, bool ARES>
 __host__ __device__ constexpr int logits_epi() { return (KIND == KIND_FWDE && !ARES) ? FWDE_EPI : NUM_EPI_WARPS; }
 template <int KIND, bool ARES>
@@ -689,10 +703,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
       Pipe<ARES_B_STAGES> bp;
       uint8_t* bring = tiles + ARES_SLICES * A_STAGE_BYTES;
       uint32_t it = 0, uphase = 0;
+#if DISCO_WAITPROBE
+      long long wp_full = 0, wp_tempty = 0;
+      const long long wp_t0 = clock64();
+#endif
       for (int u = pair; u < num_units; u += npairs, uphase ^= 1) {
         for (int ti = 0; ti < tiles_per_unit; ++ti, ++it) {
           const uint32_t buf = it & 1, use = it >> 1;
+#if DISCO_WAITPROBE
+          const long long w1 = clock64();
+#endif
           ptx::mbar_wait(&ctl->tempty[buf], (use & 1) ^ 1);
+#if DISCO_WAITPROBE
+          wp_tempty += clock64() - w1;
+#endif
           ptx::tc_fence_after();
           const uint32_t d_tmem = ctl->tmem_base + buf * BN;
           if constexpr (ARES) {
@@ -713,12 +737,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
               bp.advance();
             }
           } else {
+#if DISCO_WAITPROBE
+            for (int kb = 0; kb < nk; ++kb) {
+              const long long w0 = clock64();
+              ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
+              wp_full += clock64() - w0;
+              mma_blocks<1, false, LRS>(ctl, tiles, pipe, 1, kb, d_tmem, idesc, 0, 0, 0, 1, false, true);
+            }
+#else
             mma_tile<1, false, LRS>(ctl, tiles, pipe, nk, d_tmem, idesc, 0, 0);
+#endif
           }
           if (ptx::elect_one()) ptx::umma_commit_pair(&ctl->tfull[buf], 0x3);
           __syncwarp();
         }
       }
+#if DISCO_WAITPROBE
+      if (lane == 0) {
+        atomicAdd(&g_waitprobe[0], (unsigned long long)wp_full);
+        atomicAdd(&g_waitprobe[1], (unsigned long long)wp_tempty);
+        atomicAdd(&g_waitprobe[2], (unsigned long long)(clock64() - wp_t0));
+        atomicAdd(&g_waitprobe[3], 1ull);
+      }
+#endif
     }
   } else {  // ---------------------------- epilogue warps 2..(EPI + 1)
     const int ew = warp - 2;
@@ -735,9 +776,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (epend_rb < p.b)
+        if (epend_rb < p.b && !DISCO_FWD_NOESTORE)  // (profiling build: E stores off)
           ptx::tma_store_4d(&p.e_map[epend_dir], tile + epend_buf * (STAGING_TILE / 2), epend_cb & 127,
-                            epend_rb & 127, epend_cb >> 7, epend_rb >> 7);
+                            epend_rb & 127, epend_cb >> 7, epend_rb >> 7, DISCO_ESTORE_POLICY);
         ptx::bulk_commit();
       }
       epend = false;
@@ -776,7 +817,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
       }
       for (int ti = 0; ti < tiles_per_unit; ++ti, ++it) {
         const uint32_t buf = it & 1, use = it >> 1;
+#if DISCO_WAITPROBE
+        const long long w2 = clock64();
+#endif
         ptx::mbar_wait(&ctl->tfull[buf], use & 1);
+#if DISCO_WAITPROBE
+        if (lane == 0) atomicAdd(&g_waitprobe[4 + (ew & 3)], (unsigned long long)(clock64() - w2));
+#endif
         ptx::tc_fence_after();
         const int col0 = chunk_lo + (t0 + ti) * BN + cpart * PART_COLS;
         const uint32_t taddr = ctl->tmem_base + (uint32_t(quad * 32) << 16) + buf * BN + cpart * PART_COLS;
@@ -2974,7 +3021,10 @@ int exchange_scales(void* ws, const Geometry& g, cudaStream_t st) {
 
 // ---------------------------------------------------------------- peer transport (host side)
 int64_t peer_leaves(const Geometry& g) { return int64_t(g.N) * g.np; }
-int64_t peer_window_bytes(const Geometry& g) { return round_up(2 * peer_leaves(g) * g.b * g.Dp * 4, 1024); }
+// gradient slabs exist only for the exchange backward: the dual backward exchanges no gradients
+int64_t peer_window_bytes(const Geometry& g) {
+  return g.dual ? 0 : round_up(2 * peer_leaves(g) * g.b * g.Dp * 4, 1024);
+}
 int64_t peer_pack_bytes(const Geometry& g) { return round_up(2 * g.b * g.Dp * 2, 1024); }
 int64_t peer_ce_bytes(const Geometry& g) { return round_up(int64_t(g.N) * 2 * g.b * 4, 1024); }
 int64_t peer_total_bytes(const Geometry& g) {
@@ -3031,6 +3081,16 @@ int disco_b200_abi_version(void) { return DISCO_B200_ABI_VERSION; }
 
 int disco_b200_set_experiment_flags(int flags) { return g_debug_bits.exchange(flags); }
 
+#if DISCO_WAITPROBE
+int disco_b200_waitprobe(unsigned long long* out, int reset) {
+  CUDA_TRY(cudaMemcpyFromSymbol(out, disco::g_waitprobe, sizeof(disco::g_waitprobe)));
+  if (reset) {
+    static const unsigned long long z[8] = {};
+    CUDA_TRY(cudaMemcpyToSymbol(disco::g_waitprobe, z, sizeof(z)));
+  }
+  return DISCO_OK;
+}
+#endif
 int64_t disco_b200_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* disco_b200_last_error(void) { return g_last_error.c_str(); }
@@ -3565,6 +3625,7 @@ int disco_b200_backward_peer(void* ws, int64_t B, int64_t D, int world, int rank
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   if ((rc = check_peer(g))) return rc;
+  if (g.dual) return fail(DISCO_LAYOUT_ERROR, "peer gradient slabs need the exchange backward (DISCO_BACKWARD=exchange)");
   cudaStream_t st = st_of(stream);
   GemmParams p;
   memset(&p, 0, sizeof(p));
@@ -3697,6 +3758,7 @@ int disco_b200_combine_peer(void* ws, int64_t B, int64_t D, int world, int rank,
   int rc = make_geometry(B, D, world, rank, &g);
   if (rc) return rc;
   if ((rc = check_peer(g))) return rc;
+  if (g.dual) return fail(DISCO_LAYOUT_ERROR, "peer gradient slabs need the exchange backward (DISCO_BACKWARD=exchange)");
   if (ld_out < D) return fail(DISCO_SHAPE_ERROR, "output row stride smaller than D");
   cudaStream_t st = st_of(stream);
   Status* status = region<Status>(ws, g, DISCO_R_STATUS);

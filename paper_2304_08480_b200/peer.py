@@ -68,6 +68,13 @@ def in_process_fence(endpoint, stream) -> None:
         stream.wait_event(e)
 
 
+def window_bytes(B: int, D: int, world: int, rank: int) -> int:
+    """Size of a rank's peer window for the geometry (and backward mode) the library sees now."""
+    n = ctypes.c_int64()
+    _lib.call("disco_b200_peer_bytes", B, D, world, rank, ctypes.byref(n))
+    return n.value
+
+
 class PeerUnavailable(RuntimeError):
     """The peer transport cannot run on this group (no peer access between some pair of GPUs, or
     the IPC mapping failed on some rank).  Raised on EVERY rank (the decision is collective), so
@@ -98,9 +105,7 @@ class PeerWindow:
             devices = endpoint.exchange(torch.cuda.current_device())
             if not _peer_access_all_pairs(devices):
                 raise PeerUnavailable(f"no peer access between some pair of GPUs {sorted(set(devices))}")
-        nbytes = ctypes.c_int64()
-        _lib.call("disco_b200_peer_bytes", B, D, world, rank, ctypes.byref(nbytes))
-        self.nbytes = nbytes.value
+        self.nbytes = window_bytes(B, D, world, rank)
         handle = None if in_process else ctypes.create_string_buffer(lib.disco_b200_peer_handle_bytes())
         ptr = ctypes.c_void_p()
         _lib.call("disco_b200_peer_alloc", self.nbytes, ctypes.byref(ptr), handle)

@@ -167,8 +167,9 @@ class Plan:
     def peer_window(self, endpoint) -> "_peer.PeerWindow":
         """This rank's peer-transport window (created, and exchanged with the peers, on first use)."""
         group = getattr(endpoint, "group", None)
-        if self._peer is not None and self._peer_group is not group:  # a new group: new windows
-            self.close()
+        if self._peer is not None and (self._peer_group is not group
+                                       or self._peer.nbytes != _peer.window_bytes(self.B, self.D, self.world, self.rank)):
+            self.close()  # a new group, or the backward mode changed the window layout: new windows
         if self._peer is None:
             self._peer = _peer.PeerWindow(endpoint, self.B, self.D, self.world, self.rank)
             self._peer_group = group

@@ -105,17 +105,22 @@ def test_launch_counter_starts_at_zero_without_gpu():
     assert _lib.launch_count() >= 0
 
 
-def test_peer_window_geometry():
-    """Peer window = flag block + two parity windows of [2][N*np][b][Dp] f32 (every source's leaves)
-    + two parity areas of this rank's published [2][b][Dp] bf16 rows (the peer all-gather)."""
+@pytest.mark.parametrize("backward", ["dual", "exchange"])
+def test_peer_window_geometry(monkeypatch, backward):
+    """Peer window = flag block + two parity windows of [2][N*np][b][Dp] f32 (every source's leaves;
+    exchange backward only -- the dual backward exchanges no gradients) + two parity areas of this
+    rank's published [2][b][Dp] bf16 rows (the peer all-gather) + two of [N][2][b] f32 ce."""
+    monkeypatch.setenv("DISCO_BACKWARD", backward)
     out = ctypes.c_int64()
     lib = _lib.load()
     assert lib.disco_b200_peer_handle_bytes() == 64
-    # D = 768 (split width: wide + narrow launches) keeps one leaf per canonical chunk like D = 512
+    # D = 768 (split width: wide + narrow launches) keeps one leaf per canonical chunk like D = 512;
+    # B = 3072, N = 3 has no canonical chunks (no stored E, so no dual backward either)
     for B, D, N, leaves in [(32768, 512, 8, 8), (32768, 512, 2, 8), (65536, 768, 4, 8), (3072, 256, 3, 3)]:
         _lib.call("disco_b200_peer_bytes", B, D, N, 0, ctypes.byref(out))
         b, Dp = B // N, (D + 63) // 64 * 64
-        win = (2 * leaves * b * Dp * 4 + 1023) // 1024 * 1024
+        dual = backward == "dual" and _lib.path_info(B, D, N, 0) & _lib.PATH_DUAL
+        win = 0 if dual else (2 * leaves * b * Dp * 4 + 1023) // 1024 * 1024
         pack = (2 * b * Dp * 2 + 1023) // 1024 * 1024
         ce = (N * 2 * b * 4 + 1023) // 1024 * 1024
         assert out.value == 1024 + 2 * win + 2 * pack + 2 * ce, (B, D, N)
