@@ -2,13 +2,13 @@
 
   python tools/rank_projection.py [--batch 32768] [--dim 512] [--worlds 1 2 4 8] [--reps 10]
 
-For each N this runs rank 0's share of the step on the local GPU -- pack, unpack of a gathered
-buffer (filled once, untimed: the all_gather itself is NOT measured), the fused forward, the
-backward with the peer transport (cross tiles pushed by the GEMM epilogue into a local stand-in
-for the peer windows, arrival flags set locally) and the owner combine -- and reports the
-per-phase CUDA-event times, the per-rank FLOP rate and the compute-only projection
-B / t_rank.  NVLink traffic is replaced by local HBM writes and NCCL collectives are absent,
-so this is an upper bound on multi-GPU throughput, not a multi-GPU measurement.
+For each N this runs rank 0's share of the default (dual-backward) step on the local GPU --
+pack, unpack of a gathered buffer (filled once, untimed: the all_gather itself is NOT measured),
+the forward, the statistics "all_gather" (rank 0's 4 b statistics copied into every slot), the
+column factors, the dual backward GEMM, the combine, the fixup and the loss -- and reports the
+per-phase CUDA-event times, the per-rank FLOP rate (the reference's 12 b B D) and the
+compute-only projection B / t_rank.  The collectives are absent, so this is an upper bound on
+multi-GPU throughput, not a multi-GPU measurement.
 """
 import argparse
 import ctypes
@@ -58,40 +58,27 @@ for N, flags in [(N, f) for N in a.worlds for f in a.flags]:
         # the gathered buffer: every rank's packed rows (random unit vectors), filled once
         plan.gather.copy_(torch.nn.functional.normalize(
             torch.randn(N * 2 * b, plan.Dp, device=dev, generator=g), dim=1).bfloat16().view(-1))
-        nbytes = ctypes.c_int64()
-        _lib.call("disco_b200_peer_bytes", B, D, N, 0, ctypes.byref(nbytes))
-        window = torch.zeros(nbytes.value, dtype=torch.uint8, device=dev)
-        bases = (ctypes.c_uint64 * N)(*([window.data_ptr()] * N))
-        arrivals = window[:4 * N].view(torch.int32)
-    phases = ["pack", "forward", "backward", "combine", "loss"]
+    phases = ["pack", "forward", "stats", "backward", "combine", "loss"]
     acc = {k: [] for k in phases + ["step"]}
     for rep in range(a.reps + 3):
         flush.zero_()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(phases) + 1)]
         ev[0].record(st)
         _lib.call("disco_b200_pack", *args, I.data_ptr(), T.data_ptr(), D, D, _lib.BF16, 1, sp)
-        if N == 1:
-            ev[1].record(st)
-            _lib.call("disco_b200_forward", *args, t, sp)
-            _lib.call("disco_b200_backward_grad", *args, t, sp)
-            ev[2].record(st)
-            _lib.call("disco_b200_backward_fused", *args, sp)
-            ev[3].record(st)
-            _lib.call("disco_b200_combine", *args, t, 0, di.data_ptr(), dt.data_ptr(), D, sp)
-        else:
-            ev[1].record(st)
-            _lib.call("disco_b200_forward", *args, t, sp)
-            _lib.call("disco_b200_backward_grad", *args, t, sp)
-            ev[2].record(st)
-            epoch = rep + 1
-            _lib.call("disco_b200_backward_peer", *args, bases, epoch & 1, epoch, sp)
-            ev[3].record(st)
-            arrivals.fill_(epoch)  # the other ranks' arrivals (their pushes landed in the same window)
-            _lib.call("disco_b200_combine_peer", *args, t, 0, window.data_ptr(), epoch & 1, epoch, 5.0,
-                      di.data_ptr(), dt.data_ptr(), D, sp)
+        ev[1].record(st)
+        _lib.call("disco_b200_forward", *args, t, sp)
+        ev[2].record(st)
+        if N > 1:  # stand-in for the 16 b-byte statistics all_gather: rank 0's vector in every slot
+            plan.xall.view(N, -1).copy_(plan.xchg.view(1, -1).expand(N, -1))
+        _lib.call("disco_b200_dual_prep", *args, 0, sp)
+        ev[3].record(st)
+        _lib.call("disco_b200_backward_dual", *args, 0, b, sp)
         ev[4].record(st)
-        _lib.call("disco_b200_loss", *args, 1, sp)
+        _lib.call("disco_b200_combine_dual", *args, t, 0, b, di.data_ptr(), dt.data_ptr(), D, sp)
+        _lib.call("disco_b200_dual_fixup", *args, t, 0, di.data_ptr(), dt.data_ptr(), D, sp)
         ev[5].record(st)
+        _lib.call("disco_b200_loss", *args, 2, sp)
+        ev[6].record(st)
         torch.cuda.synchronize()
         if rep >= 3:
             for k, name in enumerate(phases):
