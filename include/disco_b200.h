@@ -290,6 +290,15 @@ int disco_b200_combine_dual(void* ws, int64_t B, int64_t D, int world, int rank,
                             float* d_image, float* d_text, int64_t ld_out, void* stream);
 int disco_b200_dual_fixup(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip, float* d_image,
                           float* d_text, int64_t ld_out, void* stream);
+/* Two-tower step: combine_dual + dual_fixup for rows [0, b) with the towers'
+ * l2_normalize_rows_backward (matrix.py:178-195) fused into the combine: besides d_image / d_text
+ * it writes dx = (d - (u . d) u) / ||raw|| per row (u = raw / ||raw||, f64 row sums, exactly the
+ * arithmetic of disco_b200_l2norm_rows_backward), rows the fixup recomputes included.
+ * norm_flags: bit0 non-finite dx, bit1 ||raw|| < 1e-12 (as disco_b200_l2norm_rows_backward). */
+int disco_b200_finish_dual_l2norm(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,
+                                  const float* raw_I, int64_t ld_raw_I, const float* raw_T, int64_t ld_raw_T,
+                                  float* d_image, float* d_text, int64_t ld_out, float* dx_image, float* dx_text,
+                                  int64_t ld_dx, int* norm_flags, void* stream);
 
 /* Loss: fixed-order f64 sum of the gathered per-row ce (DISCO_R_CE_ALL, or
  * DISCO_R_CE when world == 1 or local_only == 1) / (2 * rows) into DISCO_R_STATUS.

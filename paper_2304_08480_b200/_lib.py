@@ -86,6 +86,8 @@ SIGNATURES = {
     "disco_b200_backward_dual": [_vp, _i64, _i64, _int, _int, _i64, _i64, _vp],
     "disco_b200_combine_dual": [_vp, _i64, _i64, _int, _int, _f32, _i64, _i64, _vp, _vp, _i64, _vp],
     "disco_b200_dual_fixup": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _vp, _i64, _vp],
+    "disco_b200_finish_dual_l2norm": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _i64, _vp, _i64, _vp, _vp, _i64,
+                                      _vp, _vp, _i64, _vp, _vp],
     "disco_b200_l2norm_rows": [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp],
     "disco_b200_l2norm_rows_backward": [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp],
 }

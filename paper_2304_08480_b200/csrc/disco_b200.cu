@@ -612,25 +612,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       Pipe<LRS> pipe;
-      // L2 prefetch of the operands of the tile after the current one: the G
-      // write stream (GRAD) evicts feature lines, and a demand miss behind the
-      // DRAM write queue is longer than the smem ring can cover.
-      auto prefetch_tile = [&](int u, int ti) {
-        if (u >= num_units) return;
-        if (ti >= tiles_per_unit) {
-          u += npairs;
-          ti = 0;
-          if (u >= num_units) return;
-        }
-        int dir, rt, ch, t0;
-        decode(u, dir, rt, ch, t0);
-        const int a_row = p.rank * p.b + rt * PAIR_M + crank * BM;
-        const int col0 = ch * p.chunk_cols + (t0 + ti) * BN + crank * (BN / 2);
-        for (int kb = 0; kb < nk; ++kb) {
-          ptx::tma_prefetch_2d(&p.a_map[dir], kb * BK, a_row);
-          ptx::tma_prefetch_2d(&p.b_map[dir], kb * BK, col0);
-        }
-      };
       if constexpr (ARES) {
         Pipe<ARES_B_STAGES> bp;
         uint8_t* bring = tiles + ARES_SLICES * A_STAGE_BYTES;
@@ -2205,12 +2186,10 @@ __global__ void l2norm_rows_kernel(const float* raw, int64_t ld_raw, int rows, i
 }
 
 // d_raw = (g - (u . g) u) / ||x||, u = x / ||x||  (the backward of l2norm_rows)
-__global__ void l2norm_rows_backward_kernel(const float* raw, int64_t ld_raw, const float* grad, int64_t ld_grad,
-                                            int rows, int D, float* out, int64_t ld_out, int* flags) {
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const float* x = raw + int64_t(r) * ld_raw;
-  const float* g = grad + int64_t(r) * ld_grad;
+// (g - (u . g) u) / ||x|| for one row, one warp (matrix.py:178-195); shared by the tower kernel
+// and the fused dual finish so both produce the same bits
+__device__ __forceinline__ void l2norm_backward_row(const float* x, const float* g, int D, float* y, int* flags,
+                                                    int lane) {
   double ss = 0.0, xg = 0.0;
   for (int c = lane; c < D; c += 32) {
     ss += double(x[c]) * double(x[c]);
@@ -2225,7 +2204,6 @@ __global__ void l2norm_rows_backward_kernel(const float* raw, int64_t ld_raw, co
   if (lane == 0 && flags && n < NORM_EPSILON) atomicOr(flags, 2);
   const double inner = xg / n;  // u . g
   bool bad = false;
-  float* y = out + int64_t(r) * ld_out;
   for (int c = lane; c < D; c += 32) {
     const double u = double(x[c]) / n;
     const float v = float((double(g[c]) - inner * u) / n);
@@ -2233,6 +2211,62 @@ __global__ void l2norm_rows_backward_kernel(const float* raw, int64_t ld_raw, co
     y[c] = v;
   }
   if (flags && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1);
+}
+__global__ void l2norm_rows_backward_kernel(const float* raw, int64_t ld_raw, const float* grad, int64_t ld_grad,
+                                            int rows, int D, float* out, int64_t ld_out, int* flags) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  l2norm_backward_row(raw + int64_t(r) * ld_raw, grad + int64_t(r) * ld_grad, D, out + int64_t(r) * ld_out, flags,
+                      lane);
+}
+
+// Two-tower step: the dual combine with the towers' normalisation backward in
+// its epilogue.  One warp per (direction, row): d = combine_dual's value (same fp32 operations,
+// written out for the fixup), then dx = l2_normalize_rows_backward(raw, d) from the same row.
+struct TowerRows {
+  const float* raw[2];
+  int64_t ld_raw[2];
+  float* dx[2];
+  int64_t ld_dx;
+};
+__global__ void combine_dual_l2norm_kernel(const float* intra, int ksplit, const float* glabel,
+                                           const __nv_bfloat16* pack, int b, int Dp, int D, float s, float* d_image,
+                                           float* d_text, int64_t ld_out, TowerRows tw, Status* status,
+                                           int* norm_flags) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= 2 * b) return;
+  const int g = w / b, r = w - g * b;
+  const int64_t per_g = int64_t(b) * Dp;
+  const float* ib = intra + int64_t(g) * ksplit * per_g + int64_t(r) * Dp;
+  const float lab = glabel[r] + glabel[b + r];
+  const __nv_bfloat16* fr = pack + (int64_t(1 - g) * b + r) * Dp;
+  float* out = (g == 0 ? d_image : d_text) + int64_t(r) * ld_out;
+  constexpr float inv = 1.f / 16384.f;  // 2^-H_DUAL_LOG2
+  bool bad = false;
+  for (int c = lane; c < D; c += 32) {
+    const float y = ksplit == 2 ? ib[c] + ib[c + per_g] : ib[c];
+    const float o = fmaf(lab, __bfloat162float(fr[c]), y * inv) * s;
+    bad |= !isfinite(o);
+    out[c] = o;
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&status->flags, FLAG_GRAD_NONFINITE);
+  __syncwarp();
+  l2norm_backward_row(tw.raw[g] + int64_t(r) * tw.ld_raw[g], out, D, tw.dx[g] + int64_t(r) * tw.ld_dx, norm_flags,
+                      lane);
+}
+// ... and the rows the dual fixup recomputed: their dx again, from the fixed d
+__global__ void fixup_l2norm_kernel(const int* list, const Status* status, int cap, int b, int D,
+                                    const float* d_image, const float* d_text, int64_t ld_out, TowerRows tw,
+                                    int* norm_flags) {
+  const int n = min(status->fix_count, cap), lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n; e += nw) {
+    const int tag = list[e];
+    const int g = tag / b, r = tag % b;
+    const float* dr = (g == 0 ? d_image : d_text) + int64_t(r) * ld_out;
+    l2norm_backward_row(tw.raw[g] + int64_t(r) * tw.ld_raw[g], dr, D, tw.dx[g] + int64_t(r) * tw.ld_dx, norm_flags,
+                        lane);
+  }
 }
 
 // Fixed-order f64 sum of n floats: LOSS_BLOCKS contiguous slices, then a tree (as the loss).
@@ -3567,6 +3601,37 @@ int disco_b200_dual_fixup(void* ws, int64_t B, int64_t D, int world, int rank, f
       region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b, region<int>(ws, g, DISCO_R_FIX), region<Status>(ws, g, DISCO_R_STATUS),
       int(2 * g.ksplit * g.b), int(g.B), int(g.b), int(g.Dp), int(D), rank, t * LOG2E,
       float(0.5 * double(t) / double(g.B)), flip && world > 1, d_image, d_text, ld_out);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+int disco_b200_finish_dual_l2norm(void* ws, int64_t B, int64_t D, int world, int rank, float t, int flip,
+                                  const float* raw_I, int64_t ld_raw_I, const float* raw_T, int64_t ld_raw_T,
+                                  float* d_image, float* d_text, int64_t ld_out, float* dx_image, float* dx_text,
+                                  int64_t ld_dx, int* norm_flags, void* stream) {
+  Geometry g;
+  int rc = dual_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (ld_out < D || ld_dx < D || ld_raw_I < D || ld_raw_T < D) return fail(DISCO_SHAPE_ERROR, "row stride smaller than D");
+  cudaStream_t st = st_of(stream);
+  TowerRows tw;
+  tw.raw[0] = raw_I;
+  tw.raw[1] = raw_T;
+  tw.ld_raw[0] = ld_raw_I;
+  tw.ld_raw[1] = ld_raw_T;
+  tw.dx[0] = dx_image;
+  tw.dx[1] = dx_text;
+  tw.ld_dx = ld_dx;
+  const float s = float(0.5 * double(t) / double(g.B));
+  combine_dual_l2norm_kernel<<<int((2 * g.b * 32 + 255) / 256), 256, 0, st>>>(
+      region<float>(ws, g, DISCO_R_INTRA), g.ksplit, region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b,
+      region<__nv_bfloat16>(ws, g, DISCO_R_PACK), int(g.b), int(g.Dp), int(D), s, d_image, d_text, ld_out, tw,
+      region<Status>(ws, g, DISCO_R_STATUS), norm_flags);
+  count_launch();
+  if ((rc = disco_b200_dual_fixup(ws, B, D, world, rank, t, flip, d_image, d_text, ld_out, stream))) return rc;
+  fixup_l2norm_kernel<<<sm_count(), 256, 0, st>>>(region<int>(ws, g, DISCO_R_FIX), region<Status>(ws, g, DISCO_R_STATUS),
+                                                 int(2 * g.ksplit * g.b), int(g.b), int(D), d_image, d_text, ld_out, tw,
+                                                 norm_flags);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;

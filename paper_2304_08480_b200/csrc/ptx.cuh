@@ -229,6 +229,14 @@ __device__ __forceinline__ void st_swizzled_row64(uint8_t* tile, int r, const ui
     sts128(row + ((q ^ ((r >> 1) & 3)) << 4), make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
 }
 
+// One 32-byte (full sector) global store from registers, L1 no-allocate, with an L2 policy
+// (sm_100: STG.E.NA.ENL2.256).
+__device__ __forceinline__ void stg256(void* g, const uint32_t* w, uint64_t policy) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(g),
+               "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "l"(policy)
+               : "memory");
+}
+
 // Coalesced write-out of a 32-row x 128-byte swizzled staging tile with plain
 // LSU stores: each warp instruction stores 4 complete 128-byte rows.
 // dst(row) returns the global address of row `row` (nullptr = skip the row).

@@ -579,7 +579,7 @@ def host_pipelined(world: int, B: int, D: int, rank: int = 0) -> bool:
 
 
 def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_sign: bool = False,
-                     host_out=None):
+                     host_out=None, l2norm=None):
     """Launch one rank's DisCo fwd+bwd without any host synchronisation.
 
     Inputs are CUDA tensors (b x D), or, on a single rank with a wavefront-capable
@@ -592,6 +592,12 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
     backward then runs in output row blocks and each block's gradients are
     copied to the host on ``plan.copy_stream`` while the next block computes
     (wait on that stream, or call ``finish_status``, before reading them).
+
+    ``l2norm`` = (raw_I, raw_T, dx_I, dx_T, norm_flags), device fp32 (the two-tower caller,
+    towers.py:244-280): the features are l2_normalize_rows(raw); the combine then also writes
+    dx = l2_normalize_rows_backward(raw, d) into dx_I / dx_T (fused in its epilogue on the dual
+    path, the separate kernel otherwise; bitwise equal either way) and ORs bit0 (non-finite dx)
+    / bit1 (norm < 1e-12) into the int32 ``norm_flags``.
     """
     N, n = endpoint.world_size, endpoint.rank
     _check_step_inputs(local_I, local_T)
@@ -650,16 +656,22 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
     d_image = torch.empty((b, D), dtype=torch.float32, device=device)
     d_text = torch.empty((b, D), dtype=torch.float32, device=device)
     flip = int(bool(flip_cross_rank_sign))
+    fused = l2norm is not None and host_out is None and bool(_lib.path_info(B, D, N, n) & _lib.PATH_DUAL)
     if _lib.path_info(B, D, N, n) & _lib.PATH_DUAL:
-        _dual_backward(endpoint, plan, t, flip, d_image, d_text, host_out)
+        _dual_backward(endpoint, plan, t, flip, d_image, d_text, host_out, l2norm if fused else None)
     else:
         _exchange_backward(endpoint, plan, t, flip, d_image, d_text, host_out, pw,
                            parity if pw is not None else 0, epoch if pw is not None else 0)
+    if l2norm is not None and not fused:
+        raw_I, raw_T, dx_I, dx_T, nf = l2norm
+        for raw, d, dx in ((raw_I, d_image, dx_I), (raw_T, d_text, dx_T)):
+            _lib.call("disco_b200_l2norm_rows_backward", raw.data_ptr(), raw.stride(0), d.data_ptr(), d.stride(0),
+                      b, D, dx.data_ptr(), dx.stride(0), nf.data_ptr(), st)
     _leave(plan, cur_stream)
     return d_image, d_text, plan
 
 
-def _dual_backward(endpoint, plan: Plan, t: float, flip: int, d_image, d_text, host_out) -> None:
+def _dual_backward(endpoint, plan: Plan, t: float, flip: int, d_image, d_text, host_out, l2norm=None) -> None:
     """The dual backward (disco_b200_path_info PATH_DUAL): all_gather the 4 b row statistics, then
     one GEMM per gradient over the rank's own E block (H = G_d + G_d'^T), the combine with the
     fp32 label term, the exact recompute of any flagged rows, and the loss from the gathered ce.
@@ -683,10 +695,17 @@ def _dual_backward(endpoint, plan: Plan, t: float, flip: int, d_image, d_text, h
         d_image.record_stream(cs)
         d_text.record_stream(cs)
         plan.pending_host = (d_image, d_text, h_image, h_text)
+    elif l2norm is not None:  # two-tower step: the normalisation backward fused into the combine
+        raw_I, raw_T, dx_I, dx_T, nf = l2norm
+        _lib.call("disco_b200_backward_dual", *plan.args, 0, b, st)
+        _lib.call("disco_b200_finish_dual_l2norm", *plan.args, t, flip, raw_I.data_ptr(), raw_I.stride(0),
+                  raw_T.data_ptr(), raw_T.stride(0), d_image.data_ptr(), d_text.data_ptr(), D, dx_I.data_ptr(),
+                  dx_T.data_ptr(), dx_I.stride(0), nf.data_ptr(), st)
     else:
         _lib.call("disco_b200_backward_dual", *plan.args, 0, b, st)
         _lib.call("disco_b200_combine_dual", *plan.args, t, 0, b, d_image.data_ptr(), d_text.data_ptr(), D, st)
-    _lib.call("disco_b200_dual_fixup", *plan.args, t, flip, d_image.data_ptr(), d_text.data_ptr(), D, st)
+    if l2norm is None or host_out is not None:
+        _lib.call("disco_b200_dual_fixup", *plan.args, t, flip, d_image.data_ptr(), d_text.data_ptr(), D, st)
     _lib.call("disco_b200_loss", *plan.args, 2, st)
 
 

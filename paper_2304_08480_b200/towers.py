@@ -30,7 +30,7 @@ import torch
 from . import _lib
 from .errors import DegenerateInputError, DomainError, LayoutError, ShapeError, TrainingDivergenceError
 from .fabric import ReduceOp, SingleEndpoint, run_ranks
-from .shard import ShardLayout, disco_step
+from .shard import ShardLayout, disco_step, disco_step_async, finish_status
 
 MODES = ("naive", "disco")
 DEFAULT_TEMPERATURE = 20.0
@@ -223,9 +223,14 @@ def _tower_step(endpoint, W_i, W_t, x_i, x_t, t):
     raw_t = x_t @ W_t
     I, _ = l2_normalize_rows(raw_i, flags)
     T, _ = l2_normalize_rows(raw_t, flags)
-    d_image, d_text, loss = disco_step(endpoint, I, T, t)
-    dW_i = x_i.t() @ l2_normalize_rows_backward(raw_i, d_image, flags)
-    dW_t = x_t.t() @ l2_normalize_rows_backward(raw_t, d_text, flags)
+    # the loss step with l2_normalize_rows_backward fused into its combine epilogue (dual path;
+    # SURVEY 8(f) row 2): dx_* = d(loss)/d(raw_*) straight from the loss kernels
+    raw_i, raw_t = raw_i.contiguous(), raw_t.contiguous()
+    dx_i, dx_t = torch.empty_like(raw_i), torch.empty_like(raw_t)
+    _, _, plan = disco_step_async(endpoint, I, T, t, l2norm=(raw_i, raw_t, dx_i, dx_t, flags))
+    loss = finish_status(plan)
+    dW_i = x_i.t() @ dx_i
+    dW_t = x_t.t() @ dx_t
     return loss, dW_i, dW_t, flags
 
 

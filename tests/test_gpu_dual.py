@@ -146,3 +146,52 @@ def test_dual_matches_exchange_backward_across_n(monkeypatch):
     monkeypatch.setenv("DISCO_BACKWARD", "exchange")
     ei, et, el = run_sim(I, T, 2, t)
     assert O.max_rel_error(base[0], ei) < TOL and O.max_rel_error(base[1], et) < TOL and el[0] == base[2]
+
+
+def _raw_pair(B, D, seed, adversarial=False):
+    """Raw (unnormalised) tower outputs whose row-normalised versions are the loss features."""
+    rng = np.random.default_rng(seed)
+    if adversarial:
+        I, T = _adversarial(B, D, 16, seed)
+        scale = rng.uniform(0.5, 3.0, (B, 1))
+        return I * scale, T * scale[::-1]
+    return rng.standard_normal((B, D)) * 2.0, rng.standard_normal((B, D)) * 0.5
+
+
+@pytest.mark.parametrize("N,adversarial", [(1, False), (2, False), (1, True), (2, True)])
+def test_fused_tower_epilogue_matches_unfused_kernels(N, adversarial):
+    """the combine with l2_normalize_rows_backward fused into it (one warp per
+    row, disco_b200_finish_dual_l2norm) gives the same bits as disco_step followed by the separate
+    normalisation-backward kernel -- also for rows the dual fixup recomputes."""
+    from paper_2304_08480_b200 import towers
+    B, D, t = 2048, 64, 100.0
+    Ir, Tr = _raw_pair(B, D, 5, adversarial)
+    raw_i, raw_t = dev(Ir), dev(Tr)
+    I, _ = towers.l2_normalize_rows(raw_i)
+    T, _ = towers.l2_normalize_rows(raw_t)
+    b = B // N
+
+    def fused(ep):
+        rows = slice(ep.rank * b, (ep.rank + 1) * b)
+        ri, rt = raw_i[rows].contiguous(), raw_t[rows].contiguous()
+        dx_i, dx_t = torch.empty_like(ri), torch.empty_like(rt)
+        nf = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _, _, plan = P.disco_step_async(ep, I[rows], T[rows], t, l2norm=(ri, rt, dx_i, dx_t, nf))
+        loss = P.finish_status(plan)
+        return dx_i, dx_t, loss, int(nf.item()), plan.fixed_rows
+
+    def unfused(ep):
+        rows = slice(ep.rank * b, (ep.rank + 1) * b)
+        di, dt, loss = P.disco_step(ep, I[rows], T[rows], t)
+        return (towers.l2_normalize_rows_backward(raw_i[rows].contiguous(), di),
+                towers.l2_normalize_rows_backward(raw_t[rows].contiguous(), dt), loss)
+
+    fr = P.run_ranks(N, fused)
+    ur = P.run_ranks(N, unfused)
+    if adversarial:
+        assert sum(r[4] for r in fr) > 0, "expected rows queued for the fixup"
+    for a, u in zip(fr, ur):
+        assert a[3] == 0
+        assert a[2] == u[2]
+        assert a[0].cpu().numpy().tobytes() == u[0].cpu().numpy().tobytes()
+        assert a[1].cpu().numpy().tobytes() == u[1].cpu().numpy().tobytes()
