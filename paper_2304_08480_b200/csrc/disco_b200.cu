@@ -82,8 +82,12 @@ static_assert(Ring<1>::STAGES == 6 && Ring<2>::STAGES == 4 && Ring<2, 2>::STAGES
 constexpr int NUM_THREADS = 320;  // warp0 TMA, warp1 MMA, warps2-9 epilogue
 constexpr int NUM_EPI_WARPS = 8;
 // E-operand GEMMs add 4 transform warps (10-13) that rescale each A stage in smem (E -> G).
-constexpr int NUM_XF_WARPS = 4;
-constexpr int NUM_THREADS_XF = NUM_THREADS + 32 * NUM_XF_WARPS;
+constexpr int NUM_XF_WARPS = 4;   // transform warps per group: one 128-row A stage
+#ifndef DISCO_XF_GROUPS
+#define DISCO_XF_GROUPS 1
+#endif
+constexpr int XF_GROUPS = DISCO_XF_GROUPS;  // transform groups; group g takes the ring stages s with s % XF_GROUPS == g
+constexpr int NUM_THREADS_XF = NUM_THREADS + 32 * NUM_XF_WARPS * XF_GROUPS;
 constexpr int GROUP_COLS = 64;    // E offset granularity: one exp2 offset per (row, 64-column group)
 // The forward stores E = exp2(y - m_g + E_HEADROOM) (m_g: the row's group max without the label),
 // values in (0, 2^15].  E-operand GEMMs therefore see scaled operands: the two-GEMM (exchange)
@@ -112,8 +116,12 @@ constexpr int STAGING_BYTES = NUM_EPI_WARPS * STAGING_BUFS * STAGING_TILE;
 constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(TILE_RING_BYTES) + STAGING_BYTES + 512;
 // Logits kernel with a resident A block (Dp <= 512): A = 8 slices x 16 KiB, then a 4-stage B ring.
 constexpr int ARES_SLICES = 8;
-constexpr int ARES_B_STAGES = 4;
-static_assert(ARES_SLICES * A_STAGE_BYTES + ARES_B_STAGES * B_STAGE_BYTES == TILE_RING_BYTES, "A-resident layout");
+#ifndef DISCO_ARES_B_STAGES
+#define DISCO_ARES_B_STAGES 4
+#endif
+constexpr int ARES_B_STAGES = DISCO_ARES_B_STAGES;
+static_assert(ARES_SLICES * A_STAGE_BYTES + ARES_B_STAGES * B_STAGE_BYTES <= TILE_RING_BYTES + STAGING_BYTES / 2,
+              "A-resident layout");
 static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory limit");
 // Dual backward (E-operand GEMMs, xform = 2): per ring stage, the q factors of the stage's 64 K
 // columns (256 B) land by bulk copy beside the tiles, after the control block.
@@ -283,6 +291,16 @@ __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int mn_major, in
                   : ptx::smem_desc_sw128(base + kk * 32, 16, 1024);     // 16 K-elements = 32 B per MMA
 }
 
+#ifndef DISCO_WAITPROBE
+#define DISCO_WAITPROBE 0
+#endif
+#if DISCO_WAITPROBE
+// profiling build only: logits kernel barrier-wait cycles {MMA full, MMA tempty, MMA total, MMA
+// threads, epilogue tfull by warp quadrant x4}; backward GEMM {8: MMA operand wait (full/xfull),
+// 9: MMA tempty wait, 10: MMA total, 11: MMA threads, 12: transform TMA wait, 13: transform total,
+// 14: transform threads}; read by disco_b200_waitprobe
+__device__ unsigned long long g_waitprobe[16];
+#endif
 template <int NSTAGES = STAGES>
 struct Pipe {
   uint32_t stage = 0, phase = 0;
@@ -310,7 +328,13 @@ __device__ __forceinline__ void mma_blocks(SmemCtl* ctl, uint8_t* tiles, Pipe<RS
                                            bool wait, bool release) {
   const uint64_t a_step = a_mn ? 128 : 2, b_step = b_mn ? 128 : 2;
   for (int kb = 0; kb < nk; ++kb) {
+#if DISCO_WAITPROBE
+    const long long w0 = clock64();
+#endif
     if (wait) ptx::mbar_wait(XF ? &ctl->xfull[pipe.stage] : &ctl->full[pipe.stage], pipe.phase);
+#if DISCO_WAITPROBE
+    if (wait && (threadIdx.x & 31) == 0) atomicAdd(&g_waitprobe[8], (unsigned long long)(clock64() - w0));
+#endif
     ptx::tc_fence_after();
     const uint32_t a_base = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES);
     const uint32_t b_base = a_base + NA * A_STAGE_BYTES;
@@ -502,14 +526,9 @@ constexpr int FWDE_STAGES = FWDE_EPI == 16 ? 5 : FWD_STAGES;
 static_assert(FWDE_EPI == 8 || FWDE_EPI == 16, "FWDE epilogue warps");
 static_assert(FWDE_STAGES * STAGE_BYTES + FWDE_EPI * FWD_EBUFS * (STAGING_TILE / 2) <= TILE_RING_BYTES + STAGING_BYTES,
               "FWDE smem layout");
-#ifndef DISCO_WAITPROBE
-#define DISCO_WAITPROBE 0
-#endif
-#if DISCO_WAITPROBE
-// profiling build only: logits kernel barrier-wait cycles {MMA full, MMA tempty, MMA total, MMA
-// threads, epilogue tfull by warp quadrant x4}, read by disco_b200_waitprobe
-__device__ unsigned long long g_waitprobe[8];
-#endif
+static_assert(!XP || ARES_SLICES * A_STAGE_BYTES + ARES_B_STAGES * B_STAGE_BYTES +
+                             NUM_EPI_WARPS * FWD_EBUFS * (STAGING_TILE / 2) <= TILE_RING_BYTES + STAGING_BYTES,
+              "A-resident smem layout");
 template <int KIND, bool ARES>
 __host__ __device__ constexpr int logits_epi() { return (KIND == KIND_FWDE && !ARES) ? FWDE_EPI : NUM_EPI_WARPS; }
 template <int KIND, bool ARES>
@@ -528,7 +547,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
   constexpr int NDIR = 2;                                    // directions walked by the units
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = smem_base(smem_raw);
-  uint8_t* staging = tiles + (ARES ? TILE_RING_BYTES : LRS * STAGE_BYTES);
+  uint8_t* staging = tiles + (ARES ? ARES_SLICES * A_STAGE_BYTES + ARES_B_STAGES * B_STAGE_BYTES : LRS * STAGE_BYTES);
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tiles + TILE_RING_BYTES + STAGING_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int crank = int(ptx::cluster_ctarank());
@@ -1129,6 +1148,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     if (leader) {  // ---------------- MMA issuer (leader CTA, whole warp; one elected lane issues)
       Pipe<RS> pipe;
       uint32_t it = 0;
+#if DISCO_WAITPROBE
+      const long long wt0 = clock64();
+#endif
       for (int uk = 0; uk < my_units; ++uk) {
         const int u = unit_at(uk);
         int pi, mt, nt, kc;
@@ -1145,11 +1167,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             // accumulator 1 is free, the same stages into accumulator 1, releasing them, then the rest
             // of K into both.  Each accumulator still sums its k-blocks in the same order.
             const int pre = nk < RS ? nk : RS;
+#if DISCO_WAITPROBE
+            const long long w1 = clock64();
+#endif
             ptx::mbar_wait(&ctl->tempty[0], ph);
+#if DISCO_WAITPROBE
+            if (lane == 0) atomicAdd(&g_waitprobe[9], (unsigned long long)(clock64() - w1));
+#endif
             Pipe<RS> first = pipe;
             mma_blocks<NB, XF, RS, NA>(ctl, tiles, first, pre, 0, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major,
                                        0, 1, true, false);
+#if DISCO_WAITPROBE
+            const long long w2 = clock64();
+#endif
             ptx::mbar_wait(&ctl->tempty[1], ph);
+#if DISCO_WAITPROBE
+            if (lane == 0) atomicAdd(&g_waitprobe[9], (unsigned long long)(clock64() - w2));
+#endif
             mma_blocks<NB, XF, RS, NA>(ctl, tiles, pipe, pre, 0, ctl->tmem_base, idesc, q.a_mn_major, q.b_mn_major,
                                        1, 2, false, true);
             mma_blocks<NB, XF, RS, NA>(ctl, tiles, pipe, nk - pre, pre, ctl->tmem_base, idesc, q.a_mn_major,
@@ -1175,6 +1209,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
           }
         }
       }
+#if DISCO_WAITPROBE
+      if (lane == 0) {
+        atomicAdd(&g_waitprobe[10], (unsigned long long)(clock64() - wt0));
+        atomicAdd(&g_waitprobe[11], 1ull);
+      }
+#endif
     }
   } else if (XF && warp >= 2 + NUM_EPI_WARPS) {  // ---------------- transform warps 10..13
     // Thread xt owns one 128-byte row of this CTA's A stage:
@@ -1182,9 +1222,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
     //   MN-major A (cross, G^T): atom xt / 64, K-row xt % 64 = G row k + xt % 64,
     //   G columns [m0 + 64 * (xt / 64), +64).
     // The scale of the next stage is loaded one stage ahead (it only depends on K within a unit).
-    const int xt = threadIdx.x - 32 * (2 + NUM_EPI_WARPS);
+    const int xgroup = (warp - (2 + NUM_EPI_WARPS)) / NUM_XF_WARPS;
+    const int xt = threadIdx.x - 32 * (2 + NUM_EPI_WARPS) - 32 * NUM_XF_WARPS * xgroup;
     const uint32_t xbar = 0;  // transform completion is counted on the leader's xfull barriers
     Pipe<RS> pipe;
+#if DISCO_WAITPROBE
+    const long long xt0 = clock64();
+#endif
     for (int uk = 0; uk < my_units; ++uk) {
         const int u = unit_at(uk);
       int pi, mt, nt, kc;
@@ -1230,7 +1274,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             const float2 gm = gq[i];
             mq[i] = ld_mg(kb + XPF);
             gq[i] = ld_gm(kb + XPF);
+            if (XF_GROUPS > 1 && int(pipe.stage % XF_GROUPS) != xgroup) {  // the other group's stage
+              pipe.advance();
+              continue;
+            }
+#if DISCO_WAITPROBE
+            const long long w3 = clock64();
+#endif
             ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
+#if DISCO_WAITPROBE
+            if ((threadIdx.x & 31) == 0) atomicAdd(&g_waitprobe[12], (unsigned long long)(clock64() - w3));
+#endif
             if (act) {
               unsafe |= mg - gm.y > DUAL_SAFE_SPAN;
               const float a = ptx::ex2(mg + (H_DUAL_LOG2 - E_HEADROOM) - lse_r);
@@ -1308,6 +1362,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             const int k = k0 + kb * BK;
             const __half sc = sq[r];
             sq[r] = ld_scale(kb + XPF);
+            if (XF_GROUPS > 1 && int(pipe.stage % XF_GROUPS) != xgroup) {  // the other group's stage
+              pipe.advance();
+              continue;
+            }
             ptx::mbar_wait(&ctl->full[pipe.stage], pipe.phase);
             if (active && !(XP && (q.ablate & 1024))) {
               const uint32_t rowp = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES + rowoff);
@@ -1334,6 +1392,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
         }
       }
     }
+#if DISCO_WAITPROBE
+    if (lane == 0) {
+      atomicAdd(&g_waitprobe[13], (unsigned long long)(clock64() - xt0));
+      atomicAdd(&g_waitprobe[14], 1ull);
+    }
+#endif
   } else if (warp >= 2) {  // ---------------------------- epilogue warps 2..9
     const int ew = warp - 2;
     const int quad = warp & 3;
@@ -2355,6 +2419,8 @@ struct Geometry {
   int64_t len[DISCO_R_COUNT];
   int64_t total;
 };
+// dual fixup queue: each transform group queues its unsafe rows per K part (duplicates allowed)
+inline int64_t fix_capacity(const Geometry& g) { return int64_t(XF_GROUPS) * 2 * g.ksplit * g.b; }
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
@@ -2446,7 +2512,7 @@ int make_geometry(int64_t B, int64_t D, int world, int rank, Geometry* g) {
   len[DISCO_R_XCHG] = 4 * b * 4;
   len[DISCO_R_XALL] = N > 1 ? N * 4 * b * 4 : 0;
   len[DISCO_R_QCOL] = g->estore ? 2 * B * 4 + 2 * int64_t(g->groups) * 8 : 0;
-  len[DISCO_R_FIX] = g->estore ? 2 * int64_t(g->ksplit) * b * 4 : 0;
+  len[DISCO_R_FIX] = g->estore ? fix_capacity(*g) * 4 : 0;
   int64_t off = 0;
   for (int r = 0; r < DISCO_R_COUNT; ++r) {
     g->off[r] = off;
@@ -3020,7 +3086,7 @@ int build_dual(GemmParams& p, void* ws, const Geometry& g, int mt0 = 0, int mt1 
     q.fix_list = region<int>(ws, g, DISCO_R_FIX);
     q.fix_count = &status->fix_count;
     q.fix_tag = int(int64_t(d) * g.b);
-    q.fix_cap = int(2 * g.ksplit * g.b);
+    q.fix_cap = int(fix_capacity(g));
   }
   p.nprob = 2;
   p.split = 0;
@@ -3119,7 +3185,7 @@ int disco_b200_set_experiment_flags(int flags) { return g_debug_bits.exchange(fl
 int disco_b200_waitprobe(unsigned long long* out, int reset) {
   CUDA_TRY(cudaMemcpyFromSymbol(out, disco::g_waitprobe, sizeof(disco::g_waitprobe)));
   if (reset) {
-    static const unsigned long long z[8] = {};
+    static const unsigned long long z[16] = {};
     CUDA_TRY(cudaMemcpyToSymbol(disco::g_waitprobe, z, sizeof(z)));
   }
   return DISCO_OK;
@@ -3599,7 +3665,7 @@ int disco_b200_dual_fixup(void* ws, int64_t B, int64_t D, int world, int rank, f
   dual_fixup_kernel<<<sm_count(), FIX_THREADS, 0, st_of(stream)>>>(
       region<__nv_bfloat16>(ws, g, DISCO_R_FEAT), region<float>(ws, g, DISCO_R_XALL),
       region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b, region<int>(ws, g, DISCO_R_FIX), region<Status>(ws, g, DISCO_R_STATUS),
-      int(2 * g.ksplit * g.b), int(g.B), int(g.b), int(g.Dp), int(D), rank, t * LOG2E,
+      int(fix_capacity(g)), int(g.B), int(g.b), int(g.Dp), int(D), rank, t * LOG2E,
       float(0.5 * double(t) / double(g.B)), flip && world > 1, d_image, d_text, ld_out);
   count_launch();
   CUDA_TRY(cudaGetLastError());
@@ -3630,7 +3696,7 @@ int disco_b200_finish_dual_l2norm(void* ws, int64_t B, int64_t D, int world, int
   count_launch();
   if ((rc = disco_b200_dual_fixup(ws, B, D, world, rank, t, flip, d_image, d_text, ld_out, stream))) return rc;
   fixup_l2norm_kernel<<<sm_count(), 256, 0, st>>>(region<int>(ws, g, DISCO_R_FIX), region<Status>(ws, g, DISCO_R_STATUS),
-                                                 int(2 * g.ksplit * g.b), int(g.b), int(D), d_image, d_text, ld_out, tw,
+                                                 int(fix_capacity(g)), int(g.b), int(D), d_image, d_text, ld_out, tw,
                                                  norm_flags);
   count_launch();
   CUDA_TRY(cudaGetLastError());

@@ -31,7 +31,7 @@ for path in sys.argv[1:]:
         if fn is not None:
             fn.argtypes = argtypes
             fn.restype = _lib._RESTYPES.get(name, ctypes.c_int)
-    out = (ctypes.c_ulonglong * 8)()
+    out = (ctypes.c_ulonglong * 16)()
     for rep in range(25):
         if rep == 5:
             torch.cuda.synchronize()
@@ -39,9 +39,14 @@ for path in sys.argv[1:]:
         flush.zero_()
         lib.disco_b200_pack(*plan.args, I.data_ptr(), T.data_ptr(), D, D, _lib.BF16, 1, sp)
         lib.disco_b200_forward(*plan.args, ctypes.c_float(t), sp)
+        lib.disco_b200_dual_prep(*plan.args, 0, sp)
+        lib.disco_b200_backward_dual(*plan.args, 0, B, sp)
     torch.cuda.synchronize()
     lib.disco_b200_waitprobe(out, 0)
     v = list(out)
     tot = v[2] or 1
     print(f"{os.path.basename(path)}: MMA threads {v[3]}  full-wait {v[0] / tot:.3f}  tempty-wait {v[1] / tot:.3f}  "
           f"epilogue tfull-wait {[round(x / (tot * 4), 3) for x in v[4:8]]} (per quadrant, / MMA time)")
+    gt, xt = v[10] or 1, v[13] or 1
+    print(f"   backward GEMM: MMA threads {v[11]}  operand (xfull) wait {v[8] / gt:.3f}  tempty wait {v[9] / gt:.3f};  "
+          f"transform warps {v[14]}  TMA (full) wait {v[12] / xt:.3f}")
