@@ -83,11 +83,20 @@ constexpr int NUM_THREADS = 320;  // warp0 TMA, warp1 MMA, warps2-9 epilogue
 constexpr int NUM_EPI_WARPS = 8;
 // E-operand GEMMs add 4 transform warps (10-13) that rescale each A stage in smem (E -> G).
 constexpr int NUM_XF_WARPS = 4;   // transform warps per group: one 128-row A stage
+// Transform groups: group g takes the ring stages s with s % groups == g (build switches; one group
+// each by default: a second group measured +1.7% cycles on the wide dual backward, -6% on the
+// exchange backward and -2% on the narrow units of D = 768, where it costs 20 bytes of spills).
 #ifndef DISCO_XF_GROUPS
 #define DISCO_XF_GROUPS 1
 #endif
-constexpr int XF_GROUPS = DISCO_XF_GROUPS;  // transform groups; group g takes the ring stages s with s % XF_GROUPS == g
-constexpr int NUM_THREADS_XF = NUM_THREADS + 32 * NUM_XF_WARPS * XF_GROUPS;
+#ifndef DISCO_XF_GROUPS_NARROW
+#define DISCO_XF_GROUPS_NARROW 1
+#endif
+template <int NB>
+__host__ __device__ constexpr int xf_groups() { return NB == 1 ? DISCO_XF_GROUPS_NARROW : DISCO_XF_GROUPS; }
+constexpr int XF_GROUPS_MAX = DISCO_XF_GROUPS > DISCO_XF_GROUPS_NARROW ? DISCO_XF_GROUPS : DISCO_XF_GROUPS_NARROW;
+template <int NB, bool XF>
+__host__ __device__ constexpr int gemm_threads() { return XF ? NUM_THREADS + 32 * NUM_XF_WARPS * xf_groups<NB>() : NUM_THREADS; }
 constexpr int GROUP_COLS = 64;    // E offset granularity: one exp2 offset per (row, 64-column group)
 // The forward stores E = exp2(y - m_g + E_HEADROOM) (m_g: the row's group max without the label),
 // values in (0, 2^15].  E-operand GEMMs therefore see scaled operands: the two-GEMM (exchange)
@@ -1053,7 +1062,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
 //   level of the fixed reduction tree).
 // =====================================================================
 template <int NB, bool XF>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF : NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads<NB, XF>(), 1)
     gemm_kernel(const __grid_constant__ GemmParams p) {
   constexpr int NA = 1;  // A tiles per stage
   constexpr int RS = Ring<NB, NA>::STAGES;
@@ -1274,7 +1283,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             const float2 gm = gq[i];
             mq[i] = ld_mg(kb + XPF);
             gq[i] = ld_gm(kb + XPF);
-            if (XF_GROUPS > 1 && int(pipe.stage % XF_GROUPS) != xgroup) {  // the other group's stage
+            if (xf_groups<NB>() > 1 && int(pipe.stage % xf_groups<NB>()) != xgroup) {  // the other group's stage
               pipe.advance();
               continue;
             }
@@ -1362,7 +1371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XF ? NUM_THREADS_XF 
             const int k = k0 + kb * BK;
             const __half sc = sq[r];
             sq[r] = ld_scale(kb + XPF);
-            if (XF_GROUPS > 1 && int(pipe.stage % XF_GROUPS) != xgroup) {  // the other group's stage
+            if (xf_groups<NB>() > 1 && int(pipe.stage % xf_groups<NB>()) != xgroup) {  // the other group's stage
               pipe.advance();
               continue;
             }
@@ -2420,7 +2429,7 @@ struct Geometry {
   int64_t total;
 };
 // dual fixup queue: each transform group queues its unsafe rows per K part (duplicates allowed)
-inline int64_t fix_capacity(const Geometry& g) { return int64_t(XF_GROUPS) * 2 * g.ksplit * g.b; }
+inline int64_t fix_capacity(const Geometry& g) { return int64_t(XF_GROUPS_MAX) * 2 * g.ksplit * g.b; }
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
@@ -2831,7 +2840,7 @@ int launch_gemm_t(GemmParams& p, cudaStream_t st) {
   int rc;
   const size_t smem = XF ? SMEM_BYTES_XF : SMEM_BYTES;
   if ((rc = prepare_kernel(gemm_kernel<NB, XF>, smem))) return rc;
-  gemm_kernel<NB, XF><<<grid_for(p.units[p.nprob]), XF ? NUM_THREADS_XF : NUM_THREADS, smem, st>>>(p);
+  gemm_kernel<NB, XF><<<grid_for(p.units[p.nprob]), gemm_threads<NB, XF>(), smem, st>>>(p);
   return DISCO_OK;
 }
 
