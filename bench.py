@@ -64,7 +64,9 @@ def parse():
     ap.add_argument("--no-exchange-leg", "--no-fused", dest="no_exchange_leg", action="store_true",
                     help="skip the exchange-backward comparison leg (N = 1)")
     ap.add_argument("--no-ref-check", action="store_true",
-                    help="reference arm: skip the one-step unmodified-reference cross-check")
+                    help="reference arm: skip the one-step cross-check of the other CPU implementation")
+    ap.add_argument("--cpu-port", action="store_true",
+                    help="time the oracle port even when the unmodified reference (baseline/_ref) is installed")
     return ap.parse_args()
 
 
@@ -98,29 +100,46 @@ def cpu_port_step(I, T, world, t=TEMP, workers=None):
     return sec
 
 
-def unmodified_reference_step(I, T, world, t=TEMP):
-    """One step of the UNMODIFIED reference disco_step (shard.py:169-208) through its own
-    run_ranks (fabric.py:291, lockstep) with verification on, from baseline/_ref when that
-    install is present (python -m pip install --no-deps ... --target baseline/_ref).  A single
-    cross-check of the port's speed on the same host; None when absent."""
+def _reference_package():
+    """The UNMODIFIED reference package installed in baseline/_ref (python -m pip install --no-index
+    --no-build-isolation --no-deps --target baseline/_ref <copy of /root/reference/pkg>), or None."""
     ref = os.path.join(ROOT, "baseline", "_ref")
     if not os.path.isdir(os.path.join(ref, "disco")):
         return None
     sys.path.insert(0, ref)
     try:
-        import disco  # noqa: F401  (the reference package, unmodified)
-        from disco import disco_step, run_ranks
+        import disco  # the reference package, unmodified
+        from disco import disco_step, run_ranks  # noqa: F401
+    except Exception:
+        return None
     finally:
         sys.path.remove(ref)
+    return disco
+
+
+def unmodified_reference_step(I, T, world, t=TEMP):
+    """One step of the UNMODIFIED reference disco_step (shard.py:169-208) for all `world` ranks
+    through its own run_ranks (fabric.py:291, lockstep) with verification on, f32 features, all
+    host cores (numpy / OpenBLAS as shipped).  Returns seconds, or None without baseline/_ref."""
+    disco = _reference_package()
+    if disco is None:
+        return None
     b = I.shape[0] // world
 
     def fn(ep):
         rows = slice(ep.rank * b, (ep.rank + 1) * b)
-        return disco_step(ep, I[rows], T[rows], t)[2]
+        return disco.disco_step(ep, I[rows], T[rows], t)[2]
 
     t0 = time.perf_counter()
-    run_ranks(world, fn, mode="lockstep")
+    disco.run_ranks(world, fn, mode="lockstep")
     return time.perf_counter() - t0
+
+
+def reference_kind(args) -> str:
+    """'reference' (the unmodified package from baseline/_ref) when installed, else 'port'."""
+    if getattr(args, "cpu_port", False) or _reference_package() is None:
+        return "port"
+    return "reference"
 
 
 def cpu_cores():
@@ -131,35 +150,49 @@ def cpu_cores():
 
 
 def run_reference(args):
+    """The reference arm: the reference's own CPU implementation of the step on the host cores --
+    the unmodified package from baseline/_ref (kind "reference") when installed, else the
+    vectorised oracle port (kind "port") -- every one of the W + K steps the FULL workload (all
+    B rows, both directions); the other implementation is timed once beside it as a cross-check."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     B, D, N = args.batch, args.dim, args.gpus
     I, T = cpu_features(B, D)
     cores = cpu_cores()
+    kind = reference_kind(args)
+    step = unmodified_reference_step if kind == "reference" else cpu_port_step
     t_start = time.perf_counter()
     for _ in range(args.warmup):
-        cpu_port_step(I, T, N)
-    secs = [cpu_port_step(I, T, N) for _ in range(args.steps)]
+        step(I, T, N)
+    secs = [step(I, T, N) for _ in range(args.steps)]
     wall = time.perf_counter() - t_start
     sec = statistics.mean(secs)
     value = B / sec
-    unmod = None
+    cross = None
     if not args.no_ref_check:
-        us = unmodified_reference_step(I, T, N)
-        if us is not None:
-            unmod = {"value": B / us, "unit": UNIT, "ms_per_step": 1e3 * us, "steps": 1,
-                     "note": "unmodified reference disco_step via run_ranks(lockstep) from baseline/_ref, "
-                             "verification on, f32, one step (cross-check of the port's speed)"}
-    sample = (f"full step: all {N} rank(s) x {B // N} rows x {B} columns, D={D}, both directions "
-              f"(oracle.disco_step_blocked, f32, {cores} threads x 1-thread BLAS)")
+        if kind == "reference":
+            ps = cpu_port_step(I, T, N)
+            cross = {"kind": "port", "value": B / ps, "unit": UNIT, "ms_per_step": 1e3 * ps, "steps": 1,
+                     "note": "oracle.disco_step_blocked (f32, row blocks on all host threads, no verification pass)"}
+        else:
+            us = unmodified_reference_step(I, T, N)
+            if us is not None:
+                cross = {"kind": "reference", "value": B / us, "unit": UNIT, "ms_per_step": 1e3 * us, "steps": 1}
+    if kind == "reference":
+        sample = (f"full step: unmodified reference disco_step (shard.py:169-208) for all {N} rank(s) via "
+                  f"run_ranks(lockstep), verification on, {B // N} rows x {B} columns, D={D}, f32, "
+                  f"numpy/OpenBLAS on {cores} cores")
+    else:
+        sample = (f"full step: all {N} rank(s) x {B // N} rows x {B} columns, D={D}, both directions "
+                  f"(oracle.disco_step_blocked, f32, {cores} threads x 1-thread BLAS)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": workload_config(args, B, D, N),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
-                         "unmodified_reference": unmod},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                         "cross_check": cross},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
@@ -663,10 +696,16 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         I_c, T_c = cpu_features(B, D)
-        sec = cpu_port_step(I_c, T_c, world)
-        cpu = {"value": B / sec, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-               "sample": f"one full step: {b} rows x {B} columns, D={D}, both directions "
-                         f"(oracle.disco_step_blocked, f32, {cpu_cores()} threads; {sec:.1f} s)"}
+        kind = reference_kind(args)
+        if kind == "reference":
+            sec = unmodified_reference_step(I_c, T_c, world)
+            sample = (f"one full step: unmodified reference disco_step via run_ranks(lockstep), verification on, "
+                      f"{b} rows x {B} columns, D={D}, f32, {cpu_cores()} cores ({sec:.1f} s)")
+        else:
+            sec = cpu_port_step(I_c, T_c, world)
+            sample = (f"one full step: {b} rows x {B} columns, D={D}, both directions "
+                      f"(oracle.disco_step_blocked, f32, {cpu_cores()} threads; {sec:.1f} s)")
+        cpu = {"value": B / sec, "unit": UNIT, "cores": cpu_cores(), "kind": kind, "sample": sample}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
