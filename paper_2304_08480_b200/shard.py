@@ -656,6 +656,8 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
     d_image = torch.empty((b, D), dtype=torch.float32, device=device)
     d_text = torch.empty((b, D), dtype=torch.float32, device=device)
     flip = int(bool(flip_cross_rank_sign))
+    if l2norm is not None:
+        _check_l2norm_args(l2norm, b, D, device)
     fused = l2norm is not None and host_out is None and bool(_lib.path_info(B, D, N, n) & _lib.PATH_DUAL)
     if _lib.path_info(B, D, N, n) & _lib.PATH_DUAL:
         _dual_backward(endpoint, plan, t, flip, d_image, d_text, host_out, l2norm if fused else None)
@@ -669,6 +671,21 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
                       b, D, dx.data_ptr(), dx.stride(0), nf.data_ptr(), st)
     _leave(plan, cur_stream)
     return d_image, d_text, plan
+
+
+def _check_l2norm_args(l2norm, b: int, D: int, device) -> None:
+    """The fused normalisation backward writes through raw pointers: reject anything that is not
+    (b x D fp32 row-major CUDA tensors on the plan's device, an int32 flag word) before a launch."""
+    if len(l2norm) != 5:
+        raise TypeError("l2norm must be (raw_I, raw_T, dx_I, dx_T, norm_flags)")
+    *mats, nf = l2norm
+    for m in mats:
+        if not (isinstance(m, torch.Tensor) and m.is_cuda and m.device == device and m.dtype == torch.float32
+                and m.dim() == 2 and tuple(m.shape) == (b, D) and m.stride(1) == 1 and m.stride(0) >= D):
+            raise ShapeError(f"l2norm tensors must be ({b}, {D}) float32 row-major on {device}")
+    if not (isinstance(nf, torch.Tensor) and nf.is_cuda and nf.device == device and nf.dtype == torch.int32
+            and nf.numel() >= 1):
+        raise ShapeError("l2norm norm_flags must be an int32 CUDA tensor")
 
 
 def _dual_backward(endpoint, plan: Plan, t: float, flip: int, d_image, d_text, host_out, l2norm=None) -> None:
