@@ -195,3 +195,31 @@ def test_fused_tower_epilogue_matches_unfused_kernels(N, adversarial):
         assert a[2] == u[2]
         assert a[0].cpu().numpy().tobytes() == u[0].cpu().numpy().tobytes()
         assert a[1].cpu().numpy().tobytes() == u[1].cpu().numpy().tobytes()
+
+
+def test_fused_tower_epilogue_exchange_mode_and_validation(monkeypatch):
+    """With DISCO_BACKWARD=exchange the call runs the exchange backward and then the separate
+    normalisation kernel (equal to composing them by hand); malformed l2norm arguments raise
+    ShapeError before any launch."""
+    from paper_2304_08480_b200 import towers
+    B, D, t = 2048, 64, 10.0
+    Ir, Tr = _raw_pair(B, D, 11)
+    raw_i, raw_t = dev(Ir), dev(Tr)
+    I, _ = towers.l2_normalize_rows(raw_i)
+    T, _ = towers.l2_normalize_rows(raw_t)
+    monkeypatch.setenv("DISCO_BACKWARD", "exchange")
+    dx_i, dx_t = torch.empty_like(raw_i), torch.empty_like(raw_t)
+    nf = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _, _, plan = P.disco_step_async(P.SingleEndpoint(), I, T, t,
+                                    l2norm=(raw_i, raw_t, dx_i, dx_t, nf))
+    P.finish_status(plan)
+    di, dt, _ = P.disco_step(None, I, T, t)
+    assert torch.equal(dx_i, towers.l2_normalize_rows_backward(raw_i, di))
+    assert torch.equal(dx_t, towers.l2_normalize_rows_backward(raw_t, dt))
+    monkeypatch.delenv("DISCO_BACKWARD")
+    with pytest.raises(P.ShapeError):
+        P.disco_step_async(P.SingleEndpoint(), I, T, t, l2norm=(raw_i[:, :32], raw_t, dx_i, dx_t, nf))
+    with pytest.raises(P.ShapeError):
+        P.disco_step_async(P.SingleEndpoint(), I, T, t, l2norm=(raw_i, raw_t, dx_i.double(), dx_t, nf))
+    with pytest.raises(P.ShapeError):
+        P.disco_step_async(P.SingleEndpoint(), I, T, t, l2norm=(raw_i, raw_t, dx_i, dx_t, nf.float()))
