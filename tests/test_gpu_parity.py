@@ -322,3 +322,32 @@ def test_dual_and_exchange_backwards_vs_oracle(B, D, monkeypatch):
     assert np.array_equal(hi, di) and np.array_equal(ht, dt) and hl == loss
     ri, rt, rl = P.disco_step(None, dev(I), dev(T), 100.0)
     assert np.array_equal(ri.cpu().numpy(), di) and np.array_equal(rt.cpu().numpy(), dt) and rl == loss
+
+
+def test_input_containers_and_dtypes_give_identical_bits():
+    """The reference takes numpy float64 / float32 matrices (shard.py:169); the drop-in also takes
+    torch tensors of any float dtype on the host or the device.  Features holding bf16 values are
+    represented exactly by every one of them, so every container / dtype must give the same bits
+    (numpy in -> numpy out in the input's float dtype, torch CUDA in -> CUDA out)."""
+    B, D, t = 2048, 256, 50.0
+    I, T = O.synthetic_features(B, D, 21)
+    ref_i, ref_t, ref_l = P.disco_step(None, dev(I), dev(T), t)
+    ref_i, ref_t = ref_i.cpu().numpy(), ref_t.cpu().numpy()
+    cases = [
+        (I.astype(np.float64), T.astype(np.float64)),
+        (I.astype(np.float32), T.astype(np.float32)),
+        (torch.from_numpy(I.astype(np.float32)), torch.from_numpy(T.astype(np.float32))),
+        (torch.from_numpy(I).cuda(), torch.from_numpy(T).cuda()),
+        (torch.from_numpy(I).cuda().bfloat16(), torch.from_numpy(T).cuda().bfloat16()),
+        (torch.from_numpy(I.astype(np.float32)).pin_memory().bfloat16(),
+         torch.from_numpy(T.astype(np.float32)).pin_memory().bfloat16()),
+    ]
+    for a, b in cases:
+        di, dt, loss = P.disco_step(None, a, b, t)
+        if isinstance(a, np.ndarray):
+            assert isinstance(di, np.ndarray) and di.dtype == a.dtype
+            di, dt = di.astype(np.float32), dt.astype(np.float32)
+        else:
+            di, dt = di.float().cpu().numpy(), dt.float().cpu().numpy()
+        assert loss == ref_l, (type(a), getattr(a, "dtype", None))
+        assert np.array_equal(di, ref_i) and np.array_equal(dt, ref_t), (type(a), getattr(a, "dtype", None))
