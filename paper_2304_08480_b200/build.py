@@ -12,7 +12,9 @@ import sys
 _HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_HERE)
 SOURCES = [os.path.join(_HERE, "csrc", "disco_b200.cu")]
-DEPS = SOURCES + [os.path.join(_HERE, "csrc", "ptx.cuh"), os.path.join(ROOT, "include", "disco_b200.h")]
+DEPS = SOURCES + [os.path.join(_HERE, "csrc", f) for f in
+                  ("ptx.cuh", "common.cuh", "logits.cuh", "gemm.cuh", "tails.cuh", "host.cuh")] + \
+    [os.path.join(ROOT, "include", "disco_b200.h")]
 OUT = os.path.join(_HERE, "_disco_b200.so")
 
 NVCC_FLAGS = [

@@ -1,0 +1,423 @@
+// Shared constants, shared-memory control block, status / parameter blocks, ring and
+// pipeline helpers, and the small device helpers the tensor-core kernels share.
+// Part of the single translation unit disco_b200.cu (included there, in this order).
+#pragma once
+
+namespace disco {
+
+
+// Profiling experiments and ablations (DISCO_DEBUG_FLAGS bits, the symmetric single-rank forward,
+// the A-resident forward ring) exist only in builds with -DDISCO_EXPERIMENTS=1
+// (python -m paper_2304_08480_b200.build --out ... -D DISCO_EXPERIMENTS=1; tools/ab_kernels.py).
+// The default library compiles none of their checks into the kernels.
+#ifndef DISCO_EXPERIMENTS
+#define DISCO_EXPERIMENTS 0
+#endif
+constexpr bool XP = DISCO_EXPERIMENTS != 0;
+
+// ------------------------------------------------------------------ tiling
+constexpr int BM = 128;      // rows per CTA (the pair covers 256)
+constexpr int BN = 256;      // accumulator columns (each CTA loads 128 of the B operand rows)
+constexpr int BK = 64;
+constexpr int PAIR_M = 2 * BM;
+constexpr int A_STAGE_BYTES = BM * BK * 2;        // 16 KiB
+constexpr int B_STAGE_BYTES = (BN / 2) * BK * 2;  // 16 KiB (this CTA's half of one 256-column N tile)
+constexpr int TILE_RING_BYTES = 192 * 1024;      // operand ring: 6 x 32 KiB (NB=1) or 4 x 48 KiB (NB=2)
+// NB = number of 256-column N tiles per unit (2 = "wide": all 512 columns of D, two accumulators);
+// NA = A tiles per stage (2: the fused single-rank backward stages both directions' E tiles)
+template <int NB, int NA = 1> struct Ring {
+  static constexpr int STAGE_BYTES = NA * A_STAGE_BYTES + NB * B_STAGE_BYTES;
+  static constexpr int STAGES = TILE_RING_BYTES / STAGE_BYTES;
+};
+constexpr int STAGES = Ring<1>::STAGES;  // max stage count (barrier arrays)
+constexpr int STAGE_BYTES = Ring<1>::STAGE_BYTES;
+static_assert(Ring<1>::STAGES == 6 && Ring<2>::STAGES == 4 && Ring<2, 2>::STAGES == 3, "ring geometry");
+constexpr int NUM_THREADS = 320;  // warp0 TMA, warp1 MMA, warps2-9 epilogue
+constexpr int NUM_EPI_WARPS = 8;
+// E-operand GEMMs add 4 transform warps (10-13) that rescale each A stage in smem (E -> G).
+constexpr int NUM_XF_WARPS = 4;   // transform warps per group: one 128-row A stage
+// Transform groups: group g takes the ring stages s with s % groups == g (build switches; one group
+// each by default: a second group measured +1.7% cycles on the wide dual backward, -6% on the
+// exchange backward and -2% on the narrow units of D = 768, where it costs 20 bytes of spills).
+#ifndef DISCO_XF_GROUPS
+#define DISCO_XF_GROUPS 1
+#endif
+#ifndef DISCO_XF_GROUPS_NARROW
+#define DISCO_XF_GROUPS_NARROW 1
+#endif
+template <int NB>
+__host__ __device__ constexpr int xf_groups() { return NB == 1 ? DISCO_XF_GROUPS_NARROW : DISCO_XF_GROUPS; }
+constexpr int XF_GROUPS_MAX = DISCO_XF_GROUPS > DISCO_XF_GROUPS_NARROW ? DISCO_XF_GROUPS : DISCO_XF_GROUPS_NARROW;
+template <int NB, bool XF>
+__host__ __device__ constexpr int gemm_threads() { return XF ? NUM_THREADS + 32 * NUM_XF_WARPS * xf_groups<NB>() : NUM_THREADS; }
+constexpr int GROUP_COLS = 64;    // E offset granularity: one exp2 offset per (row, 64-column group)
+// The forward stores E = exp2(y - m_g + E_HEADROOM) (m_g: the row's group max without the label),
+// values in (0, 2^15].  E-operand GEMMs therefore see scaled operands: the two-GEMM (exchange)
+// backward forms 2^15 G, the dual backward 2^14 H (H <= 2); the combines undo the power of two.
+constexpr float E_HEADROOM = 15.f;
+constexpr float G_EXCHANGE_SCALE = 32768.f;  // 2^E_HEADROOM
+constexpr float H_DUAL_LOG2 = 14.f;
+constexpr int TMEM_COLS = 512;    // 2 accumulators of 128 lanes x 256 fp32 columns
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+struct SmemCtl {
+  uint64_t full[STAGES];   // leader: TMA bytes of both CTAs landed
+  uint64_t empty[STAGES];  // both: MMA done reading the stage (multicast commit)
+  uint64_t tfull[2];       // both: accumulator ready (multicast commit)
+  uint64_t tempty[2];      // leader: both CTAs' epilogues drained the accumulator
+  uint64_t xfull[STAGES];  // leader: both CTAs' transform warps rescaled the stage (E-operand GEMMs)
+  uint64_t afull[8];       // leader: resident A slice k of the unit landed (logits kernel, Dp <= 512)
+  uint64_t aempty[8];      // both: the unit's last MMA on A slice k retired
+  uint32_t tmem_base;
+};
+// Epilogue staging: 8 warps x STAGING_BUFS x (32 rows x 128 B), swizzled like TMA SWIZZLE_128B.
+constexpr int STAGING_TILE = 32 * 128;
+constexpr int STAGING_BUFS = 1;
+constexpr int STAGING_BYTES = NUM_EPI_WARPS * STAGING_BUFS * STAGING_TILE;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(TILE_RING_BYTES) + STAGING_BYTES + 512;
+// Logits kernel with a resident A block (Dp <= 512): A = 8 slices x 16 KiB, then a 4-stage B ring.
+constexpr int ARES_SLICES = 8;
+#ifndef DISCO_ARES_B_STAGES
+#define DISCO_ARES_B_STAGES 4
+#endif
+constexpr int ARES_B_STAGES = DISCO_ARES_B_STAGES;
+static_assert(ARES_SLICES * A_STAGE_BYTES + ARES_B_STAGES * B_STAGE_BYTES <= TILE_RING_BYTES + STAGING_BYTES / 2,
+              "A-resident layout");
+static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory limit");
+// Dual backward (E-operand GEMMs, xform = 2): per ring stage, the q factors of the stage's 64 K
+// columns (256 B) land by bulk copy beside the tiles, after the control block.
+constexpr int DUAL_Q_BYTES = 64 * 4;
+constexpr size_t SMEM_BYTES_XF = SMEM_BYTES + size_t(STAGES) * DUAL_Q_BYTES;
+static_assert(SMEM_BYTES_XF <= 232448, "E-operand GEMM smem");
+// A row is fixed up (recomputed exactly, dual_fixup_kernel) when one of its groups' maxima exceeds
+// the smallest column LSE of the group by more than this (log2 units): only then can an E entry
+// below the f16 normal range (29 binades under m_g) carry >= 2^-13 of a column's softmax mass,
+// and only then can the f16 factor a_r + p_r q_c exceed 2^15.
+constexpr float DUAL_SAFE_SPAN = 16.f;
+static_assert(sizeof(uint64_t) * 46 + 4 <= 512, "control block");
+
+// -------------------------------------------------------- status flag bits
+constexpr int FLAG_INPUT_NONFINITE = 1;
+constexpr int FLAG_LOSS_NONFINITE = 2;
+constexpr int FLAG_GRAD_NONFINITE = 4;
+constexpr int FLAG_PEER_TIMEOUT = 8;  // peer transport: a peer's slabs never arrived (wait kernel gave up)
+constexpr int FLAG_H2D_TIMEOUT = 16;  // streamed forward: an H2D chunk never landed
+
+struct Status {
+  double loss;
+  int flags;
+  int fix_count;             // dual backward: rows queued for the exact recompute (DISCO_R_FIX)
+  double dlogit;             // dL/d(logit scale), disco_b200_logit_scale_grad
+  double loss_partial[128];  // loss_partial_kernel scratch (LOSS_BLOCKS)
+  // clock probe (CTA 0 of the tensor-core kernels): {SM clock64, globaltimer ns} at entry and exit,
+  // [0..3] logits kernel, [4..7] backward GEMM -> the SM clock the kernel actually ran at
+  unsigned long long probe[8];
+  // drain probe (backward GEMM, epilogue warp 2 of every leader CTA): sum over units of the
+  // cycles from "accumulators full" to "accumulators released", and the unit count
+  unsigned long long drain[2];
+  // streamed forward (host inputs): wave k's rows landed in FEAT once wave_flags[k] >= the step's
+  // epoch; written by the copy stream (cuStreamWriteValue32), polled by the logits producers
+  unsigned int wave_flags[32];
+};
+
+// ----------------------------------------------------------- kernel params
+// One direction of the logits GEMM: A rows are the rank's local rows of the
+// gathered matrix (row offset rank*b), B rows are all B gathered rows.
+struct LogitsParams {
+  CUtensorMap a_map[2];  // dir 0: I_g, dir 1: T_g   box {64, 128}
+  CUtensorMap b_map[2];  // dir 0: T_g, dir 1: I_g   box {64, 128} (each CTA loads its half of N)
+  CUtensorMap g_map[2];  // blocked-G store maps (4-D), box {64, 32, 1, 1}
+  CUtensorMap e_map[2];  // FWDE: blocked-E store maps, half slices: box {32, 32, 1, 1}, 64-byte swizzle
+  int B, b, Dp, rank;
+  int nchunk, chunk_cols, tiles_per_chunk, row_tiles;  // row_tiles counts 256-row pair tiles
+  float tl2e;  // t * log2(e)
+  // FWD outputs
+  float2* stats;   // [2][nchunk][2 column halves][b]
+  float* target;   // [2][b]  (log2-domain target logit)
+  // GRAD inputs / outputs
+  const float* lse2;    // [2][b]
+  const float* glabel;  // [2][b]
+  __half* G;            // [2][b][ldG] row-major, or blocked (see g_blocked)
+  int64_t ldG;
+  int g_blocked;        // 1: G stored as [2][b/128][B/128][128][128] (contiguous 32 KiB blocks)
+  int debug_flags;      // DISCO_DEBUG_FLAGS (profiling experiments only): bit0 skip G stores
+  // FWDE outputs: E = exp2(y - m_g) into the blocked G region, m_g per (dir, 64-column group, row)
+  float* mg;            // [2][groups][b]
+  int groups;           // B / 64 (GROUP_COLS)
+  // wave >= 0 (single rank, H2D-pipelined forward): only the units whose row chunk or column
+  // chunk is `wave` and the other index <= wave, i.e. the units that became computable when
+  // (stats sub-)chunk `wave` of I and T landed.  rt_per_chunk = 256-row tiles per (sub-)chunk.
+  int wave, rt_per_chunk;
+  // streamed (wave == -2): one persistent launch over all waves in order; the producers wait for
+  // wave_flags[k] >= epoch before loading wave k's tiles
+  const unsigned int* wave_flags;
+  unsigned int epoch;
+  int nwaves;
+  unsigned long long timeout_ns;
+  int* status_flags;
+  unsigned long long* probe;  // Status::probe (may be null)
+};
+
+struct GemmProblem {
+  CUtensorMap a_map;
+  CUtensorMap b_map;
+  CUtensorMap out_map;    // 3-D fp32 store map {N, row_div, z}, box {32, 32, 1}
+  int tma_store;          // 1: TMA stores through staging smem; 0: direct st.global
+  int skip_store;         // profiling experiment (DISCO_DEBUG_FLAGS bit4): drain TMEM, store nothing
+  int ablate;             // profiling experiments: bit10 transform warps skip the rescale, bit11 no drain
+  // peer transport (N > 1): output rows of destination rank r = row / peer_b are TMA-stored straight
+  // into rank r's peer-mapped slab window through peer_map[r] (z = local partial index)
+  int peer, peer_b;
+  CUtensorMap peer_map[8];
+  int paired;             // 1: unit = chunks (2kc, 2kc+1), summed in the epilogue
+  int a_blocked;          // 1: A is a blocked G ([rows/128][cols/128][128][128], 4-D map)
+  int a_mn_major, b_mn_major;
+  int M, N;               // valid output extents
+  int m_tiles, n_tiles, k_chunks;  // m tiles of 256 rows (CTA pair), n tiles of 256 columns
+  int m_off;              // first m tile (row-block launches cover tiles [m_off, m_off + m_tiles))
+  int n_off;              // first output column (split-width launches: [0, 512k) wide, the rest narrow)
+  int k_chunk_len;        // elements of K per chunk (multiple of 64 unless k_chunks == 1)
+  int k_total;            // total K extent
+  int a_k_off, b_k_off;   // added to the K coordinate of MN-major operands
+  int a_row_off;          // added to the row coordinate of a K-major A
+  float* out;
+  int64_t ld_out;         // floats between rows
+  int64_t row_div;        // output row r -> (r / row_div) * stride_hi + (r % row_div) * ld_out
+  int64_t stride_hi;
+  int64_t chunk_stride;   // floats between k-chunk partial outputs
+  // E operand (xform = 1): A holds blocked E; the transform warps rescale every A stage to G
+  int xform;
+  const __half* xscale;   // [groups][xb] exp2(m_g - lse2) of this problem's direction (f16)
+  const float* xlabel;    // [xb] label-column value P_label - 1
+  int xb;                 // local rows b (pitch of xscale)
+  int lab_off;            // rank * b: global column of local row 0's positive pair
+  // dual backward (xform = 2, K-major E rows of direction d): the transform warps write
+  // H' = 2^14 (G_d + G_d'^T) = E (a_r + p_r q_c) over the rank's own E block, with
+  // a_r = exp2(m_g - 1 - lse2_d[r]), p_r = exp2(m_g - 1 - Q_g), q_c = exp2(Q_g - lse2_d'[c]) (< 2^100)
+  const float* xmg;       // [groups][xb] group maxima m_g of direction d (f32)
+  const float* xlse;      // [xb] lse2 of direction d (this rank's rows)
+  const float* xq;        // [B] q_c (bulk-copied per stage; sign -1 under the flip hook)
+  const float2* xgm;      // [groups] (Q_g, smallest column lse2 of the group or -inf)
+  int* fix_list;          // rows needing the exact recompute: fix_tag + row
+  int* fix_count;
+  int fix_tag, fix_cap;
+};
+constexpr int MAX_PROBLEMS = 4;
+constexpr int MAX_SCHED_PAIRS = 80;
+constexpr int MAX_SCHED_UNITS = 4096;
+struct GemmParams {
+  GemmProblem prob[MAX_PROBLEMS];
+  int nprob;
+  int units[MAX_PROBLEMS + 1];  // prefix sums of per-problem unit counts
+  // split > 0: problems [0, split) (list A) and [split, nprob) (list B) are interleaved in
+  // proportion to their unit counts (Bresenham), so pairs walking the unit sequence with a
+  // stride of #pairs see A and B units in different phases (spreads the accumulator drains).
+  int split;
+  unsigned long long* probe;  // Status::probe + 4 (may be null)
+  // Static longest-processing-time schedule (host-computed): pair i runs the unit sequence
+  // indices sched[sched_off[i] .. sched_off[i + 1]) in order; sched_n == 0: round-robin.
+  int sched_n;
+  uint16_t sched_off[MAX_SCHED_PAIRS + 1];
+  uint16_t sched[MAX_SCHED_UNITS];
+};
+
+// --------------------------------------------------------- shared helpers
+// TMA load of one operand stage into this CTA's smem; completion on the leader's barrier.
+// Blocked operands (G in [r/128][c/128][128][128] layout) are addressed through a 4-D map:
+// K-major: rows = G rows, K = G columns; MN-major: MN = G columns, K = G rows.
+__device__ __forceinline__ void load_blocked(const CUtensorMap* map, int mn_major, uint8_t* dst, uint32_t bar,
+                                             int mn0, int k0, int rows, uint64_t policy) {
+  if (!mn_major) {
+    ptx::tma_load_4d_pair(dst, map, bar, k0 & 127, mn0 & 127, k0 >> 7, mn0 >> 7, policy);  // box {64, rows, 1, 1}
+  } else {
+    for (int j = 0; j < rows / 64; ++j) {
+      const int c = mn0 + j * 64;
+      ptx::tma_load_4d_pair(dst + j * 8192, map, bar, c & 127, k0 & 127, c >> 7, k0 >> 7, policy);  // {64, 64, 1, 1}
+    }
+  }
+}
+
+__device__ __forceinline__ void load_operand(const CUtensorMap* map, int mn_major, uint8_t* dst, uint32_t bar,
+                                             int mn0, int k0, int rows, uint64_t policy) {
+  if (!mn_major) {
+    ptx::tma_load_2d_pair(dst, map, bar, k0, mn0, policy);  // box {64 (K), rows}
+  } else {
+    for (int j = 0; j < rows / 64; ++j)  // box {64 (MN), 64 (K)} per 8 KiB atom column
+      ptx::tma_load_2d_pair(dst + j * 8192, map, bar, mn0 + j * 64, k0, policy);
+  }
+}
+
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int mn_major, int kk) {
+  return mn_major ? ptx::smem_desc_sw128(base + kk * 2048, 8192, 1024)  // 16 K-rows of 128 B per MMA
+                  : ptx::smem_desc_sw128(base + kk * 32, 16, 1024);     // 16 K-elements = 32 B per MMA
+}
+
+#ifndef DISCO_WAITPROBE
+#define DISCO_WAITPROBE 0
+#endif
+#if DISCO_WAITPROBE
+// profiling build only: logits kernel barrier-wait cycles {MMA full, MMA tempty, MMA total, MMA
+// threads, epilogue tfull by warp quadrant x4}; backward GEMM {8: MMA operand wait (full/xfull),
+// 9: MMA tempty wait, 10: MMA total, 11: MMA threads, 12: transform TMA wait, 13: transform total,
+// 14: transform threads}; read by disco_b200_waitprobe
+__device__ unsigned long long g_waitprobe[16];
+#endif
+template <int NSTAGES = STAGES>
+struct Pipe {
+  uint32_t stage = 0, phase = 0;
+  __device__ __forceinline__ void advance() {
+    if (++stage == NSTAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+};
+
+__device__ __forceinline__ uint8_t* smem_base(uint8_t* raw) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+}
+
+// Leader-side MMA issue for one unit: nk k-blocks of BK, 4 UMMAs per N tile each.
+// NB = 2: the same A stage feeds two N tiles into accumulators d_tmem and d_tmem + BN.
+// Called by the whole (leader) MMA warp: barrier waits and descriptor arithmetic are
+// warp-uniform (uniform registers), one elected lane issues the UMMAs and the commits.
+// Successive K=16 steps advance the descriptor start address by 32 B (K-major) or 2 KiB
+// (MN-major), i.e. by 2 or 128 in the descriptor's 16-byte units.
+template <int NB, bool XF = false, int RS = Ring<NB>::STAGES, int NA = 1>
+__device__ __forceinline__ void mma_blocks(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>& pipe, int nk, int kb0,
+                                           uint32_t d_tmem, uint32_t idesc, int a_mn, int b_mn, int j_lo, int j_hi,
+                                           bool wait, bool release) {
+  const uint64_t a_step = a_mn ? 128 : 2, b_step = b_mn ? 128 : 2;
+  for (int kb = 0; kb < nk; ++kb) {
+#if DISCO_WAITPROBE
+    const long long w0 = clock64();
+#endif
+    if (wait) ptx::mbar_wait(XF ? &ctl->xfull[pipe.stage] : &ctl->full[pipe.stage], pipe.phase);
+#if DISCO_WAITPROBE
+    if (wait && (threadIdx.x & 31) == 0) atomicAdd(&g_waitprobe[8], (unsigned long long)(clock64() - w0));
+#endif
+    ptx::tc_fence_after();
+    const uint32_t a_base = ptx::smem_u32(tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES);
+    const uint32_t b_base = a_base + NA * A_STAGE_BYTES;
+    const uint64_t ad0 = operand_desc(a_base, a_mn, 0);
+    uint64_t bd0[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) bd0[j] = operand_desc(b_base + j * B_STAGE_BYTES, b_mn, 0);
+    if (ptx::elect_one()) {
+#pragma unroll
+      for (int kk = 0; kk < BK / 16; ++kk) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (j >= j_lo && j < j_hi)
+            ptx::umma_f16_pair(d_tmem + j * BN, ad0 + kk * a_step, bd0[j] + kk * b_step, idesc, ((kb0 + kb) | kk) != 0);
+      }
+      if (release) ptx::umma_commit_pair(&ctl->empty[pipe.stage], 0x3);  // both CTAs' smem slots free
+    }
+    __syncwarp();
+    pipe.advance();
+  }
+}
+
+template <int NB, bool XF = false, int RS = Ring<NB>::STAGES, int NA = 1>
+__device__ __forceinline__ void mma_tile(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>& pipe, int nk,
+                                         uint32_t d_tmem, uint32_t idesc, int a_mn, int b_mn) {
+  mma_blocks<NB, XF, RS, NA>(ctl, tiles, pipe, nk, 0, d_tmem, idesc, a_mn, b_mn, 0, NB, true, true);
+}
+
+// Producer side of one k-block: wait for the slot, arm the leader's barrier, load.
+// LOCAL (E-operand GEMMs): each CTA counts its own bytes on its own barrier, which its
+// transform warps wait on; otherwise the leader's barrier counts both CTAs' bytes.
+template <int NB, bool LOCAL = false, int RS = Ring<NB>::STAGES, int NA = 1>
+__device__ __forceinline__ uint8_t* producer_acquire(SmemCtl* ctl, uint8_t* tiles, Pipe<RS>& pipe,
+                                                     bool leader, uint32_t& bar, uint32_t crank = 0,
+                                                     uint32_t extra_bytes = 0) {
+  ptx::mbar_wait(&ctl->empty[pipe.stage], pipe.phase ^ 1);
+  if (LOCAL) {
+    ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], Ring<NB, NA>::STAGE_BYTES + extra_bytes);
+    bar = ptx::map_to_rank(&ctl->full[pipe.stage], crank);
+  } else {
+    if (leader) ptx::mbar_arrive_expect_tx(&ctl->full[pipe.stage], 2 * Ring<NB, NA>::STAGE_BYTES);
+    bar = ptx::map_to_rank(&ctl->full[pipe.stage], 0);
+  }
+  return tiles + pipe.stage * Ring<NB, NA>::STAGE_BYTES;
+}
+
+// E -> 2^15 G on one 128-byte smem row (64 f16 of one G row i, G columns [j0, j0 + 64)) of a
+// SWIZZLE_128B operand stage: multiply by the f16 factor sc = exp2(m_g - lse2) (HMUL2; E carries
+// the 2^15 headroom); the label column (j == lab) gets 2^15 (P_label - 1).  Logical 16-byte chunk c sits at physical c ^ (row & 7);
+// walking physical chunks in lane order keeps the 8 rows of a quarter-warp on distinct banks.
+__device__ __forceinline__ void xform_row(uint32_t rowp, int sw, __half sc, int lab_rel, float glab) {
+  const __half2 s2 = __half2half2(sc);  // packed f16 multiply: 4 HMUL2 per 16-byte chunk
+  uint4 x[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) x[c] = ptx::lds128(rowp + ((c ^ sw) << 4));
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    __half2* h = reinterpret_cast<__half2*>(&x[c]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __hmul2(h[k], s2);
+    ptx::sts128(rowp + ((c ^ sw) << 4), x[c]);
+  }
+  if (unsigned(lab_rel) < 64u)
+    ptx::sts16(rowp + (((lab_rel >> 3) ^ sw) << 4) + (lab_rel & 7) * 2,
+               __half_as_ushort(__float2half_rn(glab * G_EXCHANGE_SCALE)));
+}
+
+// Clock probe: CTA 0, thread 0 records {clock64, globaltimer} at slot [at, at + 1].
+__device__ __forceinline__ void probe_mark(unsigned long long* probe, int at) {
+  // ctaid / tid re-read (volatile) so the entry and exit marks share no live predicate (it spilled)
+  unsigned bid, tid;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(bid));
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+  if (probe && bid == 0 && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    probe[at] = clock64();
+    probe[at + 1] = t;
+  }
+}
+
+__device__ __forceinline__ void kernel_prologue(SmemCtl* ctl, int warp, int lane, int epi_warps = NUM_EPI_WARPS) {
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {  // the NB=2 ring uses the first Ring<2>::STAGES
+      ptx::mbar_init(&ctl->full[s], 1);
+      ptx::mbar_init(&ctl->empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&ctl->tfull[i], 1);
+      ptx::mbar_init(&ctl->tempty[i], 2 * epi_warps);  // every epilogue warp of both CTAs
+    }
+    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&ctl->xfull[s], 2 * NUM_XF_WARPS);
+    for (int s = 0; s < ARES_SLICES; ++s) {
+      ptx::mbar_init(&ctl->afull[s], 1);
+      ptx::mbar_init(&ctl->aempty[s], 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc_pair(&ctl->tmem_base, TMEM_COLS);
+    ptx::tmem_relinquish_pair();
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+}
+
+__device__ __forceinline__ void kernel_epilogue(SmemCtl* ctl, int warp) {
+  ptx::tc_fence_before();
+  ptx::cluster_sync();  // neither CTA leaves while the pair's MMAs / arrivals may touch it
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_pair(ctl->tmem_base, TMEM_COLS);
+  }
+}
+
+// Epilogue warp releases an accumulator buffer on the leader's barrier.
+__device__ __forceinline__ void release_accumulator(SmemCtl* ctl, int buf, int lane) {
+  ptx::tc_fence_before();
+  __syncwarp();
+  if (lane == 0) ptx::mbar_arrive_cluster(ptx::map_to_rank(&ctl->tempty[buf], 0));
+}
+
+}  // namespace disco
