@@ -147,6 +147,24 @@ int disco_b200_forward_waves(int64_t B, int64_t D, int world, int rank, int* wav
 int disco_b200_path_info(int64_t B, int64_t D, int world, int rank, int* bits);
 int disco_b200_forward_wave(void* ws, int64_t B, int64_t D, int world, int rank, float t, int wave, void* stream);
 int disco_b200_forward_finish(void* ws, int64_t B, int64_t D, int world, int rank, void* stream);
+/* Split schedule of the host-buffer step (single rank, pinned bf16, D % 64 == 0; what disco_step
+ * runs): the backward of one direction needs the other direction's statistics of EVERY row, so
+ * direction 1 is finished first and direction 0 row block by row block, each block's d_image
+ * gradients leaving for the host while the next block computes.
+ *   forward_streamed_split  like disco_b200_forward_streamed, but the persistent launch walks each
+ *                           wave's direction-1 units and, for waves < k0 only, its direction-0
+ *                           units; then f16 operands and the direction-1 statistics
+ *   forward_rect            the units (dir, 256-row tiles of [row0, row1), stats chunks [ch0, ch1))
+ *   stats_rows              LSE / ce / label statistics of rows [row0, row1) of direction dir
+ *                           (all of the row's chunks must have run)
+ * Every unit is the one the one-launch forward runs (same tiles, K order, outputs): bit-identical.
+ * The chunk index counts the forward's statistics sub-chunks (disco_b200_forward_waves of them). */
+int disco_b200_forward_streamed_split(void* ws, int64_t B, int64_t D, int world, int rank, float t, uint32_t epoch,
+                                      double timeout_s, int k0, void* stream);
+int disco_b200_forward_rect(void* ws, int64_t B, int64_t D, int world, int rank, float t, int dir, int64_t row0,
+                            int64_t row1, int ch0, int ch1, void* stream);
+int disco_b200_stats_rows(void* ws, int64_t B, int64_t D, int world, int rank, int dir, int64_t row0, int64_t row1,
+                          void* stream);
 
 /* Streamed forward (host bf16 features, single rank, wavefront shape, D % 64 == 0): the caller
  * copies chunk k's rows of I and T straight into DISCO_R_FEAT on a copy stream and then calls
@@ -284,6 +302,14 @@ int disco_b200_contribution(void* ws, int64_t B, int64_t D, int world, int rank,
  * Together they replace the reference's all_reduce(AVG) + slice (shard.py:199-208) with results
  * bitwise independent of N (every reduction is a fixed function of B). */
 int disco_b200_dual_prep(void* ws, int64_t B, int64_t D, int world, int rank, int flip, void* stream);
+/* One direction of dual_prep / backward_dual / combine_dual (the split schedule above): dual_prep_dir(d)
+ * needs the statistics of every row of direction 1 - d; backward_dual_dir / combine_dual_dir compute
+ * exactly the direction-d part of backward_dual / combine_dual (same bits). */
+int disco_b200_dual_prep_dir(void* ws, int64_t B, int64_t D, int world, int rank, int dir, int flip, void* stream);
+int disco_b200_backward_dual_dir(void* ws, int64_t B, int64_t D, int world, int rank, int dir, int64_t row0,
+                                 int64_t row1, void* stream);
+int disco_b200_combine_dual_dir(void* ws, int64_t B, int64_t D, int world, int rank, int dir, float t, int64_t row0,
+                                int64_t row1, float* d_image, float* d_text, int64_t ld_out, void* stream);
 int disco_b200_backward_dual(void* ws, int64_t B, int64_t D, int world, int rank, int64_t row0, int64_t row1,
                              void* stream);
 int disco_b200_combine_dual(void* ws, int64_t B, int64_t D, int world, int rank, float t, int64_t row0, int64_t row1,

@@ -86,6 +86,13 @@ SIGNATURES = {
     "disco_b200_backward_dual": [_vp, _i64, _i64, _int, _int, _i64, _i64, _vp],
     "disco_b200_combine_dual": [_vp, _i64, _i64, _int, _int, _f32, _i64, _i64, _vp, _vp, _i64, _vp],
     "disco_b200_dual_fixup": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _vp, _i64, _vp],
+    "disco_b200_forward_streamed_split": [_vp, _i64, _i64, _int, _int, _f32, ctypes.c_uint32, ctypes.c_double, _int,
+                                          _vp],
+    "disco_b200_forward_rect": [_vp, _i64, _i64, _int, _int, _f32, _int, _i64, _i64, _int, _int, _vp],
+    "disco_b200_stats_rows": [_vp, _i64, _i64, _int, _int, _int, _i64, _i64, _vp],
+    "disco_b200_dual_prep_dir": [_vp, _i64, _i64, _int, _int, _int, _int, _vp],
+    "disco_b200_backward_dual_dir": [_vp, _i64, _i64, _int, _int, _int, _i64, _i64, _vp],
+    "disco_b200_combine_dual_dir": [_vp, _i64, _i64, _int, _int, _int, _f32, _i64, _i64, _vp, _vp, _i64, _vp],
     "disco_b200_finish_dual_l2norm": [_vp, _i64, _i64, _int, _int, _f32, _int, _vp, _i64, _vp, _i64, _vp, _vp, _i64,
                                       _vp, _vp, _i64, _vp, _vp],
     "disco_b200_l2norm_rows": [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp],

@@ -154,6 +154,9 @@ struct LogitsParams {
   const unsigned int* wave_flags;
   unsigned int epoch;
   int nwaves;
+  int k0;  // wave == -4: waves [0, k0) also carry their direction-0 units
+  // wave == -5: the rectangle of units (direction, row tiles, chunks) one launch covers
+  int rect_dir, rect_rt0, rect_nrt, rect_ch0, rect_nch;
   unsigned long long timeout_ns;
   int* status_flags;
   unsigned long long* probe;  // Status::probe (may be null)

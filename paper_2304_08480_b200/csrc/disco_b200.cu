@@ -286,6 +286,57 @@ int disco_b200_forward_finish(void* ws, int64_t B, int64_t D, int world, int ran
   if (rc) return rc;
   return forward_finish(ws, g, static_cast<cudaStream_t>(stream));
 }
+int disco_b200_forward_streamed_split(void* ws, int64_t B, int64_t D, int world, int rank, float t, uint32_t epoch,
+                                      double timeout_s, int k0, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
+  if (!(world == 1 && g.estore && (g.chunk_cols / g.ssub) % PAIR_M == 0 && g.D == g.Dp))
+    return fail(DISCO_LAYOUT_ERROR, "streamed forward needs a single rank, B %% 2048 == 0 and D %% 64 == 0");
+  const int nw = g.nchunk * g.ssub;
+  if (k0 < 0 || k0 > nw) return fail(DISCO_LAYOUT_ERROR, "k0 %d outside [0, %d]", k0, nw);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  UnitRange ur;
+  ur.k0 = k0;
+  if ((rc = launch_logits(KIND_FWDE, ws, g, t, st, -4, epoch, timeout_s, ur))) return rc;
+  const int64_t n = 2 * g.B * g.Dp / 8;
+  feat16_kernel<<<elementwise_grid(n, 256), 256, 0, st>>>(region<uint4>(ws, g, DISCO_R_FEAT),
+                                                         region<uint4>(ws, g, DISCO_R_FEAT16), n,
+                                                         region<Status>(ws, g, DISCO_R_STATUS));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return forward_finish(ws, g, st, 1, 1);  // direction 1 is complete; direction 0 finishes per row block
+}
+int disco_b200_forward_rect(void* ws, int64_t B, int64_t D, int world, int rank, float t, int dir, int64_t row0,
+                            int64_t row1, int ch0, int ch1, void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (!(t > 0.f) || !std::isfinite(t)) return fail(DISCO_DOMAIN_ERROR, "temperature must be positive, got %g", t);
+  if (!g.estore) return fail(DISCO_LAYOUT_ERROR, "unit rectangles need the E-storing forward (canonical shapes)");
+  const int nch = g.nchunk * g.ssub;
+  if (dir < 0 || dir > 1 || row0 < 0 || row1 > g.b || row0 >= row1 || row0 % PAIR_M || (row1 % PAIR_M && row1 != g.b) ||
+      ch0 < 0 || ch1 > nch || ch0 >= ch1)
+    return fail(DISCO_SHAPE_ERROR, "bad unit rectangle dir %d rows [%lld, %lld) chunks [%d, %d)", dir,
+                (long long)row0, (long long)row1, ch0, ch1);
+  UnitRange ur;
+  ur.dir = dir;
+  ur.rt0 = int(row0 / PAIR_M);
+  ur.nrt = int((row1 + PAIR_M - 1) / PAIR_M) - ur.rt0;
+  ur.ch0 = ch0;
+  ur.nch = ch1 - ch0;
+  return launch_logits(KIND_FWDE, ws, g, t, static_cast<cudaStream_t>(stream), -5, 0, 0.0, ur);
+}
+int disco_b200_stats_rows(void* ws, int64_t B, int64_t D, int world, int rank, int dir, int64_t row0, int64_t row1,
+                          void* stream) {
+  Geometry g;
+  int rc = make_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (dir < 0 || dir > 1 || row0 < 0 || row1 > g.b || row0 > row1)
+    return fail(DISCO_SHAPE_ERROR, "bad statistics rows dir %d [%lld, %lld)", dir, (long long)row0, (long long)row1);
+  return forward_finish(ws, g, static_cast<cudaStream_t>(stream), dir, 1, row0, row1);
+}
 
 
 int disco_b200_backward_grad(void* ws, int64_t B, int64_t D, int world, int rank, float t, void* stream) {
@@ -508,6 +559,20 @@ int disco_b200_dual_prep(void* ws, int64_t B, int64_t D, int world, int rank, in
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;
 }
+int disco_b200_dual_prep_dir(void* ws, int64_t B, int64_t D, int world, int rank, int dir, int flip, void* stream) {
+  Geometry g;
+  int rc = dual_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (dir < 0 || dir > 1) return fail(DISCO_SHAPE_ERROR, "direction %d outside {0, 1}", dir);
+  float* qcol = region<float>(ws, g, DISCO_R_QCOL);
+  const int warps = g.groups;
+  dual_prep_kernel<<<(warps * 32 + 255) / 256, 256, 0, st_of(stream)>>>(
+      region<float>(ws, g, DISCO_R_XALL), int(g.b), g.groups, rank, flip && world > 1, qcol,
+      reinterpret_cast<float2*>(qcol + 2 * g.B), dir, 1);
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
 
 int disco_b200_backward_dual(void* ws, int64_t B, int64_t D, int world, int rank, int64_t row0, int64_t row1,
                              void* stream) {
@@ -520,6 +585,22 @@ int disco_b200_backward_dual(void* ws, int64_t B, int64_t D, int world, int rank
   GemmParams p;
   memset(&p, 0, sizeof(p));
   if ((rc = build_dual(p, ws, g, int(row0 / PAIR_M), int((row1 + PAIR_M - 1) / PAIR_M)))) return rc;
+  return launch_backward(p, st_of(stream), g);
+}
+int disco_b200_backward_dual_dir(void* ws, int64_t B, int64_t D, int world, int rank, int dir, int64_t row0,
+                                 int64_t row1, void* stream) {
+  Geometry g;
+  int rc = dual_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (dir < 0 || dir > 1) return fail(DISCO_SHAPE_ERROR, "direction %d outside {0, 1}", dir);
+  if (row0 < 0 || row1 > g.b || row0 >= row1 || row0 % PAIR_M != 0 || (row1 % PAIR_M != 0 && row1 != g.b))
+    return fail(DISCO_SHAPE_ERROR, "row block [%lld, %lld) must be 256-aligned inside [0, %lld)", (long long)row0,
+                (long long)row1, (long long)g.b);
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  if ((rc = build_dual(p, ws, g, int(row0 / PAIR_M), int((row1 + PAIR_M - 1) / PAIR_M)))) return rc;
+  if (dir == 1) p.prob[0] = p.prob[1];  // one direction: the same problem (same tiles, K order, outputs)
+  p.nprob = 1;
   return launch_backward(p, st_of(stream), g);
 }
 
@@ -537,6 +618,25 @@ int disco_b200_combine_dual(void* ws, int64_t B, int64_t D, int world, int rank,
       region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b,
       region<__nv_bfloat16>(ws, g, DISCO_R_PACK), int(g.b), int(g.Dp), int(D), float(0.5 * double(t) / double(g.B)),
       d_image, d_text, ld_out, int(row0), int(row1 - row0), region<Status>(ws, g, DISCO_R_STATUS));
+  count_launch();
+  CUDA_TRY(cudaGetLastError());
+  return DISCO_OK;
+}
+int disco_b200_combine_dual_dir(void* ws, int64_t B, int64_t D, int world, int rank, int dir, float t, int64_t row0,
+                                int64_t row1, float* d_image, float* d_text, int64_t ld_out, void* stream) {
+  Geometry g;
+  int rc = dual_geometry(B, D, world, rank, &g);
+  if (rc) return rc;
+  if (dir < 0 || dir > 1) return fail(DISCO_SHAPE_ERROR, "direction %d outside {0, 1}", dir);
+  if (ld_out < D) return fail(DISCO_SHAPE_ERROR, "output row stride smaller than D");
+  if (row0 < 0 || row1 > g.b || row0 > row1) return fail(DISCO_SHAPE_ERROR, "row range [%lld, %lld) outside [0, %lld)",
+                                                         (long long)row0, (long long)row1, (long long)g.b);
+  const int64_t n = (row1 - row0) * (g.Dp / 4);
+  if (n == 0) return DISCO_OK;
+  combine_dual_kernel<<<elementwise_grid(n, 256), 256, 0, st_of(stream)>>>(
+      region<float4>(ws, g, DISCO_R_INTRA), g.ksplit, region<float>(ws, g, DISCO_R_ROWS) + 4 * g.b,
+      region<__nv_bfloat16>(ws, g, DISCO_R_PACK), int(g.b), int(g.Dp), int(D), float(0.5 * double(t) / double(g.B)),
+      d_image, d_text, ld_out, int(row0), int(row1 - row0), region<Status>(ws, g, DISCO_R_STATUS), dir, 1);
   count_launch();
   CUDA_TRY(cudaGetLastError());
   return DISCO_OK;

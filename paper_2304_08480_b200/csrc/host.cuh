@@ -358,8 +358,14 @@ int launch_logits_t(const LogitsParams& p, int64_t units, cudaStream_t st, const
   return DISCO_OK;
 }
 
+// unit selection of the split modes (wave -4: k0; wave -5: the rectangle)
+struct UnitRange {
+  int k0 = 0;
+  int dir = 0, rt0 = 0, nrt = 0, ch0 = 0, nch = 0;
+};
+
 int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t st, int wave = -1,
-                  unsigned int epoch = 0, double timeout_s = 0.0) {
+                  unsigned int epoch = 0, double timeout_s = 0.0, UnitRange ur = UnitRange()) {
   LogitsParams p;
   memset(&p, 0, sizeof(p));
   const __nv_bfloat16* feat = region<__nv_bfloat16>(ws, g, DISCO_R_FEAT);
@@ -403,14 +409,23 @@ int launch_logits(int kind, void* ws, const Geometry& g, float t, cudaStream_t s
   }
   const int debug_flags = debug_flag_bits();
   p.debug_flags = debug_flags;
-  if (wave == -2 || wave == -3) {
+  if (wave == -2 || wave == -3 || wave == -4) {
     Status* stt = region<Status>(ws, g, DISCO_R_STATUS);
     p.wave_flags = stt->wave_flags;
     p.status_flags = &stt->flags;
-    p.nwaves = wave == -2 ? g.nchunk * g.ssub : g.N;
+    p.nwaves = wave == -3 ? g.N : g.nchunk * g.ssub;
   }
+  p.k0 = ur.k0;
+  p.rect_dir = ur.dir;
+  p.rect_rt0 = ur.rt0;
+  p.rect_nrt = ur.nrt;
+  p.rect_ch0 = ur.ch0;
+  p.rect_nch = ur.nch;
   const int64_t ndir = 2;
+  const int64_t R = p.rt_per_chunk;
   const int64_t units = wave == -3 ? int64_t(2) * p.row_tiles * p.nchunk
+                      : wave == -4 ? R * p.nwaves * p.nwaves + R * ur.k0 * ur.k0
+                      : wave == -5 ? int64_t(ur.nrt) * ur.nch
                       : wave == -2 ? ndir * p.rt_per_chunk * p.nwaves * p.nwaves
                       : wave >= 0 ? ndir * p.rt_per_chunk * (2 * wave + 1)
                                   : ndir * p.row_tiles * p.nchunk * (kind == KIND_GRAD ? p.tiles_per_chunk : 1);
@@ -721,13 +736,18 @@ int build_dual(GemmParams& p, void* ws, const Geometry& g, int mt0 = 0, int mt1 
 
 // stats combine: after every logits unit of the forward has run.  lse2 and ce land in the
 // exchange vector (DISCO_R_XCHG), the label gradients in DISCO_R_ROWS.
-int forward_finish(void* ws, const Geometry& g, cudaStream_t st) {
+int forward_finish(void* ws, const Geometry& g, cudaStream_t st, int dir0 = 0, int ndir = 2, int64_t row0 = 0,
+                   int64_t row1 = -1) {
   float* rows = region<float>(ws, g, DISCO_R_ROWS);
-  const int n = int(2 * g.b);
+  if (row1 < 0) row1 = g.b;
+  const int nrows = int(row1 - row0);
+  const int n = ndir * nrows;
+  if (n <= 0) return DISCO_OK;
   // column parts per (row, sub-chunk): the FWDE kernel's epilogue parts, or halves (FWD)
   const int nparts = g.estore ? FWDE_PARTS : 2;
   stats_combine_kernel<<<(n + 255) / 256, 256, 0, st>>>(region<float2>(ws, g, DISCO_R_STATS), rows, g.nchunk, g.ssub,
-                                                        nparts, int(g.b), 2, lse2_of(ws, g), rows + 4 * g.b,
+                                                        nparts, int(g.b), dir0, ndir, int(row0), nrows,
+                                                        lse2_of(ws, g), rows + 4 * g.b,
                                                         region<float>(ws, g, DISCO_R_CE),
                                                         region<Status>(ws, g, DISCO_R_STATUS));
   count_launch();

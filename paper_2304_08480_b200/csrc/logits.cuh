@@ -112,21 +112,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
   constexpr bool CHUNK_UNITS = KIND != KIND_GRAD;  // unit = all tiles of one column chunk
   const int wave = CHUNK_UNITS ? p.wave : -1;
   // streamed modes: -2 = H2D row/column wavefront (single rank), -3 = peer column waves (N > 1:
-  // wave k = the columns of source rank (rank + k) % N, all local row tiles)
-  const bool streamed = wave == -2 || wave == -3;
+  // wave k = the columns of source rank (rank + k) % N, all local row tiles), -4 = the H2D
+  // wavefront of direction 1 with direction 0 only for waves k < k0 (each wave's direction-1 units
+  // first), so direction 1 completes as early as the copies allow; -5 (not streamed) = one
+  // rectangle of units: direction rect_dir, row tiles [rect_rt0, +rect_nrt), chunks [rect_ch0,
+  // +rect_nch) -- the rest of direction 0 after -4, row block by row block.  Every mode walks the
+  // same units (identical tiles, K order and outputs), so results are bit-identical.
+  const bool streamed = wave == -2 || wave == -3 || wave == -4;
   const bool colwaves = wave == -3;
+  const bool split = wave == -4;
+  const bool rect = wave == -5;
   const int spr = colwaves ? p.nchunk / p.nwaves : 1;          // sub-chunks per source rank
   const int per_cwave = 2 * p.row_tiles * spr;                  // units per column wave
   const int per_dir = wave >= 0 ? p.rt_per_chunk * (2 * wave + 1)
                                 : p.row_tiles * p.nchunk * (CHUNK_UNITS ? 1 : p.tiles_per_chunk);
+  const int R = p.rt_per_chunk;
+  // -4: waves before k hold R k^2 direction-1 units and R min(k, k0)^2 direction-0 units
+  auto split_base = [&](int k) { return R * k * k + R * min(k, p.k0) * min(k, p.k0); };
   const int num_units = colwaves ? per_cwave * p.nwaves
-                                 : streamed ? NDIR * p.rt_per_chunk * p.nwaves * p.nwaves : NDIR * per_dir;
+                      : split    ? split_base(p.nwaves)
+                      : rect     ? p.rect_nrt * p.rect_nch
+                      : streamed ? NDIR * R * p.nwaves * p.nwaves : NDIR * per_dir;
   // -2: unit u belongs to wave k with 2 R k^2 <= u < 2 R (k+1)^2 (wave k holds 2 R (2k+1));
   auto wave_of = [&](int u) {
     if (colwaves) return u / per_cwave;
-    int k = int(sqrtf(float(u) / float(NDIR * p.rt_per_chunk)));
-    while (k > 0 && NDIR * p.rt_per_chunk * k * k > u) --k;
-    while (NDIR * p.rt_per_chunk * (k + 1) * (k + 1) <= u) ++k;
+    if (split) {
+      int k = 0;
+      while (k + 1 < p.nwaves && split_base(k + 1) <= u) ++k;
+      return k;
+    }
+    int k = int(sqrtf(float(u) / float(NDIR * R)));
+    while (k > 0 && NDIR * R * k * k > u) --k;
+    while (NDIR * R * (k + 1) * (k + 1) <= u) ++k;
     return k;
   };
   const int tiles_per_unit = CHUNK_UNITS ? p.tiles_per_chunk : 1;
@@ -143,14 +160,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(logits_threads<KIND,
       t0 = 0;
       return;
     }
-    int wv = wave, pd = per_dir;
-    if (streamed) {
-      wv = wave_of(u);
-      u -= NDIR * p.rt_per_chunk * wv * wv;
-      pd = p.rt_per_chunk * (2 * wv + 1);
+    if (rect) {
+      dir = p.rect_dir;
+      rt = p.rect_rt0 + u / p.rect_nch;
+      ch = p.rect_ch0 + u % p.rect_nch;
+      t0 = 0;
+      return;
     }
-    dir = u / pd;
-    int rem = u - dir * pd;
+    int wv = wave, pd = per_dir;
+    int rem;
+    if (split) {  // wave wv: R (2 wv + 1) direction-1 units, then as many direction-0 units if wv < k0
+      wv = wave_of(u);
+      u -= split_base(wv);
+      pd = R * (2 * wv + 1);
+      dir = u < pd ? 1 : 0;
+      rem = u < pd ? u : u - pd;
+    } else {
+      if (streamed) {
+        wv = wave_of(u);
+        u -= NDIR * R * wv * wv;
+        pd = R * (2 * wv + 1);
+      }
+      dir = u / pd;
+      rem = u - dir * pd;
+    }
     if (wv >= 0) {  // new row tiles x chunks [0, wave], then old row tiles x chunk `wave`
       const int fresh = p.rt_per_chunk * (wv + 1);
       if (rem < fresh) {

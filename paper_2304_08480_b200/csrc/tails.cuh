@@ -173,12 +173,14 @@ __device__ __forceinline__ void finish_row(int i, float m, float lo, float yt, f
 // Per (dir, row): the forward left one online (max, sum) per (sub-chunk, column part); combine
 // them in a fixed tree -- parts ((0 + 1) + (2 + 3)), sub-chunks, then the 8 canonical chunks
 // ((0 + 1) + (2 + 3)) + ((4 + 5) + (6 + 7)) -- a function of B only, never of N.
+// rows [row0, row0 + nrows) of directions [dir0, dir0 + ndir)
 __global__ void stats_combine_kernel(const float2* stats, const float* target, int nchunk, int ssub, int nparts,
-                                     int b, int ndir, float* lse2_out, float* glabel_out, float* ce_out,
-                                     Status* status) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ndir * b) return;
-  const int dir = i / b, r = i % b;
+                                     int b, int dir0, int ndir, int row0, int nrows, float* lse2_out,
+                                     float* glabel_out, float* ce_out, Status* status) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ndir * nrows) return;
+  const int dir = dir0 + j / nrows, r = row0 + j % nrows;
+  const int i = dir * b + r;
   const int nsc = nchunk * ssub;
   auto at = [&](int sc, int h) { return stats[((int64_t(dir) * nsc + sc) * nparts + h) * b + r]; };
   float m = -INFINITY;
@@ -408,10 +410,11 @@ struct PeerPtrs {
 // outside this rank's rows under the flip hook), and the group's smallest lse2_e, or -inf when the
 // group's spread exceeds 96 (p_r q_c would leave the f32 range: every row goes to the fixup).
 // xall: [N][4][b] gathered (lse2_0, lse2_1, ce_0, ce_1); outputs for d: q [2][B], gm [2][groups].
-__global__ void dual_prep_kernel(const float* xall, int b, int groups, int rank, int flip, float* q, float2* gm) {
+__global__ void dual_prep_kernel(const float* xall, int b, int groups, int rank, int flip, float* q, float2* gm,
+                                 int d0 = 0, int nd = 2) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= 2 * groups) return;
-  const int d = w / groups, g = w % groups, e = 1 - d;
+  if (w >= nd * groups) return;
+  const int d = d0 + w / groups, g = w % groups, e = 1 - d;
   const int64_t B = int64_t(groups) * 64;
   float L[2];
 #pragma unroll
@@ -441,17 +444,17 @@ __global__ void dual_prep_kernel(const float* xall, int b, int groups, int rank,
 // d_text: I_n[r], the packed bf16 rows the GEMMs used).
 __global__ void combine_dual_kernel(const float4* intra, int ksplit, const float* glabel, const __nv_bfloat16* pack,
                                     int b, int Dp, int D, float s, float* d_image, float* d_text, int64_t ld_out,
-                                    int row0, int nrows, Status* status) {
+                                    int row0, int nrows, Status* status, int g0 = 0, int ng = 2) {
   const int v4 = Dp / 4;
   const bool vec_out = (ld_out % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_image) | reinterpret_cast<uintptr_t>(d_text)) % 16 == 0);
   const int64_t per_g = int64_t(b) * v4;
   const unsigned pb = unsigned(int64_t(nrows) * v4), uv4 = unsigned(v4);
-  const int64_t total = 2 * int64_t(pb);
+  const int64_t total = ng * int64_t(pb);
   bool bad = false;
   for (int64_t ii = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ii < total; ii += int64_t(gridDim.x) * blockDim.x) {
     const unsigned iu = unsigned(ii);
-    const int g = int(iu / pb);
-    const int64_t rem = int64_t(iu - unsigned(g) * pb) + int64_t(row0) * v4;
+    const int gl = int(iu / pb), g = g0 + gl;
+    const int64_t rem = int64_t(iu - unsigned(gl) * pb) + int64_t(row0) * v4;
     const int r = int(unsigned(rem) / uv4), vc = int(unsigned(rem) % uv4);
     const float4* ib = intra + (int64_t(g) * ksplit) * per_g + rem;
     const float4 y = ksplit == 2 ? f4add(__ldcs(ib), __ldcs(ib + per_g)) : __ldcs(ib);

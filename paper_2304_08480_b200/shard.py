@@ -548,13 +548,16 @@ def _pipelined_pack_forward(plan: Plan, I_host: torch.Tensor, T_host: torch.Tens
 # host bf16 features with D % 64 == 0: one persistent, flag-gated logits launch (streamed forward)
 STREAMED_FORWARD = True
 H2D_TIMEOUT_S = 30.0
+# split host-buffer schedule (split_schedule): env DISCO_SPLIT=0 selects the one-launch forward
+SPLIT_SCHEDULE = os.environ.get("DISCO_SPLIT", "1") not in ("", "0")
 
 
-def _streamed_forward(plan: Plan, I_host: torch.Tensor, T_host: torch.Tensor, t: float) -> None:
+def _streamed_forward(plan: Plan, I_host: torch.Tensor, T_host: torch.Tensor, t: float, k0=None) -> None:
     """Single rank, host bf16 features: chunk k's rows are copied straight into the forward
     operands (DISCO_R_FEAT) on a copy stream, each followed by a stream write of the wave flag;
     ONE persistent logits kernel walks the waves in order, its producers waiting on each flag.
-    Bit-identical to pack + disco_b200_forward."""
+    Bit-identical to pack + disco_b200_forward.  ``k0`` (split schedule): the kernel runs all of
+    direction 1 and direction 0 only for waves < k0 (the rest: ``_split_backward``)."""
     device = plan.device
     cur = torch.cuda.current_stream(device)
     h2d, _ = plan.h2d_streams()
@@ -569,8 +572,79 @@ def _streamed_forward(plan: Plan, I_host: torch.Tensor, T_host: torch.Tensor, t:
     # every copy and wave signal is enqueued (one native call) BEFORE the kernel that waits on them
     _lib.call("disco_b200_h2d_streamed", *plan.args, I_host.data_ptr(), T_host.data_ptr(), epoch, h2d.cuda_stream)
     plan.h2d_keepalive = (I_host, T_host)  # raw-pointer copies: keep the host rows alive past this step
-    _lib.call("disco_b200_forward_streamed", *plan.args, t, epoch, H2D_TIMEOUT_S, cur.cuda_stream)
+    if k0 is None:
+        _lib.call("disco_b200_forward_streamed", *plan.args, t, epoch, H2D_TIMEOUT_S, cur.cuda_stream)
+    else:
+        _lib.call("disco_b200_forward_streamed_split", *plan.args, t, epoch, H2D_TIMEOUT_S, int(k0), cur.cuda_stream)
     cur.wait_stream(h2d)
+
+
+def split_schedule(plan: Plan):
+    """(k0, row blocks) of the split host-buffer schedule, or None when it does not apply.
+
+    Direction 1 runs inside the H2D wavefront together with direction 0 of the first k0 waves
+    (about the work the copies leave room for); the rest of direction 0 then runs row block by
+    row block, each followed by that block's d_image backward and its copy to the host, so the
+    device->host stream starts about one block after the wavefront instead of after the whole
+    forward.  Blocks hold whole waves and ~one CTA-pair wave of backward units (two K halves per
+    256-row tile of ONE direction)."""
+    if not SPLIT_SCHEDULE or plan.world != 1 or plan.waves < 4:
+        return None
+    nw = plan.waves
+    k0 = int(os.environ.get("DISCO_SPLIT_K0", "-1"))
+    if k0 < 0:
+        k0 = (3 * nw) // 4
+    k0 = max(0, min(nw, k0))
+    rows_per_wave = plan.b // nw
+    if rows_per_wave % 256:
+        return None
+    tiles_per_block = max(1, plan.pairs // 2)                  # 2 K halves per 256-row tile, one direction
+    waves_per_block = max(1, (tiles_per_block * 256) // rows_per_wave)
+    cuts = list(range(0, nw, waves_per_block)) + [nw]
+    return k0, [(w0 * rows_per_wave, w1 * rows_per_wave) for w0, w1 in zip(cuts, cuts[1:])]
+
+
+def _split_backward(plan: Plan, t: float, flip: int, k0: int, blocks, d_image, d_text, host_out) -> None:
+    """Second half of the split schedule (after ``_streamed_forward(..., k0)``): direction 0's
+    remaining units per row block, its statistics, its d_image backward + combine and the block's
+    copy to the host; then, with every row's statistics known, the d_text blocks.  Each unit,
+    tile, K order and reduction is the one of the one-launch path: the same bits."""
+    device, b, D = plan.device, plan.b, plan.D
+    st = torch.cuda.current_stream(device).cuda_stream
+    nw = plan.waves
+    rows_per_wave = b // nw
+    cs = plan.copy_stream()
+    cur = torch.cuda.current_stream(device)
+    h_image, h_text = host_out
+    _lib.call("disco_b200_dual_prep_dir", *plan.args, 0, flip, st)
+    for r0, r1 in blocks:
+        w0, w1 = r0 // rows_per_wave, r1 // rows_per_wave
+        if w0 < k0:  # waves already in the wavefront's direction-0 share: only chunks >= k0 are left
+            e = min(w1, k0) * rows_per_wave
+            if k0 < nw:
+                _lib.call("disco_b200_forward_rect", *plan.args, t, 0, r0, e, k0, nw, st)
+            if e < r1:
+                _lib.call("disco_b200_forward_rect", *plan.args, t, 0, e, r1, 0, nw, st)
+        else:
+            _lib.call("disco_b200_forward_rect", *plan.args, t, 0, r0, r1, 0, nw, st)
+        _lib.call("disco_b200_stats_rows", *plan.args, 0, r0, r1, st)
+        _lib.call("disco_b200_backward_dual_dir", *plan.args, 0, r0, r1, st)
+        _lib.call("disco_b200_combine_dual_dir", *plan.args, 0, t, r0, r1, d_image.data_ptr(), d_text.data_ptr(), D, st)
+        cs.wait_stream(cur)
+        with torch.cuda.stream(cs):
+            h_image[r0:r1].copy_(d_image[r0:r1], non_blocking=True)
+    _lib.call("disco_b200_dual_prep_dir", *plan.args, 1, flip, st)
+    for r0, r1 in blocks:
+        _lib.call("disco_b200_backward_dual_dir", *plan.args, 1, r0, r1, st)
+        _lib.call("disco_b200_combine_dual_dir", *plan.args, 1, t, r0, r1, d_image.data_ptr(), d_text.data_ptr(), D, st)
+        cs.wait_stream(cur)
+        with torch.cuda.stream(cs):
+            h_text[r0:r1].copy_(d_text[r0:r1], non_blocking=True)
+    d_image.record_stream(cs)
+    d_text.record_stream(cs)
+    plan.pending_host = (d_image, d_text, h_image, h_text)
+    _lib.call("disco_b200_dual_fixup", *plan.args, t, flip, d_image.data_ptr(), d_text.data_ptr(), D, st)
+    _lib.call("disco_b200_loss", *plan.args, 2, st)
 
 
 def host_pipelined(world: int, B: int, D: int, rank: int = 0) -> bool:
@@ -610,6 +684,7 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
     _enter(plan, cur_stream)
     st = cur_stream.cuda_stream
     pw = None  # peer window of this step (N > 1 with the peer transport)
+    split = None  # (k0, row blocks) of the split host-buffer schedule
     if on_host:
         if N != 1 or plan.waves == 0 or local_T.is_cuda:
             raise ValueError("host (CPU) features need a single rank and a wavefront shape; "
@@ -617,7 +692,10 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
         if (STREAMED_FORWARD and local_I.dtype == torch.bfloat16 and local_T.dtype == torch.bfloat16
                 and D == plan.Dp and local_I.is_contiguous() and local_T.is_contiguous()
                 and local_I.is_pinned() and local_T.is_pinned()):
-            _streamed_forward(plan, local_I.contiguous(), local_T.contiguous(), t)
+            if host_out is not None and l2norm is None and _lib.path_info(B, D, N, n) & _lib.PATH_DUAL:
+                split = split_schedule(plan)
+            _streamed_forward(plan, local_I.contiguous(), local_T.contiguous(), t,
+                              split[0] if split is not None else None)
         else:
             _pipelined_pack_forward(plan, local_I.contiguous(), local_T.contiguous(), t)
     else:
@@ -659,7 +737,9 @@ def disco_step_async(endpoint, local_I, local_T, t: float, *, flip_cross_rank_si
     if l2norm is not None:
         _check_l2norm_args(l2norm, b, D, device)
     fused = l2norm is not None and host_out is None and bool(_lib.path_info(B, D, N, n) & _lib.PATH_DUAL)
-    if _lib.path_info(B, D, N, n) & _lib.PATH_DUAL:
+    if split is not None:
+        _split_backward(plan, t, flip, split[0], split[1], d_image, d_text, host_out)
+    elif _lib.path_info(B, D, N, n) & _lib.PATH_DUAL:
         _dual_backward(endpoint, plan, t, flip, d_image, d_text, host_out, l2norm if fused else None)
     else:
         _exchange_backward(endpoint, plan, t, flip, d_image, d_text, host_out, pw,

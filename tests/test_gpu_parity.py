@@ -351,3 +351,43 @@ def test_input_containers_and_dtypes_give_identical_bits():
             di, dt = di.float().cpu().numpy(), dt.float().cpu().numpy()
         assert loss == ref_l, (type(a), getattr(a, "dtype", None))
         assert np.array_equal(di, ref_i) and np.array_equal(dt, ref_t), (type(a), getattr(a, "dtype", None))
+
+
+@pytest.mark.parametrize("B,k0", [(32768, "12"), (16384, "0"), (16384, "5"), (16384, "16"), (8192, "-1")])
+def test_split_host_schedule_bitwise(monkeypatch, B, k0):
+    """The split host-buffer schedule (direction 1 inside the H2D wavefront with direction 0 of the
+    first k0 waves, then direction 0 row block by row block with each block's d_image backward
+    and copy, then the d_text blocks) returns the device path's bits for any k0."""
+    from paper_2304_08480_b200 import shard
+    calls = []
+    real = shard._split_backward
+    monkeypatch.setattr(shard, "_split_backward", lambda *a, **k: (calls.append(1), real(*a, **k)))
+    monkeypatch.setenv("DISCO_SPLIT_K0", k0)
+    D = 512
+    I, T = O.synthetic_features(B, D, 6)
+    Ih = torch.from_numpy(I.astype(np.float32)).to(torch.bfloat16).pin_memory()
+    Th = torch.from_numpy(T.astype(np.float32)).to(torch.bfloat16).pin_memory()
+    dh_i, dh_t, lh = P.disco_step(None, Ih, Th, 100.0)
+    dd_i, dd_t, ld = P.disco_step(None, Ih.cuda(), Th.cuda(), 100.0)
+    assert calls, "the split schedule was not taken"
+    assert lh == ld
+    assert torch.equal(dh_i, dd_i.cpu()) and torch.equal(dh_t, dd_t.cpu())
+
+
+def test_split_host_schedule_refreshes_fixed_rows(monkeypatch):
+    """Rows the dual fixup recomputes after their blocks were copied reach the host copies."""
+    from paper_2304_08480_b200 import shard
+    calls = []
+    real = shard._split_backward
+    monkeypatch.setattr(shard, "_split_backward", lambda *a, **k: (calls.append(1), real(*a, **k)))
+    from paper_2304_08480_b200.shard import get_plan
+    from tests.test_gpu_dual import _adversarial
+    B, D, t = 4096, 64, 100.0
+    I, T = _adversarial(B, D, 16, 3)
+    Ih = torch.from_numpy(I.astype(np.float32)).to(torch.bfloat16).pin_memory()
+    Th = torch.from_numpy(T.astype(np.float32)).to(torch.bfloat16).pin_memory()
+    hi, ht, hl = P.disco_step(None, Ih, Th, t)
+    di, dt, dl = P.disco_step(None, Ih.cuda(), Th.cuda(), t)
+    assert calls
+    assert get_plan(B, D, 1, 0, torch.device("cuda", 0)).fixed_rows > 0
+    assert torch.equal(hi, di.cpu()) and torch.equal(ht, dt.cpu()) and hl == dl
