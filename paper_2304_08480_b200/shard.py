@@ -778,7 +778,7 @@ def _dual_backward(endpoint, plan: Plan, t: float, flip: int, d_image, d_text, h
     if N > 1:
         endpoint.all_gather_into(plan.xall, plan.xchg)
     _lib.call("disco_b200_dual_prep", *plan.args, flip, st)
-    if N == 1 and host_out is not None:
+    if host_out is not None:  # rank-local row blocks at every N: each block's copy overlaps the next
         cs = plan.copy_stream()
         cur = torch.cuda.current_stream(device)
         h_image, h_text = host_out
@@ -954,7 +954,9 @@ def disco_step(endpoint, local_I, local_T, t: float, *, loss_counters: Counters 
         T_dev = T_dev.to(I_dev.dtype)
     exchange_counters.alloc(2 * batch * dim)
     host_out = None
-    if origin != "cuda" and endpoint.world_size == 1:  # pipelined read-back (row blocks)
+    # pipelined read-back (row blocks): single rank, or any N on the dual path (rank-local rows)
+    if origin != "cuda" and (endpoint.world_size == 1
+                             or _lib.path_info(batch, dim, endpoint.world_size, endpoint.rank) & _lib.PATH_DUAL):
         shape = (layout.local_batch, dim)
         host_out = (torch.empty(shape, dtype=torch.float32, pin_memory=True),
                     torch.empty(shape, dtype=torch.float32, pin_memory=True))

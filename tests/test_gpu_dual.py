@@ -223,3 +223,27 @@ def test_fused_tower_epilogue_exchange_mode_and_validation(monkeypatch):
         P.disco_step_async(P.SingleEndpoint(), I, T, t, l2norm=(raw_i, raw_t, dx_i.double(), dx_t, nf))
     with pytest.raises(P.ShapeError):
         P.disco_step_async(P.SingleEndpoint(), I, T, t, l2norm=(raw_i, raw_t, dx_i, dx_t, nf.float()))
+
+
+@pytest.mark.parametrize("N", [2, 4])
+def test_host_outputs_at_n_gt_1_row_blocks_bitwise(N):
+    """numpy inputs at N > 1 (dual path): each rank's gradients come back in row blocks whose copies
+    overlap the next block's GEMM; same bytes as the device-tensor step."""
+    B, D, t = 16384, 256, 100.0
+    I, T = O.synthetic_features(B, D, 13)
+    b = B // N
+    Id, Td = dev(I), dev(T)
+
+    def host(ep):
+        rows = slice(ep.rank * b, (ep.rank + 1) * b)
+        return P.disco_step(ep, I[rows].astype(np.float32), T[rows].astype(np.float32), t)
+
+    def device(ep):
+        rows = slice(ep.rank * b, (ep.rank + 1) * b)
+        return P.disco_step(ep, Id[rows], Td[rows], t)
+
+    hr = P.run_ranks(N, host)
+    dr = P.run_ranks(N, device)
+    for h, d in zip(hr, dr):
+        assert isinstance(h[0], np.ndarray) and h[2] == d[2]
+        assert np.array_equal(h[0], d[0].cpu().numpy()) and np.array_equal(h[1], d[1].cpu().numpy())
